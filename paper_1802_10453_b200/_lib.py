@@ -1,0 +1,70 @@
+"""ctypes loader for libffldl_b200.so (the C-ABI in include/ffldl_b200.h).
+
+The library is built in-tree (paper_1802_10453_b200/build.py).  There is no
+fallback: if the shared library is missing or fails to load, importing the
+package raises, and every compute call needs a CUDA device.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libffldl_b200.so")
+
+_lib = None
+
+# Every symbol declared in include/ffldl_b200.h (checked by tests/test_capi.py).
+EXPORTS = [
+    "ffb_version", "ffb_status_string", "ffb_last_error", "ffb_create", "ffb_destroy",
+    "ffb_stream", "ffb_launch_count", "ffb_ldlt", "ffb_ldlt_compact", "ffb_ldlt_zero_leading",
+    "ffb_ldlt_device", "ffb_plduq", "ffb_trssyr2k", "ffb_gemm_sub", "ffb_trmm_sub",
+    "ffb_trsm_inplace", "ffb_syrdk_sub", "ffb_syr2k_sub", "ffb_generate_host",
+    "ffb_generate_device", "ffb_config5_partners",
+]
+
+P = C.c_void_p
+SZ = C.c_size_t
+U64 = C.c_uint64
+I = C.c_int
+
+_SIGS = {
+    "ffb_version": (I, []),
+    "ffb_status_string": (C.c_char_p, [I]),
+    "ffb_last_error": (C.c_char_p, []),
+    "ffb_create": (I, [C.POINTER(P), I]),
+    "ffb_destroy": (I, [P]),
+    "ffb_stream": (P, [P]),
+    "ffb_launch_count": (U64, [P]),
+    "ffb_ldlt": (I, [P, U64, SZ, SZ, P, I, SZ, P, P, P, P, P, C.POINTER(SZ)]),
+    "ffb_ldlt_compact": (I, [P, U64, SZ, P, I, I, SZ, P, P, I, P, P, P, C.POINTER(SZ)]),
+    "ffb_ldlt_zero_leading": (I, [P, U64, SZ, SZ, P, SZ, P, I, SZ, P, P, P, P, P, C.POINTER(SZ)]),
+    "ffb_ldlt_device": (I, [P, U64, SZ, P, SZ, I, SZ, P, P, SZ, P, P, P, C.POINTER(SZ)]),
+    "ffb_plduq": (I, [P, U64, SZ, SZ, P, P, P, P, P, P, C.POINTER(SZ)]),
+    "ffb_trssyr2k": (I, [P, U64, SZ, P, P, P]),
+    "ffb_gemm_sub": (I, [P, U64, SZ, SZ, SZ, P, P, P]),
+    "ffb_trmm_sub": (I, [P, U64, SZ, SZ, P, P, I, I, I, P]),
+    "ffb_trsm_inplace": (I, [P, U64, SZ, SZ, P, I, I, I, P]),
+    "ffb_syrdk_sub": (I, [P, U64, SZ, SZ, P, P, P, P, P]),
+    "ffb_syr2k_sub": (I, [P, U64, SZ, SZ, P, P, P]),
+    "ffb_generate_host": (I, [I, SZ, SZ, U64, U64, P]),
+    "ffb_generate_device": (I, [P, I, SZ, SZ, U64, U64, P]),
+    "ffb_config5_partners": (I, [SZ, SZ, U64, P]),
+}
+
+
+def lib():
+    """The loaded engine library (raises if it has not been built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_1802_10453_b200.build` "
+                "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib

@@ -1,0 +1,131 @@
+// ffb_common.cuh -- shared device/host definitions of the B200 PLDL^TP^T engine.
+//
+// Residues of GF(p) live in HBM as uint32 in [0, p) (p < 2^31).  Field
+// arithmetic follows the reference's PrimeField semantics
+// (proj/include/ffldl/field.hpp:73-134): add/sub/neg canonical, multiply with
+// Barrett reduction instead of a 128-bit '%', inverse by extended Euclid
+// (or a table for p < 2^16), halve for odd p.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+#include "../../include/ffldl_b200.h"
+
+namespace ffb {
+
+// ---------------------------------------------------------------------------
+// Errors: the C-ABI maps these 1:1 to FFB_* status codes.
+// ---------------------------------------------------------------------------
+struct Status : std::runtime_error {
+    int code;
+    Status(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define FFB_CUDA(call)                                                                       \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            throw ::ffb::Status(FFB_CUDA_ERROR, std::string(#call) + ": " +                  \
+                                                    cudaGetErrorString(e_));                 \
+    } while (0)
+
+#define FFB_CHECK_LAUNCH() FFB_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------------------
+// Field constants (passed by value to every kernel).
+// ---------------------------------------------------------------------------
+struct Fp {
+    uint32_t p;
+    uint64_t mu;            // floor((2^64-1)/p), Barrett constant
+    const uint32_t* inv;    // device inverse table (p < 2^16) or nullptr
+    int char2;              // p == 2
+};
+
+__host__ __device__ inline uint64_t umulhi64(uint64_t a, uint64_t b) {
+#ifdef __CUDA_ARCH__
+    return __umul64hi(a, b);
+#else
+    return (uint64_t)(((unsigned __int128)a * b) >> 64);
+#endif
+}
+
+// x mod p for any 64-bit x.
+__host__ __device__ inline uint32_t red64(const Fp& f, uint64_t x) {
+    uint64_t q = umulhi64(x, f.mu);
+    uint64_t r = x - q * f.p;
+    while (r >= f.p) r -= f.p;
+    return (uint32_t)r;
+}
+__host__ __device__ inline uint32_t fadd(const Fp& f, uint32_t a, uint32_t b) {
+    uint32_t s = a + b;  // < 2^32 since p < 2^31
+    return s >= f.p ? s - f.p : s;
+}
+__host__ __device__ inline uint32_t fsub(const Fp& f, uint32_t a, uint32_t b) {
+    return a >= b ? a - b : a + f.p - b;
+}
+__host__ __device__ inline uint32_t fneg(const Fp& f, uint32_t a) { return a ? f.p - a : 0; }
+__host__ __device__ inline uint32_t fmul(const Fp& f, uint32_t a, uint32_t b) {
+    return red64(f, (uint64_t)a * b);
+}
+// a/2 for odd p (field.hpp:121-124).
+__host__ __device__ inline uint32_t fhalve(const Fp& f, uint32_t a) {
+    return (a & 1) ? (uint32_t)(((uint64_t)a + f.p) >> 1) : (a >> 1);
+}
+// Extended Euclid (field.hpp:107-118); returns 0 for a == 0 (callers never pass 0).
+__host__ __device__ inline uint32_t finv_euclid(uint32_t p, uint32_t a) {
+    int64_t t = 0, nt = 1, r = p, nr = a;
+    while (nr != 0) {
+        int64_t q = r / nr, tmp;
+        tmp = t - q * nt; t = nt; nt = tmp;
+        tmp = r - q * nr; r = nr; nr = tmp;
+    }
+    if (t < 0) t += p;
+    return (uint32_t)t;
+}
+__device__ inline uint32_t finv(const Fp& f, uint32_t a) {
+    if (f.inv) return f.inv[a];
+    return finv_euclid(f.p, a);
+}
+
+// ---------------------------------------------------------------------------
+// Strided row-major views of device matrices.
+// ---------------------------------------------------------------------------
+struct DMat {
+    uint32_t* ptr = nullptr;
+    int64_t ld = 0;
+    int64_t rows = 0, cols = 0;
+    __host__ __device__ uint32_t* at(int64_t i, int64_t j) const { return ptr + i * ld + j; }
+    DMat sub(int64_t r0, int64_t c0, int64_t nr, int64_t nc) const {
+        DMat m;
+        m.ptr = ptr + r0 * ld + c0;
+        m.ld = ld;
+        m.rows = nr;
+        m.cols = nc;
+        return m;
+    }
+};
+
+// Per-pivot-column encoding of D (mirrors BlockDiag, blockdiag.hpp:20-33).
+enum DKind : int32_t {
+    D_SCALAR = 0,
+    D_ANTIDIAG_HEAD = 1,
+    D_ANTIDIAG_TAIL = 2,
+    D_ANTITRI_HEAD = 3,
+    D_ANTITRI_TAIL = 4
+};
+
+// Global device-side D arrays, indexed by global pivot column.
+struct DDiag {
+    int32_t* kind;
+    uint32_t* val;   // Scalar d / AntiDiag x / AntiTri c
+    uint32_t* val2;  // AntiTri d
+    uint32_t* inv;   // inverse of val (d^-1, x^-1, c^-1)
+};
+
+inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace ffb

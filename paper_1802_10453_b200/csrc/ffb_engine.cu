@@ -1,0 +1,931 @@
+// ffb_engine.cu -- host recursion of the B200 PLDL^TP^T engine + the C-ABI.
+//
+// The recursion tree is the reference's, node for node (proj/src/sytrf.cpp):
+// dispatch (:337-350) -> crout leaf (:35-139) or recursive_step (:298-335),
+// zero_leading (:267-292), zero_leading_pairs (:170-265).  The output triple
+// (P, L, D) depends on that tree for non-generic rank profiles, so the host
+// walks exactly the same nodes; each node's arithmetic runs on the device.
+//
+// Data layout in HBM:
+//   W   n x n uint32 residues, the input; every node updates its own block
+//       in place (Schur complements overwrite the trailing blocks).
+//   Lg  n x n uint32: L indexed by (ORIGINAL row, global pivot column).  A
+//       row's multipliers depend only on the row's identity, never on the
+//       positions later permutations give it, so nodes write their columns
+//       once and the final L is a single row gather by the output
+//       permutation (no per-level row shuffles of L).
+//   D   per-pivot-column kind / value / value2 / inverse arrays.
+// Node-local permutations and ranks are read back to the host (they decide
+// the shape of the next node); index arrays go down through a pinned ring.
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ffb_kernels.cuh"
+
+using namespace ffb;
+
+// ===========================================================================
+// Context
+// ===========================================================================
+struct ffb_context {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    char* ws_base = nullptr;
+    size_t ws_cap = 0, ws_top = 0;
+    char* up_host = nullptr;
+    size_t up_cap = 0, up_top = 0;
+    char* down_host = nullptr;
+    size_t down_cap = 0;
+    uint32_t* inv_table = nullptr;
+    uint32_t inv_p = 0;
+    int32_t* flag = nullptr;  // device scratch flag
+    uint64_t launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+// ---------------------------------------------------------------------------
+// Field setup (PrimeField checks, field.hpp:73-80).
+// ---------------------------------------------------------------------------
+uint64_t host_powmod(uint64_t a, uint64_t e, uint64_t m) {
+    unsigned __int128 r = 1 % m, x = a % m;
+    while (e) {
+        if (e & 1) r = (r * x) % m;
+        x = (x * x) % m;
+        e >>= 1;
+    }
+    return (uint64_t)r;
+}
+
+bool host_is_prime(uint64_t n) {
+    static const uint64_t bases[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+    if (n < 2) return false;
+    for (uint64_t q : bases)
+        if (n % q == 0) return n == q;
+    uint64_t d = n - 1;
+    int s = 0;
+    while ((d & 1) == 0) { d >>= 1; ++s; }
+    for (uint64_t a : bases) {
+        uint64_t x = host_powmod(a, d, n);
+        if (x == 1 || x == n - 1) continue;
+        bool composite = true;
+        for (int i = 1; i < s; ++i) {
+            x = (uint64_t)(((unsigned __int128)x * x) % n);
+            if (x == n - 1) { composite = false; break; }
+        }
+        if (composite) return false;
+    }
+    return true;
+}
+
+void check_modulus(uint64_t p) {
+    if (p < 2 || p > ((1ull << 62) - 1) || !host_is_prime(p))
+        throw Status(FFB_NOT_PRIME, "modulus " + std::to_string(p) + " is not a prime below 2^62");
+    if (p >= (1ull << 31))
+        throw Status(FFB_UNSUPPORTED, "device path supports primes below 2^31");
+}
+
+// ---------------------------------------------------------------------------
+// Workspace: stack allocator over one device allocation (stream-ordered reuse
+// is safe because every kernel runs on the context's single stream).
+// ---------------------------------------------------------------------------
+struct WsMark {
+    size_t top;
+};
+
+void ensure_workspace(ffb_context* c, size_t bytes) {
+    if (c->ws_cap >= bytes) return;
+    if (c->ws_base) {
+        FFB_CUDA(cudaStreamSynchronize(c->stream));
+        FFB_CUDA(cudaFree(c->ws_base));
+        c->ws_base = nullptr;
+        c->ws_cap = 0;
+    }
+    size_t freeb = 0, totalb = 0;
+    FFB_CUDA(cudaMemGetInfo(&freeb, &totalb));
+    if (bytes > freeb) bytes = freeb > (1ull << 30) ? freeb - (1ull << 30) : freeb / 2;
+    FFB_CUDA(cudaMalloc(&c->ws_base, bytes));
+    c->ws_cap = bytes;
+    c->ws_top = 0;
+}
+
+void* ws_alloc(ffb_context* c, size_t bytes) {
+    const size_t a = (c->ws_top + 255) & ~(size_t)255;
+    if (a + bytes > c->ws_cap)
+        throw Status(FFB_NO_MEMORY, "device workspace exhausted (" + std::to_string(a + bytes) +
+                                        " > " + std::to_string(c->ws_cap) + " bytes)");
+    c->ws_top = a + bytes;
+    return c->ws_base + a;
+}
+
+DMat ws_mat(ffb_context* c, int64_t rows, int64_t cols) {
+    DMat m;
+    m.rows = rows;
+    m.cols = cols;
+    m.ld = cols > 0 ? cols : 1;
+    m.ptr = (uint32_t*)ws_alloc(c, (size_t)std::max<int64_t>(rows, 1) * m.ld * sizeof(uint32_t));
+    return m;
+}
+
+template <class T>
+T* ws_vec(ffb_context* c, int64_t n) {
+    return (T*)ws_alloc(c, (size_t)std::max<int64_t>(n, 1) * sizeof(T));
+}
+
+// Pinned upload ring: index arrays going down to the device.
+const int32_t* upload(ffb_context* c, const int32_t* v, size_t n) {
+    int32_t* d = ws_vec<int32_t>(c, (int64_t)n);
+    if (n == 0) return d;
+    const size_t bytes = n * sizeof(int32_t);
+    if (bytes > c->up_cap) {  // rare: larger than the ring, copy synchronously
+        FFB_CUDA(cudaStreamSynchronize(c->stream));
+        FFB_CUDA(cudaMemcpy(d, v, bytes, cudaMemcpyHostToDevice));
+        return d;
+    }
+    size_t off = (c->up_top + 15) & ~(size_t)15;
+    if (off + bytes > c->up_cap) {
+        FFB_CUDA(cudaStreamSynchronize(c->stream));
+        off = 0;
+    }
+    memcpy(c->up_host + off, v, bytes);
+    FFB_CUDA(cudaMemcpyAsync(d, c->up_host + off, bytes, cudaMemcpyHostToDevice, c->stream));
+    c->up_top = off + bytes;
+    return d;
+}
+const int32_t* upload(ffb_context* c, const std::vector<int32_t>& v) {
+    return upload(c, v.data(), v.size());
+}
+
+// Device -> host read-back of a small array (a synchronization point).
+const void* readback(ffb_context* c, const void* dev, size_t bytes) {
+    if (bytes > c->down_cap) {
+        if (c->down_host) FFB_CUDA(cudaFreeHost(c->down_host));
+        c->down_cap = std::max(bytes, (size_t)1 << 20);
+        FFB_CUDA(cudaMallocHost(&c->down_host, c->down_cap));
+    }
+    FFB_CUDA(cudaMemcpyAsync(c->down_host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    FFB_CUDA(cudaStreamSynchronize(c->stream));
+    c->up_top = 0;  // every upload issued so far has completed
+    return c->down_host;
+}
+
+Fp make_field(ffb_context* c, uint64_t p) {
+    Fp f;
+    f.p = (uint32_t)p;
+    f.mu = UINT64_MAX / p;
+    f.char2 = p == 2;
+    f.inv = nullptr;
+    if (p < 65536) {
+        if (c->inv_p != p) {
+            if (c->inv_table) FFB_CUDA(cudaFree(c->inv_table));
+            std::vector<uint32_t> t(p, 0);
+            for (uint64_t a = 1; a < p; ++a) t[a] = finv_euclid((uint32_t)p, (uint32_t)a);
+            FFB_CUDA(cudaMalloc(&c->inv_table, p * sizeof(uint32_t)));
+            FFB_CUDA(cudaMemcpy(c->inv_table, t.data(), p * sizeof(uint32_t), cudaMemcpyHostToDevice));
+            c->inv_p = (uint32_t)p;
+        }
+        f.inv = c->inv_table;
+    }
+    return f;
+}
+
+// ===========================================================================
+// The recursion.
+// ===========================================================================
+struct HFact {
+    std::vector<int32_t> perm;  // image: position -> local input row
+    int64_t rank = 0;
+};
+
+struct Engine {
+    ffb_context* c;
+    cudaStream_t st;
+    Fp f;
+    int variant;
+    int64_t T;
+    DMat Lg;
+    DDiag D;
+
+    bool is_leaf(int64_t s) const {
+        if (variant == FFB_VARIANT_CROUT) return true;
+        if (variant == FFB_VARIANT_RECURSIVE) return s <= 1;
+        return s <= T || s <= 1;
+    }
+
+    // dispatch, sytrf.cpp:337-350
+    HFact dispatch(DMat A, const std::vector<int32_t>& rows, int64_t coff) {
+        if (is_leaf(A.rows)) return crout(A, rows, coff);
+        return recursive_step(A, rows, coff);
+    }
+
+    // crout_base, sytrf.cpp:35-139 (device kernel, one CTA)
+    HFact crout(DMat A, const std::vector<int32_t>& rows, int64_t coff) {
+        const int64_t s = A.rows;
+        HFact h;
+        if (s == 0) return h;
+        const WsMark mk{c->ws_top};
+        const int32_t* drows = upload(c, rows);
+        int32_t* out = ws_vec<int32_t>(c, s + 1);
+        uint32_t* scratch = nullptr;
+        if (s > 200) scratch = ws_vec<uint32_t>(c, (int64_t)leaf_scratch_words(s));
+        leaf_crout(f, st, A, drows, Lg, coff, D, out, scratch);
+        const int32_t* hb = (const int32_t*)readback(c, out, (size_t)(s + 1) * sizeof(int32_t));
+        h.rank = hb[0];
+        h.perm.assign(hb + 1, hb + 1 + s);
+        c->ws_top = mk.top;
+        return h;
+    }
+
+    // Alg. 2, sytrf.cpp:298-335
+    HFact recursive_step(DMat A, const std::vector<int32_t>& rows, int64_t coff) {
+        const int64_t s = A.rows, m = s / 2, ns = s - m;
+        const WsMark mk{c->ws_top};
+        std::vector<int32_t> rows1(rows.begin(), rows.begin() + m);
+        HFact f1 = dispatch(A.sub(0, 0, m, m), rows1, coff);  // :303
+        const int64_t r1 = f1.rank;
+
+        // B' = P1^T B (:308)
+        DMat BP = ws_mat(c, m, ns);
+        gather_rows(st, BP, A.sub(0, m, m, ns), upload(c, f1.perm));
+        // [L1; M1] in f1's position order, from Lg
+        std::vector<int32_t> prow(m);
+        for (int64_t i = 0; i < m; ++i) prow[i] = rows[f1.perm[i]];
+        DMat LM = ws_mat(c, m, r1);
+        gather_lg(st, LM, Lg, upload(c, prow), coff);
+        DMat X = BP.sub(0, 0, r1, ns);
+        trsm_lower_unit(f, st, LM.sub(0, 0, r1, r1), X);  // :310
+        DMat Y = BP.sub(r1, 0, m - r1, ns);
+        gemm(f, st, GEMM_SUB, Y, LM.sub(r1, 0, m - r1, r1), false, X, false, m - r1, ns, r1);  // :312
+        DMat G = ws_mat(c, ns, r1);
+        inverse_apply_T(f, st, G, X, D, coff);  // :313
+        std::vector<int32_t> rows2(rows.begin() + m, rows.end());
+        scatter_lg(st, Lg, upload(c, rows2), coff, 1, G);  // rows m..s of N1 (:319-322)
+        DMat Z = A.sub(m, m, ns, ns);
+        gemm(f, st, GEMM_SUB, Z, G, false, X, false, ns, ns, r1);  // Z = C - G D1 G^T (:315)
+
+        std::vector<int32_t> rowsz;  // rows of [[0 Y],[Y^t Z]]
+        rowsz.reserve(s - r1);
+        for (int64_t i = r1; i < m; ++i) rowsz.push_back(rows[f1.perm[i]]);
+        for (int64_t i = m; i < s; ++i) rowsz.push_back(rows[i]);
+        HFact f2 = zero_leading(Y, Z, rowsz, coff + r1);  // :317
+
+        HFact h;  // P = compose(embed(P1,0,n), embed(P2,r1,n)) (:332-334)
+        h.rank = r1 + f2.rank;
+        h.perm.resize(s);
+        for (int64_t pos = 0; pos < r1; ++pos) h.perm[pos] = f1.perm[pos];
+        for (int64_t pos = r1; pos < s; ++pos) {
+            const int64_t cix = f2.perm[pos - r1];
+            h.perm[pos] = cix < m - r1 ? f1.perm[r1 + cix] : (int32_t)(m + (cix - (m - r1)));
+        }
+        c->ws_top = mk.top;
+        return h;
+    }
+
+    bool is_zero(DMat Y) {
+        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), st));
+        any_nonzero(st, Y, c->flag);
+        const int32_t v = *(const int32_t*)readback(c, c->flag, sizeof(int32_t));
+        return v == 0;
+    }
+
+    // sytrf.cpp:267-292
+    HFact zero_leading(DMat Y, DMat Z, const std::vector<int32_t>& rows, int64_t coff) {
+        const int64_t m = Y.rows, nz = Z.rows;
+        if (m == 0) return dispatch(Z, rows, coff);
+        HFact h;
+        if (nz == 0) {
+            h.perm.resize(m);
+            for (int64_t i = 0; i < m; ++i) h.perm[i] = (int32_t)i;
+            return h;
+        }
+        if (is_zero(Y)) {  // :274-290
+            std::vector<int32_t> rz(rows.begin() + m, rows.end());
+            HFact f3 = dispatch(Z, rz, coff);
+            const int64_t r3 = f3.rank;
+            h.rank = r3;
+            h.perm.resize(m + nz);
+            for (int64_t k = 0; k < r3; ++k) h.perm[k] = (int32_t)(m + f3.perm[k]);
+            for (int64_t t = 0; t < m; ++t) h.perm[r3 + t] = (int32_t)t;
+            for (int64_t k = r3; k < nz; ++k) h.perm[m + k] = (int32_t)(m + f3.perm[k]);
+            return h;
+        }
+        return zero_leading_pairs(Y, Z, rows, coff);
+    }
+
+    // PLDUQ of Y (destroyed); returns rank, fills row/col images and device factors.
+    struct Pl {
+        int64_t r;
+        std::vector<int32_t> rimg, cimg;
+        DMat L, U;
+        uint32_t *d, *dinv;
+    };
+    Pl run_plduq(DMat Y) {
+        const int64_t m = Y.rows, n = Y.cols, mn = std::min(m, n);
+        Pl pl;
+        int32_t* info = ws_vec<int32_t>(c, 1 + m + n + mn);
+        int32_t* colflag = ws_vec<int32_t>(c, n);
+        uint32_t* lvec = ws_vec<uint32_t>(c, m);
+        DMat Lo = ws_mat(c, m, mn), Uo = ws_mat(c, mn, n);
+        pl.d = ws_vec<uint32_t>(c, mn);
+        pl.dinv = ws_vec<uint32_t>(c, mn);
+        plduq(f, st, Y, info, colflag, lvec, Lo, pl.d, Uo);
+        const int32_t* hb = (const int32_t*)readback(c, info, (size_t)(1 + m + n) * sizeof(int32_t));
+        pl.r = hb[0];
+        pl.rimg.assign(hb + 1, hb + 1 + m);
+        pl.cimg.assign(hb + 1 + m, hb + 1 + m + n);
+        pl.L = Lo.sub(0, 0, m, pl.r);
+        pl.U = Uo.sub(0, 0, pl.r, n);
+        invert_vec(f, st, pl.dinv, pl.d, pl.r);
+        return pl;
+    }
+
+    // Solve X^T U1 + U1^T X = C1 for upper X (Alg. 1, trssyr2k.cpp) in closed
+    // form: Ct = U1^-T C1 U1^-1, Y = strict_upper(Ct) + diag(Ct)/2, X = Y U1.
+    // The solution is unique for odd p (and unique with zero diagonal for
+    // p = 2), so it equals the reference's halving recursion.  X -> Xout.
+    void trssyr2k_dev(DMat U1, DMat U1T, DMat C1, DMat Xout, int32_t* flag) {
+        const int64_t r = U1.rows;
+        if (r == 0) return;
+        const WsMark mk{c->ws_top};
+        trsm_lower_unit(f, st, U1T, C1);  // W = U1^-T C1 (in place)
+        DMat Wt = ws_mat(c, r, r);
+        transpose(st, Wt, C1);
+        trsm_lower_unit(f, st, U1T, Wt);  // Ct = U1^-T W^T
+        trssyr2k_mid(f, st, Wt, flag);
+        gemm(f, st, GEMM_SET, Xout, Wt, false, U1, false, r, r, r);
+        c->ws_top = mk.top;
+    }
+
+    // Alg. 3, sytrf.cpp:170-265
+    HFact zero_leading_pairs(DMat Y, DMat Z, const std::vector<int32_t>& rows, int64_t coff) {
+        const int64_t m = Y.rows, nz = Z.rows;
+        const WsMark mk{c->ws_top};
+        Pl py = run_plduq(Y);  // :175
+        const int64_t r = py.r;
+        const std::vector<int32_t>& q = py.cimg;
+
+        DMat Cp = ws_mat(c, nz, nz);  // C' = Q^T Z Q (:183)
+        gather_sym(st, Cp, Z, upload(c, q));
+        DMat C1 = Cp.sub(0, 0, r, r), C2 = Cp.sub(0, r, r, nz - r), C3 = Cp.sub(r, r, nz - r, nz - r);
+        DMat U1 = py.U.sub(0, 0, r, r), V1 = py.U.sub(0, r, r, nz - r);
+        DMat UpT = ws_mat(c, nz, r);  // [U1^T; V1^T]
+        transpose(st, UpT, py.U);
+        DMat U1T = UpT.sub(0, 0, r, r);
+
+        uint32_t* delta = nullptr;
+        if (f.char2) {  // :188-200
+            delta = ws_vec<uint32_t>(c, r);
+            char2_delta(f, st, C1, U1, delta);
+            DMat H = ws_mat(c, r, r);
+            scale_rows(f, st, H, U1, delta);
+            gemm(f, st, GEMM_SUB, C1, H, true, U1, false, r, r, r);  // C1 -= U1^T diag(delta) U1
+        }
+        DMat X = ws_mat(c, r, r);
+        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), st));
+        trssyr2k_dev(U1, U1T, C1, X, c->flag);  // :202
+        DMat G12 = ws_mat(c, nz, r);  // [G1; G2]
+        scale_T(f, st, G12.sub(0, 0, r, r), X, py.dinv);  // G1 = (diag(d)^-1 X)^T (:203)
+        if (f.char2) add_scaled_rows_upper(f, st, X, U1, delta);  // X += Delta U1 (:204-208)
+        gemm(f, st, GEMM_SUB, C2, X, true, V1, false, r, nz - r, r);  // C2 -= X^T V1 (:210)
+        trsm_lower_unit(f, st, U1T, C2);  // Y2 = U1^-T C2 (:211)
+        gemm(f, st, GEMM_SUB, C3, C2, true, V1, false, nz - r, nz - r, r);  // :213
+        gemm(f, st, GEMM_SUB, C3, V1, true, C2, false, nz - r, nz - r, r);
+        if (f.char2) {  // :214
+            DMat H = ws_mat(c, r, nz - r);
+            scale_rows(f, st, H, V1, delta);
+            gemm(f, st, GEMM_SUB, C3, H, true, V1, false, nz - r, nz - r, r);
+        }
+        scale_T(f, st, G12.sub(r, 0, nz - r, r), C2, py.dinv);  // G2 (:215)
+
+        // L columns [coff, coff + 2r) (:222-252), keyed by original row:
+        //   Y rows (row_perm order):  even columns <- [L1; M1]
+        //   Z rows (col_perm order):  even <- [G1; G2], odd <- [U1^T; V1^T]
+        std::vector<int32_t> idy(m), idz(nz);
+        for (int64_t a = 0; a < m; ++a) idy[a] = rows[py.rimg[a]];
+        for (int64_t a = 0; a < nz; ++a) idz[a] = rows[m + q[a]];
+        scatter_lg(st, Lg, upload(c, idy), coff, 2, py.L);
+        const int32_t* didz = upload(c, idz);
+        scatter_lg(st, Lg, didz, coff, 2, G12);
+        scatter_lg(st, Lg, didz, coff + 1, 2, UpT);
+        write_pair_diag(f, st, D, coff, py.d, py.dinv, delta, r);  // :254-260
+
+        std::vector<int32_t> rows3(idz.begin() + r, idz.end());
+        HFact f3 = dispatch(C3, rows3, coff + 2 * r);  // :217
+        const int64_t r3 = f3.rank;
+
+        HFact h;  // P_i interleave + rotations (:226-251)
+        h.rank = 2 * r + r3;
+        h.perm.resize(m + nz);
+        for (int64_t i = 0; i < r; ++i) {
+            h.perm[2 * i] = py.rimg[i];
+            h.perm[2 * i + 1] = (int32_t)(m + q[i]);
+        }
+        for (int64_t k = 0; k < nz - r; ++k) {
+            const int64_t row = k < r3 ? 2 * r + k : 2 * r + (m - r) + k;
+            h.perm[row] = (int32_t)(m + q[r + f3.perm[k]]);
+        }
+        for (int64_t t = 0; t < m - r; ++t) h.perm[2 * r + r3 + t] = py.rimg[r + t];
+        c->ws_top = mk.top;
+        return h;
+    }
+};
+
+// Estimated workspace for an n x n factorization (W, Lg, D, recursion temps).
+size_t workspace_bytes(int64_t n) {
+    const size_t n2 = (size_t)n * n * sizeof(uint32_t);
+    return 12 * n2 + 64 * (size_t)n * sizeof(uint32_t) + ((size_t)256 << 20);
+}
+
+int set_error(const std::exception& e) {
+    g_last_error = e.what();
+    if (const Status* s = dynamic_cast<const Status*>(&e)) return s->code;
+    if (dynamic_cast<const std::bad_alloc*>(&e)) return FFB_NO_MEMORY;
+    return FFB_ERROR;
+}
+
+template <class F>
+int guarded(ffb_context* c, F&& fn) {
+    try {
+        if (!c) throw Status(FFB_ERROR, "null context");
+        FFB_CUDA(cudaSetDevice(c->device));
+        const uint64_t l0 = g_launches;
+        fn();
+        c->launches = g_launches - l0;
+        g_last_error.clear();
+        return FFB_OK;
+    } catch (const std::exception& e) {
+        if (c) {
+            cudaStreamSynchronize(c->stream);
+            c->ws_top = 0;
+            c->up_top = 0;
+        }
+        return set_error(e);
+    }
+}
+
+struct DevFact {
+    int64_t n = 0, rank = 0;
+    std::vector<int32_t> perm;
+    DMat Lg;
+    DDiag D;
+};
+
+// Run the factorization of the n x n device matrix W (destroyed).
+DevFact run_ldlt(ffb_context* c, const Fp& f, DMat W, int variant, int64_t threshold,
+                 bool check_symmetric) {
+    const int64_t n = W.rows;
+    cudaStream_t st = c->stream;
+    DevFact out;
+    out.n = n;
+    if (check_symmetric) {  // ldlt validation, sytrf.cpp:355-356
+        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), st));
+        any_asymmetric(st, W, c->flag);
+        if (*(const int32_t*)readback(c, c->flag, sizeof(int32_t)))
+            throw Status(FFB_NOT_SYMMETRIC, "ldlt: matrix must be symmetric");
+    }
+    out.Lg = ws_mat(c, n, n);
+    zero_mat(st, out.Lg);
+    out.D.kind = ws_vec<int32_t>(c, n);
+    out.D.val = ws_vec<uint32_t>(c, n);
+    out.D.val2 = ws_vec<uint32_t>(c, n);
+    out.D.inv = ws_vec<uint32_t>(c, n);
+    Engine e{c, st, f, variant, (int64_t)threshold, out.Lg, out.D};
+    std::vector<int32_t> rows(n);
+    for (int64_t i = 0; i < n; ++i) rows[i] = (int32_t)i;
+    if (n > 0) {
+        HFact h = e.dispatch(W, rows, 0);
+        out.rank = h.rank;
+        out.perm = std::move(h.perm);
+    }
+    return out;
+}
+
+// Copy a device factorization to caller host buffers (uint64 element type).
+void export_host(ffb_context* c, const DevFact& df, int64_t* perm, void* lower, int lower_eb,
+                 int32_t* dkind, uint64_t* dval, uint64_t* dval2, size_t* rank) {
+    cudaStream_t st = c->stream;
+    const int64_t n = df.n, r = df.rank;
+    for (int64_t i = 0; i < n; ++i) perm[i] = df.perm[i];
+    *rank = (size_t)r;
+    if (n == 0) return;
+    if (r > 0) {
+        DMat Lout = ws_mat(c, n, r);
+        gather_lower_out(st, Lout, df.Lg, upload(c, df.perm));
+        void* dl = ws_alloc(c, (size_t)n * r * lower_eb);
+        convert_out(st, dl, lower_eb, Lout);
+        FFB_CUDA(cudaMemcpyAsync(lower, dl, (size_t)n * r * lower_eb, cudaMemcpyDeviceToHost, st));
+        std::vector<int32_t> k(r);
+        std::vector<uint32_t> v(r), v2(r);
+        FFB_CUDA(cudaMemcpyAsync(k.data(), df.D.kind, r * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        FFB_CUDA(cudaMemcpyAsync(v.data(), df.D.val, r * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        FFB_CUDA(cudaMemcpyAsync(v2.data(), df.D.val2, r * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        FFB_CUDA(cudaStreamSynchronize(st));
+        for (int64_t t = 0; t < r; ++t) {
+            dkind[t] = k[t];
+            dval[t] = v[t];
+            dval2[t] = v2[t];
+        }
+    }
+}
+
+// Upload a host matrix (elem bytes eb, dense rows x cols) into a fresh device view.
+DMat upload_matrix(ffb_context* c, const Fp& f, const void* h, int64_t rows, int64_t cols, int eb) {
+    DMat m = ws_mat(c, rows, cols);
+    if (rows * cols == 0) return m;
+    const size_t bytes = (size_t)rows * cols * eb;
+    void* tmp = ws_alloc(c, bytes);
+    FFB_CUDA(cudaMemcpyAsync(tmp, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    convert_in(f, c->stream, m, tmp, eb);
+    return m;
+}
+
+void download_matrix(ffb_context* c, DMat m, uint64_t* h) {
+    if (m.rows * m.cols == 0) return;
+    void* tmp = ws_alloc(c, (size_t)m.rows * m.cols * 8);
+    convert_out(c->stream, tmp, 8, m);
+    FFB_CUDA(cudaMemcpyAsync(h, tmp, (size_t)m.rows * m.cols * 8, cudaMemcpyDeviceToHost, c->stream));
+    FFB_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+int elem_bytes(int t) {
+    if (t == FFB_U8 || t == FFB_U16 || t == FFB_U32 || t == FFB_U64) return t;
+    throw Status(FFB_ERROR, "unknown element type");
+}
+
+}  // namespace
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+extern "C" {
+
+int ffb_version(void) { return 1; }
+
+const char* ffb_status_string(int s) {
+    switch (s) {
+    case FFB_OK: return "OK";
+    case FFB_DIMENSION_MISMATCH: return "DimensionMismatch";
+    case FFB_NOT_SYMMETRIC: return "NotSymmetric";
+    case FFB_NOT_PRIME: return "NotPrime";
+    case FFB_ZERO_INVERSE: return "ZeroInverse";
+    case FFB_CHAR_TWO_DIVISION: return "CharTwoDivision";
+    case FFB_NON_UNIT_TRIANGULAR: return "NonUnitTriangular";
+    case FFB_SINGULAR_TRIANGULAR: return "SingularTriangular";
+    case FFB_CHAR_TWO_NONZERO_DIAGONAL: return "CharTwoNonzeroDiagonal";
+    case FFB_BAD_BLOCK_SIZES: return "BadBlockSizes";
+    case FFB_NO_MEMORY: return "NoMemory";
+    case FFB_CUDA_ERROR: return "CudaError";
+    case FFB_UNSUPPORTED: return "Unsupported";
+    default: return "Error";
+    }
+}
+
+const char* ffb_last_error(void) { return g_last_error.c_str(); }
+
+int ffb_create(ffb_context** out, int device) {
+    try {
+        ffb_context* c = new ffb_context();
+        c->device = device;
+        FFB_CUDA(cudaSetDevice(device));
+        FFB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->up_cap = (size_t)64 << 20;
+        FFB_CUDA(cudaMallocHost(&c->up_host, c->up_cap));
+        c->down_cap = (size_t)16 << 20;
+        FFB_CUDA(cudaMallocHost(&c->down_host, c->down_cap));
+        FFB_CUDA(cudaMalloc(&c->flag, 256));
+        *out = c;
+        return FFB_OK;
+    } catch (const std::exception& e) {
+        *out = nullptr;
+        return set_error(e);
+    }
+}
+
+int ffb_destroy(ffb_context* c) {
+    if (!c) return FFB_OK;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    if (c->ws_base) cudaFree(c->ws_base);
+    if (c->inv_table) cudaFree(c->inv_table);
+    if (c->flag) cudaFree(c->flag);
+    if (c->up_host) cudaFreeHost(c->up_host);
+    if (c->down_host) cudaFreeHost(c->down_host);
+    cudaStreamDestroy(c->stream);
+    delete c;
+    return FFB_OK;
+}
+
+void* ffb_stream(ffb_context* c) { return c ? (void*)c->stream : nullptr; }
+uint64_t ffb_launch_count(ffb_context* c) { return c ? c->launches : 0; }
+
+int ffb_ldlt_compact(ffb_context* c, uint64_t p, size_t n, const void* a, int a_type, int variant,
+                     size_t threshold, int64_t* perm, void* lower, int lower_type, int32_t* dkind,
+                     uint64_t* dval, uint64_t* dval2, size_t* rank) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        const int aeb = elem_bytes(a_type), leb = elem_bytes(lower_type);
+        ensure_workspace(c, workspace_bytes((int64_t)n) + (size_t)n * n * (aeb + leb));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat W = upload_matrix(c, f, a, (int64_t)n, (int64_t)n, aeb);
+        DevFact df = run_ldlt(c, f, W, variant, (int64_t)threshold, true);
+        export_host(c, df, perm, lower, leb, dkind, dval, dval2, rank);
+        c->ws_top = 0;
+    });
+}
+
+int ffb_ldlt(ffb_context* c, uint64_t p, size_t rows, size_t cols, const uint64_t* a, int variant,
+             size_t threshold, int64_t* perm, uint64_t* lower, int32_t* dkind, uint64_t* dval,
+             uint64_t* dval2, size_t* rank) {
+    if (rows != cols) {
+        g_last_error = "ldlt: matrix must be square";
+        return FFB_DIMENSION_MISMATCH;  // sytrf.cpp:355
+    }
+    return ffb_ldlt_compact(c, p, rows, a, FFB_U64, variant, threshold, perm, lower, FFB_U64,
+                            dkind, dval, dval2, rank);
+}
+
+int ffb_ldlt_zero_leading(ffb_context* c, uint64_t p, size_t m, size_t ny, const uint64_t* y,
+                          size_t nz, const uint64_t* z, int variant, size_t threshold,
+                          int64_t* perm, uint64_t* lower, int32_t* dkind, uint64_t* dval,
+                          uint64_t* dval2, size_t* rank) {
+    return guarded(c, [&] {
+        if (ny != nz) throw Status(FFB_DIMENSION_MISMATCH, "ldlt_zero_leading: Y and Z have mismatched widths");
+        check_modulus(p);
+        const int64_t N = (int64_t)(m + nz);
+        ensure_workspace(c, workspace_bytes(N) + (size_t)N * N * 16);
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat Zd = upload_matrix(c, f, z, (int64_t)nz, (int64_t)nz, 8);
+        {
+            FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), c->stream));
+            any_asymmetric(c->stream, Zd, c->flag);
+            if (*(const int32_t*)readback(c, c->flag, sizeof(int32_t)))
+                throw Status(FFB_NOT_SYMMETRIC, "ldlt_zero_leading: Z must be symmetric");
+        }
+        DMat Yd = upload_matrix(c, f, y, (int64_t)m, (int64_t)nz, 8);
+        DevFact df;
+        df.n = N;
+        df.Lg = ws_mat(c, N, N);
+        zero_mat(c->stream, df.Lg);
+        df.D.kind = ws_vec<int32_t>(c, N);
+        df.D.val = ws_vec<uint32_t>(c, N);
+        df.D.val2 = ws_vec<uint32_t>(c, N);
+        df.D.inv = ws_vec<uint32_t>(c, N);
+        Engine e{c, c->stream, f, variant, (int64_t)threshold, df.Lg, df.D};
+        std::vector<int32_t> rows(N);
+        for (int64_t i = 0; i < N; ++i) rows[i] = (int32_t)i;
+        HFact h = e.zero_leading(Yd, Zd, rows, 0);
+        df.rank = h.rank;
+        df.perm = h.perm;
+        export_host(c, df, perm, lower, 8, dkind, dval, dval2, rank);
+        c->ws_top = 0;
+    });
+}
+
+int ffb_ldlt_device(ffb_context* c, uint64_t p, size_t n, uint32_t* d_a, size_t lda, int variant,
+                    size_t threshold, int32_t* d_perm, uint32_t* d_lower, size_t ldl,
+                    int32_t* d_dkind, uint32_t* d_dval, uint32_t* d_dval2, size_t* rank) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        ensure_workspace(c, workspace_bytes((int64_t)n));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat W;
+        W.ptr = d_a;
+        W.ld = (int64_t)lda;
+        W.rows = W.cols = (int64_t)n;
+        DevFact df = run_ldlt(c, f, W, variant, (int64_t)threshold, true);
+        const int64_t r = df.rank;
+        *rank = (size_t)r;
+        if (n > 0) {
+            const int32_t* dp = upload(c, df.perm);
+            FFB_CUDA(cudaMemcpyAsync(d_perm, dp, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
+            DMat Lout;
+            Lout.ptr = d_lower;
+            Lout.ld = (int64_t)ldl;
+            Lout.rows = (int64_t)n;
+            Lout.cols = r;
+            gather_lower_out(c->stream, Lout, df.Lg, dp);
+            if (r > 0) {
+                FFB_CUDA(cudaMemcpyAsync(d_dkind, df.D.kind, r * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
+                FFB_CUDA(cudaMemcpyAsync(d_dval, df.D.val, r * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
+                FFB_CUDA(cudaMemcpyAsync(d_dval2, df.D.val2, r * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
+            }
+        }
+        FFB_CUDA(cudaStreamSynchronize(c->stream));
+        c->ws_top = 0;
+    });
+}
+
+int ffb_plduq(ffb_context* c, uint64_t p, size_t m, size_t n, const uint64_t* b, int64_t* row_image,
+              int64_t* col_image, uint64_t* lower, uint64_t* diag, uint64_t* upper, size_t* rank) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        ensure_workspace(c, (size_t)(m + 1) * (n + 1) * 40 + ((size_t)64 << 20));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat Y = upload_matrix(c, f, b, (int64_t)m, (int64_t)n, 8);
+        Engine e{c, c->stream, f, FFB_VARIANT_CASCADE, 64, DMat(), DDiag()};
+        Engine::Pl pl = e.run_plduq(Y);
+        for (size_t i = 0; i < m; ++i) row_image[i] = pl.rimg[i];
+        for (size_t j = 0; j < n; ++j) col_image[j] = pl.cimg[j];
+        *rank = (size_t)pl.r;
+        if (pl.r > 0) {
+            download_matrix(c, pl.L, lower);
+            download_matrix(c, pl.U, upper);
+            std::vector<uint32_t> d(pl.r);
+            FFB_CUDA(cudaMemcpy(d.data(), pl.d, pl.r * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+            for (int64_t k = 0; k < pl.r; ++k) diag[k] = d[k];
+        }
+        c->ws_top = 0;
+    });
+}
+
+int ffb_trssyr2k(ffb_context* c, uint64_t p, size_t n, const uint64_t* u, const uint64_t* cc,
+                 uint64_t* x) {
+    return guarded(c, [&] {
+        check_modulus(p);  // validation order of trssyr2k.cpp:55-66
+        for (size_t i = 0; i < n; ++i)
+            if (u[i * n + i] % p != 1 % p)
+                throw Status(FFB_NON_UNIT_TRIANGULAR, "trssyr2k: U must have unit diagonal");
+        for (size_t i = 0; i < n; ++i)
+            for (size_t j = i + 1; j < n; ++j)
+                if (cc[i * n + j] % p != cc[j * n + i] % p)
+                    throw Status(FFB_NOT_SYMMETRIC, "trssyr2k: C must be symmetric");
+        if (n == 0) return;
+        ensure_workspace(c, (size_t)n * n * 64 + ((size_t)64 << 20));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        const int64_t N = (int64_t)n;
+        // Only the upper triangle of U is read (trssyr2k.hpp:8-10).
+        std::vector<uint64_t> hu(n * n), hut(n * n);
+        for (size_t i = 0; i < n; ++i)
+            for (size_t j = 0; j < n; ++j) {
+                hu[i * n + j] = (j >= i) ? u[i * n + j] % p : 0;
+                hut[j * n + i] = hu[i * n + j];
+            }
+        DMat U = upload_matrix(c, f, hu.data(), N, N, 8);
+        DMat UT = upload_matrix(c, f, hut.data(), N, N, 8);
+        DMat C = upload_matrix(c, f, cc, N, N, 8);
+        DMat X = ws_mat(c, N, N);
+        Engine e{c, c->stream, f, FFB_VARIANT_CASCADE, 64, DMat(), DDiag()};
+        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), c->stream));
+        e.trssyr2k_dev(U, UT, C, X, c->flag);
+        if (f.char2 && *(const int32_t*)readback(c, c->flag, sizeof(int32_t)))
+            throw Status(FFB_CHAR_TWO_NONZERO_DIAGONAL, "trssyr2k: diagonal entry has no solution");
+        download_matrix(c, X, x);
+        c->ws_top = 0;
+    });
+}
+
+// ---- kernels.hpp:13-32 --------------------------------------------------------
+int ffb_gemm_sub(ffb_context* c, uint64_t p, size_t m, size_t n, size_t k, uint64_t* cc,
+                 const uint64_t* a, const uint64_t* b) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        ensure_workspace(c, ((size_t)m * n + m * k + k * n) * 16 + ((size_t)64 << 20));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat C = upload_matrix(c, f, cc, m, n, 8), A = upload_matrix(c, f, a, m, k, 8),
+             B = upload_matrix(c, f, b, k, n, 8);
+        gemm(f, c->stream, GEMM_SUB, C, A, false, B, false, m, n, k);
+        download_matrix(c, C, cc);
+        c->ws_top = 0;
+    });
+}
+
+// Dense op(T) on the host (triangle/unit conventions of kernels.cpp:23-29).
+static std::vector<uint64_t> dense_op(const uint64_t* t, size_t n, uint64_t p, int upper, int trans,
+                                      int unit) {
+    std::vector<uint64_t> o(n * n, 0);
+    for (size_t i = 0; i < n; ++i)
+        for (size_t j = 0; j < n; ++j) {
+            size_t a = i, b = j;
+            if (trans) std::swap(a, b);
+            uint64_t v;
+            if (a == b) v = unit ? 1 % p : t[a * n + a] % p;
+            else v = ((upper == 0) ? (a > b) : (a < b)) ? t[a * n + b] % p : 0;
+            o[i * n + j] = v;
+        }
+    return o;
+}
+
+int ffb_trmm_sub(ffb_context* c, uint64_t p, size_t n, size_t ncols, uint64_t* cc, const uint64_t* t,
+                 int upper, int trans, int unit, const uint64_t* b) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        std::vector<uint64_t> o = dense_op(t, n, p, upper, trans, unit);
+        ensure_workspace(c, ((size_t)n * ncols * 2 + n * n) * 16 + ((size_t)64 << 20));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat C = upload_matrix(c, f, cc, n, ncols, 8), T = upload_matrix(c, f, o.data(), n, n, 8),
+             B = upload_matrix(c, f, b, n, ncols, 8);
+        gemm(f, c->stream, GEMM_SUB, C, T, false, B, false, n, ncols, n);
+        download_matrix(c, C, cc);
+        c->ws_top = 0;
+    });
+}
+
+int ffb_trsm_inplace(ffb_context* c, uint64_t p, size_t n, size_t ncols, const uint64_t* t, int upper,
+                     int trans, int unit, uint64_t* b) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        std::vector<uint64_t> o = dense_op(t, n, p, upper, trans, unit);
+        const bool lower = (upper == 0) != (trans != 0);
+        // kernels.cpp:64-71: the first zero pivot met in solve order raises
+        if (!unit)
+            for (size_t s = 0; s < n; ++s) {
+                const size_t i = lower ? s : n - 1 - s;
+                if (o[i * n + i] == 0) throw Status(FFB_SINGULAR_TRIANGULAR, "trsm_inplace: zero diagonal");
+            }
+        if (n == 0 || ncols == 0) return;
+        // Normalize to a unit lower solve: reverse the index order for upper,
+        // scale rows by the inverse diagonal for non-unit.
+        std::vector<uint64_t> L(n * n, 0), Bv(n * ncols);
+        std::vector<uint64_t> dinv(n, 1);
+        for (size_t i = 0; i < n; ++i) {
+            const uint64_t d = o[i * n + i];
+            dinv[i] = unit ? 1 : finv_euclid((uint32_t)p, (uint32_t)d);
+        }
+        auto idx = [&](size_t i) { return lower ? i : n - 1 - i; };
+        for (size_t i = 0; i < n; ++i) {
+            for (size_t k = 0; k < n; ++k)
+                L[i * n + k] = (k < i) ? (uint64_t)(((unsigned __int128)o[idx(i) * n + idx(k)] * dinv[idx(i)]) % p) : (k == i ? 1 : 0);
+            for (size_t j = 0; j < ncols; ++j)
+                Bv[i * ncols + j] = (uint64_t)(((unsigned __int128)(b[idx(i) * ncols + j] % p) * dinv[idx(i)]) % p);
+        }
+        ensure_workspace(c, ((size_t)n * ncols + n * n) * 16 + ((size_t)64 << 20));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat Ld = upload_matrix(c, f, L.data(), n, n, 8), Bd = upload_matrix(c, f, Bv.data(), n, ncols, 8);
+        trsm_lower_unit(f, c->stream, Ld, Bd);
+        download_matrix(c, Bd, Bv.data());
+        for (size_t i = 0; i < n; ++i)
+            for (size_t j = 0; j < ncols; ++j) b[idx(i) * ncols + j] = Bv[i * ncols + j];
+        c->ws_top = 0;
+    });
+}
+
+int ffb_syrdk_sub(ffb_context* c, uint64_t p, size_t n, size_t k, uint64_t* cc, const uint64_t* g,
+                  const int32_t* dkind, const uint64_t* dval, const uint64_t* dval2) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        ensure_workspace(c, ((size_t)n * n + 2 * n * k) * 16 + ((size_t)64 << 20));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat C = upload_matrix(c, f, cc, n, n, 8), G = upload_matrix(c, f, g, n, k, 8);
+        // D in the per-column encoding -> device arrays (inverse of val per column)
+        std::vector<int32_t> kk(k);
+        std::vector<uint64_t> v(k), v2(k), vi(k);
+        for (size_t t = 0; t < k; ++t) {
+            kk[t] = dkind[t];
+            v[t] = dval[t] % p;
+            v2[t] = dval2[t] % p;
+            if (v[t] == 0) throw Status(FFB_ZERO_INVERSE, "inverse of zero");
+            vi[t] = finv_euclid((uint32_t)p, (uint32_t)v[t]);
+        }
+        // C -= G D G^T = G (D G^T): H^T = D G^T computed as (G D^T)... use H = G*D
+        // (D symmetric), then C -= H G^T.
+        std::vector<uint64_t> hg(n * k), hgv(n * k);
+        std::vector<uint64_t> gh(n * k);
+        download_matrix(c, G, gh.data());
+        for (size_t i = 0; i < n; ++i)
+            for (size_t t = 0; t < k; ++t) {
+                const uint64_t* row = &gh[i * k];
+                uint64_t val;
+                if (kk[t] == FFB_D_SCALAR) val = (uint64_t)(((unsigned __int128)row[t] * v[t]) % p);
+                else if (kk[t] == FFB_D_ANTIDIAG_HEAD || kk[t] == FFB_D_ANTITRI_HEAD)
+                    val = (uint64_t)(((unsigned __int128)row[t + 1] * v[t]) % p);
+                else if (kk[t] == FFB_D_ANTIDIAG_TAIL) val = (uint64_t)(((unsigned __int128)row[t - 1] * v[t]) % p);
+                else val = (uint64_t)((((unsigned __int128)row[t - 1] * v[t]) + (unsigned __int128)row[t] * v2[t]) % p);
+                hg[i * k + t] = val;
+            }
+        DMat H = upload_matrix(c, f, hg.data(), n, k, 8);
+        gemm(f, c->stream, GEMM_SUB, C, H, false, G, true, n, n, k);
+        download_matrix(c, C, cc);
+        c->ws_top = 0;
+    });
+}
+
+int ffb_syr2k_sub(ffb_context* c, uint64_t p, size_t n, size_t k, uint64_t* cc, const uint64_t* a,
+                  const uint64_t* b) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        ensure_workspace(c, ((size_t)n * n + 2 * n * k) * 16 + ((size_t)64 << 20));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat C = upload_matrix(c, f, cc, n, n, 8), A = upload_matrix(c, f, a, k, n, 8),
+             B = upload_matrix(c, f, b, k, n, 8);
+        gemm(f, c->stream, GEMM_SUB, C, A, true, B, false, n, n, k);
+        gemm(f, c->stream, GEMM_SUB, C, B, true, A, false, n, n, k);
+        download_matrix(c, C, cc);
+        c->ws_top = 0;
+    });
+}
+
+}  // extern "C"

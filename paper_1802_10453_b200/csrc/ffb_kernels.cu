@@ -1,0 +1,907 @@
+// ffb_kernels.cu -- SIMT kernels of the PLDL^TP^T engine.
+//
+// Bandwidth-bound helpers (gathers, transposes, scaling), the Crout leaf
+// (Alg. 4), PLDUQ (row-order Crout with leftmost pivots), the small
+// triangular solves, and the generic modular GEMM used for every
+// contraction that the tcgen05 path (ffb_tc_gemm.cu) does not take.
+#include <algorithm>
+
+#include "ffb_kernels.cuh"
+
+namespace ffb {
+
+thread_local uint64_t g_launches = 0;
+
+static inline void count_launch() { ++g_launches; }
+
+// ===========================================================================
+// Generic modular GEMM (SIMT).  64x64 tile, 256 threads, 4x4 per thread,
+// uint64 accumulation with delayed reduction (p < 2^23: one reduction per
+// output; larger p: products reduced before accumulation).
+// ===========================================================================
+namespace {
+
+constexpr int GB_M = 64, GB_N = 64, GB_K = 16;
+
+template <bool TA, bool TB, bool kLargeP>
+__global__ void __launch_bounds__(256) k_gemm_simt(Fp f, int mode, uint32_t* __restrict__ C,
+                                                   int64_t ldc, const uint32_t* __restrict__ A,
+                                                   int64_t lda, const uint32_t* __restrict__ B,
+                                                   int64_t ldb, int64_t M, int64_t N, int64_t K) {
+    __shared__ uint32_t As[GB_K][GB_M + 4];
+    __shared__ uint32_t Bs[GB_K][GB_N + 4];
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    const int64_t m0 = (int64_t)blockIdx.y * GB_M, n0 = (int64_t)blockIdx.x * GB_N;
+    uint64_t acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0;
+
+    for (int64_t k0 = 0; k0 < K; k0 += GB_K) {
+        // A tile: (i, k) -> op(A)[m0+i][k0+k]
+        for (int e = threadIdx.x; e < GB_M * GB_K; e += 256) {
+            int i, k;
+            if (TA) { i = e % GB_M; k = e / GB_M; } else { k = e % GB_K; i = e / GB_K; }
+            const int64_t gi = m0 + i, gk = k0 + k;
+            uint32_t v = 0;
+            if (gi < M && gk < K) v = TA ? A[gk * lda + gi] : A[gi * lda + gk];
+            As[k][i] = v;
+        }
+        for (int e = threadIdx.x; e < GB_N * GB_K; e += 256) {
+            int j, k;
+            if (TB) { k = e % GB_K; j = e / GB_K; } else { j = e % GB_N; k = e / GB_N; }
+            const int64_t gj = n0 + j, gk = k0 + k;
+            uint32_t v = 0;
+            if (gj < N && gk < K) v = TB ? B[gj * ldb + gk] : B[gk * ldb + gj];
+            Bs[k][j] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < GB_K; ++k) {
+            uint32_t a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = As[k][ty + 16 * i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx + 16 * j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint64_t prod = (uint64_t)a[i] * b[j];
+                    acc[i][j] += kLargeP ? (uint64_t)red64(f, prod) : prod;
+                }
+        }
+        __syncthreads();
+        if (!kLargeP && ((k0 / GB_K) & 0x1FFF) == 0x1FFF) {  // 2^17 products: fold
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = red64(f, acc[i][j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int64_t gi = m0 + ty + 16 * i;
+        if (gi >= M) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t gj = n0 + tx + 16 * j;
+            if (gj >= N) continue;
+            const uint32_t v = red64(f, acc[i][j]);
+            uint32_t* c = C + gi * ldc + gj;
+            if (mode == GEMM_SUB) *c = fsub(f, *c, v);
+            else if (mode == GEMM_ADD) *c = fadd(f, *c, v);
+            else *c = v;
+        }
+    }
+}
+
+template <bool TA, bool TB>
+void launch_gemm_simt(const Fp& f, cudaStream_t st, int mode, DMat C, DMat A, DMat B, int64_t M,
+                      int64_t N, int64_t K) {
+    dim3 grid((unsigned)cdiv(N, GB_N), (unsigned)cdiv(M, GB_M));
+    if (f.p < (1u << 23))
+        k_gemm_simt<TA, TB, false><<<grid, 256, 0, st>>>(f, mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr,
+                                                          B.ld, M, N, K);
+    else
+        k_gemm_simt<TA, TB, true><<<grid, 256, 0, st>>>(f, mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr,
+                                                         B.ld, M, N, K);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+void gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
+          int64_t M, int64_t N, int64_t K) {
+    if (M <= 0 || N <= 0) return;
+    if (K <= 0) {
+        if (mode == GEMM_SET) zero_mat(st, C.sub(0, 0, M, N));
+        return;
+    }
+    if (!ta && !tb) launch_gemm_simt<false, false>(f, st, mode, C, A, B, M, N, K);
+    else if (ta && !tb) launch_gemm_simt<true, false>(f, st, mode, C, A, B, M, N, K);
+    else if (!ta && tb) launch_gemm_simt<false, true>(f, st, mode, C, A, B, M, N, K);
+    else launch_gemm_simt<true, true>(f, st, mode, C, A, B, M, N, K);
+}
+
+// ===========================================================================
+// Triangular solve with a unit lower triangular matrix.
+// Base: n <= 64, one thread per right-hand-side column, T and the column
+// slices staged in shared memory.  Larger n: recursive halving with GEMM.
+// ===========================================================================
+namespace {
+
+constexpr int TRSM_NB = 64;
+constexpr int TRSM_THREADS = 64;
+
+template <bool kLargeP>
+__global__ void __launch_bounds__(TRSM_THREADS) k_trsm_base(Fp f, const uint32_t* __restrict__ T,
+                                                            int64_t ldt, uint32_t* B, int64_t ldb,
+                                                            int n, int64_t ncols) {
+    __shared__ uint32_t Ts[TRSM_NB][TRSM_NB + 1];
+    __shared__ uint32_t Xs[TRSM_NB][TRSM_THREADS];
+    for (int e = threadIdx.x; e < n * n; e += TRSM_THREADS) {
+        const int i = e / n, k = e % n;
+        Ts[i][k] = (k < i) ? T[i * ldt + k] : 0;
+    }
+    const int64_t j = (int64_t)blockIdx.x * TRSM_THREADS + threadIdx.x;
+    const bool live = j < ncols;
+    if (live)
+        for (int i = 0; i < n; ++i) Xs[i][threadIdx.x] = B[i * ldb + j];
+    __syncthreads();
+    if (!live) return;
+    for (int i = 1; i < n; ++i) {
+        uint64_t acc = 0;
+        for (int k = 0; k < i; ++k) {
+            const uint64_t prod = (uint64_t)Ts[i][k] * Xs[k][threadIdx.x];
+            acc += kLargeP ? (uint64_t)red64(f, prod) : prod;
+        }
+        Xs[i][threadIdx.x] = fsub(f, Xs[i][threadIdx.x], red64(f, acc));
+    }
+    for (int i = 0; i < n; ++i) B[i * ldb + j] = Xs[i][threadIdx.x];
+}
+
+}  // namespace
+
+void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
+    const int64_t n = T.rows;
+    if (n <= 0 || B.cols <= 0) return;
+    if (n <= TRSM_NB) {
+        dim3 grid((unsigned)cdiv(B.cols, TRSM_THREADS));
+        if (f.p < (1u << 23))
+            k_trsm_base<false><<<grid, TRSM_THREADS, 0, st>>>(f, T.ptr, T.ld, B.ptr, B.ld, (int)n,
+                                                              B.cols);
+        else
+            k_trsm_base<true><<<grid, TRSM_THREADS, 0, st>>>(f, T.ptr, T.ld, B.ptr, B.ld, (int)n,
+                                                             B.cols);
+        count_launch();
+        FFB_CHECK_LAUNCH();
+        return;
+    }
+    int64_t n1 = (n / 2) / TRSM_NB * TRSM_NB;
+    if (n1 < TRSM_NB) n1 = TRSM_NB;
+    const int64_t n2 = n - n1;
+    DMat B1 = B.sub(0, 0, n1, B.cols), B2 = B.sub(n1, 0, n2, B.cols);
+    trsm_lower_unit(f, st, T.sub(0, 0, n1, n1), B1);
+    gemm(f, st, GEMM_SUB, B2, T.sub(n1, 0, n2, n1), false, B1, false, n2, B.cols, n1);
+    trsm_lower_unit(f, st, T.sub(n1, n1, n2, n2), B2);
+}
+
+// ===========================================================================
+// Bandwidth-bound data movement.
+// ===========================================================================
+namespace {
+
+__global__ void k_gather_rows(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
+                              const int32_t* idx, int64_t rows, int64_t cols) {
+    const int64_t i = blockIdx.y;
+    const uint32_t* s = src + (int64_t)idx[i] * lds;
+    uint32_t* d = dst + i * ldd;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        d[j] = s[j];
+}
+
+__global__ void k_gather_sym(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
+                             const int32_t* ridx, const int32_t* idx, int64_t n) {
+    const int64_t a = blockIdx.y;
+    const uint32_t* s = src + (int64_t)ridx[a] * lds;
+    uint32_t* d = dst + a * ldd;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < n;
+         b += (int64_t)gridDim.x * blockDim.x)
+        d[b] = s[idx[b]];
+}
+
+__global__ void k_transpose(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
+                            int64_t rows, int64_t cols) {
+    __shared__ uint32_t tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t r = r0 + k, c = c0 + threadIdx.x;
+        if (r < rows && c < cols) tile[k][threadIdx.x] = src[r * lds + c];
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t c = c0 + k, r = r0 + threadIdx.x;
+        if (r < rows && c < cols) dst[c * ldd + r] = tile[threadIdx.x][k];
+    }
+}
+
+__global__ void k_scatter_lg(uint32_t* Lg, int64_t ldl, const int32_t* ids, int64_t col0,
+                             int cstride, const uint32_t* src, int64_t lds, int64_t rows,
+                             int64_t cols) {
+    const int64_t i = blockIdx.y;
+    uint32_t* d = Lg + (int64_t)ids[i] * ldl + col0;
+    const uint32_t* s = src + i * lds;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        d[j * cstride] = s[j];
+}
+
+__global__ void k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int64_t ldl,
+                            const int32_t* ids, int64_t col0, int64_t cols) {
+    const int64_t i = blockIdx.y;
+    const uint32_t* s = Lg + (int64_t)ids[i] * ldl + col0;
+    uint32_t* d = dst + i * ldd;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        d[j] = s[j];
+}
+
+// G[j][k] = (D^-1 X)[k][j], X is r x ncols.  Tile: 32 k x 32 j, with one
+// extra row on each side for the 2x2 partners.
+__global__ void k_inverse_apply_T(Fp f, uint32_t* G, int64_t ldg, const uint32_t* X,
+                                  int64_t ldx, int64_t r, int64_t ncols, DDiag D, int64_t coff) {
+    __shared__ uint32_t tile[34][33];
+    const int64_t k0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+    for (int kk = threadIdx.y; kk < 34; kk += blockDim.y) {
+        const int64_t k = k0 - 1 + kk, j = j0 + threadIdx.x;
+        tile[kk][threadIdx.x] = (k >= 0 && k < r && j < ncols) ? X[k * ldx + j] : 0;
+    }
+    __syncthreads();
+    for (int jj = threadIdx.y; jj < 32; jj += blockDim.y) {
+        const int64_t j = j0 + jj, k = k0 + threadIdx.x;
+        if (j >= ncols || k >= r) continue;
+        const int kk = threadIdx.x + 1;
+        const int32_t kind = D.kind[coff + k];
+        const uint32_t inv = D.inv[coff + k];
+        uint32_t v;
+        if (kind == D_SCALAR) {
+            v = fmul(f, inv, tile[kk][jj]);
+        } else if (kind == D_ANTIDIAG_HEAD) {
+            v = fmul(f, inv, tile[kk + 1][jj]);
+        } else if (kind == D_ANTIDIAG_TAIL || kind == D_ANTITRI_TAIL) {
+            v = fmul(f, inv, tile[kk - 1][jj]);
+        } else {  // AntiTri head: -d c^-2 x_t + c^-1 x_{t+1}   (blockdiag.hpp:127-134)
+            const uint32_t top = fneg(f, fmul(f, D.val2[coff + k], fmul(f, inv, inv)));
+            v = fadd(f, fmul(f, top, tile[kk][jj]), fmul(f, inv, tile[kk + 1][jj]));
+        }
+        G[j * ldg + k] = v;
+    }
+}
+
+__global__ void k_scale_T(Fp f, uint32_t* G, int64_t ldg, const uint32_t* X, int64_t ldx,
+                          int64_t r, int64_t ncols, const uint32_t* dinv) {
+    __shared__ uint32_t tile[32][33];
+    const int64_t k0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
+    for (int kk = threadIdx.y; kk < 32; kk += blockDim.y) {
+        const int64_t k = k0 + kk, j = j0 + threadIdx.x;
+        tile[kk][threadIdx.x] = (k < r && j < ncols) ? fmul(f, dinv[k], X[k * ldx + j]) : 0;
+    }
+    __syncthreads();
+    for (int jj = threadIdx.y; jj < 32; jj += blockDim.y) {
+        const int64_t j = j0 + jj, k = k0 + threadIdx.x;
+        if (j < ncols && k < r) G[j * ldg + k] = tile[threadIdx.x][jj];
+    }
+}
+
+__global__ void k_invert_vec(Fp f, uint32_t* out, const uint32_t* v, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) out[i] = finv(f, v[i]);
+}
+
+__global__ void k_any_nonzero(const uint32_t* m, int64_t ld, int64_t rows, int64_t cols,
+                              int32_t* flag) {
+    const int64_t i = blockIdx.y;
+    int found = 0;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        found |= m[i * ld + j] != 0;
+    if (__syncthreads_or(found) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+__global__ void k_any_asym(const uint32_t* a, int64_t ld, int64_t n, int32_t* flag) {
+    __shared__ uint32_t tile[32][33];
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    if (c0 > r0 + 31) return;  // only blocks touching the lower triangle
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t r = c0 + k, c = r0 + threadIdx.x;  // transposed tile
+        if (r < n && c < n) tile[k][threadIdx.x] = a[r * ld + c];
+    }
+    __syncthreads();
+    int bad = 0;
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t r = r0 + k, c = c0 + threadIdx.x;
+        if (r < n && c < n) bad |= a[r * ld + c] != tile[threadIdx.x][k];
+    }
+    if (__syncthreads_or(bad) && threadIdx.x == 0 && threadIdx.y == 0) atomicOr(flag, 1);
+}
+
+__global__ void k_trssyr2k_mid(Fp f, uint32_t* C, int64_t ld, int64_t n, int32_t* flag) {
+    const int64_t i = blockIdx.y;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t* c = C + i * ld + j;
+        if (j < i) {
+            *c = 0;
+        } else if (j == i) {
+            if (f.char2) {
+                if (*c) atomicOr(flag, 1);
+                *c = 0;
+            } else {
+                *c = fhalve(f, *c);
+            }
+        }
+    }
+}
+
+__global__ void k_write_pair_diag(DDiag D, int64_t coff, const uint32_t* d, const uint32_t* dinv,
+                                  const uint32_t* delta, int64_t r) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= r) return;
+    const uint32_t dl = delta ? delta[i] : 0;
+    const int64_t t = coff + 2 * i;
+    D.kind[t] = dl ? D_ANTITRI_HEAD : D_ANTIDIAG_HEAD;
+    D.kind[t + 1] = dl ? D_ANTITRI_TAIL : D_ANTIDIAG_TAIL;
+    D.val[t] = D.val[t + 1] = d[i];
+    D.val2[t] = D.val2[t + 1] = dl;
+    D.inv[t] = D.inv[t + 1] = dinv[i];
+}
+
+__global__ void k_char2_delta(Fp f, const uint32_t* C1, int64_t ldc, const uint32_t* U1,
+                              int64_t ldu, int64_t r, uint32_t* delta) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    for (int64_t i = 0; i < r; ++i) {
+        uint32_t acc = C1[i * ldc + i];
+        for (int64_t j = 0; j < i; ++j) {
+            const uint32_t u = U1[j * ldu + i];
+            acc = fsub(f, acc, fmul(f, fmul(f, delta[j], u), u));
+        }
+        delta[i] = acc;
+    }
+}
+
+__global__ void k_scale_rows(Fp f, uint32_t* H, int64_t ldh, const uint32_t* S, int64_t lds,
+                             int64_t cols, const uint32_t* v) {
+    const int64_t i = blockIdx.y;
+    const uint32_t s = v[i];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        H[i * ldh + j] = fmul(f, s, S[i * lds + j]);
+}
+
+__global__ void k_add_scaled_rows_upper(Fp f, uint32_t* X, int64_t ldx, const uint32_t* U,
+                                        int64_t ldu, int64_t cols, const uint32_t* v) {
+    const int64_t i = blockIdx.y;
+    const uint32_t s = v[i];
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        if (j >= i) X[i * ldx + j] = fadd(f, X[i * ldx + j], fmul(f, s, U[i * ldu + j]));
+}
+
+__global__ void k_zero(uint32_t* m, int64_t ld, int64_t cols) {
+    const int64_t i = blockIdx.y;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        m[i * ld + j] = 0;
+}
+
+template <typename T>
+__global__ void k_convert_in(Fp f, uint32_t* dst, int64_t ldd, const T* src, int64_t rows,
+                             int64_t cols) {
+    const int64_t i = blockIdx.y;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const uint64_t v = (uint64_t)src[i * cols + j];
+        dst[i * ldd + j] = red64(f, v);
+    }
+}
+
+template <typename T>
+__global__ void k_convert_out(T* dst, const uint32_t* src, int64_t lds, int64_t rows,
+                              int64_t cols) {
+    const int64_t i = blockIdx.y;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        dst[i * cols + j] = (T)src[i * lds + j];
+}
+
+inline dim3 rowgrid(int64_t rows, int64_t cols, int threads = 256) {
+    int64_t gx = cdiv(cols, threads);
+    if (gx > 64) gx = 64;
+    if (gx < 1) gx = 1;
+    return dim3((unsigned)gx, (unsigned)rows);
+}
+
+}  // namespace
+
+// Row-indexed launches put rows on grid.y (max 65535); split bigger jobs.
+#define FFB_ROWCHUNK 65535
+
+void gather_rows(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
+    if (dst.rows <= 0 || dst.cols <= 0) return;
+    for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
+        const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
+        k_gather_rows<<<rowgrid(nr, dst.cols), 256, 0, st>>>(dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
+                                                             src.ld, idx + r0, nr, dst.cols);
+        count_launch();
+    }
+    FFB_CHECK_LAUNCH();
+}
+
+void gather_sym(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
+    if (dst.rows <= 0) return;
+    for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
+        const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
+        k_gather_sym<<<rowgrid(nr, dst.cols), 256, 0, st>>>(dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
+                                                            src.ld, idx + r0, idx, dst.cols);
+        count_launch();
+    }
+    FFB_CHECK_LAUNCH();
+}
+
+void transpose(cudaStream_t st, DMat dst, DMat src) {
+    if (src.rows <= 0 || src.cols <= 0) return;
+    dim3 grid((unsigned)cdiv(src.cols, 32), (unsigned)cdiv(src.rows, 32));
+    k_transpose<<<grid, dim3(32, 8), 0, st>>>(dst.ptr, dst.ld, src.ptr, src.ld, src.rows, src.cols);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int cstride, DMat src) {
+    if (src.rows <= 0 || src.cols <= 0) return;
+    for (int64_t r0 = 0; r0 < src.rows; r0 += FFB_ROWCHUNK) {
+        const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, src.rows - r0);
+        k_scatter_lg<<<rowgrid(nr, src.cols), 256, 0, st>>>(Lg.ptr, Lg.ld, ids + r0, col0, cstride,
+                                                            src.ptr + r0 * src.ld, src.ld, nr,
+                                                            src.cols);
+        count_launch();
+    }
+    FFB_CHECK_LAUNCH();
+}
+
+void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t col0) {
+    if (dst.rows <= 0 || dst.cols <= 0) return;
+    for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
+        const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
+        k_gather_lg<<<rowgrid(nr, dst.cols), 256, 0, st>>>(dst.ptr + r0 * dst.ld, dst.ld, Lg.ptr,
+                                                           Lg.ld, ids + r0, col0, dst.cols);
+        count_launch();
+    }
+    FFB_CHECK_LAUNCH();
+}
+
+void inverse_apply_T(const Fp& f, cudaStream_t st, DMat G, DMat X, DDiag D, int64_t coff) {
+    if (X.rows <= 0 || X.cols <= 0) return;
+    dim3 grid((unsigned)cdiv(X.cols, 32), (unsigned)cdiv(X.rows, 32));
+    k_inverse_apply_T<<<grid, dim3(32, 8), 0, st>>>(f, G.ptr, G.ld, X.ptr, X.ld, X.rows, X.cols, D,
+                                                    coff);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void scale_T(const Fp& f, cudaStream_t st, DMat G, DMat X, const uint32_t* dinv) {
+    if (X.rows <= 0 || X.cols <= 0) return;
+    dim3 grid((unsigned)cdiv(X.cols, 32), (unsigned)cdiv(X.rows, 32));
+    k_scale_T<<<grid, dim3(32, 8), 0, st>>>(f, G.ptr, G.ld, X.ptr, X.ld, X.rows, X.cols, dinv);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void invert_vec(const Fp& f, cudaStream_t st, uint32_t* out, const uint32_t* v, int64_t n) {
+    if (n <= 0) return;
+    k_invert_vec<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(f, out, v, n);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void any_nonzero(cudaStream_t st, DMat m, int32_t* flag) {
+    if (m.rows <= 0 || m.cols <= 0) return;
+    for (int64_t r0 = 0; r0 < m.rows; r0 += FFB_ROWCHUNK) {
+        const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, m.rows - r0);
+        k_any_nonzero<<<rowgrid(nr, m.cols), 256, 0, st>>>(m.ptr + r0 * m.ld, m.ld, nr, m.cols, flag);
+        count_launch();
+    }
+    FFB_CHECK_LAUNCH();
+}
+
+void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag) {
+    if (a.rows <= 1) return;
+    dim3 grid((unsigned)cdiv(a.rows, 32), (unsigned)cdiv(a.rows, 32));
+    k_any_asym<<<grid, dim3(32, 8), 0, st>>>(a.ptr, a.ld, a.rows, flag);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void trssyr2k_mid(const Fp& f, cudaStream_t st, DMat Ct, int32_t* flag) {
+    if (Ct.rows <= 0) return;
+    k_trssyr2k_mid<<<rowgrid(Ct.rows, Ct.cols), 256, 0, st>>>(f, Ct.ptr, Ct.ld, Ct.rows, flag);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void write_pair_diag(const Fp& f, cudaStream_t st, DDiag D, int64_t coff, const uint32_t* d,
+                     const uint32_t* dinv, const uint32_t* delta, int64_t r) {
+    (void)f;
+    if (r <= 0) return;
+    k_write_pair_diag<<<(unsigned)cdiv(r, 256), 256, 0, st>>>(D, coff, d, dinv, delta, r);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void char2_delta(const Fp& f, cudaStream_t st, DMat C1, DMat U1, uint32_t* delta) {
+    if (C1.rows <= 0) return;
+    k_char2_delta<<<1, 32, 0, st>>>(f, C1.ptr, C1.ld, U1.ptr, U1.ld, C1.rows, delta);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void scale_rows(const Fp& f, cudaStream_t st, DMat H, DMat S, const uint32_t* v) {
+    if (S.rows <= 0 || S.cols <= 0) return;
+    k_scale_rows<<<rowgrid(S.rows, S.cols), 256, 0, st>>>(f, H.ptr, H.ld, S.ptr, S.ld, S.cols, v);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void add_scaled_rows_upper(const Fp& f, cudaStream_t st, DMat X, DMat U, const uint32_t* v) {
+    if (X.rows <= 0) return;
+    k_add_scaled_rows_upper<<<rowgrid(X.rows, X.cols), 256, 0, st>>>(f, X.ptr, X.ld, U.ptr, U.ld,
+                                                                     X.cols, v);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void zero_mat(cudaStream_t st, DMat m) {
+    if (m.rows <= 0 || m.cols <= 0) return;
+    if (m.ld == m.cols) {
+        FFB_CUDA(cudaMemsetAsync(m.ptr, 0, (size_t)m.rows * m.cols * sizeof(uint32_t), st));
+        return;
+    }
+    for (int64_t r0 = 0; r0 < m.rows; r0 += FFB_ROWCHUNK) {
+        const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, m.rows - r0);
+        k_zero<<<rowgrid(nr, m.cols), 256, 0, st>>>(m.ptr + r0 * m.ld, m.ld, m.cols);
+        count_launch();
+    }
+    FFB_CHECK_LAUNCH();
+}
+
+void convert_in(const Fp& f, cudaStream_t st, DMat dst, const void* src, int eb) {
+    for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
+        const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
+        dim3 g = rowgrid(nr, dst.cols);
+        uint32_t* d = dst.ptr + r0 * dst.ld;
+        const size_t off = (size_t)r0 * dst.cols;
+        if (eb == 8) k_convert_in<uint64_t><<<g, 256, 0, st>>>(f, d, dst.ld, (const uint64_t*)src + off, nr, dst.cols);
+        else if (eb == 4) k_convert_in<uint32_t><<<g, 256, 0, st>>>(f, d, dst.ld, (const uint32_t*)src + off, nr, dst.cols);
+        else if (eb == 2) k_convert_in<uint16_t><<<g, 256, 0, st>>>(f, d, dst.ld, (const uint16_t*)src + off, nr, dst.cols);
+        else k_convert_in<uint8_t><<<g, 256, 0, st>>>(f, d, dst.ld, (const uint8_t*)src + off, nr, dst.cols);
+        count_launch();
+    }
+    FFB_CHECK_LAUNCH();
+}
+
+void convert_out(cudaStream_t st, void* dst, int eb, DMat src) {
+    for (int64_t r0 = 0; r0 < src.rows; r0 += FFB_ROWCHUNK) {
+        const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, src.rows - r0);
+        dim3 g = rowgrid(nr, src.cols);
+        const uint32_t* s = src.ptr + r0 * src.ld;
+        const size_t off = (size_t)r0 * src.cols;
+        if (eb == 8) k_convert_out<uint64_t><<<g, 256, 0, st>>>((uint64_t*)dst + off, s, src.ld, nr, src.cols);
+        else if (eb == 4) k_convert_out<uint32_t><<<g, 256, 0, st>>>((uint32_t*)dst + off, s, src.ld, nr, src.cols);
+        else if (eb == 2) k_convert_out<uint16_t><<<g, 256, 0, st>>>((uint16_t*)dst + off, s, src.ld, nr, src.cols);
+        else k_convert_out<uint8_t><<<g, 256, 0, st>>>((uint8_t*)dst + off, s, src.ld, nr, src.cols);
+        count_launch();
+    }
+    FFB_CHECK_LAUNCH();
+}
+
+void gather_lower_out(cudaStream_t st, DMat out, DMat Lg, const int32_t* perm) {
+    gather_lg(st, out, Lg, perm, 0);
+}
+
+// ===========================================================================
+// Crout leaf, Alg. 4 (sytrf.cpp:35-139), executed right-looking.
+//
+// The reference recomputes each residual column from the stored multipliers
+// (Crout); here the Schur complement S of the active rows is kept updated
+// instead, which yields the same field values.  Rows are visited in index
+// order (the rotations of `order` never reorder the unprocessed rows,
+// sytrf.cpp:93,128-129); the first nonzero of the residual column among the
+// active rows selects a 1x1 (j == front) or 2x2 antidiagonal pivot.
+// ===========================================================================
+namespace {
+
+constexpr int LEAF_THREADS = 256;
+constexpr int LEAF_SMEM_MAX_S = 200;
+
+struct LeafState {  // laid out after S in (shared or global) scratch
+    int32_t* status;  // 0 active, 1 pivot, 2 pivotless
+    uint32_t* l1;
+    uint32_t* l2;
+    uint32_t* u1;
+    uint32_t* u2;
+};
+
+__global__ void __launch_bounds__(LEAF_THREADS)
+    k_leaf_crout(Fp f, const uint32_t* __restrict__ A, int64_t lda, int s, uint32_t* gscratch,
+                 int use_smem, const int32_t* __restrict__ rows, uint32_t* Lg, int64_t ldL,
+                 int64_t coff, DDiag D, int32_t* out) {
+    extern __shared__ uint32_t smem[];
+    uint32_t* base = use_smem ? smem : gscratch;
+    uint32_t* S = base;
+    LeafState st;
+    st.status = (int32_t*)(base + (size_t)s * s);
+    st.l1 = (uint32_t*)(st.status + s);
+    st.l2 = st.l1 + s;
+    st.u1 = st.l2 + s;
+    st.u2 = st.u1 + s;
+    __shared__ int jmin;
+    __shared__ uint32_t sx, sxi, syeff, syd;
+    const int tid = threadIdx.x;
+
+    for (int e = tid; e < s * s; e += LEAF_THREADS) S[e] = A[(int64_t)(e / s) * lda + (e % s)];
+    for (int i = tid; i < s; i += LEAF_THREADS) st.status[i] = 0;
+    __syncthreads();
+
+    int r = 0;
+    int npl = 0;  // pivotless rows found so far (their order is ascending)
+    for (int p1 = 0; p1 < s; ++p1) {
+        if (st.status[p1] != 0) continue;  // consumed as a 2x2 partner (uniform)
+        if (tid == 0) jmin = s;
+        __syncthreads();
+        for (int i = p1 + tid; i < s; i += LEAF_THREADS)
+            if (st.status[i] == 0 && S[(size_t)i * s + p1] != 0) atomicMin(&jmin, i);
+        __syncthreads();
+        const int j = jmin;
+        if (j == s) {  // zero residual column: pivotless (sytrf.cpp:82-85)
+            if (tid == 0) {
+                st.status[p1] = 2;
+                out[1 + (s - 1 - npl)] = p1;  // temporarily stored from the back
+            }
+            ++npl;
+            __syncthreads();
+            continue;
+        }
+        if (j == p1) {  // 1x1 pivot (sytrf.cpp:87-97)
+            if (tid == 0) {
+                const uint32_t x = S[(size_t)p1 * s + p1];
+                const uint32_t xi = finv(f, x);
+                sx = x;
+                sxi = xi;
+                D.kind[coff + r] = D_SCALAR;
+                D.val[coff + r] = x;
+                D.val2[coff + r] = 0;
+                D.inv[coff + r] = xi;
+                Lg[(int64_t)rows[p1] * ldL + coff + r] = 1 % f.p;
+                st.status[p1] = 1;
+                out[1 + r] = p1;
+            }
+            __syncthreads();
+            const uint32_t xi = sxi;
+            for (int i = p1 + 1 + tid; i < s; i += LEAF_THREADS) {
+                if (st.status[i] != 0) continue;
+                const uint32_t l = fmul(f, S[(size_t)i * s + p1], xi);
+                st.l1[i] = l;
+                Lg[(int64_t)rows[i] * ldL + coff + r] = l;
+            }
+            __syncthreads();
+            const int w = s - p1 - 1;
+            for (int e = tid; e < w * w; e += LEAF_THREADS) {
+                const int i = p1 + 1 + e / w, k = p1 + 1 + e % w;
+                if (st.status[i] != 0 || st.status[k] != 0) continue;
+                uint32_t* sik = &S[(size_t)i * s + k];
+                *sik = fsub(f, *sik, fmul(f, S[(size_t)i * s + p1], st.l1[k]));
+            }
+            r += 1;
+            __syncthreads();
+            continue;
+        }
+        // 2x2 antidiagonal pivot pairing p1 with p2 = j (sytrf.cpp:99-131)
+        const int p2 = j;
+        if (tid == 0) {
+            const uint32_t x = S[(size_t)p2 * s + p1];
+            const uint32_t xi = finv(f, x);
+            const uint32_t y = S[(size_t)p2 * s + p2];
+            const uint32_t y_eff = f.char2 ? y : fhalve(f, y);
+            const uint32_t yd = f.char2 ? y : 0;  // AntiTri d (char 2 only)
+            sx = x;
+            sxi = xi;
+            syeff = y_eff;
+            syd = yd;
+            const int32_t hk = yd ? D_ANTITRI_HEAD : D_ANTIDIAG_HEAD;
+            D.kind[coff + r] = hk;
+            D.kind[coff + r + 1] = hk + 1;
+            D.val[coff + r] = D.val[coff + r + 1] = x;
+            D.val2[coff + r] = D.val2[coff + r + 1] = yd;
+            D.inv[coff + r] = D.inv[coff + r + 1] = xi;
+            Lg[(int64_t)rows[p1] * ldL + coff + r] = 1 % f.p;
+            Lg[(int64_t)rows[p2] * ldL + coff + r + 1] = 1 % f.p;
+            Lg[(int64_t)rows[p2] * ldL + coff + r] = f.char2 ? 0 : fmul(f, xi, y_eff);
+            st.status[p1] = 1;
+            st.status[p2] = 1;
+            out[1 + r] = p1;
+            out[2 + r] = p2;
+        }
+        __syncthreads();
+        {
+            const uint32_t x = sx, xi = sxi, y_eff = syeff;
+            for (int i = p1 + 1 + tid; i < s; i += LEAF_THREADS) {
+                if (st.status[i] != 0) continue;
+                const uint32_t l2 = fmul(f, xi, S[(size_t)i * s + p1]);
+                const uint32_t l1 = fmul(f, xi, fsub(f, S[(size_t)i * s + p2], fmul(f, y_eff, l2)));
+                st.l1[i] = l1;
+                st.l2[i] = l2;
+                st.u1[i] = fmul(f, x, l1);
+                st.u2[i] = fmul(f, x, l2);
+                Lg[(int64_t)rows[i] * ldL + coff + r] = l1;
+                Lg[(int64_t)rows[i] * ldL + coff + r + 1] = l2;
+            }
+        }
+        __syncthreads();
+        {
+            const uint32_t yd = syd;
+            const int w = s - p1 - 1;
+            for (int e = tid; e < w * w; e += LEAF_THREADS) {
+                const int i = p1 + 1 + e / w, k = p1 + 1 + e % w;
+                if (st.status[i] != 0 || st.status[k] != 0) continue;
+                uint64_t t = (uint64_t)st.u1[i] * st.l2[k] + (uint64_t)st.u2[i] * st.l1[k];
+                uint32_t v = red64(f, t);
+                if (yd) v = fadd(f, v, fmul(f, fmul(f, yd, st.l2[i]), st.l2[k]));
+                uint32_t* sik = &S[(size_t)i * s + k];
+                *sik = fsub(f, *sik, v);
+            }
+        }
+        r += 2;
+        __syncthreads();
+    }
+    // Pivotless rows were stored from the back in ascending order of discovery;
+    // reverse them into positions [r, s).
+    __syncthreads();
+    if (tid == 0) {
+        out[0] = r;
+        for (int a = 0, b = npl - 1; a < b; ++a, --b) {
+            const int32_t t = out[1 + r + a];
+            out[1 + r + a] = out[1 + r + b];
+            out[1 + r + b] = t;
+        }
+    }
+}
+
+}  // namespace
+
+size_t leaf_scratch_words(int64_t s) { return (size_t)s * s + 5 * (size_t)s + 8; }
+
+void leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
+                DDiag D, int32_t* out, uint32_t* scratch) {
+    const int s = (int)A.rows;
+    const bool smem = s <= LEAF_SMEM_MAX_S;
+    size_t bytes = smem ? leaf_scratch_words(s) * sizeof(uint32_t) : 0;
+    if (smem && bytes > 48 * 1024) {
+        FFB_CUDA(cudaFuncSetAttribute(k_leaf_crout, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)bytes));
+    }
+    k_leaf_crout<<<1, LEAF_THREADS, bytes, st>>>(f, A.ptr, A.ld, s, scratch, smem ? 1 : 0, rows,
+                                                 Lg.ptr, Lg.ld, coff, D, out);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+// ===========================================================================
+// PLDUQ (plduq.cpp:36-123), right-looking row-order Crout in one CTA.
+// Rows are processed in order; the pivot of a row is the leftmost nonzero of
+// its residual over non-pivot columns.  W keeps the reference's packed
+// storage: U coefficients in pivot rows, L multipliers in pivot columns,
+// explicit zeros for rows that went pivotless before a pivot column appeared.
+// ===========================================================================
+namespace {
+
+constexpr int PLDUQ_THREADS = 1024;
+
+__global__ void __launch_bounds__(PLDUQ_THREADS)
+    k_plduq_v1(Fp f, uint32_t* W, int64_t ldw, int m, int n, int32_t* info, int32_t* colflag,
+               uint32_t* lvec, uint32_t* Lo, int64_t ldlo, uint32_t* d, uint32_t* Uo, int64_t lduo) {
+    __shared__ int jmin;
+    __shared__ uint32_t sxi;
+    const int tid = threadIdx.x;
+    int32_t* row_image = info + 1;
+    int32_t* col_image = info + 1 + m;
+    int32_t* pc = info + 1 + m + n;
+    for (int j = tid; j < n; j += PLDUQ_THREADS) colflag[j] = 0;
+    __syncthreads();
+    int r = 0, nm = 0;
+    for (int i = 0; i < m; ++i) {
+        if (tid == 0) jmin = n;
+        __syncthreads();
+        uint32_t* wi = W + (int64_t)i * ldw;
+        for (int j = tid; j < n; j += PLDUQ_THREADS)
+            if (!colflag[j] && wi[j] != 0) atomicMin(&jmin, j);
+        __syncthreads();
+        const int jp = jmin;
+        if (jp == n) {  // pivotless row (plduq.cpp:60-63); stored from the back for now
+            if (tid == 0) row_image[m - 1 - nm] = i;
+            ++nm;
+            __syncthreads();
+            continue;
+        }
+        if (tid == 0) {
+            const uint32_t x = wi[jp];
+            sxi = finv(f, x);
+            d[r] = x;
+            row_image[r] = i;
+            pc[r] = jp;
+        }
+        __syncthreads();
+        const uint32_t xi = sxi;
+        for (int j = tid; j < n; j += PLDUQ_THREADS)  // U coefficients (plduq.cpp:65-70)
+            if (!colflag[j] && j != jp) wi[j] = fmul(f, xi, wi[j]);
+        for (int i2 = i + 1 + tid; i2 < m; i2 += PLDUQ_THREADS) lvec[i2] = W[(int64_t)i2 * ldw + jp];
+        __syncthreads();
+        // trailing rows: residual update on non-pivot columns, L multiplier in column jp
+        const int rows_left = m - i - 1;
+        const int64_t total = (int64_t)rows_left * n;
+        for (int64_t e = tid; e < total; e += PLDUQ_THREADS) {
+            const int i2 = i + 1 + (int)(e / n), j = (int)(e % n);
+            if (colflag[j]) continue;
+            uint32_t* w = W + (int64_t)i2 * ldw + j;
+            if (j == jp) *w = fmul(f, lvec[i2], xi);
+            else *w = fsub(f, *w, fmul(f, lvec[i2], wi[j]));
+        }
+        __syncthreads();
+        if (tid == 0) colflag[jp] = 1;
+        ++r;
+        __syncthreads();
+    }
+    // Pivotless rows ascending after the pivot rows (plduq.cpp:86-90).
+    if (tid == 0) {
+        info[0] = r;
+        for (int a = 0, b = nm - 1; a < b; ++a, --b) {
+            const int32_t t = row_image[r + a];
+            row_image[r + a] = row_image[r + b];
+            row_image[r + b] = t;
+        }
+        for (int k = 0; k < r; ++k) col_image[k] = pc[k];
+        int q = r;
+        for (int j = 0; j < n; ++j)
+            if (!colflag[j]) col_image[q++] = j;
+    }
+    __syncthreads();
+    // Dense factors (plduq.cpp:96-115).
+    for (int64_t e = tid; e < (int64_t)m * r; e += PLDUQ_THREADS) {
+        const int a = (int)(e / r), k = (int)(e % r);
+        uint32_t v = 0;
+        if (a == k) v = 1 % f.p;
+        else if (a > k) v = W[(int64_t)row_image[a] * ldw + pc[k]];
+        Lo[(int64_t)a * ldlo + k] = v;
+    }
+    for (int64_t e = tid; e < (int64_t)r * n; e += PLDUQ_THREADS) {
+        const int k = (int)(e / n), a = (int)(e % n);
+        uint32_t v = 0;
+        if (a == k) v = 1 % f.p;
+        else if (a > k) v = W[(int64_t)row_image[k] * ldw + col_image[a]];
+        Uo[(int64_t)k * lduo + a] = v;
+    }
+}
+
+}  // namespace
+
+void plduq(const Fp& f, cudaStream_t st, DMat W, int32_t* info, int32_t* colflag, uint32_t* lvec,
+           DMat Lo, uint32_t* d, DMat Uo) {
+    k_plduq_v1<<<1, PLDUQ_THREADS, 0, st>>>(f, W.ptr, W.ld, (int)W.rows, (int)W.cols, info, colflag,
+                                            lvec, Lo.ptr, Lo.ld, d, Uo.ptr, Uo.ld);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+}  // namespace ffb

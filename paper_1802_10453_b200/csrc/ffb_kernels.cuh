@@ -1,0 +1,74 @@
+// ffb_kernels.cuh -- host-side launchers of the device kernels (one stream).
+#pragma once
+
+#include "ffb_common.cuh"
+
+namespace ffb {
+
+// Launch accounting (reported by ffb_launch_count and bench.py's gpu_launches).
+extern thread_local uint64_t g_launches;
+
+enum GemmMode { GEMM_SUB = 0, GEMM_ADD = 1, GEMM_SET = 2 };
+
+// C (M x N) = C -/+ op(A) * op(B)  or  C = op(A) * op(B), all mod p.
+// op(A) is M x K (A stored K x M when ta), op(B) is K x N (B stored N x K when tb).
+void gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
+          int64_t M, int64_t N, int64_t K);
+
+// B <- T^-1 B for unit lower triangular T (n x n, only the strict lower part is read).
+void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B);
+
+// dst[i][j] = src[idx[i]][j]
+void gather_rows(cudaStream_t st, DMat dst, DMat src, const int32_t* idx);
+// dst[a][b] = src[idx[a]][idx[b]]
+void gather_sym(cudaStream_t st, DMat dst, DMat src, const int32_t* idx);
+// dst (cols x rows) = src^T
+void transpose(cudaStream_t st, DMat dst, DMat src);
+// Lg[ids[i]][col0 + j*cstride] = src[i][j]
+void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int cstride, DMat src);
+// dst[i][k] = Lg[ids[i]][col0 + k]
+void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t col0);
+// G (ncols x r) = (D^-1 X)^T with D the global block diagonal at columns [coff, coff+r)
+void inverse_apply_T(const Fp& f, cudaStream_t st, DMat G, DMat X, DDiag D, int64_t coff);
+// G (ncols x r) = (diag(dinv) X)^T
+void scale_T(const Fp& f, cudaStream_t st, DMat G, DMat X, const uint32_t* dinv);
+// out[i] = v[i]^-1
+void invert_vec(const Fp& f, cudaStream_t st, uint32_t* out, const uint32_t* v, int64_t n);
+// flag (device int) |= any nonzero in m
+void any_nonzero(cudaStream_t st, DMat m, int32_t* flag);
+// flag |= any a[i][j] != a[j][i]
+void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag);
+// Y <- strict_upper(Ct) + diag(Ct)/2 (odd p) or 0 (p = 2); lower part zeroed; in place.
+// flag |= nonzero diagonal when p = 2 (no solution: CharTwoNonzeroDiagonal).
+void trssyr2k_mid(const Fp& f, cudaStream_t st, DMat Ct, int32_t* flag);
+// Pair blocks of zero_leading_pairs: D[coff+2i], D[coff+2i+1] from d, dinv, delta.
+void write_pair_diag(const Fp& f, cudaStream_t st, DDiag D, int64_t coff, const uint32_t* d,
+                     const uint32_t* dinv, const uint32_t* delta, int64_t r);
+// Characteristic-2 delta recurrence (sytrf.cpp:188-198): delta_i = C1_ii - sum_{j<i} delta_j U1_ji^2
+void char2_delta(const Fp& f, cudaStream_t st, DMat C1, DMat U1, uint32_t* delta);
+// H[i][j] = v[i] * S[i][j]  (row scaling)
+void scale_rows(const Fp& f, cudaStream_t st, DMat H, DMat S, const uint32_t* v);
+// X[i][j] += v[i] * U[i][j] for j >= i
+void add_scaled_rows_upper(const Fp& f, cudaStream_t st, DMat X, DMat U, const uint32_t* v);
+// Set a view to zero.
+void zero_mat(cudaStream_t st, DMat m);
+// Residue conversion at the host boundary.
+void convert_in(const Fp& f, cudaStream_t st, DMat dst, const void* src, int elem_bytes);
+void convert_out(cudaStream_t st, void* dst, int elem_bytes, DMat src);
+// Final L: out[pos][k] = Lg[perm[pos]][k]
+void gather_lower_out(cudaStream_t st, DMat out, DMat Lg, const int32_t* perm);
+
+// Crout leaf (Alg. 4, sytrf.cpp:35-139) on an s x s block; writes L columns
+// [coff, coff+rank) of rows rows[0..s) into Lg, D entries, and out[0] = rank,
+// out[1..s] = local permutation (image).  scratch: device buffer for large s.
+void leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg,
+                int64_t coff, DDiag D, int32_t* out, uint32_t* scratch);
+size_t leaf_scratch_words(int64_t s);
+
+// PLDUQ (plduq.cpp:36-123) of W (m x n, destroyed).  Outputs: info[0] = r,
+// info[1..m] row_image, info[1+m..1+m+n] col_image, pc[r] in info after that;
+// Lo (m x min(m,n)) = [L1;M1], d (r), Uo (min(m,n) x n) = [U1 V1].
+void plduq(const Fp& f, cudaStream_t st, DMat W, int32_t* info, int32_t* colflag,
+           uint32_t* lvec, DMat Lo, uint32_t* d, DMat Uo);
+
+}  // namespace ffb

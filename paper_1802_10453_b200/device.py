@@ -1,0 +1,55 @@
+"""Device-resident entry point (the benchmark's timed region).
+
+``ldlt_device`` factors a matrix that already lives in HBM (uint32 residues in
+a torch int32 tensor) and leaves P, L, D in HBM: no host copies.  It wraps
+``ffb_ldlt_device`` of include/ffldl_b200.h.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+from typing import Optional
+
+from ._lib import lib
+from .ffldl import Context, SytrfConfig, _check, _p, default_context
+
+
+@dataclass
+class DeviceFactorization:
+    perm: "object"    # torch int32 [n]
+    lower: "object"   # torch int32 [n, n] (first `rank` columns valid)
+    dkind: "object"   # torch int32 [n]
+    dval: "object"    # torch int32 [n]
+    dval2: "object"   # torch int32 [n]
+    rank: int
+
+
+class DeviceBuffers:
+    """Preallocated outputs, reused across calls."""
+
+    def __init__(self, n: int, device: int = 0):
+        import torch
+        dev = f"cuda:{device}"
+        self.n = n
+        self.perm = torch.empty(n, dtype=torch.int32, device=dev)
+        self.lower = torch.empty((n, n), dtype=torch.int32, device=dev)
+        self.dkind = torch.empty(n, dtype=torch.int32, device=dev)
+        self.dval = torch.empty(n, dtype=torch.int32, device=dev)
+        self.dval2 = torch.empty(n, dtype=torch.int32, device=dev)
+
+
+def ldlt_device(a, field, config: Optional[SytrfConfig] = None, ctx: Optional[Context] = None,
+                out: Optional[DeviceBuffers] = None) -> DeviceFactorization:
+    """Factor the device matrix ``a`` (n x n int32 tensor of residues; OVERWRITTEN)."""
+    config = config or SytrfConfig()
+    p = _p(field)
+    ctx = ctx or default_context()
+    n = a.shape[0]
+    out = out or DeviceBuffers(n, ctx.device)
+    rank = C.c_size_t(0)
+    _check(lib().ffb_ldlt_device(ctx.handle, p, n, a.data_ptr(), a.stride(0),
+                                 int(config.variant), int(config.base_case_threshold),
+                                 out.perm.data_ptr(), out.lower.data_ptr(), out.lower.stride(0),
+                                 out.dkind.data_ptr(), out.dval.data_ptr(), out.dval2.data_ptr(),
+                                 C.byref(rank)))
+    return DeviceFactorization(out.perm, out.lower, out.dkind, out.dval, out.dval2, rank.value)

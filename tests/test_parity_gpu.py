@@ -1,0 +1,263 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bit-exact on P, L, D and rank for every case (integer arithmetic: no
+tolerance).  Covers the reference's own known answers, its exhaustive sweeps,
+random inputs over p in {2,3,7,11,131,8388593}, every variant, the bordered
+entry point, PLDUQ, TRSSYR2K, the BLAS3 kernels, error behaviour, and the five
+benchmark families."""
+import itertools
+import json
+import os
+
+import numpy as np
+import pytest
+
+from helpers import describe_diff, fact_equal, hollow, rand_low_rank, rand_rook_rpm, rand_sym
+
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+VARIANTS = [("cascade", 64), ("recursive", 64), ("crout", 64), ("cascade", 2), ("cascade", 4),
+            ("cascade", 8)]
+
+
+def cfg(v, t):
+    import paper_1802_10453_b200 as ffb
+    return ffb.SytrfConfig({"cascade": ffb.Variant.Cascade, "recursive": ffb.Variant.Recursive,
+                            "crout": ffb.Variant.Crout}[v], t)
+
+
+def check(gpu, oracle, p, a, v="cascade", t=64):
+    import paper_1802_10453_b200 as ffb
+    g = ffb.ldlt(a, p, cfg(v, t), ctx=gpu)
+    o = oracle.ldlt(p, a, v, t)
+    assert fact_equal(g, o), f"p={p} n={a.shape[0]} {v}{t}: {describe_diff(g, o)}"
+    return g
+
+
+def test_known_answers(gpu, oracle):
+    import paper_1802_10453_b200 as ffb
+    with open(os.path.join(GOLDEN, "known_answers.json")) as fh:
+        k = json.load(fh)
+    for case in k["ldlt"]:
+        g = check(gpu, oracle, case["p"], np.array(case["a"], np.uint64))
+        assert g.rank == case["rank"] and g.perm.image_array().tolist() == case["perm"]
+    for case in k["ldlt_zero_leading"]:
+        y, z = np.array(case["y"], np.uint64), np.array(case["z"], np.uint64)
+        g = ffb.ldlt_zero_leading(y, z, case["p"], ctx=gpu)
+        o = oracle.ldlt_zero_leading(case["p"], y, z)
+        assert fact_equal(g, o) and g.lower.tolist() == case["lower"]
+    c = k["trssyr2k"][0]
+    x = ffb.trssyr2k(np.array(c["u"]), np.array(c["c"]), c["p"], ctx=gpu)
+    assert x.tolist() == c["x"]
+    e = k["trssyr2k_errors"][0]
+    with pytest.raises(ffb.CharTwoNonzeroDiagonal):
+        ffb.trssyr2k(np.array(e["u"]), np.array(e["c"]), e["p"], ctx=gpu)
+    c = k["plduq"][0]
+    pf = ffb.plduq(np.array(c["b"]), c["p"], ctx=gpu)
+    assert pf.rank == 2 and pf.col_perm.image_array().tolist() == c["col_image"]
+    assert pf.diag.tolist() == c["diag"]
+
+
+def test_regression_f2(gpu, oracle):
+    with open(os.path.join(GOLDEN, "known_answers.json")) as fh:
+        a = np.array(json.load(fh)["regressions"][0]["a"], np.uint64)
+    for v, t in VARIANTS:
+        check(gpu, oracle, 2, a, v, t)
+
+
+def test_degenerate_inputs(gpu, oracle):
+    for a in (np.zeros((0, 0), np.uint64), np.zeros((5, 5), np.uint64), np.eye(6, dtype=np.uint64),
+              np.array([[3]], np.uint64), np.zeros((1, 1), np.uint64)):
+        for v, t in VARIANTS:
+            check(gpu, oracle, 7, a, v, t)
+
+
+@pytest.mark.parametrize("p", [2, 3])
+def test_exhaustive_3x3(gpu, oracle, p):
+    for code in range(p ** 6):
+        a = np.zeros((3, 3), np.uint64)
+        v = code
+        for i in range(3):
+            for j in range(i + 1):
+                a[i, j] = a[j, i] = v % p
+                v //= p
+        for var, t in VARIANTS[:5]:
+            check(gpu, oracle, p, a, var, t)
+
+
+def test_exhaustive_4x4_f2(gpu, oracle):
+    for code in range(1 << 10):
+        a = np.zeros((4, 4), np.uint64)
+        v = code
+        for i in range(4):
+            for j in range(i + 1):
+                a[i, j] = a[j, i] = v & 1
+                v >>= 1
+        check(gpu, oracle, 2, a)
+
+
+@pytest.mark.parametrize("p", [2, 3, 7, 11, 131, 8388593])
+def test_random_small(gpu, oracle, p):
+    rng = np.random.default_rng(10 + p)
+    for n in (1, 2, 3, 5, 9, 16, 31, 64, 65, 100):
+        for a in (rand_sym(rng, p, n), rand_low_rank(rng, p, n, n // 2), hollow(rng, p, n),
+                  rand_rook_rpm(rng, p, n, n // 2)):
+            for v, t in VARIANTS:
+                if v == "crout" and n > 64:
+                    continue
+                check(gpu, oracle, p, a, v, t)
+
+
+@pytest.mark.parametrize("p", [3, 131, 8388593])
+def test_random_medium(gpu, oracle, p):
+    rng = np.random.default_rng(20 + p)
+    for n in (129, 200, 257, 400):
+        for a in (rand_sym(rng, p, n), rand_rook_rpm(rng, p, n, n // 2), rand_low_rank(rng, p, n, n // 3)):
+            check(gpu, oracle, p, a)
+            check(gpu, oracle, p, a, "cascade", 16)
+
+
+def test_zero_leading_entry(gpu, oracle):
+    import paper_1802_10453_b200 as ffb
+    for p in (2, 7, 8388593):
+        rng = np.random.default_rng(p + 111)
+        for m, n in [(1, 1), (2, 3), (3, 2), (4, 4), (0, 3), (3, 0), (5, 2), (20, 33), (40, 70)]:
+            y = rng.integers(0, p, (m, n), dtype=np.uint64)
+            z = rand_sym(rng, p, n)
+            for v, t in VARIANTS[:5]:
+                g = ffb.ldlt_zero_leading(y, z, p, cfg(v, t), ctx=gpu)
+                o = oracle.ldlt_zero_leading(p, y, z, v, t)
+                assert fact_equal(g, o), (p, m, n, v, t, describe_diff(g, o))
+        # Y = 0 and Z = 0 (test_sytrf.cpp:187-210)
+        y0 = np.zeros((3, 4), np.uint64)
+        z = rand_sym(rng, p, 4)
+        assert fact_equal(ffb.ldlt_zero_leading(y0, z, p, ctx=gpu), oracle.ldlt_zero_leading(p, y0, z))
+        y = rng.integers(0, p, (3, 4), dtype=np.uint64)
+        z0 = np.zeros((4, 4), np.uint64)
+        assert fact_equal(ffb.ldlt_zero_leading(y, z0, p, ctx=gpu), oracle.ldlt_zero_leading(p, y, z0))
+
+
+def test_plduq(gpu, oracle):
+    import paper_1802_10453_b200 as ffb
+    for p in (2, 3, 7, 11, 131, 8388593):
+        rng = np.random.default_rng(p + 3)
+        for m, n in [(1, 1), (1, 5), (5, 1), (3, 7), (7, 3), (10, 10), (40, 70), (130, 90)]:
+            for b in (rng.integers(0, p, (m, n), dtype=np.uint64),
+                      (rng.integers(0, p, (m, 2)).astype(object).dot(rng.integers(0, p, (2, n))) % p).astype(np.uint64)):
+                g = ffb.plduq(b, p, ctx=gpu)
+                o = oracle.plduq(p, b)
+                assert g.rank == o["rank"]
+                assert np.array_equal(g.row_perm.image_array(), o["row_image"])
+                assert np.array_equal(g.col_perm.image_array(), o["col_image"])
+                assert np.array_equal(g.lower, o["lower"]) and np.array_equal(g.upper, o["upper"])
+                assert np.array_equal(g.diag, o["diag"])
+
+
+def test_trssyr2k(gpu, oracle):
+    import paper_1802_10453_b200 as ffb
+    for p in (3, 7, 131, 8388593):
+        rng = np.random.default_rng(p * 17 + 1)
+        for n in (1, 2, 3, 5, 8, 16, 33, 64, 65, 150):
+            u = np.triu(rng.integers(0, p, (n, n), dtype=np.uint64), 1) + np.eye(n, dtype=np.uint64)
+            c = rand_sym(rng, p, n)
+            assert np.array_equal(ffb.trssyr2k(u, c, p, ctx=gpu), oracle.trssyr2k(p, u, c))
+    rng = np.random.default_rng(99)
+    for n in (1, 2, 3, 6, 17):  # characteristic 2 with zero-diagonal right-hand sides
+        u = np.triu(rng.integers(0, 2, (n, n), dtype=np.uint64), 1) + np.eye(n, dtype=np.uint64)
+        c = rand_sym(rng, 2, n)
+        np.fill_diagonal(c, 0)
+        assert np.array_equal(ffb.trssyr2k(u, c, 2, ctx=gpu), oracle.trssyr2k(2, u, c))
+
+
+def test_kernels(gpu, oracle):
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(5)
+    for p in (2, 7, 131, 8388593):
+        for (m, n, k) in [(9, 11, 13), (70, 130, 65), (1, 1, 1), (200, 3, 300)]:
+            c = rng.integers(0, p, (m, n), dtype=np.uint64)
+            a = rng.integers(0, p, (m, k), dtype=np.uint64)
+            b = rng.integers(0, p, (k, n), dtype=np.uint64)
+            assert np.array_equal(ffb.gemm_sub(c, a, b, p, ctx=gpu), oracle.gemm_sub(p, c, a, b))
+        for n in (5, 64, 100):
+            t = rng.integers(0, p, (n, n), dtype=np.uint64)
+            t[np.diag_indices(n)] = rng.integers(1, p, n).astype(np.uint64)
+            bb = rng.integers(0, p, (n, 7), dtype=np.uint64)
+            cc = rng.integers(0, p, (n, 7), dtype=np.uint64)
+            for up, tr, un in itertools.product((0, 1), repeat=3):
+                assert np.array_equal(ffb.trsm_inplace(t, up, tr, un, bb, p, ctx=gpu),
+                                      oracle.trsm_inplace(p, t, up, tr, un, bb))
+                assert np.array_equal(ffb.trmm_sub(cc, t, up, tr, un, bb, p, ctx=gpu),
+                                      oracle.trmm_sub(p, cc, t, up, tr, un, bb))
+        n = 20
+        g = rng.integers(0, p, (n, 6), dtype=np.uint64)
+        cs = rand_sym(rng, p, n)
+        blocks = [ffb.ScalarBlock(int(rng.integers(1, p))), ffb.AntiDiagBlock(int(rng.integers(1, p))),
+                  ffb.ScalarBlock(int(rng.integers(1, p)))]
+        blocks.append(ffb.AntiTriBlock(1, 1) if p == 2 else ffb.AntiDiagBlock(int(rng.integers(1, p))))
+        d = ffb.BlockDiag(blocks)
+        kind, val, val2 = d.columns()
+        assert np.array_equal(ffb.syrdk_sub(cs, g, d, p, ctx=gpu), oracle.syrdk_sub(p, cs, g, kind, val, val2))
+        a2 = rng.integers(0, p, (4, n), dtype=np.uint64)
+        b2 = rng.integers(0, p, (4, n), dtype=np.uint64)
+        assert np.array_equal(ffb.syr2k_sub(cs, a2, b2, p, ctx=gpu), oracle.syr2k_sub(p, cs, a2, b2))
+
+
+def test_errors(gpu):
+    import paper_1802_10453_b200 as ffb
+    with pytest.raises(ffb.DimensionMismatch):
+        ffb.ldlt(np.zeros((2, 3), np.uint64), 7, ctx=gpu)
+    a = np.zeros((2, 2), np.uint64)
+    a[0, 1] = 1
+    with pytest.raises(ffb.NotSymmetric):
+        ffb.ldlt(a, 7, ctx=gpu)
+    with pytest.raises(ffb.NotPrime):
+        ffb.ldlt(np.zeros((2, 2), np.uint64), 8, ctx=gpu)
+    with pytest.raises(ffb.DimensionMismatch):
+        ffb.ldlt_zero_leading(np.zeros((2, 3), np.uint64), rand_sym(np.random.default_rng(0), 7, 4), 7, ctx=gpu)
+    zasym = np.zeros((3, 3), np.uint64)
+    zasym[0, 2] = 1
+    with pytest.raises(ffb.NotSymmetric):
+        ffb.ldlt_zero_leading(np.zeros((2, 3), np.uint64), zasym, 7, ctx=gpu)
+    with pytest.raises(ffb.Unsupported):
+        ffb.ldlt(np.zeros((2, 2), np.uint64), 2147483659, ctx=gpu)
+    u = np.eye(3, dtype=np.uint64)
+    u[1, 1] = 2
+    with pytest.raises(ffb.NonUnitTriangular):
+        ffb.trssyr2k(u, np.zeros((3, 3), np.uint64), 7, ctx=gpu)
+
+
+def test_device_generator_matches_host(gpu):
+    from paper_1802_10453_b200 import configs
+    for c in (1, 2, 3, 4, 5):
+        w = configs.CONFIGS[c].scaled(300)
+        d = configs.generate_device(w, gpu).cpu().numpy().view(np.uint32).astype(np.uint64)
+        assert np.array_equal(d, configs.generate(w)), c
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
+def test_config_families_bit_exact(gpu, oracle, c):
+    """Each benchmark family at sizes the oracle finishes in seconds."""
+    from paper_1802_10453_b200 import configs
+    for n in (256, 1024):
+        w = configs.CONFIGS[c].scaled(n)
+        a = configs.generate(w)
+        g = check(gpu, oracle, w.p, a)
+        if c == 5:
+            assert g.rank == w.r
+
+
+def test_golden_reference_outputs(gpu):
+    """GPU against the UNMODIFIED reference's pinned outputs (tests/golden/ref_outputs.npz)."""
+    import paper_1802_10453_b200 as ffb
+    from golden_cases import golden_cases
+    z = np.load(os.path.join(GOLDEN, "ref_outputs.npz"))
+    for name, p, a, v, t in golden_cases():
+        g = ffb.ldlt(a, p, cfg(v, t), ctx=gpu)
+        kind, val, val2 = g.diag.columns()
+        assert g.rank == int(z[f"{name}/rank"][0]), name
+        assert np.array_equal(g.perm.image_array(), z[f"{name}/perm"]), name
+        assert np.array_equal(g.lower, z[f"{name}/lower"].astype(np.uint64)), name
+        assert np.array_equal(kind, z[f"{name}/dkind"].astype(np.int32)), name
+        assert np.array_equal(val, z[f"{name}/dval"].astype(np.uint64)), name
+        assert np.array_equal(val2, z[f"{name}/dval2"].astype(np.uint64)), name
