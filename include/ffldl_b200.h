@@ -79,8 +79,16 @@ int ffb_create(ffb_context** ctx, int device);
 int ffb_destroy(ffb_context* ctx);
 /* The context's CUDA stream (cudaStream_t), for callers that time on it. */
 void* ffb_stream(ffb_context* ctx);
-/* Kernel launches issued by the most recent factorization (instrumentation). */
+/* Kernel launches issued by the most recent call (instrumentation). */
 uint64_t ffb_launch_count(ffb_context* ctx);
+/* Host<->device synchronization points (rank/permutation read-backs) of the most recent call. */
+uint64_t ffb_sync_count(ffb_context* ctx);
+/* Per-kernel-class timing of subsequent calls (CUDA events around every launch, on the
+ * launching stream; adds overhead, off by default).  enable resets the totals.
+ * Classes: 0 GEMM, 1 Crout leaf, 2 PLDUQ, 3 TRSM base, 4 data movement, 5 other. */
+int ffb_profile_enable(ffb_context* ctx, int enable);
+int ffb_profile_read(ffb_context* ctx, int klass, uint64_t* launches, double* ms, double* ops,
+                     double* bytes);
 
 /* ffldl::ldlt(const Matrix&, const SytrfConfig&)  -- proj/include/ffldl/sytrf.hpp:30,
  * proj/src/sytrf.cpp:354-358.  Host buffers. */

@@ -17,7 +17,8 @@ _lib = None
 # Every symbol declared in include/ffldl_b200.h (checked by tests/test_capi.py).
 EXPORTS = [
     "ffb_version", "ffb_status_string", "ffb_last_error", "ffb_create", "ffb_destroy",
-    "ffb_stream", "ffb_launch_count", "ffb_ldlt", "ffb_ldlt_compact", "ffb_ldlt_zero_leading",
+    "ffb_stream", "ffb_launch_count", "ffb_sync_count", "ffb_profile_enable", "ffb_profile_read",
+    "ffb_ldlt", "ffb_ldlt_compact", "ffb_ldlt_zero_leading",
     "ffb_ldlt_device", "ffb_plduq", "ffb_trssyr2k", "ffb_gemm_sub", "ffb_trmm_sub",
     "ffb_trsm_inplace", "ffb_syrdk_sub", "ffb_syr2k_sub", "ffb_generate_host",
     "ffb_generate_device", "ffb_config5_partners",
@@ -36,6 +37,10 @@ _SIGS = {
     "ffb_destroy": (I, [P]),
     "ffb_stream": (P, [P]),
     "ffb_launch_count": (U64, [P]),
+    "ffb_sync_count": (U64, [P]),
+    "ffb_profile_enable": (I, [P, I]),
+    "ffb_profile_read": (I, [P, I, C.POINTER(U64), C.POINTER(C.c_double), C.POINTER(C.c_double),
+                             C.POINTER(C.c_double)]),
     "ffb_ldlt": (I, [P, U64, SZ, SZ, P, I, SZ, P, P, P, P, P, C.POINTER(SZ)]),
     "ffb_ldlt_compact": (I, [P, U64, SZ, P, I, I, SZ, P, P, I, P, P, P, C.POINTER(SZ)]),
     "ffb_ldlt_zero_leading": (I, [P, U64, SZ, SZ, P, SZ, P, I, SZ, P, P, P, P, P, C.POINTER(SZ)]),

@@ -42,6 +42,8 @@ struct ffb_context {
     uint32_t inv_p = 0;
     int32_t* flag = nullptr;  // device scratch flag
     uint64_t launches = 0;
+    uint64_t syncs = 0, syncs_last = 0;
+    Profiler prof;
 };
 
 namespace {
@@ -169,6 +171,7 @@ const void* readback(ffb_context* c, const void* dev, size_t bytes) {
     }
     FFB_CUDA(cudaMemcpyAsync(c->down_host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
     FFB_CUDA(cudaStreamSynchronize(c->stream));
+    ++c->syncs;
     c->up_top = 0;  // every upload issued so far has completed
     return c->down_host;
 }
@@ -452,13 +455,22 @@ int guarded(ffb_context* c, F&& fn) {
     try {
         if (!c) throw Status(FFB_ERROR, "null context");
         FFB_CUDA(cudaSetDevice(c->device));
-        const uint64_t l0 = g_launches;
+        const uint64_t l0 = g_launches, s0 = c->syncs;
+        g_prof = &c->prof;
         fn();
+        if (c->prof.on) {
+            FFB_CUDA(cudaStreamSynchronize(c->stream));
+            c->prof.flush();
+        }
+        g_prof = nullptr;
         c->launches = g_launches - l0;
+        c->syncs_last = c->syncs - s0;
         g_last_error.clear();
         return FFB_OK;
     } catch (const std::exception& e) {
+        g_prof = nullptr;
         if (c) {
+            c->prof.recs.clear();
             cudaStreamSynchronize(c->stream);
             c->ws_top = 0;
             c->up_top = 0;
@@ -620,6 +632,24 @@ int ffb_destroy(ffb_context* c) {
 }
 
 void* ffb_stream(ffb_context* c) { return c ? (void*)c->stream : nullptr; }
+uint64_t ffb_sync_count(ffb_context* c) { return c ? c->syncs_last : 0; }
+
+int ffb_profile_enable(ffb_context* c, int on) {
+    if (!c) return FFB_ERROR;
+    c->prof.on = on != 0;
+    c->prof.reset();
+    return FFB_OK;
+}
+
+int ffb_profile_read(ffb_context* c, int klass, uint64_t* launches, double* ms, double* ops,
+                     double* bytes) {
+    if (!c || klass < 0 || klass >= K_NCLASS) return FFB_ERROR;
+    *launches = c->prof.cnt[klass];
+    *ms = c->prof.ms[klass];
+    *ops = c->prof.ops[klass];
+    *bytes = c->prof.bytes[klass];
+    return FFB_OK;
+}
 uint64_t ffb_launch_count(ffb_context* c) { return c ? c->launches : 0; }
 
 int ffb_ldlt_compact(ffb_context* c, uint64_t p, size_t n, const void* a, int a_type, int variant,

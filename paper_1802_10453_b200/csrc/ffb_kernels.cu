@@ -11,8 +11,50 @@
 namespace ffb {
 
 thread_local uint64_t g_launches = 0;
+thread_local Profiler* g_prof = nullptr;
 
 static inline void count_launch() { ++g_launches; }
+
+cudaEvent_t Profiler::get() {
+    if (!pool.empty()) {
+        cudaEvent_t e = pool.back();
+        pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    FFB_CUDA(cudaEventCreate(&e));
+    return e;
+}
+void Profiler::flush() {
+    for (Rec& r : recs) {
+        float t = 0.f;
+        if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) ms[r.cls] += t;
+        ops[r.cls] += r.ops;
+        bytes[r.cls] += r.bytes;
+        cnt[r.cls] += 1;
+        pool.push_back(r.a);
+        pool.push_back(r.b);
+    }
+    recs.clear();
+}
+void Profiler::reset() {
+    for (int i = 0; i < K_NCLASS; ++i) ms[i] = ops[i] = bytes[i] = 0, cnt[i] = 0;
+}
+ProfScope::ProfScope(int cls, cudaStream_t s, double ops, double bytes) : st(s) {
+    live = g_prof && g_prof->on;
+    if (!live) return;
+    rec.cls = cls;
+    rec.ops = ops;
+    rec.bytes = bytes;
+    rec.a = g_prof->get();
+    rec.b = g_prof->get();
+    cudaEventRecord(rec.a, st);
+}
+ProfScope::~ProfScope() {
+    if (!live) return;
+    cudaEventRecord(rec.b, st);
+    g_prof->recs.push_back(rec);
+}
 
 // ===========================================================================
 // Generic modular GEMM (SIMT).  64x64 tile, 256 threads, 4x4 per thread,
@@ -101,6 +143,7 @@ template <bool TA, bool TB>
 void launch_gemm_simt(const Fp& f, cudaStream_t st, int mode, DMat C, DMat A, DMat B, int64_t M,
                       int64_t N, int64_t K) {
     dim3 grid((unsigned)cdiv(N, GB_N), (unsigned)cdiv(M, GB_M));
+    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, 4.0 * (M * K + K * N + 2 * M * N));
     if (f.p < (1u << 23))
         k_gemm_simt<TA, TB, false><<<grid, 256, 0, st>>>(f, mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr,
                                                           B.ld, M, N, K);
@@ -170,6 +213,7 @@ void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
     if (n <= 0 || B.cols <= 0) return;
     if (n <= TRSM_NB) {
         dim3 grid((unsigned)cdiv(B.cols, TRSM_THREADS));
+        ProfScope ps(K_TRSM, st, (double)n * n * B.cols, 4.0 * (n * n + 2 * n * B.cols));
         if (f.p < (1u << 23))
             k_trsm_base<false><<<grid, TRSM_THREADS, 0, st>>>(f, T.ptr, T.ld, B.ptr, B.ld, (int)n,
                                                               B.cols);
@@ -431,6 +475,7 @@ inline dim3 rowgrid(int64_t rows, int64_t cols, int threads = 256) {
 #define FFB_ROWCHUNK 65535
 
 void gather_rows(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (dst.rows <= 0 || dst.cols <= 0) return;
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
@@ -442,6 +487,7 @@ void gather_rows(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
 }
 
 void gather_sym(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (dst.rows <= 0) return;
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
@@ -453,6 +499,7 @@ void gather_sym(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
 }
 
 void transpose(cudaStream_t st, DMat dst, DMat src) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (src.rows <= 0 || src.cols <= 0) return;
     dim3 grid((unsigned)cdiv(src.cols, 32), (unsigned)cdiv(src.rows, 32));
     k_transpose<<<grid, dim3(32, 8), 0, st>>>(dst.ptr, dst.ld, src.ptr, src.ld, src.rows, src.cols);
@@ -461,6 +508,7 @@ void transpose(cudaStream_t st, DMat dst, DMat src) {
 }
 
 void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int cstride, DMat src) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (src.rows <= 0 || src.cols <= 0) return;
     for (int64_t r0 = 0; r0 < src.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, src.rows - r0);
@@ -473,6 +521,7 @@ void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int 
 }
 
 void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t col0) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (dst.rows <= 0 || dst.cols <= 0) return;
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
@@ -484,6 +533,7 @@ void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t c
 }
 
 void inverse_apply_T(const Fp& f, cudaStream_t st, DMat G, DMat X, DDiag D, int64_t coff) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (X.rows <= 0 || X.cols <= 0) return;
     dim3 grid((unsigned)cdiv(X.cols, 32), (unsigned)cdiv(X.rows, 32));
     k_inverse_apply_T<<<grid, dim3(32, 8), 0, st>>>(f, G.ptr, G.ld, X.ptr, X.ld, X.rows, X.cols, D,
@@ -493,6 +543,7 @@ void inverse_apply_T(const Fp& f, cudaStream_t st, DMat G, DMat X, DDiag D, int6
 }
 
 void scale_T(const Fp& f, cudaStream_t st, DMat G, DMat X, const uint32_t* dinv) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (X.rows <= 0 || X.cols <= 0) return;
     dim3 grid((unsigned)cdiv(X.cols, 32), (unsigned)cdiv(X.rows, 32));
     k_scale_T<<<grid, dim3(32, 8), 0, st>>>(f, G.ptr, G.ld, X.ptr, X.ld, X.rows, X.cols, dinv);
@@ -501,6 +552,7 @@ void scale_T(const Fp& f, cudaStream_t st, DMat G, DMat X, const uint32_t* dinv)
 }
 
 void invert_vec(const Fp& f, cudaStream_t st, uint32_t* out, const uint32_t* v, int64_t n) {
+    ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (n <= 0) return;
     k_invert_vec<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(f, out, v, n);
     count_launch();
@@ -508,6 +560,7 @@ void invert_vec(const Fp& f, cudaStream_t st, uint32_t* out, const uint32_t* v, 
 }
 
 void any_nonzero(cudaStream_t st, DMat m, int32_t* flag) {
+    ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (m.rows <= 0 || m.cols <= 0) return;
     for (int64_t r0 = 0; r0 < m.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, m.rows - r0);
@@ -518,6 +571,7 @@ void any_nonzero(cudaStream_t st, DMat m, int32_t* flag) {
 }
 
 void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag) {
+    ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (a.rows <= 1) return;
     dim3 grid((unsigned)cdiv(a.rows, 32), (unsigned)cdiv(a.rows, 32));
     k_any_asym<<<grid, dim3(32, 8), 0, st>>>(a.ptr, a.ld, a.rows, flag);
@@ -526,6 +580,7 @@ void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag) {
 }
 
 void trssyr2k_mid(const Fp& f, cudaStream_t st, DMat Ct, int32_t* flag) {
+    ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (Ct.rows <= 0) return;
     k_trssyr2k_mid<<<rowgrid(Ct.rows, Ct.cols), 256, 0, st>>>(f, Ct.ptr, Ct.ld, Ct.rows, flag);
     count_launch();
@@ -534,6 +589,7 @@ void trssyr2k_mid(const Fp& f, cudaStream_t st, DMat Ct, int32_t* flag) {
 
 void write_pair_diag(const Fp& f, cudaStream_t st, DDiag D, int64_t coff, const uint32_t* d,
                      const uint32_t* dinv, const uint32_t* delta, int64_t r) {
+    ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     (void)f;
     if (r <= 0) return;
     k_write_pair_diag<<<(unsigned)cdiv(r, 256), 256, 0, st>>>(D, coff, d, dinv, delta, r);
@@ -542,6 +598,7 @@ void write_pair_diag(const Fp& f, cudaStream_t st, DDiag D, int64_t coff, const 
 }
 
 void char2_delta(const Fp& f, cudaStream_t st, DMat C1, DMat U1, uint32_t* delta) {
+    ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (C1.rows <= 0) return;
     k_char2_delta<<<1, 32, 0, st>>>(f, C1.ptr, C1.ld, U1.ptr, U1.ld, C1.rows, delta);
     count_launch();
@@ -549,6 +606,7 @@ void char2_delta(const Fp& f, cudaStream_t st, DMat C1, DMat U1, uint32_t* delta
 }
 
 void scale_rows(const Fp& f, cudaStream_t st, DMat H, DMat S, const uint32_t* v) {
+    ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (S.rows <= 0 || S.cols <= 0) return;
     k_scale_rows<<<rowgrid(S.rows, S.cols), 256, 0, st>>>(f, H.ptr, H.ld, S.ptr, S.ld, S.cols, v);
     count_launch();
@@ -556,6 +614,7 @@ void scale_rows(const Fp& f, cudaStream_t st, DMat H, DMat S, const uint32_t* v)
 }
 
 void add_scaled_rows_upper(const Fp& f, cudaStream_t st, DMat X, DMat U, const uint32_t* v) {
+    ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (X.rows <= 0) return;
     k_add_scaled_rows_upper<<<rowgrid(X.rows, X.cols), 256, 0, st>>>(f, X.ptr, X.ld, U.ptr, U.ld,
                                                                      X.cols, v);
@@ -564,6 +623,7 @@ void add_scaled_rows_upper(const Fp& f, cudaStream_t st, DMat X, DMat U, const u
 }
 
 void zero_mat(cudaStream_t st, DMat m) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (m.rows <= 0 || m.cols <= 0) return;
     if (m.ld == m.cols) {
         FFB_CUDA(cudaMemsetAsync(m.ptr, 0, (size_t)m.rows * m.cols * sizeof(uint32_t), st));
@@ -578,6 +638,7 @@ void zero_mat(cudaStream_t st, DMat m) {
 }
 
 void convert_in(const Fp& f, cudaStream_t st, DMat dst, const void* src, int eb) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
         dim3 g = rowgrid(nr, dst.cols);
@@ -593,6 +654,7 @@ void convert_in(const Fp& f, cudaStream_t st, DMat dst, const void* src, int eb)
 }
 
 void convert_out(cudaStream_t st, void* dst, int eb, DMat src) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     for (int64_t r0 = 0; r0 < src.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, src.rows - r0);
         dim3 g = rowgrid(nr, src.cols);
@@ -792,6 +854,7 @@ void leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat 
         FFB_CUDA(cudaFuncSetAttribute(k_leaf_crout, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)bytes));
     }
+    ProfScope ps(K_LEAF, st, 2.0 * s * s * s / 3.0, 4.0 * s * s);
     k_leaf_crout<<<1, LEAF_THREADS, bytes, st>>>(f, A.ptr, A.ld, s, scratch, smem ? 1 : 0, rows,
                                                  Lg.ptr, Lg.ld, coff, D, out);
     count_launch();
@@ -898,6 +961,7 @@ __global__ void __launch_bounds__(PLDUQ_THREADS)
 
 void plduq(const Fp& f, cudaStream_t st, DMat W, int32_t* info, int32_t* colflag, uint32_t* lvec,
            DMat Lo, uint32_t* d, DMat Uo) {
+    ProfScope ps(K_PLDUQ, st, 0.0, 4.0 * W.rows * W.cols);
     k_plduq_v1<<<1, PLDUQ_THREADS, 0, st>>>(f, W.ptr, W.ld, (int)W.rows, (int)W.cols, info, colflag,
                                             lvec, Lo.ptr, Lo.ld, d, Uo.ptr, Uo.ld);
     count_launch();

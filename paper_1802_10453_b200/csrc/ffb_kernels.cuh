@@ -1,12 +1,41 @@
 // ffb_kernels.cuh -- host-side launchers of the device kernels (one stream).
 #pragma once
 
+#include <vector>
+
 #include "ffb_common.cuh"
 
 namespace ffb {
 
 // Launch accounting (reported by ffb_launch_count and bench.py's gpu_launches).
 extern thread_local uint64_t g_launches;
+
+// Optional per-kernel-class instrumentation (ffb_profile_enable): CUDA events
+// around each launch on the launching stream, summed per class.
+enum KClass { K_GEMM = 0, K_LEAF = 1, K_PLDUQ = 2, K_TRSM = 3, K_MOVE = 4, K_OTHER = 5, K_NCLASS = 6 };
+struct Profiler {
+    struct Rec {
+        int cls;
+        cudaEvent_t a, b;
+        double ops, bytes;
+    };
+    bool on = false;
+    std::vector<Rec> recs;
+    std::vector<cudaEvent_t> pool;
+    double ms[K_NCLASS] = {}, ops[K_NCLASS] = {}, bytes[K_NCLASS] = {};
+    uint64_t cnt[K_NCLASS] = {};
+    cudaEvent_t get();
+    void flush();  // caller has synchronized the stream
+    void reset();
+};
+extern thread_local Profiler* g_prof;
+struct ProfScope {
+    Profiler::Rec rec;
+    cudaStream_t st;
+    bool live;
+    ProfScope(int cls, cudaStream_t s, double ops, double bytes);
+    ~ProfScope();
+};
 
 enum GemmMode { GEMM_SUB = 0, GEMM_ADD = 1, GEMM_SET = 2 };
 

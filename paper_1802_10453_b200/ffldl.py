@@ -374,6 +374,24 @@ class Context:
     def launch_count(self) -> int:
         return int(lib().ffb_launch_count(self.handle))
 
+    def sync_count(self) -> int:
+        return int(lib().ffb_sync_count(self.handle))
+
+    KERNEL_CLASSES = ("gemm", "leaf", "plduq", "trsm", "move", "other")
+
+    def profile(self, enable: bool = True) -> None:
+        """Per-kernel-class CUDA-event timing of subsequent calls (resets totals)."""
+        _check(lib().ffb_profile_enable(self.handle, int(enable)))
+
+    def profile_read(self) -> dict:
+        out = {}
+        for k, name in enumerate(self.KERNEL_CLASSES):
+            n, ms, ops, by = C.c_uint64(), C.c_double(), C.c_double(), C.c_double()
+            _check(lib().ffb_profile_read(self.handle, k, C.byref(n), C.byref(ms), C.byref(ops),
+                                          C.byref(by)))
+            out[name] = dict(launches=n.value, ms=ms.value, ops=ops.value, bytes=by.value)
+        return out
+
 
 _tls = threading.local()
 
