@@ -1,0 +1,373 @@
+"""Benchmark: effective GF(p) ops/s of PLDL^TP^T (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config C] [--n N_OVERRIDE]
+
+A step is one device-resident factorization (ffb_ldlt_device) of the
+workload's n x n matrix, already in HBM: W = 2n^3/3 effective field ops
+(BASELINE.json).  Default workload: configuration 5 (n=32768, p=131, rank
+16384), the size BASELINE.json quotes its metric on.  The input (4 GiB of
+uint32 residues at n=32768) is larger than L2; it is restored from a pristine
+copy before every step, outside the timed region, which also evicts L2.
+
+Multi-GPU: the path does not shard;
+with torchrun each rank factors its own replica, no collective on the data
+path, value = ranks * W / max-over-ranks time ("scaling": "weak").
+
+--impl reference times the reference's own CPU implementation (the unmodified
+ffldl library built into oracle/_ref) on the GPU box's host cores, on bounded
+samples of the same workload family.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+INT8_DENSE_PEAK_TOPS = 4500.0  # B200 datasheet dense INT8 (no int8 entry in MEASURED_PEAKS.json)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing (replicas only)
+# ---------------------------------------------------------------------------
+def dist_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")),
+            int(os.environ.get("WORLD_SIZE", "1")))
+
+
+def init_dist(world, backend):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group(backend=backend)
+    return dist
+
+
+def barrier(dist, device=None):
+    if dist is not None:
+        if device is not None:
+            dist.barrier(device_ids=[device])
+        else:
+            dist.barrier()
+
+
+def max_over_ranks(dist, value, device=None):
+    if dist is None:
+        return value
+    import torch
+    t = torch.tensor([value], dtype=torch.float64, device=device if device is not None else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 8:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.thread is not None:
+            self.thread.join(timeout=2)
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            for k, name in enumerate(names):
+                if r[4 + k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU legs (reference / oracle)
+# ---------------------------------------------------------------------------
+def reference_sample(n_sample, w_full, threads):
+    """Time the unmodified reference on `threads` concurrent cfg-family samples."""
+    from oracle.bind import LIBS, Checker
+    from paper_1802_10453_b200 import configs
+    kind = "reference" if os.path.exists(LIBS["ref"]) else "port"
+    chk = Checker("ref" if kind == "reference" else "oracle")
+    ws = [configs.Workload(w_full.config, n_sample, w_full.p,
+                           (w_full.r * n_sample) // w_full.n if w_full.r else 0, w_full.seed + k,
+                           w_full.description) for k in range(threads)]
+    mats = [configs.generate(w) for w in ws]
+    results = [None] * threads
+
+    def work(k):
+        t0 = time.perf_counter()
+        chk.ldlt(ws[k].p, mats[k])
+        results[k] = time.perf_counter() - t0
+
+    t0 = time.perf_counter()
+    ths = [threading.Thread(target=work, args=(k,)) for k in range(threads)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    wall = time.perf_counter() - t0
+    ops = threads * 2.0 * n_sample ** 3 / 3.0
+    return kind, ops / wall, wall
+
+
+def run_reference_arm(args, w, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_sample = args.ref_n
+    times = []
+    kind = "reference"
+    for i in range(args.warmup + args.steps):
+        kind, rate, wall = reference_sample(n_sample, w, threads)
+        if i >= args.warmup:
+            times.append((rate, wall))
+    value = statistics.median(r for r, _ in times) / 1e12
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": statistics.median(t for _, t in times) * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic", "config": config_block(w, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                         "sample": f"{threads} concurrent single-threaded ffldl::ldlt calls "
+                                   f"(Cascade, T=64) on config-{w.config}-family matrices of "
+                                   f"n={n_sample} per step; rate = {threads}*2n^3/3 / wall"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+METRIC = "effective GF(p) ops/s for PLDL^TP^T at n=32768 (2n^3/3 basis); % of tensor peak"
+UNIT = "Tops/s (1e12 effective GF(p) ops/s, 2n^3/3 basis)"
+
+
+def config_block(w, args):
+    return {"workload": f"config{w.config}: n={w.n}, p={w.p}" + (f", rank={w.r}" if w.r else "")
+            + f", {w.description}",
+            "n": w.n, "p": w.p, "rank_param": w.r, "seed": w.seed,
+            "variant": "Cascade", "base_case_threshold": args.threshold,
+            "timed": "device-resident ffb_ldlt_device (input in HBM -> P, L, D in HBM)",
+            "l2": f"input {w.n * w.n * 4 / 2**30:.2f} GiB > 126 MB L2, restored before each step",
+            "parallelism": f"replicas x{args.gpus}"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--n", type=int, default=0, help="override n (family scaled)")
+    ap.add_argument("--threshold", type=int, default=64)
+    ap.add_argument("--ref-n", type=int, default=1024, help="CPU sample size")
+    ap.add_argument("--cpu-n", type=int, default=2048, help="cpu_baseline sample size")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--backend", default="nccl")
+    args = ap.parse_args()
+
+    from paper_1802_10453_b200 import configs
+    w = configs.CONFIGS[args.config]
+    if args.n:
+        w = w.scaled(args.n)
+    rank, local, world = dist_env()
+
+    if args.impl == "reference":
+        run_reference_arm(args, w, rank, world)
+        return
+
+    import torch
+    import paper_1802_10453_b200 as ffb
+    from paper_1802_10453_b200.device import DeviceBuffers, ldlt_device
+
+    torch.cuda.set_device(local)
+    dist = init_dist(world, args.backend)
+    ctx = ffb.Context(local)
+    cfg = ffb.SytrfConfig(ffb.Variant.Cascade, args.threshold)
+    st = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    a0 = configs.generate_device(w, ctx)
+    a = torch.empty_like(a0)
+    out = DeviceBuffers(w.n, local)
+
+    def one_step():
+        a.copy_(a0)
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        f = ldlt_device(a, w.p, cfg, ctx, out)
+        e1.record(st)
+        e1.synchronize()
+        return e0.elapsed_time(e1), f
+
+    for _ in range(args.warmup):
+        one_step()
+    launches = 0
+    barrier(dist, local if args.backend == "nccl" else None)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    total_ms = 0.0
+    f = None
+    for _ in range(args.steps):
+        ms, f = one_step()
+        total_ms += ms
+        launches += ctx.launch_count()
+    clocks_info = clocks.stop()
+    torch.cuda.synchronize()
+    barrier(dist, local if args.backend == "nccl" else None)
+    total_ms = max_over_ranks(dist, total_ms, torch.device("cuda", local) if args.backend == "nccl" else None)
+    ops = 2.0 * w.n ** 3 / 3.0
+    value = world * args.steps * ops / (total_ms / 1e3) / 1e12
+    rank_out = f.rank
+    syncs = ctx.sync_count()
+
+    # instrumented pass (same workload): per-kernel-class CUDA-event totals
+    a.copy_(a0)
+    torch.cuda.synchronize()
+    ctx.profile(True)
+    ldlt_device(a, w.p, cfg, ctx, out)
+    prof = ctx.profile_read()
+    ctx.profile(False)
+    gemm = prof["gemm"]
+    roofline = None
+    if gemm["ms"] > 0:
+        achieved = gemm["ops"] / (gemm["ms"] / 1e3) / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": INT8_DENSE_PEAK_TOPS,
+                    "unit": "TFLOP/s", "frac": achieved / INT8_DENSE_PEAK_TOPS, "traffic": None,
+                    "kernel": "modular GEMM (all GEMM launches of one factorization)",
+                    "algorithmic": "2*M*N*K int ops per launch, summed; duration = CUDA events "
+                                   "around each launch on the engine stream",
+                    "peak_source": "B200 datasheet dense INT8 4.5 POPS (MEASURED_PEAKS.json has "
+                                   "no int8 entry)",
+                    "launches": gemm["launches"], "gemm_ms": gemm["ms"]}
+
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        e2e = run_e2e(w, ctx, cfg, args, local)
+
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        kind, rate, wall = reference_sample(args.cpu_n, w, 1)
+        cpu = {"value": rate / 1e12, "unit": UNIT, "cores": 1, "kind": kind,
+               "sample": f"one single-threaded ffldl::ldlt (Cascade, T=64) on a config-"
+                         f"{w.config}-family matrix of n={args.cpu_n} ({wall:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (seeded counter-based generator, csrc/ffb_gen.cu)",
+            "config": config_block(w, args),
+            "frac_of_int8_peak": value / INT8_DENSE_PEAK_TOPS, "rank": rank_out,
+            "rank_aware_tops": value * (2 * (rank_out ** 3 / 3 + w.n ** 2 * rank_out
+                                             - rank_out ** 2 * w.n)) / ops if rank_out else 0,
+            "gpu_launches": launches, "host_syncs_per_step": syncs,
+            "kernel_classes_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks_info,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def run_e2e(w, ctx, cfg, args, local):
+    """Same metric through the host-buffer C-ABI call (ffb_ldlt_compact) from pinned memory."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+
+    from paper_1802_10453_b200 import configs
+    from paper_1802_10453_b200._lib import lib
+    from paper_1802_10453_b200.ffldl import _check
+
+    eb = 1 if w.p <= 256 else 4
+    np_dt = np.uint8 if eb == 1 else np.uint32
+    a_dev = configs.generate_device(w, ctx)
+    host_a = torch.empty((w.n, w.n), dtype=torch.uint8 if eb == 1 else torch.int32).pin_memory()
+    host_a.copy_(a_dev.to(torch.uint8 if eb == 1 else torch.int32).cpu())
+    del a_dev
+    host_l = torch.empty(w.n * w.n * eb, dtype=torch.uint8).pin_memory()
+    perm = np.zeros(w.n, np.int64)
+    dk = np.zeros(w.n, np.int32)
+    dv = np.zeros(w.n, np.uint64)
+    dv2 = np.zeros(w.n, np.uint64)
+    rank = C.c_size_t(0)
+    ptr = lambda x: x.ctypes.data_as(C.c_void_p)
+    st = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    times = []
+    for i in range(2):
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        _check(lib().ffb_ldlt_compact(ctx.handle, w.p, w.n, host_a.data_ptr(), eb,
+                                      int(cfg.variant), int(cfg.base_case_threshold), ptr(perm),
+                                      host_l.data_ptr(), eb, ptr(dk), ptr(dv), ptr(dv2),
+                                      C.byref(rank)))
+        e1.record(st)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1) / 1e3)
+    t = times[-1]
+    r = rank.value
+    return {"value": 2.0 * w.n ** 3 / 3.0 / t / 1e12, "unit": UNIT,
+            "h2d_bytes_per_step": w.n * w.n * eb, "d2h_bytes_per_step": w.n * r * eb + w.n * 28,
+            "ms_per_step": t * 1e3,
+            "api": "ffb_ldlt_compact (host pinned buffers; H2D + symmetric check + "
+                   "factorization + L gather + D2H inside the timed call)"}
+
+
+if __name__ == "__main__":
+    main()
