@@ -17,12 +17,14 @@
 //   D   per-pivot-column kind / value / value2 / inverse arrays.
 // Node-local permutations and ranks are read back to the host (they decide
 // the shape of the next node); index arrays go down through a pinned ring.
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
 #include <vector>
 
 #include "ffb_kernels.cuh"
+#include "ffb_plduq.cuh"
 
 using namespace ffb;
 
@@ -199,6 +201,10 @@ Fp make_field(ffb_context* c, uint64_t p) {
 // ===========================================================================
 // The recursion.
 // ===========================================================================
+// Y with at most this many rows goes to the one-launch sequential PLDUQ.
+static int64_t PLDUQ_SEQ_MAX_ROWS =
+    getenv("FFB_PLDUQ_SEQ_ROWS") ? atoll(getenv("FFB_PLDUQ_SEQ_ROWS")) : 48;
+
 struct HFact {
     std::vector<int32_t> perm;  // image: position -> local input row
     int64_t rank = 0;
@@ -329,20 +335,38 @@ struct Engine {
     Pl run_plduq(DMat Y) {
         const int64_t m = Y.rows, n = Y.cols, mn = std::min(m, n);
         Pl pl;
-        int32_t* info = ws_vec<int32_t>(c, 1 + m + n + mn);
-        int32_t* colflag = ws_vec<int32_t>(c, n);
-        uint32_t* lvec = ws_vec<uint32_t>(c, m);
         DMat Lo = ws_mat(c, m, mn), Uo = ws_mat(c, mn, n);
         pl.d = ws_vec<uint32_t>(c, mn);
         pl.dinv = ws_vec<uint32_t>(c, mn);
-        plduq(f, st, Y, info, colflag, lvec, Lo, pl.d, Uo);
-        const int32_t* hb = (const int32_t*)readback(c, info, (size_t)(1 + m + n) * sizeof(int32_t));
-        pl.r = hb[0];
-        pl.rimg.assign(hb + 1, hb + 1 + m);
-        pl.cimg.assign(hb + 1 + m, hb + 1 + m + n);
+        if (m <= PLDUQ_SEQ_MAX_ROWS) {
+            // short Y: one launch of the row-sequential kernel
+            int32_t* info = ws_vec<int32_t>(c, 1 + m + n + mn);
+            int32_t* colflag = ws_vec<int32_t>(c, n);
+            uint32_t* lvec = ws_vec<uint32_t>(c, m);
+            plduq(f, st, Y, info, colflag, lvec, Lo, pl.d, Uo);
+            const int32_t* hb = (const int32_t*)readback(c, info, (size_t)(1 + m + n) * sizeof(int32_t));
+            pl.r = hb[0];
+            pl.rimg.assign(hb + 1, hb + 1 + m);
+            pl.cimg.assign(hb + 1 + m, hb + 1 + m + n);
+            invert_vec(f, st, pl.dinv, pl.d, pl.r);
+        } else {
+            Workspace ws{c->ws_base, c->ws_cap, &c->ws_top};
+            PlduqIO io;
+            io.upload = [this](const std::vector<int32_t>& v) { return upload(c, v); };
+            io.readback = [this](const void* p, size_t b) { return readback(c, p, b); };
+            io.Lo = Lo;
+            io.Uo = Uo;
+            io.d = pl.d;
+            io.dinv = pl.dinv;
+            const size_t mk = c->ws_top;
+            PlduqOut o = plduq_parallel(f, st, Y, ws, io);
+            c->ws_top = mk;
+            pl.r = o.r;
+            pl.rimg = std::move(o.rimg);
+            pl.cimg = std::move(o.cimg);
+        }
         pl.L = Lo.sub(0, 0, m, pl.r);
         pl.U = Uo.sub(0, 0, pl.r, n);
-        invert_vec(f, st, pl.dinv, pl.d, pl.r);
         return pl;
     }
 

@@ -261,3 +261,48 @@ def test_golden_reference_outputs(gpu):
         assert np.array_equal(kind, z[f"{name}/dkind"].astype(np.int32)), name
         assert np.array_equal(val, z[f"{name}/dval"].astype(np.uint64)), name
         assert np.array_equal(val2, z[f"{name}/dval2"].astype(np.uint64)), name
+
+
+def _run_in_subprocess(env_extra, code):
+    import subprocess
+    import sys
+    env = dict(os.environ, **env_extra)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
+
+
+PLDUQ_PATH_CHECK = r'''
+import sys, numpy as np
+sys.path.insert(0, "tests")
+import paper_1802_10453_b200 as ffb
+from oracle.bind import Checker
+from helpers import rand_rook_rpm, rand_sym, fact_equal
+o = Checker("oracle")
+for p in (2, 3, 131, 8388593):
+    rng = np.random.default_rng(p)
+    for (m, n) in [(1, 1), (5, 9), (64, 40), (130, 90), (300, 257), (129, 700)]:
+        for b in (rng.integers(0, p, (m, n), dtype=np.uint64),
+                  (rng.integers(0, p, (m, 3)).astype(object).dot(rng.integers(0, p, (3, n))) % p).astype(np.uint64),
+                  np.zeros((m, n), np.uint64)):
+            g = ffb.plduq(b, p); r = o.plduq(p, b)
+            assert g.rank == r["rank"], (p, m, n)
+            assert np.array_equal(g.row_perm.image_array(), r["row_image"])
+            assert np.array_equal(g.col_perm.image_array(), r["col_image"])
+            assert np.array_equal(g.lower, r["lower"]) and np.array_equal(g.upper, r["upper"])
+            assert np.array_equal(g.diag, r["diag"])
+    for n in (64, 130, 400):
+        a = rand_rook_rpm(rng, p, n, n // 2)
+        assert fact_equal(ffb.ldlt(a, p), o.ldlt(p, a)), (p, n)
+print("ok")
+'''
+
+
+@pytest.mark.parametrize("env", [{"FFB_PLDUQ_SEQ_ROWS": "0"},
+                                 {"FFB_PLDUQ_SEQ_ROWS": "0", "FFB_PLDUQ_FORCE_FALLBACK": "1"},
+                                 {"FFB_PLDUQ_SEQ_ROWS": "100000"}],
+                         ids=["parallel", "parallel-fallback", "sequential"])
+def test_plduq_paths(gpu, env):
+    """Every PLDUQ path (sketch-based parallel, its exact fallback, the sequential kernel)."""
+    _run_in_subprocess(env, PLDUQ_PATH_CHECK)
