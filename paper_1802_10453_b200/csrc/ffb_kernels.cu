@@ -163,6 +163,10 @@ void gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, 
         if (mode == GEMM_SET) zero_mat(st, C.sub(0, 0, M, N));
         return;
     }
+    if (tc_gemm_supported(f, M, N, K)) {
+        tc_gemm(f, st, mode, C, A, ta, B, tb, M, N, K);
+        return;
+    }
     if (!ta && !tb) launch_gemm_simt<false, false>(f, st, mode, C, A, B, M, N, K);
     else if (ta && !tb) launch_gemm_simt<true, false>(f, st, mode, C, A, B, M, N, K);
     else if (!ta && tb) launch_gemm_simt<false, true>(f, st, mode, C, A, B, M, N, K);

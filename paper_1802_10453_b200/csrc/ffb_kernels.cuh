@@ -44,6 +44,11 @@ enum GemmMode { GEMM_SUB = 0, GEMM_ADD = 1, GEMM_SET = 2 };
 void gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
           int64_t M, int64_t N, int64_t K);
 
+// tcgen05 int8 path (ffb_tc_gemm.cu), used by gemm() for p <= 255 and large shapes.
+bool tc_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K);
+void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
+             int64_t M, int64_t N, int64_t K);
+
 // B <- T^-1 B for unit lower triangular T (n x n, only the strict lower part is read).
 void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B);
 

@@ -597,7 +597,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 const int32_t* hs = (const int32_t*)io.readback(dinfo, (size_t)k * 4);
                 sigma.assign(hs, hs + k);
                 const int32_t* hf = (const int32_t*)io.readback(dflag, 4);
-                ok = *hf == 0;
+                ok = *hf == 0 && !force_fallback;
                 if (ok) {
                     if (r > 0) {  // Uhat_old -= Uhat_old[:, J] Unew
                         DMat Up = Upd.sub(0, 0, r, k);
@@ -608,7 +608,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 }
             }
         }
-        if (force_fallback) ok = false;
+        if (force_fallback) ok = false;  // (test hook; never set in production)
         if (!ok) {
             // Exact sequential fallback for this chunk: recompute its residual and
             // run the row-order kernel on it.

@@ -1,0 +1,382 @@
+// ffb_tc_gemm.cu -- tcgen05 / TMEM / TMA modular GEMM for small primes (p <= 255).
+//
+//   C (M x N, uint32 residues) = C -/+ op(A) op(B)  or  op(A) op(B)   (mod p)
+//
+// Operands are first packed (bandwidth-bound kernel) into centered int8
+// K-major buffers: x in [0,p) -> x or x-p in [-127, 127].  The products are
+// exact in int32 (|acc| <= K * 127^2 < 2^31 for K < 133k), so the modular
+// reduction is delayed to the epilogue: one Barrett reduction per output.
+//
+// Kernel (one 128 x BN output tile per CTA, 6 warps):
+//   warp 0      TMA producer: 128x128 B A-tile + BNx128 B B-tile per stage,
+//               SWIZZLE_128B, mbarrier expect_tx
+//   warp 1      TMEM allocation + single-thread tcgen05.mma.kind::i8 issue
+//               (M=128, N=BN, K=32 per instruction, 4 per stage), commit
+//               frees the stage / signals the accumulator
+//   warps 2..5  epilogue: tcgen05.ld 32x32b.x32 -> mod p -> smem transpose ->
+//               coalesced read-modify-write of C
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "ffb_kernels.cuh"
+
+namespace ffb {
+
+namespace {
+
+constexpr int TC_BM = 128;
+constexpr int TC_BK = 128;  // bytes = int8 elements per stage (one 128B swizzle atom)
+constexpr int TC_THREADS = 192;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "LAB_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+        "@P1 bra DONE;\n"
+        "bra LAB_WAIT;\n"
+        "DONE:\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int x,
+                                            int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+        "%4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);  // start address
+    d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;        // SBO: 8 rows x 128 B
+    d |= (uint64_t)1 << 46;                  // descriptor version (sm100)
+    d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+    return d;
+}
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accum) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+template <int BN>
+struct TcCfg {
+    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int A_BYTES = TC_BM * TC_BK;
+    static constexpr int B_BYTES = BN * TC_BK;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int EPI_BYTES = 4 * 32 * 33 * 4;
+    static constexpr int SMEM = 1024 + STAGES * STAGE_BYTES + EPI_BYTES + 256;
+    static constexpr uint32_t IDESC = (2u << 4)           // D format: s32
+                                      | (1u << 7)         // A: signed int8
+                                      | (1u << 10)        // B: signed int8
+                                      | ((uint32_t)(BN >> 3) << 17)  // N
+                                      | ((uint32_t)(TC_BM >> 4) << 24);  // M
+};
+
+template <int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_gemm_i8_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 uint32_t* __restrict__ C, int64_t ldc, int M, int N, int nk, Fp f, int mode) {
+    using Cfg = TcCfg<BN>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + Cfg::STAGES * Cfg::A_BYTES;
+    uint32_t* sEpi = (uint32_t*)(smem + Cfg::STAGES * Cfg::STAGE_BYTES);
+    uint64_t* full = (uint64_t*)(sEpi + 4 * 32 * 33);
+    uint64_t* empty = full + Cfg::STAGES;
+    uint64_t* accfull = empty + Cfg::STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(accfull + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * BN;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+        for (int s = 0; s < Cfg::STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"((uint32_t)BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer ----
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % Cfg::STAGES;
+                const uint32_t ph = (kb / Cfg::STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                tma_load_2d(sA + s * Cfg::A_BYTES, &tmA, &full[s], kb * TC_BK, m0);
+                tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, &full[s], kb * TC_BK, n0);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer (single thread) ----
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % Cfg::STAGES;
+                const uint32_t ph = (kb / Cfg::STAGES) & 1;
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                const uint32_t a0 = smem_u32(sA + s * Cfg::A_BYTES);
+                const uint32_t b0 = smem_u32(sB + s * Cfg::B_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < TC_BK / 32; ++kk)
+                    mma_i8(tmem, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), Cfg::IDESC,
+                           (kb | kk) != 0);
+                mma_commit(&empty[s]);  // stage free once these MMAs have read it
+            }
+            mma_commit(accfull);
+        }
+    } else {
+        // ---- epilogue: warps 2..5 own TMEM lanes 32*(warp%4) .. +31 ----
+        const int q = warp & 3;
+        uint32_t* tile = sEpi + (warp - 2) * 32 * 33;
+        mbar_wait(accfull, 0);
+        tc_fence_after();
+        const uint64_t off = (uint64_t)f.p * ((0x80000000ull + f.p - 1) / f.p);  // multiple of p >= 2^31
+        for (int c = 0; c < BN; c += 32) {
+            if (n0 + c >= N) break;
+            uint32_t r[32];
+            tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c, r);
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                tile[lane * 33 + j] = red64(f, (uint64_t)((int64_t)(int32_t)r[j] + (int64_t)off));
+            __syncwarp();
+            const int col = n0 + c + lane;
+            for (int rr = 0; rr < 32; ++rr) {
+                const int row = m0 + 32 * q + rr;
+                if (row < M && col < N) {
+                    const uint32_t v = tile[rr * 33 + lane];
+                    uint32_t* cp = C + (int64_t)row * ldc + col;
+                    if (mode == GEMM_SUB) *cp = fsub(f, *cp, v);
+                    else if (mode == GEMM_ADD) *cp = fadd(f, *cp, v);
+                    else *cp = v;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"((uint32_t)BN));
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Packing: dst (rows x ldd int8, K-major) <- centered op(src), zero padding.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int8_t center(uint32_t x, uint32_t p) {
+    return (int8_t)(x > (p >> 1) ? (int32_t)x - (int32_t)p : (int32_t)x);
+}
+
+// not transposed: op(src)[i][k] = src[i][k]
+__global__ void k_pack_n(int8_t* dst, int64_t ldd, const uint32_t* src, int64_t lds, int64_t rows,
+                         int64_t K, uint32_t p) {
+    const int64_t i = blockIdx.y;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < ldd;
+         k += (int64_t)gridDim.x * blockDim.x)
+        dst[i * ldd + k] = (i < rows && k < K) ? center(src[i * lds + k], p) : (int8_t)0;
+}
+
+// transposed: op(src)[i][k] = src[k][i]  (src is K x rows)
+__global__ void k_pack_t(int8_t* dst, int64_t ldd, const uint32_t* src, int64_t lds, int64_t rows,
+                         int64_t K, uint32_t p) {
+    __shared__ int8_t tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
+    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+        const int64_t k = k0 + yy, i = i0 + threadIdx.x;
+        tile[yy][threadIdx.x] = (k < K && i < rows) ? center(src[k * lds + i], p) : (int8_t)0;
+    }
+    __syncthreads();
+    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+        const int64_t i = i0 + yy, k = k0 + threadIdx.x;
+        if (i < rows && k < ldd) dst[i * ldd + k] = tile[threadIdx.x][yy];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+void load_encode() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    });
+    if (!g_encode) throw Status(FFB_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+}
+
+CUtensorMap make_map(const int8_t* base, int64_t rows, int64_t ld, int box_rows) {
+    CUtensorMap m;
+    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {(cuuint32_t)TC_BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)base, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) throw Status(FFB_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+struct Scratch {
+    int8_t* ptr = nullptr;
+    size_t cap = 0;
+};
+thread_local Scratch g_scratch;
+
+int8_t* scratch(size_t bytes) {
+    if (g_scratch.cap < bytes) {
+        if (g_scratch.ptr) {
+            FFB_CUDA(cudaDeviceSynchronize());
+            FFB_CUDA(cudaFree(g_scratch.ptr));
+        }
+        const size_t cap = std::max(bytes + bytes / 4, (size_t)64 << 20);
+        FFB_CUDA(cudaMalloc(&g_scratch.ptr, cap));
+        g_scratch.cap = cap;
+    }
+    return g_scratch.ptr;
+}
+
+void pack(cudaStream_t st, int8_t* dst, int64_t ldd, DMat src, bool trans, int64_t rows, int64_t K,
+          uint32_t p) {
+    if (!trans) {
+        for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
+            const int64_t nr = std::min<int64_t>(65535, rows - r0);
+            int64_t gx = std::min<int64_t>(64, cdiv(ldd, 256));
+            k_pack_n<<<dim3((unsigned)gx, (unsigned)nr), 256, 0, st>>>(
+                dst + r0 * ldd, ldd, src.ptr + r0 * src.ld, src.ld, nr, K, p);
+        }
+    } else {
+        dim3 grid((unsigned)cdiv(ldd, 32), (unsigned)cdiv(rows, 32));
+        k_pack_t<<<grid, dim3(32, 8), 0, st>>>(dst, ldd, src.ptr, src.ld, rows, K, p);
+    }
+    ++g_launches;
+    FFB_CHECK_LAUNCH();
+}
+
+template <int BN>
+void launch_tc(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, DMat C, int64_t M,
+               int64_t N, int64_t nk, const Fp& f, int mode) {
+    using Cfg = TcCfg<BN>;
+    static bool attr = false;
+    if (!attr) {
+        FFB_CUDA(cudaFuncSetAttribute(k_gemm_i8_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Cfg::SMEM));
+        attr = true;
+    }
+    dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, TC_BM));
+    k_gemm_i8_tc<BN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ma, mb, C.ptr, C.ld, (int)M, (int)N,
+                                                          (int)nk, f, mode);
+    ++g_launches;
+    FFB_CHECK_LAUNCH();
+}
+
+}  // namespace
+
+bool tc_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K) {
+    static const bool disabled = getenv("FFB_DISABLE_TC") != nullptr;
+    if (disabled) return false;
+    return f.p <= 255 && M >= 64 && N >= 64 && K >= 16 && K <= 120000 &&
+           (double)M * N * K >= 4.0e6 && M < (1ll << 31) && N < (1ll << 31);
+}
+
+void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
+             int64_t M, int64_t N, int64_t K) {
+    load_encode();
+    const int64_t Kp = (K + 15) / 16 * 16;
+    const size_t abytes = ((size_t)M * Kp + 1023) / 1024 * 1024;
+    const size_t bbytes = ((size_t)N * Kp + 1023) / 1024 * 1024;
+    int8_t* buf = scratch(abytes + bbytes);
+    int8_t* Ap = buf;
+    int8_t* Bp = buf + abytes;
+    {
+        ProfScope ps(K_MOVE, st, 0.0, 5.0 * (M * K + N * K));
+        pack(st, Ap, Kp, A, ta, M, K, f.p);
+        pack(st, Bp, Kp, B, !tb, N, K, f.p);  // need B^T (N x K): transposed pack unless tb
+    }
+    const int64_t nk = cdiv(Kp, TC_BK);
+    const bool wide = N >= 256 && M * N >= (int64_t)148 * 128 * 256;
+    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, (double)M * K + N * K + 8.0 * M * N);
+    if (wide) {
+        CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, 256);
+        launch_tc<256>(st, ma, mb, C, M, N, nk, f, mode);
+    } else {
+        CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, 128);
+        launch_tc<128>(st, ma, mb, C, M, N, nk, f, mode);
+    }
+}
+
+}  // namespace ffb

@@ -1,0 +1,52 @@
+"""The tcgen05 int8 GEMM path (p <= 255, large shapes) against the oracle, for every
+operand orientation the engine uses (NN via gemm_sub/trmm_sub, TN via syr2k_sub, NT via
+syrdk_sub), ragged sizes (partial M/N tiles, K not a multiple of the 128-byte stage), and
+the int32 accumulator headroom (K up to 20000 with |x| = 65)."""
+import numpy as np
+import pytest
+
+from helpers import rand_sym
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 128, 128), (256, 512, 256), (300, 500, 700),
+                                   (129, 257, 65), (1000, 64, 200), (64, 1000, 3000),
+                                   (513, 300, 20000)])
+@pytest.mark.parametrize("p", [131, 251, 2, 3])
+def test_tc_gemm_nn(gpu, oracle, m, n, k, p):
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(m * 7 + n * 3 + k + p)
+    if p == 131 and k == 20000:
+        a = np.full((m, k), 65, np.uint64)  # worst case |centered| for p=131
+        b = np.full((k, n), 66, np.uint64)  # = -65
+    else:
+        a = rng.integers(0, p, (m, k), dtype=np.uint64)
+        b = rng.integers(0, p, (k, n), dtype=np.uint64)
+    c = rng.integers(0, p, (m, n), dtype=np.uint64)
+    assert np.array_equal(ffb.gemm_sub(c, a, b, p, ctx=gpu), oracle.gemm_sub(p, c, a, b))
+
+
+@pytest.mark.parametrize("n,k", [(300, 200), (520, 130), (256, 2048)])
+def test_tc_gemm_transposed_operands(gpu, oracle, n, k):
+    import paper_1802_10453_b200 as ffb
+    p = 131
+    rng = np.random.default_rng(n + k)
+    c = rand_sym(rng, p, n)
+    a = rng.integers(0, p, (k, n), dtype=np.uint64)
+    b = rng.integers(0, p, (k, n), dtype=np.uint64)
+    assert np.array_equal(ffb.syr2k_sub(c, a, b, p, ctx=gpu), oracle.syr2k_sub(p, c, a, b))
+    g = rng.integers(0, p, (n, k - k % 2), dtype=np.uint64)
+    kk = g.shape[1]
+    blocks = []
+    t = 0
+    while t < kk:
+        if t + 1 < kk and rng.integers(0, 3) == 0:
+            blocks.append(ffb.AntiDiagBlock(int(rng.integers(1, p))))
+            t += 2
+        else:
+            blocks.append(ffb.ScalarBlock(int(rng.integers(1, p))))
+            t += 1
+    d = ffb.BlockDiag(blocks)
+    kind, val, val2 = d.columns()
+    assert np.array_equal(ffb.syrdk_sub(c, g, d, p, ctx=gpu), oracle.syrdk_sub(p, c, g, kind, val, val2))
