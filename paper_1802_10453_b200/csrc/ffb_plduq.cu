@@ -137,32 +137,65 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
 }
 
 // ---------------------------------------------------------------------------
-// Column rank profile of RI (k x n), phase 1: per block of CRP_W columns, the
-// local candidates (columns independent of the earlier columns of the block).
-// Column vectors have length k (<= 128).  cand[block*kmax + t], ccount[block].
+// Column rank profile (CRP) of RI (k x n) by a reduction tree.  Each CTA scans
+// an ordered set of columns and keeps those independent of the earlier
+// columns of the set (a local CRP).  A column dropped at any level depends on
+// earlier columns, so it is dependent globally too, and the CRP of a union of
+// surviving sets equals the CRP of the union of the underlying column ranges.
+// Level 0 (range mode): CTA g scans columns [g*CRP_W, (g+1)*CRP_W).
+// Level > 0 (list mode): CTA g scans the concatenation of input lists
+// g*fan .. g*fan+fan-1 (each <= k columns, ascending).  Output: out[g*k + t],
+// ocount[g].  The last level (one CTA) yields the CRP J.
 // ---------------------------------------------------------------------------
-constexpr int CRP_W = 256, CRP_G = 32, CRP_KMAX = 128;
+constexpr int CRP_W = 256, CRP_G = 32, CRP_KMAX = 128, CRP_FAN = 8;
 
-__global__ void __launch_bounds__(256) k_crp_local(Fp f, const uint32_t* RI, int64_t ldr, int k,
-                                                   int64_t n, int32_t* cand, int32_t* ccount) {
+__global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int64_t ldr, int k,
+                                                  int64_t n, const int32_t* in, const int32_t* icount,
+                                                  int nin, int32_t* out, int32_t* ocount) {
     extern __shared__ uint32_t sm[];
     uint32_t* E = sm;                           // basis: up to k vectors of length k
     uint32_t* V = E + (size_t)CRP_KMAX * k;     // CRP_G columns, each length k: V[c*k + i]
     __shared__ int rho[CRP_KMAX];
+    __shared__ int colid[CRP_G];
     __shared__ int nb;
     __shared__ int nzmask[CRP_G];
+    __shared__ int total, lead;
+    __shared__ uint32_t vr[CRP_KMAX];
+    __shared__ uint32_t il;
     const int tid = threadIdx.x;
-    const int64_t c0 = (int64_t)blockIdx.x * CRP_W;
-    const int64_t c1 = (c0 + CRP_W < n) ? c0 + CRP_W : n;
-    if (tid == 0) nb = 0;
+    const int g = blockIdx.x;
+    // the ordered column set of this CTA
+    auto column_at = [&](int idx) -> int {
+        if (!in) return g * CRP_W + idx;
+        int q = idx;
+        for (int l = g * CRP_FAN; l < g * CRP_FAN + CRP_FAN && l < nin; ++l) {
+            const int c = icount[l];
+            if (q < c) return in[(int64_t)l * k + q];
+            q -= c;
+        }
+        return -1;
+    };
+    if (tid == 0) {
+        nb = 0;
+        if (!in) {
+            const int64_t c0 = (int64_t)g * CRP_W;
+            total = (int)((c0 + CRP_W < n ? c0 + CRP_W : n) - c0);
+        } else {
+            int t = 0;
+            for (int l = g * CRP_FAN; l < g * CRP_FAN + CRP_FAN && l < nin; ++l) t += icount[l];
+            total = t;
+        }
+    }
     __syncthreads();
-    for (int64_t g0 = c0; g0 < c1 && nb < k; g0 += CRP_G) {
-        const int gw = (int)((g0 + CRP_G <= c1) ? CRP_G : c1 - g0);
+    for (int s0 = 0; s0 < total && nb < k; s0 += CRP_G) {
+        const int gw = (s0 + CRP_G <= total) ? CRP_G : total - s0;
+        if (tid < gw) colid[tid] = column_at(s0 + tid);
+        if (tid < CRP_G) nzmask[tid] = 0;
+        __syncthreads();
         for (int e = tid; e < gw * k; e += blockDim.x) {
             const int c = e % gw, i = e / gw;
-            V[(size_t)c * k + i] = RI[(int64_t)i * ldr + g0 + c];
+            V[(size_t)c * k + i] = RI[(int64_t)i * ldr + colid[c]];
         }
-        if (tid < CRP_G) nzmask[tid] = 0;
         __syncthreads();
         // reduce every column of the group against the current basis; flag the
         // columns that stay nonzero (candidates for a new basis vector)
@@ -177,13 +210,10 @@ __global__ void __launch_bounds__(256) k_crp_local(Fp f, const uint32_t* RI, int
             if (fsub(f, V[(size_t)c * k + i], red64(f, acc)) != 0) atomicOr(&nzmask[c], 1);
         }
         __syncthreads();
-        // Sequential handling of columns with a nonzero reduction (rare after the
-        // basis fills): recompute each candidate's reduction exactly in order.
+        // flagged columns in order: exact reduction against the current basis
         for (int c = 0; c < gw; ++c) {
             if (!nzmask[c]) continue;  // uniform (shared)
             const int kb2 = nb;
-            __shared__ uint32_t vr[CRP_KMAX];
-            __shared__ int lead;
             for (int i = tid; i < k; i += blockDim.x) {
                 uint64_t acc = 0;
                 for (int t = 0; t < kb2; ++t) {
@@ -199,7 +229,6 @@ __global__ void __launch_bounds__(256) k_crp_local(Fp f, const uint32_t* RI, int
             __syncthreads();
             const int ld = lead;
             if (ld < k) {
-                __shared__ uint32_t il;
                 if (tid == 0) il = finv(f, vr[ld]);
                 __syncthreads();
                 for (int i = tid; i < k; i += blockDim.x) vr[i] = fmul(f, vr[i], il);
@@ -213,7 +242,7 @@ __global__ void __launch_bounds__(256) k_crp_local(Fp f, const uint32_t* RI, int
                 for (int i = tid; i < k; i += blockDim.x) E[(size_t)kb2 * k + i] = vr[i];
                 if (tid == 0) {
                     rho[kb2] = ld;
-                    cand[(int64_t)blockIdx.x * k + kb2] = (int32_t)(g0 + c);
+                    out[(int64_t)g * k + kb2] = colid[c];
                     nb = kb2 + 1;
                 }
             }
@@ -222,67 +251,19 @@ __global__ void __launch_bounds__(256) k_crp_local(Fp f, const uint32_t* RI, int
         }
         __syncthreads();
     }
-    if (tid == 0) ccount[blockIdx.x] = nb;
+    if (tid == 0) ocount[g] = nb;
 }
 
-// Phase 2 (1 CTA): merge the per-block candidates left to right into the
-// global CRP.  out[0] = |J|, out[1..] = J ascending.
-__global__ void __launch_bounds__(128) k_crp_merge(Fp f, const uint32_t* RI, int64_t ldr, int k,
-                                                   int nblocks, const int32_t* cand,
-                                                   const int32_t* ccount, int32_t* out) {
-    extern __shared__ uint32_t sm[];
-    uint32_t* E = sm;  // k x k basis
-    __shared__ uint32_t vr[CRP_KMAX];
-    __shared__ int rho[CRP_KMAX];
-    __shared__ int nb, lead;
-    __shared__ uint32_t il;
-    const int tid = threadIdx.x;
-    if (tid == 0) nb = 0;
-    __syncthreads();
-    for (int blk = 0; blk < nblocks && nb < k; ++blk) {
-        const int cc = ccount[blk];
-        for (int q = 0; q < cc && nb < k; ++q) {
-            const int j = cand[(int64_t)blk * k + q];
-            const int kb = nb;
-            __shared__ uint32_t col[CRP_KMAX];
-            for (int i = tid; i < k; i += blockDim.x) col[i] = RI[(int64_t)i * ldr + j];
-            __syncthreads();
-            for (int i = tid; i < k; i += blockDim.x) {
-                uint64_t acc = 0;
-                for (int t = 0; t < kb; ++t) {
-                    acc += (uint64_t)col[rho[t]] * E[(size_t)t * k + i];
-                    if ((t & 15) == 15 && f.p >= (1u << 26)) acc = red64(f, acc);
-                }
-                vr[i] = fsub(f, col[i], red64(f, acc));
-            }
-            if (tid == 0) lead = k;
-            __syncthreads();
-            for (int i = tid; i < k; i += blockDim.x)
-                if (vr[i]) atomicMin(&lead, i);
-            __syncthreads();
-            const int ld = lead;
-            if (ld < k) {
-                if (tid == 0) il = finv(f, vr[ld]);
-                __syncthreads();
-                for (int i = tid; i < k; i += blockDim.x) vr[i] = fmul(f, vr[i], il);
-                __syncthreads();
-                for (int e = tid; e < kb * k; e += blockDim.x) {
-                    const int t = e / k, i = e % k;
-                    const uint32_t c = E[(size_t)t * k + ld];
-                    if (c) E[(size_t)t * k + i] = fsub(f, E[(size_t)t * k + i], fmul(f, c, vr[i]));
-                }
-                __syncthreads();
-                for (int i = tid; i < k; i += blockDim.x) E[(size_t)kb * k + i] = vr[i];
-                if (tid == 0) {
-                    rho[kb] = ld;
-                    out[1 + kb] = j;
-                    nb = kb + 1;
-                }
-            }
-            __syncthreads();
-        }
+// Append a chunk's pivots to the device bookkeeping: Uhat row order J,
+// pivot rows c0 + I[t] with columns J[sigma[t]].
+__global__ void k_append_pivots(int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r,
+                                int64_t c0, const int32_t* I, const int32_t* J,
+                                const int32_t* sigma, int k) {
+    for (int t = threadIdx.x; t < k; t += blockDim.x) {
+        uhat_col[r + t] = J[t];
+        prow[r + t] = (int32_t)(c0 + I[t]);
+        pcol[r + t] = J[sigma[t]];
     }
-    if (tid == 0) out[0] = nb;
 }
 
 // ---------------------------------------------------------------------------
@@ -499,8 +480,6 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     const int64_t m = Y.rows, n = Y.cols, mn = std::min(m, n);
     const int B = 128, SK = B + 16;
     PlduqOut out;
-    std::vector<int32_t> pr, pcol_rows;  // pivot rows (global, in pivot order), pivot columns
-    std::vector<int32_t> uhat_col;       // pivot column of each Uhat row (Uhat row order)
     DMat Uhat = ws.mat(std::max<int64_t>(mn, 1), n);
     DMat Om = ws.mat(n, SK);
     {
@@ -510,27 +489,29 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     DMat R = ws.mat(B, n), S = ws.mat(B, SK), RI = ws.mat(B, n), Unew = ws.mat(B, n);
     DMat Kc = ws.mat(B, B), Kinv = ws.mat(B, B), G = ws.mat(B, std::max<int64_t>(mn, 1));
     DMat Gc = ws.mat(B, B), Upd = ws.mat(std::max<int64_t>(mn, 1), B);
-    const int nblk = (int)cdiv(n, CRP_W);
-    int32_t* dinfo = ws.vec<int32_t>(4 * B + 16);  // row detect out / crp out / sigma / flags
-    int32_t* cand = ws.vec<int32_t>((int64_t)nblk * B);
-    int32_t* ccount = ws.vec<int32_t>(nblk);
-    int32_t* dflag = ws.vec<int32_t>(4);
-    int64_t r = 0;
+    const int nblk0 = (int)cdiv(n, CRP_W);
+    int32_t* dinfo = ws.vec<int32_t>(2 * B + 16);     // row detect: k, I[0..k)
+    int32_t* lists[2] = {ws.vec<int32_t>((int64_t)nblk0 * B), ws.vec<int32_t>((int64_t)nblk0 * B)};
+    int32_t* counts[2] = {ws.vec<int32_t>(nblk0), ws.vec<int32_t>(nblk0)};
+    int32_t* dsig = ws.vec<int32_t>(B);
+    int32_t* dflag = ws.vec<int32_t>(4);              // sticky: any chunk failed its exact check
+    int32_t* d_uhat_col = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
+    int32_t* d_prow = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
+    int32_t* d_pcol = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
 
     const size_t rd_smem = ((size_t)RD_MAX_B * SK + SK) * 4;
     const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + (size_t)CRP_G * CRP_KMAX) * 4;
     static bool attrs = false;
     if (!attrs) {
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
-        FFB_CUDA(cudaFuncSetAttribute(k_crp_local, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crp_smem));
-        FFB_CUDA(cudaFuncSetAttribute(k_crp_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(CRP_KMAX * CRP_KMAX * 4)));
+        FFB_CUDA(cudaFuncSetAttribute(k_crp_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crp_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * CRP_KMAX * CRP_KMAX * 4)));
         attrs = true;
     }
+    static const bool force_exact = getenv("FFB_PLDUQ_FORCE_FALLBACK") != nullptr;  // test hook
 
-    for (int64_t c0 = 0; c0 < m; c0 += B) {
-        const int64_t bc = std::min<int64_t>(B, m - c0);
-        DMat Yc = Y.sub(c0, 0, bc, n), Rc = R.sub(0, 0, bc, n);
+    // Residual of chunk rows [c0, c0+bc) against the r pivots found so far.
+    auto residual = [&](DMat Rc, DMat Yc, int64_t bc, int64_t r) {
         {
             ProfScope ps(K_MOVE, st, 0.0, 8.0 * bc * n);
             k_copy_rows<<<rgrid(bc, n), 256, 0, st>>>(Rc.ptr, Rc.ld, Yc.ptr, Yc.ld, n);
@@ -538,143 +519,122 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         }
         if (r > 0) {
             DMat Gv = G.sub(0, 0, bc, r);
-            gather2d(st, Gv, Yc, nullptr, io.upload(uhat_col));
+            gather2d(st, Gv, Yc, nullptr, d_uhat_col);
             gemm(f, st, GEMM_SUB, Rc, Gv, false, Uhat.sub(0, 0, r, n), false, bc, n, r);
         }
-        DMat Sc = S.sub(0, 0, bc, SK);
-        gemm(f, st, GEMM_SET, Sc, Rc, false, Om, false, bc, SK, n);
+    };
+    // Given the chunk's pivot rows (device dI, k of them) and pivot column set
+    // (device dJ, ascending) with the pairing dsig: Uhat absorbs the chunk.
+    auto absorb = [&](DMat Rc, int64_t bc, int64_t r, int k, const int32_t* dI, const int32_t* dJ,
+                      bool verify, int64_t c0) {
+        DMat RIk = RI.sub(0, 0, k, n), Un = Unew.sub(0, 0, k, n);
+        DMat Kck = Kc.sub(0, 0, k, k), Kik = Kinv.sub(0, 0, k, k);
+        gather2d(st, Kck, RIk, nullptr, dJ);
         {
             ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-            k_row_detect<<<1, 256, rd_smem, st>>>(f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo);
+            k_pair<<<1, 256, (size_t)3 * k * k * 4, st>>>(f, Kck.ptr, Kck.ld, k, dsig, Kik.ptr,
+                                                          Kik.ld, dflag);
             count_launch();
             FFB_CHECK_LAUNCH();
         }
-        const int32_t* hb = (const int32_t*)io.readback(dinfo, (size_t)(1 + bc) * 4);
-        const int k = hb[0];
-        static const bool force_fallback = getenv("FFB_PLDUQ_FORCE_FALLBACK") != nullptr;
-        std::vector<int32_t> I(hb + 1, hb + 1 + k);
-        bool ok = true;
-        std::vector<int32_t> J, sigma;
-        if (k == 0) {
-            FFB_CUDA(cudaMemsetAsync(dflag, 0, 4, st));
+        gemm(f, st, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);  // Unew = Kc^-1 R_I
+        if (verify) {  // exact check: R - R[:, J] Unew == 0 (sticky flag)
+            DMat Gck = Gc.sub(0, 0, bc, k);
+            gather2d(st, Gck, Rc, nullptr, dJ);
+            gemm(f, st, GEMM_SUB, Rc, Gck, false, Un, false, bc, n, k);
             any_nonzero(st, Rc, dflag);
-            ok = *(const int32_t*)io.readback(dflag, 4) == 0;
-        } else {
-            DMat RIk = RI.sub(0, 0, k, n);
-            gather_rows(st, RIk, Rc, io.upload(I));
-            {
-                ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-                k_crp_local<<<nblk, 256, crp_smem, st>>>(f, RIk.ptr, RIk.ld, k, n, cand, ccount);
-                count_launch();
-                k_crp_merge<<<1, 128, (size_t)CRP_KMAX * CRP_KMAX * 4, st>>>(f, RIk.ptr, RIk.ld, k, nblk,
-                                                                              cand, ccount, dinfo);
-                count_launch();
-                FFB_CHECK_LAUNCH();
-            }
-            const int32_t* hj = (const int32_t*)io.readback(dinfo, (size_t)(1 + k) * 4);
-            if (hj[0] != k) {
-                ok = false;
-            } else {
-                J.assign(hj + 1, hj + 1 + k);
-                DMat Kck = Kc.sub(0, 0, k, k), Kik = Kinv.sub(0, 0, k, k);
-                gather2d(st, Kck, RIk, nullptr, io.upload(J));
-                FFB_CUDA(cudaMemsetAsync(dflag, 0, 4, st));
+        }
+        if (r > 0) {  // Uhat_old -= Uhat_old[:, J] Unew
+            DMat Up = Upd.sub(0, 0, r, k);
+            gather2d(st, Up, Uhat.sub(0, 0, r, n), nullptr, dJ);
+            gemm(f, st, GEMM_SUB, Uhat.sub(0, 0, r, n), Up, false, Un, false, r, n, k);
+        }
+        copy_mat(st, Uhat.sub(r, 0, k, n), Un);
+        k_append_pivots<<<1, 128, 0, st>>>(d_uhat_col, d_prow, d_pcol, r, c0, dI, dJ, dsig, k);
+        count_launch();
+    };
+
+    int64_t r = 0;
+    bool exact = force_exact;
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        r = 0;
+        FFB_CUDA(cudaMemsetAsync(dflag, 0, 4, st));
+        for (int64_t c0 = 0; c0 < m; c0 += B) {
+            const int64_t bc = std::min<int64_t>(B, m - c0);
+            DMat Yc = Y.sub(c0, 0, bc, n), Rc = R.sub(0, 0, bc, n);
+            residual(Rc, Yc, bc, r);
+            if (!exact) {
+                // pivot rows from the sketch
+                DMat Sc = S.sub(0, 0, bc, SK);
+                gemm(f, st, GEMM_SET, Sc, Rc, false, Om, false, bc, SK, n);
                 {
                     ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-                    k_pair<<<1, 256, (size_t)3 * k * k * 4, st>>>(f, Kck.ptr, Kck.ld, k, dinfo,
-                                                                  Kik.ptr, Kik.ld, dflag);
+                    k_row_detect<<<1, 256, rd_smem, st>>>(f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo);
                     count_launch();
                     FFB_CHECK_LAUNCH();
                 }
-                DMat Un = Unew.sub(0, 0, k, n);
-                gemm(f, st, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);
-                // exact check: R - R[:, J] Unew == 0
-                DMat Gck = Gc.sub(0, 0, bc, k);
-                const int32_t* dJ = io.upload(J);
-                gather2d(st, Gck, Rc, nullptr, dJ);
-                gemm(f, st, GEMM_SUB, Rc, Gck, false, Un, false, bc, n, k);
-                any_nonzero(st, Rc, dflag);
-                const int32_t* hs = (const int32_t*)io.readback(dinfo, (size_t)k * 4);
-                sigma.assign(hs, hs + k);
-                const int32_t* hf = (const int32_t*)io.readback(dflag, 4);
-                ok = *hf == 0 && !force_fallback;
-                if (ok) {
-                    if (r > 0) {  // Uhat_old -= Uhat_old[:, J] Unew
-                        DMat Up = Upd.sub(0, 0, r, k);
-                        gather2d(st, Up, Uhat.sub(0, 0, r, n), nullptr, dJ);
-                        gemm(f, st, GEMM_SUB, Uhat.sub(0, 0, r, n), Up, false, Un, false, r, n, k);
+                const int k = *(const int32_t*)io.readback(dinfo, 4);
+                if (k == 0) {
+                    any_nonzero(st, Rc, dflag);  // the chunk must be entirely dependent
+                    continue;
+                }
+                const int32_t* dI = dinfo + 1;
+                gather_rows(st, RI.sub(0, 0, k, n), Rc, dI);
+                // pivot column set: CRP reduction tree
+                {
+                    ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
+                    k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, nullptr, nullptr,
+                                                             0, lists[0], counts[0]);
+                    count_launch();
+                    int groups = nblk0, cur = 0;
+                    while (groups > 1) {
+                        const int ng = (groups + CRP_FAN - 1) / CRP_FAN;
+                        k_crp_list<<<ng, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, lists[cur],
+                                                              counts[cur], groups, lists[cur ^ 1],
+                                                              counts[cur ^ 1]);
+                        count_launch();
+                        groups = ng;
+                        cur ^= 1;
                     }
-                    copy_mat(st, Uhat.sub(r, 0, k, n), Un);
+                    FFB_CHECK_LAUNCH();
+                    absorb(Rc, bc, r, k, dI, lists[cur], true, c0);
                 }
+                r += k;
+            } else {
+                // Exact row-order kernel on a copy of the residual.
+                const size_t mk = ws.mark();
+                DMat Rw = ws.mat(bc, n);
+                copy_mat(st, Rw, Rc);
+                int32_t* info = ws.vec<int32_t>(1 + bc + n + bc);
+                int32_t* colflag = ws.vec<int32_t>(n);
+                uint32_t* lvec = ws.vec<uint32_t>(bc);
+                DMat Lo = ws.mat(bc, std::min<int64_t>(bc, n)), Uo = ws.mat(std::min<int64_t>(bc, n), n);
+                uint32_t* dd = ws.vec<uint32_t>(bc);
+                plduq(f, st, Rw, info, colflag, lvec, Lo, dd, Uo);
+                const int32_t* hi = (const int32_t*)io.readback(info, (size_t)(1 + bc + n + bc) * 4);
+                const int k = hi[0];
+                std::vector<int32_t> I(hi + 1, hi + 1 + k);
+                std::vector<int32_t> J(hi + 1 + bc + n, hi + 1 + bc + n + k);
+                std::sort(J.begin(), J.end());
+                ws.release(mk);
+                if (k == 0) continue;
+                const int32_t* dI = io.upload(I);
+                gather_rows(st, RI.sub(0, 0, k, n), Rc, dI);
+                absorb(Rc, bc, r, k, dI, io.upload(J), false, c0);
+                r += k;
             }
         }
-        if (force_fallback) ok = false;  // (test hook; never set in production)
-        if (!ok) {
-            // Exact sequential fallback for this chunk: recompute its residual and
-            // run the row-order kernel on it.
-            ++out.fallbacks;
-            DMat Rf = R.sub(0, 0, bc, n);
-            k_copy_rows<<<rgrid(bc, n), 256, 0, st>>>(Rf.ptr, Rf.ld, Yc.ptr, Yc.ld, n);
-            count_launch();
-            if (r > 0) {
-                DMat Gv = G.sub(0, 0, bc, r);
-                gather2d(st, Gv, Yc, nullptr, io.upload(uhat_col));
-                gemm(f, st, GEMM_SUB, Rf, Gv, false, Uhat.sub(0, 0, r, n), false, bc, n, r);
-            }
-            const size_t mk = ws.mark();
-            int32_t* info = ws.vec<int32_t>(1 + bc + n + bc);
-            int32_t* colflag = ws.vec<int32_t>(n);
-            uint32_t* lvec = ws.vec<uint32_t>(bc);
-            DMat Lo = ws.mat(bc, std::min<int64_t>(bc, n)), Uo = ws.mat(std::min<int64_t>(bc, n), n);
-            uint32_t* dd = ws.vec<uint32_t>(bc);
-            plduq(f, st, Rf, info, colflag, lvec, Lo, dd, Uo);
-            const int32_t* hi = (const int32_t*)io.readback(info, (size_t)(1 + bc + n + bc) * 4);
-            const int kk = hi[0];
-            I.assign(hi + 1, hi + 1 + kk);  // pivot rows in order
-            std::vector<int32_t> pcs(hi + 1 + bc + n, hi + 1 + bc + n + kk);
-            // Unew rows: fully reduced basis of the new pivot rows (Kinv R_I) -> recompute
-            // simply from the chunk residual with J = sorted pivot columns.
-            J = pcs;
-            std::sort(J.begin(), J.end());
-            sigma.assign(kk, 0);
-            for (int t = 0; t < kk; ++t)
-                sigma[t] = (int32_t)(std::lower_bound(J.begin(), J.end(), pcs[t]) - J.begin());
-            ws.release(mk);
-            if (kk > 0) {
-                // recompute residual (plduq destroyed Rf), then Unew = Kc^-1 R_I
-                k_copy_rows<<<rgrid(bc, n), 256, 0, st>>>(Rf.ptr, Rf.ld, Yc.ptr, Yc.ld, n);
-                count_launch();
-                if (r > 0) {
-                    DMat Gv = G.sub(0, 0, bc, r);
-                    gather2d(st, Gv, Yc, nullptr, io.upload(uhat_col));
-                    gemm(f, st, GEMM_SUB, Rf, Gv, false, Uhat.sub(0, 0, r, n), false, bc, n, r);
-                }
-                DMat RIk = RI.sub(0, 0, kk, n);
-                gather_rows(st, RIk, Rf, io.upload(I));
-                DMat Kck = Kc.sub(0, 0, kk, kk), Kik = Kinv.sub(0, 0, kk, kk);
-                const int32_t* dJ = io.upload(J);
-                gather2d(st, Kck, RIk, nullptr, dJ);
-                FFB_CUDA(cudaMemsetAsync(dflag, 0, 4, st));
-                k_pair<<<1, 256, (size_t)3 * kk * kk * 4, st>>>(f, Kck.ptr, Kck.ld, kk, dinfo, Kik.ptr,
-                                                                Kik.ld, dflag);
-                count_launch();
-                DMat Un = Unew.sub(0, 0, kk, n);
-                gemm(f, st, GEMM_SET, Un, Kik, false, RIk, false, kk, n, kk);
-                if (r > 0) {
-                    DMat Up = Upd.sub(0, 0, r, kk);
-                    gather2d(st, Up, Uhat.sub(0, 0, r, n), nullptr, dJ);
-                    gemm(f, st, GEMM_SUB, Uhat.sub(0, 0, r, n), Up, false, Un, false, r, n, kk);
-                }
-                copy_mat(st, Uhat.sub(r, 0, kk, n), Un);
-            }
-        }
-        const int kk = (int)I.size();
-        for (int t = 0; t < kk; ++t) {
-            pr.push_back((int32_t)(c0 + I[t]));
-            pcol_rows.push_back(J[sigma[t]]);
-        }
-        for (int t = 0; t < kk; ++t) uhat_col.push_back(J[t]);
-        r += kk;
+        if (exact) break;
+        if (*(const int32_t*)io.readback(dflag, 4) == 0) break;
+        ++out.fallbacks;  // the sketch missed rank somewhere: redo exactly
+        exact = true;
+    }
+    std::vector<int32_t> pr, pcol_rows;
+    if (r > 0) {
+        const int32_t* hp = (const int32_t*)io.readback(d_prow, (size_t)r * 4);
+        pr.assign(hp, hp + r);
+        const int32_t* hc = (const int32_t*)io.readback(d_pcol, (size_t)r * 4);
+        pcol_rows.assign(hc, hc + r);
     }
 
     // ---- phase 2: factors from the pivots ----
