@@ -129,3 +129,21 @@ struct DDiag {
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace ffb
+
+namespace ffb {
+// Fast arithmetic for p < 2^16 (products < 2^32): 32-bit Barrett.
+struct Fp16 {
+    uint32_t p;
+    uint32_t mu;  // floor(2^32 / p)
+    __host__ __device__ explicit Fp16(uint32_t pp) : p(pp), mu((uint32_t)(0x100000000ull / pp)) {}
+    __device__ __forceinline__ uint32_t red(uint32_t x) const {
+        uint32_t q = __umulhi(x, mu);
+        uint32_t r = x - q * p;
+        return r >= p ? r - p : r;
+    }
+    __device__ __forceinline__ uint32_t mul(uint32_t a, uint32_t b) const { return red(a * b); }
+    __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const {
+        return a >= b ? a - b : a + p - b;
+    }
+};
+}  // namespace ffb

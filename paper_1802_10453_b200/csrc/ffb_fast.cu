@@ -1,0 +1,322 @@
+// ffb_fast.cu -- latency-critical small kernels: the 64x64 Crout leaf and the
+// inverse-based triangular-solve base.
+//
+// Leaf (Alg. 4, sytrf.cpp:35-139), right-looking, one CTA of 256 threads:
+// thread (ty, tx) owns S[ty + 4q][tx], q < 16, in registers, so the Schur
+// update has no index arithmetic and no shared-memory traffic for S.  The
+// pivot search of a step is a 64-bit ballot over the residual column masked
+// by the active rows; L is staged in shared memory and written to HBM once.
+#include <algorithm>
+
+#include "ffb_kernels.cuh"
+
+namespace ffb {
+
+namespace {
+
+// Field arithmetic selector: 32-bit Barrett for p < 2^16, 64-bit otherwise.
+template <bool kSmall>
+struct Ar;
+template <>
+struct Ar<true> {
+    Fp16 h;
+    Fp f;
+    __device__ explicit Ar(const Fp& ff) : h(ff.p), f(ff) {}
+    __device__ __forceinline__ uint32_t mul(uint32_t a, uint32_t b) const { return h.mul(a, b); }
+    __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const { return h.sub(a, b); }
+    __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) const { return fadd(f, a, b); }
+};
+template <>
+struct Ar<false> {
+    Fp f;
+    __device__ explicit Ar(const Fp& ff) : f(ff) {}
+    __device__ __forceinline__ uint32_t mul(uint32_t a, uint32_t b) const { return fmul(f, a, b); }
+    __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const { return fsub(f, a, b); }
+    __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) const { return fadd(f, a, b); }
+};
+
+template <bool kSmall>
+__global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict__ A, int64_t lda,
+                                                int s, const int32_t* __restrict__ rows,
+                                                uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
+                                                int32_t* out) {
+    __shared__ uint32_t Ls[64][65];
+    __shared__ uint32_t col1[64], col2[64];
+    __shared__ uint32_t l1v[64], l2v[64], u1v[64], u2v[64];
+    __shared__ int32_t order[64];
+    __shared__ int jsel;
+    const Ar<kSmall> ar(f);
+    const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6;
+    const uint32_t one = 1 % f.p;
+    uint32_t S[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int i = ty + 4 * q;
+        S[q] = (i < s && tx < s) ? A[(int64_t)i * lda + tx] : 0;
+    }
+    for (int e = tid; e < 64 * 65; e += 256) (&Ls[0][0])[e] = 0;
+    uint64_t active = (s == 64) ? ~0ull : ((1ull << s) - 1);
+    int r = 0, npl = 0;
+    __syncthreads();
+    for (int p1 = 0; p1 < s; ++p1) {
+        if (!((active >> p1) & 1)) continue;  // consumed as a 2x2 partner (uniform)
+        if (tx == p1) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) col1[ty + 4 * q] = S[q];
+        }
+        __syncthreads();
+        if (tid < 32) {
+            const uint32_t b0 = __ballot_sync(0xffffffffu, col1[tid] != 0);
+            const uint32_t b1 = __ballot_sync(0xffffffffu, col1[tid + 32] != 0);
+            if (tid == 0) {
+                const uint64_t m = (((uint64_t)b1 << 32) | b0) & active;
+                jsel = m ? __ffsll((long long)m) - 1 : s;
+            }
+        }
+        __syncthreads();
+        const int j = jsel;
+        if (j >= s) {  // zero residual column: pivotless (sytrf.cpp:82-85)
+            if (tid == 0) out[1 + (s - 1 - npl)] = p1;
+            ++npl;
+            active &= ~(1ull << p1);
+            continue;  // col1/jsel are rewritten only after the next barrier
+        }
+        if (j == p1) {  // 1x1 pivot (sytrf.cpp:87-97)
+            const uint32_t x = col1[p1];
+            const uint32_t xi = finv(f, x);
+            if (tid < 64) {
+                const int i = tid;
+                uint32_t l = 0;
+                if (((active >> i) & 1) && i != p1) {
+                    l = ar.mul(col1[i], xi);
+                    Ls[i][r] = l;
+                }
+                l1v[i] = l;
+            }
+            if (tid == 0) {
+                Ls[p1][r] = one;
+                D.kind[coff + r] = D_SCALAR;
+                D.val[coff + r] = x;
+                D.val2[coff + r] = 0;
+                D.inv[coff + r] = xi;
+                order[r] = p1;
+            }
+            __syncthreads();
+            const uint32_t lk = l1v[tx];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) S[q] = ar.sub(S[q], ar.mul(col1[ty + 4 * q], lk));
+            active &= ~(1ull << p1);
+            r += 1;
+            __syncthreads();
+            continue;
+        }
+        // 2x2 antidiagonal pivot pairing p1 with p2 = j (sytrf.cpp:99-131)
+        const int p2 = j;
+        if (tx == p2) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) col2[ty + 4 * q] = S[q];
+        }
+        __syncthreads();
+        const uint32_t x = col1[p2];
+        const uint32_t xi = finv(f, x);
+        const uint32_t y = col2[p2];
+        const uint32_t y_eff = f.char2 ? y : fhalve(f, y);
+        const uint32_t yd = f.char2 ? y : 0;
+        active &= ~((1ull << p1) | (1ull << p2));
+        if (tid < 64) {
+            const int i = tid;
+            uint32_t l1 = 0, l2 = 0;
+            if ((active >> i) & 1) {
+                l2 = ar.mul(xi, col1[i]);
+                l1 = ar.mul(xi, ar.sub(col2[i], ar.mul(y_eff, l2)));
+                Ls[i][r] = l1;
+                Ls[i][r + 1] = l2;
+            }
+            l1v[i] = l1;
+            l2v[i] = l2;
+            u1v[i] = ar.mul(x, l1);
+            u2v[i] = ar.mul(x, l2);
+        }
+        if (tid == 0) {
+            const int32_t hk = yd ? D_ANTITRI_HEAD : D_ANTIDIAG_HEAD;
+            D.kind[coff + r] = hk;
+            D.kind[coff + r + 1] = hk + 1;
+            D.val[coff + r] = D.val[coff + r + 1] = x;
+            D.val2[coff + r] = D.val2[coff + r + 1] = yd;
+            D.inv[coff + r] = D.inv[coff + r + 1] = xi;
+            Ls[p1][r] = one;
+            Ls[p2][r + 1] = one;
+            Ls[p2][r] = f.char2 ? 0 : ar.mul(xi, y_eff);
+            order[r] = p1;
+            order[r + 1] = p2;
+        }
+        __syncthreads();
+        const uint32_t l1k = l1v[tx], l2k = l2v[tx];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int i = ty + 4 * q;
+            uint32_t v = ar.add(ar.mul(u1v[i], l2k), ar.mul(u2v[i], l1k));
+            if (yd) v = ar.add(v, ar.mul(ar.mul(yd, l2v[i]), l2k));
+            S[q] = ar.sub(S[q], v);
+        }
+        r += 2;
+        __syncthreads();
+    }
+    // L columns [coff, coff + r) of the leaf rows, one coalesced row write each
+    for (int e = tid; e < s * r; e += 256) {
+        const int i = e / r, c = e % r;
+        Lg[(int64_t)rows[i] * ldL + coff + c] = Ls[i][c];
+    }
+    if (tid == 0) {
+        out[0] = r;
+        for (int t = 0; t < r; ++t) out[1 + t] = order[t];
+        // pivotless rows were stored from the back: reverse into ascending order
+        for (int a = 0, b = npl - 1; a < b; ++a, --b) {
+            const int32_t tmp = out[1 + r + a];
+            out[1 + r + a] = out[1 + r + b];
+            out[1 + r + b] = tmp;
+        }
+    }
+}
+
+// Inverse of each 64 x 64 diagonal block of a unit lower triangular T:
+// row-by-row, row i of T^-1 = e_i - sum_{k<i} T[i][k] (row k of T^-1).
+template <bool kSmall>
+__global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
+                                                 int64_t n, uint32_t* Tinv) {
+    __shared__ uint32_t Ts[64][65];
+    __shared__ uint32_t X[64][65];
+    __shared__ uint64_t part[4][64];
+    const int b = blockIdx.x;
+    const int64_t i0 = (int64_t)b * 64;
+    const int nb = (int)std::min<int64_t>(64, n - i0);
+    const int tid = threadIdx.x, c = tid & 63, qd = tid >> 6;
+    for (int e = tid; e < 64 * 64; e += 256) {
+        const int i = e >> 6, k = e & 63;
+        Ts[i][k] = (i < nb && k < i) ? T[(i0 + i) * ldt + i0 + k] : 0;
+        X[i][k] = 0;
+    }
+    __syncthreads();
+    for (int i = 0; i < nb; ++i) {
+        uint64_t acc = 0;
+        for (int k = qd; k < i; k += 4) {
+            const uint64_t prod = (uint64_t)Ts[i][k] * X[k][c];
+            acc += kSmall ? prod : (uint64_t)red64(f, prod);
+        }
+        part[qd][c] = acc;
+        __syncthreads();
+        if (qd == 0) {
+            const uint64_t sum = (uint64_t)red64(f, part[0][c]) + red64(f, part[1][c]) +
+                                 red64(f, part[2][c]) + red64(f, part[3][c]);
+            const uint32_t v = red64(f, sum);
+            X[i][c] = fsub(f, (c == i) ? 1 % f.p : 0, v);
+        }
+        __syncthreads();
+    }
+    uint32_t* o = Tinv + (int64_t)b * 64 * 64;
+    for (int e = tid; e < 64 * 64; e += 256) o[e] = X[e >> 6][e & 63];
+}
+
+// B[rows, c0:c0+64] <- Tinv (nb x nb) * B[rows, c0:c0+64], in place.
+template <bool kSmall>
+__global__ void __launch_bounds__(256) k_trsm_apply64(Fp f, const uint32_t* __restrict__ Tinv,
+                                                      uint32_t* B, int64_t ldb, int nb,
+                                                      int64_t ncols) {
+    __shared__ uint32_t Ts[64][65];
+    __shared__ uint32_t Bs[64][65];
+    const int tid = threadIdx.x, c = tid & 63, rg = tid >> 6;
+    const int64_t c0 = (int64_t)blockIdx.x * 64;
+    for (int e = tid; e < 64 * 64; e += 256) {
+        const int i = e >> 6, k = e & 63;
+        Ts[i][k] = Tinv[e];
+        const int64_t col = c0 + k;
+        Bs[i][k] = (i < nb && col < ncols) ? B[(int64_t)i * ldb + col] : 0;
+    }
+    __syncthreads();
+    const int64_t col = c0 + c;
+    for (int i = rg; i < nb; i += 4) {
+        uint64_t acc = 0;
+        for (int k = 0; k <= i; ++k) {
+            const uint64_t prod = (uint64_t)Ts[i][k] * Bs[k][c];
+            acc += kSmall ? prod : (uint64_t)red64(f, prod);
+        }
+        if (col < ncols) B[(int64_t)i * ldb + col] = red64(f, acc);
+    }
+}
+
+struct TrsmScratch {
+    uint32_t* ptr = nullptr;
+    size_t cap = 0;
+};
+thread_local TrsmScratch g_tscratch;
+
+uint32_t* trsm_scratch(size_t words) {
+    if (g_tscratch.cap < words) {
+        if (g_tscratch.ptr) {
+            FFB_CUDA(cudaDeviceSynchronize());
+            FFB_CUDA(cudaFree(g_tscratch.ptr));
+        }
+        const size_t cap = std::max(words * 2, (size_t)1 << 20);
+        FFB_CUDA(cudaMalloc(&g_tscratch.ptr, cap * sizeof(uint32_t)));
+        g_tscratch.cap = cap;
+    }
+    return g_tscratch.ptr;
+}
+
+void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tinv, int64_t i0) {
+    const int64_t n = T.rows;
+    if (n <= 64) {
+        ProfScope ps(K_TRSM, st, 2.0 * n * n * B.cols / 2, 8.0 * n * B.cols);
+        const uint32_t* ti = Tinv + (i0 / 64) * 64 * 64;
+        dim3 grid((unsigned)cdiv(B.cols, 64));
+        if (f.p < (1u << 16) || f.p < (1u << 23))
+            k_trsm_apply64<true><<<grid, 256, 0, st>>>(f, ti, B.ptr, B.ld, (int)n, B.cols);
+        else
+            k_trsm_apply64<false><<<grid, 256, 0, st>>>(f, ti, B.ptr, B.ld, (int)n, B.cols);
+        ++g_launches;
+        FFB_CHECK_LAUNCH();
+        return;
+    }
+    int64_t n1 = (n / 2) / 64 * 64;
+    if (n1 < 64) n1 = 64;
+    const int64_t n2 = n - n1;
+    DMat B1 = B.sub(0, 0, n1, B.cols), B2 = B.sub(n1, 0, n2, B.cols);
+    solve_rec(f, st, T.sub(0, 0, n1, n1), B1, Tinv, i0);
+    gemm(f, st, GEMM_SUB, B2, T.sub(n1, 0, n2, n1), false, B1, false, n2, B.cols, n1);
+    solve_rec(f, st, T.sub(n1, n1, n2, n2), B2, Tinv, i0 + n1);
+}
+
+}  // namespace
+
+bool leaf64_supported(int64_t s) { return s <= 64; }
+
+void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
+            DDiag D, int32_t* out) {
+    const int s = (int)A.rows;
+    ProfScope ps(K_LEAF, st, 2.0 * s * s * s / 3.0, 4.0 * s * s);
+    if (f.p < (1u << 16))
+        k_leaf64<true><<<1, 256, 0, st>>>(f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out);
+    else
+        k_leaf64<false><<<1, 256, 0, st>>>(f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out);
+    ++g_launches;
+    FFB_CHECK_LAUNCH();
+}
+
+void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
+    const int64_t n = T.rows;
+    if (n <= 0 || B.cols <= 0) return;
+    const int64_t nblk = cdiv(n, 64);
+    uint32_t* Tinv = trsm_scratch((size_t)nblk * 64 * 64);
+    {
+        ProfScope ps(K_TRSM, st, (double)n * 64 * 64 / 3, 8.0 * n * 64);
+        if (f.p < (1u << 23))
+            k_trinv64<true><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+        else
+            k_trinv64<false><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+        ++g_launches;
+        FFB_CHECK_LAUNCH();
+    }
+    solve_rec(f, st, T, B, Tinv, 0);
+}
+
+}  // namespace ffb

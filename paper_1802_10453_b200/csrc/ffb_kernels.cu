@@ -4,6 +4,8 @@
 // (Alg. 4), PLDUQ (row-order Crout with leftmost pivots), the small
 // triangular solves, and the generic modular GEMM used for every
 // contraction that the tcgen05 path (ffb_tc_gemm.cu) does not take.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "ffb_kernels.cuh"
@@ -171,70 +173,6 @@ void gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, 
     else if (ta && !tb) launch_gemm_simt<true, false>(f, st, mode, C, A, B, M, N, K);
     else if (!ta && tb) launch_gemm_simt<false, true>(f, st, mode, C, A, B, M, N, K);
     else launch_gemm_simt<true, true>(f, st, mode, C, A, B, M, N, K);
-}
-
-// ===========================================================================
-// Triangular solve with a unit lower triangular matrix.
-// Base: n <= 64, one thread per right-hand-side column, T and the column
-// slices staged in shared memory.  Larger n: recursive halving with GEMM.
-// ===========================================================================
-namespace {
-
-constexpr int TRSM_NB = 64;
-constexpr int TRSM_THREADS = 64;
-
-template <bool kLargeP>
-__global__ void __launch_bounds__(TRSM_THREADS) k_trsm_base(Fp f, const uint32_t* __restrict__ T,
-                                                            int64_t ldt, uint32_t* B, int64_t ldb,
-                                                            int n, int64_t ncols) {
-    __shared__ uint32_t Ts[TRSM_NB][TRSM_NB + 1];
-    __shared__ uint32_t Xs[TRSM_NB][TRSM_THREADS];
-    for (int e = threadIdx.x; e < n * n; e += TRSM_THREADS) {
-        const int i = e / n, k = e % n;
-        Ts[i][k] = (k < i) ? T[i * ldt + k] : 0;
-    }
-    const int64_t j = (int64_t)blockIdx.x * TRSM_THREADS + threadIdx.x;
-    const bool live = j < ncols;
-    if (live)
-        for (int i = 0; i < n; ++i) Xs[i][threadIdx.x] = B[i * ldb + j];
-    __syncthreads();
-    if (!live) return;
-    for (int i = 1; i < n; ++i) {
-        uint64_t acc = 0;
-        for (int k = 0; k < i; ++k) {
-            const uint64_t prod = (uint64_t)Ts[i][k] * Xs[k][threadIdx.x];
-            acc += kLargeP ? (uint64_t)red64(f, prod) : prod;
-        }
-        Xs[i][threadIdx.x] = fsub(f, Xs[i][threadIdx.x], red64(f, acc));
-    }
-    for (int i = 0; i < n; ++i) B[i * ldb + j] = Xs[i][threadIdx.x];
-}
-
-}  // namespace
-
-void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
-    const int64_t n = T.rows;
-    if (n <= 0 || B.cols <= 0) return;
-    if (n <= TRSM_NB) {
-        dim3 grid((unsigned)cdiv(B.cols, TRSM_THREADS));
-        ProfScope ps(K_TRSM, st, (double)n * n * B.cols, 4.0 * (n * n + 2 * n * B.cols));
-        if (f.p < (1u << 23))
-            k_trsm_base<false><<<grid, TRSM_THREADS, 0, st>>>(f, T.ptr, T.ld, B.ptr, B.ld, (int)n,
-                                                              B.cols);
-        else
-            k_trsm_base<true><<<grid, TRSM_THREADS, 0, st>>>(f, T.ptr, T.ld, B.ptr, B.ld, (int)n,
-                                                             B.cols);
-        count_launch();
-        FFB_CHECK_LAUNCH();
-        return;
-    }
-    int64_t n1 = (n / 2) / TRSM_NB * TRSM_NB;
-    if (n1 < TRSM_NB) n1 = TRSM_NB;
-    const int64_t n2 = n - n1;
-    DMat B1 = B.sub(0, 0, n1, B.cols), B2 = B.sub(n1, 0, n2, B.cols);
-    trsm_lower_unit(f, st, T.sub(0, 0, n1, n1), B1);
-    gemm(f, st, GEMM_SUB, B2, T.sub(n1, 0, n2, n1), false, B1, false, n2, B.cols, n1);
-    trsm_lower_unit(f, st, T.sub(n1, n1, n2, n2), B2);
 }
 
 // ===========================================================================
@@ -852,6 +790,11 @@ size_t leaf_scratch_words(int64_t s) { return (size_t)s * s + 5 * (size_t)s + 8;
 void leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
                 DDiag D, int32_t* out, uint32_t* scratch) {
     const int s = (int)A.rows;
+    static const bool generic_only = getenv("FFB_GENERIC_LEAF") != nullptr;  // test hook
+    if (!generic_only && leaf64_supported(s)) {
+        leaf64(f, st, A, rows, Lg, coff, D, out);
+        return;
+    }
     const bool smem = s <= LEAF_SMEM_MAX_S;
     size_t bytes = smem ? leaf_scratch_words(s) * sizeof(uint32_t) : 0;
     if (smem && bytes > 48 * 1024) {

@@ -98,6 +98,10 @@ void gather_lower_out(cudaStream_t st, DMat out, DMat Lg, const int32_t* perm);
 void leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg,
                 int64_t coff, DDiag D, int32_t* out, uint32_t* scratch);
 size_t leaf_scratch_words(int64_t s);
+// Register-resident leaf for s <= 64 (ffb_fast.cu).
+bool leaf64_supported(int64_t s);
+void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
+            DDiag D, int32_t* out);
 
 // PLDUQ (plduq.cpp:36-123) of W (m x n, destroyed).  Outputs: info[0] = r,
 // info[1..m] row_image, info[1+m..1+m+n] col_image, pc[r] in info after that;
