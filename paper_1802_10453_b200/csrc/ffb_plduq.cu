@@ -88,6 +88,7 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
     uint32_t* E = sm;                            // RD_MAX_B x s basis rows
     uint32_t* v = E + (size_t)RD_MAX_B * s;      // current row (s)
     __shared__ int rho[RD_MAX_B];
+    __shared__ uint32_t coef[RD_MAX_B];
     __shared__ int kcount, firstnz;
     __shared__ uint32_t inv_lead;
     const int tid = threadIdx.x;
@@ -118,10 +119,13 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
         const uint32_t il = inv_lead;
         for (int j = tid; j < s; j += blockDim.x) v[j] = fmul(f, v[j], il);
         __syncthreads();
-        // eliminate column rh from the existing basis rows, append v
+        // eliminate column rh from the existing basis rows (coefficients are
+        // snapshotted first: the update itself zeroes column rh), append v
+        for (int t = tid; t < k; t += blockDim.x) coef[t] = E[(size_t)t * s + rh];
+        __syncthreads();
         for (int e = tid; e < k * s; e += blockDim.x) {
             const int t = e / s, j = e % s;
-            const uint32_t c = E[(size_t)t * s + rh];
+            const uint32_t c = coef[t];
             if (c) E[(size_t)t * s + j] = fsub(f, E[(size_t)t * s + j], fmul(f, c, v[j]));
         }
         __syncthreads();
@@ -161,6 +165,7 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
     __shared__ int nzmask[CRP_G];
     __shared__ int total, lead;
     __shared__ uint32_t vr[CRP_KMAX];
+    __shared__ uint32_t coefs[CRP_KMAX];
     __shared__ uint32_t il;
     const int tid = threadIdx.x;
     const int g = blockIdx.x;
@@ -233,9 +238,11 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
                 __syncthreads();
                 for (int i = tid; i < k; i += blockDim.x) vr[i] = fmul(f, vr[i], il);
                 __syncthreads();
+                for (int t = tid; t < kb2; t += blockDim.x) coefs[t] = E[(size_t)t * k + ld];
+                __syncthreads();
                 for (int e = tid; e < kb2 * k; e += blockDim.x) {
                     const int t = e / k, i = e % k;
-                    const uint32_t cc = E[(size_t)t * k + ld];
+                    const uint32_t cc = coefs[t];
                     if (cc) E[(size_t)t * k + i] = fsub(f, E[(size_t)t * k + i], fmul(f, cc, vr[i]));
                 }
                 __syncthreads();
