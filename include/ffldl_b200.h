@@ -143,6 +143,14 @@ int ffb_syrdk_sub(ffb_context* ctx, uint64_t p, size_t n, size_t k, uint64_t* c,
 int ffb_syr2k_sub(ffb_context* ctx, uint64_t p, size_t n, size_t k, uint64_t* c,
                   const uint64_t* a, const uint64_t* b);
 
+/* Device-buffer modular GEMM (the engine's contraction kernel, kernels.hpp:13 semantics):
+ * C (m x n) = C - op(A) op(B) (mode 0), C + op(A) op(B) (mode 1), op(A) op(B) (mode 2);
+ * op(A) = A (m x k) or A^T when ta (A stored k x m); op(B) = B (k x n) or B^T when tb.
+ * uint32 residues, row strides ldc/lda/ldb, on the context stream (asynchronous). */
+int ffb_gemm_device(ffb_context* ctx, uint64_t p, int mode, size_t m, size_t n, size_t k,
+                    uint32_t* d_c, size_t ldc, const uint32_t* d_a, size_t lda, int ta,
+                    const uint32_t* d_b, size_t ldb, int tb);
+
 /* Seeded counter-based generators of the benchmark configurations
  * (BASELINE.json configs 1..5).  Host version
  * writes uint64 residues; device version writes uint32 residues (row stride n).

@@ -20,7 +20,7 @@ EXPORTS = [
     "ffb_stream", "ffb_launch_count", "ffb_sync_count", "ffb_profile_enable", "ffb_profile_read",
     "ffb_ldlt", "ffb_ldlt_compact", "ffb_ldlt_zero_leading",
     "ffb_ldlt_device", "ffb_plduq", "ffb_trssyr2k", "ffb_gemm_sub", "ffb_trmm_sub",
-    "ffb_trsm_inplace", "ffb_syrdk_sub", "ffb_syr2k_sub", "ffb_generate_host",
+    "ffb_trsm_inplace", "ffb_syrdk_sub", "ffb_syr2k_sub", "ffb_gemm_device", "ffb_generate_host",
     "ffb_generate_device", "ffb_config5_partners",
 ]
 
@@ -52,6 +52,7 @@ _SIGS = {
     "ffb_trsm_inplace": (I, [P, U64, SZ, SZ, P, I, I, I, P]),
     "ffb_syrdk_sub": (I, [P, U64, SZ, SZ, P, P, P, P, P]),
     "ffb_syr2k_sub": (I, [P, U64, SZ, SZ, P, P, P]),
+    "ffb_gemm_device": (I, [P, U64, I, SZ, SZ, SZ, P, SZ, P, SZ, I, P, SZ, I]),
     "ffb_generate_host": (I, [I, SZ, SZ, U64, U64, P]),
     "ffb_generate_device": (I, [P, I, SZ, SZ, U64, U64, P]),
     "ffb_config5_partners": (I, [SZ, SZ, U64, P]),

@@ -837,6 +837,24 @@ int ffb_trssyr2k(ffb_context* c, uint64_t p, size_t n, const uint64_t* u, const 
     });
 }
 
+int ffb_gemm_device(ffb_context* c, uint64_t p, int mode, size_t m, size_t n, size_t k,
+                    uint32_t* d_c, size_t ldc, const uint32_t* d_a, size_t lda, int ta,
+                    const uint32_t* d_b, size_t ldb, int tb) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        if (mode < 0 || mode > 2) throw Status(FFB_ERROR, "gemm: bad mode");
+        Fp f = make_field(c, p);
+        DMat C, A, B;
+        C.ptr = d_c; C.ld = (int64_t)ldc; C.rows = (int64_t)m; C.cols = (int64_t)n;
+        A.ptr = (uint32_t*)d_a; A.ld = (int64_t)lda; A.rows = ta ? (int64_t)k : (int64_t)m;
+        A.cols = ta ? (int64_t)m : (int64_t)k;
+        B.ptr = (uint32_t*)d_b; B.ld = (int64_t)ldb; B.rows = tb ? (int64_t)n : (int64_t)k;
+        B.cols = tb ? (int64_t)k : (int64_t)n;
+        gemm(f, c->stream, (GemmMode)mode, C, A, ta != 0, B, tb != 0, (int64_t)m, (int64_t)n,
+             (int64_t)k);
+    });
+}
+
 // ---- kernels.hpp:13-32 --------------------------------------------------------
 int ffb_gemm_sub(ffb_context* c, uint64_t p, size_t m, size_t n, size_t k, uint64_t* cc,
                  const uint64_t* a, const uint64_t* b) {
