@@ -194,26 +194,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // ---- epilogue: warps 2..5 own TMEM lanes 32*(warp%4) .. +31 ----
         const int q = warp & 3;
         uint32_t* tile = sEpi + (warp - 2) * 32 * 33;
+        // acc in (-2^31, 2^31): (acc + 2^31) mod p by 32-bit Barrett, minus 2^31 mod p
+        const Fp16 h(f.p);
+        const uint32_t bias = (uint32_t)((0x80000000ull) % f.p);
         mbar_wait(accfull, 0);
         tc_fence_after();
-        const uint64_t off = (uint64_t)f.p * ((0x80000000ull + f.p - 1) / f.p);  // multiple of p >= 2^31
+        const int rbase = m0 + 32 * q;
         for (int c = 0; c < BN; c += 32) {
             if (n0 + c >= N) break;
             uint32_t r[32];
             tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c, r);
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-                tile[lane * 33 + j] = red64(f, (uint64_t)((int64_t)(int32_t)r[j] + (int64_t)off));
+            for (int j = 0; j < 32; ++j) {
+                const uint32_t x = r[j] ^ 0x80000000u;  // = acc + 2^31 as unsigned
+                tile[lane * 33 + j] = h.sub(h.red(x), bias);
+            }
             __syncwarp();
             const int col = n0 + c + lane;
+            const bool colok = col < N;
+            uint32_t cv[32];
+            if (mode != GEMM_SET) {
+#pragma unroll
+                for (int rr = 0; rr < 32; ++rr) {
+                    const int row = rbase + rr;
+                    cv[rr] = (colok && row < M) ? __ldg(C + (int64_t)row * ldc + col) : 0u;
+                }
+            }
+#pragma unroll
             for (int rr = 0; rr < 32; ++rr) {
-                const int row = m0 + 32 * q + rr;
-                if (row < M && col < N) {
+                const int row = rbase + rr;
+                if (colok && row < M) {
                     const uint32_t v = tile[rr * 33 + lane];
-                    uint32_t* cp = C + (int64_t)row * ldc + col;
-                    if (mode == GEMM_SUB) *cp = fsub(f, *cp, v);
-                    else if (mode == GEMM_ADD) *cp = fadd(f, *cp, v);
-                    else *cp = v;
+                    uint32_t o;
+                    if (mode == GEMM_SUB) o = h.sub(cv[rr], v);
+                    else if (mode == GEMM_ADD) o = fadd(f, cv[rr], v);
+                    else o = v;
+                    C[(int64_t)row * ldc + col] = o;
                 }
             }
             __syncwarp();
