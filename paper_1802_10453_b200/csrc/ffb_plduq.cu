@@ -5,24 +5,27 @@
 // is unique: the pivots are the rank profile matrix (RPM) of Y, row_perm =
 // pivot rows ascending then the rest ascending, col_perm = pivot columns in
 // pivot order then the rest ascending, and [L1;M1], d, [U1 V1] are then
-// determined (plduq.hpp:24-40).  This file computes the same thing in two
-// phases:
+// determined (plduq.hpp:24-40).  Two phases:
 //
-//  1. Pivot search (the RPM), in row chunks of B rows:
-//       R   = Y_c - Y_c[:, pc] * Uhat         residual against earlier pivots (GEMM)
-//       S   = R * Omega                        random sketch, Omega n x (B+16)
-//       I   = rows of S independent of the earlier rows of S   (1 CTA, tiny)
-//       J   = column rank profile of R[I, :]   (parallel local scan + merge)
-//       pairing = RPM of the k x k block R[I, J]  (1 CTA, tiny)
-//     Rows of S independent => rows of R independent; the converse holds
-//     unless Omega is degenerate on the row space of R, which the exact check
-//     R - R[:, J] * (R[I,J]^-1 R[I,:]) == 0 rules out; on failure the chunk
-//     is redone by the sequential kernel, so the result is always exact.
-//     Uhat (rows fully reduced at their pivot columns) absorbs each chunk's
-//     new rows by one GEMM.
-//  2. Factors from the pivots: K = Y[pr, pc] = L1 D U1 (LDU without pivoting,
-//     leading minors are the Crout pivots), U = D^-1 L1^-1 Y[pr, Q] and
-//     M1 = Y[np, pc] U1^-1 D^-1 (TRSM + scaling).
+//  1. Pivot search (the RPM) in row chunks of B rows, against a basis Uhat of
+//     the pivot rows found so far (each row 1 at its own pivot column, 0 at
+//     the others):
+//       S   = (Y Omega)_c - Y_c[:, pc] (Uhat Omega)   sketch of the chunk residual
+//       I   = rows of S independent of the earlier rows of S      (1 CTA)
+//       R_I = Y_I - Y_I[:, pc] Uhat                   exact residual of those rows
+//       J   = column rank profile of R_I              (reduction tree of local CRPs)
+//       pairing = RPM of R_I[:, J]; Unew = R_I[:,J]^-1 R_I joins Uhat (GEMMs)
+//     Y Omega is computed once; Uhat Omega is maintained alongside Uhat.
+//  2. Factors from the pivots: K = Y[pr, pc] = L1 D U1 (LDU without pivoting),
+//     U = D^-1 L1^-1 Y[pr, Q], M1 = Y[np, pc] U1^-1 D^-1.
+//
+// Exactness (Las Vegas): a sketch can only MISS rank (rows of S independent
+// => rows of R independent).  A miss makes the result either fail to
+// reproduce Y or contain a pivotless row that depends on a LATER pivot row,
+// so the certificate  P [L1;M1] D [U1 V1] Q^T == Y  and  M1(t,k) == 0 for
+// pr_k > t  (plus nonzero LDU pivots) accepts exactly the reference's output.
+// On rejection (probability ~ p^-16 per chunk) the search is redone with the
+// exact row-sequential kernel.
 #include <stdlib.h>
 
 #include <algorithm>
@@ -37,24 +40,16 @@ namespace {
 
 inline void count_launch() { ++g_launches; }
 
-// dst[a][b] = src[ridx ? ridx[a] : a][cidx[b]]
+// dst[a][b] = src[roff + (ridx ? ridx[a] : a)][cidx[b]]
 __global__ void k_gather2d(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
-                           const int32_t* ridx, const int32_t* cidx, int64_t cols) {
+                           const int32_t* ridx, int64_t roff, const int32_t* cidx, int64_t cols) {
     const int64_t a = blockIdx.y;
-    const int64_t sr = ridx ? ridx[a] : a;
+    const int64_t sr = roff + (ridx ? ridx[a] : a);
     const uint32_t* s = src + sr * lds;
     uint32_t* d = dst + a * ldd;
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < cols;
          b += (int64_t)gridDim.x * blockDim.x)
         d[b] = s[cidx[b]];
-}
-
-__global__ void k_copy_rows(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
-                            int64_t cols) {
-    const int64_t a = blockIdx.y;
-    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < cols;
-         b += (int64_t)gridDim.x * blockDim.x)
-        dst[a * ldd + b] = src[a * lds + b];
 }
 
 __global__ void k_random(uint32_t* out, int64_t n, uint64_t seed, uint32_t p) {
@@ -75,52 +70,52 @@ inline dim3 rgrid(int64_t rows, int64_t cols) {
 }
 
 // ---------------------------------------------------------------------------
-// Row detection on the sketch S (b x s, b <= 128, s <= 160), one CTA.
-// Fully reduced basis: E_t with pivot column rho_t (E_t[rho_t] = 1, other
-// basis rows 0 there).  Row i is independent iff its reduction is nonzero.
+// Row detection on the sketch S (b x s, b <= 128, s <= 160), one CTA, S in
+// shared memory.  Fully reduced basis E_t with pivot position rho_t.  A
+// dependent row costs one barrier (__syncthreads_or); an independent row is
+// normalised and eliminated from the basis.  The pivot position of a basis
+// vector is arbitrary (any nonzero entry), only independence matters.
 // out: out[0] = k, out[1..k] = independent rows (ascending).
 // ---------------------------------------------------------------------------
-constexpr int RD_MAX_B = 128;
+constexpr int RD_MAX_B = 128, RD_S = 144;
 
 __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int64_t lds, int b,
                                                     int s, int32_t* out) {
     extern __shared__ uint32_t sm[];
-    uint32_t* E = sm;                            // RD_MAX_B x s basis rows
-    uint32_t* v = E + (size_t)RD_MAX_B * s;      // current row (s)
+    uint32_t* Ss = sm;                          // b x s
+    uint32_t* E = Ss + (size_t)RD_MAX_B * s;    // basis rows
+    uint32_t* v = E + (size_t)RD_MAX_B * s;     // current row
     __shared__ int rho[RD_MAX_B];
     __shared__ uint32_t coef[RD_MAX_B];
-    __shared__ int kcount, firstnz;
-    __shared__ uint32_t inv_lead;
+    __shared__ int rhs;
+    __shared__ uint32_t ils;
     const int tid = threadIdx.x;
-    if (tid == 0) kcount = 0;
+    for (int e = tid; e < b * s; e += blockDim.x) Ss[e] = S[(int64_t)(e / s) * lds + e % s];
+    if (tid == 0) rhs = s;
     __syncthreads();
+    int k = 0;
     for (int i = 0; i < b; ++i) {
-        const int k = kcount;
-        // v = S_i - sum_t S_i[rho_t] E_t
+        const uint32_t* si = Ss + (size_t)i * s;
+        int nz = 0;
         for (int j = tid; j < s; j += blockDim.x) {
             uint64_t acc = 0;
-            const uint32_t* si = S + (int64_t)i * lds;
             for (int t = 0; t < k; ++t) {
                 acc += (uint64_t)si[rho[t]] * E[(size_t)t * s + j];
                 if ((t & 15) == 15 && f.p >= (1u << 26)) acc = red64(f, acc);
             }
-            v[j] = fsub(f, si[j], red64(f, acc));
+            const uint32_t x = fsub(f, si[j], red64(f, acc));
+            v[j] = x;
+            nz |= x != 0;
         }
-        if (tid == 0) firstnz = s;
-        __syncthreads();
+        if (!__syncthreads_or(nz)) continue;  // dependent row (uniform)
         for (int j = tid; j < s; j += blockDim.x)
-            if (v[j] != 0) atomicMin(&firstnz, j);
+            if (v[j]) atomicMin(&rhs, j);
         __syncthreads();
-        const int rh = firstnz;
-        __syncthreads();  // everyone has read firstnz before it is reset
-        if (rh == s) continue;  // dependent row (uniform)
-        if (tid == 0) inv_lead = finv(f, v[rh]);
+        const int rh = rhs;
+        if (tid == 0) ils = finv(f, v[rh]);
         __syncthreads();
-        const uint32_t il = inv_lead;
+        const uint32_t il = ils;
         for (int j = tid; j < s; j += blockDim.x) v[j] = fmul(f, v[j], il);
-        __syncthreads();
-        // eliminate column rh from the existing basis rows (coefficients are
-        // snapshotted first: the update itself zeroes column rh), append v
         for (int t = tid; t < k; t += blockDim.x) coef[t] = E[(size_t)t * s + rh];
         __syncthreads();
         for (int e = tid; e < k * s; e += blockDim.x) {
@@ -128,16 +123,38 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
             const uint32_t c = coef[t];
             if (c) E[(size_t)t * s + j] = fsub(f, E[(size_t)t * s + j], fmul(f, c, v[j]));
         }
-        __syncthreads();
         for (int j = tid; j < s; j += blockDim.x) E[(size_t)k * s + j] = v[j];
         if (tid == 0) {
             rho[k] = rh;
             out[1 + k] = i;
-            kcount = k + 1;
+            rhs = s;
         }
         __syncthreads();
+        ++k;
     }
-    if (tid == 0) out[0] = kcount;
+    if (tid == 0) out[0] = k;
+}
+
+// Sketch of the chunk residual: S[i][t] = YO[c0+i][t] - sum_j Y[c0+i][uc[j]] UO[j][t].
+__global__ void __launch_bounds__(160) k_sketch_chunk(Fp f, uint32_t* S, int64_t lds,
+                                                     const uint32_t* YO, int64_t ldyo,
+                                                     const uint32_t* Y, int64_t ldy,
+                                                     const uint32_t* UO, int64_t lduo,
+                                                     const int32_t* uc, int64_t r, int64_t c0,
+                                                     int s) {
+    extern __shared__ uint32_t g[];  // r gathered entries of row c0+i
+    const int64_t i = blockIdx.x;
+    const uint32_t* yrow = Y + (c0 + i) * ldy;
+    for (int64_t j = threadIdx.x; j < r; j += blockDim.x) g[j] = yrow[uc[j]];
+    __syncthreads();
+    const int t = threadIdx.x;
+    if (t >= s) return;
+    uint64_t acc = 0;
+    for (int64_t j = 0; j < r; ++j) {
+        acc += (uint64_t)g[j] * UO[j * lduo + t];
+        if (f.p >= (1u << 23) || (j & 0x3FFF) == 0x3FFF) acc = red64(f, acc);
+    }
+    S[i * lds + t] = fsub(f, YO[(c0 + i) * ldyo + t], red64(f, acc));
 }
 
 // ---------------------------------------------------------------------------
@@ -163,10 +180,9 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
     __shared__ int colid[CRP_G];
     __shared__ int nb;
     __shared__ int nzmask[CRP_G];
-    __shared__ int total, lead;
+    __shared__ int total;
     __shared__ uint32_t vr[CRP_KMAX];
     __shared__ uint32_t coefs[CRP_KMAX];
-    __shared__ uint32_t il;
     const int tid = threadIdx.x;
     const int g = blockIdx.x;
     // the ordered column set of this CTA
@@ -215,89 +231,83 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
             if (fsub(f, V[(size_t)c * k + i], red64(f, acc)) != 0) atomicOr(&nzmask[c], 1);
         }
         __syncthreads();
-        // flagged columns in order: exact reduction against the current basis
-        for (int c = 0; c < gw; ++c) {
-            if (!nzmask[c]) continue;  // uniform (shared)
-            const int kb2 = nb;
-            for (int i = tid; i < k; i += blockDim.x) {
-                uint64_t acc = 0;
-                for (int t = 0; t < kb2; ++t) {
-                    acc += (uint64_t)V[(size_t)c * k + rho[t]] * E[(size_t)t * k + i];
-                    if ((t & 15) == 15 && f.p >= (1u << 26)) acc = red64(f, acc);
+        // flagged columns in order, by warp 0 alone (warp-synchronous, no block
+        // barriers): exact reduction against the current basis, then either
+        // dependent or a new basis vector (normalised, eliminated from the rest).
+        if (tid < 32) {
+            const int lane = tid;
+            int nbl = nb;
+            for (int c = 0; c < gw && nbl < k; ++c) {
+                if (!nzmask[c]) continue;
+                int lead_l = k;
+                for (int i = lane; i < k; i += 32) {
+                    uint64_t acc = 0;
+                    for (int t = 0; t < nbl; ++t) {
+                        acc += (uint64_t)V[(size_t)c * k + rho[t]] * E[(size_t)t * k + i];
+                        if ((t & 15) == 15 && f.p >= (1u << 26)) acc = red64(f, acc);
+                    }
+                    const uint32_t x = fsub(f, V[(size_t)c * k + i], red64(f, acc));
+                    vr[i] = x;
+                    if (x && i < lead_l) lead_l = i;
                 }
-                vr[i] = fsub(f, V[(size_t)c * k + i], red64(f, acc));
-            }
-            if (tid == 0) lead = k;
-            __syncthreads();
-            for (int i = tid; i < k; i += blockDim.x)
-                if (vr[i]) atomicMin(&lead, i);
-            __syncthreads();
-            const int ld = lead;
-            if (ld < k) {
-                if (tid == 0) il = finv(f, vr[ld]);
-                __syncthreads();
-                for (int i = tid; i < k; i += blockDim.x) vr[i] = fmul(f, vr[i], il);
-                __syncthreads();
-                for (int t = tid; t < kb2; t += blockDim.x) coefs[t] = E[(size_t)t * k + ld];
-                __syncthreads();
-                for (int e = tid; e < kb2 * k; e += blockDim.x) {
+                for (int off = 16; off; off >>= 1) lead_l = min(lead_l, __shfl_xor_sync(0xffffffffu, lead_l, off));
+                __syncwarp();
+                if (lead_l >= k) continue;
+                const int ld = lead_l;
+                const uint32_t ilv = finv(f, vr[ld]);
+                for (int i = lane; i < k; i += 32) vr[i] = fmul(f, vr[i], ilv);
+                for (int t = lane; t < nbl; t += 32) coefs[t] = E[(size_t)t * k + ld];
+                __syncwarp();
+                for (int e = lane; e < nbl * k; e += 32) {
                     const int t = e / k, i = e % k;
                     const uint32_t cc = coefs[t];
                     if (cc) E[(size_t)t * k + i] = fsub(f, E[(size_t)t * k + i], fmul(f, cc, vr[i]));
                 }
-                __syncthreads();
-                for (int i = tid; i < k; i += blockDim.x) E[(size_t)kb2 * k + i] = vr[i];
-                if (tid == 0) {
-                    rho[kb2] = ld;
-                    out[(int64_t)g * k + kb2] = colid[c];
-                    nb = kb2 + 1;
+                for (int i = lane; i < k; i += 32) E[(size_t)nbl * k + i] = vr[i];
+                if (lane == 0) {
+                    rho[nbl] = ld;
+                    out[(int64_t)g * k + nbl] = colid[c];
                 }
+                __syncwarp();
+                ++nbl;
             }
-            __syncthreads();
-            if (nb >= k) break;
+            if (lane == 0) nb = nbl;
         }
         __syncthreads();
     }
     if (tid == 0) ocount[g] = nb;
 }
 
-// Append a chunk's pivots to the device bookkeeping: Uhat row order J,
-// pivot rows c0 + I[t] with columns J[sigma[t]].
-__global__ void k_append_pivots(int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r,
-                                int64_t c0, const int32_t* I, const int32_t* J,
-                                const int32_t* sigma, int k) {
-    for (int t = threadIdx.x; t < k; t += blockDim.x) {
-        uhat_col[r + t] = J[t];
-        prow[r + t] = (int32_t)(c0 + I[t]);
-        pcol[r + t] = J[sigma[t]];
-    }
-}
-
 // ---------------------------------------------------------------------------
-// Pairing + inverse (1 CTA): Kc = RI[:, J] (k x k, nonsingular).  Row-order
-// leftmost elimination gives sigma (row t -> column sigma[t] of Kc); Gauss-
-// Jordan gives Kinv.  out: sigma[k]; Kinv (k x k).
+// Pairing + inverse + bookkeeping (1 CTA).  Kc = RI[:, J] (k x k, nonsingular).
+// Row-order leftmost elimination on Kc gives the RPM pairing sigma (the
+// reference's Crout rule restricted to Kc); Gauss-Jordan gives Kinv.  Then:
+//   Kinv -> global (for Unew = Kinv RI), UO[r+i] = (Kinv S[I,:])[i] when
+//   sketching, uhat_col[r+t] = J[t], prow[r+t] = c0+I[t], pcol[r+t] = J[sigma t].
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_pair(Fp f, const uint32_t* Kc, int64_t ldk, int k,
-                                              int32_t* sigma, uint32_t* Kinv, int64_t ldi,
-                                              int32_t* fail) {
+__global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t ldr, int k,
+                                               const int32_t* J, const int32_t* I, int64_t c0,
+                                               const uint32_t* S, int64_t lds, int s,
+                                               uint32_t* Kinv, uint32_t* UO, int64_t lduo,
+                                               int32_t* uhat_col, int32_t* prow, int32_t* pcol,
+                                               int64_t r, int32_t* fail) {
     extern __shared__ uint32_t sm[];
     uint32_t* A = sm;                       // k x k working copy (row-order elimination)
     uint32_t* G = A + (size_t)k * k;        // k x 2k Gauss-Jordan
     __shared__ int colused[CRP_KMAX];
+    __shared__ int sig[CRP_KMAX];
     __shared__ int lead;
     __shared__ uint32_t il;
     const int tid = threadIdx.x;
     for (int e = tid; e < k * k; e += blockDim.x) {
         const int i = e / k, j = e % k;
-        const uint32_t v = Kc[(int64_t)i * ldk + j];
+        const uint32_t v = RI[(int64_t)i * ldr + J[j]];
         A[e] = v;
         G[(size_t)i * 2 * k + j] = v;
         G[(size_t)i * 2 * k + k + j] = (i == j) ? 1 % f.p : 0;
     }
     for (int j = tid; j < k; j += blockDim.x) colused[j] = 0;
     __syncthreads();
-    // row-order leftmost (the reference's Crout rule restricted to Kc)
     for (int t = 0; t < k; ++t) {
         if (tid == 0) lead = k;
         __syncthreads();
@@ -310,24 +320,21 @@ __global__ void __launch_bounds__(256) k_pair(Fp f, const uint32_t* Kc, int64_t 
             return;
         }
         if (tid == 0) {
-            sigma[t] = jp;
+            sig[t] = jp;
             colused[jp] = 1;
             il = finv(f, A[(size_t)t * k + jp]);
         }
         __syncthreads();
-        // eliminate column jp from the rows below t
         for (int e = tid; e < (k - t - 1) * k; e += blockDim.x) {
             const int i = t + 1 + e / k, j = e % k;
-            if (colused[j] && j != jp) continue;
+            if (colused[j]) continue;  // jp included: its column is zeroed below
             const uint32_t m = fmul(f, A[(size_t)i * k + jp], il);
-            if (j == jp) continue;
             A[(size_t)i * k + j] = fsub(f, A[(size_t)i * k + j], fmul(f, m, A[(size_t)t * k + j]));
         }
         __syncthreads();
         for (int i = t + 1 + tid; i < k; i += blockDim.x) A[(size_t)i * k + jp] = 0;
         __syncthreads();
     }
-    // Gauss-Jordan inverse (any nonzero pivot; result unique)
     const int w = 2 * k;
     for (int c = 0; c < k; ++c) {
         if (tid == 0) lead = k;
@@ -353,9 +360,9 @@ __global__ void __launch_bounds__(256) k_pair(Fp f, const uint32_t* Kc, int64_t 
         __syncthreads();
         for (int e = tid; e < k * w; e += blockDim.x) {
             const int i = e / w, j = e % w;
-            if (i == c) continue;
+            if (i == c || j == c) continue;
             const uint32_t m = G[(size_t)i * w + c];
-            if (m && j != c) G[(size_t)i * w + j] = fsub(f, G[(size_t)i * w + j], fmul(f, m, G[(size_t)c * w + j]));
+            if (m) G[(size_t)i * w + j] = fsub(f, G[(size_t)i * w + j], fmul(f, m, G[(size_t)c * w + j]));
         }
         __syncthreads();
         for (int i = tid; i < k; i += blockDim.x)
@@ -364,8 +371,45 @@ __global__ void __launch_bounds__(256) k_pair(Fp f, const uint32_t* Kc, int64_t 
     }
     for (int e = tid; e < k * k; e += blockDim.x) {
         const int i = e / k, j = e % k;
-        Kinv[(int64_t)i * ldi + j] = G[(size_t)i * w + k + j];
+        Kinv[(int64_t)i * k + j] = G[(size_t)i * w + k + j];
     }
+    if (S) {
+        for (int e = tid; e < k * s; e += blockDim.x) {
+            const int i = e / s, col = e % s;
+            uint64_t acc = 0;
+            for (int t = 0; t < k; ++t) {
+                acc += (uint64_t)G[(size_t)i * w + k + t] * S[(int64_t)I[t] * lds + col];
+                if (f.p >= (1u << 23)) acc = red64(f, acc);
+            }
+            UO[(r + i) * lduo + col] = red64(f, acc);
+        }
+    }
+    for (int t = tid; t < k; t += blockDim.x) {
+        uhat_col[r + t] = J[t];
+        prow[r + t] = (int32_t)(c0 + I[t]);
+        pcol[r + t] = J[sig[t]];
+    }
+}
+
+// H[i][t] = L[i][t] * d[t]
+__global__ void k_scale_cols(Fp f, uint32_t* H, int64_t ldh, const uint32_t* L, int64_t ldl,
+                             const uint32_t* d, int64_t cols) {
+    const int64_t i = blockIdx.y;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cols;
+         t += (int64_t)gridDim.x * blockDim.x)
+        H[i * ldh + t] = fmul(f, L[i * ldl + t], d[t]);
+}
+
+// Certificate part: pivotless row t (= np[a]) may only depend on pivots found before it.
+__global__ void k_m1_pattern(const uint32_t* M1, int64_t ldm, const int32_t* np,
+                             const int32_t* prow, int64_t r, int32_t* flag) {
+    const int64_t a = blockIdx.y;
+    const int32_t t = np[a];
+    int bad = 0;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < r;
+         k += (int64_t)gridDim.x * blockDim.x)
+        bad |= prow[k] > t && M1[a * ldm + k] != 0;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -418,13 +462,15 @@ __global__ void k_unpack_l(uint32_t* L, int64_t ldl, const uint32_t* K, int64_t 
 // Host side
 // ===========================================================================
 
-void gather2d(cudaStream_t st, DMat dst, DMat src, const int32_t* ridx, const int32_t* cidx) {
+void gather2d(cudaStream_t st, DMat dst, DMat src, const int32_t* ridx, const int32_t* cidx,
+              int64_t roff) {
     if (dst.rows <= 0 || dst.cols <= 0) return;
     ProfScope ps(K_MOVE, st, 0.0, 8.0 * dst.rows * dst.cols);
     for (int64_t r0 = 0; r0 < dst.rows; r0 += 65535) {
         const int64_t nr = std::min<int64_t>(65535, dst.rows - r0);
         k_gather2d<<<rgrid(nr, dst.cols), 256, 0, st>>>(dst.ptr + r0 * dst.ld, dst.ld, src.ptr, src.ld,
-                                                        ridx ? ridx + r0 : nullptr, cidx, dst.cols);
+                                                        ridx ? ridx + r0 : nullptr,
+                                                        ridx ? roff : roff + r0, cidx, dst.cols);
         count_launch();
     }
     FFB_CHECK_LAUNCH();
@@ -485,131 +531,138 @@ void ldu_inplace(const Fp& f, cudaStream_t st, DMat K, Workspace& ws, int32_t* f
 
 PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, const PlduqIO& io) {
     const int64_t m = Y.rows, n = Y.cols, mn = std::min(m, n);
-    const int B = 128, SK = B + 16;
+    // test hook: a narrow sketch makes misses likely, exercising the certificate
+    static const int sk_env = getenv("FFB_PLDUQ_SKETCH_COLS") ? atoi(getenv("FFB_PLDUQ_SKETCH_COLS")) : 0;
+    const int B = 128, SK = (sk_env > 0 && sk_env <= RD_S) ? sk_env : RD_S;
     PlduqOut out;
+    const size_t mark0 = ws.mark();
     DMat Uhat = ws.mat(std::max<int64_t>(mn, 1), n);
-    DMat Om = ws.mat(n, SK);
-    {
-        k_random<<<(unsigned)cdiv(n * SK, 256), 256, 0, st>>>(Om.ptr, n * SK, 0x5EEDull + n, f.p);
-        count_launch();
-    }
-    DMat R = ws.mat(B, n), S = ws.mat(B, SK), RI = ws.mat(B, n), Unew = ws.mat(B, n);
-    DMat Kc = ws.mat(B, B), Kinv = ws.mat(B, B), G = ws.mat(B, std::max<int64_t>(mn, 1));
-    DMat Gc = ws.mat(B, B), Upd = ws.mat(std::max<int64_t>(mn, 1), B);
+    DMat UO = ws.mat(std::max<int64_t>(mn, 1), SK);   // Uhat * Omega
+    DMat RI = ws.mat(B, n), S = ws.mat(B, SK);
+    DMat Kinv = ws.mat(B, B), Gi = ws.mat(B, std::max<int64_t>(mn, 1));
+    DMat Upd = ws.mat(std::max<int64_t>(mn, 1), B);
     const int nblk0 = (int)cdiv(n, CRP_W);
     int32_t* dinfo = ws.vec<int32_t>(2 * B + 16);     // row detect: k, I[0..k)
     int32_t* lists[2] = {ws.vec<int32_t>((int64_t)nblk0 * B), ws.vec<int32_t>((int64_t)nblk0 * B)};
     int32_t* counts[2] = {ws.vec<int32_t>(nblk0), ws.vec<int32_t>(nblk0)};
-    int32_t* dsig = ws.vec<int32_t>(B);
-    int32_t* dflag = ws.vec<int32_t>(4);              // sticky: any chunk failed its exact check
+    int32_t* dflag = ws.vec<int32_t>(4);
     int32_t* d_uhat_col = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
     int32_t* d_prow = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
     int32_t* d_pcol = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
+    const size_t mark1 = ws.mark();
 
-    const size_t rd_smem = ((size_t)RD_MAX_B * SK + SK) * 4;
+    const size_t rd_smem = ((size_t)2 * RD_MAX_B * SK + SK) * 4;
     const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + (size_t)CRP_G * CRP_KMAX) * 4;
     static bool attrs = false;
     if (!attrs) {
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_crp_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crp_smem));
-        FFB_CUDA(cudaFuncSetAttribute(k_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * CRP_KMAX * CRP_KMAX * 4)));
+        FFB_CUDA(cudaFuncSetAttribute(k_pair2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * CRP_KMAX * CRP_KMAX * 4)));
+        FFB_CUDA(cudaFuncSetAttribute(k_sketch_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attrs = true;
     }
     static const bool force_exact = getenv("FFB_PLDUQ_FORCE_FALLBACK") != nullptr;  // test hook
+    const bool sketch_ok = mn <= 200 * 1024 / 4;  // k_sketch_chunk keeps r entries in smem
 
-    // Residual of chunk rows [c0, c0+bc) against the r pivots found so far.
-    auto residual = [&](DMat Rc, DMat Yc, int64_t bc, int64_t r) {
-        {
-            ProfScope ps(K_MOVE, st, 0.0, 8.0 * bc * n);
-            k_copy_rows<<<rgrid(bc, n), 256, 0, st>>>(Rc.ptr, Rc.ld, Yc.ptr, Yc.ld, n);
-            count_launch();
-        }
-        if (r > 0) {
-            DMat Gv = G.sub(0, 0, bc, r);
-            gather2d(st, Gv, Yc, nullptr, d_uhat_col);
-            gemm(f, st, GEMM_SUB, Rc, Gv, false, Uhat.sub(0, 0, r, n), false, bc, n, r);
-        }
-    };
-    // Given the chunk's pivot rows (device dI, k of them) and pivot column set
-    // (device dJ, ascending) with the pairing dsig: Uhat absorbs the chunk.
-    auto absorb = [&](DMat Rc, int64_t bc, int64_t r, int k, const int32_t* dI, const int32_t* dJ,
-                      bool verify, int64_t c0) {
-        DMat RIk = RI.sub(0, 0, k, n), Un = Unew.sub(0, 0, k, n);
-        DMat Kck = Kc.sub(0, 0, k, k), Kik = Kinv.sub(0, 0, k, k);
-        gather2d(st, Kck, RIk, nullptr, dJ);
+    // Given the chunk's pivot rows (device dI: chunk-local rows, k of them, with
+    // R_I in RI) and pivot column set dJ (ascending): pairing, Unew into Uhat
+    // rows [r, r+k), old rows reduced at J, Uhat*Omega maintained when sketching.
+    auto absorb = [&](int64_t r, int k, const int32_t* dI, const int32_t* dJ, int64_t c0,
+                      bool sketching) {
+        DMat RIk = RI.sub(0, 0, k, n), Kik = Kinv.sub(0, 0, k, k);
+        Kik.ld = k;
         {
             ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-            k_pair<<<1, 256, (size_t)3 * k * k * 4, st>>>(f, Kck.ptr, Kck.ld, k, dsig, Kik.ptr,
-                                                          Kik.ld, dflag);
-            count_launch();
+            k_pair2<<<1, 256, (size_t)3 * k * k * 4, st>>>(
+                f, RIk.ptr, RIk.ld, k, dJ, dI, c0, sketching ? S.ptr : nullptr, S.ld, SK, Kik.ptr,
+                UO.ptr, UO.ld, d_uhat_col, d_prow, d_pcol, r, dflag);
+            ++g_launches;
             FFB_CHECK_LAUNCH();
         }
-        gemm(f, st, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);  // Unew = Kc^-1 R_I
-        if (verify) {  // exact check: R - R[:, J] Unew == 0 (sticky flag)
-            DMat Gck = Gc.sub(0, 0, bc, k);
-            gather2d(st, Gck, Rc, nullptr, dJ);
-            gemm(f, st, GEMM_SUB, Rc, Gck, false, Un, false, bc, n, k);
-            any_nonzero(st, Rc, dflag);
-        }
-        if (r > 0) {  // Uhat_old -= Uhat_old[:, J] Unew
+        DMat Un = Uhat.sub(r, 0, k, n);
+        if (r > 0) {  // Up = Uhat_old[:, J] before Uhat_old changes
             DMat Up = Upd.sub(0, 0, r, k);
-            gather2d(st, Up, Uhat.sub(0, 0, r, n), nullptr, dJ);
+            gather2d(st, Up, Uhat.sub(0, 0, r, n), nullptr, dJ, 0);
+            gemm(f, st, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);  // Unew = Kc^-1 R_I
             gemm(f, st, GEMM_SUB, Uhat.sub(0, 0, r, n), Up, false, Un, false, r, n, k);
+            if (sketching)
+                gemm(f, st, GEMM_SUB, UO.sub(0, 0, r, SK), Up, false, UO.sub(r, 0, k, SK), false, r,
+                     SK, k);
+        } else {
+            gemm(f, st, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);
         }
-        copy_mat(st, Uhat.sub(r, 0, k, n), Un);
-        k_append_pivots<<<1, 128, 0, st>>>(d_uhat_col, d_prow, d_pcol, r, c0, dI, dJ, dsig, k);
-        count_launch();
     };
 
     int64_t r = 0;
-    bool exact = force_exact;
+    bool exact = force_exact || !sketch_ok;
     for (int attempt = 0; attempt < 2; ++attempt) {
+        ws.release(mark1);
         r = 0;
         FFB_CUDA(cudaMemsetAsync(dflag, 0, 4, st));
+        DMat YO;
+        if (!exact) {  // Y * Omega, once
+            DMat Om = ws.mat(n, SK);
+            k_random<<<(unsigned)cdiv(n * SK, 256), 256, 0, st>>>(Om.ptr, n * SK, 0x5EEDull + n + 977 * attempt, f.p);
+            ++g_launches;
+            YO = ws.mat(m, SK);
+            gemm(f, st, GEMM_SET, YO, Y, false, Om, false, m, SK, n);
+        }
         for (int64_t c0 = 0; c0 < m; c0 += B) {
             const int64_t bc = std::min<int64_t>(B, m - c0);
-            DMat Yc = Y.sub(c0, 0, bc, n), Rc = R.sub(0, 0, bc, n);
-            residual(Rc, Yc, bc, r);
+            DMat Yc = Y.sub(c0, 0, bc, n);
             if (!exact) {
-                // pivot rows from the sketch
                 DMat Sc = S.sub(0, 0, bc, SK);
-                gemm(f, st, GEMM_SET, Sc, Rc, false, Om, false, bc, SK, n);
                 {
-                    ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
+                    ProfScope ps(K_PLDUQ, st, 2.0 * bc * SK * r, 0.0);
+                    k_sketch_chunk<<<(unsigned)bc, 160, (size_t)std::max<int64_t>(r, 1) * 4, st>>>(
+                        f, Sc.ptr, Sc.ld, YO.ptr, YO.ld, Y.ptr, Y.ld, UO.ptr, UO.ld, d_uhat_col, r,
+                        c0, SK);
+                    ++g_launches;
                     k_row_detect<<<1, 256, rd_smem, st>>>(f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo);
-                    count_launch();
+                    ++g_launches;
                     FFB_CHECK_LAUNCH();
                 }
                 const int k = *(const int32_t*)io.readback(dinfo, 4);
-                if (k == 0) {
-                    any_nonzero(st, Rc, dflag);  // the chunk must be entirely dependent
-                    continue;
-                }
+                if (k == 0) continue;
                 const int32_t* dI = dinfo + 1;
-                gather_rows(st, RI.sub(0, 0, k, n), Rc, dI);
-                // pivot column set: CRP reduction tree
+                // exact residual of the k detected rows: R_I = Y_I - Y_I[:, pc] Uhat
+                DMat RIk = RI.sub(0, 0, k, n);
+                gather_rows(st, RIk, Yc, dI);
+                if (r > 0) {
+                    DMat Gk = Gi.sub(0, 0, k, r);
+                    gather2d(st, Gk, Y, dI, d_uhat_col, c0);
+                    gemm(f, st, GEMM_SUB, RIk, Gk, false, Uhat.sub(0, 0, r, n), false, k, n, r);
+                }
+                int cur = 0;
                 {
                     ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
                     k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, nullptr, nullptr,
                                                              0, lists[0], counts[0]);
-                    count_launch();
-                    int groups = nblk0, cur = 0;
+                    ++g_launches;
+                    int groups = nblk0;
                     while (groups > 1) {
                         const int ng = (groups + CRP_FAN - 1) / CRP_FAN;
                         k_crp_list<<<ng, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, lists[cur],
                                                               counts[cur], groups, lists[cur ^ 1],
                                                               counts[cur ^ 1]);
-                        count_launch();
+                        ++g_launches;
                         groups = ng;
                         cur ^= 1;
                     }
                     FFB_CHECK_LAUNCH();
-                    absorb(Rc, bc, r, k, dI, lists[cur], true, c0);
                 }
+                absorb(r, k, dI, lists[cur], c0, true);
                 r += k;
             } else {
-                // Exact row-order kernel on a copy of the residual.
+                // exact: residual of the whole chunk, then the row-sequential kernel
                 const size_t mk = ws.mark();
+                DMat Rc = ws.mat(bc, n);
+                copy_mat(st, Rc, Yc);
+                if (r > 0) {
+                    DMat Gk = Gi.sub(0, 0, bc, r);
+                    gather2d(st, Gk, Yc, nullptr, d_uhat_col, 0);
+                    gemm(f, st, GEMM_SUB, Rc, Gk, false, Uhat.sub(0, 0, r, n), false, bc, n, r);
+                }
                 DMat Rw = ws.mat(bc, n);
                 copy_mat(st, Rw, Rc);
                 int32_t* info = ws.vec<int32_t>(1 + bc + n + bc);
@@ -623,67 +676,92 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 std::vector<int32_t> I(hi + 1, hi + 1 + k);
                 std::vector<int32_t> J(hi + 1 + bc + n, hi + 1 + bc + n + k);
                 std::sort(J.begin(), J.end());
+                if (k > 0) {
+                    const int32_t* dI = io.upload(I);
+                    gather_rows(st, RI.sub(0, 0, k, n), Rc, dI);
+                    absorb(r, k, dI, io.upload(J), c0, false);
+                    r += k;
+                }
                 ws.release(mk);
-                if (k == 0) continue;
-                const int32_t* dI = io.upload(I);
-                gather_rows(st, RI.sub(0, 0, k, n), Rc, dI);
-                absorb(Rc, bc, r, k, dI, io.upload(J), false, c0);
-                r += k;
             }
         }
-        if (exact) break;
+        out.r = r;
+        std::vector<int32_t> pr, pcol_rows;
+        if (r > 0) {
+            const int32_t* hp = (const int32_t*)io.readback(d_prow, (size_t)r * 4);
+            pr.assign(hp, hp + r);
+            const int32_t* hc = (const int32_t*)io.readback(d_pcol, (size_t)r * 4);
+            pcol_rows.assign(hc, hc + r);
+        }
+
+        // ---- phase 2: factors from the pivots ----
+        std::vector<char> isp(n, 0), isr(m, 0);
+        for (int64_t t = 0; t < r; ++t) {
+            isp[pcol_rows[t]] = 1;
+            isr[pr[t]] = 1;
+        }
+        out.rimg = pr;
+        for (int64_t i = 0; i < m; ++i)
+            if (!isr[i]) out.rimg.push_back((int32_t)i);
+        out.cimg = pcol_rows;
+        for (int64_t j = 0; j < n; ++j)
+            if (!isp[j]) out.cimg.push_back((int32_t)j);
+        if (r == 0) {
+            if (exact) break;
+            // certificate: Y must be zero
+            any_nonzero(st, Y, dflag);
+            if (*(const int32_t*)io.readback(dflag, 4) == 0) break;
+            ++out.fallbacks;
+            exact = true;
+            continue;
+        }
+        DMat Kf = ws.mat(r, r);
+        const int32_t* dpr = io.upload(pr);
+        const int32_t* dpc = io.upload(pcol_rows);
+        gather2d(st, Kf, Y, dpr, dpc, 0);
+        ldu_inplace(f, st, Kf, ws, dflag);
+        k_unpack_l<<<rgrid(r, r), 256, 0, st>>>(io.Lo.ptr, io.Lo.ld, Kf.ptr, Kf.ld, r, io.d, 1 % f.p);
+        ++g_launches;
+        invert_vec(f, st, io.dinv, io.d, r);
+        DMat Uo = io.Uo.sub(0, 0, r, n);
+        const int32_t* dcimg = io.upload(out.cimg);
+        gather2d(st, Uo, Y, dpr, dcimg, 0);
+        trsm_lower_unit(f, st, io.Lo.sub(0, 0, r, r), Uo);
+        scale_rows(f, st, Uo, Uo, io.dinv);
+        const int32_t* dnp = nullptr;
+        if (m > r) {
+            std::vector<int32_t> np(out.rimg.begin() + r, out.rimg.end());
+            dnp = io.upload(np);
+            DMat T = ws.mat(m - r, r), Tt = ws.mat(r, m - r), U1t = ws.mat(r, r);
+            gather2d(st, T, Y, dnp, dpc, 0);
+            transpose(st, Tt, T);
+            transpose(st, U1t, Uo.sub(0, 0, r, r));
+            trsm_lower_unit(f, st, U1t, Tt);
+            scale_T(f, st, io.Lo.sub(r, 0, m - r, r), Tt, io.dinv);
+        }
+        if (exact) {
+            if (*(const int32_t*)io.readback(dflag, 4)) throw Status(FFB_ERROR, "plduq: singular pivot block");
+            break;
+        }
+        // ---- certificate (sketch path only) ----
+        {
+            DMat W = ws.mat(m, n), H = ws.mat(m, r);
+            gather2d(st, W, Y, io.upload(out.rimg), dcimg, 0);
+            k_scale_cols<<<rgrid(m, r), 256, 0, st>>>(f, H.ptr, H.ld, io.Lo.ptr, io.Lo.ld, io.d, r);
+            ++g_launches;
+            gemm(f, st, GEMM_SUB, W, H, false, Uo, false, m, n, r);
+            any_nonzero(st, W, dflag);
+            if (m > r) {
+                k_m1_pattern<<<rgrid(m - r, r), 256, 0, st>>>(io.Lo.ptr + r * io.Lo.ld, io.Lo.ld, dnp,
+                                                              d_prow, r, dflag);
+                ++g_launches;
+            }
+        }
         if (*(const int32_t*)io.readback(dflag, 4) == 0) break;
-        ++out.fallbacks;  // the sketch missed rank somewhere: redo exactly
+        ++out.fallbacks;  // a sketch missed rank: redo the search exactly
         exact = true;
     }
-    std::vector<int32_t> pr, pcol_rows;
-    if (r > 0) {
-        const int32_t* hp = (const int32_t*)io.readback(d_prow, (size_t)r * 4);
-        pr.assign(hp, hp + r);
-        const int32_t* hc = (const int32_t*)io.readback(d_pcol, (size_t)r * 4);
-        pcol_rows.assign(hc, hc + r);
-    }
-
-    // ---- phase 2: factors from the pivots ----
-    out.r = r;
-    std::vector<char> isp(n, 0), isr(m, 0);
-    for (int64_t t = 0; t < r; ++t) {
-        isp[pcol_rows[t]] = 1;
-        isr[pr[t]] = 1;
-    }
-    out.rimg = pr;
-    for (int64_t i = 0; i < m; ++i)
-        if (!isr[i]) out.rimg.push_back((int32_t)i);
-    out.cimg = pcol_rows;
-    for (int64_t j = 0; j < n; ++j)
-        if (!isp[j]) out.cimg.push_back((int32_t)j);
-    if (r == 0) return out;
-    FFB_CUDA(cudaMemsetAsync(dflag, 0, 4, st));
-    DMat Kf = ws.mat(r, r);
-    const int32_t* dpr = io.upload(pr);
-    const int32_t* dpc = io.upload(pcol_rows);
-    gather2d(st, Kf, Y, dpr, dpc);
-    ldu_inplace(f, st, Kf, ws, dflag);
-    // L1 into Lo rows [0, r), d
-    k_unpack_l<<<rgrid(r, r), 256, 0, st>>>(io.Lo.ptr, io.Lo.ld, Kf.ptr, Kf.ld, r, io.d, 1 % f.p);
-    count_launch();
-    invert_vec(f, st, io.dinv, io.d, r);
-    // U = D^-1 L1^-1 Y[pr, Q]
-    DMat Uo = io.Uo.sub(0, 0, r, n);
-    gather2d(st, Uo, Y, dpr, io.upload(out.cimg));
-    trsm_lower_unit(f, st, io.Lo.sub(0, 0, r, r), Uo);
-    scale_rows(f, st, Uo, Uo, io.dinv);
-    // M1 = Y[np, pc] U1^-1 D^-1
-    if (m > r) {
-        std::vector<int32_t> np(out.rimg.begin() + r, out.rimg.end());
-        DMat T = ws.mat(m - r, r), Tt = ws.mat(r, m - r), U1t = ws.mat(r, r);
-        gather2d(st, T, Y, io.upload(np), dpc);
-        transpose(st, Tt, T);
-        transpose(st, U1t, Uo.sub(0, 0, r, r));
-        trsm_lower_unit(f, st, U1t, Tt);
-        scale_T(f, st, io.Lo.sub(r, 0, m - r, r), Tt, io.dinv);
-    }
-    if (*(const int32_t*)io.readback(dflag, 4)) throw Status(FFB_ERROR, "plduq: singular pivot block");
+    ws.release(mark0);
     return out;
 }
 

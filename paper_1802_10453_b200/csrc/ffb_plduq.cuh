@@ -55,7 +55,8 @@ struct PlduqOut {
 // PLDUQ of Y (m x n, preserved) into io.Lo/io.Uo/io.d/io.dinv.
 PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, const PlduqIO& io);
 
-void gather2d(cudaStream_t st, DMat dst, DMat src, const int32_t* ridx, const int32_t* cidx);
+void gather2d(cudaStream_t st, DMat dst, DMat src, const int32_t* ridx, const int32_t* cidx,
+              int64_t roff = 0);
 void copy_mat(cudaStream_t st, DMat dst, DMat src);
 // In-place LDU without pivoting (strict lower L, diagonal d, strict upper U).
 void ldu_inplace(const Fp& f, cudaStream_t st, DMat K, Workspace& ws, int32_t* fail);

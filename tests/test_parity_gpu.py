@@ -301,8 +301,9 @@ print("ok")
 
 @pytest.mark.parametrize("env", [{"FFB_PLDUQ_SEQ_ROWS": "0"},
                                  {"FFB_PLDUQ_SEQ_ROWS": "0", "FFB_PLDUQ_FORCE_FALLBACK": "1"},
+                                 {"FFB_PLDUQ_SEQ_ROWS": "0", "FFB_PLDUQ_SKETCH_COLS": "3"},
                                  {"FFB_PLDUQ_SEQ_ROWS": "100000"}],
-                         ids=["parallel", "parallel-fallback", "sequential"])
+                         ids=["parallel", "exact-forced", "sketch-misses-certificate", "sequential"])
 def test_plduq_paths(gpu, env):
     """Every PLDUQ path (sketch-based parallel, its exact fallback, the sequential kernel)."""
     _run_in_subprocess(env, PLDUQ_PATH_CHECK)
