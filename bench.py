@@ -315,6 +315,7 @@ def main():
                                              - rank_out ** 2 * w.n)) / ops if rank_out else 0,
             "gpu_launches": launches, "host_syncs_per_step": syncs,
             "kernel_classes_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
+            "kernel_classes_launches": {k: v["launches"] for k, v in prof.items()},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks_info,
         }
         print(json.dumps(line), flush=True)

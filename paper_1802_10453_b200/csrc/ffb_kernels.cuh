@@ -12,7 +12,10 @@ extern thread_local uint64_t g_launches;
 
 // Optional per-kernel-class instrumentation (ffb_profile_enable): CUDA events
 // around each launch on the launching stream, summed per class.
-enum KClass { K_GEMM = 0, K_LEAF = 1, K_PLDUQ = 2, K_TRSM = 3, K_MOVE = 4, K_OTHER = 5, K_NCLASS = 6 };
+enum KClass {
+    K_GEMM = 0, K_LEAF = 1, K_PLDUQ = 2, K_TRSM = 3, K_MOVE = 4, K_OTHER = 5,
+    K_PQ_SKETCH = 6, K_PQ_CRP = 7, K_PQ_PAIR = 8, K_LDU = 9, K_PACK = 10, K_NCLASS = 11
+};
 struct Profiler {
     struct Rec {
         int cls;

@@ -493,7 +493,7 @@ void ldu_inplace(const Fp& f, cudaStream_t st, DMat K, Workspace& ws, int32_t* f
     const int64_t n = K.rows;
     if (n <= 0) return;
     if (n <= 64) {
-        ProfScope ps(K_PLDUQ, st, 2.0 * n * n * n / 3.0, 8.0 * n * n);
+        ProfScope ps(K_LDU, st, 2.0 * n * n * n / 3.0, 8.0 * n * n);
         k_ldu_base<<<1, 256, 0, st>>>(f, K.ptr, K.ld, (int)n, fail);
         count_launch();
         FFB_CHECK_LAUNCH();
@@ -572,7 +572,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         DMat RIk = RI.sub(0, 0, k, n), Kik = Kinv.sub(0, 0, k, k);
         Kik.ld = k;
         {
-            ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
+            ProfScope ps(K_PQ_PAIR, st, 0.0, 0.0);
             k_pair2<<<1, 256, (size_t)3 * k * k * 4, st>>>(
                 f, RIk.ptr, RIk.ld, k, dJ, dI, c0, sketching ? S.ptr : nullptr, S.ld, SK, Kik.ptr,
                 UO.ptr, UO.ld, d_uhat_col, d_prow, d_pcol, r, dflag);
@@ -613,11 +613,14 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             if (!exact) {
                 DMat Sc = S.sub(0, 0, bc, SK);
                 {
-                    ProfScope ps(K_PLDUQ, st, 2.0 * bc * SK * r, 0.0);
+                    ProfScope ps(K_PQ_SKETCH, st, 2.0 * bc * SK * r, 0.0);
                     k_sketch_chunk<<<(unsigned)bc, 160, (size_t)std::max<int64_t>(r, 1) * 4, st>>>(
                         f, Sc.ptr, Sc.ld, YO.ptr, YO.ld, Y.ptr, Y.ld, UO.ptr, UO.ld, d_uhat_col, r,
                         c0, SK);
                     ++g_launches;
+                }
+                {
+                    ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
                     k_row_detect<<<1, 256, rd_smem, st>>>(f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo);
                     ++g_launches;
                     FFB_CHECK_LAUNCH();
@@ -635,7 +638,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 }
                 int cur = 0;
                 {
-                    ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
+                    ProfScope ps(K_PQ_CRP, st, 0.0, 0.0);
                     k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, nullptr, nullptr,
                                                              0, lists[0], counts[0]);
                     ++g_launches;

@@ -379,7 +379,7 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
     int8_t* Ap = buf;
     int8_t* Bp = buf + abytes;
     {
-        ProfScope ps(K_MOVE, st, 0.0, 5.0 * (M * K + N * K));
+        ProfScope ps(K_PACK, st, 0.0, 5.0 * (M * K + N * K));
         pack(st, Ap, Kp, A, ta, M, K, f.p);
         pack(st, Bp, Kp, B, !tb, N, K, f.p);  // need B^T (N x K): transposed pack unless tb
     }

@@ -377,7 +377,8 @@ class Context:
     def sync_count(self) -> int:
         return int(lib().ffb_sync_count(self.handle))
 
-    KERNEL_CLASSES = ("gemm", "leaf", "plduq", "trsm", "move", "other")
+    KERNEL_CLASSES = ("gemm", "leaf", "plduq_rowdetect_seq", "trsm", "move", "other", "plduq_sketch",
+                      "plduq_crp", "plduq_pair", "ldu", "pack")
 
     def profile(self, enable: bool = True) -> None:
         """Per-kernel-class CUDA-event timing of subsequent calls (resets totals)."""
