@@ -245,6 +245,220 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Limb variant for 255 < p < 2^23 (configuration 3).  A centered residue x,
+// |x| < 2^22, is split into signed int8 limbs x = a0 + 2^8 a1 + 2^16 a2
+// (|a2| <= 64).  Per 32-deep K step the single MMA thread issues the 9 limb
+// products A_i B_j^T into 5 TMEM accumulators, one per shift class s = i + j
+// (5 x 64 columns); each class sum is exact in int32 for K < 65536.  The
+// epilogue folds  sum_s (acc_s mod p) * (2^{8s} mod p)  mod p.
+// Operands: 3 limb planes stacked by rows ([plane][rows][Kp]); one 2-D tensor
+// map covers all planes (rows a plane over-reads land only in masked output
+// rows/columns; the last plane is zero-filled by TMA).
+// ---------------------------------------------------------------------------
+constexpr int LB_BN = 64, LB_STAGES = 2;
+constexpr int LB_A_BYTES = 3 * TC_BM * TC_BK, LB_B_BYTES = 3 * LB_BN * TC_BK;
+constexpr int LB_STAGE_BYTES = LB_A_BYTES + LB_B_BYTES;
+constexpr int LB_EPI_BYTES = 4 * 32 * 33 * 4;
+constexpr int LB_SMEM = 1024 + LB_STAGES * LB_STAGE_BYTES + LB_EPI_BYTES + 256;
+constexpr uint32_t LB_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(LB_BN >> 3) << 17) |
+                              ((uint32_t)(TC_BM >> 4) << 24);
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    k_gemm_limb_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                   uint32_t* __restrict__ C, int64_t ldc, int M, int N, int nk, int Mrows, int Nrows,
+                   Fp f, int mode) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + LB_STAGES * LB_A_BYTES;
+    uint32_t* sEpi = (uint32_t*)(smem + LB_STAGES * LB_STAGE_BYTES);
+    uint64_t* full = (uint64_t*)(sEpi + 4 * 32 * 33);
+    uint64_t* empty = full + LB_STAGES;
+    uint64_t* accfull = empty + LB_STAGES;
+    uint32_t* tmem_slot = (uint32_t*)(accfull + 1);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m0 = blockIdx.y * TC_BM, n0 = blockIdx.x * LB_BN;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+        for (int s = 0; s < LB_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(accfull, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512u));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % LB_STAGES;
+                const uint32_t ph = (kb / LB_STAGES) & 1;
+                mbar_wait(&empty[s], ph ^ 1);
+                mbar_expect_tx(&full[s], LB_STAGE_BYTES);
+                for (int l = 0; l < 3; ++l) {
+                    tma_load_2d(sA + s * LB_A_BYTES + l * TC_BM * TC_BK, &tmA, &full[s], kb * TC_BK,
+                                l * Mrows + m0);
+                    tma_load_2d(sB + s * LB_B_BYTES + l * LB_BN * TC_BK, &tmB, &full[s], kb * TC_BK,
+                                l * Nrows + n0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            for (int kb = 0; kb < nk; ++kb) {
+                const int s = kb % LB_STAGES;
+                const uint32_t ph = (kb / LB_STAGES) & 1;
+                mbar_wait(&full[s], ph);
+                tc_fence_after();
+                const uint32_t a0 = smem_u32(sA + s * LB_A_BYTES);
+                const uint32_t b0 = smem_u32(sB + s * LB_B_BYTES);
+#pragma unroll
+                for (int kk = 0; kk < TC_BK / 32; ++kk)
+#pragma unroll
+                    for (int i = 0; i < 3; ++i)
+#pragma unroll
+                        for (int j = 0; j < 3; ++j) {
+                            // first product of each shift class in this (i, j) order
+                            const bool first = (i == 0) || (i == 1 && j == 2) || (i == 2 && j == 2);
+                            mma_i8(tmem + (uint32_t)((i + j) * LB_BN),
+                                   sw128_desc(a0 + i * TC_BM * TC_BK + kk * 32),
+                                   sw128_desc(b0 + j * LB_BN * TC_BK + kk * 32), LB_IDESC,
+                                   ((kb | kk) != 0 || !first) ? 1u : 0u);
+                        }
+                mma_commit(&empty[s]);
+            }
+            mma_commit(accfull);
+        }
+    } else {
+        const int q = warp & 3;
+        uint32_t* tile = sEpi + (warp - 2) * 32 * 33;
+        const uint32_t mu32 = (uint32_t)(0x100000000ull / f.p);
+        const uint32_t bias = (uint32_t)((0x80000000ull) % f.p);
+        uint32_t wsh[5];
+        {
+            uint64_t w = 1 % f.p;
+            for (int s = 0; s < 5; ++s) {
+                wsh[s] = (uint32_t)w;
+                w = (w << 8) % f.p;
+            }
+        }
+        mbar_wait(accfull, 0);
+        tc_fence_after();
+        const int rbase = m0 + 32 * q;
+        for (int c = 0; c < LB_BN; c += 32) {
+            if (n0 + c >= N) break;
+            uint32_t v[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] = 0;
+#pragma unroll
+            for (int s = 0; s < 5; ++s) {
+                uint32_t r[32];
+                tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(s * LB_BN + c), r);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const uint32_t x = r[j] ^ 0x80000000u;  // acc + 2^31
+                    uint32_t qq = __umulhi(x, mu32);
+                    uint32_t rr = x - qq * f.p;
+                    if (rr >= f.p) rr -= f.p;
+                    rr = fsub(f, rr, bias);                  // acc mod p
+                    v[j] = fadd(f, v[j], fmul(f, rr, wsh[s]));
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < 32; ++j) tile[lane * 33 + j] = v[j];
+            __syncwarp();
+            const int col = n0 + c + lane;
+            const bool colok = col < N;
+            uint32_t cv[32];
+            if (mode != GEMM_SET) {
+#pragma unroll
+                for (int rr = 0; rr < 32; ++rr) {
+                    const int row = rbase + rr;
+                    cv[rr] = (colok && row < M) ? __ldg(C + (int64_t)row * ldc + col) : 0u;
+                }
+            }
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) {
+                const int row = rbase + rr;
+                if (colok && row < M) {
+                    const uint32_t val = tile[rr * 33 + lane];
+                    uint32_t o;
+                    if (mode == GEMM_SUB) o = fsub(f, cv[rr], val);
+                    else if (mode == GEMM_ADD) o = fadd(f, cv[rr], val);
+                    else o = val;
+                    C[(int64_t)row * ldc + col] = o;
+                }
+            }
+            __syncwarp();
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512u));
+    }
+}
+
+// 3 limb planes of centered op(src): dst[l][i][k]  (plane stride rows*ldd)
+__device__ __forceinline__ void limbs(uint32_t x, uint32_t p, int8_t& a0, int8_t& a1, int8_t& a2) {
+    int32_t c = x > (p >> 1) ? (int32_t)x - (int32_t)p : (int32_t)x;
+    const int32_t l0 = ((c + 128) & 255) - 128;
+    c = (c - l0) >> 8;
+    const int32_t l1 = ((c + 128) & 255) - 128;
+    c = (c - l1) >> 8;
+    a0 = (int8_t)l0;
+    a1 = (int8_t)l1;
+    a2 = (int8_t)c;
+}
+
+__global__ void k_pack_limb_n(int8_t* dst, int64_t ldd, int64_t plane, const uint32_t* src,
+                              int64_t lds, int64_t rows, int64_t K, uint32_t p) {
+    const int64_t i = blockIdx.y;
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < ldd;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        int8_t a0 = 0, a1 = 0, a2 = 0;
+        if (i < rows && k < K) limbs(src[i * lds + k], p, a0, a1, a2);
+        dst[i * ldd + k] = a0;
+        dst[plane + i * ldd + k] = a1;
+        dst[2 * plane + i * ldd + k] = a2;
+    }
+}
+
+__global__ void k_pack_limb_t(int8_t* dst, int64_t ldd, int64_t plane, const uint32_t* src,
+                              int64_t lds, int64_t rows, int64_t K, uint32_t p) {
+    __shared__ uint32_t tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
+    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+        const int64_t k = k0 + yy, i = i0 + threadIdx.x;
+        tile[yy][threadIdx.x] = (k < K && i < rows) ? src[k * lds + i] : 0u;
+    }
+    __syncthreads();
+    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+        const int64_t i = i0 + yy, k = k0 + threadIdx.x;
+        if (i < rows && k < ldd) {
+            int8_t a0, a1, a2;
+            limbs(tile[threadIdx.x][yy], p, a0, a1, a2);
+            dst[i * ldd + k] = a0;
+            dst[plane + i * ldd + k] = a1;
+            dst[2 * plane + i * ldd + k] = a2;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Packing: dst (rows x ldd int8, K-major) <- centered op(src), zero padding.
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ int8_t center(uint32_t x, uint32_t p) {
@@ -365,13 +579,62 @@ void launch_tc(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, DM
 bool tc_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K) {
     static const bool disabled = getenv("FFB_DISABLE_TC") != nullptr;
     if (disabled) return false;
-    return f.p <= 255 && M >= 64 && N >= 64 && K >= 16 && K <= 120000 &&
-           (double)M * N * K >= 4.0e6 && M < (1ll << 31) && N < (1ll << 31);
+    const bool shape = M >= 64 && N >= 64 && K >= 16 && (double)M * N * K >= 4.0e6 &&
+                       M < (1ll << 30) && N < (1ll << 30);
+    if (f.p <= 255) return shape && K <= 120000;
+    return f.p < (1u << 23) && shape && K <= 60000;  // int8 limbs
+}
+
+void tc_gemm_limb(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B,
+                  bool tb, int64_t M, int64_t N, int64_t K) {
+    const int64_t Kp = (K + 15) / 16 * 16;
+    const int64_t Mr = cdiv(M, TC_BM) * TC_BM, Nr = cdiv(N, LB_BN) * LB_BN;
+    const size_t aplane = (size_t)Mr * Kp, bplane = (size_t)Nr * Kp;
+    const size_t abytes = (3 * aplane + 1023) / 1024 * 1024, bbytes = (3 * bplane + 1023) / 1024 * 1024;
+    int8_t* buf = scratch(abytes + bbytes);
+    int8_t* Ap = buf;
+    int8_t* Bp = buf + abytes;
+    {
+        ProfScope ps(K_PACK, st, 0.0, 7.0 * (M * K + N * K));
+        FFB_CUDA(cudaMemsetAsync(buf, 0, abytes + bbytes, st));
+        auto pk = [&](int8_t* dst, size_t plane, DMat src, bool trans, int64_t rows) {
+            if (!trans) {
+                for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
+                    const int64_t nr = std::min<int64_t>(65535, rows - r0);
+                    k_pack_limb_n<<<dim3((unsigned)std::min<int64_t>(64, cdiv(Kp, 256)), (unsigned)nr), 256, 0, st>>>(
+                        dst + r0 * Kp, Kp, (int64_t)plane, src.ptr + r0 * src.ld, src.ld, nr, K, f.p);
+                }
+            } else {
+                k_pack_limb_t<<<dim3((unsigned)cdiv(Kp, 32), (unsigned)cdiv(rows, 32)), dim3(32, 8), 0, st>>>(
+                    dst, Kp, (int64_t)plane, src.ptr, src.ld, rows, K, f.p);
+            }
+            ++g_launches;
+            FFB_CHECK_LAUNCH();
+        };
+        pk(Ap, aplane, A, ta, M);
+        pk(Bp, bplane, B, !tb, N);
+    }
+    static bool attr = false;
+    if (!attr) {
+        FFB_CUDA(cudaFuncSetAttribute(k_gemm_limb_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, LB_SMEM));
+        attr = true;
+    }
+    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, 3.0 * (M * K + N * K) + 8.0 * M * N);
+    CUtensorMap ma = make_map(Ap, 3 * Mr, Kp, TC_BM), mb = make_map(Bp, 3 * Nr, Kp, LB_BN);
+    dim3 grid((unsigned)cdiv(N, LB_BN), (unsigned)cdiv(M, TC_BM));
+    k_gemm_limb_tc<<<grid, TC_THREADS, LB_SMEM, st>>>(ma, mb, C.ptr, C.ld, (int)M, (int)N,
+                                                     (int)cdiv(Kp, TC_BK), (int)Mr, (int)Nr, f, mode);
+    ++g_launches;
+    FFB_CHECK_LAUNCH();
 }
 
 void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
              int64_t M, int64_t N, int64_t K) {
     load_encode();
+    if (f.p > 255) {
+        tc_gemm_limb(f, st, mode, C, A, ta, B, tb, M, N, K);
+        return;
+    }
     const int64_t Kp = (K + 15) / 16 * 16;
     const size_t abytes = ((size_t)M * Kp + 1023) / 1024 * 1024;
     const size_t bbytes = ((size_t)N * Kp + 1023) / 1024 * 1024;
