@@ -582,7 +582,7 @@ bool tc_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K) {
     const bool shape = M >= 64 && N >= 64 && K >= 16 && (double)M * N * K >= 4.0e6 &&
                        M < (1ll << 30) && N < (1ll << 30);
     if (f.p <= 255) return shape && K <= 120000;
-    return f.p < (1u << 23) && shape && K <= 60000;  // int8 limbs
+    return f.p < (1u << 23) && shape && K <= 40000;  // int8 limbs: 3 * 2^14 * K < 2^31
 }
 
 void tc_gemm_limb(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B,

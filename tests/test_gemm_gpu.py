@@ -50,3 +50,23 @@ def test_tc_gemm_transposed_operands(gpu, oracle, n, k):
     d = ffb.BlockDiag(blocks)
     kind, val, val2 = d.columns()
     assert np.array_equal(ffb.syrdk_sub(c, g, d, p, ctx=gpu), oracle.syrdk_sub(p, c, g, kind, val, val2))
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 64, 128), (300, 500, 700), (129, 257, 65), (513, 300, 8000)])
+@pytest.mark.parametrize("p", [8388593, 65521, 1000003, 257])
+def test_tc_limb_gemm(gpu, oracle, m, n, k, p):
+    """int8-limb tcgen05 path (255 < p < 2^23): 9 limb products into 5 shift classes."""
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(m + n + k + p)
+    if k == 8000:  # extreme centered residues: |x| = (p-1)/2
+        a = np.full((m, k), (p - 1) // 2, np.uint64)
+        b = np.full((k, n), (p + 1) // 2, np.uint64)
+    else:
+        a = rng.integers(0, p, (m, k), dtype=np.uint64)
+        b = rng.integers(0, p, (k, n), dtype=np.uint64)
+    c = rng.integers(0, p, (m, n), dtype=np.uint64)
+    assert np.array_equal(ffb.gemm_sub(c, a, b, p, ctx=gpu), oracle.gemm_sub(p, c, a, b))
+    c2 = rand_sym(rng, p, n)
+    a2 = rng.integers(0, p, (k, n), dtype=np.uint64)
+    b2 = rng.integers(0, p, (k, n), dtype=np.uint64)
+    assert np.array_equal(ffb.syr2k_sub(c2, a2, b2, p, ctx=gpu), oracle.syr2k_sub(p, c2, a2, b2))
