@@ -257,22 +257,19 @@ struct Engine {
         HFact f1 = dispatch(A.sub(0, 0, m, m), rows1, coff);  // :303
         const int64_t r1 = f1.rank;
 
-        // B' = P1^T B (:308)
+        // B' = P1^T B (:308) and [L1; M1] in f1's position order (from Lg), one launch
         DMat BP = ws_mat(c, m, ns);
-        gather_rows(st, BP, A.sub(0, m, m, ns), upload(c, f1.perm));
-        // [L1; M1] in f1's position order, from Lg
         std::vector<int32_t> prow(m);
         for (int64_t i = 0; i < m; ++i) prow[i] = rows[f1.perm[i]];
         DMat LM = ws_mat(c, m, r1);
-        gather_lg(st, LM, Lg, upload(c, prow), coff);
+        gather_rows2(st, BP, A, upload(c, f1.perm), m, LM, Lg, upload(c, prow), coff);
         DMat X = BP.sub(0, 0, r1, ns);
         trsm_lower_unit(f, st, LM.sub(0, 0, r1, r1), X);  // :310
         DMat Y = BP.sub(r1, 0, m - r1, ns);
         gemm(f, st, GEMM_SUB, Y, LM.sub(r1, 0, m - r1, r1), false, X, false, m - r1, ns, r1);  // :312
         DMat G = ws_mat(c, ns, r1);
-        inverse_apply_T(f, st, G, X, D, coff);  // :313
         std::vector<int32_t> rows2(rows.begin() + m, rows.end());
-        scatter_lg(st, Lg, upload(c, rows2), coff, 1, G);  // rows m..s of N1 (:319-322)
+        inverse_apply_T(f, st, G, X, D, coff, Lg, upload(c, rows2));  // :313 + rows m..s of N1
         DMat Z = A.sub(m, m, ns, ns);
         gemm(f, st, GEMM_SUB, Z, G, false, X, false, ns, ns, r1);  // Z = C - G D1 G^T (:315)
 

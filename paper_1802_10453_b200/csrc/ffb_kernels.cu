@@ -190,6 +190,26 @@ __global__ void k_gather_rows(uint32_t* dst, int64_t ldd, const uint32_t* src, i
         d[j] = s[j];
 }
 
+// Two independent row gathers in one launch (blockIdx.z): dst[i][j] = src[idx[i]][c0 + j].
+struct RowGather {
+    uint32_t* dst;
+    int64_t ldd;
+    const uint32_t* src;
+    int64_t lds;
+    const int32_t* idx;
+    int64_t c0, rows, cols;
+};
+__global__ void k_gather_rows2(RowGather g0, RowGather g1) {
+    const RowGather& g = blockIdx.z == 0 ? g0 : g1;
+    const int64_t i = blockIdx.y;
+    if (i >= g.rows) return;
+    const uint32_t* s = g.src + (int64_t)g.idx[i] * g.lds + g.c0;
+    uint32_t* d = g.dst + i * g.ldd;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g.cols;
+         j += (int64_t)gridDim.x * blockDim.x)
+        d[j] = s[j];
+}
+
 __global__ void k_gather_sym(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
                              const int32_t* ridx, const int32_t* idx, int64_t n) {
     const int64_t a = blockIdx.y;
@@ -239,7 +259,8 @@ __global__ void k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int6
 // G[j][k] = (D^-1 X)[k][j], X is r x ncols.  Tile: 32 k x 32 j, with one
 // extra row on each side for the 2x2 partners.
 __global__ void k_inverse_apply_T(Fp f, uint32_t* G, int64_t ldg, const uint32_t* X,
-                                  int64_t ldx, int64_t r, int64_t ncols, DDiag D, int64_t coff) {
+                                  int64_t ldx, int64_t r, int64_t ncols, DDiag D, int64_t coff,
+                                  uint32_t* Lg, int64_t ldl, const int32_t* ids) {
     __shared__ uint32_t tile[34][33];
     const int64_t k0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
     for (int kk = threadIdx.y; kk < 34; kk += blockDim.y) {
@@ -265,6 +286,7 @@ __global__ void k_inverse_apply_T(Fp f, uint32_t* G, int64_t ldg, const uint32_t
             v = fadd(f, fmul(f, top, tile[kk][jj]), fmul(f, inv, tile[kk + 1][jj]));
         }
         G[j * ldg + k] = v;
+        if (Lg) Lg[(int64_t)ids[j] * ldl + coff + k] = v;  // rows of N1 (sytrf.cpp:319-322)
     }
 }
 
@@ -462,6 +484,25 @@ void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int 
     FFB_CHECK_LAUNCH();
 }
 
+void gather_rows2(cudaStream_t st, DMat d0, DMat s0, const int32_t* i0, int64_t c0, DMat d1, DMat s1,
+                  const int32_t* i1, int64_t c1) {
+    const int64_t rows = std::max(d0.rows, d1.rows), cols = std::max(d0.cols, d1.cols);
+    if (rows <= 0 || cols <= 0) return;
+    if (rows > FFB_ROWCHUNK) {  // rare: fall back to two launches
+        gather_rows(st, d0, s0.sub(0, c0, s0.rows, d0.cols), i0);
+        gather_rows(st, d1, s1.sub(0, c1, s1.rows, d1.cols), i1);
+        return;
+    }
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
+    RowGather g0{d0.ptr, d0.ld, s0.ptr, s0.ld, i0, c0, d0.cols > 0 ? d0.rows : 0, d0.cols};
+    RowGather g1{d1.ptr, d1.ld, s1.ptr, s1.ld, i1, c1, d1.cols > 0 ? d1.rows : 0, d1.cols};
+    dim3 g = rowgrid(rows, cols);
+    g.z = 2;
+    k_gather_rows2<<<g, 256, 0, st>>>(g0, g1);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
 void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t col0) {
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (dst.rows <= 0 || dst.cols <= 0) return;
@@ -474,12 +515,13 @@ void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t c
     FFB_CHECK_LAUNCH();
 }
 
-void inverse_apply_T(const Fp& f, cudaStream_t st, DMat G, DMat X, DDiag D, int64_t coff) {
+void inverse_apply_T(const Fp& f, cudaStream_t st, DMat G, DMat X, DDiag D, int64_t coff,
+                     DMat Lg, const int32_t* ids) {
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (X.rows <= 0 || X.cols <= 0) return;
     dim3 grid((unsigned)cdiv(X.cols, 32), (unsigned)cdiv(X.rows, 32));
     k_inverse_apply_T<<<grid, dim3(32, 8), 0, st>>>(f, G.ptr, G.ld, X.ptr, X.ld, X.rows, X.cols, D,
-                                                    coff);
+                                                    coff, ids ? Lg.ptr : nullptr, Lg.ld, ids);
     count_launch();
     FFB_CHECK_LAUNCH();
 }

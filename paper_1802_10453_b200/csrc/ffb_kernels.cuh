@@ -65,8 +65,13 @@ void transpose(cudaStream_t st, DMat dst, DMat src);
 void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int cstride, DMat src);
 // dst[i][k] = Lg[ids[i]][col0 + k]
 void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t col0);
-// G (ncols x r) = (D^-1 X)^T with D the global block diagonal at columns [coff, coff+r)
-void inverse_apply_T(const Fp& f, cudaStream_t st, DMat G, DMat X, DDiag D, int64_t coff);
+// G (ncols x r) = (D^-1 X)^T with D the global block diagonal at columns [coff, coff+r);
+// when ids is given, also Lg[ids[j]][coff + k] = G[j][k] (fused scatter).
+void inverse_apply_T(const Fp& f, cudaStream_t st, DMat G, DMat X, DDiag D, int64_t coff,
+                     DMat Lg = DMat(), const int32_t* ids = nullptr);
+// d0[i][j] = s0[i0[i]][c0 + j] and d1[i][j] = s1[i1[i]][c1 + j] in one launch
+void gather_rows2(cudaStream_t st, DMat d0, DMat s0, const int32_t* i0, int64_t c0, DMat d1, DMat s1,
+                  const int32_t* i1, int64_t c1);
 // G (ncols x r) = (diag(dinv) X)^T
 void scale_T(const Fp& f, cudaStream_t st, DMat G, DMat X, const uint32_t* dinv);
 // out[i] = v[i]^-1

@@ -547,8 +547,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     int32_t* counts[2] = {ws.vec<int32_t>(nblk0), ws.vec<int32_t>(nblk0)};
     int32_t* dflag = ws.vec<int32_t>(4);
     int32_t* d_uhat_col = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
-    int32_t* d_prow = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
-    int32_t* d_pcol = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
+    const int64_t pstride = (std::max<int64_t>(mn, 1) + 63) / 64 * 64;
+    int32_t* d_prow = ws.vec<int32_t>(2 * pstride);
+    int32_t* d_pcol = d_prow + pstride;
     const size_t mark1 = ws.mark();
 
     const size_t rd_smem = ((size_t)2 * RD_MAX_B * SK + SK) * 4;
@@ -690,11 +691,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         }
         out.r = r;
         std::vector<int32_t> pr, pcol_rows;
-        if (r > 0) {
-            const int32_t* hp = (const int32_t*)io.readback(d_prow, (size_t)r * 4);
+        if (r > 0) {  // d_prow and d_pcol are adjacent: one read-back
+            const int32_t* hp = (const int32_t*)io.readback(d_prow, (size_t)(2 * pstride) * 4);
             pr.assign(hp, hp + r);
-            const int32_t* hc = (const int32_t*)io.readback(d_pcol, (size_t)r * 4);
-            pcol_rows.assign(hc, hc + r);
+            pcol_rows.assign(hp + pstride, hp + pstride + r);
         }
 
         // ---- phase 2: factors from the pivots ----

@@ -465,6 +465,39 @@ __device__ __forceinline__ int8_t center(uint32_t x, uint32_t p) {
     return (int8_t)(x > (p >> 1) ? (int32_t)x - (int32_t)p : (int32_t)x);
 }
 
+// Both operands in one launch: blockIdx.z selects the job.
+struct PackJob {
+    int8_t* dst;
+    int64_t ldd;
+    const uint32_t* src;
+    int64_t lds;
+    int64_t rows, K;
+    int trans;
+};
+__global__ void k_pack2(PackJob j0, PackJob j1, uint32_t p) {
+    const PackJob& j = blockIdx.z == 0 ? j0 : j1;
+    __shared__ int8_t tile[32][33];
+    const int64_t i0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
+    if (i0 >= j.rows || k0 >= j.ldd) return;  // uniform per block
+    if (!j.trans) {
+        for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+            const int64_t i = i0 + yy, k = k0 + threadIdx.x;
+            if (i < j.rows && k < j.ldd)
+                j.dst[i * j.ldd + k] = (k < j.K) ? center(j.src[i * j.lds + k], p) : (int8_t)0;
+        }
+        return;
+    }
+    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+        const int64_t k = k0 + yy, i = i0 + threadIdx.x;
+        tile[yy][threadIdx.x] = (k < j.K && i < j.rows) ? center(j.src[k * j.lds + i], p) : (int8_t)0;
+    }
+    __syncthreads();
+    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
+        const int64_t i = i0 + yy, k = k0 + threadIdx.x;
+        if (i < j.rows && k < j.ldd) j.dst[i * j.ldd + k] = tile[threadIdx.x][yy];
+    }
+}
+
 // not transposed: op(src)[i][k] = src[i][k]
 __global__ void k_pack_n(int8_t* dst, int64_t ldd, const uint32_t* src, int64_t lds, int64_t rows,
                          int64_t K, uint32_t p) {
@@ -579,7 +612,7 @@ void launch_tc(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, DM
 bool tc_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K) {
     static const bool disabled = getenv("FFB_DISABLE_TC") != nullptr;
     if (disabled) return false;
-    const bool shape = M >= 64 && N >= 64 && K >= 16 && (double)M * N * K >= 4.0e6 &&
+    const bool shape = M >= 64 && N >= 64 && K >= 16 && (double)M * N * K >= 2.0e7 &&
                        M < (1ll << 30) && N < (1ll << 30);
     if (f.p <= 255) return shape && K <= 120000;
     return f.p < (1u << 23) && shape && K <= 40000;  // int8 limbs: 3 * 2^14 * K < 2^31
@@ -643,8 +676,18 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
     int8_t* Bp = buf + abytes;
     {
         ProfScope ps(K_PACK, st, 0.0, 5.0 * (M * K + N * K));
-        pack(st, Ap, Kp, A, ta, M, K, f.p);
-        pack(st, Bp, Kp, B, !tb, N, K, f.p);  // need B^T (N x K): transposed pack unless tb
+        // B^T (N x K) is needed: transposed pack unless tb
+        PackJob ja{Ap, Kp, A.ptr, A.ld, M, K, ta ? 1 : 0}, jb{Bp, Kp, B.ptr, B.ld, N, K, tb ? 0 : 1};
+        const int64_t rmax = std::max(M, N);
+        if (rmax <= (int64_t)65535 * 32) {
+            dim3 grid((unsigned)cdiv(Kp, 32), (unsigned)cdiv(rmax, 32), 2);
+            k_pack2<<<grid, dim3(32, 8), 0, st>>>(ja, jb, f.p);
+            ++g_launches;
+            FFB_CHECK_LAUNCH();
+        } else {
+            pack(st, Ap, Kp, A, ta, M, K, f.p);
+            pack(st, Bp, Kp, B, !tb, N, K, f.p);
+        }
     }
     const int64_t nk = cdiv(Kp, TC_BK);
     const bool wide = N >= 256 && M * N >= (int64_t)148 * 128 * 256;
