@@ -180,41 +180,42 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
 }
 
 // Inverse of each 64 x 64 diagonal block of a unit lower triangular T:
-// row-by-row, row i of T^-1 = e_i - sum_{k<i} T[i][k] (row k of T^-1).
+// thread c computes column c of T^-1 by forward substitution (no barriers in
+// the solve; T is read as warp-broadcasts from shared memory).
 template <bool kSmall>
-__global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
-                                                 int64_t n, uint32_t* Tinv) {
+__global__ void __launch_bounds__(64) k_trinv64(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
+                                                int64_t n, uint32_t* Tinv) {
     __shared__ uint32_t Ts[64][65];
     __shared__ uint32_t X[64][65];
-    __shared__ uint64_t part[4][64];
     const int b = blockIdx.x;
     const int64_t i0 = (int64_t)b * 64;
     const int nb = (int)std::min<int64_t>(64, n - i0);
-    const int tid = threadIdx.x, c = tid & 63, qd = tid >> 6;
-    for (int e = tid; e < 64 * 64; e += 256) {
+    const int c = threadIdx.x;
+    for (int e = c; e < 64 * 64; e += 64) {
         const int i = e >> 6, k = e & 63;
         Ts[i][k] = (i < nb && k < i) ? T[(i0 + i) * ldt + i0 + k] : 0;
-        X[i][k] = 0;
     }
     __syncthreads();
-    for (int i = 0; i < nb; ++i) {
-        uint64_t acc = 0;
-        for (int k = qd; k < i; k += 4) {
-            const uint64_t prod = (uint64_t)Ts[i][k] * X[k][c];
-            acc += kSmall ? prod : (uint64_t)red64(f, prod);
+    const uint32_t one = 1 % f.p;
+    for (int i = 0; i < 64; ++i) {
+        uint32_t v;
+        if (i < c) {
+            v = 0;
+        } else if (i == c) {
+            v = one;
+        } else {
+            uint64_t acc = 0;
+            for (int k = c; k < i; ++k) {
+                const uint64_t prod = (uint64_t)Ts[i][k] * X[k][c];
+                acc += kSmall ? prod : (uint64_t)red64(f, prod);
+            }
+            v = fneg(f, red64(f, acc));
         }
-        part[qd][c] = acc;
-        __syncthreads();
-        if (qd == 0) {
-            const uint64_t sum = (uint64_t)red64(f, part[0][c]) + red64(f, part[1][c]) +
-                                 red64(f, part[2][c]) + red64(f, part[3][c]);
-            const uint32_t v = red64(f, sum);
-            X[i][c] = fsub(f, (c == i) ? 1 % f.p : 0, v);
-        }
-        __syncthreads();
+        X[i][c] = (i < nb && c < nb) ? v : 0;
     }
+    __syncthreads();
     uint32_t* o = Tinv + (int64_t)b * 64 * 64;
-    for (int e = tid; e < 64 * 64; e += 256) o[e] = X[e >> 6][e & 63];
+    for (int e = c; e < 64 * 64; e += 64) o[e] = X[e >> 6][e & 63];
 }
 
 // B[rows, c0:c0+64] <- Tinv (nb x nb) * B[rows, c0:c0+64], in place.
@@ -310,9 +311,9 @@ void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
     {
         ProfScope ps(K_TRSM, st, (double)n * 64 * 64 / 3, 8.0 * n * 64);
         if (f.p < (1u << 23))
-            k_trinv64<true><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+            k_trinv64<true><<<(unsigned)nblk, 64, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
         else
-            k_trinv64<false><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+            k_trinv64<false><<<(unsigned)nblk, 64, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
         ++g_launches;
         FFB_CHECK_LAUNCH();
     }

@@ -93,15 +93,25 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
     for (int e = tid; e < b * s; e += blockDim.x) Ss[e] = S[(int64_t)(e / s) * lds + e % s];
     if (tid == 0) rhs = s;
     __syncthreads();
+    __shared__ uint32_t cf[2][RD_MAX_B];  // S_i[rho_t], double-buffered by row parity
     int k = 0;
     for (int i = 0; i < b; ++i) {
         const uint32_t* si = Ss + (size_t)i * s;
+        uint32_t* c = cf[i & 1];
+        for (int t = tid; t < k; t += blockDim.x) c[t] = si[rho[t]];
+        __syncthreads();
         int nz = 0;
         for (int j = tid; j < s; j += blockDim.x) {
             uint64_t acc = 0;
-            for (int t = 0; t < k; ++t) {
-                acc += (uint64_t)si[rho[t]] * E[(size_t)t * s + j];
-                if ((t & 15) == 15 && f.p >= (1u << 26)) acc = red64(f, acc);
+            const uint32_t* ej = E + j;
+            int t = 0;
+            if (f.p < (1u << 26)) {
+                for (; t + 4 <= k; t += 4)
+                    acc += (uint64_t)c[t] * ej[(size_t)t * s] + (uint64_t)c[t + 1] * ej[(size_t)(t + 1) * s] +
+                           (uint64_t)c[t + 2] * ej[(size_t)(t + 2) * s] + (uint64_t)c[t + 3] * ej[(size_t)(t + 3) * s];
+                for (; t < k; ++t) acc += (uint64_t)c[t] * ej[(size_t)t * s];
+            } else {
+                for (; t < k; ++t) acc = red64(f, acc + (uint64_t)c[t] * ej[(size_t)t * s]);
             }
             const uint32_t x = fsub(f, si[j], red64(f, acc));
             v[j] = x;
@@ -176,6 +186,7 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
     extern __shared__ uint32_t sm[];
     uint32_t* E = sm;                           // basis: up to k vectors of length k
     uint32_t* V = E + (size_t)CRP_KMAX * k;     // CRP_G columns, each length k: V[c*k + i]
+    uint32_t* VC = V + (size_t)CRP_G * k;       // CRP_G x CRP_KMAX gathered coefficients
     __shared__ int rho[CRP_KMAX];
     __shared__ int colid[CRP_G];
     __shared__ int nb;
@@ -221,12 +232,19 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
         // reduce every column of the group against the current basis; flag the
         // columns that stay nonzero (candidates for a new basis vector)
         const int kb = nb;
+        for (int e = tid; e < gw * kb; e += blockDim.x) {  // coefficient gather
+            const int c = e / kb, t = e % kb;
+            VC[(size_t)c * CRP_KMAX + t] = V[(size_t)c * k + rho[t]];
+        }
+        __syncthreads();
         for (int e = tid; e < gw * k; e += blockDim.x) {
             const int c = e / k, i = e % k;
+            const uint32_t* vc = VC + (size_t)c * CRP_KMAX;
             uint64_t acc = 0;
-            for (int t = 0; t < kb; ++t) {
-                acc += (uint64_t)V[(size_t)c * k + rho[t]] * E[(size_t)t * k + i];
-                if ((t & 15) == 15 && f.p >= (1u << 26)) acc = red64(f, acc);
+            if (f.p < (1u << 26)) {
+                for (int t = 0; t < kb; ++t) acc += (uint64_t)vc[t] * E[(size_t)t * k + i];
+            } else {
+                for (int t = 0; t < kb; ++t) acc = red64(f, acc + (uint64_t)vc[t] * E[(size_t)t * k + i]);
             }
             if (fsub(f, V[(size_t)c * k + i], red64(f, acc)) != 0) atomicOr(&nzmask[c], 1);
         }
@@ -240,10 +258,13 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
             for (int c = 0; c < gw && nbl < k; ++c) {
                 if (!nzmask[c]) continue;
                 int lead_l = k;
+                uint32_t* vc = VC + (size_t)c * CRP_KMAX;
+                for (int t = lane; t < nbl; t += 32) vc[t] = V[(size_t)c * k + rho[t]];
+                __syncwarp();
                 for (int i = lane; i < k; i += 32) {
                     uint64_t acc = 0;
                     for (int t = 0; t < nbl; ++t) {
-                        acc += (uint64_t)V[(size_t)c * k + rho[t]] * E[(size_t)t * k + i];
+                        acc += (uint64_t)vc[t] * E[(size_t)t * k + i];
                         if ((t & 15) == 15 && f.p >= (1u << 26)) acc = red64(f, acc);
                     }
                     const uint32_t x = fsub(f, V[(size_t)c * k + i], red64(f, acc));
@@ -553,7 +574,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     const size_t mark1 = ws.mark();
 
     const size_t rd_smem = ((size_t)2 * RD_MAX_B * SK + SK) * 4;
-    const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + (size_t)CRP_G * CRP_KMAX) * 4;
+    const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + 2 * (size_t)CRP_G * CRP_KMAX) * 4;
     static bool attrs = false;
     if (!attrs) {
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
