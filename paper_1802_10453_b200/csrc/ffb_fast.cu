@@ -41,12 +41,11 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
                                                 uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
                                                 int32_t* out) {
     __shared__ uint32_t Ls[64][65];
-    __shared__ uint32_t col1[64], col2[64];
-    __shared__ uint32_t l1v[64], l2v[64], u1v[64], u2v[64];
+    __shared__ uint32_t colb[2][64];  // residual column of the front row, double-buffered
+    __shared__ uint32_t col2[64];     // residual column of the 2x2 partner
     __shared__ int32_t order[64];
-    __shared__ int jsel;
     const Ar<kSmall> ar(f);
-    const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6;
+    const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6, lane = tid & 31;
     const uint32_t one = 1 % f.p;
     uint32_t S[16];
 #pragma unroll
@@ -56,58 +55,47 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
     }
     for (int e = tid; e < 64 * 65; e += 256) (&Ls[0][0])[e] = 0;
     uint64_t active = (s == 64) ? ~0ull : ((1ull << s) - 1);
-    int r = 0, npl = 0;
+    int r = 0, npl = 0, buf = 0;
     __syncthreads();
     for (int p1 = 0; p1 < s; ++p1) {
         if (!((active >> p1) & 1)) continue;  // consumed as a 2x2 partner (uniform)
+        uint32_t* col1 = colb[buf];
+        buf ^= 1;
         if (tx == p1) {
 #pragma unroll
             for (int q = 0; q < 16; ++q) col1[ty + 4 * q] = S[q];
         }
         __syncthreads();
-        if (tid < 32) {
-            const uint32_t b0 = __ballot_sync(0xffffffffu, col1[tid] != 0);
-            const uint32_t b1 = __ballot_sync(0xffffffffu, col1[tid + 32] != 0);
-            if (tid == 0) {
-                const uint64_t m = (((uint64_t)b1 << 32) | b0) & active;
-                jsel = m ? __ffsll((long long)m) - 1 : s;
-            }
-        }
-        __syncthreads();
-        const int j = jsel;
-        if (j >= s) {  // zero residual column: pivotless (sytrf.cpp:82-85)
+        // every warp finds the first active row with a nonzero residual (sytrf.cpp:78-81)
+        const uint32_t b0 = __ballot_sync(0xffffffffu, col1[lane] != 0);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, col1[lane + 32] != 0);
+        const uint64_t msk = (((uint64_t)b1 << 32) | b0) & active;
+        const int j = msk ? __ffsll((long long)msk) - 1 : s;
+        if (j >= s) {  // pivotless (sytrf.cpp:82-85)
             if (tid == 0) out[1 + (s - 1 - npl)] = p1;
             ++npl;
             active &= ~(1ull << p1);
-            continue;  // col1/jsel are rewritten only after the next barrier
+            continue;
         }
         if (j == p1) {  // 1x1 pivot (sytrf.cpp:87-97)
             const uint32_t x = col1[p1];
             const uint32_t xi = finv(f, x);
-            if (tid < 64) {
-                const int i = tid;
-                uint32_t l = 0;
-                if (((active >> i) & 1) && i != p1) {
-                    l = ar.mul(col1[i], xi);
-                    Ls[i][r] = l;
-                }
-                l1v[i] = l;
+            active &= ~(1ull << p1);
+            const uint32_t lk = ar.mul(col1[tx], xi);  // multiplier of this thread's column
+#pragma unroll
+            for (int q = 0; q < 16; ++q) S[q] = ar.sub(S[q], ar.mul(col1[ty + 4 * q], lk));
+            if (ty == 0) {
+                if (tx == p1) Ls[p1][r] = one;
+                else if ((active >> tx) & 1) Ls[tx][r] = lk;
             }
             if (tid == 0) {
-                Ls[p1][r] = one;
                 D.kind[coff + r] = D_SCALAR;
                 D.val[coff + r] = x;
                 D.val2[coff + r] = 0;
                 D.inv[coff + r] = xi;
                 order[r] = p1;
             }
-            __syncthreads();
-            const uint32_t lk = l1v[tx];
-#pragma unroll
-            for (int q = 0; q < 16; ++q) S[q] = ar.sub(S[q], ar.mul(col1[ty + 4 * q], lk));
-            active &= ~(1ull << p1);
             r += 1;
-            __syncthreads();
             continue;
         }
         // 2x2 antidiagonal pivot pairing p1 with p2 = j (sytrf.cpp:99-131)
@@ -123,19 +111,28 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
         const uint32_t y_eff = f.char2 ? y : fhalve(f, y);
         const uint32_t yd = f.char2 ? y : 0;
         active &= ~((1ull << p1) | (1ull << p2));
-        if (tid < 64) {
-            const int i = tid;
-            uint32_t l1 = 0, l2 = 0;
-            if ((active >> i) & 1) {
-                l2 = ar.mul(xi, col1[i]);
-                l1 = ar.mul(xi, ar.sub(col2[i], ar.mul(y_eff, l2)));
-                Ls[i][r] = l1;
-                Ls[i][r + 1] = l2;
+        // multipliers of this thread's column k = tx
+        const uint32_t l2k = ar.mul(xi, col1[tx]);
+        const uint32_t l1k = ar.mul(xi, ar.sub(col2[tx], ar.mul(y_eff, l2k)));
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int i = ty + 4 * q;
+            const uint32_t l2i = ar.mul(xi, col1[i]);
+            const uint32_t l1i = ar.mul(xi, ar.sub(col2[i], ar.mul(y_eff, l2i)));
+            uint32_t v = ar.add(ar.mul(ar.mul(x, l1i), l2k), ar.mul(ar.mul(x, l2i), l1k));
+            if (yd) v = ar.add(v, ar.mul(ar.mul(yd, l2i), l2k));
+            S[q] = ar.sub(S[q], v);
+        }
+        if (ty == 0) {
+            if (tx == p1) {
+                Ls[p1][r] = one;
+            } else if (tx == p2) {
+                Ls[p2][r + 1] = one;
+                Ls[p2][r] = f.char2 ? 0 : ar.mul(xi, y_eff);
+            } else if ((active >> tx) & 1) {
+                Ls[tx][r] = l1k;
+                Ls[tx][r + 1] = l2k;
             }
-            l1v[i] = l1;
-            l2v[i] = l2;
-            u1v[i] = ar.mul(x, l1);
-            u2v[i] = ar.mul(x, l2);
         }
         if (tid == 0) {
             const int32_t hk = yd ? D_ANTITRI_HEAD : D_ANTIDIAG_HEAD;
@@ -144,24 +141,12 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
             D.val[coff + r] = D.val[coff + r + 1] = x;
             D.val2[coff + r] = D.val2[coff + r + 1] = yd;
             D.inv[coff + r] = D.inv[coff + r + 1] = xi;
-            Ls[p1][r] = one;
-            Ls[p2][r + 1] = one;
-            Ls[p2][r] = f.char2 ? 0 : ar.mul(xi, y_eff);
             order[r] = p1;
             order[r + 1] = p2;
         }
-        __syncthreads();
-        const uint32_t l1k = l1v[tx], l2k = l2v[tx];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const int i = ty + 4 * q;
-            uint32_t v = ar.add(ar.mul(u1v[i], l2k), ar.mul(u2v[i], l1k));
-            if (yd) v = ar.add(v, ar.mul(ar.mul(yd, l2v[i]), l2k));
-            S[q] = ar.sub(S[q], v);
-        }
         r += 2;
-        __syncthreads();
     }
+    __syncthreads();
     // L columns [coff, coff + r) of the leaf rows, one coalesced row write each
     for (int e = tid; e < s * r; e += 256) {
         const int i = e / r, c = e % r;
@@ -170,8 +155,7 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
     if (tid == 0) {
         out[0] = r;
         for (int t = 0; t < r; ++t) out[1 + t] = order[t];
-        // pivotless rows were stored from the back: reverse into ascending order
-        for (int a = 0, b = npl - 1; a < b; ++a, --b) {
+        for (int a = 0, b = npl - 1; a < b; ++a, --b) {  // pivotless rows: ascending
             const int32_t tmp = out[1 + r + a];
             out[1 + r + a] = out[1 + r + b];
             out[1 + r + b] = tmp;

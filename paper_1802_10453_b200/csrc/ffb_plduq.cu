@@ -439,30 +439,48 @@ __global__ void k_m1_pattern(const uint32_t* M1, int64_t ldm, const int32_t* np,
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_ldu_base(Fp f, uint32_t* K, int64_t ldk, int n,
                                                   int32_t* fail) {
-    __shared__ uint32_t A[64][65];
-    __shared__ uint32_t il;
-    const int tid = threadIdx.x;
-    for (int e = tid; e < n * n; e += blockDim.x) A[e / n][e % n] = K[(int64_t)(e / n) * ldk + e % n];
-    __syncthreads();
-    for (int t = 0; t < n; ++t) {
-        if (tid == 0) {
-            if (A[t][t] == 0) *fail = 1;
-            il = A[t][t] ? finv(f, A[t][t]) : 0;
-        }
-        __syncthreads();
-        const int w = n - t - 1;
-        for (int e = tid; e < w * w; e += blockDim.x) {
-            const int i = t + 1 + e / w, j = t + 1 + e % w;
-            A[i][j] = fsub(f, A[i][j], fmul(f, fmul(f, A[i][t], il), A[t][j]));
-        }
-        __syncthreads();
-        for (int i = t + 1 + tid; i < n; i += blockDim.x) {
-            A[i][t] = fmul(f, A[i][t], il);  // L
-            A[t][i] = fmul(f, A[t][i], il);  // U
-        }
-        __syncthreads();
+    // Register ownership as in the leaf: thread (ty, tx) holds K[ty + 4q][tx].
+    // Step t broadcasts column t and row t (double-buffered) with one barrier.
+    __shared__ uint32_t colb[2][64], rowb[2][64];
+    const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6;
+    uint32_t A[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int i = ty + 4 * q;
+        A[q] = (i < n && tx < n) ? K[(int64_t)i * ldk + tx] : 0;
     }
-    for (int e = tid; e < n * n; e += blockDim.x) K[(int64_t)(e / n) * ldk + e % n] = A[e / n][e % n];
+    for (int t = 0; t < n; ++t) {
+        uint32_t* cb = colb[t & 1];
+        uint32_t* rb = rowb[t & 1];
+        if (tx == t) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) cb[ty + 4 * q] = A[q];
+        }
+        if (ty == (t & 3)) rb[tx] = A[t >> 2];
+        __syncthreads();
+        const uint32_t d = cb[t];
+        if (d == 0) {
+            if (tid == 0) *fail = 1;
+            return;  // uniform
+        }
+        const uint32_t di = finv(f, d);
+        const uint32_t uj = fmul(f, rb[tx], di);  // U[t][tx] for tx > t
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int i = ty + 4 * q;
+            if (i > t) {
+                if (tx > t) A[q] = fsub(f, A[q], fmul(f, cb[i], uj));
+                else if (tx == t) A[q] = fmul(f, cb[i], di);  // L[i][t]
+            } else if (i == t && tx > t) {
+                A[q] = uj;  // U[t][tx]
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+        const int i = ty + 4 * q;
+        if (i < n && tx < n) K[(int64_t)i * ldk + tx] = A[q];
+    }
 }
 
 // L (unit lower with zeros above) from the packed LDU block; d from the diagonal.
