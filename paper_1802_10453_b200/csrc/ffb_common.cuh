@@ -91,6 +91,44 @@ __device__ inline uint32_t finv(const Fp& f, uint32_t a) {
     return finv_euclid(f.p, a);
 }
 
+// Inverse-table staging for latency-critical single-CTA kernels: for small p
+// the table is copied to shared memory once (batched read-only loads), so an
+// inverse on the critical path is a shared-memory lookup, not an L2 round trip.
+constexpr int SINV_MAX = 4096;
+struct SmemInv {
+    const uint32_t* t;  // shared copy, or nullptr
+    __device__ __forceinline__ uint32_t operator()(const Fp& f, uint32_t a) const {
+        return t ? t[a] : finv(f, a);
+    }
+};
+__device__ inline SmemInv stage_inverses(const Fp& f, uint32_t* buf /* SINV_MAX words */) {
+    if (!f.inv || f.p > SINV_MAX) return SmemInv{nullptr};
+    for (uint32_t a = threadIdx.x; a < f.p; a += blockDim.x) buf[a] = __ldg(f.inv + a);
+    __syncthreads();
+    return SmemInv{buf};
+}
+
+// Batched read-only copy global -> shared of a rows x cols tile (row stride lds),
+// with U independent loads in flight per thread.
+template <int U>
+__device__ __forceinline__ void load_tile(uint32_t* dst, int ldd, const uint32_t* __restrict__ src,
+                                          int64_t lds, int rows, int cols) {
+    const int total = rows * cols, nt = blockDim.x;
+    for (int base = threadIdx.x; base < total; base += U * nt) {
+        uint32_t v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = base + u * nt;
+            v[u] = e < total ? __ldg(src + (int64_t)(e / cols) * lds + (e % cols)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int e = base + u * nt;
+            if (e < total) dst[(e / cols) * ldd + (e % cols)] = v[u];
+        }
+    }
+}
+
 // ---------------------------------------------------------------------------
 // Strided row-major views of device matrices.
 // ---------------------------------------------------------------------------

@@ -44,6 +44,7 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
     __shared__ uint32_t colb[2][64];  // residual column of the front row, double-buffered
     __shared__ uint32_t col2[64];     // residual column of the 2x2 partner
     __shared__ int32_t order[64];
+    __shared__ uint32_t sinv[SINV_MAX];
     const Ar<kSmall> ar(f);
     const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6, lane = tid & 31;
     const uint32_t one = 1 % f.p;
@@ -51,9 +52,10 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
         const int i = ty + 4 * q;
-        S[q] = (i < s && tx < s) ? A[(int64_t)i * lda + tx] : 0;
+        S[q] = (i < s && tx < s) ? __ldg(A + (int64_t)i * lda + tx) : 0;
     }
     for (int e = tid; e < 64 * 65; e += 256) (&Ls[0][0])[e] = 0;
+    const SmemInv inv = stage_inverses(f, sinv);
     uint64_t active = (s == 64) ? ~0ull : ((1ull << s) - 1);
     int r = 0, npl = 0, buf = 0;
     __syncthreads();
@@ -79,7 +81,7 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
         }
         if (j == p1) {  // 1x1 pivot (sytrf.cpp:87-97)
             const uint32_t x = col1[p1];
-            const uint32_t xi = finv(f, x);
+            const uint32_t xi = inv(f, x);
             active &= ~(1ull << p1);
             const uint32_t lk = ar.mul(col1[tx], xi);  // multiplier of this thread's column
 #pragma unroll
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
         }
         __syncthreads();
         const uint32_t x = col1[p2];
-        const uint32_t xi = finv(f, x);
+        const uint32_t xi = inv(f, x);
         const uint32_t y = col2[p2];
         const uint32_t y_eff = f.char2 ? y : fhalve(f, y);
         const uint32_t yd = f.char2 ? y : 0;
@@ -175,9 +177,11 @@ __global__ void __launch_bounds__(64) k_trinv64(Fp f, const uint32_t* __restrict
     const int64_t i0 = (int64_t)b * 64;
     const int nb = (int)std::min<int64_t>(64, n - i0);
     const int c = threadIdx.x;
-    for (int e = c; e < 64 * 64; e += 64) {
+    load_tile<16>(&Ts[0][0], 65, T + i0 * ldt + i0, ldt, nb, nb);
+    __syncthreads();
+    for (int e = c; e < 64 * 64; e += 64) {  // strict lower part only
         const int i = e >> 6, k = e & 63;
-        Ts[i][k] = (i < nb && k < i) ? T[(i0 + i) * ldt + i0 + k] : 0;
+        if (i >= nb || k >= i) Ts[i][k] = 0;
     }
     __syncthreads();
     const uint32_t one = 1 % f.p;
@@ -211,12 +215,9 @@ __global__ void __launch_bounds__(256) k_trsm_apply64(Fp f, const uint32_t* __re
     __shared__ uint32_t Bs[64][65];
     const int tid = threadIdx.x, c = tid & 63, rg = tid >> 6;
     const int64_t c0 = (int64_t)blockIdx.x * 64;
-    for (int e = tid; e < 64 * 64; e += 256) {
-        const int i = e >> 6, k = e & 63;
-        Ts[i][k] = Tinv[e];
-        const int64_t col = c0 + k;
-        Bs[i][k] = (i < nb && col < ncols) ? B[(int64_t)i * ldb + col] : 0;
-    }
+    const int bc = (int)std::min<int64_t>(64, ncols - c0);
+    load_tile<8>(&Ts[0][0], 65, Tinv, 64, 64, 64);
+    load_tile<8>(&Bs[0][0], 65, B + c0, ldb, nb, bc);
     __syncthreads();
     const int64_t col = c0 + c;
     for (int i = rg; i < nb; i += 4) {

@@ -89,9 +89,11 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
     __shared__ uint32_t coef[RD_MAX_B];
     __shared__ int rhs;
     __shared__ uint32_t ils;
+    __shared__ uint32_t sinv[SINV_MAX];
     const int tid = threadIdx.x;
-    for (int e = tid; e < b * s; e += blockDim.x) Ss[e] = S[(int64_t)(e / s) * lds + e % s];
+    load_tile<8>(Ss, s, S, lds, b, s);
     if (tid == 0) rhs = s;
+    const SmemInv inv = stage_inverses(f, sinv);
     __syncthreads();
     __shared__ uint32_t cf[2][RD_MAX_B];  // S_i[rho_t], double-buffered by row parity
     int k = 0;
@@ -122,7 +124,7 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
             if (v[j]) atomicMin(&rhs, j);
         __syncthreads();
         const int rh = rhs;
-        if (tid == 0) ils = finv(f, v[rh]);
+        if (tid == 0) ils = inv(f, v[rh]);
         __syncthreads();
         const uint32_t il = ils;
         for (int j = tid; j < s; j += blockDim.x) v[j] = fmul(f, v[j], il);
@@ -194,8 +196,10 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
     __shared__ int total;
     __shared__ uint32_t vr[CRP_KMAX];
     __shared__ uint32_t coefs[CRP_KMAX];
+    __shared__ uint32_t sinv[SINV_MAX];
     const int tid = threadIdx.x;
     const int g = blockIdx.x;
+    const SmemInv inv = stage_inverses(f, sinv);
     // the ordered column set of this CTA
     auto column_at = [&](int idx) -> int {
         if (!in) return g * CRP_W + idx;
@@ -224,9 +228,18 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
         if (tid < gw) colid[tid] = column_at(s0 + tid);
         if (tid < CRP_G) nzmask[tid] = 0;
         __syncthreads();
-        for (int e = tid; e < gw * k; e += blockDim.x) {
-            const int c = e % gw, i = e / gw;
-            V[(size_t)c * k + i] = RI[(int64_t)i * ldr + colid[c]];
+        for (int base = tid; base < gw * k; base += 4 * blockDim.x) {  // 4 loads in flight
+            uint32_t vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = base + u * blockDim.x;
+                vv[u] = e < gw * k ? __ldg(RI + (int64_t)(e / gw) * ldr + colid[e % gw]) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = base + u * blockDim.x;
+                if (e < gw * k) V[(size_t)(e % gw) * k + e / gw] = vv[u];
+            }
         }
         __syncthreads();
         // reduce every column of the group against the current basis; flag the
@@ -275,7 +288,7 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
                 __syncwarp();
                 if (lead_l >= k) continue;
                 const int ld = lead_l;
-                const uint32_t ilv = finv(f, vr[ld]);
+                const uint32_t ilv = inv(f, vr[ld]);
                 for (int i = lane; i < k; i += 32) vr[i] = fmul(f, vr[i], ilv);
                 for (int t = lane; t < nbl; t += 32) coefs[t] = E[(size_t)t * k + ld];
                 __syncwarp();
@@ -319,10 +332,12 @@ __global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t
     __shared__ int sig[CRP_KMAX];
     __shared__ int lead;
     __shared__ uint32_t il;
+    __shared__ uint32_t sinv[SINV_MAX];
     const int tid = threadIdx.x;
+    const SmemInv inv = stage_inverses(f, sinv);
     for (int e = tid; e < k * k; e += blockDim.x) {
         const int i = e / k, j = e % k;
-        const uint32_t v = RI[(int64_t)i * ldr + J[j]];
+        const uint32_t v = __ldg(RI + (int64_t)i * ldr + J[j]);
         A[e] = v;
         G[(size_t)i * 2 * k + j] = v;
         G[(size_t)i * 2 * k + k + j] = (i == j) ? 1 % f.p : 0;
@@ -343,7 +358,7 @@ __global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t
         if (tid == 0) {
             sig[t] = jp;
             colused[jp] = 1;
-            il = finv(f, A[(size_t)t * k + jp]);
+            il = inv(f, A[(size_t)t * k + jp]);
         }
         __syncthreads();
         for (int e = tid; e < (k - t - 1) * k; e += blockDim.x) {
@@ -375,7 +390,7 @@ __global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t
                 G[(size_t)pr * w + j] = tmp;
             }
         __syncthreads();
-        if (tid == 0) il = finv(f, G[(size_t)c * w + c]);
+        if (tid == 0) il = inv(f, G[(size_t)c * w + c]);
         __syncthreads();
         for (int j = tid; j < w; j += blockDim.x) G[(size_t)c * w + j] = fmul(f, G[(size_t)c * w + j], il);
         __syncthreads();
@@ -442,6 +457,7 @@ __global__ void __launch_bounds__(256) k_ldu_base(Fp f, uint32_t* K, int64_t ldk
     // Register ownership as in the leaf: thread (ty, tx) holds K[ty + 4q][tx].
     // Step t broadcasts column t and row t (double-buffered) with one barrier.
     __shared__ uint32_t colb[2][64], rowb[2][64];
+    __shared__ uint32_t sinv[SINV_MAX];
     const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6;
     uint32_t A[16];
 #pragma unroll
@@ -449,6 +465,7 @@ __global__ void __launch_bounds__(256) k_ldu_base(Fp f, uint32_t* K, int64_t ldk
         const int i = ty + 4 * q;
         A[q] = (i < n && tx < n) ? K[(int64_t)i * ldk + tx] : 0;
     }
+    const SmemInv inv = stage_inverses(f, sinv);
     for (int t = 0; t < n; ++t) {
         uint32_t* cb = colb[t & 1];
         uint32_t* rb = rowb[t & 1];
@@ -463,7 +480,7 @@ __global__ void __launch_bounds__(256) k_ldu_base(Fp f, uint32_t* K, int64_t ldk
             if (tid == 0) *fail = 1;
             return;  // uniform
         }
-        const uint32_t di = finv(f, d);
+        const uint32_t di = inv(f, d);
         const uint32_t uj = fmul(f, rb[tx], di);  // U[t][tx] for tx > t
 #pragma unroll
         for (int q = 0; q < 16; ++q) {

@@ -612,7 +612,7 @@ void launch_tc(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, DM
 bool tc_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K) {
     static const bool disabled = getenv("FFB_DISABLE_TC") != nullptr;
     if (disabled) return false;
-    const bool shape = M >= 64 && N >= 64 && K >= 16 && (double)M * N * K >= 2.0e7 &&
+    const bool shape = M >= 64 && N >= 64 && K >= 16 && (double)M * N * K >= 1.0e6 &&
                        M < (1ll << 30) && N < (1ll << 30);
     if (f.p <= 255) return shape && K <= 120000;
     return f.p < (1u << 23) && shape && K <= 40000;  // int8 limbs: 3 * 2^14 * K < 2^31
