@@ -165,68 +165,101 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
     }
 }
 
-// Inverse of each 64 x 64 diagonal block of a unit lower triangular T:
-// thread c computes column c of T^-1 by forward substitution (no barriers in
-// the solve; T is read as warp-broadcasts from shared memory).
+// Inverse of each 64 x 64 diagonal block of a unit lower triangular T,
+// row by row: row i of T^-1 = e_i - sum_{k<i} T[i][k] (row k of T^-1);
+// 4 threads per column split the k-sum.
 template <bool kSmall>
-__global__ void __launch_bounds__(64) k_trinv64(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
-                                                int64_t n, uint32_t* Tinv) {
+__global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
+                                                 int64_t n, uint32_t* Tinv) {
     __shared__ uint32_t Ts[64][65];
     __shared__ uint32_t X[64][65];
+    __shared__ uint64_t part[4][64];
     const int b = blockIdx.x;
     const int64_t i0 = (int64_t)b * 64;
     const int nb = (int)std::min<int64_t>(64, n - i0);
-    const int c = threadIdx.x;
+    const int tid = threadIdx.x, c = tid & 63, qd = tid >> 6;
     load_tile<16>(&Ts[0][0], 65, T + i0 * ldt + i0, ldt, nb, nb);
     __syncthreads();
-    for (int e = c; e < 64 * 64; e += 64) {  // strict lower part only
+    for (int e = tid; e < 64 * 64; e += 256) {
         const int i = e >> 6, k = e & 63;
         if (i >= nb || k >= i) Ts[i][k] = 0;
+        X[i][k] = 0;
     }
     __syncthreads();
-    const uint32_t one = 1 % f.p;
-    for (int i = 0; i < 64; ++i) {
-        uint32_t v;
-        if (i < c) {
-            v = 0;
-        } else if (i == c) {
-            v = one;
-        } else {
-            uint64_t acc = 0;
-            for (int k = c; k < i; ++k) {
-                const uint64_t prod = (uint64_t)Ts[i][k] * X[k][c];
-                acc += kSmall ? prod : (uint64_t)red64(f, prod);
-            }
-            v = fneg(f, red64(f, acc));
-        }
-        X[i][c] = (i < nb && c < nb) ? v : 0;
-    }
-    __syncthreads();
-    uint32_t* o = Tinv + (int64_t)b * 64 * 64;
-    for (int e = c; e < 64 * 64; e += 64) o[e] = X[e >> 6][e & 63];
-}
-
-// B[rows, c0:c0+64] <- Tinv (nb x nb) * B[rows, c0:c0+64], in place.
-template <bool kSmall>
-__global__ void __launch_bounds__(256) k_trsm_apply64(Fp f, const uint32_t* __restrict__ Tinv,
-                                                      uint32_t* B, int64_t ldb, int nb,
-                                                      int64_t ncols) {
-    __shared__ uint32_t Ts[64][65];
-    __shared__ uint32_t Bs[64][65];
-    const int tid = threadIdx.x, c = tid & 63, rg = tid >> 6;
-    const int64_t c0 = (int64_t)blockIdx.x * 64;
-    const int bc = (int)std::min<int64_t>(64, ncols - c0);
-    load_tile<8>(&Ts[0][0], 65, Tinv, 64, 64, 64);
-    load_tile<8>(&Bs[0][0], 65, B + c0, ldb, nb, bc);
-    __syncthreads();
-    const int64_t col = c0 + c;
-    for (int i = rg; i < nb; i += 4) {
+    for (int i = 0; i < nb; ++i) {
         uint64_t acc = 0;
-        for (int k = 0; k <= i; ++k) {
-            const uint64_t prod = (uint64_t)Ts[i][k] * Bs[k][c];
+        for (int k = qd; k < i; k += 4) {
+            const uint64_t prod = (uint64_t)Ts[i][k] * X[k][c];
             acc += kSmall ? prod : (uint64_t)red64(f, prod);
         }
-        if (col < ncols) B[(int64_t)i * ldb + col] = red64(f, acc);
+        part[qd][c] = acc;
+        __syncthreads();
+        if (qd == 0) {
+            const uint64_t sum = (uint64_t)red64(f, part[0][c]) + red64(f, part[1][c]) +
+                                 red64(f, part[2][c]) + red64(f, part[3][c]);
+            X[i][c] = fsub(f, (c == i) ? 1 % f.p : 0, red64(f, sum));
+        }
+        __syncthreads();
+    }
+    uint32_t* o = Tinv + (int64_t)b * 64 * 64;
+    for (int e = tid; e < 64 * 64; e += 256) o[e] = X[e >> 6][e & 63];
+}
+
+// Panel solve: rows [r0, r0 + nb) (nb <= 256, 64-aligned r0), column tile of
+// 32: x_b = Tinv_b (b_b - sum_{c<b} T_{bc} x_c) block by block, in place.
+// The four diagonal inverses and the strictly lower 64x64 couplings are read
+// from L2 per tile (they are shared by all column tiles).
+constexpr int PNL_COLS = 32;
+template <bool kSmall>
+__global__ void __launch_bounds__(256) k_trsm_panel(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
+                                                    const uint32_t* __restrict__ Tinv, uint32_t* B,
+                                                    int64_t ldb, int nb, int64_t ncols) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* Xs = sm;                     // 256 x (PNL_COLS+1)
+    uint32_t* Ms = Xs + 256 * (PNL_COLS + 1);  // one 64 x 65 matrix block
+    const int tid = threadIdx.x;
+    const int64_t c0 = (int64_t)blockIdx.x * PNL_COLS;
+    const int bc = (int)std::min<int64_t>(PNL_COLS, ncols - c0);
+    load_tile<8>(Xs, PNL_COLS + 1, B + c0, ldb, nb, bc);
+    const int nblk = (nb + 63) / 64;
+    const int col = tid & 31, rg = tid >> 5;  // 8 row groups of 8 rows
+    for (int bi = 0; bi < nblk; ++bi) {
+        const int rb = bi * 64, rows = std::min(64, nb - rb);
+        // b_bi -= T_{bi,bj} x_bj for bj < bi
+        for (int bj = 0; bj < bi; ++bj) {
+            __syncthreads();
+            load_tile<16>(Ms, 65, T + (int64_t)rb * ldt + bj * 64, ldt, rows, 64);
+            __syncthreads();
+            for (int r = rg; r < rows; r += 8) {
+                uint64_t acc = 0;
+                for (int k = 0; k < 64; ++k) {
+                    const uint64_t prod = (uint64_t)Ms[r * 65 + k] * Xs[(bj * 64 + k) * (PNL_COLS + 1) + col];
+                    acc += kSmall ? prod : (uint64_t)red64(f, prod);
+                }
+                uint32_t* x = &Xs[(rb + r) * (PNL_COLS + 1) + col];
+                *x = fsub(f, *x, red64(f, acc));
+            }
+        }
+        // x_bi = Tinv_bi b_bi
+        __syncthreads();
+        load_tile<16>(Ms, 65, Tinv + (int64_t)(rb / 64) * 64 * 64, 64, 64, 64);
+        __syncthreads();
+        uint32_t outv[8];
+        for (int t = 0, r = rg; r < rows; r += 8, ++t) {
+            uint64_t acc = 0;
+            for (int k = 0; k <= r; ++k) {
+                const uint64_t prod = (uint64_t)Ms[r * 65 + k] * Xs[(rb + k) * (PNL_COLS + 1) + col];
+                acc += kSmall ? prod : (uint64_t)red64(f, prod);
+            }
+            outv[t] = red64(f, acc);
+        }
+        __syncthreads();
+        for (int t = 0, r = rg; r < rows; r += 8, ++t) Xs[(rb + r) * (PNL_COLS + 1) + col] = outv[t];
+    }
+    __syncthreads();
+    for (int e = tid; e < nb * bc; e += 256) {
+        const int r = e / bc, cc = e % bc;
+        B[(int64_t)r * ldb + c0 + cc] = Xs[r * (PNL_COLS + 1) + cc];
     }
 }
 
@@ -251,20 +284,27 @@ uint32_t* trsm_scratch(size_t words) {
 
 void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tinv, int64_t i0) {
     const int64_t n = T.rows;
-    if (n <= 64) {
+    if (n <= 256) {
         ProfScope ps(K_TRSM, st, 2.0 * n * n * B.cols / 2, 8.0 * n * B.cols);
         const uint32_t* ti = Tinv + (i0 / 64) * 64 * 64;
-        dim3 grid((unsigned)cdiv(B.cols, 64));
-        if (f.p < (1u << 16) || f.p < (1u << 23))
-            k_trsm_apply64<true><<<grid, 256, 0, st>>>(f, ti, B.ptr, B.ld, (int)n, B.cols);
+        const size_t smem = (size_t)(256 * (PNL_COLS + 1) + 64 * 65) * 4;
+        static bool attr = false;
+        if (!attr) {
+            FFB_CUDA(cudaFuncSetAttribute(k_trsm_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            FFB_CUDA(cudaFuncSetAttribute(k_trsm_panel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = true;
+        }
+        dim3 grid((unsigned)cdiv(B.cols, PNL_COLS));
+        if (f.p < (1u << 23))
+            k_trsm_panel<true><<<grid, 256, smem, st>>>(f, T.ptr, T.ld, ti, B.ptr, B.ld, (int)n, B.cols);
         else
-            k_trsm_apply64<false><<<grid, 256, 0, st>>>(f, ti, B.ptr, B.ld, (int)n, B.cols);
+            k_trsm_panel<false><<<grid, 256, smem, st>>>(f, T.ptr, T.ld, ti, B.ptr, B.ld, (int)n, B.cols);
         ++g_launches;
         FFB_CHECK_LAUNCH();
         return;
     }
-    int64_t n1 = (n / 2) / 64 * 64;
-    if (n1 < 64) n1 = 64;
+    int64_t n1 = (n / 2) / 256 * 256;
+    if (n1 < 256) n1 = 256;
     const int64_t n2 = n - n1;
     DMat B1 = B.sub(0, 0, n1, B.cols), B2 = B.sub(n1, 0, n2, B.cols);
     solve_rec(f, st, T.sub(0, 0, n1, n1), B1, Tinv, i0);
@@ -296,9 +336,9 @@ void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
     {
         ProfScope ps(K_TRSM, st, (double)n * 64 * 64 / 3, 8.0 * n * 64);
         if (f.p < (1u << 23))
-            k_trinv64<true><<<(unsigned)nblk, 64, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+            k_trinv64<true><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
         else
-            k_trinv64<false><<<(unsigned)nblk, 64, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+            k_trinv64<false><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
         ++g_launches;
         FFB_CHECK_LAUNCH();
     }

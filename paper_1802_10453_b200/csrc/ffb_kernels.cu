@@ -82,32 +82,47 @@ __global__ void __launch_bounds__(256) k_gemm_simt(Fp f, int mode, uint32_t* __r
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0;
 
-    for (int64_t k0 = 0; k0 < K; k0 += GB_K) {
-        // A tile: (i, k) -> op(A)[m0+i][k0+k]
-        for (int e = threadIdx.x; e < GB_M * GB_K; e += 256) {
-            int i, k;
-            if (TA) { i = e % GB_M; k = e / GB_M; } else { k = e % GB_K; i = e / GB_K; }
-            const int64_t gi = m0 + i, gk = k0 + k;
-            uint32_t v = 0;
-            if (gi < M && gk < K) v = TA ? A[gk * lda + gi] : A[gi * lda + gk];
-            As[k][i] = v;
-        }
-        for (int e = threadIdx.x; e < GB_N * GB_K; e += 256) {
-            int j, k;
-            if (TB) { k = e % GB_K; j = e / GB_K; } else { j = e % GB_N; k = e / GB_N; }
-            const int64_t gj = n0 + j, gk = k0 + k;
-            uint32_t v = 0;
-            if (gj < N && gk < K) v = TB ? B[gj * ldb + gk] : B[gk * ldb + gj];
-            Bs[k][j] = v;
-        }
-        __syncthreads();
+    // Each thread moves 4 A and 4 B elements per K tile; the next tile is
+    // prefetched into registers while the current one is consumed.
+    uint32_t ra[4], rb[4];
+    auto fetch = [&](int64_t k0) {
 #pragma unroll
-        for (int k = 0; k < GB_K; ++k) {
+        for (int u = 0; u < 4; ++u) {
+            const int e = threadIdx.x + 256 * u;
+            int i, kk;
+            if (TA) { i = e % GB_M; kk = e / GB_M; } else { kk = e % GB_K; i = e / GB_K; }
+            const int64_t gi = m0 + i, gk = k0 + kk;
+            ra[u] = (gi < M && gk < K) ? __ldg(TA ? A + gk * lda + gi : A + gi * lda + gk) : 0u;
+            int j, kb;
+            if (TB) { kb = e % GB_K; j = e / GB_K; } else { j = e % GB_N; kb = e / GB_N; }
+            const int64_t gj = n0 + j, gkb = k0 + kb;
+            rb[u] = (gj < N && gkb < K) ? __ldg(TB ? B + gj * ldb + gkb : B + gkb * ldb + gj) : 0u;
+        }
+    };
+    auto stash = [&]() {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = threadIdx.x + 256 * u;
+            int i, kk;
+            if (TA) { i = e % GB_M; kk = e / GB_M; } else { kk = e % GB_K; i = e / GB_K; }
+            As[kk][i] = ra[u];
+            int j, kb;
+            if (TB) { kb = e % GB_K; j = e / GB_K; } else { j = e % GB_N; kb = e / GB_N; }
+            Bs[kb][j] = rb[u];
+        }
+    };
+    fetch(0);
+    for (int64_t k0 = 0; k0 < K; k0 += GB_K) {
+        stash();
+        __syncthreads();
+        if (k0 + GB_K < K) fetch(k0 + GB_K);
+#pragma unroll
+        for (int kk = 0; kk < GB_K; ++kk) {
             uint32_t a[4], b[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = As[k][ty + 16 * i];
+            for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = Bs[k][tx + 16 * j];
+            for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
 #pragma unroll
             for (int i = 0; i < 4; ++i)
 #pragma unroll
