@@ -43,7 +43,19 @@ struct Fp {
     uint64_t mu;            // floor((2^64-1)/p), Barrett constant
     const uint32_t* inv;    // device inverse table (p < 2^16) or nullptr
     int char2;              // p == 2
+    uint32_t mu32;          // floor(2^32/p) when p < 2^16 (32-bit Barrett), else 0
 };
+
+// Field constants for modulus p (host side).
+inline Fp make_fp(uint64_t p, const uint32_t* inv_table) {
+    Fp f;
+    f.p = (uint32_t)p;
+    f.mu = UINT64_MAX / p;
+    f.inv = inv_table;
+    f.char2 = p == 2;
+    f.mu32 = p < 65536 ? (uint32_t)(0x100000000ull / p) : 0u;
+    return f;
+}
 
 __host__ __device__ inline uint64_t umulhi64(uint64_t a, uint64_t b) {
 #ifdef __CUDA_ARCH__
@@ -69,6 +81,14 @@ __host__ __device__ inline uint32_t fsub(const Fp& f, uint32_t a, uint32_t b) {
 }
 __host__ __device__ inline uint32_t fneg(const Fp& f, uint32_t a) { return a ? f.p - a : 0; }
 __host__ __device__ inline uint32_t fmul(const Fp& f, uint32_t a, uint32_t b) {
+#ifdef __CUDA_ARCH__
+    if (f.mu32) {  // p < 2^16: the product fits 32 bits (warp-uniform branch)
+        const uint32_t x = a * b;
+        const uint32_t q = __umulhi(x, f.mu32);
+        const uint32_t r = x - q * f.p;
+        return r >= f.p ? r - f.p : r;
+    }
+#endif
     return red64(f, (uint64_t)a * b);
 }
 // a/2 for odd p (field.hpp:121-124).

@@ -179,11 +179,7 @@ const void* readback(ffb_context* c, const void* dev, size_t bytes) {
 }
 
 Fp make_field(ffb_context* c, uint64_t p) {
-    Fp f;
-    f.p = (uint32_t)p;
-    f.mu = UINT64_MAX / p;
-    f.char2 = p == 2;
-    f.inv = nullptr;
+    Fp f = make_fp(p, nullptr);
     if (p < 65536) {
         if (c->inv_p != p) {
             if (c->inv_table) FFB_CUDA(cudaFree(c->inv_table));

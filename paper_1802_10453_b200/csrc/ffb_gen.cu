@@ -119,14 +119,7 @@ using namespace ffb;
 
 namespace {
 
-Fp host_field(uint64_t p) {
-    Fp f;
-    f.p = (uint32_t)p;
-    f.mu = UINT64_MAX / p;
-    f.inv = nullptr;
-    f.char2 = p == 2;
-    return f;
-}
+Fp host_field(uint64_t p) { return make_fp(p, nullptr); }
 
 int check_gen_args(int config, size_t n, size_t r, uint64_t p) {
     if (config < 1 || config > 5) return FFB_ERROR;
