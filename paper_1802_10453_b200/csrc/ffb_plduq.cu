@@ -313,6 +313,104 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
 }
 
 // ---------------------------------------------------------------------------
+// RPM of the chunk's pivot rows from the level-0 candidates (1 CTA).  Every
+// column dropped by a level-0 scan depends on earlier columns, so the RPM of
+// R_I equals the RPM of R_I restricted to the candidate columns C (ascending).
+// Row-order leftmost elimination on R_I[:, C] (the reference's Crout rule,
+// plduq.cpp:46-84, on the compressed problem) yields each pivot row's column:
+//   J = sorted pivot columns, sigma[t] = index in J of row t's pivot column.
+// Rc lives in shared memory when k*|C| fits, else in the global scratch.
+// ---------------------------------------------------------------------------
+constexpr int RE_SMEM_WORDS = 40 * 1024;
+__global__ void __launch_bounds__(256) k_crp_rowelim(Fp f, const uint32_t* RI, int64_t ldr, int k,
+                                                     const int32_t* lists, const int32_t* counts,
+                                                     int nblk, uint32_t* gscratch, int32_t* Jout,
+                                                     int32_t* sigma_out, int32_t* fail) {
+    extern __shared__ uint32_t sm[];
+    __shared__ int32_t off[1025];
+    __shared__ int32_t pcol[CRP_KMAX];
+    __shared__ uint32_t mcol[CRP_KMAX];
+    __shared__ uint32_t sinv[SINV_MAX];
+    __shared__ int lead, total;
+    const int tid = threadIdx.x;
+    const SmemInv inv = stage_inverses(f, sinv);
+    if (tid == 0) {
+        int t = 0;
+        for (int b = 0; b < nblk; ++b) {
+            off[b] = t;
+            t += counts[b];
+        }
+        off[nblk] = t;
+        total = t;
+    }
+    __syncthreads();
+    const int C = total;
+    uint32_t* Rc = ((size_t)k * C <= RE_SMEM_WORDS) ? sm : gscratch;
+    int32_t* cand = (int32_t*)(gscratch + (size_t)CRP_KMAX * nblk * CRP_KMAX);  // column ids
+    for (int b = 0; b < nblk; ++b)
+        for (int q = tid; q < counts[b]; q += blockDim.x) cand[off[b] + q] = lists[(int64_t)b * k + q];
+    __syncthreads();
+    for (int base = tid; base < k * C; base += 4 * blockDim.x) {
+        uint32_t vv[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = base + u * blockDim.x;
+            vv[u] = e < k * C ? __ldg(RI + (int64_t)(e / C) * ldr + cand[e % C]) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = base + u * blockDim.x;
+            if (e < k * C) Rc[e] = vv[u];
+        }
+    }
+    __syncthreads();
+    for (int t = 0; t < k; ++t) {
+        if (tid == 0) lead = C;
+        __syncthreads();
+        const uint32_t* rt = Rc + (size_t)t * C;
+        for (int j = tid; j < C; j += blockDim.x)
+            if (rt[j]) atomicMin(&lead, j);  // used columns are already zero in row t
+        __syncthreads();
+        const int jp = lead;
+        if (jp >= C) {
+            if (tid == 0) *fail = 1;
+            return;
+        }
+        const uint32_t xi = inv(f, rt[jp]);
+        for (int i = t + 1 + tid; i < k; i += blockDim.x) mcol[i] = fmul(f, Rc[(size_t)i * C + jp], xi);
+        if (tid == 0) pcol[t] = cand[jp];
+        __syncthreads();
+        const int w = C - jp;
+        for (int e = tid; e < (k - t - 1) * w; e += blockDim.x) {
+            const int i = t + 1 + e / w, j = jp + e % w;
+            const uint32_t m = mcol[i];
+            if (m) Rc[(size_t)i * C + j] = fsub(f, Rc[(size_t)i * C + j], fmul(f, m, rt[j]));
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        // J = sorted pivot columns; sigma[t] = position of pcol[t] in J
+        int32_t js[CRP_KMAX];
+        for (int t = 0; t < k; ++t) js[t] = pcol[t];
+        for (int a = 1; a < k; ++a) {
+            const int32_t v = js[a];
+            int b = a - 1;
+            while (b >= 0 && js[b] > v) { js[b + 1] = js[b]; --b; }
+            js[b + 1] = v;
+        }
+        for (int t = 0; t < k; ++t) Jout[t] = js[t];
+        for (int t = 0; t < k; ++t) {
+            int lo = 0, hi = k - 1;
+            while (lo < hi) {
+                const int mid = (lo + hi) / 2;
+                if (js[mid] < pcol[t]) lo = mid + 1; else hi = mid;
+            }
+            sigma_out[t] = lo;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Pairing + inverse + bookkeeping (1 CTA).  Kc = RI[:, J] (k x k, nonsingular).
 // Row-order leftmost elimination on Kc gives the RPM pairing sigma (the
 // reference's Crout rule restricted to Kc); Gauss-Jordan gives Kinv.  Then:
@@ -324,7 +422,7 @@ __global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t
                                                const uint32_t* S, int64_t lds, int s,
                                                uint32_t* Kinv, uint32_t* UO, int64_t lduo,
                                                int32_t* uhat_col, int32_t* prow, int32_t* pcol,
-                                               int64_t r, int32_t* fail) {
+                                               int64_t r, int32_t* fail, const int32_t* sigma_in) {
     extern __shared__ uint32_t sm[];
     uint32_t* A = sm;                       // k x k working copy (row-order elimination)
     uint32_t* G = A + (size_t)k * k;        // k x 2k Gauss-Jordan
@@ -343,8 +441,10 @@ __global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t
         G[(size_t)i * 2 * k + k + j] = (i == j) ? 1 % f.p : 0;
     }
     for (int j = tid; j < k; j += blockDim.x) colused[j] = 0;
+    if (sigma_in)
+        for (int t = tid; t < k; t += blockDim.x) sig[t] = sigma_in[t];
     __syncthreads();
-    for (int t = 0; t < k; ++t) {
+    for (int t = 0; t < (sigma_in ? 0 : k); ++t) {
         if (tid == 0) lead = k;
         __syncthreads();
         for (int j = tid; j < k; j += blockDim.x)
@@ -602,6 +702,8 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     int32_t* lists[2] = {ws.vec<int32_t>((int64_t)nblk0 * B), ws.vec<int32_t>((int64_t)nblk0 * B)};
     int32_t* counts[2] = {ws.vec<int32_t>(nblk0), ws.vec<int32_t>(nblk0)};
     int32_t* dflag = ws.vec<int32_t>(4);
+    int32_t* dsig = ws.vec<int32_t>(B);
+    uint32_t* re_scratch = ws.vec<uint32_t>((int64_t)CRP_KMAX * nblk0 * CRP_KMAX + (int64_t)nblk0 * CRP_KMAX + 64);
     int32_t* d_uhat_col = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
     const int64_t pstride = (std::max<int64_t>(mn, 1) + 63) / 64 * 64;
     int32_t* d_prow = ws.vec<int32_t>(2 * pstride);
@@ -616,6 +718,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         FFB_CUDA(cudaFuncSetAttribute(k_crp_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crp_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_pair2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * CRP_KMAX * CRP_KMAX * 4)));
         FFB_CUDA(cudaFuncSetAttribute(k_sketch_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        FFB_CUDA(cudaFuncSetAttribute(k_crp_rowelim, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attrs = true;
     }
     static const bool force_exact = getenv("FFB_PLDUQ_FORCE_FALLBACK") != nullptr;  // test hook
@@ -625,14 +728,14 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     // R_I in RI) and pivot column set dJ (ascending): pairing, Unew into Uhat
     // rows [r, r+k), old rows reduced at J, Uhat*Omega maintained when sketching.
     auto absorb = [&](int64_t r, int k, const int32_t* dI, const int32_t* dJ, int64_t c0,
-                      bool sketching) {
+                      bool sketching, const int32_t* sigma_in) {
         DMat RIk = RI.sub(0, 0, k, n), Kik = Kinv.sub(0, 0, k, k);
         Kik.ld = k;
         {
             ProfScope ps(K_PQ_PAIR, st, 0.0, 0.0);
             k_pair2<<<1, 256, (size_t)3 * k * k * 4, st>>>(
                 f, RIk.ptr, RIk.ld, k, dJ, dI, c0, sketching ? S.ptr : nullptr, S.ld, SK, Kik.ptr,
-                UO.ptr, UO.ld, d_uhat_col, d_prow, d_pcol, r, dflag);
+                UO.ptr, UO.ld, d_uhat_col, d_prow, d_pcol, r, dflag, sigma_in);
             ++g_launches;
             FFB_CHECK_LAUNCH();
         }
@@ -693,25 +796,21 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     gather2d(st, Gk, Y, dI, d_uhat_col, c0);
                     gemm(f, st, GEMM_SUB, RIk, Gk, false, Uhat.sub(0, 0, r, n), false, k, n, r);
                 }
-                int cur = 0;
                 {
                     ProfScope ps(K_PQ_CRP, st, 0.0, 0.0);
+                    // level 0: local CRPs of 256-column blocks (parallel)
                     k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, nullptr, nullptr,
                                                              0, lists[0], counts[0]);
                     ++g_launches;
-                    int groups = nblk0;
-                    while (groups > 1) {
-                        const int ng = (groups + CRP_FAN - 1) / CRP_FAN;
-                        k_crp_list<<<ng, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, lists[cur],
-                                                              counts[cur], groups, lists[cur ^ 1],
-                                                              counts[cur ^ 1]);
-                        ++g_launches;
-                        groups = ng;
-                        cur ^= 1;
-                    }
+                    // RPM of R_I on the surviving candidate columns (1 CTA)
+                    const int64_t maxc = (int64_t)nblk0 * k;
+                    const size_t resmem = std::min<int64_t>((int64_t)k * maxc, RE_SMEM_WORDS) * 4;
+                    k_crp_rowelim<<<1, 256, resmem, st>>>(f, RI.ptr, RI.ld, k, lists[0], counts[0], nblk0,
+                                                          re_scratch, lists[1], dsig, dflag);
+                    ++g_launches;
                     FFB_CHECK_LAUNCH();
                 }
-                absorb(r, k, dI, lists[cur], c0, true);
+                absorb(r, k, dI, lists[1], c0, true, dsig);
                 r += k;
             } else {
                 // exact: residual of the whole chunk, then the row-sequential kernel
@@ -739,7 +838,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 if (k > 0) {
                     const int32_t* dI = io.upload(I);
                     gather_rows(st, RI.sub(0, 0, k, n), Rc, dI);
-                    absorb(r, k, dI, io.upload(J), c0, false);
+                    absorb(r, k, dI, io.upload(J), c0, false, nullptr);
                     r += k;
                 }
                 ws.release(mk);
