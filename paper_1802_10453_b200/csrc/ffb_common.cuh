@@ -133,18 +133,22 @@ __device__ inline SmemInv stage_inverses(const Fp& f, uint32_t* buf /* SINV_MAX 
 template <int U>
 __device__ __forceinline__ void load_tile(uint32_t* dst, int ldd, const uint32_t* __restrict__ src,
                                           int64_t lds, int rows, int cols) {
-    const int total = rows * cols, nt = blockDim.x;
-    for (int base = threadIdx.x; base < total; base += U * nt) {
-        uint32_t v[U];
+    // warp w copies rows w, w + nwarps, ...; lanes stride the columns; U rows
+    // of loads are in flight before the stores (no integer division).
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r0 = w; r0 < rows; r0 += U * nw) {
+        for (int c0 = lane; c0 < cols; c0 += 32) {
+            uint32_t v[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int e = base + u * nt;
-            v[u] = e < total ? __ldg(src + (int64_t)(e / cols) * lds + (e % cols)) : 0u;
-        }
+            for (int u = 0; u < U; ++u) {
+                const int r = r0 + u * nw;
+                v[u] = r < rows ? __ldg(src + (int64_t)r * lds + c0) : 0u;
+            }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-            const int e = base + u * nt;
-            if (e < total) dst[(e / cols) * ldd + (e % cols)] = v[u];
+            for (int u = 0; u < U; ++u) {
+                const int r = r0 + u * nw;
+                if (r < rows) dst[r * ldd + c0] = v[u];
+            }
         }
     }
 }

@@ -130,12 +130,14 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
         for (int j = tid; j < s; j += blockDim.x) v[j] = fmul(f, v[j], il);
         for (int t = tid; t < k; t += blockDim.x) coef[t] = E[(size_t)t * s + rh];
         __syncthreads();
-        for (int e = tid; e < k * s; e += blockDim.x) {
-            const int t = e / s, j = e % s;
-            const uint32_t c = coef[t];
-            if (c) E[(size_t)t * s + j] = fsub(f, E[(size_t)t * s + j], fmul(f, c, v[j]));
+        for (int j = tid; j < s; j += blockDim.x) {
+            const uint32_t vj = v[j];
+            for (int t = 0; t < k; ++t) {
+                const uint32_t c = coef[t];
+                if (c) E[(size_t)t * s + j] = fsub(f, E[(size_t)t * s + j], fmul(f, c, vj));
+            }
+            E[(size_t)k * s + j] = vj;
         }
-        for (int j = tid; j < s; j += blockDim.x) E[(size_t)k * s + j] = v[j];
         if (tid == 0) {
             rho[k] = rh;
             out[1 + k] = i;
@@ -228,30 +230,35 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
         if (tid < gw) colid[tid] = column_at(s0 + tid);
         if (tid < CRP_G) nzmask[tid] = 0;
         __syncthreads();
-        for (int base = tid; base < gw * k; base += 4 * blockDim.x) {  // 4 loads in flight
-            uint32_t vv[4];
+        {  // warp w loads rows w, w+8, ... (4 in flight), lane = column of the group
+            const int lane = tid & 31, wp = tid >> 5;
+            for (int i0 = wp; i0 < k; i0 += 32) {
+                uint32_t vv[4];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = base + u * blockDim.x;
-                vv[u] = e < gw * k ? __ldg(RI + (int64_t)(e / gw) * ldr + colid[e % gw]) : 0u;
-            }
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + 8 * u;
+                    vv[u] = (i < k && lane < gw) ? __ldg(RI + (int64_t)i * ldr + colid[lane]) : 0u;
+                }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = base + u * blockDim.x;
-                if (e < gw * k) V[(size_t)(e % gw) * k + e / gw] = vv[u];
+                for (int u = 0; u < 4; ++u) {
+                    const int i = i0 + 8 * u;
+                    if (i < k && lane < gw) V[(size_t)lane * k + i] = vv[u];
+                }
             }
         }
         __syncthreads();
         // reduce every column of the group against the current basis; flag the
         // columns that stay nonzero (candidates for a new basis vector)
         const int kb = nb;
-        for (int e = tid; e < gw * kb; e += blockDim.x) {  // coefficient gather
-            const int c = e / kb, t = e % kb;
-            VC[(size_t)c * CRP_KMAX + t] = V[(size_t)c * k + rho[t]];
+        {
+            const int lane = tid & 31, wp = tid >> 5;
+            for (int c = wp; c < gw; c += 8)  // coefficient gather
+                for (int t = lane; t < kb; t += 32) VC[(size_t)c * CRP_KMAX + t] = V[(size_t)c * k + rho[t]];
         }
         __syncthreads();
-        for (int e = tid; e < gw * k; e += blockDim.x) {
-            const int c = e / k, i = e % k;
+        for (int e = tid; e < CRP_G * CRP_KMAX; e += blockDim.x) {
+            const int c = e >> 7, i = e & (CRP_KMAX - 1);  // CRP_KMAX = 128
+            if (c >= gw || i >= k) continue;
             const uint32_t* vc = VC + (size_t)c * CRP_KMAX;
             uint64_t acc = 0;
             if (f.p < (1u << 26)) {
@@ -292,10 +299,12 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
                 for (int i = lane; i < k; i += 32) vr[i] = fmul(f, vr[i], ilv);
                 for (int t = lane; t < nbl; t += 32) coefs[t] = E[(size_t)t * k + ld];
                 __syncwarp();
-                for (int e = lane; e < nbl * k; e += 32) {
-                    const int t = e / k, i = e % k;
-                    const uint32_t cc = coefs[t];
-                    if (cc) E[(size_t)t * k + i] = fsub(f, E[(size_t)t * k + i], fmul(f, cc, vr[i]));
+                for (int i = lane; i < k; i += 32) {
+                    const uint32_t vi = vr[i];
+                    for (int t = 0; t < nbl; ++t) {
+                        const uint32_t cc = coefs[t];
+                        if (cc) E[(size_t)t * k + i] = fsub(f, E[(size_t)t * k + i], fmul(f, cc, vi));
+                    }
                 }
                 for (int i = lane; i < k; i += 32) E[(size_t)nbl * k + i] = vr[i];
                 if (lane == 0) {
@@ -350,18 +359,22 @@ __global__ void __launch_bounds__(256) k_crp_rowelim(Fp f, const uint32_t* RI, i
     for (int b = 0; b < nblk; ++b)
         for (int q = tid; q < counts[b]; q += blockDim.x) cand[off[b] + q] = lists[(int64_t)b * k + q];
     __syncthreads();
-    for (int base = tid; base < k * C; base += 4 * blockDim.x) {
-        uint32_t vv[4];
+    {
+        const int lane = tid & 31, wp = tid >> 5;
+        for (int i = wp; i < k; i += 8)
+            for (int j0 = lane; j0 < C; j0 += 128) {
+                uint32_t vv[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = base + u * blockDim.x;
-            vv[u] = e < k * C ? __ldg(RI + (int64_t)(e / C) * ldr + cand[e % C]) : 0u;
-        }
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + 32 * u;
+                    vv[u] = j < C ? __ldg(RI + (int64_t)i * ldr + cand[j]) : 0u;
+                }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int e = base + u * blockDim.x;
-            if (e < k * C) Rc[e] = vv[u];
-        }
+                for (int u = 0; u < 4; ++u) {
+                    const int j = j0 + 32 * u;
+                    if (j < C) Rc[(size_t)i * C + j] = vv[u];
+                }
+            }
     }
     __syncthreads();
     for (int t = 0; t < k; ++t) {
@@ -380,11 +393,14 @@ __global__ void __launch_bounds__(256) k_crp_rowelim(Fp f, const uint32_t* RI, i
         for (int i = t + 1 + tid; i < k; i += blockDim.x) mcol[i] = fmul(f, Rc[(size_t)i * C + jp], xi);
         if (tid == 0) pcol[t] = cand[jp];
         __syncthreads();
-        const int w = C - jp;
-        for (int e = tid; e < (k - t - 1) * w; e += blockDim.x) {
-            const int i = t + 1 + e / w, j = jp + e % w;
-            const uint32_t m = mcol[i];
-            if (m) Rc[(size_t)i * C + j] = fsub(f, Rc[(size_t)i * C + j], fmul(f, m, rt[j]));
+        {
+            const int lane = tid & 31, wp = tid >> 5;
+            for (int i = t + 1 + wp; i < k; i += 8) {
+                const uint32_t m = mcol[i];
+                if (!m) continue;
+                uint32_t* ri = Rc + (size_t)i * C;
+                for (int j = jp + lane; j < C; j += 32) ri[j] = fsub(f, ri[j], fmul(f, m, rt[j]));
+            }
         }
         __syncthreads();
     }
@@ -494,11 +510,15 @@ __global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t
         __syncthreads();
         for (int j = tid; j < w; j += blockDim.x) G[(size_t)c * w + j] = fmul(f, G[(size_t)c * w + j], il);
         __syncthreads();
-        for (int e = tid; e < k * w; e += blockDim.x) {
-            const int i = e / w, j = e % w;
-            if (i == c || j == c) continue;
-            const uint32_t m = G[(size_t)i * w + c];
-            if (m) G[(size_t)i * w + j] = fsub(f, G[(size_t)i * w + j], fmul(f, m, G[(size_t)c * w + j]));
+        {
+            const int lane = tid & 31, wp = tid >> 5;
+            for (int i = wp; i < k; i += 8) {
+                if (i == c) continue;
+                const uint32_t m = G[(size_t)i * w + c];
+                if (!m) continue;
+                for (int j = lane; j < w; j += 32)
+                    if (j != c) G[(size_t)i * w + j] = fsub(f, G[(size_t)i * w + j], fmul(f, m, G[(size_t)c * w + j]));
+            }
         }
         __syncthreads();
         for (int i = tid; i < k; i += blockDim.x)
