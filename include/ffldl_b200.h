@@ -87,7 +87,7 @@ uint64_t ffb_sync_count(ffb_context* ctx);
  * launching stream; adds overhead, off by default).  enable resets the totals.
  * Classes: 0 GEMM, 1 Crout leaf, 2 PLDUQ row detection / sequential kernel, 3 TRSM base,
  * 4 data movement, 5 other, 6 PLDUQ sketch, 7 PLDUQ column rank profile, 8 PLDUQ pairing,
- * 9 LDU base, 10 tensor-core operand packing. */
+ * 9 LDU base, 10 tensor-core operand packing, 11 PLDUQ row elimination on candidates. */
 int ffb_profile_enable(ffb_context* ctx, int enable);
 int ffb_profile_read(ffb_context* ctx, int klass, uint64_t* launches, double* ms, double* ops,
                      double* bytes);

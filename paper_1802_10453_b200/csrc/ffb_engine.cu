@@ -17,6 +17,8 @@
 //   D   per-pivot-column kind / value / value2 / inverse arrays.
 // Node-local permutations and ranks are read back to the host (they decide
 // the shape of the next node); index arrays go down through a pinned ring.
+#include <nvtx3/nvToolsExt.h>
+#include <chrono>
 #include <stdlib.h>
 #include <string.h>
 
@@ -45,6 +47,7 @@ struct ffb_context {
     int32_t* flag = nullptr;  // device scratch flag
     uint64_t launches = 0;
     uint64_t syncs = 0, syncs_last = 0;
+    double sync_wait_ms = 0;  // host time blocked in read-backs (FFB_HOST_STATS)
     Profiler prof;
 };
 
@@ -172,21 +175,32 @@ const void* readback(ffb_context* c, const void* dev, size_t bytes) {
         FFB_CUDA(cudaMallocHost(&c->down_host, c->down_cap));
     }
     FFB_CUDA(cudaMemcpyAsync(c->down_host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    const auto t0 = std::chrono::steady_clock::now();
     FFB_CUDA(cudaStreamSynchronize(c->stream));
+    c->sync_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     ++c->syncs;
     c->up_top = 0;  // every upload issued so far has completed
     return c->down_host;
 }
 
+__global__ void k_inv_table(uint32_t* t, uint32_t p) {
+    const uint32_t a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a < p) t[a] = a ? finv_euclid(p, a) : 0u;
+}
+
+// Field constants; an inverse table for p < 2^24 (built once per modulus on
+// the device) turns every pivot inverse into one load.
 Fp make_field(ffb_context* c, uint64_t p) {
     Fp f = make_fp(p, nullptr);
-    if (p < 65536) {
+    if (p < (1ull << 24)) {
         if (c->inv_p != p) {
             if (c->inv_table) FFB_CUDA(cudaFree(c->inv_table));
-            std::vector<uint32_t> t(p, 0);
-            for (uint64_t a = 1; a < p; ++a) t[a] = finv_euclid((uint32_t)p, (uint32_t)a);
+            c->inv_table = nullptr;
+            c->inv_p = 0;
             FFB_CUDA(cudaMalloc(&c->inv_table, p * sizeof(uint32_t)));
-            FFB_CUDA(cudaMemcpy(c->inv_table, t.data(), p * sizeof(uint32_t), cudaMemcpyHostToDevice));
+            k_inv_table<<<(unsigned)cdiv((int64_t)p, 256), 256, 0, c->stream>>>(c->inv_table, (uint32_t)p);
+            FFB_CHECK_LAUNCH();
+            FFB_CUDA(cudaStreamSynchronize(c->stream));
             c->inv_p = (uint32_t)p;
         }
         f.inv = c->inv_table;
@@ -325,9 +339,21 @@ struct Engine {
         DMat L, U;
         uint32_t *d, *dinv;
     };
+    double pq_t0 = 0;
     Pl run_plduq(DMat Y) {
         const int64_t m = Y.rows, n = Y.cols, mn = std::min(m, n);
         Pl pl;
+        if (getenv("FFB_PLDUQ_TRACE")) {
+            FFB_CUDA(cudaStreamSynchronize(st));
+            pq_t0 = std::chrono::duration<double, std::milli>(
+                        std::chrono::steady_clock::now().time_since_epoch()).count();
+        }
+        // NVTX range around large PLDUQs (profiling filter; no-op without a tool)
+        struct Range {
+            bool on;
+            explicit Range(bool b) : on(b) { if (on) nvtxRangePushA("plduq_big"); }
+            ~Range() { if (on) nvtxRangePop(); }
+        } range(m * n >= (int64_t)1 << 24);
         DMat Lo = ws_mat(c, m, mn), Uo = ws_mat(c, mn, n);
         pl.d = ws_vec<uint32_t>(c, mn);
         pl.dinv = ws_vec<uint32_t>(c, mn);
@@ -360,6 +386,13 @@ struct Engine {
         }
         pl.L = Lo.sub(0, 0, m, pl.r);
         pl.U = Uo.sub(0, 0, pl.r, n);
+        static FILE* tr = getenv("FFB_PLDUQ_TRACE") ? fopen(getenv("FFB_PLDUQ_TRACE"), "a") : nullptr;
+        if (tr) {  // shape + wall time of each PLDUQ (diagnostics; synchronizes)
+            FFB_CUDA(cudaStreamSynchronize(st));
+            const double t1 = std::chrono::duration<double, std::milli>(
+                                  std::chrono::steady_clock::now().time_since_epoch()).count();
+            fprintf(tr, "%lld %lld %lld %.3f\n", (long long)m, (long long)n, (long long)pl.r, t1 - pq_t0);
+        }
         return pl;
     }
 
@@ -473,8 +506,18 @@ int guarded(ffb_context* c, F&& fn) {
         if (!c) throw Status(FFB_ERROR, "null context");
         FFB_CUDA(cudaSetDevice(c->device));
         const uint64_t l0 = g_launches, s0 = c->syncs;
+        const auto t0 = std::chrono::steady_clock::now();
+        const double w0 = c->sync_wait_ms;
         g_prof = &c->prof;
         fn();
+        static const bool host_stats = getenv("FFB_HOST_STATS") != nullptr;
+        if (host_stats) {  // host-side balance: wall vs time blocked on the device
+            FFB_CUDA(cudaStreamSynchronize(c->stream));
+            const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+            fprintf(stderr, "[ffb host] wall %.2f ms, blocked in %llu read-backs %.2f ms, launches %llu\n",
+                    wall, (unsigned long long)(c->syncs - s0), c->sync_wait_ms - w0,
+                    (unsigned long long)(g_launches - l0));
+        }
         if (c->prof.on) {
             FFB_CUDA(cudaStreamSynchronize(c->stream));
             c->prof.flush();

@@ -4,6 +4,7 @@
 // (Alg. 4), PLDUQ (row-order Crout with leftmost pivots), the small
 // triangular solves, and the generic modular GEMM used for every
 // contraction that the tcgen05 path (ffb_tc_gemm.cu) does not take.
+#include <cstdio>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -28,9 +29,12 @@ cudaEvent_t Profiler::get() {
     return e;
 }
 void Profiler::flush() {
+    // FFB_PROF_TRACE=<file>: one line per profiled launch (class, shape, ms), appended
+    static FILE* trace = getenv("FFB_PROF_TRACE") ? fopen(getenv("FFB_PROF_TRACE"), "a") : nullptr;
     for (Rec& r : recs) {
         float t = 0.f;
         if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) ms[r.cls] += t;
+        if (trace) fprintf(trace, "%d %lld %lld %lld %.4f\n", r.cls, (long long)r.m, (long long)r.n, (long long)r.k, t);
         ops[r.cls] += r.ops;
         bytes[r.cls] += r.bytes;
         cnt[r.cls] += 1;
@@ -42,10 +46,15 @@ void Profiler::flush() {
 void Profiler::reset() {
     for (int i = 0; i < K_NCLASS; ++i) ms[i] = ops[i] = bytes[i] = 0, cnt[i] = 0;
 }
-ProfScope::ProfScope(int cls, cudaStream_t s, double ops, double bytes) : st(s) {
+ProfScope::ProfScope(int cls, cudaStream_t s, double ops, double bytes, int64_t m, int64_t n,
+                     int64_t k)
+    : st(s) {
     live = g_prof && g_prof->on;
     if (!live) return;
     rec.cls = cls;
+    rec.m = m;
+    rec.n = n;
+    rec.k = k;
     rec.ops = ops;
     rec.bytes = bytes;
     rec.a = g_prof->get();
@@ -160,7 +169,7 @@ template <bool TA, bool TB>
 void launch_gemm_simt(const Fp& f, cudaStream_t st, int mode, DMat C, DMat A, DMat B, int64_t M,
                       int64_t N, int64_t K) {
     dim3 grid((unsigned)cdiv(N, GB_N), (unsigned)cdiv(M, GB_M));
-    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, 4.0 * (M * K + K * N + 2 * M * N));
+    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, 4.0 * (M * K + K * N + 2 * M * N), -M, N, K);  // -M marks SIMT
     if (f.p < (1u << 23))
         k_gemm_simt<TA, TB, false><<<grid, 256, 0, st>>>(f, mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr,
                                                           B.ld, M, N, K);

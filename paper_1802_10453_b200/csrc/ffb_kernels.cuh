@@ -14,13 +14,14 @@ extern thread_local uint64_t g_launches;
 // around each launch on the launching stream, summed per class.
 enum KClass {
     K_GEMM = 0, K_LEAF = 1, K_PLDUQ = 2, K_TRSM = 3, K_MOVE = 4, K_OTHER = 5,
-    K_PQ_SKETCH = 6, K_PQ_CRP = 7, K_PQ_PAIR = 8, K_LDU = 9, K_PACK = 10, K_NCLASS = 11
+    K_PQ_SKETCH = 6, K_PQ_CRP = 7, K_PQ_PAIR = 8, K_LDU = 9, K_PACK = 10, K_PQ_ROWELIM = 11, K_NCLASS = 12
 };
 struct Profiler {
     struct Rec {
         int cls;
         cudaEvent_t a, b;
         double ops, bytes;
+        int64_t m, n, k;  // GEMM shape (trace only)
     };
     bool on = false;
     std::vector<Rec> recs;
@@ -36,7 +37,8 @@ struct ProfScope {
     Profiler::Rec rec;
     cudaStream_t st;
     bool live;
-    ProfScope(int cls, cudaStream_t s, double ops, double bytes);
+    ProfScope(int cls, cudaStream_t s, double ops, double bytes, int64_t m = 0, int64_t n = 0,
+              int64_t k = 0);
     ~ProfScope();
 };
 

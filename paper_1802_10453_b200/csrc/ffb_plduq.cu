@@ -79,96 +79,100 @@ inline dim3 rgrid(int64_t rows, int64_t cols) {
 // ---------------------------------------------------------------------------
 constexpr int RD_MAX_B = 128, RD_S = 144;
 
+constexpr int RD_BATCH = 16;
 __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int64_t lds, int b,
                                                     int s, int32_t* out) {
     extern __shared__ uint32_t sm[];
     uint32_t* Ss = sm;                          // b x s
-    uint32_t* E = Ss + (size_t)RD_MAX_B * s;    // basis rows
-    uint32_t* v = E + (size_t)RD_MAX_B * s;     // current row
+    uint32_t* E = Ss + (size_t)RD_MAX_B * s;    // basis rows (fully reduced)
+    uint32_t* V = E + (size_t)RD_MAX_B * s;     // RD_BATCH reduced rows of the current batch
     __shared__ int rho[RD_MAX_B];
     __shared__ uint32_t coef[RD_MAX_B];
+    __shared__ uint32_t cfb[RD_BATCH][RD_MAX_B];  // batch coefficients S_i[rho_t]
+    __shared__ uint32_t vcol[RD_BATCH];
+    __shared__ int flag[RD_BATCH];
     __shared__ int rhs;
     __shared__ uint32_t ils;
     __shared__ uint32_t sinv[SINV_MAX];
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     load_tile<8>(Ss, s, S, lds, b, s);
     if (tid == 0) rhs = s;
     const SmemInv inv = stage_inverses(f, sinv);
     __syncthreads();
-    __shared__ uint32_t cf[2][RD_MAX_B];  // S_i[rho_t], double-buffered by row parity
     int k = 0;
-    for (int i = 0; i < b; ++i) {
-        const uint32_t* si = Ss + (size_t)i * s;
-        uint32_t* c = cf[i & 1];
-        for (int t = tid; t < k; t += blockDim.x) c[t] = si[rho[t]];
+    for (int i0 = 0; i0 < b; i0 += RD_BATCH) {
+        const int nr = min(RD_BATCH, b - i0);
+        // 1. reduce the whole batch against the basis (parallel)
+        for (int r = wp; r < nr; r += 8)
+            for (int t = lane; t < k; t += 32) cfb[r][t] = Ss[(size_t)(i0 + r) * s + rho[t]];
+        if (tid < RD_BATCH) flag[tid] = 0;
         __syncthreads();
-        int nz = 0;
-        for (int j = tid; j < s; j += blockDim.x) {
-            uint64_t acc = 0;
-            const uint32_t* ej = E + j;
-            int t = 0;
-            if (f.p < (1u << 26)) {
-                for (; t + 4 <= k; t += 4)
-                    acc += (uint64_t)c[t] * ej[(size_t)t * s] + (uint64_t)c[t + 1] * ej[(size_t)(t + 1) * s] +
-                           (uint64_t)c[t + 2] * ej[(size_t)(t + 2) * s] + (uint64_t)c[t + 3] * ej[(size_t)(t + 3) * s];
-                for (; t < k; ++t) acc += (uint64_t)c[t] * ej[(size_t)t * s];
-            } else {
-                for (; t < k; ++t) acc = red64(f, acc + (uint64_t)c[t] * ej[(size_t)t * s]);
+        for (int r = wp; r < nr; r += 8) {
+            const uint32_t* si = Ss + (size_t)(i0 + r) * s;
+            int nz = 0;
+            for (int j = lane; j < s; j += 32) {
+                uint64_t acc = 0;
+                if (f.p < (1u << 26)) {
+                    for (int t = 0; t < k; ++t) acc += (uint64_t)cfb[r][t] * E[(size_t)t * s + j];
+                } else {
+                    for (int t = 0; t < k; ++t) acc = red64(f, acc + (uint64_t)cfb[r][t] * E[(size_t)t * s + j]);
+                }
+                const uint32_t x = fsub(f, si[j], red64(f, acc));
+                V[(size_t)r * s + j] = x;
+                nz |= x != 0;
             }
-            const uint32_t x = fsub(f, si[j], red64(f, acc));
-            v[j] = x;
-            nz |= x != 0;
+            nz = __any_sync(0xffffffffu, nz);
+            if (lane == 0) flag[r] = nz;
         }
-        if (!__syncthreads_or(nz)) continue;  // dependent row (uniform)
-        for (int j = tid; j < s; j += blockDim.x)
-            if (v[j]) atomicMin(&rhs, j);
         __syncthreads();
-        const int rh = rhs;
-        if (tid == 0) ils = inv(f, v[rh]);
-        __syncthreads();
-        const uint32_t il = ils;
-        for (int j = tid; j < s; j += blockDim.x) v[j] = fmul(f, v[j], il);
-        for (int t = tid; t < k; t += blockDim.x) coef[t] = E[(size_t)t * s + rh];
-        __syncthreads();
-        for (int j = tid; j < s; j += blockDim.x) {
-            const uint32_t vj = v[j];
-            for (int t = 0; t < k; ++t) {
-                const uint32_t c = coef[t];
-                if (c) E[(size_t)t * s + j] = fsub(f, E[(size_t)t * s + j], fmul(f, c, vj));
+        // 2. flagged rows in order: exact re-check, then insertion
+        for (int r = 0; r < nr; ++r) {
+            if (!flag[r]) continue;  // in the span of the basis at batch start (uniform)
+            uint32_t* vr = V + (size_t)r * s;
+            int nz = 0;
+            for (int j = tid; j < s; j += blockDim.x) nz |= vr[j] != 0;
+            if (!__syncthreads_or(nz)) continue;  // made dependent by an earlier batch row
+            for (int j = tid; j < s; j += blockDim.x)
+                if (vr[j]) atomicMin(&rhs, j);
+            __syncthreads();
+            const int rh = rhs;
+            if (tid == 0) ils = inv(f, vr[rh]);
+            __syncthreads();
+            const uint32_t il = ils;
+            for (int j = tid; j < s; j += blockDim.x) vr[j] = fmul(f, vr[j], il);
+            for (int t = tid; t < k; t += blockDim.x) coef[t] = E[(size_t)t * s + rh];
+            for (int q = r + 1 + tid; q < nr; q += blockDim.x) vcol[q] = V[(size_t)q * s + rh];
+            __syncthreads();
+            // full reduction: E rows and the later batch rows lose column rh
+            // ((vector, component) pairs over all warps)
+            {
+                const int nrows = k + (nr - r - 1);
+                for (int rr = wp; rr < nrows; rr += 8) {
+                    uint32_t* dst;
+                    uint32_t c;
+                    if (rr < k) {
+                        dst = E + (size_t)rr * s;
+                        c = coef[rr];
+                    } else {
+                        const int q = r + 1 + (rr - k);
+                        dst = V + (size_t)q * s;
+                        c = vcol[q];
+                    }
+                    if (!c) continue;  // warp-uniform
+                    for (int j = lane; j < s; j += 32) dst[j] = fsub(f, dst[j], fmul(f, c, vr[j]));
+                }
             }
-            E[(size_t)k * s + j] = vj;
+            for (int j = tid; j < s; j += blockDim.x) E[(size_t)k * s + j] = vr[j];
+            if (tid == 0) {
+                rho[k] = rh;
+                out[1 + k] = i0 + r;
+                rhs = s;
+            }
+            __syncthreads();
+            ++k;
         }
-        if (tid == 0) {
-            rho[k] = rh;
-            out[1 + k] = i;
-            rhs = s;
-        }
-        __syncthreads();
-        ++k;
     }
     if (tid == 0) out[0] = k;
-}
-
-// Sketch of the chunk residual: S[i][t] = YO[c0+i][t] - sum_j Y[c0+i][uc[j]] UO[j][t].
-__global__ void __launch_bounds__(160) k_sketch_chunk(Fp f, uint32_t* S, int64_t lds,
-                                                     const uint32_t* YO, int64_t ldyo,
-                                                     const uint32_t* Y, int64_t ldy,
-                                                     const uint32_t* UO, int64_t lduo,
-                                                     const int32_t* uc, int64_t r, int64_t c0,
-                                                     int s) {
-    extern __shared__ uint32_t g[];  // r gathered entries of row c0+i
-    const int64_t i = blockIdx.x;
-    const uint32_t* yrow = Y + (c0 + i) * ldy;
-    for (int64_t j = threadIdx.x; j < r; j += blockDim.x) g[j] = yrow[uc[j]];
-    __syncthreads();
-    const int t = threadIdx.x;
-    if (t >= s) return;
-    uint64_t acc = 0;
-    for (int64_t j = 0; j < r; ++j) {
-        acc += (uint64_t)g[j] * UO[j * lduo + t];
-        if (f.p >= (1u << 23) || (j & 0x3FFF) == 0x3FFF) acc = red64(f, acc);
-    }
-    S[i * lds + t] = fsub(f, YO[(c0 + i) * ldyo + t], red64(f, acc));
 }
 
 // ---------------------------------------------------------------------------
@@ -196,8 +200,9 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
     __shared__ int nb;
     __shared__ int nzmask[CRP_G];
     __shared__ int total;
-    __shared__ uint32_t vr[CRP_KMAX];
+    __shared__ uint32_t qcoef[CRP_G];
     __shared__ uint32_t coefs[CRP_KMAX];
+    __shared__ int lead;
     __shared__ uint32_t sinv[SINV_MAX];
     const int tid = threadIdx.x;
     const int g = blockIdx.x;
@@ -215,6 +220,7 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
     };
     if (tid == 0) {
         nb = 0;
+        lead = k;
         if (!in) {
             const int64_t c0 = (int64_t)g * CRP_W;
             total = (int)((c0 + CRP_W < n ? c0 + CRP_W : n) - c0);
@@ -266,56 +272,57 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
             } else {
                 for (int t = 0; t < kb; ++t) acc = red64(f, acc + (uint64_t)vc[t] * E[(size_t)t * k + i]);
             }
-            if (fsub(f, V[(size_t)c * k + i], red64(f, acc)) != 0) atomicOr(&nzmask[c], 1);
+            const uint32_t x = fsub(f, V[(size_t)c * k + i], red64(f, acc));
+            V[(size_t)c * k + i] = x;  // keep the reduced column (same thread reads/writes e)
+            if (x) atomicOr(&nzmask[c], 1);
         }
         __syncthreads();
-        // flagged columns in order, by warp 0 alone (warp-synchronous, no block
-        // barriers): exact reduction against the current basis, then either
-        // dependent or a new basis vector (normalised, eliminated from the rest).
-        if (tid < 32) {
-            const int lane = tid;
-            int nbl = nb;
-            for (int c = 0; c < gw && nbl < k; ++c) {
-                if (!nzmask[c]) continue;
-                int lead_l = k;
-                uint32_t* vc = VC + (size_t)c * CRP_KMAX;
-                for (int t = lane; t < nbl; t += 32) vc[t] = V[(size_t)c * k + rho[t]];
-                __syncwarp();
-                for (int i = lane; i < k; i += 32) {
-                    uint64_t acc = 0;
-                    for (int t = 0; t < nbl; ++t) {
-                        acc += (uint64_t)vc[t] * E[(size_t)t * k + i];
-                        if ((t & 15) == 15 && f.p >= (1u << 26)) acc = red64(f, acc);
+        // flagged columns in order, whole block: a column still nonzero after the
+        // insertions made earlier in this group becomes a basis vector; it is
+        // normalised and eliminated from the basis and from the later columns of
+        // the group, so every stored vector stays reduced against the basis.
+        int nbl = kb;
+        for (int c = 0; c < gw && nbl < k; ++c) {
+            if (!nzmask[c]) continue;  // in the span of the group-start basis (uniform)
+            const uint32_t* vc = V + (size_t)c * k;
+            for (int i = tid; i < k; i += blockDim.x)
+                if (vc[i]) atomicMin(&lead, i);
+            __syncthreads();
+            const int ld = lead;
+            if (ld >= k) continue;  // made dependent by an earlier column of the group
+            const uint32_t ilv = inv(f, vc[ld]);
+            for (int t = tid; t < nbl; t += blockDim.x) coefs[t] = E[(size_t)t * k + ld];
+            for (int q = c + 1 + tid; q < gw; q += blockDim.x) qcoef[q] = V[(size_t)q * k + ld];
+            __syncthreads();
+            {  // (vector, component) pairs over all warps: basis rows, then later columns
+                const int lane = tid & 31, wp = tid >> 5;
+                const int nrows = nbl + (gw - c - 1);
+                for (int rr = wp; rr < nrows; rr += 8) {
+                    uint32_t* dst;
+                    uint32_t cc;
+                    if (rr < nbl) {
+                        dst = E + (size_t)rr * k;
+                        cc = coefs[rr];
+                    } else {
+                        const int q = c + 1 + (rr - nbl);
+                        dst = V + (size_t)q * k;
+                        cc = qcoef[q];
                     }
-                    const uint32_t x = fsub(f, V[(size_t)c * k + i], red64(f, acc));
-                    vr[i] = x;
-                    if (x && i < lead_l) lead_l = i;
+                    if (!cc) continue;  // warp-uniform
+                    const uint32_t ccn = fmul(f, cc, ilv);
+                    for (int i = lane; i < k; i += 32) dst[i] = fsub(f, dst[i], fmul(f, ccn, vc[i]));
                 }
-                for (int off = 16; off; off >>= 1) lead_l = min(lead_l, __shfl_xor_sync(0xffffffffu, lead_l, off));
-                __syncwarp();
-                if (lead_l >= k) continue;
-                const int ld = lead_l;
-                const uint32_t ilv = inv(f, vr[ld]);
-                for (int i = lane; i < k; i += 32) vr[i] = fmul(f, vr[i], ilv);
-                for (int t = lane; t < nbl; t += 32) coefs[t] = E[(size_t)t * k + ld];
-                __syncwarp();
-                for (int i = lane; i < k; i += 32) {
-                    const uint32_t vi = vr[i];
-                    for (int t = 0; t < nbl; ++t) {
-                        const uint32_t cc = coefs[t];
-                        if (cc) E[(size_t)t * k + i] = fsub(f, E[(size_t)t * k + i], fmul(f, cc, vi));
-                    }
-                }
-                for (int i = lane; i < k; i += 32) E[(size_t)nbl * k + i] = vr[i];
-                if (lane == 0) {
-                    rho[nbl] = ld;
-                    out[(int64_t)g * k + nbl] = colid[c];
-                }
-                __syncwarp();
-                ++nbl;
             }
-            if (lane == 0) nb = nbl;
+            for (int i = tid; i < k; i += blockDim.x) E[(size_t)nbl * k + i] = fmul(f, vc[i], ilv);
+            if (tid == 0) {
+                rho[nbl] = ld;
+                out[(int64_t)g * k + nbl] = colid[c];
+                lead = k;
+            }
+            __syncthreads();
+            ++nbl;
         }
+        if (tid == 0) nb = nbl;
         __syncthreads();
     }
     if (tid == 0) ocount[g] = nb;
@@ -714,7 +721,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     const size_t mark0 = ws.mark();
     DMat Uhat = ws.mat(std::max<int64_t>(mn, 1), n);
     DMat UO = ws.mat(std::max<int64_t>(mn, 1), SK);   // Uhat * Omega
-    DMat RI = ws.mat(B, n), S = ws.mat(B, SK);
+    DMat RI = ws.mat(B, n), Gs = ws.mat(B, std::max<int64_t>(mn, 1));
     DMat Kinv = ws.mat(B, B), Gi = ws.mat(B, std::max<int64_t>(mn, 1));
     DMat Upd = ws.mat(std::max<int64_t>(mn, 1), B);
     const int nblk0 = (int)cdiv(n, CRP_W);
@@ -730,31 +737,29 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     int32_t* d_pcol = d_prow + pstride;
     const size_t mark1 = ws.mark();
 
-    const size_t rd_smem = ((size_t)2 * RD_MAX_B * SK + SK) * 4;
+    const size_t rd_smem = ((size_t)2 * RD_MAX_B * SK + (size_t)RD_BATCH * SK) * 4;
     const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + 2 * (size_t)CRP_G * CRP_KMAX) * 4;
     static bool attrs = false;
     if (!attrs) {
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_crp_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crp_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_pair2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * CRP_KMAX * CRP_KMAX * 4)));
-        FFB_CUDA(cudaFuncSetAttribute(k_sketch_chunk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         FFB_CUDA(cudaFuncSetAttribute(k_crp_rowelim, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         attrs = true;
     }
     static const bool force_exact = getenv("FFB_PLDUQ_FORCE_FALLBACK") != nullptr;  // test hook
-    const bool sketch_ok = mn <= 200 * 1024 / 4;  // k_sketch_chunk keeps r entries in smem
 
     // Given the chunk's pivot rows (device dI: chunk-local rows, k of them, with
     // R_I in RI) and pivot column set dJ (ascending): pairing, Unew into Uhat
     // rows [r, r+k), old rows reduced at J, Uhat*Omega maintained when sketching.
     auto absorb = [&](int64_t r, int k, const int32_t* dI, const int32_t* dJ, int64_t c0,
-                      bool sketching, const int32_t* sigma_in) {
+                      bool sketching, const int32_t* sigma_in, DMat Sk) {
         DMat RIk = RI.sub(0, 0, k, n), Kik = Kinv.sub(0, 0, k, k);
         Kik.ld = k;
         {
             ProfScope ps(K_PQ_PAIR, st, 0.0, 0.0);
             k_pair2<<<1, 256, (size_t)3 * k * k * 4, st>>>(
-                f, RIk.ptr, RIk.ld, k, dJ, dI, c0, sketching ? S.ptr : nullptr, S.ld, SK, Kik.ptr,
+                f, RIk.ptr, RIk.ld, k, dJ, dI, c0, sketching ? Sk.ptr : nullptr, Sk.ld, SK, Kik.ptr,
                 UO.ptr, UO.ld, d_uhat_col, d_prow, d_pcol, r, dflag, sigma_in);
             ++g_launches;
             FFB_CHECK_LAUNCH();
@@ -774,7 +779,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     };
 
     int64_t r = 0;
-    bool exact = force_exact || !sketch_ok;
+    bool exact = force_exact;
     for (int attempt = 0; attempt < 2; ++attempt) {
         ws.release(mark1);
         r = 0;
@@ -791,13 +796,16 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             const int64_t bc = std::min<int64_t>(B, m - c0);
             DMat Yc = Y.sub(c0, 0, bc, n);
             if (!exact) {
-                DMat Sc = S.sub(0, 0, bc, SK);
-                {
-                    ProfScope ps(K_PQ_SKETCH, st, 2.0 * bc * SK * r, 0.0);
-                    k_sketch_chunk<<<(unsigned)bc, 160, (size_t)std::max<int64_t>(r, 1) * 4, st>>>(
-                        f, Sc.ptr, Sc.ld, YO.ptr, YO.ld, Y.ptr, Y.ld, UO.ptr, UO.ld, d_uhat_col, r,
-                        c0, SK);
-                    ++g_launches;
+                // sketch of the chunk residual, in place in its (otherwise unused)
+                // rows of Y*Omega: S = (Y Omega)_c - Y_c[:, pc] (Uhat Omega), a GEMM
+                DMat Sc = YO.sub(c0, 0, bc, SK);
+                if (r > 0) {
+                    DMat Gc = Gs.sub(0, 0, bc, r);
+                    {
+                        ProfScope ps(K_PQ_SKETCH, st, 0.0, 0.0);
+                        gather2d(st, Gc, Yc, nullptr, d_uhat_col, 0);
+                    }
+                    gemm(f, st, GEMM_SUB, Sc, Gc, false, UO.sub(0, 0, r, SK), false, bc, SK, r);
                 }
                 {
                     ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
@@ -822,6 +830,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, nullptr, nullptr,
                                                              0, lists[0], counts[0]);
                     ++g_launches;
+                }
+                {
+                    ProfScope ps(K_PQ_ROWELIM, st, 0.0, 0.0);
                     // RPM of R_I on the surviving candidate columns (1 CTA)
                     const int64_t maxc = (int64_t)nblk0 * k;
                     const size_t resmem = std::min<int64_t>((int64_t)k * maxc, RE_SMEM_WORDS) * 4;
@@ -830,7 +841,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     ++g_launches;
                     FFB_CHECK_LAUNCH();
                 }
-                absorb(r, k, dI, lists[1], c0, true, dsig);
+                absorb(r, k, dI, lists[1], c0, true, dsig, Sc);
                 r += k;
             } else {
                 // exact: residual of the whole chunk, then the row-sequential kernel
@@ -858,7 +869,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 if (k > 0) {
                     const int32_t* dI = io.upload(I);
                     gather_rows(st, RI.sub(0, 0, k, n), Rc, dI);
-                    absorb(r, k, dI, io.upload(J), c0, false, nullptr);
+                    absorb(r, k, dI, io.upload(J), c0, false, nullptr, DMat{});
                     r += k;
                 }
                 ws.release(mk);

@@ -108,9 +108,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-template <int BN>
+template <int BN, int ST = 0>
 struct TcCfg {
-    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr int STAGES = ST ? ST : (BN == 256 ? 4 : 6);
     static constexpr int A_BYTES = TC_BM * TC_BK;
     static constexpr int B_BYTES = BN * TC_BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -123,11 +123,11 @@ struct TcCfg {
                                       | ((uint32_t)(TC_BM >> 4) << 24);  // M
 };
 
-template <int BN>
+template <int BN, int ST>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_i8_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  uint32_t* __restrict__ C, int64_t ldc, int M, int N, int nk, Fp f, int mode) {
-    using Cfg = TcCfg<BN>;
+    using Cfg = TcCfg<BN, ST>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* sA = smem;
@@ -197,9 +197,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // acc in (-2^31, 2^31): (acc + 2^31) mod p by 32-bit Barrett, minus 2^31 mod p
         const Fp16 h(f.p);
         const uint32_t bias = (uint32_t)((0x80000000ull) % f.p);
+        const int rbase = m0 + 32 * q;
+        // the C slab is read before the accumulator is waited on (and, for the
+        // next slab, while this one is reduced): C traffic overlaps the MMAs
+        uint32_t cv[32];
+        auto load_c = [&](int c) {
+            const int col = n0 + c + lane;
+            const bool colok = col < N;
+#pragma unroll
+            for (int rr = 0; rr < 32; ++rr) {
+                const int row = rbase + rr;
+                cv[rr] = (mode != GEMM_SET && colok && row < M) ? __ldg(C + (int64_t)row * ldc + col) : 0u;
+            }
+        };
+        load_c(0);
         mbar_wait(accfull, 0);
         tc_fence_after();
-        const int rbase = m0 + 32 * q;
         for (int c = 0; c < BN; c += 32) {
             if (n0 + c >= N) break;
             uint32_t r[32];
@@ -212,14 +225,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             __syncwarp();
             const int col = n0 + c + lane;
             const bool colok = col < N;
-            uint32_t cv[32];
-            if (mode != GEMM_SET) {
-#pragma unroll
-                for (int rr = 0; rr < 32; ++rr) {
-                    const int row = rbase + rr;
-                    cv[rr] = (colok && row < M) ? __ldg(C + (int64_t)row * ldc + col) : 0u;
-                }
-            }
 #pragma unroll
             for (int rr = 0; rr < 32; ++rr) {
                 const int row = rbase + rr;
@@ -232,6 +237,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     C[(int64_t)row * ldc + col] = o;
                 }
             }
+            if (c + 32 < BN && n0 + c + 32 < N) load_c(c + 32);
             __syncwarp();
         }
     }
@@ -590,18 +596,18 @@ void pack(cudaStream_t st, int8_t* dst, int64_t ldd, DMat src, bool trans, int64
     FFB_CHECK_LAUNCH();
 }
 
-template <int BN>
+template <int BN, int ST = 0>
 void launch_tc(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, DMat C, int64_t M,
                int64_t N, int64_t nk, const Fp& f, int mode) {
-    using Cfg = TcCfg<BN>;
+    using Cfg = TcCfg<BN, ST>;
     static bool attr = false;
     if (!attr) {
-        FFB_CUDA(cudaFuncSetAttribute(k_gemm_i8_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        FFB_CUDA(cudaFuncSetAttribute(k_gemm_i8_tc<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       Cfg::SMEM));
         attr = true;
     }
     dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, TC_BM));
-    k_gemm_i8_tc<BN><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ma, mb, C.ptr, C.ld, (int)M, (int)N,
+    k_gemm_i8_tc<BN, ST><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ma, mb, C.ptr, C.ld, (int)M, (int)N,
                                                           (int)nk, f, mode);
     ++g_launches;
     FFB_CHECK_LAUNCH();
@@ -612,7 +618,8 @@ void launch_tc(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, DM
 bool tc_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K) {
     static const bool disabled = getenv("FFB_DISABLE_TC") != nullptr;
     if (disabled) return false;
-    const bool shape = M >= 64 && N >= 64 && K >= 16 && (double)M * N * K >= 1.0e6 &&
+    // small M is fine: TMA zero-fills the rows of the A box beyond M
+    const bool shape = M >= 8 && N >= 64 && K >= 16 && (double)M * N * K >= 1.0e6 &&
                        M < (1ll << 30) && N < (1ll << 30);
     if (f.p <= 255) return shape && K <= 120000;
     return f.p < (1u << 23) && shape && K <= 40000;  // int8 limbs: 3 * 2^14 * K < 2^31
@@ -652,7 +659,7 @@ void tc_gemm_limb(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, b
         FFB_CUDA(cudaFuncSetAttribute(k_gemm_limb_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, LB_SMEM));
         attr = true;
     }
-    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, 3.0 * (M * K + N * K) + 8.0 * M * N);
+    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, 3.0 * (M * K + N * K) + 8.0 * M * N, M, N, -K);
     CUtensorMap ma = make_map(Ap, 3 * Mr, Kp, TC_BM), mb = make_map(Bp, 3 * Nr, Kp, LB_BN);
     dim3 grid((unsigned)cdiv(N, LB_BN), (unsigned)cdiv(M, TC_BM));
     k_gemm_limb_tc<<<grid, TC_THREADS, LB_SMEM, st>>>(ma, mb, C.ptr, C.ld, (int)M, (int)N,
@@ -691,8 +698,11 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
     }
     const int64_t nk = cdiv(Kp, TC_BK);
     const bool wide = N >= 256 && M * N >= (int64_t)148 * 128 * 256;
-    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, (double)M * K + N * K + 8.0 * M * N);
-    if (wide) {
+    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, (double)M * K + N * K + 8.0 * M * N, M, N, K);
+    if (nk <= 2) {  // short K: epilogue-bound, 2 CTAs per SM (2-stage pipeline)
+        CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, 128);
+        launch_tc<128, 2>(st, ma, mb, C, M, N, nk, f, mode);
+    } else if (wide) {
         CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, 256);
         launch_tc<256>(st, ma, mb, C, M, N, nk, f, mode);
     } else {

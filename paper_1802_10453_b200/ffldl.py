@@ -378,7 +378,7 @@ class Context:
         return int(lib().ffb_sync_count(self.handle))
 
     KERNEL_CLASSES = ("gemm", "leaf", "plduq_rowdetect_seq", "trsm", "move", "other", "plduq_sketch",
-                      "plduq_crp", "plduq_pair", "ldu", "pack")
+                      "plduq_crp", "plduq_pair", "ldu", "pack", "plduq_rowelim")
 
     def profile(self, enable: bool = True) -> None:
         """Per-kernel-class CUDA-event timing of subsequent calls (resets totals)."""

@@ -12,7 +12,11 @@ pytestmark = pytest.mark.gpu
 
 @pytest.mark.parametrize("m,n,k", [(128, 128, 128), (256, 512, 256), (300, 500, 700),
                                    (129, 257, 65), (1000, 64, 200), (64, 1000, 3000),
-                                   (513, 300, 20000)])
+                                   (513, 300, 20000),
+                                   # small M (rows beyond M are TMA zero-fill) and short K
+                                   # (the 2-stage, two-CTAs-per-SM variant)
+                                   (8, 4096, 1024), (17, 3000, 500), (100, 2048, 64),
+                                   (1000, 3000, 16), (700, 2500, 250)])
 @pytest.mark.parametrize("p", [131, 251, 2, 3])
 def test_tc_gemm_nn(gpu, oracle, m, n, k, p):
     import paper_1802_10453_b200 as ffb
@@ -52,7 +56,8 @@ def test_tc_gemm_transposed_operands(gpu, oracle, n, k):
     assert np.array_equal(ffb.syrdk_sub(c, g, d, p, ctx=gpu), oracle.syrdk_sub(p, c, g, kind, val, val2))
 
 
-@pytest.mark.parametrize("m,n,k", [(128, 64, 128), (300, 500, 700), (129, 257, 65), (513, 300, 8000)])
+@pytest.mark.parametrize("m,n,k", [(128, 64, 128), (300, 500, 700), (129, 257, 65), (513, 300, 8000),
+                                   (9, 4000, 600)])
 @pytest.mark.parametrize("p", [8388593, 65521, 1000003, 257])
 def test_tc_limb_gemm(gpu, oracle, m, n, k, p):
     """int8-limb tcgen05 path (255 < p < 2^23): 9 limb products into 5 shift classes."""

@@ -13,7 +13,8 @@ for r in rows[hi + 1:]:
     if len(r) <= vi or r[mi] != "gpu__time_duration.sum":
         continue
     v = float(r[vi].replace(",", "")) * scale[r[ui]]
-    name = r[ki].split("(")[0].split("<")[0].replace("unnamed>::", "").replace("void ", "").strip()
+    name = r[ki].replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("void ", "")
+    name = name.split("(")[0].split("<")[0].strip().split("::")[-1]
     tot[name] += v
     cnt[name] += 1
 total = sum(tot.values())

@@ -19,7 +19,7 @@ from paper_1802_10453_b200 import configs  # noqa: E402
 from paper_1802_10453_b200.device import DeviceBuffers, ldlt_device  # noqa: E402
 
 
-def run(c, n, reps=2, threshold=64):
+def run(c, n, reps=int(os.environ.get("PROF_REPS", 2)), threshold=64):
     w = configs.CONFIGS[c].scaled(n)
     ctx = ffb.default_context(0)
     a0 = configs.generate_device(w, ctx)

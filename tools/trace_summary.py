@@ -1,0 +1,26 @@
+"""Summarise an FFB_PROF_TRACE file: per-class totals and GEMM time by (path, shape bucket)."""
+import math
+import sys
+from collections import defaultdict
+
+NAMES = ["gemm", "leaf", "rowdet", "trsm", "move", "other", "sketch", "crp", "pair", "ldu", "pack",
+         "rowelim"]
+recs = [l.split() for l in open(sys.argv[1])]
+g = [(int(c), int(m), int(n), int(k), float(t)) for c, m, n, k, t in recs]
+tot = defaultdict(float)
+for c, m, n, k, t in g:
+    tot[NAMES[c]] += t
+print({k: round(v, 1) for k, v in sorted(tot.items(), key=lambda x: -x[1])}, round(sum(tot.values()), 1))
+agg = defaultdict(lambda: [0, 0.0, 0.0])
+for c, m, n, k, t in g:
+    if c != 0:
+        continue
+    pth = "simt" if m < 0 else ("limb" if k < 0 else "i8")
+    m, k = abs(m), abs(k)
+    b = lambda x: 2 ** int(math.log2(max(x, 1)))
+    a = agg[(pth, b(m), b(n), b(k))]
+    a[0] += 1
+    a[1] += t
+    a[2] += 2 * m * n * k
+for key, (cnt, t, ops) in sorted(agg.items(), key=lambda x: -x[1][1])[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
+    print(key, cnt, round(t, 2), "ms", round(ops / t / 1e9, 1), "TOPS", round(t / cnt * 1000, 1), "us/call")
