@@ -91,6 +91,24 @@ __host__ __device__ inline uint32_t fmul(const Fp& f, uint32_t a, uint32_t b) {
 #endif
     return red64(f, (uint64_t)a * b);
 }
+// x mod p for x < 2^32 when p < 2^16 (f.mu32 set): 32-bit Barrett, one correction.
+__device__ __forceinline__ uint32_t red32(const Fp& f, uint32_t x) {
+    const uint32_t q = __umulhi(x, f.mu32);
+    const uint32_t r = x - q * f.p;
+    return r >= f.p ? r - f.p : r;
+}
+// d - c v mod p with one reduction when p < 2^16 (d + (p - c) v < p^2 < 2^32).
+__host__ __device__ inline uint32_t fmsub(const Fp& f, uint32_t d, uint32_t c, uint32_t v) {
+#ifdef __CUDA_ARCH__
+    if (f.mu32) {
+        const uint32_t x = d + (f.p - c) * v;
+        const uint32_t q = __umulhi(x, f.mu32);
+        const uint32_t r = x - q * f.p;
+        return r >= f.p ? r - f.p : r;
+    }
+#endif
+    return fsub(f, d, fmul(f, c, v));
+}
 // a/2 for odd p (field.hpp:121-124).
 __host__ __device__ inline uint32_t fhalve(const Fp& f, uint32_t a) {
     return (a & 1) ? (uint32_t)(((uint64_t)a + f.p) >> 1) : (a >> 1);
@@ -151,6 +169,43 @@ __device__ __forceinline__ void load_tile(uint32_t* dst, int ldd, const uint32_t
             }
         }
     }
+}
+
+// One-shot TMA bulk copy (cp.async.bulk) global -> shared of a contiguous
+// range, completed on an mbarrier; used by the single-CTA latency kernels to
+// stage their whole input with one instruction instead of rounds of loads.
+// Requirements: dst, src and bytes multiples of 16.  Call with all threads.
+__device__ __forceinline__ void bulk_stage(void* dst, const void* src, uint32_t bytes,
+                                           uint64_t* bar) {
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(bar);
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(b));
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes)
+                     : "memory");
+        for (uint32_t off = 0; off < bytes; off += 32768u) {
+            const uint32_t len = bytes - off < 32768u ? bytes - off : 32768u;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    (uint32_t)__cvta_generic_to_shared((char*)dst + off)),
+                "l"((const char*)src + off), "r"(len), "r"(b)
+                : "memory");
+        }
+    }
+    __syncthreads();  // barrier initialised before anyone waits on it
+    asm volatile(
+        "{\n"
+        ".reg .pred P1;\n"
+        "BULK_WAIT:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n"
+        "@P1 bra BULK_DONE;\n"
+        "bra BULK_WAIT;\n"
+        "BULK_DONE:\n"
+        "}\n" ::"r"(b)
+        : "memory");
+}
+__host__ __device__ inline bool bulk_ok(const void* src, size_t bytes) {
+    return ((uintptr_t)src & 15) == 0 && (bytes & 15) == 0;
 }
 
 // ---------------------------------------------------------------------------

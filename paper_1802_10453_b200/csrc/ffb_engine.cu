@@ -1037,3 +1037,17 @@ int ffb_syr2k_sub(ffb_context* c, uint64_t p, size_t n, size_t k, uint64_t* cc, 
 }
 
 }  // extern "C"
+
+// Debug-only export (not declared in include/ffldl_b200.h): PLDUQ kernel
+// micro-benchmark on a host matrix (tools/pq_kernel_bench.py).
+extern "C" int ffb_dbg_pq_bench(ffb_context* c, uint64_t p, int which, int rows, int cols,
+                                const uint32_t* host, int reps, double* ms, int32_t* out) {
+    return guarded(c, [&] {
+        Fp f = make_field(c, p);
+        uint32_t* d;
+        FFB_CUDA(cudaMalloc(&d, (size_t)rows * cols * 4));
+        FFB_CUDA(cudaMemcpy(d, host, (size_t)rows * cols * 4, cudaMemcpyHostToDevice));
+        dbg_pq_bench(f, c->stream, which, rows, cols, d, reps, ms, out);
+        FFB_CUDA(cudaFree(d));
+    });
+}

@@ -26,6 +26,7 @@
 // pr_k > t  (plus nonzero LDU pivots) accepts exactly the reference's output.
 // On rejection (probability ~ p^-16 per chunk) the search is redone with the
 // exact row-sequential kernel.
+#include <type_traits>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -77,253 +78,291 @@ inline dim3 rgrid(int64_t rows, int64_t cols) {
 // vector is arbitrary (any nonzero entry), only independence matters.
 // out: out[0] = k, out[1..k] = independent rows (ascending).
 // ---------------------------------------------------------------------------
+// ---------------------------------------------------------------------------
+// Batch reduction against a fully reduced basis (row detection and CRP):
+//   X[r][j] = X0[r][j] - sum_{t<kb} CF[r][t] E[t][j]   (r < nr <= 32, j < len <= 32 NQ)
+// and bit r of *mask is set when row r stays nonzero.  Warp w owns the row
+// pairs (2w, 2w+1), (2w+2nw, ...); lane l the components l + 32q, so every
+// thread keeps 2 NQ independent accumulators and each E load feeds two MACs.
+// MODE 0: 32-bit lazy sums (kb p^2 < 2^31), 1: 64-bit lazy (p < 2^26), 2: reduce per term.
+// X may alias X0 (each element is read and written by the same thread).
+// ---------------------------------------------------------------------------
+template <int NQ, int MODE>
+__device__ __forceinline__ void reduce_rows(const Fp& f, uint32_t* X, int ldx, const uint32_t* X0,
+                                            int ldx0, const uint32_t* CF, int ldcf,
+                                            const uint32_t* E, int lde, int nr, int len, int kb,
+                                            unsigned* mask) {
+    using Acc = typename std::conditional<MODE == 0, uint32_t, uint64_t>::type;
+    const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int ra = 2 * wp; ra < nr; ra += 2 * nw) {
+        const int rb = ra + 1;
+        const bool hb = rb < nr;
+        Acc a0[NQ], a1[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) a0[q] = a1[q] = 0;
+        const uint32_t* cfa = CF + (size_t)ra * ldcf;
+        const uint32_t* cfb = CF + (size_t)(hb ? rb : ra) * ldcf;
+        for (int t = 0; t < kb; ++t) {
+            const uint32_t ca = cfa[t], cb = cfb[t];
+            const uint32_t* et = E + (size_t)t * lde;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int j = lane + 32 * q;
+                const uint32_t e = j < len ? et[j] : 0u;
+                if (MODE == 2) {
+                    a0[q] = red64(f, (uint64_t)a0[q] + (uint64_t)ca * e);
+                    a1[q] = red64(f, (uint64_t)a1[q] + (uint64_t)cb * e);
+                } else {
+                    a0[q] += (Acc)ca * e;
+                    a1[q] += (Acc)cb * e;
+                }
+            }
+        }
+        int nza = 0, nzb = 0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int j = lane + 32 * q;
+            if (j < len) {
+                const uint32_t xa = fsub(f, X0[(size_t)ra * ldx0 + j],
+                                         MODE == 0 ? red32(f, (uint32_t)a0[q]) : red64(f, (uint64_t)a0[q]));
+                X[(size_t)ra * ldx + j] = xa;
+                nza |= xa != 0;
+                if (hb) {
+                    const uint32_t xb = fsub(f, X0[(size_t)rb * ldx0 + j],
+                                             MODE == 0 ? red32(f, (uint32_t)a1[q]) : red64(f, (uint64_t)a1[q]));
+                    X[(size_t)rb * ldx + j] = xb;
+                    nzb |= xb != 0;
+                }
+            }
+        }
+        nza = __any_sync(0xffffffffu, nza);
+        nzb = __any_sync(0xffffffffu, nzb);
+        if (lane == 0 && (nza || nzb)) atomicOr(mask, (nza ? 1u << ra : 0u) | (nzb ? 1u << rb : 0u));
+    }
+}
+template <int NQ>
+__device__ __forceinline__ void reduce_rows_any(const Fp& f, uint32_t* X, int ldx, const uint32_t* X0,
+                                                int ldx0, const uint32_t* CF, int ldcf,
+                                                const uint32_t* E, int lde, int nr, int len, int kb,
+                                                unsigned* mask) {
+    if (f.p < 4096u && kb <= 128)
+        reduce_rows<NQ, 0>(f, X, ldx, X0, ldx0, CF, ldcf, E, lde, nr, len, kb, mask);
+    else if (f.p < (1u << 26))
+        reduce_rows<NQ, 1>(f, X, ldx, X0, ldx0, CF, ldcf, E, lde, nr, len, kb, mask);
+    else
+        reduce_rows<NQ, 2>(f, X, ldx, X0, ldx0, CF, ldcf, E, lde, nr, len, kb, mask);
+}
+
 constexpr int RD_MAX_B = 128, RD_S = 144;
 
 constexpr int RD_BATCH = 16;
+
+// Blocked insertion of the flagged vectors of a reduced batch into a fully
+// reduced basis.  V holds nr <= 32 vectors (stride ldv, length len), each
+// already reduced against E (kb rows of stride len, pivots rho); bits of
+// `pend` mark the nonzero ones.  Pass 1 walks the flagged vectors in order:
+// a vector still nonzero gets its leading entry as pivot, which is eliminated
+// from the other live vectors of the batch only (one barrier per vector).
+// Pass 2 applies all new pivots to the basis at once,
+//   E <- E - E[:, piv] N   (N = normalised new vectors, coefficients by shuffle),
+// and appends N.  Returns the count; ins[a] = batch index of the a-th new vector.
+// At most kmax - kb vectors are inserted.  Uniform control flow; 256 threads.
+// ---------------------------------------------------------------------------
+struct BatchScratch {
+    int ins[32];
+    int piv[32];
+    uint32_t il[32];
+};
+template <int NQ>
+__device__ int batch_insert(const Fp& f, const SmemInv& inv, uint32_t* V, int ldv, unsigned pend,
+                            int len, uint32_t* E, int kb, int kmax, int* rho, BatchScratch& bs) {
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    int cnt = 0;
+    unsigned done = 0;
+    while (pend && kb + cnt < kmax) {
+        const int r = __ffs(pend) - 1;
+        pend &= pend - 1;
+        const uint32_t* v = V + (size_t)r * ldv;
+        // leading entry, found by every warp with ballots (v is stable: the last
+        // write to it was before the previous insertion's barrier)
+        int rh = len;
+#pragma unroll
+        for (int qq = 0; qq < NQ; ++qq) {
+            const int j = lane + 32 * qq;
+            const unsigned bal = __ballot_sync(0xffffffffu, j < len && v[j] != 0);
+            if (bal && rh == len) rh = 32 * qq + __ffs(bal) - 1;
+        }
+        if (rh >= len) continue;  // dependent on the vectors inserted before it (uniform)
+        const uint32_t il = inv(f, v[rh]);
+        {  // live batch vectors (inserted and pending): the rk-th one goes to warp rk mod 8
+            const unsigned live = done | pend;
+            const bool has = (live >> lane) & 1;
+            const int rank = __popc(live & ((1u << lane) - 1));
+            const int nlive = __popc(live);
+            for (int rk = wp; rk < nlive; rk += 8) {
+                const int q = __ffs(__ballot_sync(0xffffffffu, has && rank == rk)) - 1;
+                uint32_t* dst = V + (size_t)q * ldv;
+                const uint32_t c = dst[rh];
+                __syncwarp();
+                if (c) {
+                    const uint32_t cn = fmul(f, c, il);
+#pragma unroll
+                    for (int qq = 0; qq < NQ; ++qq) {
+                        const int j = lane + 32 * qq;
+                        if (j < len) dst[j] = fmsub(f, dst[j], cn, v[j]);
+                    }
+                }
+            }
+        }
+        if (tid == 0) {
+            bs.ins[cnt] = r;
+            bs.piv[cnt] = rh;
+            bs.il[cnt] = il;
+        }
+        done |= 1u << r;
+        ++cnt;
+        __syncthreads();
+    }
+    if (cnt == 0) return 0;
+    // pass 2: E <- E - E[:, piv] N, row t by warp t mod 8, lane a holds coefficient a
+    const bool small = f.p < 4096u;
+    for (int t = wp; t < kb; t += 8) {
+        uint32_t* et = E + (size_t)t * len;
+        const uint32_t ct = lane < cnt ? fmul(f, et[bs.piv[lane]], bs.il[lane]) : 0u;
+        __syncwarp();
+        uint64_t acc[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) acc[q] = 0;
+        for (int a = 0; a < cnt; ++a) {
+            const uint32_t ca = __shfl_sync(0xffffffffu, ct, a);
+            if (!ca) continue;  // warp-uniform
+            const uint32_t* na = V + (size_t)bs.ins[a] * ldv;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int j = lane + 32 * q;
+                const uint64_t prod = (uint64_t)ca * (j < len ? na[j] : 0u);
+                acc[q] = small ? acc[q] + prod : (uint64_t)red64(f, acc[q] + prod);
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int j = lane + 32 * q;
+            if (j < len) et[j] = fsub(f, et[j], red64(f, acc[q]));
+        }
+    }
+    // append the normalised new vectors
+    for (int a = wp; a < cnt; a += 8) {
+        const uint32_t* na = V + (size_t)bs.ins[a] * ldv;
+        const uint32_t il = bs.il[a];
+        uint32_t* dst = E + (size_t)(kb + a) * len;
+        for (int j = lane; j < len; j += 32) dst[j] = fmul(f, na[j], il);
+    }
+    if (tid < cnt) rho[kb + tid] = bs.piv[tid];
+    __syncthreads();
+    return cnt;
+}
+
+// Row rank profile of a b x s chunk sketch (b <= 128, s <= 160), 1 CTA.
+// Batches of 16 rows are reduced against the basis in parallel; a row that
+// reduces to zero lies in the span of earlier rows and is dependent for good,
+// so only the flagged rows go through the sequential insertion.
+// out[0] = k, out[1..k] = independent rows (ascending).
 __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int64_t lds, int b,
                                                     int s, int32_t* out) {
-    extern __shared__ uint32_t sm[];
+    extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* Ss = sm;                          // b x s
     uint32_t* E = Ss + (size_t)RD_MAX_B * s;    // basis rows (fully reduced)
     uint32_t* V = E + (size_t)RD_MAX_B * s;     // RD_BATCH reduced rows of the current batch
     __shared__ int rho[RD_MAX_B];
-    __shared__ uint32_t coef[RD_MAX_B];
     __shared__ uint32_t cfb[RD_BATCH][RD_MAX_B];  // batch coefficients S_i[rho_t]
-    __shared__ uint32_t vcol[RD_BATCH];
-    __shared__ int flag[RD_BATCH];
-    __shared__ int rhs;
-    __shared__ uint32_t ils;
+    __shared__ unsigned fmask[2];
+    __shared__ BatchScratch bs;
     __shared__ uint32_t sinv[SINV_MAX];
+    __shared__ uint64_t bar;
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-    load_tile<8>(Ss, s, S, lds, b, s);
-    if (tid == 0) rhs = s;
+    if (lds == s && bulk_ok(S, (size_t)b * s * 4))
+        bulk_stage(Ss, S, (uint32_t)((size_t)b * s * 4), &bar);
+    else
+        load_tile<16>(Ss, s, S, lds, b, s);
     const SmemInv inv = stage_inverses(f, sinv);
     __syncthreads();
-    int k = 0;
-    for (int i0 = 0; i0 < b; i0 += RD_BATCH) {
+    int k = 0, bi = 0;
+    for (int i0 = 0; i0 < b; i0 += RD_BATCH, ++bi) {
         const int nr = min(RD_BATCH, b - i0);
-        // 1. reduce the whole batch against the basis (parallel)
         for (int r = wp; r < nr; r += 8)
             for (int t = lane; t < k; t += 32) cfb[r][t] = Ss[(size_t)(i0 + r) * s + rho[t]];
-        if (tid < RD_BATCH) flag[tid] = 0;
+        if (tid == 0) fmask[bi & 1] = 0;
         __syncthreads();
-        for (int r = wp; r < nr; r += 8) {
-            const uint32_t* si = Ss + (size_t)(i0 + r) * s;
-            int nz = 0;
-            for (int j = lane; j < s; j += 32) {
-                uint64_t acc = 0;
-                if (f.p < (1u << 26)) {
-                    for (int t = 0; t < k; ++t) acc += (uint64_t)cfb[r][t] * E[(size_t)t * s + j];
-                } else {
-                    for (int t = 0; t < k; ++t) acc = red64(f, acc + (uint64_t)cfb[r][t] * E[(size_t)t * s + j]);
-                }
-                const uint32_t x = fsub(f, si[j], red64(f, acc));
-                V[(size_t)r * s + j] = x;
-                nz |= x != 0;
-            }
-            nz = __any_sync(0xffffffffu, nz);
-            if (lane == 0) flag[r] = nz;
-        }
+        reduce_rows_any<5>(f, V, s, Ss + (size_t)i0 * s, s, &cfb[0][0], RD_MAX_B, E, s, nr, s, k,
+                           &fmask[bi & 1]);
         __syncthreads();
-        // 2. flagged rows in order: exact re-check, then insertion
-        for (int r = 0; r < nr; ++r) {
-            if (!flag[r]) continue;  // in the span of the basis at batch start (uniform)
-            uint32_t* vr = V + (size_t)r * s;
-            int nz = 0;
-            for (int j = tid; j < s; j += blockDim.x) nz |= vr[j] != 0;
-            if (!__syncthreads_or(nz)) continue;  // made dependent by an earlier batch row
-            for (int j = tid; j < s; j += blockDim.x)
-                if (vr[j]) atomicMin(&rhs, j);
-            __syncthreads();
-            const int rh = rhs;
-            if (tid == 0) ils = inv(f, vr[rh]);
-            __syncthreads();
-            const uint32_t il = ils;
-            for (int j = tid; j < s; j += blockDim.x) vr[j] = fmul(f, vr[j], il);
-            for (int t = tid; t < k; t += blockDim.x) coef[t] = E[(size_t)t * s + rh];
-            for (int q = r + 1 + tid; q < nr; q += blockDim.x) vcol[q] = V[(size_t)q * s + rh];
-            __syncthreads();
-            // full reduction: E rows and the later batch rows lose column rh
-            // ((vector, component) pairs over all warps)
-            {
-                const int nrows = k + (nr - r - 1);
-                for (int rr = wp; rr < nrows; rr += 8) {
-                    uint32_t* dst;
-                    uint32_t c;
-                    if (rr < k) {
-                        dst = E + (size_t)rr * s;
-                        c = coef[rr];
-                    } else {
-                        const int q = r + 1 + (rr - k);
-                        dst = V + (size_t)q * s;
-                        c = vcol[q];
-                    }
-                    if (!c) continue;  // warp-uniform
-                    for (int j = lane; j < s; j += 32) dst[j] = fsub(f, dst[j], fmul(f, c, vr[j]));
-                }
-            }
-            for (int j = tid; j < s; j += blockDim.x) E[(size_t)k * s + j] = vr[j];
-            if (tid == 0) {
-                rho[k] = rh;
-                out[1 + k] = i0 + r;
-                rhs = s;
-            }
-            __syncthreads();
-            ++k;
-        }
+        const unsigned pending = fmask[bi & 1];  // rows outside the span of the batch-start basis
+        if (!pending) continue;
+        const int cnt = batch_insert<5>(f, inv, V, s, pending, s, E, k, s, rho, bs);
+        if (tid < cnt) out[1 + k + tid] = i0 + bs.ins[tid];  // inserted in row order
+        k += cnt;
     }
     if (tid == 0) out[0] = k;
 }
 
 // ---------------------------------------------------------------------------
-// Column rank profile (CRP) of RI (k x n) by a reduction tree.  Each CTA scans
-// an ordered set of columns and keeps those independent of the earlier
-// columns of the set (a local CRP).  A column dropped at any level depends on
-// earlier columns, so it is dependent globally too, and the CRP of a union of
-// surviving sets equals the CRP of the union of the underlying column ranges.
-// Level 0 (range mode): CTA g scans columns [g*CRP_W, (g+1)*CRP_W).
-// Level > 0 (list mode): CTA g scans the concatenation of input lists
-// g*fan .. g*fan+fan-1 (each <= k columns, ascending).  Output: out[g*k + t],
-// ocount[g].  The last level (one CTA) yields the CRP J.
+// Candidate columns for the column rank profile of RI (k x n): CTA g scans
+// columns [g*CRP_W, (g+1)*CRP_W) in groups of CRP_G and keeps those
+// independent of the earlier columns of its range (a local CRP).  A dropped
+// column depends on earlier columns, so it is dependent globally too: the
+// union of the kept lists contains the CRP J.  Output out[g*k + t], ocount[g].
 // ---------------------------------------------------------------------------
-constexpr int CRP_W = 256, CRP_G = 32, CRP_KMAX = 128, CRP_FAN = 8;
+constexpr int CRP_W = 256, CRP_G = 32, CRP_KMAX = 128;
 
-__global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int64_t ldr, int k,
-                                                  int64_t n, const int32_t* in, const int32_t* icount,
-                                                  int nin, int32_t* out, int32_t* ocount) {
+__global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* __restrict__ RI, int64_t ldr,
+                                                  int k, int64_t n, int32_t* out, int32_t* ocount) {
     extern __shared__ uint32_t sm[];
     uint32_t* E = sm;                           // basis: up to k vectors of length k
     uint32_t* V = E + (size_t)CRP_KMAX * k;     // CRP_G columns, each length k: V[c*k + i]
     uint32_t* VC = V + (size_t)CRP_G * k;       // CRP_G x CRP_KMAX gathered coefficients
     __shared__ int rho[CRP_KMAX];
-    __shared__ int colid[CRP_G];
-    __shared__ int nb;
-    __shared__ int nzmask[CRP_G];
-    __shared__ int total;
-    __shared__ uint32_t qcoef[CRP_G];
-    __shared__ uint32_t coefs[CRP_KMAX];
-    __shared__ int lead;
+    __shared__ unsigned fmask[2];
+    __shared__ BatchScratch bs;
     __shared__ uint32_t sinv[SINV_MAX];
-    const int tid = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     const int g = blockIdx.x;
+    const int64_t c0 = (int64_t)g * CRP_W;
+    const int total = (int)std::min<int64_t>(CRP_W, n - c0);
     const SmemInv inv = stage_inverses(f, sinv);
-    // the ordered column set of this CTA
-    auto column_at = [&](int idx) -> int {
-        if (!in) return g * CRP_W + idx;
-        int q = idx;
-        for (int l = g * CRP_FAN; l < g * CRP_FAN + CRP_FAN && l < nin; ++l) {
-            const int c = icount[l];
-            if (q < c) return in[(int64_t)l * k + q];
-            q -= c;
+    // group prefetch: thread (wp, lane) holds rows wp + 8u of column lane
+    uint32_t vv[CRP_KMAX / 8];
+    auto fetch = [&](int s0) {
+        const bool ok = s0 + lane < total;
+        const uint32_t* src = RI + c0 + s0 + lane;
+#pragma unroll
+        for (int u = 0; u < CRP_KMAX / 8; ++u) {
+            const int i = wp + 8 * u;
+            vv[u] = (ok && i < k) ? __ldg(src + (int64_t)i * ldr) : 0u;
         }
-        return -1;
     };
-    if (tid == 0) {
-        nb = 0;
-        lead = k;
-        if (!in) {
-            const int64_t c0 = (int64_t)g * CRP_W;
-            total = (int)((c0 + CRP_W < n ? c0 + CRP_W : n) - c0);
-        } else {
-            int t = 0;
-            for (int l = g * CRP_FAN; l < g * CRP_FAN + CRP_FAN && l < nin; ++l) t += icount[l];
-            total = t;
-        }
-    }
-    __syncthreads();
-    for (int s0 = 0; s0 < total && nb < k; s0 += CRP_G) {
-        const int gw = (s0 + CRP_G <= total) ? CRP_G : total - s0;
-        if (tid < gw) colid[tid] = column_at(s0 + tid);
-        if (tid < CRP_G) nzmask[tid] = 0;
-        __syncthreads();
-        {  // warp w loads rows w, w+8, ... (4 in flight), lane = column of the group
-            const int lane = tid & 31, wp = tid >> 5;
-            for (int i0 = wp; i0 < k; i0 += 32) {
-                uint32_t vv[4];
+    fetch(0);
+    int nb = 0, gi = 0;
+    for (int s0 = 0; s0 < total && nb < k; s0 += CRP_G, ++gi) {
+        const int gw = min(CRP_G, total - s0);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = i0 + 8 * u;
-                    vv[u] = (i < k && lane < gw) ? __ldg(RI + (int64_t)i * ldr + colid[lane]) : 0u;
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int i = i0 + 8 * u;
-                    if (i < k && lane < gw) V[(size_t)lane * k + i] = vv[u];
-                }
-            }
+        for (int u = 0; u < CRP_KMAX / 8; ++u) {
+            const int i = wp + 8 * u;
+            if (i < k) V[(size_t)lane * k + i] = vv[u];
         }
+        if (s0 + CRP_G < total) fetch(s0 + CRP_G);  // overlaps this group's work
+        if (tid == 0) fmask[gi & 1] = 0;
         __syncthreads();
-        // reduce every column of the group against the current basis; flag the
-        // columns that stay nonzero (candidates for a new basis vector)
-        const int kb = nb;
-        {
-            const int lane = tid & 31, wp = tid >> 5;
-            for (int c = wp; c < gw; c += 8)  // coefficient gather
-                for (int t = lane; t < kb; t += 32) VC[(size_t)c * CRP_KMAX + t] = V[(size_t)c * k + rho[t]];
-        }
+        for (int c = wp; c < gw; c += 8)  // coefficients V[c][rho_t]
+            for (int t = lane; t < nb; t += 32) VC[(size_t)c * CRP_KMAX + t] = V[(size_t)c * k + rho[t]];
         __syncthreads();
-        for (int e = tid; e < CRP_G * CRP_KMAX; e += blockDim.x) {
-            const int c = e >> 7, i = e & (CRP_KMAX - 1);  // CRP_KMAX = 128
-            if (c >= gw || i >= k) continue;
-            const uint32_t* vc = VC + (size_t)c * CRP_KMAX;
-            uint64_t acc = 0;
-            if (f.p < (1u << 26)) {
-                for (int t = 0; t < kb; ++t) acc += (uint64_t)vc[t] * E[(size_t)t * k + i];
-            } else {
-                for (int t = 0; t < kb; ++t) acc = red64(f, acc + (uint64_t)vc[t] * E[(size_t)t * k + i]);
-            }
-            const uint32_t x = fsub(f, V[(size_t)c * k + i], red64(f, acc));
-            V[(size_t)c * k + i] = x;  // keep the reduced column (same thread reads/writes e)
-            if (x) atomicOr(&nzmask[c], 1);
-        }
+        // reduce the group against the basis; flagged columns are outside its span
+        reduce_rows_any<4>(f, V, k, V, k, VC, CRP_KMAX, E, k, gw, k, nb, &fmask[gi & 1]);
         __syncthreads();
-        // flagged columns in order, whole block: a column still nonzero after the
-        // insertions made earlier in this group becomes a basis vector; it is
-        // normalised and eliminated from the basis and from the later columns of
-        // the group, so every stored vector stays reduced against the basis.
-        int nbl = kb;
-        for (int c = 0; c < gw && nbl < k; ++c) {
-            if (!nzmask[c]) continue;  // in the span of the group-start basis (uniform)
-            const uint32_t* vc = V + (size_t)c * k;
-            for (int i = tid; i < k; i += blockDim.x)
-                if (vc[i]) atomicMin(&lead, i);
-            __syncthreads();
-            const int ld = lead;
-            if (ld >= k) continue;  // made dependent by an earlier column of the group
-            const uint32_t ilv = inv(f, vc[ld]);
-            for (int t = tid; t < nbl; t += blockDim.x) coefs[t] = E[(size_t)t * k + ld];
-            for (int q = c + 1 + tid; q < gw; q += blockDim.x) qcoef[q] = V[(size_t)q * k + ld];
-            __syncthreads();
-            {  // (vector, component) pairs over all warps: basis rows, then later columns
-                const int lane = tid & 31, wp = tid >> 5;
-                const int nrows = nbl + (gw - c - 1);
-                for (int rr = wp; rr < nrows; rr += 8) {
-                    uint32_t* dst;
-                    uint32_t cc;
-                    if (rr < nbl) {
-                        dst = E + (size_t)rr * k;
-                        cc = coefs[rr];
-                    } else {
-                        const int q = c + 1 + (rr - nbl);
-                        dst = V + (size_t)q * k;
-                        cc = qcoef[q];
-                    }
-                    if (!cc) continue;  // warp-uniform
-                    const uint32_t ccn = fmul(f, cc, ilv);
-                    for (int i = lane; i < k; i += 32) dst[i] = fsub(f, dst[i], fmul(f, ccn, vc[i]));
-                }
-            }
-            for (int i = tid; i < k; i += blockDim.x) E[(size_t)nbl * k + i] = fmul(f, vc[i], ilv);
-            if (tid == 0) {
-                rho[nbl] = ld;
-                out[(int64_t)g * k + nbl] = colid[c];
-                lead = k;
-            }
-            __syncthreads();
-            ++nbl;
-        }
-        if (tid == 0) nb = nbl;
-        __syncthreads();
+        const unsigned pending = fmask[gi & 1];
+        if (!pending) continue;
+        const int cnt = batch_insert<4>(f, inv, V, k, pending, k, E, nb, k, rho, bs);
+        if (tid < cnt) out[(int64_t)g * k + nb + tid] = (int32_t)(c0 + s0 + bs.ins[tid]);
+        nb += cnt;
     }
     if (tid == 0) ocount[g] = nb;
 }
@@ -827,8 +866,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 {
                     ProfScope ps(K_PQ_CRP, st, 0.0, 0.0);
                     // level 0: local CRPs of 256-column blocks (parallel)
-                    k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, nullptr, nullptr,
-                                                             0, lists[0], counts[0]);
+                    k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, lists[0], counts[0]);
                     ++g_launches;
                 }
                 {
@@ -840,6 +878,15 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                                                           re_scratch, lists[1], dsig, dflag);
                     ++g_launches;
                     FFB_CHECK_LAUNCH();
+                }
+                static FILE* jtr = getenv("FFB_PLDUQ_JTRACE") ? fopen(getenv("FFB_PLDUQ_JTRACE"), "a") : nullptr;
+                if (jtr) {  // diagnostics: k, n, candidate count, pivot column positions
+                    const int32_t* hc = (const int32_t*)io.readback(counts[0], (size_t)nblk0 * 4);
+                    int64_t C = 0;
+                    for (int b = 0; b < nblk0; ++b) C += hc[b];
+                    const int32_t* hj = (const int32_t*)io.readback(lists[1], (size_t)k * 4);
+                    fprintf(jtr, "%d %lld %lld %lld %d %d %d\n", k, (long long)n, (long long)C, (long long)r,
+                            hj[0], hj[k / 2], hj[k - 1]);
                 }
                 absorb(r, k, dI, lists[1], c0, true, dsig, Sc);
                 r += k;
@@ -954,4 +1001,86 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     return out;
 }
 
+// ---------------------------------------------------------------------------
+// Kernel micro-benchmark (tools/pq_kernel_bench.py; not part of the C-ABI):
+//   which 0: row detection of S (rows x cols)         ms[0]
+//   which 1: CRP list, row elimination, pairing of R  ms[0..2]
+// on a device matrix, averaged over reps launches (CUDA events).
+// ---------------------------------------------------------------------------
+void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, const uint32_t* d_in,
+                  int reps, double* ms, int32_t* out_k) {
+    cudaEvent_t e[4];
+    for (auto& x : e) FFB_CUDA(cudaEventCreate(&x));
+    float t = 0;
+    if (which == 0) {
+        const size_t rd_smem = ((size_t)2 * RD_MAX_B * cols + (size_t)RD_BATCH * cols) * 4;
+        FFB_CUDA(cudaFuncSetAttribute(k_row_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
+        int32_t* info;
+        FFB_CUDA(cudaMalloc(&info, (2 * RD_MAX_B + 16) * 4));
+        k_row_detect<<<1, 256, rd_smem, st>>>(f, d_in, cols, rows, cols, info);
+        FFB_CUDA(cudaEventRecord(e[0], st));
+        for (int i = 0; i < reps; ++i) k_row_detect<<<1, 256, rd_smem, st>>>(f, d_in, cols, rows, cols, info);
+        FFB_CUDA(cudaEventRecord(e[1], st));
+        FFB_CUDA(cudaEventSynchronize(e[1]));
+        FFB_CUDA(cudaEventElapsedTime(&t, e[0], e[1]));
+        ms[0] = t / reps;
+        FFB_CUDA(cudaMemcpy(out_k, info, 4, cudaMemcpyDeviceToHost));
+        FFB_CUDA(cudaFree(info));
+    } else {
+        const int k = rows;
+        const int64_t n = cols;
+        const int nblk0 = (int)cdiv(n, CRP_W);
+        const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + 2 * (size_t)CRP_G * CRP_KMAX) * 4;
+        FFB_CUDA(cudaFuncSetAttribute(k_crp_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crp_smem));
+        FFB_CUDA(cudaFuncSetAttribute(k_crp_rowelim, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        FFB_CUDA(cudaFuncSetAttribute(k_pair2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * CRP_KMAX * CRP_KMAX * 4)));
+        int32_t *lists0, *counts0, *lists1, *dsig, *flag, *ucol, *prow, *pcol, *dI;
+        uint32_t *re_scratch, *Kinv;
+        FFB_CUDA(cudaMalloc(&lists0, (size_t)nblk0 * k * 4));
+        FFB_CUDA(cudaMalloc(&counts0, (size_t)nblk0 * 4));
+        FFB_CUDA(cudaMalloc(&lists1, (size_t)k * 4 + 64));
+        FFB_CUDA(cudaMalloc(&dsig, (size_t)k * 4 + 64));
+        FFB_CUDA(cudaMalloc(&flag, 64));
+        FFB_CUDA(cudaMalloc(&ucol, (size_t)k * 4 + 64));
+        FFB_CUDA(cudaMalloc(&prow, (size_t)k * 4 + 64));
+        FFB_CUDA(cudaMalloc(&pcol, (size_t)k * 4 + 64));
+        FFB_CUDA(cudaMalloc(&dI, (size_t)k * 4 + 64));
+        FFB_CUDA(cudaMalloc(&Kinv, (size_t)k * k * 4 + 64));
+        FFB_CUDA(cudaMalloc(&re_scratch, ((size_t)CRP_KMAX * nblk0 * CRP_KMAX + (size_t)nblk0 * CRP_KMAX + 64) * 4));
+        FFB_CUDA(cudaMemset(flag, 0, 64));
+        FFB_CUDA(cudaMemset(dI, 0, (size_t)k * 4));
+        const int64_t maxc = (int64_t)nblk0 * k;
+        const size_t resmem = std::min<int64_t>((int64_t)k * maxc, RE_SMEM_WORDS) * 4;
+        double acc[3] = {0, 0, 0};
+        for (int i = 0; i <= reps; ++i) {
+            FFB_CUDA(cudaEventRecord(e[0], st));
+            k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, d_in, n, k, n, lists0, counts0);
+            FFB_CUDA(cudaEventRecord(e[1], st));
+            k_crp_rowelim<<<1, 256, resmem, st>>>(f, d_in, n, k, lists0, counts0, nblk0, re_scratch, lists1, dsig, flag);
+            FFB_CUDA(cudaEventRecord(e[2], st));
+            k_pair2<<<1, 256, (size_t)3 * k * k * 4, st>>>(f, d_in, n, k, lists1, dI, 0, nullptr, 0, 0, Kinv,
+                                                             nullptr, 0, ucol, prow, pcol, 0, flag, dsig);
+            FFB_CUDA(cudaEventRecord(e[3], st));
+            FFB_CUDA(cudaEventSynchronize(e[3]));
+            if (i == 0) continue;  // warm-up
+            for (int j = 0; j < 3; ++j) {
+                FFB_CUDA(cudaEventElapsedTime(&t, e[j], e[j + 1]));
+                acc[j] += t;
+            }
+        }
+        for (int j = 0; j < 3; ++j) ms[j] = acc[j] / reps;
+        int32_t hf = 0;
+        FFB_CUDA(cudaMemcpy(&hf, flag, 4, cudaMemcpyDeviceToHost));
+        out_k[0] = hf;
+        FFB_CUDA(cudaMemcpy(out_k + 1, lists1, (size_t)k * 4, cudaMemcpyDeviceToHost));
+        FFB_CUDA(cudaMemcpy(out_k + 1 + k, dsig, (size_t)k * 4, cudaMemcpyDeviceToHost));
+        for (void* q : {(void*)lists0, (void*)counts0, (void*)lists1, (void*)dsig, (void*)flag, (void*)ucol,
+                        (void*)prow, (void*)pcol, (void*)dI, (void*)Kinv, (void*)re_scratch})
+            FFB_CUDA(cudaFree(q));
+    }
+    FFB_CHECK_LAUNCH();
+    for (auto& x : e) FFB_CUDA(cudaEventDestroy(x));
+}
+
 }  // namespace ffb
+

@@ -61,4 +61,8 @@ void copy_mat(cudaStream_t st, DMat dst, DMat src);
 // In-place LDU without pivoting (strict lower L, diagonal d, strict upper U).
 void ldu_inplace(const Fp& f, cudaStream_t st, DMat K, Workspace& ws, int32_t* fail);
 
+// Kernel micro-benchmark hook (see ffb_plduq.cu).
+void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, const uint32_t* d_in,
+                  int reps, double* ms, int32_t* out_k);
+
 }  // namespace ffb
