@@ -6,6 +6,8 @@
 // update has no index arithmetic and no shared-memory traffic for S.  The
 // pivot search of a step is a 64-bit ballot over the residual column masked
 // by the active rows; L is staged in shared memory and written to HBM once.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "ffb_kernels.cuh"
@@ -165,39 +167,79 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
     }
 }
 
-// Inverse of each 64 x 64 diagonal block of a unit lower triangular T,
-// row by row: row i of T^-1 = e_i - sum_{k<i} T[i][k] (row k of T^-1);
-// 4 threads per column split the k-sum.
-template <bool kSmall>
+// Inverse of the unit lower triangular 64x64 diagonal blocks of T, one CTA per
+// block, by recursive doubling: each warp inverts one 8x8 diagonal block by
+// forward substitution (warp-local), then three levels h = 8, 16, 32 fill the
+// off-diagonal blocks of every 2h x 2h diagonal block,
+//   inv([[A, 0], [C, B]]) = [[A^-1, 0], [-B^-1 (C A^-1), B^-1]],
+// as parallel products (two barriers per level instead of two per row).
+// Rows >= nb of a ragged last block are completed with the identity.
+// kMode 0: 32-bit sums (p < 4096), 1: 64-bit lazy (p < 2^23), 2: reduce per product.
+template <int kMode>
+__device__ __forceinline__ uint32_t dot_lt(const Fp& f, const uint32_t* a, int sa, const uint32_t* b, int sb,
+                                           int k0, int k1) {
+    if (kMode == 0) {
+        uint32_t acc = 0;
+        for (int k = k0; k < k1; ++k) acc += a[k * sa] * b[k * sb];
+        return red32(f, acc);
+    }
+    uint64_t acc = 0;
+    for (int k = k0; k < k1; ++k) {
+        const uint64_t prod = (uint64_t)a[k * sa] * b[k * sb];
+        acc = kMode == 1 ? acc + prod : (uint64_t)red64(f, acc + prod);
+    }
+    return red64(f, acc);
+}
+template <int kMode>
 __global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
                                                  int64_t n, uint32_t* Tinv) {
     __shared__ uint32_t Ts[64][65];
-    __shared__ uint32_t X[64][65];
-    __shared__ uint64_t part[4][64];
+    __shared__ uint32_t X[64][65];  // W = C A^-1 of a level is kept transposed in Ts's upper triangle
     const int b = blockIdx.x;
     const int64_t i0 = (int64_t)b * 64;
     const int nb = (int)std::min<int64_t>(64, n - i0);
-    const int tid = threadIdx.x, c = tid & 63, qd = tid >> 6;
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     load_tile<16>(&Ts[0][0], 65, T + i0 * ldt + i0, ldt, nb, nb);
     __syncthreads();
     for (int e = tid; e < 64 * 64; e += 256) {
         const int i = e >> 6, k = e & 63;
-        if (i >= nb || k >= i) Ts[i][k] = 0;
+        if (i >= nb || k >= i) Ts[i][k] = 0;  // strict lower part only (unit diagonal implied)
         X[i][k] = 0;
     }
     __syncthreads();
-    for (int i = 0; i < nb; ++i) {
-        uint64_t acc = 0;
-        for (int k = qd; k < i; k += 4) {
-            const uint64_t prod = (uint64_t)Ts[i][k] * X[k][c];
-            acc += kSmall ? prod : (uint64_t)red64(f, prod);
+    {  // 8x8 diagonal blocks: warp wp, lane l < 8 computes column 8wp + l
+        const int o = 8 * wp;
+        if (lane < 8) {
+            uint32_t x[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                uint64_t acc = 0;
+#pragma unroll
+                for (int k = 0; k < i; ++k) {
+                    const uint64_t prod = (uint64_t)Ts[o + i][o + k] * x[k];
+                    acc = kMode == 2 ? (uint64_t)red64(f, acc + prod) : acc + prod;
+                }
+                x[i] = fsub(f, i == lane ? 1 % f.p : 0u, red64(f, acc));
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) X[o + i][o + lane] = x[i];
         }
-        part[qd][c] = acc;
+    }
+    __syncthreads();
+    for (int lg = 3; lg <= 5; ++lg) {  // h = 8, 16, 32
+        const int h = 1 << lg, npair = 32 >> lg, per = h * h;
+        // W = C A^-1 : W[r][c] = sum_{k >= c} C[r][k] A^-1[k][c]
+        for (int e = tid; e < npair * per; e += 256) {
+            const int j = e >> (2 * lg), r = (e >> lg) & (h - 1), c = e & (h - 1);
+            const int a0 = 2 * j * h, b0 = a0 + h;
+            Ts[a0 + c][b0 + r] = dot_lt<kMode>(f, &Ts[b0 + r][a0], 1, &X[a0][a0 + c], 65, c, h);
+        }
         __syncthreads();
-        if (qd == 0) {
-            const uint64_t sum = (uint64_t)red64(f, part[0][c]) + red64(f, part[1][c]) +
-                                 red64(f, part[2][c]) + red64(f, part[3][c]);
-            X[i][c] = fsub(f, (c == i) ? 1 % f.p : 0, red64(f, sum));
+        // X_BA = -B^-1 W : X[r][c] = -sum_{k <= r} B^-1[r][k] W[k][c]
+        for (int e = tid; e < npair * per; e += 256) {
+            const int j = e >> (2 * lg), r = (e >> lg) & (h - 1), c = e & (h - 1);
+            const int a0 = 2 * j * h, b0 = a0 + h;
+            X[b0 + r][a0 + c] = fneg(f, dot_lt<kMode>(f, &X[b0 + r][b0], 1, &Ts[a0 + c][b0], 1, 0, r + 1));
         }
         __syncthreads();
     }
@@ -263,6 +305,144 @@ __global__ void __launch_bounds__(256) k_trsm_panel(Fp f, const uint32_t* __rest
     }
 }
 
+// ---------------------------------------------------------------------------
+// Panel solve on the int8 tensor cores (p <= 255): mma.sync m16n8k32 s8 x s8
+// -> s32 with residues centered to [-(p-1)/2, (p-1)/2].  Rows [0, nb) of the
+// panel (nb <= 256) x PM_COLS columns per CTA:
+//   for each 64-row block bi:  Y = X_bi - sum_{bj<bi} T_{bi,bj} X_bj,
+//                              X_bi = Tinv_bi Y        (both as warp MMAs)
+// X lives in shared memory as exact residues (u32) and as a transposed int8
+// copy (the B operand).  Warp w owns the 16-row m-tile (w & 3) and four 8-col
+// n-tiles of the 64 x PM_COLS block result; |acc| <= 192 * 127^2 < 2^31.
+// ---------------------------------------------------------------------------
+constexpr int PM_COLS = 64, PM_XU = PM_COLS + 8, PM_XB = 256 + 16, PM_AB = 64 + 16;
+constexpr size_t PM_SMEM = (size_t)256 * PM_XU * 4 + (size_t)PM_COLS * PM_XB + (size_t)64 * PM_AB;
+
+__device__ __forceinline__ void mma_s8_16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                             uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ int8_t center8(uint32_t x, uint32_t p, uint32_t half) {
+    return (int8_t)(x > half ? (int)x - (int)p : (int)x);
+}
+// 64 x 64 block of u32 residues (rows < rv, cols < cv; zero elsewhere) -> centered int8 in Ab
+__device__ __forceinline__ void pm_load_a(int8_t* Ab, const uint32_t* __restrict__ src, int64_t ld, int rv,
+                                          int cv, uint32_t p, uint32_t half) {
+    uint32_t v[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const int e = threadIdx.x + 256 * u, r = e >> 6, c = e & 63;
+        v[u] = (r < rv && c < cv) ? __ldg(src + (int64_t)r * ld + c) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const int e = threadIdx.x + 256 * u, r = e >> 6, c = e & 63;
+        Ab[r * PM_AB + c] = center8(v[u], p, half);
+    }
+}
+// acc[t] += A(64x64 block in Ab, rows of m-tile mt) x X^T[k0 .. k0+64)[n-tiles nt0..nt0+3]
+__device__ __forceinline__ void pm_mma(int (&acc)[4][4], const int8_t* Ab, const int8_t* XbT, int k0, int mt,
+                                       int nt0, int gid, int tig) {
+#pragma unroll
+    for (int ks = 0; ks < 64; ks += 32) {
+        const int8_t* ar0 = Ab + (16 * mt + gid) * PM_AB + ks + tig * 4;
+        const int8_t* ar1 = ar0 + 8 * PM_AB;
+        const uint32_t a0 = *(const uint32_t*)ar0, a1 = *(const uint32_t*)ar1;
+        const uint32_t a2 = *(const uint32_t*)(ar0 + 16), a3 = *(const uint32_t*)(ar1 + 16);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const int8_t* bp = XbT + (8 * (nt0 + t) + gid) * PM_XB + k0 + ks + tig * 4;
+            mma_s8_16832(acc[t], a0, a1, a2, a3, *(const uint32_t*)bp, *(const uint32_t*)(bp + 16));
+        }
+    }
+}
+__global__ void __launch_bounds__(256, 2) k_trsm_panel_mma(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
+                                                           const uint32_t* __restrict__ Tinv, uint32_t* B,
+                                                           int64_t ldb, int nb, int64_t ncols) {
+    extern __shared__ __align__(16) uint8_t pm_smem[];
+    uint32_t* Xu = (uint32_t*)pm_smem;                     // 256 x PM_XU
+    int8_t* XbT = (int8_t*)(Xu + 256 * PM_XU);             // PM_COLS x PM_XB (column-major int8 X)
+    int8_t* Ab = XbT + PM_COLS * PM_XB;                    // 64 x PM_AB
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5, gid = lane >> 2, tig = lane & 3;
+    const int mt = wp & 3, nt0 = (wp >> 2) * 4;
+    const int64_t c0 = (int64_t)blockIdx.x * PM_COLS;
+    const int bc = (int)std::min<int64_t>(PM_COLS, ncols - c0);
+    const uint32_t p = f.p, half = (p - 1) / 2, bias = (uint32_t)(0x80000000ull % p);
+    // panel -> Xu (zero outside rows < nb, cols < bc) and its int8 transpose
+    for (int r0 = wp; r0 < 256; r0 += 64) {
+        uint32_t v[8][2];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int r = r0 + 8 * u;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = lane + 32 * h;
+                v[u][h] = (r < nb && c < bc) ? B[(int64_t)r * ldb + c0 + c] : 0u;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int r = r0 + 8 * u;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = lane + 32 * h;
+                Xu[r * PM_XU + c] = v[u][h];
+                XbT[c * PM_XB + r] = center8(v[u][h], p, half);
+            }
+        }
+    }
+    const int nblk = (nb + 63) >> 6;
+    auto reduce_acc = [&](int a) -> uint32_t {  // s32 accumulator -> residue
+        return fsub(f, red32(f, (uint32_t)a ^ 0x80000000u), bias);
+    };
+    for (int bi = 0; bi < nblk; ++bi) {
+        const int rb = bi * 64, rv = min(64, nb - rb);
+        int acc[4][4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0;
+        for (int bj = 0; bj < bi; ++bj) {
+            __syncthreads();  // Ab free, X_bj complete
+            pm_load_a(Ab, T + (int64_t)rb * ldt + bj * 64, ldt, rv, 64, p, half);
+            __syncthreads();
+            pm_mma(acc, Ab, XbT, bj * 64, mt, nt0, gid, tig);
+        }
+        __syncthreads();  // Ab free; XbT rows of block bi not read any more by the updates
+        pm_load_a(Ab, Tinv + (int64_t)bi * 64 * 64, 64, 64, 64, p, half);
+        // Y = X_bi - acc (own fragment elements), exact and int8
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int row = rb + 16 * mt + gid + 8 * (e >> 1), col = 8 * (nt0 + t) + 2 * tig + (e & 1);
+                const uint32_t y = fsub(f, Xu[row * PM_XU + col], reduce_acc(acc[t][e]));
+                Xu[row * PM_XU + col] = y;
+                XbT[col * PM_XB + row] = center8(y, p, half);
+            }
+        __syncthreads();
+        int acc2[4][4];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) acc2[t][0] = acc2[t][1] = acc2[t][2] = acc2[t][3] = 0;
+        pm_mma(acc2, Ab, XbT, rb, mt, nt0, gid, tig);
+        __syncthreads();  // every warp has read Y before X_bi overwrites it
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const int row = rb + 16 * mt + gid + 8 * (e >> 1), col = 8 * (nt0 + t) + 2 * tig + (e & 1);
+                const uint32_t x = row < nb ? reduce_acc(acc2[t][e]) : 0u;
+                Xu[row * PM_XU + col] = x;
+                XbT[col * PM_XB + row] = center8(x, p, half);
+            }
+    }
+    __syncthreads();
+    for (int r0 = wp; r0 < nb; r0 += 8)
+        for (int c = lane; c < bc; c += 32) B[(int64_t)r0 * ldb + c0 + c] = Xu[r0 * PM_XU + c];
+}
+
 struct TrsmScratch {
     uint32_t* ptr = nullptr;
     size_t cap = 0;
@@ -285,8 +465,22 @@ uint32_t* trsm_scratch(size_t words) {
 void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tinv, int64_t i0) {
     const int64_t n = T.rows;
     if (n <= 256) {
-        ProfScope ps(K_TRSM, st, 2.0 * n * n * B.cols / 2, 8.0 * n * B.cols);
+        ProfScope ps(K_TRSM, st, 2.0 * n * n * B.cols / 2, 8.0 * n * B.cols, n, B.cols, 1);
         const uint32_t* ti = Tinv + (i0 / 64) * 64 * 64;
+        static const bool no_mma = getenv("FFB_TRSM_SIMT") != nullptr;  // test hook
+        if (f.p <= 255 && !no_mma) {
+            static bool attr_mma = false;
+            if (!attr_mma) {
+                FFB_CUDA(cudaFuncSetAttribute(k_trsm_panel_mma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)PM_SMEM));
+                attr_mma = true;
+            }
+            k_trsm_panel_mma<<<(unsigned)cdiv(B.cols, PM_COLS), 256, PM_SMEM, st>>>(f, T.ptr, T.ld, ti, B.ptr,
+                                                                                 B.ld, (int)n, B.cols);
+            ++g_launches;
+            FFB_CHECK_LAUNCH();
+            return;
+        }
         const size_t smem = (size_t)(256 * (PNL_COLS + 1) + 64 * 65) * 4;
         static bool attr = false;
         if (!attr) {
@@ -334,11 +528,13 @@ void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
     const int64_t nblk = cdiv(n, 64);
     uint32_t* Tinv = trsm_scratch((size_t)nblk * 64 * 64);
     {
-        ProfScope ps(K_TRSM, st, (double)n * 64 * 64 / 3, 8.0 * n * 64);
-        if (f.p < (1u << 23))
-            k_trinv64<true><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+        ProfScope ps(K_TRSM, st, (double)n * 64 * 64 / 3, 8.0 * n * 64, n, B.cols, 0);
+        if (f.p < 4096u)
+            k_trinv64<0><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+        else if (f.p < (1u << 23))
+            k_trinv64<1><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
         else
-            k_trinv64<false><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+            k_trinv64<2><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
         ++g_launches;
         FFB_CHECK_LAUNCH();
     }

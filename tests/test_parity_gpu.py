@@ -307,3 +307,17 @@ print("ok")
 def test_plduq_paths(gpu, env):
     """Every PLDUQ path (sketch-based parallel, its exact fallback, the sequential kernel)."""
     _run_in_subprocess(env, PLDUQ_PATH_CHECK)
+
+
+@pytest.mark.parametrize("n,cols", [(64, 64), (256, 65), (300, 130), (700, 64), (1000, 200), (129, 1)])
+@pytest.mark.parametrize("p", [2, 3, 131, 251, 257])
+def test_trsm_panel_paths(gpu, oracle, n, cols, p):
+    """Unit lower solves through the 256-row panel kernels (int8 mma.sync for p <= 255,
+    SIMT above), with 64-row blocks, ragged blocks, recursive splits and ragged column tiles."""
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(n * 31 + cols + p)
+    t = rng.integers(0, p, (n, n), dtype=np.uint64)
+    bb = rng.integers(0, p, (n, cols), dtype=np.uint64)
+    for up, tr in ((0, 0), (1, 0)):
+        assert np.array_equal(ffb.trsm_inplace(t, up, tr, 1, bb, p, ctx=gpu),
+                              oracle.trsm_inplace(p, t, up, tr, 1, bb))

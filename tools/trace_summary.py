@@ -24,3 +24,15 @@ for c, m, n, k, t in g:
     a[2] += 2 * m * n * k
 for key, (cnt, t, ops) in sorted(agg.items(), key=lambda x: -x[1][1])[:int(sys.argv[2]) if len(sys.argv) > 2 else 25]:
     print(key, cnt, round(t, 2), "ms", round(ops / t / 1e9, 1), "TOPS", round(t / cnt * 1000, 1), "us/call")
+
+if len(sys.argv) > 3:  # TRSM breakdown: (kind, n bucket, cols bucket)
+    agg = defaultdict(lambda: [0, 0.0])
+    for c, m, n, k, t in g:
+        if c != 3:
+            continue
+        b = lambda x: 2 ** int(math.log2(max(x, 1)))
+        a = agg[("panel" if k == 1 else "trinv", b(m), b(n))]
+        a[0] += 1
+        a[1] += t
+    for key, (cnt, t) in sorted(agg.items(), key=lambda x: -x[1][1])[:int(sys.argv[3])]:
+        print(key, cnt, round(t, 2), "ms", round(t / cnt * 1000, 1), "us/call")
