@@ -11,6 +11,7 @@
 #include <algorithm>
 
 #include "ffb_kernels.cuh"
+#include "ffb_mma.cuh"
 
 namespace ffb {
 
@@ -318,17 +319,6 @@ __global__ void __launch_bounds__(256) k_trsm_panel(Fp f, const uint32_t* __rest
 constexpr int PM_COLS = 64, PM_XU = PM_COLS + 8, PM_XB = 256 + 16, PM_AB = 64 + 16;
 constexpr size_t PM_SMEM = (size_t)256 * PM_XU * 4 + (size_t)PM_COLS * PM_XB + (size_t)64 * PM_AB;
 
-__device__ __forceinline__ void mma_s8_16832(int (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
-                                             uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k32.row.col.s32.s8.s8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
-        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ int8_t center8(uint32_t x, uint32_t p, uint32_t half) {
-    return (int8_t)(x > half ? (int)x - (int)p : (int)x);
-}
 // 64 x 64 block of u32 residues (rows < rv, cols < cv; zero elsewhere) -> centered int8 in Ab
 __device__ __forceinline__ void pm_load_a(int8_t* Ab, const uint32_t* __restrict__ src, int64_t ld, int rv,
                                           int cv, uint32_t p, uint32_t half) {

@@ -4,6 +4,7 @@
 // (Alg. 4), PLDUQ (row-order Crout with leftmost pivots), the small
 // triangular solves, and the generic modular GEMM used for every
 // contraction that the tcgen05 path (ffb_tc_gemm.cu) does not take.
+#include <string.h>
 #include <cstdio>
 #include <stdlib.h>
 
@@ -189,10 +190,26 @@ void gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, 
         if (mode == GEMM_SET) zero_mat(st, C.sub(0, 0, M, N));
         return;
     }
-    if (tc_gemm_supported(f, M, N, K)) {
+    // p <= 255: the tcgen05 pipeline (packed operands, TMA) from ~2^28 MACs with
+    // both output dims >= 128; warp-level mma.sync on the raw residues below that
+    // (measured crossover, tools/gemm_bench.py)
+    bool big = M >= 128 && N >= 128 && (double)M * N * K >= 2.7e8;
+    // test hook, read per call: FFB_GEMM_PATH=tc|mma|simt forces a path where it applies
+    const char* force = getenv("FFB_GEMM_PATH");
+    if (force) {
+        if (!strcmp(force, "tc")) big = true;
+        else if (!strcmp(force, "simt")) goto simt;
+        else if (!strcmp(force, "mma")) big = false;
+    }
+    if ((f.p > 255 || big) && tc_gemm_supported(f, M, N, K)) {
         tc_gemm(f, st, mode, C, A, ta, B, tb, M, N, K);
         return;
     }
+    if (mma_gemm_supported(f, M, N, K)) {
+        mma_gemm(f, st, mode, C, A, ta, B, tb, M, N, K);
+        return;
+    }
+simt:
     if (!ta && !tb) launch_gemm_simt<false, false>(f, st, mode, C, A, B, M, N, K);
     else if (ta && !tb) launch_gemm_simt<true, false>(f, st, mode, C, A, B, M, N, K);
     else if (!ta && tb) launch_gemm_simt<false, true>(f, st, mode, C, A, B, M, N, K);

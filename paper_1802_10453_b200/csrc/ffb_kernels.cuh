@@ -49,6 +49,11 @@ enum GemmMode { GEMM_SUB = 0, GEMM_ADD = 1, GEMM_SET = 2 };
 void gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
           int64_t M, int64_t N, int64_t K);
 
+// int8 mma.sync path (ffb_mma.cu): p <= 255, small and mid shapes, no operand packing.
+bool mma_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K);
+void mma_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
+              int64_t M, int64_t N, int64_t K);
+
 // tcgen05 int8 path (ffb_tc_gemm.cu), used by gemm() for p <= 255 and large shapes.
 bool tc_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K);
 void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,

@@ -16,10 +16,13 @@ pytestmark = pytest.mark.gpu
                                    # small M (rows beyond M are TMA zero-fill) and short K
                                    # (the 2-stage, two-CTAs-per-SM variant)
                                    (8, 4096, 1024), (17, 3000, 500), (100, 2048, 64),
-                                   (1000, 3000, 16), (700, 2500, 250)])
+                                   (1000, 3000, 16), (700, 2500, 250), (128, 128, 4096)])
 @pytest.mark.parametrize("p", [131, 251, 2, 3])
-def test_tc_gemm_nn(gpu, oracle, m, n, k, p):
+@pytest.mark.parametrize("path", ["tc", "mma"])
+def test_tc_gemm_nn(gpu, oracle, m, n, k, p, path, monkeypatch):
+    """Both int8 paths: tcgen05 (packed, TMA) and warp mma.sync (raw residues)."""
     import paper_1802_10453_b200 as ffb
+    monkeypatch.setenv("FFB_GEMM_PATH", path)
     rng = np.random.default_rng(m * 7 + n * 3 + k + p)
     if p == 131 and k == 20000:
         a = np.full((m, k), 65, np.uint64)  # worst case |centered| for p=131
@@ -32,8 +35,10 @@ def test_tc_gemm_nn(gpu, oracle, m, n, k, p):
 
 
 @pytest.mark.parametrize("n,k", [(300, 200), (520, 130), (256, 2048)])
-def test_tc_gemm_transposed_operands(gpu, oracle, n, k):
+@pytest.mark.parametrize("path", ["tc", "mma", "simt"])
+def test_tc_gemm_transposed_operands(gpu, oracle, n, k, path, monkeypatch):
     import paper_1802_10453_b200 as ffb
+    monkeypatch.setenv("FFB_GEMM_PATH", path)
     p = 131
     rng = np.random.default_rng(n + k)
     c = rand_sym(rng, p, n)

@@ -61,8 +61,13 @@ if __name__ == "__main__":
     ap.add_argument("shape", nargs="*", type=int)
     ap.add_argument("--p", type=int, default=131)
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--path", default=None, help="tc | mma | simt (FFB_GEMM_PATH)")
     a = ap.parse_args()
+    if a.path:
+        os.environ["FFB_GEMM_PATH"] = a.path
     shapes = [tuple(a.shape[i:i + 3]) for i in range(0, len(a.shape), 3)] or \
         [(8192, 8192, 8192), (4096, 4096, 4096), (16384, 16384, 2048), (8192, 8192, 256)]
     for s in shapes:
-        print(json.dumps(run(*s, a.p, a.reps)), flush=True)
+        r = run(*s, a.p, a.reps)
+        r["path"] = a.path or "auto"
+        print(json.dumps(r), flush=True)

@@ -15,8 +15,8 @@ agg = defaultdict(lambda: [0, 0.0, 0.0])
 for c, m, n, k, t in g:
     if c != 0:
         continue
-    pth = "simt" if m < 0 else ("limb" if k < 0 else "i8")
-    m, k = abs(m), abs(k)
+    pth = "simt" if m < 0 else ("limb" if k < 0 else ("mma" if n < 0 else "i8"))
+    m, n, k = abs(m), abs(n), abs(k)
     b = lambda x: 2 ** int(math.log2(max(x, 1)))
     a = agg[(pth, b(m), b(n), b(k))]
     a[0] += 1
