@@ -314,26 +314,21 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
 // ---------------------------------------------------------------------------
 constexpr int CRP_W = 256, CRP_G = 32, CRP_KMAX = 128;
 
-__global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* __restrict__ RI, int64_t ldr,
-                                                  int k, int64_t n, int32_t* out, int32_t* ocount) {
-    extern __shared__ uint32_t sm[];
-    uint32_t* E = sm;                           // basis: up to k vectors of length k
-    uint32_t* V = E + (size_t)CRP_KMAX * k;     // CRP_G columns, each length k: V[c*k + i]
-    uint32_t* VC = V + (size_t)CRP_G * k;       // CRP_G x CRP_KMAX gathered coefficients
-    __shared__ int rho[CRP_KMAX];
-    __shared__ unsigned fmask[2];
-    __shared__ BatchScratch bs;
-    __shared__ uint32_t sinv[SINV_MAX];
+// Column scan shared by the level-0 CTAs and the chunk finish: the columns
+// colfn(0 .. total) of RI (in this order) are processed in groups of CRP_G
+// (prefetched into registers one group ahead), each reduced against the basis
+// E in parallel; the flagged ones go through the blocked insertion.  The ids
+// of the independent columns are written to out[0 .. nb) in scan order.
+// Stops once k columns are found.  E, V, VC: shared (see k_crp_list).
+template <class ColFn>
+__device__ int crp_scan(const Fp& f, const SmemInv& inv, const uint32_t* __restrict__ RI, int64_t ldr,
+                        int k, int total, ColFn colfn, uint32_t* E, uint32_t* V, uint32_t* VC, int* rho,
+                        unsigned* fmask, BatchScratch& bs, int32_t* out) {
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-    const int g = blockIdx.x;
-    const int64_t c0 = (int64_t)g * CRP_W;
-    const int total = (int)std::min<int64_t>(CRP_W, n - c0);
-    const SmemInv inv = stage_inverses(f, sinv);
-    // group prefetch: thread (wp, lane) holds rows wp + 8u of column lane
-    uint32_t vv[CRP_KMAX / 8];
+    uint32_t vv[CRP_KMAX / 8];  // thread (wp, lane) holds rows wp + 8u of column lane of a group
     auto fetch = [&](int s0) {
         const bool ok = s0 + lane < total;
-        const uint32_t* src = RI + c0 + s0 + lane;
+        const uint32_t* src = RI + (ok ? colfn(s0 + lane) : 0);
 #pragma unroll
         for (int u = 0; u < CRP_KMAX / 8; ++u) {
             const int i = wp + 8 * u;
@@ -361,10 +356,29 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* __restri
         const unsigned pending = fmask[gi & 1];
         if (!pending) continue;
         const int cnt = batch_insert<4>(f, inv, V, k, pending, k, E, nb, k, rho, bs);
-        if (tid < cnt) out[(int64_t)g * k + nb + tid] = (int32_t)(c0 + s0 + bs.ins[tid]);
+        if (tid < cnt) out[nb + tid] = colfn(s0 + bs.ins[tid]);
         nb += cnt;
     }
-    if (tid == 0) ocount[g] = nb;
+    return nb;
+}
+
+__global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* __restrict__ RI, int64_t ldr,
+                                                  int k, int64_t n, int32_t* out, int32_t* ocount) {
+    extern __shared__ uint32_t sm[];
+    uint32_t* E = sm;                           // basis: up to k vectors of length k
+    uint32_t* V = E + (size_t)CRP_KMAX * k;     // CRP_G columns, each length k: V[c*k + i]
+    uint32_t* VC = V + (size_t)CRP_G * k;       // CRP_G x CRP_KMAX gathered coefficients
+    __shared__ int rho[CRP_KMAX];
+    __shared__ unsigned fmask[2];
+    __shared__ BatchScratch bs;
+    __shared__ uint32_t sinv[SINV_MAX];
+    const int g = blockIdx.x;
+    const int64_t c0 = (int64_t)g * CRP_W;
+    const int total = (int)std::min<int64_t>(CRP_W, n - c0);
+    const SmemInv inv = stage_inverses(f, sinv);
+    const int nb = crp_scan(f, inv, RI, ldr, k, total, [c0](int idx) { return (int32_t)(c0 + idx); }, E, V,
+                            VC, rho, fmask, bs, out + (int64_t)g * k);
+    if (threadIdx.x == 0) ocount[g] = nb;
 }
 
 // ---------------------------------------------------------------------------
@@ -469,6 +483,186 @@ __global__ void __launch_bounds__(256) k_crp_rowelim(Fp f, const uint32_t* RI, i
             }
             sigma_out[t] = lo;
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Chunk finish (1 CTA): RPM of R_I on the level-0 candidate columns, the
+// inverse of Kc = R_I[:, J] and the chunk bookkeeping, in one launch.
+//   1. candidate list C (ascending) from the level-0 lists (warp scan);
+//   2. row-order leftmost elimination on R_I[:, C] (plduq.cpp:46-84 on the
+//      compressed problem): row t's pivot is its leading nonzero; the same row
+//      operations on the identity give L^-1, the reduced rows give U' (row t,
+//      pivot column of row t') upper triangular;
+//   3. X = U'^-1 L^-1 by back substitution (one barrier per row);
+//   4. J = sorted pivot columns, sigma[t] = position of row t's column in J,
+//      Kinv = (R_I[:, J])^-1 = row sigma[t] <- X[t];  UO[r + i] = (Kinv S_I)[i];
+//      uhat_col[r+i] = J[i], prow[r+t] = c0 + I[t], pcol[r+t] = J[sigma t].
+// Pivot searches are ballots in every warp (no atomics); each elimination row
+// belongs to one warp, so a step needs one block barrier.
+// ---------------------------------------------------------------------------
+// dynamic smem: G (k^2) + max(rc_cap = min(k nblk k, CF_RC_WORDS), scan buffers)
+constexpr int CF_RC_WORDS = 32 * 1024;
+constexpr int CF_SMEM_WORDS = CRP_KMAX * CRP_KMAX + CF_RC_WORDS;
+__host__ __device__ inline size_t cf_smem_bytes(int k, int nblk, int* rc_cap) {
+    *rc_cap = (int)std::min<int64_t>((int64_t)k * nblk * k, CF_RC_WORDS);
+    const size_t scan = (size_t)(CRP_KMAX + CRP_G) * k + CRP_G * CRP_KMAX;
+    return ((size_t)k * k + std::max<size_t>((size_t)*rc_cap, scan)) * 4;
+}
+__global__ void __launch_bounds__(256) k_crp_finish(
+    Fp f, const uint32_t* __restrict__ RI, int64_t ldr, int k, const int32_t* __restrict__ lists,
+    const int32_t* __restrict__ counts, int nblk, int32_t* cand, int rc_cap, const int32_t* I, int64_t c0,
+    const uint32_t* S, int64_t lds, int s, uint32_t* Kinv, int32_t* Jout, uint32_t* UO, int64_t lduo,
+    int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r, int32_t* fail) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    __shared__ int32_t off[1025];
+    __shared__ int32_t Js[CRP_KMAX], rho[CRP_KMAX], pci[CRP_KMAX], pcv[CRP_KMAX], sig[CRP_KMAX], Is[CRP_KMAX];
+    __shared__ uint32_t dinv[CRP_KMAX];
+    __shared__ unsigned fmask[2];
+    __shared__ BatchScratch bs;
+    __shared__ uint32_t sinv[SINV_MAX];
+    __shared__ int total;
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    const SmemInv inv = stage_inverses(f, sinv);
+    if (wp == 0) {  // exclusive offsets of the level-0 lists
+        int run = 0;
+        for (int b0 = 0; b0 < nblk; b0 += 32) {
+            const int c = b0 + lane < nblk ? counts[b0 + lane] : 0;
+            int x = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
+            }
+            if (b0 + lane < nblk) off[b0 + lane] = run + x - c;
+            run += __shfl_sync(0xffffffffu, x, 31);
+        }
+        if (lane == 0) total = run;
+    }
+    for (int t = tid; t < k; t += 256) Is[t] = I ? I[t] : 0;
+    __syncthreads();
+    for (int b = wp; b < nblk; b += 8) {
+        const int cb = counts[b], ob = off[b];
+        for (int q = lane; q < cb; q += 32) cand[ob + q] = lists[(int64_t)b * k + q];
+    }
+    __syncthreads();
+    // 1. the k x Cx elimination matrix M: R_I on all candidates when it fits
+    //    (Cx = C, ids = cand), else R_I on J = its column rank profile over the
+    //    candidates, found by the batched scan (Cx = k, ids = Js): the RPM of R_I
+    //    is the RPM of M either way, every other column depending on earlier ones
+    const int C = total;
+    uint32_t* G = sm;                   // k x k: L^-1, then U'^-1 L^-1
+    uint32_t* M = sm + (size_t)k * k;
+    const bool direct = k * C <= rc_cap;
+    const int Cx = direct ? C : k;
+    const int32_t* ids = direct ? cand : Js;
+    if (!direct) {
+        uint32_t* E = M;
+        uint32_t* V = E + (size_t)CRP_KMAX * k;
+        uint32_t* VC = V + (size_t)CRP_G * k;
+        const int nb = crp_scan(f, inv, RI, ldr, k, C, [cand](int idx) { return cand[idx]; }, E, V, VC, rho,
+                                fmask, bs, Js);
+        if (nb < k) {  // R_I rank deficient: cannot happen for detected rows
+            if (tid == 0) *fail = 1;
+            return;
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < k * k; e += 256) G[e] = (e / k == e % k) ? 1 % f.p : 0u;
+    for (int i = wp; i < k; i += 8)
+        for (int j0 = lane; j0 < Cx; j0 += 128) {
+            uint32_t vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + 32 * u;
+                vv[u] = j < Cx ? __ldg(RI + (int64_t)i * ldr + ids[j]) : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = j0 + 32 * u;
+                if (j < Cx) M[(size_t)i * Cx + j] = vv[u];
+            }
+        }
+    __syncthreads();
+    // 2. row-order leftmost elimination on M, tracking L^-1 in G
+    for (int t = 0; t < k; ++t) {
+        const uint32_t* rt = M + (size_t)t * Cx;
+        int jp = Cx;
+        for (int j0 = 0; j0 < Cx; j0 += 32) {
+            const unsigned bal = __ballot_sync(0xffffffffu, j0 + lane < Cx && rt[j0 + lane] != 0);
+            if (bal) {
+                jp = j0 + __ffs(bal) - 1;
+                break;
+            }
+        }
+        if (jp >= Cx) {
+            if (tid == 0) *fail = 1;
+            return;
+        }
+        const uint32_t il = inv(f, rt[jp]);
+        if (tid == 0) {
+            pci[t] = jp;
+            pcv[t] = ids[jp];
+            dinv[t] = il;
+        }
+        const uint32_t* gt = G + (size_t)t * k;
+        for (int i = t + 1 + wp; i < k; i += 8) {
+            uint32_t* ri = M + (size_t)i * Cx;
+            const uint32_t c = ri[jp];
+            __syncwarp();
+            if (!c) continue;
+            const uint32_t m = fmul(f, c, il);
+            for (int j = jp + lane; j < Cx; j += 32) ri[j] = fmsub(f, ri[j], m, rt[j]);
+            uint32_t* gi = G + (size_t)i * k;
+            for (int j = lane; j <= t; j += 32) gi[j] = fmsub(f, gi[j], m, gt[j]);
+        }
+        __syncthreads();
+    }
+    // 3. back substitution X = U'^-1 L^-1, U'[t][t'] = M[t][pci[t']]
+    for (int tp = k - 1; tp > 0; --tp) {
+        const uint32_t* gp = G + (size_t)tp * k;
+        const int jc = pci[tp];
+        const uint32_t dp = dinv[tp];
+        for (int t = wp; t < tp; t += 8) {
+            const uint32_t c = M[(size_t)t * Cx + jc];
+            if (!c) continue;  // warp-uniform
+            const uint32_t m = fmul(f, c, dp);
+            uint32_t* gr = G + (size_t)t * k;
+            for (int j = lane; j < k; j += 32) gr[j] = fmsub(f, gr[j], m, gp[j]);
+        }
+        __syncthreads();
+    }
+    // 4. outputs: J = sorted pivot columns, sigma[t] = rank of row t's column,
+    //    Kinv row sigma[t] = X[t]
+    for (int t = tid; t < k; t += 256) {
+        int rank = 0;
+        const int v = pcv[t];
+        for (int u = 0; u < k; ++u) rank += pcv[u] < v;
+        sig[t] = rank;
+        Jout[rank] = v;
+    }
+    for (int e = tid; e < k * k; e += 256) G[e] = fmul(f, G[e], dinv[e / k]);
+    __syncthreads();
+    for (int e = tid; e < k * k; e += 256) {
+        const int t = e / k, j = e - t * k;
+        Kinv[(int64_t)sig[t] * k + j] = G[e];
+    }
+    if (S) {
+        for (int e = tid; e < k * s; e += 256) {
+            const int t = e / s, col = e - t * s;
+            const uint32_t* xt = G + (size_t)t * k;
+            uint64_t acc = 0;
+            for (int u = 0; u < k; ++u) {
+                acc += (uint64_t)xt[u] * S[(int64_t)Is[u] * lds + col];
+                if (f.p >= (1u << 23)) acc = red64(f, acc);
+            }
+            UO[(r + sig[t]) * lduo + col] = red64(f, acc);
+        }
+    }
+    for (int t = tid; t < k; t += 256) {
+        uhat_col[r + sig[t]] = pcv[t];
+        prow[r + t] = (int32_t)(c0 + Is[t]);
+        pcol[r + t] = pcv[t];
     }
 }
 
@@ -769,7 +963,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     int32_t* counts[2] = {ws.vec<int32_t>(nblk0), ws.vec<int32_t>(nblk0)};
     int32_t* dflag = ws.vec<int32_t>(4);
     int32_t* dsig = ws.vec<int32_t>(B);
-    uint32_t* re_scratch = ws.vec<uint32_t>((int64_t)CRP_KMAX * nblk0 * CRP_KMAX + (int64_t)nblk0 * CRP_KMAX + 64);
+    uint32_t* re_scratch = ws.vec<uint32_t>((int64_t)nblk0 * CRP_KMAX + 64);  // candidate list
     int32_t* d_uhat_col = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
     const int64_t pstride = (std::max<int64_t>(mn, 1) + 63) / 64 * 64;
     int32_t* d_prow = ws.vec<int32_t>(2 * pstride);
@@ -784,6 +978,8 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         FFB_CUDA(cudaFuncSetAttribute(k_crp_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crp_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_pair2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * CRP_KMAX * CRP_KMAX * 4)));
         FFB_CUDA(cudaFuncSetAttribute(k_crp_rowelim, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        FFB_CUDA(cudaFuncSetAttribute(k_crp_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)((size_t)CF_SMEM_WORDS * 4)));
         attrs = true;
     }
     static const bool force_exact = getenv("FFB_PLDUQ_FORCE_FALLBACK") != nullptr;  // test hook
@@ -792,10 +988,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     // R_I in RI) and pivot column set dJ (ascending): pairing, Unew into Uhat
     // rows [r, r+k), old rows reduced at J, Uhat*Omega maintained when sketching.
     auto absorb = [&](int64_t r, int k, const int32_t* dI, const int32_t* dJ, int64_t c0,
-                      bool sketching, const int32_t* sigma_in, DMat Sk) {
+                      bool sketching, const int32_t* sigma_in, DMat Sk, bool paired) {
         DMat RIk = RI.sub(0, 0, k, n), Kik = Kinv.sub(0, 0, k, k);
         Kik.ld = k;
-        {
+        if (!paired) {
             ProfScope ps(K_PQ_PAIR, st, 0.0, 0.0);
             k_pair2<<<1, 256, (size_t)3 * k * k * 4, st>>>(
                 f, RIk.ptr, RIk.ld, k, dJ, dI, c0, sketching ? Sk.ptr : nullptr, Sk.ld, SK, Kik.ptr,
@@ -871,11 +1067,14 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 }
                 {
                     ProfScope ps(K_PQ_ROWELIM, st, 0.0, 0.0);
-                    // RPM of R_I on the surviving candidate columns (1 CTA)
-                    const int64_t maxc = (int64_t)nblk0 * k;
-                    const size_t resmem = std::min<int64_t>((int64_t)k * maxc, RE_SMEM_WORDS) * 4;
-                    k_crp_rowelim<<<1, 256, resmem, st>>>(f, RI.ptr, RI.ld, k, lists[0], counts[0], nblk0,
-                                                          re_scratch, lists[1], dsig, dflag);
+                    // RPM of R_I on the candidates, Kinv and bookkeeping (1 CTA)
+                    int rc_cap;
+                    const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap);
+                    DMat Kik = Kinv.sub(0, 0, k, k);
+                    k_crp_finish<<<1, 256, cfmem, st>>>(f, RI.ptr, RI.ld, k, lists[0], counts[0], nblk0,
+                                                        (int32_t*)re_scratch, rc_cap, dI, c0, Sc.ptr, Sc.ld, SK,
+                                                        Kik.ptr, lists[1], UO.ptr, UO.ld, d_uhat_col,
+                                                        d_prow, d_pcol, r, dflag);
                     ++g_launches;
                     FFB_CHECK_LAUNCH();
                 }
@@ -888,7 +1087,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     fprintf(jtr, "%d %lld %lld %lld %d %d %d\n", k, (long long)n, (long long)C, (long long)r,
                             hj[0], hj[k / 2], hj[k - 1]);
                 }
-                absorb(r, k, dI, lists[1], c0, true, dsig, Sc);
+                absorb(r, k, dI, lists[1], c0, true, dsig, Sc, true);
                 r += k;
             } else {
                 // exact: residual of the whole chunk, then the row-sequential kernel
@@ -916,7 +1115,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 if (k > 0) {
                     const int32_t* dI = io.upload(I);
                     gather_rows(st, RI.sub(0, 0, k, n), Rc, dI);
-                    absorb(r, k, dI, io.upload(J), c0, false, nullptr, DMat{});
+                    absorb(r, k, dI, io.upload(J), c0, false, nullptr, DMat{}, false);
                     r += k;
                 }
                 ws.release(mk);
@@ -1033,6 +1232,8 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
         const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + 2 * (size_t)CRP_G * CRP_KMAX) * 4;
         FFB_CUDA(cudaFuncSetAttribute(k_crp_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crp_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_crp_rowelim, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        FFB_CUDA(cudaFuncSetAttribute(k_crp_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)((size_t)CF_SMEM_WORDS * 4)));
         FFB_CUDA(cudaFuncSetAttribute(k_pair2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * CRP_KMAX * CRP_KMAX * 4)));
         int32_t *lists0, *counts0, *lists1, *dsig, *flag, *ucol, *prow, *pcol, *dI;
         uint32_t *re_scratch, *Kinv;
@@ -1056,10 +1257,14 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
             FFB_CUDA(cudaEventRecord(e[0], st));
             k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, d_in, n, k, n, lists0, counts0);
             FFB_CUDA(cudaEventRecord(e[1], st));
-            k_crp_rowelim<<<1, 256, resmem, st>>>(f, d_in, n, k, lists0, counts0, nblk0, re_scratch, lists1, dsig, flag);
+            {
+                int rc_cap;
+                const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap);
+                k_crp_finish<<<1, 256, cfmem, st>>>(f, d_in, n, k, lists0, counts0, nblk0, (int32_t*)re_scratch,
+                                                    rc_cap, dI, 0, nullptr, 0, 0, Kinv, lists1, nullptr, 0, ucol,
+                                                    prow, pcol, 0, flag);
+            }
             FFB_CUDA(cudaEventRecord(e[2], st));
-            k_pair2<<<1, 256, (size_t)3 * k * k * 4, st>>>(f, d_in, n, k, lists1, dI, 0, nullptr, 0, 0, Kinv,
-                                                             nullptr, 0, ucol, prow, pcol, 0, flag, dsig);
             FFB_CUDA(cudaEventRecord(e[3], st));
             FFB_CUDA(cudaEventSynchronize(e[3]));
             if (i == 0) continue;  // warm-up

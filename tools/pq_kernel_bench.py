@@ -58,8 +58,8 @@ def main():
     for k, n, nz in ((25, 8192, 20), (25, 8192, 400), (64, 8192, 40), (128, 16384, 100)):
         ms, out = bench(ctx, p, 1, crp_input(rng, p, k, n, nz))
         print(json.dumps(dict(kernel="crp", k=k, n=n, nz=nz, fail=out[0],
-                              crp_list_us=round(ms[0] * 1e3, 2), rowelim_us=round(ms[1] * 1e3, 2),
-                              pair_us=round(ms[2] * 1e3, 2))))
+                              crp_list_us=round(ms[0] * 1e3, 2), finish_us=round(ms[1] * 1e3, 2),
+                              jsorted=bool(all(out[1 + i] < out[2 + i] for i in range(k - 1))))))
 
 
 if __name__ == "__main__":
