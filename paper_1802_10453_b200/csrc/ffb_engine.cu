@@ -237,8 +237,11 @@ struct Engine {
 
     // dispatch, sytrf.cpp:337-350
     HFact dispatch(DMat A, const std::vector<int32_t>& rows, int64_t coff) {
-        if (is_leaf(A.rows)) return crout(A, rows, coff);
-        return recursive_step(A, rows, coff);
+        const int64_t saved = g_node;
+        g_node = A.rows;  // trace tag: the innermost node a launch belongs to
+        HFact h = is_leaf(A.rows) ? crout(A, rows, coff) : recursive_step(A, rows, coff);
+        g_node = saved;
+        return h;
     }
 
     // crout_base, sytrf.cpp:35-139 (device kernel, one CTA)

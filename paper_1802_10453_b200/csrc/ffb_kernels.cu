@@ -15,6 +15,7 @@
 namespace ffb {
 
 thread_local uint64_t g_launches = 0;
+thread_local int64_t g_node = 0;
 thread_local Profiler* g_prof = nullptr;
 
 static inline void count_launch() { ++g_launches; }
@@ -35,7 +36,9 @@ void Profiler::flush() {
     for (Rec& r : recs) {
         float t = 0.f;
         if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) ms[r.cls] += t;
-        if (trace) fprintf(trace, "%d %lld %lld %lld %.4f\n", r.cls, (long long)r.m, (long long)r.n, (long long)r.k, t);
+        if (trace)
+            fprintf(trace, "%d %lld %lld %lld %.4f %lld\n", r.cls, (long long)r.m, (long long)r.n, (long long)r.k, t,
+                    (long long)r.node);
         ops[r.cls] += r.ops;
         bytes[r.cls] += r.bytes;
         cnt[r.cls] += 1;
@@ -56,6 +59,7 @@ ProfScope::ProfScope(int cls, cudaStream_t s, double ops, double bytes, int64_t 
     rec.m = m;
     rec.n = n;
     rec.k = k;
+    rec.node = g_node;
     rec.ops = ops;
     rec.bytes = bytes;
     rec.a = g_prof->get();

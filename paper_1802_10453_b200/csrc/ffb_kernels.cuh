@@ -22,6 +22,7 @@ struct Profiler {
         cudaEvent_t a, b;
         double ops, bytes;
         int64_t m, n, k;  // GEMM shape (trace only)
+        int64_t node;     // recursion node size (trace only)
     };
     bool on = false;
     std::vector<Rec> recs;
@@ -33,6 +34,7 @@ struct Profiler {
     void reset();
 };
 extern thread_local Profiler* g_prof;
+extern thread_local int64_t g_node;  // size of the recursion node being executed (trace tag)
 struct ProfScope {
     Profiler::Rec rec;
     cudaStream_t st;

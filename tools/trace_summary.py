@@ -6,7 +6,14 @@ from collections import defaultdict
 NAMES = ["gemm", "leaf", "rowdet", "trsm", "move", "other", "sketch", "crp", "pair", "ldu", "pack",
          "rowelim"]
 recs = [l.split() for l in open(sys.argv[1])]
-g = [(int(c), int(m), int(n), int(k), float(t)) for c, m, n, k, t in recs]
+nodes = [int(r[5]) if len(r) > 5 else 0 for r in recs]
+g = [(int(r[0]), int(r[1]), int(r[2]), int(r[3]), float(r[4])) for r in recs]
+bynode = defaultdict(lambda: [0, 0.0])
+for (c, m, n, k, t), nd in zip(g, nodes):
+    b = 2 ** int(math.log2(max(nd, 1)))
+    bynode[b][0] += 1
+    bynode[b][1] += t
+print("by recursion node size (launches, ms):", {k: (v[0], round(v[1], 1)) for k, v in sorted(bynode.items())})
 tot = defaultdict(float)
 for c, m, n, k, t in g:
     tot[NAMES[c]] += t
