@@ -16,6 +16,7 @@ namespace ffb {
 
 thread_local uint64_t g_launches = 0;
 thread_local int64_t g_node = 0;
+thread_local int g_slot = 0;
 thread_local Profiler* g_prof = nullptr;
 
 static inline void count_launch() { ++g_launches; }
@@ -200,10 +201,16 @@ void gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, 
     bool big = M >= 128 && N >= 128 && (double)M * N * K >= 2.7e8;
     // test hook, read per call: FFB_GEMM_PATH=tc|mma|simt forces a path where it applies
     const char* force = getenv("FFB_GEMM_PATH");
+    bool rk = K <= 32 && rankk_supported(f, M, N, K);  // short K: C streaming dominates
     if (force) {
+        rk = !strcmp(force, "rankk") && rankk_supported(f, M, N, K);
         if (!strcmp(force, "tc")) big = true;
         else if (!strcmp(force, "simt")) goto simt;
         else if (!strcmp(force, "mma")) big = false;
+    }
+    if (rk) {
+        rankk_gemm(f, st, mode, C, A, ta, B, tb, M, N, K);
+        return;
     }
     if ((f.p > 255 || big) && tc_gemm_supported(f, M, N, K)) {
         tc_gemm(f, st, mode, C, A, ta, B, tb, M, N, K);

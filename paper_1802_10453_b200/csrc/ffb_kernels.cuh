@@ -34,7 +34,15 @@ struct Profiler {
     void reset();
 };
 extern thread_local Profiler* g_prof;
-extern thread_local int64_t g_node;  // size of the recursion node being executed (trace tag)
+extern thread_local int64_t g_node;
+// Scratch slot of the GEMM packing / split-K buffers: launches on a secondary
+// stream use slot 1 so they never share a buffer with the main stream.
+extern thread_local int g_slot;
+struct SlotGuard {
+    int saved;
+    explicit SlotGuard(int s) : saved(g_slot) { g_slot = s; }
+    ~SlotGuard() { g_slot = saved; }
+};  // size of the recursion node being executed (trace tag)
 struct ProfScope {
     Profiler::Rec rec;
     cudaStream_t st;
@@ -55,6 +63,11 @@ void gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, 
 bool mma_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K);
 void mma_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
               int64_t M, int64_t N, int64_t K);
+
+// short-K bandwidth kernel (ffb_mma.cu): p <= 255, K <= 128, dp4a on int8 packs.
+bool rankk_supported(const Fp& f, int64_t M, int64_t N, int64_t K);
+void rankk_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
+                int64_t M, int64_t N, int64_t K);
 
 // tcgen05 int8 path (ffb_tc_gemm.cu), used by gemm() for p <= 255 and large shapes.
 bool tc_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K);

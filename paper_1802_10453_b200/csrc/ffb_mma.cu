@@ -128,8 +128,9 @@ struct MmaScratch {
     uint32_t* ptr = nullptr;
     size_t cap = 0;
 };
-thread_local MmaScratch g_mscratch;
+thread_local MmaScratch g_mscratch_slots[2];
 uint32_t* mma_scratch(size_t words) {
+    MmaScratch& g_mscratch = g_mscratch_slots[g_slot];
     if (g_mscratch.cap < words) {
         if (g_mscratch.ptr) {
             FFB_CUDA(cudaDeviceSynchronize());
@@ -175,6 +176,142 @@ void mma_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool 
         k_splitk_fold<<<dim3((unsigned)cdiv(N, 256), (unsigned)M), 256, 0, st>>>(f, (int)mode, C.ptr, C.ld, W, M,
                                                                                   N, S);
     }
+    ++g_launches;
+    FFB_CHECK_LAUNCH();
+}
+
+
+// ===========================================================================
+// Short-K update (p <= 255, K <= 128): C -/+= op(A) op(B) or C = op(A) op(B)
+// is a stream over C with K multiply-adds per element, so it is written as a
+// bandwidth kernel: a CTA owns 256 columns and a strip of TR rows; op(B) for
+// its columns and op(A) for its rows are staged once in shared memory as
+// centered int8 x 4 packs along k, and each thread streams 16-byte C vectors
+// (4 columns), RK rows in flight, with one dp4a per k-quad and column.
+// ===========================================================================
+namespace {
+
+constexpr int RK_COLS = 256, RK_RU = 4;  // columns per CTA, row unroll (loads in flight)
+
+__device__ __forceinline__ uint32_t pack4c(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t p,
+                                           uint32_t half) {
+    return (uint32_t)(uint8_t)center8(a, p, half) | ((uint32_t)(uint8_t)center8(b, p, half) << 8) |
+           ((uint32_t)(uint8_t)center8(c, p, half) << 16) | ((uint32_t)(uint8_t)center8(d, p, half) << 24);
+}
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(256) k_rankk_dp4a(Fp f, int mode, uint32_t* __restrict__ C, int64_t ldc,
+                                                    const uint32_t* __restrict__ A, int64_t lda,
+                                                    const uint32_t* __restrict__ B, int64_t ldb, int64_t M,
+                                                    int64_t N, int K, int TR) {
+    extern __shared__ __align__(16) uint32_t rk_sm[];
+    const int K4 = (K + 3) >> 2;
+    uint32_t* Bp = rk_sm;                       // [K4][RK_COLS]  packs of op(B)[4q..4q+3][j]
+    uint32_t* Ap = Bp + (size_t)K4 * RK_COLS;   // [TR][K4]       packs of op(A)[i][4q..4q+3]
+    const int tid = threadIdx.x;
+    const int64_t n0 = (int64_t)blockIdx.x * RK_COLS, m0 = (int64_t)blockIdx.y * TR;
+    const int rows = (int)std::min<int64_t>(TR, M - m0);
+    const uint32_t p = f.p, half = (p - 1) / 2, bias = (uint32_t)(0x80000000ull % p);
+    auto opB = [&](int k, int64_t n) -> uint32_t {
+        return (k < K && n < N) ? __ldg(TB ? B + n * ldb + k : B + (int64_t)k * ldb + n) : 0u;
+    };
+    auto opA = [&](int64_t m, int k) -> uint32_t {
+        return (k < K && m < M) ? __ldg(TA ? A + (int64_t)k * lda + m : A + m * lda + k) : 0u;
+    };
+    for (int e = tid; e < K4 * RK_COLS; e += 256) {
+        const int q = e / RK_COLS, j = e - q * RK_COLS;
+        const int64_t n = n0 + j;
+        Bp[e] = pack4c(opB(4 * q, n), opB(4 * q + 1, n), opB(4 * q + 2, n), opB(4 * q + 3, n), p, half);
+    }
+    for (int e = tid; e < rows * K4; e += 256) {
+        const int i = e / K4, q = e - i * K4;
+        const int64_t m = m0 + i;
+        Ap[e] = pack4c(opA(m, 4 * q), opA(m, 4 * q + 1), opA(m, 4 * q + 2), opA(m, 4 * q + 3), p, half);
+    }
+    __syncthreads();
+    const int cg = tid & 63, rp = tid >> 6;  // 4 columns per thread, 4 row phases
+    const int64_t col = n0 + 4 * cg;
+    const bool vec = col + 3 < N && ((ldc & 3) == 0) && ((((uintptr_t)C) & 15) == 0);
+    for (int i0 = rp; i0 < rows; i0 += 4 * RK_RU) {
+        uint4 cv[RK_RU];
+#pragma unroll
+        for (int u = 0; u < RK_RU; ++u) {  // C loads in flight
+            const int i = i0 + 4 * u;
+            cv[u] = make_uint4(0, 0, 0, 0);
+            if (i < rows && mode != GEMM_SET) {
+                const uint32_t* cp = C + (m0 + i) * ldc + col;
+                if (vec) cv[u] = __ldg(reinterpret_cast<const uint4*>(cp));
+                else {
+                    cv[u].x = col < N ? cp[0] : 0u;
+                    cv[u].y = col + 1 < N ? cp[1] : 0u;
+                    cv[u].z = col + 2 < N ? cp[2] : 0u;
+                    cv[u].w = col + 3 < N ? cp[3] : 0u;
+                }
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < RK_RU; ++u) {
+            const int i = i0 + 4 * u;
+            if (i >= rows) break;
+            const uint32_t* ai = Ap + (size_t)i * K4;
+            int a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+            for (int q = 0; q < K4; ++q) {
+                const int av = (int)ai[q];
+                const uint4 bv = *reinterpret_cast<const uint4*>(Bp + (size_t)q * RK_COLS + 4 * cg);
+                a0 = __dp4a(av, (int)bv.x, a0);
+                a1 = __dp4a(av, (int)bv.y, a1);
+                a2 = __dp4a(av, (int)bv.z, a2);
+                a3 = __dp4a(av, (int)bv.w, a3);
+            }
+            uint32_t v[4] = {mma_reduce(f, a0, bias), mma_reduce(f, a1, bias), mma_reduce(f, a2, bias),
+                             mma_reduce(f, a3, bias)};
+            uint32_t c[4] = {cv[u].x, cv[u].y, cv[u].z, cv[u].w};
+#pragma unroll
+            for (int h = 0; h < 4; ++h) {
+                if (mode == GEMM_SUB) c[h] = fsub(f, c[h], v[h]);
+                else if (mode == GEMM_ADD) c[h] = fadd(f, c[h], v[h]);
+                else c[h] = v[h];
+            }
+            uint32_t* cp = C + (m0 + i) * ldc + col;
+            if (vec) *reinterpret_cast<uint4*>(cp) = make_uint4(c[0], c[1], c[2], c[3]);
+            else
+                for (int h = 0; h < 4; ++h)
+                    if (col + h < N) cp[h] = c[h];
+        }
+    }
+}
+
+}  // namespace
+
+bool rankk_supported(const Fp& f, int64_t M, int64_t N, int64_t K) {
+    static const bool disabled = getenv("FFB_DISABLE_RANKK") != nullptr;  // test hook
+    return !disabled && f.p <= 255 && K >= 1 && K <= 128 && N >= 64 && M * N >= ((int64_t)1 << 18);
+}
+
+void rankk_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
+                int64_t M, int64_t N, int64_t K) {
+    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, 8.0 * M * N, -M, -N, K);  // -M,-N marks the rank-k kernel
+    // rows per CTA: B re-reads (M / TR) K N 4 bytes stay <= 1/4 of the C traffic 8 M N
+    int TR = (int)std::max<int64_t>(64, 2 * K);
+    const int64_t ncb = cdiv(N, RK_COLS);
+    while (TR > 16 && ncb * cdiv(M, TR) < 4 * 148) TR /= 2;  // enough CTAs to fill the GPU
+    const int K4 = (int)((K + 3) / 4);
+    const size_t smem = ((size_t)K4 * RK_COLS + (size_t)TR * K4) * 4;
+    static bool attr = false;
+    if (!attr) {
+        for (auto fn : {k_rankk_dp4a<false, false>, k_rankk_dp4a<true, false>, k_rankk_dp4a<false, true>,
+                        k_rankk_dp4a<true, true>})
+            FFB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        attr = true;
+    }
+    const dim3 grid((unsigned)ncb, (unsigned)cdiv(M, TR));
+#define FFB_RK_LAUNCH(TA, TB) \
+    k_rankk_dp4a<TA, TB><<<grid, 256, smem, st>>>(f, (int)mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr, B.ld, M, N, (int)K, TR)
+    if (!ta && !tb) FFB_RK_LAUNCH(false, false);
+    else if (ta && !tb) FFB_RK_LAUNCH(true, false);
+    else if (!ta && tb) FFB_RK_LAUNCH(false, true);
+    else FFB_RK_LAUNCH(true, true);
+#undef FFB_RK_LAUNCH
     ++g_launches;
     FFB_CHECK_LAUNCH();
 }

@@ -507,7 +507,8 @@ constexpr int CF_SMEM_WORDS = CRP_KMAX * CRP_KMAX + CF_RC_WORDS;
 __host__ __device__ inline size_t cf_smem_bytes(int k, int nblk, int* rc_cap) {
     *rc_cap = (int)std::min<int64_t>((int64_t)k * nblk * k, CF_RC_WORDS);
     const size_t scan = (size_t)(CRP_KMAX + CRP_G) * k + CRP_G * CRP_KMAX;
-    return ((size_t)k * k + std::max<size_t>((size_t)*rc_cap, scan)) * 4;
+    const size_t sketch = (size_t)k * RD_S;  // staged S_I rows
+    return ((size_t)k * k + std::max<size_t>(std::max<size_t>((size_t)*rc_cap, scan), sketch)) * 4;
 }
 __global__ void __launch_bounds__(256) k_crp_finish(
     Fp f, const uint32_t* __restrict__ RI, int64_t ldr, int k, const int32_t* __restrict__ lists,
@@ -647,13 +648,17 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         const int t = e / k, j = e - t * k;
         Kinv[(int64_t)sig[t] * k + j] = G[e];
     }
-    if (S) {
+    if (S) {  // UO rows: stage the k sketch rows S_I (coalesced) in the free M buffer
+        uint32_t* SI = M;
+        for (int u = wp; u < k; u += 8)
+            for (int col = lane; col < s; col += 32) SI[(size_t)u * s + col] = __ldg(S + (int64_t)Is[u] * lds + col);
+        __syncthreads();
         for (int e = tid; e < k * s; e += 256) {
             const int t = e / s, col = e - t * s;
             const uint32_t* xt = G + (size_t)t * k;
             uint64_t acc = 0;
             for (int u = 0; u < k; ++u) {
-                acc += (uint64_t)xt[u] * S[(int64_t)Is[u] * lds + col];
+                acc += (uint64_t)xt[u] * SI[(size_t)u * s + col];
                 if (f.p >= (1u << 23)) acc = red64(f, acc);
             }
             UO[(r + sig[t]) * lduo + col] = red64(f, acc);
@@ -984,6 +989,23 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     }
     static const bool force_exact = getenv("FFB_PLDUQ_FORCE_FALLBACK") != nullptr;  // test hook
 
+    // side stream for the Uhat updates (see absorb)
+    static thread_local cudaStream_t side = nullptr;
+    static thread_local cudaEvent_t ev_main = nullptr, ev_side = nullptr;
+    static const bool overlap_ok = !getenv("FFB_PLDUQ_NO_OVERLAP");  // test hook
+    if (!side) {
+        FFB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        FFB_CUDA(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
+        FFB_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
+    }
+    bool side_pending = false;
+    auto join_side = [&]() {
+        if (side_pending) {
+            FFB_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
+            side_pending = false;
+        }
+    };
+
     // Given the chunk's pivot rows (device dI: chunk-local rows, k of them, with
     // R_I in RI) and pivot column set dJ (ascending): pairing, Unew into Uhat
     // rows [r, r+k), old rows reduced at J, Uhat*Omega maintained when sketching.
@@ -1000,16 +1022,31 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             FFB_CHECK_LAUNCH();
         }
         DMat Un = Uhat.sub(r, 0, k, n);
+        // Unew = Kc^-1 R_I and Uhat_old -= Up Unew are needed only by the next
+        // chunk's residual: when sketching they run on the side stream, overlapped
+        // with the next chunk's sketch, row detection and read-back (join_side).
+        cudaStream_t us = st;
+        DMat Up;
         if (r > 0) {  // Up = Uhat_old[:, J] before Uhat_old changes
-            DMat Up = Upd.sub(0, 0, r, k);
+            Up = Upd.sub(0, 0, r, k);
             gather2d(st, Up, Uhat.sub(0, 0, r, n), nullptr, dJ, 0);
-            gemm(f, st, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);  // Unew = Kc^-1 R_I
-            gemm(f, st, GEMM_SUB, Uhat.sub(0, 0, r, n), Up, false, Un, false, r, n, k);
             if (sketching)
                 gemm(f, st, GEMM_SUB, UO.sub(0, 0, r, SK), Up, false, UO.sub(r, 0, k, SK), false, r,
                      SK, k);
-        } else {
-            gemm(f, st, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);
+        }
+        if (sketching && overlap_ok) {
+            FFB_CUDA(cudaEventRecord(ev_main, st));
+            FFB_CUDA(cudaStreamWaitEvent(side, ev_main, 0));
+            us = side;
+        }
+        {
+            SlotGuard slot(us == st ? g_slot : 1);
+            gemm(f, us, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);  // Unew = Kc^-1 R_I
+            if (r > 0) gemm(f, us, GEMM_SUB, Uhat.sub(0, 0, r, n), Up, false, Un, false, r, n, k);
+        }
+        if (us != st) {
+            FFB_CUDA(cudaEventRecord(ev_side, side));
+            side_pending = true;
         }
     };
 
@@ -1050,6 +1087,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 }
                 const int k = *(const int32_t*)io.readback(dinfo, 4);
                 if (k == 0) continue;
+                join_side();  // the previous chunk's Uhat update, before RI / Kinv / Upd are reused
                 const int32_t* dI = dinfo + 1;
                 // exact residual of the k detected rows: R_I = Y_I - Y_I[:, pc] Uhat
                 DMat RIk = RI.sub(0, 0, k, n);
@@ -1091,6 +1129,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 r += k;
             } else {
                 // exact: residual of the whole chunk, then the row-sequential kernel
+                join_side();
                 const size_t mk = ws.mark();
                 DMat Rc = ws.mat(bc, n);
                 copy_mat(st, Rc, Yc);
@@ -1121,6 +1160,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 ws.release(mk);
             }
         }
+        join_side();
         out.r = r;
         std::vector<int32_t> pr, pcol_rows;
         if (r > 0) {  // d_prow and d_pcol are adjacent: one read-back

@@ -564,9 +564,10 @@ struct Scratch {
     int8_t* ptr = nullptr;
     size_t cap = 0;
 };
-thread_local Scratch g_scratch;
+thread_local Scratch g_scratch_slots[2];
 
 int8_t* scratch(size_t bytes) {
+    Scratch& g_scratch = g_scratch_slots[g_slot];
     if (g_scratch.cap < bytes) {
         if (g_scratch.ptr) {
             FFB_CUDA(cudaDeviceSynchronize());

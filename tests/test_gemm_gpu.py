@@ -16,9 +16,10 @@ pytestmark = pytest.mark.gpu
                                    # small M (rows beyond M are TMA zero-fill) and short K
                                    # (the 2-stage, two-CTAs-per-SM variant)
                                    (8, 4096, 1024), (17, 3000, 500), (100, 2048, 64),
-                                   (1000, 3000, 16), (700, 2500, 250), (128, 128, 4096)])
+                                   (1000, 3000, 16), (700, 2500, 250), (128, 128, 4096),
+                                   (513, 1000, 1), (300, 777, 37), (2000, 300, 128)])
 @pytest.mark.parametrize("p", [131, 251, 2, 3])
-@pytest.mark.parametrize("path", ["tc", "mma"])
+@pytest.mark.parametrize("path", ["tc", "mma", "rankk"])
 def test_tc_gemm_nn(gpu, oracle, m, n, k, p, path, monkeypatch):
     """Both int8 paths: tcgen05 (packed, TMA) and warp mma.sync (raw residues)."""
     import paper_1802_10453_b200 as ffb
@@ -35,7 +36,7 @@ def test_tc_gemm_nn(gpu, oracle, m, n, k, p, path, monkeypatch):
 
 
 @pytest.mark.parametrize("n,k", [(300, 200), (520, 130), (256, 2048)])
-@pytest.mark.parametrize("path", ["tc", "mma", "simt"])
+@pytest.mark.parametrize("path", ["tc", "mma", "simt", "rankk"])
 def test_tc_gemm_transposed_operands(gpu, oracle, n, k, path, monkeypatch):
     import paper_1802_10453_b200 as ffb
     monkeypatch.setenv("FFB_GEMM_PATH", path)
