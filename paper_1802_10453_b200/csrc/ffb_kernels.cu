@@ -303,9 +303,22 @@ __global__ void k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int6
     const int64_t i = blockIdx.y;
     const uint32_t* s = Lg + (int64_t)ids[i] * ldl + col0;
     uint32_t* d = dst + i * ldd;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
-         j += (int64_t)gridDim.x * blockDim.x)
-        d[j] = s[j];
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if ((((uintptr_t)s | (uintptr_t)d) & 15) == 0) {  // 16-byte vectors, 2 in flight
+        const int64_t c4 = cols >> 2;
+        const uint4* s4 = reinterpret_cast<const uint4*>(s);
+        uint4* d4 = reinterpret_cast<uint4*>(d);
+        for (; j + step < c4; j += 2 * step) {
+            const uint4 a = __ldg(s4 + j), b = __ldg(s4 + j + step);
+            d4[j] = a;
+            d4[j + step] = b;
+        }
+        for (; j < c4; j += step) d4[j] = __ldg(s4 + j);
+        for (int64_t t = 4 * c4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cols; t += step) d[t] = s[t];
+        return;
+    }
+    for (; j < cols; j += step) d[j] = s[j];
 }
 
 // G[j][k] = (D^-1 X)[k][j], X is r x ncols.  Tile: 32 k x 32 j, with one
@@ -372,19 +385,34 @@ __global__ void k_any_nonzero(const uint32_t* m, int64_t ld, int64_t rows, int64
     if (__syncthreads_or(found) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+// Symmetry check: block (x, y) compares the 32-row band y against the transposed
+// column tiles 8x .. 8x+7 (lower triangle only), both tiles' loads in flight.
 __global__ void k_any_asym(const uint32_t* a, int64_t ld, int64_t n, int32_t* flag) {
     __shared__ uint32_t tile[32][33];
-    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
-    if (c0 > r0 + 31) return;  // only blocks touching the lower triangle
-    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-        const int64_t r = c0 + k, c = r0 + threadIdx.x;  // transposed tile
-        if (r < n && c < n) tile[k][threadIdx.x] = a[r * ld + c];
-    }
-    __syncthreads();
+    const int64_t r0 = (int64_t)blockIdx.y * 32;
     int bad = 0;
-    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
-        const int64_t r = r0 + k, c = c0 + threadIdx.x;
-        if (r < n && c < n) bad |= a[r * ld + c] != tile[threadIdx.x][k];
+    for (int t = 0; t < 8; ++t) {
+        const int64_t c0 = ((int64_t)blockIdx.x * 8 + t) * 32;
+        if (c0 > r0 + 31 || c0 >= n) break;  // uniform
+        uint32_t up[4], lo[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = threadIdx.y + 8 * u;
+            const int64_t r = c0 + k, c = r0 + threadIdx.x;  // transposed tile
+            up[u] = (r < n && c < n) ? __ldg(a + r * ld + c) : 0u;
+            const int64_t rr = r0 + k, cc = c0 + threadIdx.x;
+            lo[u] = (rr < n && cc < n) ? __ldg(a + rr * ld + cc) : 0u;
+        }
+        __syncthreads();  // previous tile's comparisons done
+#pragma unroll
+        for (int u = 0; u < 4; ++u) tile[threadIdx.y + 8 * u][threadIdx.x] = up[u];
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int k = threadIdx.y + 8 * u;
+            const int64_t r = r0 + k, c = c0 + threadIdx.x;
+            if (r < n && c < n) bad |= lo[u] != tile[threadIdx.x][k];
+        }
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0 && threadIdx.y == 0) atomicOr(flag, 1);
 }
@@ -609,7 +637,7 @@ void any_nonzero(cudaStream_t st, DMat m, int32_t* flag) {
 void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (a.rows <= 1) return;
-    dim3 grid((unsigned)cdiv(a.rows, 32), (unsigned)cdiv(a.rows, 32));
+    dim3 grid((unsigned)cdiv(cdiv(a.rows, 32), 8), (unsigned)cdiv(a.rows, 32));
     k_any_asym<<<grid, dim3(32, 8), 0, st>>>(a.ptr, a.ld, a.rows, flag);
     count_launch();
     FFB_CHECK_LAUNCH();
