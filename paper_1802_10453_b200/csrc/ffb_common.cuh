@@ -9,6 +9,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <stdexcept>
 #include <string>
@@ -34,6 +35,41 @@ struct Status : std::runtime_error {
     } while (0)
 
 #define FFB_CHECK_LAUNCH() FFB_CUDA(cudaGetLastError())
+
+// ---------------------------------------------------------------------------
+// Programmatic dependent launch.  Every kernel starts with FFB_PDL_ENTRY():
+// it lets the next kernel in the stream be scheduled right away and then waits
+// until this kernel's predecessor has completed (its writes visible) -- so a
+// kernel never touches memory before its predecessor is done, while the
+// launch latency and CTA ramp-up overlap the predecessor's tail.  Without a
+// programmatic launch both instructions are no-ops.
+// ---------------------------------------------------------------------------
+#define FFB_PDL_ENTRY()                                                    \
+    do {                                                                   \
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");     \
+        asm volatile("griddepcontrol.wait;" ::: "memory");                  \
+    } while (0)
+
+// kernel<<<grid, block, smem, st>>>(args...) with the programmatic-serialization
+// attribute (FFB_NO_PDL=1 disables it); arguments are coerced to the kernel's
+// parameter types like a <<<>>> launch.
+template <typename... KArgs, typename... Args>
+inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                     Args&&... args) {
+    static_assert(sizeof...(KArgs) == sizeof...(Args), "kernel argument count");
+    static const bool pdl = getenv("FFB_NO_PDL") == nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
 
 // ---------------------------------------------------------------------------
 // Field constants (passed by value to every kernel).

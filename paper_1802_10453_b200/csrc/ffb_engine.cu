@@ -184,6 +184,7 @@ const void* readback(ffb_context* c, const void* dev, size_t bytes) {
 }
 
 __global__ void k_inv_table(uint32_t* t, uint32_t p) {
+    FFB_PDL_ENTRY();
     const uint32_t a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a < p) t[a] = a ? finv_euclid(p, a) : 0u;
 }
@@ -198,7 +199,7 @@ Fp make_field(ffb_context* c, uint64_t p) {
             c->inv_table = nullptr;
             c->inv_p = 0;
             FFB_CUDA(cudaMalloc(&c->inv_table, p * sizeof(uint32_t)));
-            k_inv_table<<<(unsigned)cdiv((int64_t)p, 256), 256, 0, c->stream>>>(c->inv_table, (uint32_t)p);
+            launch_k(k_inv_table, (unsigned)cdiv((int64_t)p, 256), 256, 0, c->stream, c->inv_table, (uint32_t)p);
             FFB_CHECK_LAUNCH();
             FFB_CUDA(cudaStreamSynchronize(c->stream));
             c->inv_p = (uint32_t)p;

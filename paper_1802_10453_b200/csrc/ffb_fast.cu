@@ -43,6 +43,7 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
                                                 int s, const int32_t* __restrict__ rows,
                                                 uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
                                                 int32_t* out) {
+    FFB_PDL_ENTRY();
     __shared__ uint32_t Ls[64][65];
     __shared__ uint32_t colb[2][64];  // residual column of the front row, double-buffered
     __shared__ uint32_t col2[64];     // residual column of the 2x2 partner
@@ -194,6 +195,7 @@ __device__ __forceinline__ uint32_t dot_lt(const Fp& f, const uint32_t* a, int s
 template <int kMode>
 __global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
                                                  int64_t n, uint32_t* Tinv) {
+    FFB_PDL_ENTRY();
     __shared__ uint32_t Ts[64][65];
     __shared__ uint32_t X[64][65];  // W = C A^-1 of a level is kept transposed in Ts's upper triangle
     const int b = blockIdx.x;
@@ -257,6 +259,7 @@ template <bool kSmall>
 __global__ void __launch_bounds__(256) k_trsm_panel(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
                                                     const uint32_t* __restrict__ Tinv, uint32_t* B,
                                                     int64_t ldb, int nb, int64_t ncols) {
+    FFB_PDL_ENTRY();
     extern __shared__ uint32_t sm[];
     uint32_t* Xs = sm;                     // 256 x (PNL_COLS+1)
     uint32_t* Ms = Xs + 256 * (PNL_COLS + 1);  // one 64 x 65 matrix block
@@ -353,6 +356,7 @@ __device__ __forceinline__ void pm_mma(int (&acc)[4][4], const int8_t* Ab, const
 __global__ void __launch_bounds__(256, 2) k_trsm_panel_mma(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
                                                            const uint32_t* __restrict__ Tinv, uint32_t* B,
                                                            int64_t ldb, int nb, int64_t ncols) {
+    FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint8_t pm_smem[];
     uint32_t* Xu = (uint32_t*)pm_smem;                     // 256 x PM_XU
     int8_t* XbT = (int8_t*)(Xu + 256 * PM_XU);             // PM_COLS x PM_XB (column-major int8 X)
@@ -465,7 +469,7 @@ void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tin
                                               (int)PM_SMEM));
                 attr_mma = true;
             }
-            k_trsm_panel_mma<<<(unsigned)cdiv(B.cols, PM_COLS), 256, PM_SMEM, st>>>(f, T.ptr, T.ld, ti, B.ptr,
+            launch_k(k_trsm_panel_mma, (unsigned)cdiv(B.cols, PM_COLS), 256, PM_SMEM, st, f, T.ptr, T.ld, ti, B.ptr,
                                                                                  B.ld, (int)n, B.cols);
             ++g_launches;
             FFB_CHECK_LAUNCH();
@@ -480,9 +484,9 @@ void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tin
         }
         dim3 grid((unsigned)cdiv(B.cols, PNL_COLS));
         if (f.p < (1u << 23))
-            k_trsm_panel<true><<<grid, 256, smem, st>>>(f, T.ptr, T.ld, ti, B.ptr, B.ld, (int)n, B.cols);
+            launch_k(k_trsm_panel<true>, grid, 256, smem, st, f, T.ptr, T.ld, ti, B.ptr, B.ld, (int)n, B.cols);
         else
-            k_trsm_panel<false><<<grid, 256, smem, st>>>(f, T.ptr, T.ld, ti, B.ptr, B.ld, (int)n, B.cols);
+            launch_k(k_trsm_panel<false>, grid, 256, smem, st, f, T.ptr, T.ld, ti, B.ptr, B.ld, (int)n, B.cols);
         ++g_launches;
         FFB_CHECK_LAUNCH();
         return;
@@ -505,9 +509,9 @@ void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, 
     const int s = (int)A.rows;
     ProfScope ps(K_LEAF, st, 2.0 * s * s * s / 3.0, 4.0 * s * s);
     if (f.p < (1u << 16))
-        k_leaf64<true><<<1, 256, 0, st>>>(f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out);
+        launch_k(k_leaf64<true>, 1, 256, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out);
     else
-        k_leaf64<false><<<1, 256, 0, st>>>(f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out);
+        launch_k(k_leaf64<false>, 1, 256, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out);
     ++g_launches;
     FFB_CHECK_LAUNCH();
 }
@@ -520,11 +524,11 @@ void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
     {
         ProfScope ps(K_TRSM, st, (double)n * 64 * 64 / 3, 8.0 * n * 64, n, B.cols, 0);
         if (f.p < 4096u)
-            k_trinv64<0><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+            launch_k(k_trinv64<0>, (unsigned)nblk, 256, 0, st, f, T.ptr, T.ld, n, Tinv);
         else if (f.p < (1u << 23))
-            k_trinv64<1><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+            launch_k(k_trinv64<1>, (unsigned)nblk, 256, 0, st, f, T.ptr, T.ld, n, Tinv);
         else
-            k_trinv64<2><<<(unsigned)nblk, 256, 0, st>>>(f, T.ptr, T.ld, n, Tinv);
+            launch_k(k_trinv64<2>, (unsigned)nblk, 256, 0, st, f, T.ptr, T.ld, n, Tinv);
         ++g_launches;
         FFB_CHECK_LAUNCH();
     }

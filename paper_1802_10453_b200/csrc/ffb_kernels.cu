@@ -87,6 +87,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(Fp f, int mode, uint32_t* __r
                                                    int64_t ldc, const uint32_t* __restrict__ A,
                                                    int64_t lda, const uint32_t* __restrict__ B,
                                                    int64_t ldb, int64_t M, int64_t N, int64_t K) {
+    FFB_PDL_ENTRY();
     __shared__ uint32_t As[GB_K][GB_M + 4];
     __shared__ uint32_t Bs[GB_K][GB_N + 4];
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
@@ -177,10 +178,10 @@ void launch_gemm_simt(const Fp& f, cudaStream_t st, int mode, DMat C, DMat A, DM
     dim3 grid((unsigned)cdiv(N, GB_N), (unsigned)cdiv(M, GB_M));
     ProfScope ps(K_GEMM, st, 2.0 * M * N * K, 4.0 * (M * K + K * N + 2 * M * N), -M, N, K);  // -M marks SIMT
     if (f.p < (1u << 23))
-        k_gemm_simt<TA, TB, false><<<grid, 256, 0, st>>>(f, mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr,
+        launch_k(k_gemm_simt<TA, TB, false>, grid, 256, 0, st, f, mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr,
                                                           B.ld, M, N, K);
     else
-        k_gemm_simt<TA, TB, true><<<grid, 256, 0, st>>>(f, mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr,
+        launch_k(k_gemm_simt<TA, TB, true>, grid, 256, 0, st, f, mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr,
                                                          B.ld, M, N, K);
     count_launch();
     FFB_CHECK_LAUNCH();
@@ -234,6 +235,7 @@ namespace {
 
 __global__ void k_gather_rows(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
                               const int32_t* idx, int64_t rows, int64_t cols) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     const uint32_t* s = src + (int64_t)idx[i] * lds;
     uint32_t* d = dst + i * ldd;
@@ -252,6 +254,7 @@ struct RowGather {
     int64_t c0, rows, cols;
 };
 __global__ void k_gather_rows2(RowGather g0, RowGather g1) {
+    FFB_PDL_ENTRY();
     const RowGather& g = blockIdx.z == 0 ? g0 : g1;
     const int64_t i = blockIdx.y;
     if (i >= g.rows) return;
@@ -264,6 +267,7 @@ __global__ void k_gather_rows2(RowGather g0, RowGather g1) {
 
 __global__ void k_gather_sym(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
                              const int32_t* ridx, const int32_t* idx, int64_t n) {
+    FFB_PDL_ENTRY();
     const int64_t a = blockIdx.y;
     const uint32_t* s = src + (int64_t)ridx[a] * lds;
     uint32_t* d = dst + a * ldd;
@@ -274,6 +278,7 @@ __global__ void k_gather_sym(uint32_t* dst, int64_t ldd, const uint32_t* src, in
 
 __global__ void k_transpose(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
                             int64_t rows, int64_t cols) {
+    FFB_PDL_ENTRY();
     __shared__ uint32_t tile[32][33];
     const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
     for (int k = threadIdx.y; k < 32; k += blockDim.y) {
@@ -290,6 +295,7 @@ __global__ void k_transpose(uint32_t* dst, int64_t ldd, const uint32_t* src, int
 __global__ void k_scatter_lg(uint32_t* Lg, int64_t ldl, const int32_t* ids, int64_t col0,
                              int cstride, const uint32_t* src, int64_t lds, int64_t rows,
                              int64_t cols) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     uint32_t* d = Lg + (int64_t)ids[i] * ldl + col0;
     const uint32_t* s = src + i * lds;
@@ -300,6 +306,7 @@ __global__ void k_scatter_lg(uint32_t* Lg, int64_t ldl, const int32_t* ids, int6
 
 __global__ void k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int64_t ldl,
                             const int32_t* ids, int64_t col0, int64_t cols) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     const uint32_t* s = Lg + (int64_t)ids[i] * ldl + col0;
     uint32_t* d = dst + i * ldd;
@@ -326,6 +333,7 @@ __global__ void k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int6
 __global__ void k_inverse_apply_T(Fp f, uint32_t* G, int64_t ldg, const uint32_t* X,
                                   int64_t ldx, int64_t r, int64_t ncols, DDiag D, int64_t coff,
                                   uint32_t* Lg, int64_t ldl, const int32_t* ids) {
+    FFB_PDL_ENTRY();
     __shared__ uint32_t tile[34][33];
     const int64_t k0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
     for (int kk = threadIdx.y; kk < 34; kk += blockDim.y) {
@@ -357,6 +365,7 @@ __global__ void k_inverse_apply_T(Fp f, uint32_t* G, int64_t ldg, const uint32_t
 
 __global__ void k_scale_T(Fp f, uint32_t* G, int64_t ldg, const uint32_t* X, int64_t ldx,
                           int64_t r, int64_t ncols, const uint32_t* dinv) {
+    FFB_PDL_ENTRY();
     __shared__ uint32_t tile[32][33];
     const int64_t k0 = (int64_t)blockIdx.y * 32, j0 = (int64_t)blockIdx.x * 32;
     for (int kk = threadIdx.y; kk < 32; kk += blockDim.y) {
@@ -371,12 +380,14 @@ __global__ void k_scale_T(Fp f, uint32_t* G, int64_t ldg, const uint32_t* X, int
 }
 
 __global__ void k_invert_vec(Fp f, uint32_t* out, const uint32_t* v, int64_t n) {
+    FFB_PDL_ENTRY();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i < n) out[i] = finv(f, v[i]);
 }
 
 __global__ void k_any_nonzero(const uint32_t* m, int64_t ld, int64_t rows, int64_t cols,
                               int32_t* flag) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     int found = 0;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
@@ -388,6 +399,7 @@ __global__ void k_any_nonzero(const uint32_t* m, int64_t ld, int64_t rows, int64
 // Symmetry check: block (x, y) compares the 32-row band y against the transposed
 // column tiles 8x .. 8x+7 (lower triangle only), both tiles' loads in flight.
 __global__ void k_any_asym(const uint32_t* a, int64_t ld, int64_t n, int32_t* flag) {
+    FFB_PDL_ENTRY();
     __shared__ uint32_t tile[32][33];
     const int64_t r0 = (int64_t)blockIdx.y * 32;
     int bad = 0;
@@ -418,6 +430,7 @@ __global__ void k_any_asym(const uint32_t* a, int64_t ld, int64_t n, int32_t* fl
 }
 
 __global__ void k_trssyr2k_mid(Fp f, uint32_t* C, int64_t ld, int64_t n, int32_t* flag) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x) {
@@ -437,6 +450,7 @@ __global__ void k_trssyr2k_mid(Fp f, uint32_t* C, int64_t ld, int64_t n, int32_t
 
 __global__ void k_write_pair_diag(DDiag D, int64_t coff, const uint32_t* d, const uint32_t* dinv,
                                   const uint32_t* delta, int64_t r) {
+    FFB_PDL_ENTRY();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= r) return;
     const uint32_t dl = delta ? delta[i] : 0;
@@ -450,6 +464,7 @@ __global__ void k_write_pair_diag(DDiag D, int64_t coff, const uint32_t* d, cons
 
 __global__ void k_char2_delta(Fp f, const uint32_t* C1, int64_t ldc, const uint32_t* U1,
                               int64_t ldu, int64_t r, uint32_t* delta) {
+    FFB_PDL_ENTRY();
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     for (int64_t i = 0; i < r; ++i) {
         uint32_t acc = C1[i * ldc + i];
@@ -463,6 +478,7 @@ __global__ void k_char2_delta(Fp f, const uint32_t* C1, int64_t ldc, const uint3
 
 __global__ void k_scale_rows(Fp f, uint32_t* H, int64_t ldh, const uint32_t* S, int64_t lds,
                              int64_t cols, const uint32_t* v) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     const uint32_t s = v[i];
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
@@ -472,6 +488,7 @@ __global__ void k_scale_rows(Fp f, uint32_t* H, int64_t ldh, const uint32_t* S, 
 
 __global__ void k_add_scaled_rows_upper(Fp f, uint32_t* X, int64_t ldx, const uint32_t* U,
                                         int64_t ldu, int64_t cols, const uint32_t* v) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     const uint32_t s = v[i];
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
@@ -480,6 +497,7 @@ __global__ void k_add_scaled_rows_upper(Fp f, uint32_t* X, int64_t ldx, const ui
 }
 
 __global__ void k_zero(uint32_t* m, int64_t ld, int64_t cols) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
          j += (int64_t)gridDim.x * blockDim.x)
@@ -489,6 +507,7 @@ __global__ void k_zero(uint32_t* m, int64_t ld, int64_t cols) {
 template <typename T>
 __global__ void k_convert_in(Fp f, uint32_t* dst, int64_t ldd, const T* src, int64_t rows,
                              int64_t cols) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
          j += (int64_t)gridDim.x * blockDim.x) {
@@ -500,6 +519,7 @@ __global__ void k_convert_in(Fp f, uint32_t* dst, int64_t ldd, const T* src, int
 template <typename T>
 __global__ void k_convert_out(T* dst, const uint32_t* src, int64_t lds, int64_t rows,
                               int64_t cols) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
          j += (int64_t)gridDim.x * blockDim.x)
@@ -523,7 +543,7 @@ void gather_rows(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
     if (dst.rows <= 0 || dst.cols <= 0) return;
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
-        k_gather_rows<<<rowgrid(nr, dst.cols), 256, 0, st>>>(dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
+        launch_k(k_gather_rows, rowgrid(nr, dst.cols), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
                                                              src.ld, idx + r0, nr, dst.cols);
         count_launch();
     }
@@ -535,7 +555,7 @@ void gather_sym(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
     if (dst.rows <= 0) return;
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
-        k_gather_sym<<<rowgrid(nr, dst.cols), 256, 0, st>>>(dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
+        launch_k(k_gather_sym, rowgrid(nr, dst.cols), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
                                                             src.ld, idx + r0, idx, dst.cols);
         count_launch();
     }
@@ -546,7 +566,7 @@ void transpose(cudaStream_t st, DMat dst, DMat src) {
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (src.rows <= 0 || src.cols <= 0) return;
     dim3 grid((unsigned)cdiv(src.cols, 32), (unsigned)cdiv(src.rows, 32));
-    k_transpose<<<grid, dim3(32, 8), 0, st>>>(dst.ptr, dst.ld, src.ptr, src.ld, src.rows, src.cols);
+    launch_k(k_transpose, grid, dim3(32, 8), 0, st, dst.ptr, dst.ld, src.ptr, src.ld, src.rows, src.cols);
     count_launch();
     FFB_CHECK_LAUNCH();
 }
@@ -556,7 +576,7 @@ void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int 
     if (src.rows <= 0 || src.cols <= 0) return;
     for (int64_t r0 = 0; r0 < src.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, src.rows - r0);
-        k_scatter_lg<<<rowgrid(nr, src.cols), 256, 0, st>>>(Lg.ptr, Lg.ld, ids + r0, col0, cstride,
+        launch_k(k_scatter_lg, rowgrid(nr, src.cols), 256, 0, st, Lg.ptr, Lg.ld, ids + r0, col0, cstride,
                                                             src.ptr + r0 * src.ld, src.ld, nr,
                                                             src.cols);
         count_launch();
@@ -578,7 +598,7 @@ void gather_rows2(cudaStream_t st, DMat d0, DMat s0, const int32_t* i0, int64_t 
     RowGather g1{d1.ptr, d1.ld, s1.ptr, s1.ld, i1, c1, d1.cols > 0 ? d1.rows : 0, d1.cols};
     dim3 g = rowgrid(rows, cols);
     g.z = 2;
-    k_gather_rows2<<<g, 256, 0, st>>>(g0, g1);
+    launch_k(k_gather_rows2, g, 256, 0, st, g0, g1);
     count_launch();
     FFB_CHECK_LAUNCH();
 }
@@ -588,7 +608,7 @@ void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t c
     if (dst.rows <= 0 || dst.cols <= 0) return;
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
-        k_gather_lg<<<rowgrid(nr, dst.cols), 256, 0, st>>>(dst.ptr + r0 * dst.ld, dst.ld, Lg.ptr,
+        launch_k(k_gather_lg, rowgrid(nr, dst.cols), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, Lg.ptr,
                                                            Lg.ld, ids + r0, col0, dst.cols);
         count_launch();
     }
@@ -600,7 +620,7 @@ void inverse_apply_T(const Fp& f, cudaStream_t st, DMat G, DMat X, DDiag D, int6
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (X.rows <= 0 || X.cols <= 0) return;
     dim3 grid((unsigned)cdiv(X.cols, 32), (unsigned)cdiv(X.rows, 32));
-    k_inverse_apply_T<<<grid, dim3(32, 8), 0, st>>>(f, G.ptr, G.ld, X.ptr, X.ld, X.rows, X.cols, D,
+    launch_k(k_inverse_apply_T, grid, dim3(32, 8), 0, st, f, G.ptr, G.ld, X.ptr, X.ld, X.rows, X.cols, D,
                                                     coff, ids ? Lg.ptr : nullptr, Lg.ld, ids);
     count_launch();
     FFB_CHECK_LAUNCH();
@@ -610,7 +630,7 @@ void scale_T(const Fp& f, cudaStream_t st, DMat G, DMat X, const uint32_t* dinv)
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (X.rows <= 0 || X.cols <= 0) return;
     dim3 grid((unsigned)cdiv(X.cols, 32), (unsigned)cdiv(X.rows, 32));
-    k_scale_T<<<grid, dim3(32, 8), 0, st>>>(f, G.ptr, G.ld, X.ptr, X.ld, X.rows, X.cols, dinv);
+    launch_k(k_scale_T, grid, dim3(32, 8), 0, st, f, G.ptr, G.ld, X.ptr, X.ld, X.rows, X.cols, dinv);
     count_launch();
     FFB_CHECK_LAUNCH();
 }
@@ -618,7 +638,7 @@ void scale_T(const Fp& f, cudaStream_t st, DMat G, DMat X, const uint32_t* dinv)
 void invert_vec(const Fp& f, cudaStream_t st, uint32_t* out, const uint32_t* v, int64_t n) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (n <= 0) return;
-    k_invert_vec<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(f, out, v, n);
+    launch_k(k_invert_vec, (unsigned)cdiv(n, 256), 256, 0, st, f, out, v, n);
     count_launch();
     FFB_CHECK_LAUNCH();
 }
@@ -628,7 +648,7 @@ void any_nonzero(cudaStream_t st, DMat m, int32_t* flag) {
     if (m.rows <= 0 || m.cols <= 0) return;
     for (int64_t r0 = 0; r0 < m.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, m.rows - r0);
-        k_any_nonzero<<<rowgrid(nr, m.cols), 256, 0, st>>>(m.ptr + r0 * m.ld, m.ld, nr, m.cols, flag);
+        launch_k(k_any_nonzero, rowgrid(nr, m.cols), 256, 0, st, m.ptr + r0 * m.ld, m.ld, nr, m.cols, flag);
         count_launch();
     }
     FFB_CHECK_LAUNCH();
@@ -638,7 +658,7 @@ void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (a.rows <= 1) return;
     dim3 grid((unsigned)cdiv(cdiv(a.rows, 32), 8), (unsigned)cdiv(a.rows, 32));
-    k_any_asym<<<grid, dim3(32, 8), 0, st>>>(a.ptr, a.ld, a.rows, flag);
+    launch_k(k_any_asym, grid, dim3(32, 8), 0, st, a.ptr, a.ld, a.rows, flag);
     count_launch();
     FFB_CHECK_LAUNCH();
 }
@@ -646,7 +666,7 @@ void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag) {
 void trssyr2k_mid(const Fp& f, cudaStream_t st, DMat Ct, int32_t* flag) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (Ct.rows <= 0) return;
-    k_trssyr2k_mid<<<rowgrid(Ct.rows, Ct.cols), 256, 0, st>>>(f, Ct.ptr, Ct.ld, Ct.rows, flag);
+    launch_k(k_trssyr2k_mid, rowgrid(Ct.rows, Ct.cols), 256, 0, st, f, Ct.ptr, Ct.ld, Ct.rows, flag);
     count_launch();
     FFB_CHECK_LAUNCH();
 }
@@ -656,7 +676,7 @@ void write_pair_diag(const Fp& f, cudaStream_t st, DDiag D, int64_t coff, const 
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     (void)f;
     if (r <= 0) return;
-    k_write_pair_diag<<<(unsigned)cdiv(r, 256), 256, 0, st>>>(D, coff, d, dinv, delta, r);
+    launch_k(k_write_pair_diag, (unsigned)cdiv(r, 256), 256, 0, st, D, coff, d, dinv, delta, r);
     count_launch();
     FFB_CHECK_LAUNCH();
 }
@@ -664,7 +684,7 @@ void write_pair_diag(const Fp& f, cudaStream_t st, DDiag D, int64_t coff, const 
 void char2_delta(const Fp& f, cudaStream_t st, DMat C1, DMat U1, uint32_t* delta) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (C1.rows <= 0) return;
-    k_char2_delta<<<1, 32, 0, st>>>(f, C1.ptr, C1.ld, U1.ptr, U1.ld, C1.rows, delta);
+    launch_k(k_char2_delta, 1, 32, 0, st, f, C1.ptr, C1.ld, U1.ptr, U1.ld, C1.rows, delta);
     count_launch();
     FFB_CHECK_LAUNCH();
 }
@@ -672,7 +692,7 @@ void char2_delta(const Fp& f, cudaStream_t st, DMat C1, DMat U1, uint32_t* delta
 void scale_rows(const Fp& f, cudaStream_t st, DMat H, DMat S, const uint32_t* v) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (S.rows <= 0 || S.cols <= 0) return;
-    k_scale_rows<<<rowgrid(S.rows, S.cols), 256, 0, st>>>(f, H.ptr, H.ld, S.ptr, S.ld, S.cols, v);
+    launch_k(k_scale_rows, rowgrid(S.rows, S.cols), 256, 0, st, f, H.ptr, H.ld, S.ptr, S.ld, S.cols, v);
     count_launch();
     FFB_CHECK_LAUNCH();
 }
@@ -680,7 +700,7 @@ void scale_rows(const Fp& f, cudaStream_t st, DMat H, DMat S, const uint32_t* v)
 void add_scaled_rows_upper(const Fp& f, cudaStream_t st, DMat X, DMat U, const uint32_t* v) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (X.rows <= 0) return;
-    k_add_scaled_rows_upper<<<rowgrid(X.rows, X.cols), 256, 0, st>>>(f, X.ptr, X.ld, U.ptr, U.ld,
+    launch_k(k_add_scaled_rows_upper, rowgrid(X.rows, X.cols), 256, 0, st, f, X.ptr, X.ld, U.ptr, U.ld,
                                                                      X.cols, v);
     count_launch();
     FFB_CHECK_LAUNCH();
@@ -695,7 +715,7 @@ void zero_mat(cudaStream_t st, DMat m) {
     }
     for (int64_t r0 = 0; r0 < m.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, m.rows - r0);
-        k_zero<<<rowgrid(nr, m.cols), 256, 0, st>>>(m.ptr + r0 * m.ld, m.ld, m.cols);
+        launch_k(k_zero, rowgrid(nr, m.cols), 256, 0, st, m.ptr + r0 * m.ld, m.ld, m.cols);
         count_launch();
     }
     FFB_CHECK_LAUNCH();
@@ -708,10 +728,10 @@ void convert_in(const Fp& f, cudaStream_t st, DMat dst, const void* src, int eb)
         dim3 g = rowgrid(nr, dst.cols);
         uint32_t* d = dst.ptr + r0 * dst.ld;
         const size_t off = (size_t)r0 * dst.cols;
-        if (eb == 8) k_convert_in<uint64_t><<<g, 256, 0, st>>>(f, d, dst.ld, (const uint64_t*)src + off, nr, dst.cols);
-        else if (eb == 4) k_convert_in<uint32_t><<<g, 256, 0, st>>>(f, d, dst.ld, (const uint32_t*)src + off, nr, dst.cols);
-        else if (eb == 2) k_convert_in<uint16_t><<<g, 256, 0, st>>>(f, d, dst.ld, (const uint16_t*)src + off, nr, dst.cols);
-        else k_convert_in<uint8_t><<<g, 256, 0, st>>>(f, d, dst.ld, (const uint8_t*)src + off, nr, dst.cols);
+        if (eb == 8) launch_k(k_convert_in<uint64_t>, g, 256, 0, st, f, d, dst.ld, (const uint64_t*)src + off, nr, dst.cols);
+        else if (eb == 4) launch_k(k_convert_in<uint32_t>, g, 256, 0, st, f, d, dst.ld, (const uint32_t*)src + off, nr, dst.cols);
+        else if (eb == 2) launch_k(k_convert_in<uint16_t>, g, 256, 0, st, f, d, dst.ld, (const uint16_t*)src + off, nr, dst.cols);
+        else launch_k(k_convert_in<uint8_t>, g, 256, 0, st, f, d, dst.ld, (const uint8_t*)src + off, nr, dst.cols);
         count_launch();
     }
     FFB_CHECK_LAUNCH();
@@ -724,10 +744,10 @@ void convert_out(cudaStream_t st, void* dst, int eb, DMat src) {
         dim3 g = rowgrid(nr, src.cols);
         const uint32_t* s = src.ptr + r0 * src.ld;
         const size_t off = (size_t)r0 * src.cols;
-        if (eb == 8) k_convert_out<uint64_t><<<g, 256, 0, st>>>((uint64_t*)dst + off, s, src.ld, nr, src.cols);
-        else if (eb == 4) k_convert_out<uint32_t><<<g, 256, 0, st>>>((uint32_t*)dst + off, s, src.ld, nr, src.cols);
-        else if (eb == 2) k_convert_out<uint16_t><<<g, 256, 0, st>>>((uint16_t*)dst + off, s, src.ld, nr, src.cols);
-        else k_convert_out<uint8_t><<<g, 256, 0, st>>>((uint8_t*)dst + off, s, src.ld, nr, src.cols);
+        if (eb == 8) launch_k(k_convert_out<uint64_t>, g, 256, 0, st, (uint64_t*)dst + off, s, src.ld, nr, src.cols);
+        else if (eb == 4) launch_k(k_convert_out<uint32_t>, g, 256, 0, st, (uint32_t*)dst + off, s, src.ld, nr, src.cols);
+        else if (eb == 2) launch_k(k_convert_out<uint16_t>, g, 256, 0, st, (uint16_t*)dst + off, s, src.ld, nr, src.cols);
+        else launch_k(k_convert_out<uint8_t>, g, 256, 0, st, (uint8_t*)dst + off, s, src.ld, nr, src.cols);
         count_launch();
     }
     FFB_CHECK_LAUNCH();
@@ -764,6 +784,7 @@ __global__ void __launch_bounds__(LEAF_THREADS)
     k_leaf_crout(Fp f, const uint32_t* __restrict__ A, int64_t lda, int s, uint32_t* gscratch,
                  int use_smem, const int32_t* __restrict__ rows, uint32_t* Lg, int64_t ldL,
                  int64_t coff, DDiag D, int32_t* out) {
+    FFB_PDL_ENTRY();
     extern __shared__ uint32_t smem[];
     uint32_t* base = use_smem ? smem : gscratch;
     uint32_t* S = base;
@@ -924,7 +945,7 @@ void leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat 
                                       (int)bytes));
     }
     ProfScope ps(K_LEAF, st, 2.0 * s * s * s / 3.0, 4.0 * s * s);
-    k_leaf_crout<<<1, LEAF_THREADS, bytes, st>>>(f, A.ptr, A.ld, s, scratch, smem ? 1 : 0, rows,
+    launch_k(k_leaf_crout, 1, LEAF_THREADS, bytes, st, f, A.ptr, A.ld, s, scratch, smem ? 1 : 0, rows,
                                                  Lg.ptr, Lg.ld, coff, D, out);
     count_launch();
     FFB_CHECK_LAUNCH();
@@ -944,6 +965,7 @@ constexpr int PLDUQ_THREADS = 1024;
 __global__ void __launch_bounds__(PLDUQ_THREADS)
     k_plduq_v1(Fp f, uint32_t* W, int64_t ldw, int m, int n, int32_t* info, int32_t* colflag,
                uint32_t* lvec, uint32_t* Lo, int64_t ldlo, uint32_t* d, uint32_t* Uo, int64_t lduo) {
+    FFB_PDL_ENTRY();
     __shared__ int jmin;
     __shared__ uint32_t sxi;
     const int tid = threadIdx.x;
@@ -1031,7 +1053,7 @@ __global__ void __launch_bounds__(PLDUQ_THREADS)
 void plduq(const Fp& f, cudaStream_t st, DMat W, int32_t* info, int32_t* colflag, uint32_t* lvec,
            DMat Lo, uint32_t* d, DMat Uo) {
     ProfScope ps(K_PLDUQ, st, 0.0, 4.0 * W.rows * W.cols);
-    k_plduq_v1<<<1, PLDUQ_THREADS, 0, st>>>(f, W.ptr, W.ld, (int)W.rows, (int)W.cols, info, colflag,
+    launch_k(k_plduq_v1, 1, PLDUQ_THREADS, 0, st, f, W.ptr, W.ld, (int)W.rows, (int)W.cols, info, colflag,
                                             lvec, Lo.ptr, Lo.ld, d, Uo.ptr, Uo.ld);
     count_launch();
     FFB_CHECK_LAUNCH();

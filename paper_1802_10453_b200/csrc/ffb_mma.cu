@@ -25,6 +25,7 @@ __global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* __re
                                                   const uint32_t* __restrict__ A, int64_t lda,
                                                   const uint32_t* __restrict__ B, int64_t ldb, int64_t M,
                                                   int64_t N, int64_t K, int64_t kc, uint32_t* __restrict__ W) {
+    FFB_PDL_ENTRY();
     __shared__ __align__(16) int8_t As[MM_T * MM_S];  // op(A) tile [m][k]
     __shared__ __align__(16) int8_t Bs[MM_T * MM_S];  // op(B) tile transposed [n][k]
     __shared__ uint32_t Cs[MM_T][MM_T + 1];           // reduced tile, for a coalesced epilogue
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* __re
 // C = C -/+ sum_z W[z]  or  sum_z W[z]   (mod p)
 __global__ void k_splitk_fold(Fp f, int mode, uint32_t* C, int64_t ldc, const uint32_t* W, int64_t M,
                               int64_t N, int S) {
+    FFB_PDL_ENTRY();
     const int64_t row = blockIdx.y;
     for (int64_t col = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; col < N;
          col += (int64_t)gridDim.x * blockDim.x) {
@@ -164,7 +166,7 @@ void mma_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool 
     uint32_t* W = S > 1 ? mma_scratch((size_t)S * M * N) : nullptr;
     const dim3 grid((unsigned)cdiv(N, MM_T), (unsigned)cdiv(M, MM_T), (unsigned)S);
 #define FFB_MMA_LAUNCH(TA, TB)                                                                       \
-    k_gemm_mma<TA, TB><<<grid, 256, 0, st>>>(f, (int)mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr, B.ld, M, N, K, \
+    launch_k(k_gemm_mma<TA, TB>, grid, 256, 0, st, f, (int)mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr, B.ld, M, N, K, \
                                              kc, W)
     if (!ta && !tb) FFB_MMA_LAUNCH(false, false);
     else if (ta && !tb) FFB_MMA_LAUNCH(true, false);
@@ -173,7 +175,7 @@ void mma_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool 
 #undef FFB_MMA_LAUNCH
     if (S > 1) {
         ++g_launches;
-        k_splitk_fold<<<dim3((unsigned)cdiv(N, 256), (unsigned)M), 256, 0, st>>>(f, (int)mode, C.ptr, C.ld, W, M,
+        launch_k(k_splitk_fold, dim3((unsigned)cdiv(N, 256), (unsigned)M), 256, 0, st, f, (int)mode, C.ptr, C.ld, W, M,
                                                                                   N, S);
     }
     ++g_launches;
@@ -204,6 +206,7 @@ __global__ void __launch_bounds__(256) k_rankk_dp4a(Fp f, int mode, uint32_t* __
                                                     const uint32_t* __restrict__ A, int64_t lda,
                                                     const uint32_t* __restrict__ B, int64_t ldb, int64_t M,
                                                     int64_t N, int K, int TR) {
+    FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint32_t rk_sm[];
     const int K4 = (K + 3) >> 2;
     uint32_t* Bp = rk_sm;                       // [K4][RK_COLS]  packs of op(B)[4q..4q+3][j]
@@ -306,7 +309,7 @@ void rankk_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, boo
     }
     const dim3 grid((unsigned)ncb, (unsigned)cdiv(M, TR));
 #define FFB_RK_LAUNCH(TA, TB) \
-    k_rankk_dp4a<TA, TB><<<grid, 256, smem, st>>>(f, (int)mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr, B.ld, M, N, (int)K, TR)
+    launch_k(k_rankk_dp4a<TA, TB>, grid, 256, smem, st, f, (int)mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr, B.ld, M, N, (int)K, TR)
     if (!ta && !tb) FFB_RK_LAUNCH(false, false);
     else if (ta && !tb) FFB_RK_LAUNCH(true, false);
     else if (!ta && tb) FFB_RK_LAUNCH(false, true);

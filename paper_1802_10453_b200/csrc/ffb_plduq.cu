@@ -44,6 +44,7 @@ inline void count_launch() { ++g_launches; }
 // dst[a][b] = src[roff + (ridx ? ridx[a] : a)][cidx[b]]
 __global__ void k_gather2d(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
                            const int32_t* ridx, int64_t roff, const int32_t* cidx, int64_t cols) {
+    FFB_PDL_ENTRY();
     const int64_t a = blockIdx.y;
     const int64_t sr = roff + (ridx ? ridx[a] : a);
     const uint32_t* s = src + sr * lds;
@@ -54,6 +55,7 @@ __global__ void k_gather2d(uint32_t* dst, int64_t ldd, const uint32_t* src, int6
 }
 
 __global__ void k_random(uint32_t* out, int64_t n, uint64_t seed, uint32_t p) {
+    FFB_PDL_ENTRY();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     uint64_t z = seed + 0x9E3779B97F4A7C15ull * (uint64_t)(i + 1);
@@ -269,6 +271,7 @@ __device__ int batch_insert(const Fp& f, const SmemInv& inv, uint32_t* V, int ld
 // out[0] = k, out[1..k] = independent rows (ascending).
 __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int64_t lds, int b,
                                                     int s, int32_t* out) {
+    FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* Ss = sm;                          // b x s
     uint32_t* E = Ss + (size_t)RD_MAX_B * s;    // basis rows (fully reduced)
@@ -364,6 +367,7 @@ __device__ int crp_scan(const Fp& f, const SmemInv& inv, const uint32_t* __restr
 
 __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* __restrict__ RI, int64_t ldr,
                                                   int k, int64_t n, int32_t* out, int32_t* ocount) {
+    FFB_PDL_ENTRY();
     extern __shared__ uint32_t sm[];
     uint32_t* E = sm;                           // basis: up to k vectors of length k
     uint32_t* V = E + (size_t)CRP_KMAX * k;     // CRP_G columns, each length k: V[c*k + i]
@@ -395,6 +399,7 @@ __global__ void __launch_bounds__(256) k_crp_rowelim(Fp f, const uint32_t* RI, i
                                                      const int32_t* lists, const int32_t* counts,
                                                      int nblk, uint32_t* gscratch, int32_t* Jout,
                                                      int32_t* sigma_out, int32_t* fail) {
+    FFB_PDL_ENTRY();
     extern __shared__ uint32_t sm[];
     __shared__ int32_t off[1025];
     __shared__ int32_t pcol[CRP_KMAX];
@@ -515,6 +520,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     const int32_t* __restrict__ counts, int nblk, int32_t* cand, int rc_cap, const int32_t* I, int64_t c0,
     const uint32_t* S, int64_t lds, int s, uint32_t* Kinv, int32_t* Jout, uint32_t* UO, int64_t lduo,
     int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r, int32_t* fail) {
+    FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t off[1025];
     __shared__ int32_t Js[CRP_KMAX], rho[CRP_KMAX], pci[CRP_KMAX], pcv[CRP_KMAX], sig[CRP_KMAX], Is[CRP_KMAX];
@@ -684,6 +690,7 @@ __global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t
                                                uint32_t* Kinv, uint32_t* UO, int64_t lduo,
                                                int32_t* uhat_col, int32_t* prow, int32_t* pcol,
                                                int64_t r, int32_t* fail, const int32_t* sigma_in) {
+    FFB_PDL_ENTRY();
     extern __shared__ uint32_t sm[];
     uint32_t* A = sm;                       // k x k working copy (row-order elimination)
     uint32_t* G = A + (size_t)k * k;        // k x 2k Gauss-Jordan
@@ -795,6 +802,7 @@ __global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t
 // H[i][t] = L[i][t] * d[t]
 __global__ void k_scale_cols(Fp f, uint32_t* H, int64_t ldh, const uint32_t* L, int64_t ldl,
                              const uint32_t* d, int64_t cols) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cols;
          t += (int64_t)gridDim.x * blockDim.x)
@@ -804,6 +812,7 @@ __global__ void k_scale_cols(Fp f, uint32_t* H, int64_t ldh, const uint32_t* L, 
 // Certificate part: pivotless row t (= np[a]) may only depend on pivots found before it.
 __global__ void k_m1_pattern(const uint32_t* M1, int64_t ldm, const int32_t* np,
                              const int32_t* prow, int64_t r, int32_t* flag) {
+    FFB_PDL_ENTRY();
     const int64_t a = blockIdx.y;
     const int32_t t = np[a];
     int bad = 0;
@@ -819,6 +828,7 @@ __global__ void k_m1_pattern(const uint32_t* M1, int64_t ldm, const int32_t* np,
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(256) k_ldu_base(Fp f, uint32_t* K, int64_t ldk, int n,
                                                   int32_t* fail) {
+    FFB_PDL_ENTRY();
     // Register ownership as in the leaf: thread (ty, tx) holds K[ty + 4q][tx].
     // Step t broadcasts column t and row t (double-buffered) with one barrier.
     __shared__ uint32_t colb[2][64], rowb[2][64];
@@ -868,6 +878,7 @@ __global__ void __launch_bounds__(256) k_ldu_base(Fp f, uint32_t* K, int64_t ldk
 // L (unit lower with zeros above) from the packed LDU block; d from the diagonal.
 __global__ void k_unpack_l(uint32_t* L, int64_t ldl, const uint32_t* K, int64_t ldk, int64_t n,
                            uint32_t* d, uint32_t one) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
          j += (int64_t)gridDim.x * blockDim.x) {
@@ -889,7 +900,7 @@ void gather2d(cudaStream_t st, DMat dst, DMat src, const int32_t* ridx, const in
     ProfScope ps(K_MOVE, st, 0.0, 8.0 * dst.rows * dst.cols);
     for (int64_t r0 = 0; r0 < dst.rows; r0 += 65535) {
         const int64_t nr = std::min<int64_t>(65535, dst.rows - r0);
-        k_gather2d<<<rgrid(nr, dst.cols), 256, 0, st>>>(dst.ptr + r0 * dst.ld, dst.ld, src.ptr, src.ld,
+        launch_k(k_gather2d, rgrid(nr, dst.cols), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, src.ptr, src.ld,
                                                         ridx ? ridx + r0 : nullptr,
                                                         ridx ? roff : roff + r0, cidx, dst.cols);
         count_launch();
@@ -915,7 +926,7 @@ void ldu_inplace(const Fp& f, cudaStream_t st, DMat K, Workspace& ws, int32_t* f
     if (n <= 0) return;
     if (n <= 64) {
         ProfScope ps(K_LDU, st, 2.0 * n * n * n / 3.0, 8.0 * n * n);
-        k_ldu_base<<<1, 256, 0, st>>>(f, K.ptr, K.ld, (int)n, fail);
+        launch_k(k_ldu_base, 1, 256, 0, st, f, K.ptr, K.ld, (int)n, fail);
         count_launch();
         FFB_CHECK_LAUNCH();
         return;
@@ -930,7 +941,7 @@ void ldu_inplace(const Fp& f, cudaStream_t st, DMat K, Workspace& ws, int32_t* f
     uint32_t* dinv = ws.vec<uint32_t>(n1);
     uint32_t* d = ws.vec<uint32_t>(n1);
     DMat L11 = ws.mat(n1, n1);
-    k_unpack_l<<<rgrid(n1, n1), 256, 0, st>>>(L11.ptr, L11.ld, K11.ptr, K11.ld, n1, d, 1 % f.p);
+    launch_k(k_unpack_l, rgrid(n1, n1), 256, 0, st, L11.ptr, L11.ld, K11.ptr, K11.ld, n1, d, 1 % f.p);
     count_launch();
     invert_vec(f, st, dinv, d, n1);
     // U12 = D1^-1 L11^-1 K12 (in place)
@@ -1015,8 +1026,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         Kik.ld = k;
         if (!paired) {
             ProfScope ps(K_PQ_PAIR, st, 0.0, 0.0);
-            k_pair2<<<1, 256, (size_t)3 * k * k * 4, st>>>(
-                f, RIk.ptr, RIk.ld, k, dJ, dI, c0, sketching ? Sk.ptr : nullptr, Sk.ld, SK, Kik.ptr,
+            launch_k(k_pair2, 1, 256, (size_t)3 * k * k * 4, st, f, RIk.ptr, RIk.ld, k, dJ, dI, c0, sketching ? Sk.ptr : nullptr, Sk.ld, SK, Kik.ptr,
                 UO.ptr, UO.ld, d_uhat_col, d_prow, d_pcol, r, dflag, sigma_in);
             ++g_launches;
             FFB_CHECK_LAUNCH();
@@ -1059,7 +1069,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         DMat YO;
         if (!exact) {  // Y * Omega, once
             DMat Om = ws.mat(n, SK);
-            k_random<<<(unsigned)cdiv(n * SK, 256), 256, 0, st>>>(Om.ptr, n * SK, 0x5EEDull + n + 977 * attempt, f.p);
+            launch_k(k_random, (unsigned)cdiv(n * SK, 256), 256, 0, st, Om.ptr, n * SK, 0x5EEDull + n + 977 * attempt, f.p);
             ++g_launches;
             YO = ws.mat(m, SK);
             gemm(f, st, GEMM_SET, YO, Y, false, Om, false, m, SK, n);
@@ -1081,7 +1091,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 }
                 {
                     ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-                    k_row_detect<<<1, 256, rd_smem, st>>>(f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo);
+                    launch_k(k_row_detect, 1, 256, rd_smem, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo);
                     ++g_launches;
                     FFB_CHECK_LAUNCH();
                 }
@@ -1100,7 +1110,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 {
                     ProfScope ps(K_PQ_CRP, st, 0.0, 0.0);
                     // level 0: local CRPs of 256-column blocks (parallel)
-                    k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, RI.ptr, RI.ld, k, n, lists[0], counts[0]);
+                    launch_k(k_crp_list, nblk0, 256, crp_smem, st, f, RI.ptr, RI.ld, k, n, lists[0], counts[0]);
                     ++g_launches;
                 }
                 {
@@ -1109,7 +1119,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     int rc_cap;
                     const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap);
                     DMat Kik = Kinv.sub(0, 0, k, k);
-                    k_crp_finish<<<1, 256, cfmem, st>>>(f, RI.ptr, RI.ld, k, lists[0], counts[0], nblk0,
+                    launch_k(k_crp_finish, 1, 256, cfmem, st, f, RI.ptr, RI.ld, k, lists[0], counts[0], nblk0,
                                                         (int32_t*)re_scratch, rc_cap, dI, c0, Sc.ptr, Sc.ld, SK,
                                                         Kik.ptr, lists[1], UO.ptr, UO.ld, d_uhat_col,
                                                         d_prow, d_pcol, r, dflag);
@@ -1195,7 +1205,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         const int32_t* dpc = io.upload(pcol_rows);
         gather2d(st, Kf, Y, dpr, dpc, 0);
         ldu_inplace(f, st, Kf, ws, dflag);
-        k_unpack_l<<<rgrid(r, r), 256, 0, st>>>(io.Lo.ptr, io.Lo.ld, Kf.ptr, Kf.ld, r, io.d, 1 % f.p);
+        launch_k(k_unpack_l, rgrid(r, r), 256, 0, st, io.Lo.ptr, io.Lo.ld, Kf.ptr, Kf.ld, r, io.d, 1 % f.p);
         ++g_launches;
         invert_vec(f, st, io.dinv, io.d, r);
         DMat Uo = io.Uo.sub(0, 0, r, n);
@@ -1222,12 +1232,12 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         {
             DMat W = ws.mat(m, n), H = ws.mat(m, r);
             gather2d(st, W, Y, io.upload(out.rimg), dcimg, 0);
-            k_scale_cols<<<rgrid(m, r), 256, 0, st>>>(f, H.ptr, H.ld, io.Lo.ptr, io.Lo.ld, io.d, r);
+            launch_k(k_scale_cols, rgrid(m, r), 256, 0, st, f, H.ptr, H.ld, io.Lo.ptr, io.Lo.ld, io.d, r);
             ++g_launches;
             gemm(f, st, GEMM_SUB, W, H, false, Uo, false, m, n, r);
             any_nonzero(st, W, dflag);
             if (m > r) {
-                k_m1_pattern<<<rgrid(m - r, r), 256, 0, st>>>(io.Lo.ptr + r * io.Lo.ld, io.Lo.ld, dnp,
+                launch_k(k_m1_pattern, rgrid(m - r, r), 256, 0, st, io.Lo.ptr + r * io.Lo.ld, io.Lo.ld, dnp,
                                                               d_prow, r, dflag);
                 ++g_launches;
             }
@@ -1256,9 +1266,9 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         int32_t* info;
         FFB_CUDA(cudaMalloc(&info, (2 * RD_MAX_B + 16) * 4));
-        k_row_detect<<<1, 256, rd_smem, st>>>(f, d_in, cols, rows, cols, info);
+        launch_k(k_row_detect, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info);
         FFB_CUDA(cudaEventRecord(e[0], st));
-        for (int i = 0; i < reps; ++i) k_row_detect<<<1, 256, rd_smem, st>>>(f, d_in, cols, rows, cols, info);
+        for (int i = 0; i < reps; ++i) launch_k(k_row_detect, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info);
         FFB_CUDA(cudaEventRecord(e[1], st));
         FFB_CUDA(cudaEventSynchronize(e[1]));
         FFB_CUDA(cudaEventElapsedTime(&t, e[0], e[1]));
@@ -1295,12 +1305,12 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
         double acc[3] = {0, 0, 0};
         for (int i = 0; i <= reps; ++i) {
             FFB_CUDA(cudaEventRecord(e[0], st));
-            k_crp_list<<<nblk0, 256, crp_smem, st>>>(f, d_in, n, k, n, lists0, counts0);
+            launch_k(k_crp_list, nblk0, 256, crp_smem, st, f, d_in, n, k, n, lists0, counts0);
             FFB_CUDA(cudaEventRecord(e[1], st));
             {
                 int rc_cap;
                 const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap);
-                k_crp_finish<<<1, 256, cfmem, st>>>(f, d_in, n, k, lists0, counts0, nblk0, (int32_t*)re_scratch,
+                launch_k(k_crp_finish, 1, 256, cfmem, st, f, d_in, n, k, lists0, counts0, nblk0, (int32_t*)re_scratch,
                                                     rc_cap, dI, 0, nullptr, 0, 0, Kinv, lists1, nullptr, 0, ucol,
                                                     prow, pcol, 0, flag);
             }

@@ -127,6 +127,7 @@ template <int BN, int ST>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_i8_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                  uint32_t* __restrict__ C, int64_t ldc, int M, int N, int nk, Fp f, int mode) {
+    FFB_PDL_ENTRY();
     using Cfg = TcCfg<BN, ST>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -273,6 +274,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_limb_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    uint32_t* __restrict__ C, int64_t ldc, int M, int N, int nk, int Mrows, int Nrows,
                    Fp f, int mode) {
+    FFB_PDL_ENTRY();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* sA = smem;
@@ -432,6 +434,7 @@ __device__ __forceinline__ void limbs(uint32_t x, uint32_t p, int8_t& a0, int8_t
 
 __global__ void k_pack_limb_n(int8_t* dst, int64_t ldd, int64_t plane, const uint32_t* src,
                               int64_t lds, int64_t rows, int64_t K, uint32_t p) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < ldd;
          k += (int64_t)gridDim.x * blockDim.x) {
@@ -445,6 +448,7 @@ __global__ void k_pack_limb_n(int8_t* dst, int64_t ldd, int64_t plane, const uin
 
 __global__ void k_pack_limb_t(int8_t* dst, int64_t ldd, int64_t plane, const uint32_t* src,
                               int64_t lds, int64_t rows, int64_t K, uint32_t p) {
+    FFB_PDL_ENTRY();
     __shared__ uint32_t tile[32][33];
     const int64_t i0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
     for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
@@ -481,6 +485,7 @@ struct PackJob {
     int trans;
 };
 __global__ void k_pack2(PackJob j0, PackJob j1, uint32_t p) {
+    FFB_PDL_ENTRY();
     const PackJob& j = blockIdx.z == 0 ? j0 : j1;
     __shared__ int8_t tile[32][33];
     const int64_t i0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
@@ -507,6 +512,7 @@ __global__ void k_pack2(PackJob j0, PackJob j1, uint32_t p) {
 // not transposed: op(src)[i][k] = src[i][k]
 __global__ void k_pack_n(int8_t* dst, int64_t ldd, const uint32_t* src, int64_t lds, int64_t rows,
                          int64_t K, uint32_t p) {
+    FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < ldd;
          k += (int64_t)gridDim.x * blockDim.x)
@@ -516,6 +522,7 @@ __global__ void k_pack_n(int8_t* dst, int64_t ldd, const uint32_t* src, int64_t 
 // transposed: op(src)[i][k] = src[k][i]  (src is K x rows)
 __global__ void k_pack_t(int8_t* dst, int64_t ldd, const uint32_t* src, int64_t lds, int64_t rows,
                          int64_t K, uint32_t p) {
+    FFB_PDL_ENTRY();
     __shared__ int8_t tile[32][33];
     const int64_t i0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
     for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
@@ -586,12 +593,11 @@ void pack(cudaStream_t st, int8_t* dst, int64_t ldd, DMat src, bool trans, int64
         for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
             const int64_t nr = std::min<int64_t>(65535, rows - r0);
             int64_t gx = std::min<int64_t>(64, cdiv(ldd, 256));
-            k_pack_n<<<dim3((unsigned)gx, (unsigned)nr), 256, 0, st>>>(
-                dst + r0 * ldd, ldd, src.ptr + r0 * src.ld, src.ld, nr, K, p);
+            launch_k(k_pack_n, dim3((unsigned)gx, (unsigned)nr), 256, 0, st, dst + r0 * ldd, ldd, src.ptr + r0 * src.ld, src.ld, nr, K, p);
         }
     } else {
         dim3 grid((unsigned)cdiv(ldd, 32), (unsigned)cdiv(rows, 32));
-        k_pack_t<<<grid, dim3(32, 8), 0, st>>>(dst, ldd, src.ptr, src.ld, rows, K, p);
+        launch_k(k_pack_t, grid, dim3(32, 8), 0, st, dst, ldd, src.ptr, src.ld, rows, K, p);
     }
     ++g_launches;
     FFB_CHECK_LAUNCH();
@@ -608,7 +614,7 @@ void launch_tc(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, DM
         attr = true;
     }
     dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, TC_BM));
-    k_gemm_i8_tc<BN, ST><<<grid, TC_THREADS, Cfg::SMEM, st>>>(ma, mb, C.ptr, C.ld, (int)M, (int)N,
+    launch_k(k_gemm_i8_tc<BN, ST>, grid, TC_THREADS, Cfg::SMEM, st, ma, mb, C.ptr, C.ld, (int)M, (int)N,
                                                           (int)nk, f, mode);
     ++g_launches;
     FFB_CHECK_LAUNCH();
@@ -642,12 +648,10 @@ void tc_gemm_limb(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, b
             if (!trans) {
                 for (int64_t r0 = 0; r0 < rows; r0 += 65535) {
                     const int64_t nr = std::min<int64_t>(65535, rows - r0);
-                    k_pack_limb_n<<<dim3((unsigned)std::min<int64_t>(64, cdiv(Kp, 256)), (unsigned)nr), 256, 0, st>>>(
-                        dst + r0 * Kp, Kp, (int64_t)plane, src.ptr + r0 * src.ld, src.ld, nr, K, f.p);
+                    launch_k(k_pack_limb_n, dim3((unsigned)std::min<int64_t>(64, cdiv(Kp, 256)), (unsigned)nr), 256, 0, st, dst + r0 * Kp, Kp, (int64_t)plane, src.ptr + r0 * src.ld, src.ld, nr, K, f.p);
                 }
             } else {
-                k_pack_limb_t<<<dim3((unsigned)cdiv(Kp, 32), (unsigned)cdiv(rows, 32)), dim3(32, 8), 0, st>>>(
-                    dst, Kp, (int64_t)plane, src.ptr, src.ld, rows, K, f.p);
+                launch_k(k_pack_limb_t, dim3((unsigned)cdiv(Kp, 32), (unsigned)cdiv(rows, 32)), dim3(32, 8), 0, st, dst, Kp, (int64_t)plane, src.ptr, src.ld, rows, K, f.p);
             }
             ++g_launches;
             FFB_CHECK_LAUNCH();
@@ -663,7 +667,7 @@ void tc_gemm_limb(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, b
     ProfScope ps(K_GEMM, st, 2.0 * M * N * K, 3.0 * (M * K + N * K) + 8.0 * M * N, M, N, -K);
     CUtensorMap ma = make_map(Ap, 3 * Mr, Kp, TC_BM), mb = make_map(Bp, 3 * Nr, Kp, LB_BN);
     dim3 grid((unsigned)cdiv(N, LB_BN), (unsigned)cdiv(M, TC_BM));
-    k_gemm_limb_tc<<<grid, TC_THREADS, LB_SMEM, st>>>(ma, mb, C.ptr, C.ld, (int)M, (int)N,
+    launch_k(k_gemm_limb_tc, grid, TC_THREADS, LB_SMEM, st, ma, mb, C.ptr, C.ld, (int)M, (int)N,
                                                      (int)cdiv(Kp, TC_BK), (int)Mr, (int)Nr, f, mode);
     ++g_launches;
     FFB_CHECK_LAUNCH();
@@ -689,7 +693,7 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
         const int64_t rmax = std::max(M, N);
         if (rmax <= (int64_t)65535 * 32) {
             dim3 grid((unsigned)cdiv(Kp, 32), (unsigned)cdiv(rmax, 32), 2);
-            k_pack2<<<grid, dim3(32, 8), 0, st>>>(ja, jb, f.p);
+            launch_k(k_pack2, grid, dim3(32, 8), 0, st, ja, jb, f.p);
             ++g_launches;
             FFB_CHECK_LAUNCH();
         } else {
