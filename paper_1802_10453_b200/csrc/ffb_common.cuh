@@ -9,6 +9,7 @@
 
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <stdexcept>
@@ -43,6 +44,13 @@ struct Status : std::runtime_error {
 // kernel never touches memory before its predecessor is done, while the
 // launch latency and CTA ramp-up overlap the predecessor's tail.  Without a
 // programmatic launch both instructions are no-ops.
+//
+// Consequence for loads: a kernel's lifetime now overlaps its predecessor's
+// writes, which breaks the contract of the non-coherent read-only path
+// (ld.global.nc: data read-only for the kernel's lifetime).  Kernels therefore
+// use coherent loads only -- __ldcg (L2) instead of __ldg, and no __restrict__
+// on pointers (nvcc turns const __restrict__ loads into ld.global.nc).  The
+// SASS check is `cuobjdump -sass | grep LDG.*CONSTANT` (must be empty).
 // ---------------------------------------------------------------------------
 #define FFB_PDL_ENTRY()                                                    \
     do {                                                                   \
@@ -53,11 +61,69 @@ struct Status : std::runtime_error {
 // kernel<<<grid, block, smem, st>>>(args...) with the programmatic-serialization
 // attribute (FFB_NO_PDL=1 disables it); arguments are coerced to the kernel's
 // parameter types like a <<<>>> launch.
+//
+// A programmatic launch may only follow a kernel: after a copy, memset or event
+// wait on a stream, pdl_fence(stream) makes the next kernel there launch with
+// full stream serialization (griddepcontrol.wait orders kernels, not copies).
+struct PdlFences {
+    cudaStream_t s[8];
+    int n = 0;
+};
+inline PdlFences& pdl_fences() {
+    static thread_local PdlFences f;
+    return f;
+}
+inline void pdl_fence(cudaStream_t st) {
+    PdlFences& f = pdl_fences();
+    for (int i = 0; i < f.n; ++i)
+        if (f.s[i] == st) return;
+    if (f.n < 8) f.s[f.n++] = st;
+}
+inline bool pdl_take(cudaStream_t st) {
+    PdlFences& f = pdl_fences();
+    for (int i = 0; i < f.n; ++i)
+        if (f.s[i] == st) {
+            f.s[i] = f.s[--f.n];
+            return true;
+        }
+    return false;
+}
+
+inline long long& pdl_launch_index() {
+    static thread_local long long i = 0;
+    return i;
+}
+inline bool& pdl_enabled() {
+    static thread_local bool on = true;
+    return on;
+}
+struct PdlScope {  // disables programmatic launches within a scope
+    bool saved;
+    explicit PdlScope(bool on) : saved(pdl_enabled()) { pdl_enabled() = on && saved; }
+    ~PdlScope() { pdl_enabled() = saved; }
+};
+
 template <typename... KArgs, typename... Args>
 inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                      Args&&... args) {
     static_assert(sizeof...(KArgs) == sizeof...(Args), "kernel argument count");
-    static const bool pdl = getenv("FFB_NO_PDL") == nullptr;
+    static const bool pdl_on = getenv("FFB_NO_PDL") == nullptr;
+    // bisection hook: FFB_PDL_RANGE=a:b (global launch indices)
+    static long long ra = -1, rb = -1;
+    static bool rinit = false;
+    if (!rinit) {
+        if (const char* r = getenv("FFB_PDL_RANGE")) sscanf(r, "%lld:%lld", &ra, &rb);
+        rinit = true;
+    }
+    const long long me = pdl_launch_index()++;
+    static const bool log = getenv("FFB_LAUNCH_LOG") != nullptr;
+    if (log) {
+        const char* nm = nullptr;
+        cudaFuncGetName(&nm, (const void*)kern);
+        fprintf(stderr, "[launch %lld] %s grid %u,%u,%u\n", me, nm ? nm : "?", grid.x, grid.y, grid.z);
+    }
+    const bool in_range = ra < 0 || (me >= ra && me < rb);
+    const bool pdl = pdl_on && !pdl_take(st) && pdl_enabled() && in_range;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
@@ -68,7 +134,9 @@ inline void launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
     at[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = pdl ? 1 : 0;
-    cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+    if (e != cudaSuccess)
+        throw Status(FFB_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(e));
 }
 
 // ---------------------------------------------------------------------------
@@ -177,7 +245,7 @@ struct SmemInv {
 };
 __device__ inline SmemInv stage_inverses(const Fp& f, uint32_t* buf /* SINV_MAX words */) {
     if (!f.inv || f.p > SINV_MAX) return SmemInv{nullptr};
-    for (uint32_t a = threadIdx.x; a < f.p; a += blockDim.x) buf[a] = __ldg(f.inv + a);
+    for (uint32_t a = threadIdx.x; a < f.p; a += blockDim.x) buf[a] = __ldcg(f.inv + a);
     __syncthreads();
     return SmemInv{buf};
 }
@@ -185,7 +253,7 @@ __device__ inline SmemInv stage_inverses(const Fp& f, uint32_t* buf /* SINV_MAX 
 // Batched read-only copy global -> shared of a rows x cols tile (row stride lds),
 // with U independent loads in flight per thread.
 template <int U>
-__device__ __forceinline__ void load_tile(uint32_t* dst, int ldd, const uint32_t* __restrict__ src,
+__device__ __forceinline__ void load_tile(uint32_t* dst, int ldd, const uint32_t* src,
                                           int64_t lds, int rows, int cols) {
     // warp w copies rows w, w + nwarps, ...; lanes stride the columns; U rows
     // of loads are in flight before the stores (no integer division).
@@ -196,7 +264,7 @@ __device__ __forceinline__ void load_tile(uint32_t* dst, int ldd, const uint32_t
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int r = r0 + u * nw;
-                v[u] = r < rows ? __ldg(src + (int64_t)r * lds + c0) : 0u;
+                v[u] = r < rows ? __ldcg(src + (int64_t)r * lds + c0) : 0u;
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {

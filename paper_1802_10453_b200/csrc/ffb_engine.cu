@@ -23,6 +23,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <array>
 #include <vector>
 
 #include "ffb_kernels.cuh"
@@ -45,9 +46,12 @@ struct ffb_context {
     uint32_t* inv_table = nullptr;
     uint32_t inv_p = 0;
     int32_t* flag = nullptr;  // device scratch flag
+    int32_t* zero_flag = nullptr;  // is_zero tag (never reset; see is_zero)
+    uint32_t zero_gen = 0;
     uint64_t launches = 0;
     uint64_t syncs = 0, syncs_last = 0;
     double sync_wait_ms = 0;  // host time blocked in read-backs (FFB_HOST_STATS)
+    uint64_t uploads = 0;     // host -> device index uploads (FFB_HOST_STATS)
     Profiler prof;
 };
 
@@ -159,12 +163,30 @@ const int32_t* upload(ffb_context* c, const int32_t* v, size_t n) {
         off = 0;
     }
     memcpy(c->up_host + off, v, bytes);
-    FFB_CUDA(cudaMemcpyAsync(d, c->up_host + off, bytes, cudaMemcpyHostToDevice, c->stream));
+    FFB_CUDA(cudaMemcpyAsync(d, c->up_host + off, bytes, cudaMemcpyHostToDevice, c->stream)); pdl_fence(c->stream);
+    ++c->uploads;
     c->up_top = off + bytes;
     return d;
 }
 const int32_t* upload(ffb_context* c, const std::vector<int32_t>& v) {
     return upload(c, v.data(), v.size());
+}
+// Several index arrays in one workspace block and one copy (each copy is a
+// stream operation that also breaks the programmatic-launch chain).
+template <size_t N>
+std::array<const int32_t*, N> upload_batch(ffb_context* c, const std::array<const std::vector<int32_t>*, N>& vs) {
+    std::array<size_t, N> off{};
+    size_t total = 0;
+    for (size_t i = 0; i < N; ++i) {
+        off[i] = total;
+        total += (vs[i]->size() + 3) & ~(size_t)3;  // 16-byte aligned sub-arrays
+    }
+    std::vector<int32_t> host(std::max<size_t>(total, 1), 0);
+    for (size_t i = 0; i < N; ++i) std::copy(vs[i]->begin(), vs[i]->end(), host.begin() + off[i]);
+    const int32_t* d = upload(c, host.data(), total);
+    std::array<const int32_t*, N> out{};
+    for (size_t i = 0; i < N; ++i) out[i] = d + off[i];
+    return out;
 }
 
 // Device -> host read-back of a small array (a synchronization point).
@@ -174,7 +196,7 @@ const void* readback(ffb_context* c, const void* dev, size_t bytes) {
         c->down_cap = std::max(bytes, (size_t)1 << 20);
         FFB_CUDA(cudaMallocHost(&c->down_host, c->down_cap));
     }
-    FFB_CUDA(cudaMemcpyAsync(c->down_host, dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+    FFB_CUDA(cudaMemcpyAsync(c->down_host, dev, bytes, cudaMemcpyDeviceToHost, c->stream)); pdl_fence(c->stream);
     const auto t0 = std::chrono::steady_clock::now();
     FFB_CUDA(cudaStreamSynchronize(c->stream));
     c->sync_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -237,21 +259,23 @@ struct Engine {
     }
 
     // dispatch, sytrf.cpp:337-350
-    HFact dispatch(DMat A, const std::vector<int32_t>& rows, int64_t coff) {
+    // rows: original row ids of the node (host); drows: the same on the device
+    // (a prefix/suffix of an array the parent uploaded) or nullptr
+    HFact dispatch(DMat A, const std::vector<int32_t>& rows, const int32_t* drows, int64_t coff) {
         const int64_t saved = g_node;
         g_node = A.rows;  // trace tag: the innermost node a launch belongs to
-        HFact h = is_leaf(A.rows) ? crout(A, rows, coff) : recursive_step(A, rows, coff);
+        HFact h = is_leaf(A.rows) ? crout(A, rows, drows, coff) : recursive_step(A, rows, drows, coff);
         g_node = saved;
         return h;
     }
 
     // crout_base, sytrf.cpp:35-139 (device kernel, one CTA)
-    HFact crout(DMat A, const std::vector<int32_t>& rows, int64_t coff) {
+    HFact crout(DMat A, const std::vector<int32_t>& rows, const int32_t* drows_in, int64_t coff) {
         const int64_t s = A.rows;
         HFact h;
         if (s == 0) return h;
         const WsMark mk{c->ws_top};
-        const int32_t* drows = upload(c, rows);
+        const int32_t* drows = drows_in ? drows_in : upload(c, rows);
         int32_t* out = ws_vec<int32_t>(c, s + 1);
         uint32_t* scratch = nullptr;
         if (s > 200) scratch = ws_vec<uint32_t>(c, (int64_t)leaf_scratch_words(s));
@@ -264,34 +288,36 @@ struct Engine {
     }
 
     // Alg. 2, sytrf.cpp:298-335
-    HFact recursive_step(DMat A, const std::vector<int32_t>& rows, int64_t coff) {
+    HFact recursive_step(DMat A, const std::vector<int32_t>& rows, const int32_t* drows, int64_t coff) {
         const int64_t s = A.rows, m = s / 2, ns = s - m;
         const WsMark mk{c->ws_top};
         std::vector<int32_t> rows1(rows.begin(), rows.begin() + m);
-        HFact f1 = dispatch(A.sub(0, 0, m, m), rows1, coff);  // :303
+        HFact f1 = dispatch(A.sub(0, 0, m, m), rows1, drows, coff);  // :303
         const int64_t r1 = f1.rank;
 
         // B' = P1^T B (:308) and [L1; M1] in f1's position order (from Lg), one launch
         DMat BP = ws_mat(c, m, ns);
         std::vector<int32_t> prow(m);
         for (int64_t i = 0; i < m; ++i) prow[i] = rows[f1.perm[i]];
+        std::vector<int32_t> rows2(rows.begin() + m, rows.end());
+        std::vector<int32_t> rowsz;  // rows of [[0 Y],[Y^t Z]]
+        rowsz.reserve(s - r1);
+        for (int64_t i = r1; i < m; ++i) rowsz.push_back(prow[i]);
+        for (int64_t i = m; i < s; ++i) rowsz.push_back(rows[i]);
+        // every index array of this node in one copy
+        const auto up = upload_batch<4>(c, {&f1.perm, &prow, &rows2, &rowsz});
         DMat LM = ws_mat(c, m, r1);
-        gather_rows2(st, BP, A, upload(c, f1.perm), m, LM, Lg, upload(c, prow), coff);
+        gather_rows2(st, BP, A, up[0], m, LM, Lg, up[1], coff);
         DMat X = BP.sub(0, 0, r1, ns);
         trsm_lower_unit(f, st, LM.sub(0, 0, r1, r1), X);  // :310
         DMat Y = BP.sub(r1, 0, m - r1, ns);
         gemm(f, st, GEMM_SUB, Y, LM.sub(r1, 0, m - r1, r1), false, X, false, m - r1, ns, r1);  // :312
         DMat G = ws_mat(c, ns, r1);
-        std::vector<int32_t> rows2(rows.begin() + m, rows.end());
-        inverse_apply_T(f, st, G, X, D, coff, Lg, upload(c, rows2));  // :313 + rows m..s of N1
+        inverse_apply_T(f, st, G, X, D, coff, Lg, up[2]);  // :313 + rows m..s of N1
         DMat Z = A.sub(m, m, ns, ns);
         gemm(f, st, GEMM_SUB, Z, G, false, X, false, ns, ns, r1);  // Z = C - G D1 G^T (:315)
 
-        std::vector<int32_t> rowsz;  // rows of [[0 Y],[Y^t Z]]
-        rowsz.reserve(s - r1);
-        for (int64_t i = r1; i < m; ++i) rowsz.push_back(rows[f1.perm[i]]);
-        for (int64_t i = m; i < s; ++i) rowsz.push_back(rows[i]);
-        HFact f2 = zero_leading(Y, Z, rowsz, coff + r1);  // :317
+        HFact f2 = zero_leading(Y, Z, rowsz, up[3], coff + r1);  // :317
 
         HFact h;  // P = compose(embed(P1,0,n), embed(P2,r1,n)) (:332-334)
         h.rank = r1 + f2.rank;
@@ -306,16 +332,17 @@ struct Engine {
     }
 
     bool is_zero(DMat Y) {
-        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), st));
-        any_nonzero(st, Y, c->flag);
-        const int32_t v = *(const int32_t*)readback(c, c->flag, sizeof(int32_t));
-        return v == 0;
+        // generation tag instead of a memset: the flag holds an older tag unless Y != 0
+        const int32_t tag = (int32_t)(++c->zero_gen);
+        any_nonzero(st, Y, c->zero_flag, tag);
+        const int32_t v = *(const int32_t*)readback(c, c->zero_flag, sizeof(int32_t));
+        return v != tag;
     }
 
     // sytrf.cpp:267-292
-    HFact zero_leading(DMat Y, DMat Z, const std::vector<int32_t>& rows, int64_t coff) {
+    HFact zero_leading(DMat Y, DMat Z, const std::vector<int32_t>& rows, const int32_t* drows, int64_t coff) {
         const int64_t m = Y.rows, nz = Z.rows;
-        if (m == 0) return dispatch(Z, rows, coff);
+        if (m == 0) return dispatch(Z, rows, drows, coff);
         HFact h;
         if (nz == 0) {
             h.perm.resize(m);
@@ -324,7 +351,7 @@ struct Engine {
         }
         if (is_zero(Y)) {  // :274-290
             std::vector<int32_t> rz(rows.begin() + m, rows.end());
-            HFact f3 = dispatch(Z, rz, coff);
+            HFact f3 = dispatch(Z, rz, drows ? drows + m : nullptr, coff);
             const int64_t r3 = f3.rank;
             h.rank = r3;
             h.perm.resize(m + nz);
@@ -333,7 +360,7 @@ struct Engine {
             for (int64_t k = r3; k < nz; ++k) h.perm[m + k] = (int32_t)(m + f3.perm[k]);
             return h;
         }
-        return zero_leading_pairs(Y, Z, rows, coff);
+        return zero_leading_pairs(Y, Z, rows, coff);  // (device rows rebuilt from the PLDUQ perms)
     }
 
     // PLDUQ of Y (destroyed); returns rank, fills row/col images and device factors.
@@ -346,6 +373,8 @@ struct Engine {
     double pq_t0 = 0;
     Pl run_plduq(DMat Y) {
         const int64_t m = Y.rows, n = Y.cols, mn = std::min(m, n);
+        static const bool pq_pdl = getenv("FFB_PDL_NO_PLDUQ") == nullptr;  // bisection hook
+        PdlScope pdl_scope(pq_pdl);
         Pl pl;
         if (getenv("FFB_PLDUQ_TRACE")) {
             FFB_CUDA(cudaStreamSynchronize(st));
@@ -425,8 +454,14 @@ struct Engine {
         const int64_t r = py.r;
         const std::vector<int32_t>& q = py.cimg;
 
+        // L columns [coff, coff + 2r) (:222-252) are keyed by original row:
+        //   Y rows (row_perm order), Z rows (col_perm order); all index arrays in one copy
+        std::vector<int32_t> idy(m), idz(nz);
+        for (int64_t a = 0; a < m; ++a) idy[a] = rows[py.rimg[a]];
+        for (int64_t a = 0; a < nz; ++a) idz[a] = rows[m + q[a]];
+        const auto up = upload_batch<3>(c, {&q, &idy, &idz});
         DMat Cp = ws_mat(c, nz, nz);  // C' = Q^T Z Q (:183)
-        gather_sym(st, Cp, Z, upload(c, q));
+        gather_sym(st, Cp, Z, up[0]);
         DMat C1 = Cp.sub(0, 0, r, r), C2 = Cp.sub(0, r, r, nz - r), C3 = Cp.sub(r, r, nz - r, nz - r);
         DMat U1 = py.U.sub(0, 0, r, r), V1 = py.U.sub(0, r, r, nz - r);
         DMat UpT = ws_mat(c, nz, r);  // [U1^T; V1^T]
@@ -442,7 +477,7 @@ struct Engine {
             gemm(f, st, GEMM_SUB, C1, H, true, U1, false, r, r, r);  // C1 -= U1^T diag(delta) U1
         }
         DMat X = ws_mat(c, r, r);
-        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), st));
+        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), st)); pdl_fence(st);
         trssyr2k_dev(U1, U1T, C1, X, c->flag);  // :202
         DMat G12 = ws_mat(c, nz, r);  // [G1; G2]
         scale_T(f, st, G12.sub(0, 0, r, r), X, py.dinv);  // G1 = (diag(d)^-1 X)^T (:203)
@@ -458,20 +493,16 @@ struct Engine {
         }
         scale_T(f, st, G12.sub(r, 0, nz - r, r), C2, py.dinv);  // G2 (:215)
 
-        // L columns [coff, coff + 2r) (:222-252), keyed by original row:
         //   Y rows (row_perm order):  even columns <- [L1; M1]
         //   Z rows (col_perm order):  even <- [G1; G2], odd <- [U1^T; V1^T]
-        std::vector<int32_t> idy(m), idz(nz);
-        for (int64_t a = 0; a < m; ++a) idy[a] = rows[py.rimg[a]];
-        for (int64_t a = 0; a < nz; ++a) idz[a] = rows[m + q[a]];
-        scatter_lg(st, Lg, upload(c, idy), coff, 2, py.L);
-        const int32_t* didz = upload(c, idz);
+        scatter_lg(st, Lg, up[1], coff, 2, py.L);
+        const int32_t* didz = up[2];
         scatter_lg(st, Lg, didz, coff, 2, G12);
         scatter_lg(st, Lg, didz, coff + 1, 2, UpT);
         write_pair_diag(f, st, D, coff, py.d, py.dinv, delta, r);  // :254-260
 
         std::vector<int32_t> rows3(idz.begin() + r, idz.end());
-        HFact f3 = dispatch(C3, rows3, coff + 2 * r);  // :217
+        HFact f3 = dispatch(C3, rows3, didz + r, coff + 2 * r);  // :217
         const int64_t r3 = f3.rank;
 
         HFact h;  // P_i interleave + rotations (:226-251)
@@ -509,7 +540,7 @@ int guarded(ffb_context* c, F&& fn) {
     try {
         if (!c) throw Status(FFB_ERROR, "null context");
         FFB_CUDA(cudaSetDevice(c->device));
-        const uint64_t l0 = g_launches, s0 = c->syncs;
+        const uint64_t l0 = g_launches, s0 = c->syncs, u0 = c->uploads;
         const auto t0 = std::chrono::steady_clock::now();
         const double w0 = c->sync_wait_ms;
         g_prof = &c->prof;
@@ -518,9 +549,9 @@ int guarded(ffb_context* c, F&& fn) {
         if (host_stats) {  // host-side balance: wall vs time blocked on the device
             FFB_CUDA(cudaStreamSynchronize(c->stream));
             const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-            fprintf(stderr, "[ffb host] wall %.2f ms, blocked in %llu read-backs %.2f ms, launches %llu\n",
+            fprintf(stderr, "[ffb host] wall %.2f ms, blocked in %llu read-backs %.2f ms, launches %llu, uploads %llu\n",
                     wall, (unsigned long long)(c->syncs - s0), c->sync_wait_ms - w0,
-                    (unsigned long long)(g_launches - l0));
+                    (unsigned long long)(g_launches - l0), (unsigned long long)(c->uploads - u0));
         }
         if (c->prof.on) {
             FFB_CUDA(cudaStreamSynchronize(c->stream));
@@ -558,7 +589,7 @@ DevFact run_ldlt(ffb_context* c, const Fp& f, DMat W, int variant, int64_t thres
     DevFact out;
     out.n = n;
     if (check_symmetric) {  // ldlt validation, sytrf.cpp:355-356
-        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), st));
+        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), st)); pdl_fence(st);
         any_asymmetric(st, W, c->flag);
         if (*(const int32_t*)readback(c, c->flag, sizeof(int32_t)))
             throw Status(FFB_NOT_SYMMETRIC, "ldlt: matrix must be symmetric");
@@ -573,7 +604,7 @@ DevFact run_ldlt(ffb_context* c, const Fp& f, DMat W, int variant, int64_t thres
     std::vector<int32_t> rows(n);
     for (int64_t i = 0; i < n; ++i) rows[i] = (int32_t)i;
     if (n > 0) {
-        HFact h = e.dispatch(W, rows, 0);
+        HFact h = e.dispatch(W, rows, upload(c, rows), 0);
         out.rank = h.rank;
         out.perm = std::move(h.perm);
     }
@@ -593,12 +624,12 @@ void export_host(ffb_context* c, const DevFact& df, int64_t* perm, void* lower, 
         gather_lower_out(st, Lout, df.Lg, upload(c, df.perm));
         void* dl = ws_alloc(c, (size_t)n * r * lower_eb);
         convert_out(st, dl, lower_eb, Lout);
-        FFB_CUDA(cudaMemcpyAsync(lower, dl, (size_t)n * r * lower_eb, cudaMemcpyDeviceToHost, st));
+        FFB_CUDA(cudaMemcpyAsync(lower, dl, (size_t)n * r * lower_eb, cudaMemcpyDeviceToHost, st)); pdl_fence(st);
         std::vector<int32_t> k(r);
         std::vector<uint32_t> v(r), v2(r);
-        FFB_CUDA(cudaMemcpyAsync(k.data(), df.D.kind, r * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-        FFB_CUDA(cudaMemcpyAsync(v.data(), df.D.val, r * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
-        FFB_CUDA(cudaMemcpyAsync(v2.data(), df.D.val2, r * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        FFB_CUDA(cudaMemcpyAsync(k.data(), df.D.kind, r * sizeof(int32_t), cudaMemcpyDeviceToHost, st)); pdl_fence(st);
+        FFB_CUDA(cudaMemcpyAsync(v.data(), df.D.val, r * sizeof(uint32_t), cudaMemcpyDeviceToHost, st)); pdl_fence(st);
+        FFB_CUDA(cudaMemcpyAsync(v2.data(), df.D.val2, r * sizeof(uint32_t), cudaMemcpyDeviceToHost, st)); pdl_fence(st);
         FFB_CUDA(cudaStreamSynchronize(st));
         for (int64_t t = 0; t < r; ++t) {
             dkind[t] = k[t];
@@ -614,7 +645,7 @@ DMat upload_matrix(ffb_context* c, const Fp& f, const void* h, int64_t rows, int
     if (rows * cols == 0) return m;
     const size_t bytes = (size_t)rows * cols * eb;
     void* tmp = ws_alloc(c, bytes);
-    FFB_CUDA(cudaMemcpyAsync(tmp, h, bytes, cudaMemcpyHostToDevice, c->stream));
+    FFB_CUDA(cudaMemcpyAsync(tmp, h, bytes, cudaMemcpyHostToDevice, c->stream)); pdl_fence(c->stream);
     convert_in(f, c->stream, m, tmp, eb);
     return m;
 }
@@ -623,7 +654,7 @@ void download_matrix(ffb_context* c, DMat m, uint64_t* h) {
     if (m.rows * m.cols == 0) return;
     void* tmp = ws_alloc(c, (size_t)m.rows * m.cols * 8);
     convert_out(c->stream, tmp, 8, m);
-    FFB_CUDA(cudaMemcpyAsync(h, tmp, (size_t)m.rows * m.cols * 8, cudaMemcpyDeviceToHost, c->stream));
+    FFB_CUDA(cudaMemcpyAsync(h, tmp, (size_t)m.rows * m.cols * 8, cudaMemcpyDeviceToHost, c->stream)); pdl_fence(c->stream);
     FFB_CUDA(cudaStreamSynchronize(c->stream));
 }
 
@@ -673,6 +704,8 @@ int ffb_create(ffb_context** out, int device) {
         c->down_cap = (size_t)16 << 20;
         FFB_CUDA(cudaMallocHost(&c->down_host, c->down_cap));
         FFB_CUDA(cudaMalloc(&c->flag, 256));
+        FFB_CUDA(cudaMemset(c->flag, 0, 256));
+        c->zero_flag = c->flag + 32;
         *out = c;
         return FFB_OK;
     } catch (const std::exception& e) {
@@ -756,7 +789,7 @@ int ffb_ldlt_zero_leading(ffb_context* c, uint64_t p, size_t m, size_t ny, const
         Fp f = make_field(c, p);
         DMat Zd = upload_matrix(c, f, z, (int64_t)nz, (int64_t)nz, 8);
         {
-            FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), c->stream));
+            FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), c->stream)); pdl_fence(c->stream);
             any_asymmetric(c->stream, Zd, c->flag);
             if (*(const int32_t*)readback(c, c->flag, sizeof(int32_t)))
                 throw Status(FFB_NOT_SYMMETRIC, "ldlt_zero_leading: Z must be symmetric");
@@ -773,7 +806,7 @@ int ffb_ldlt_zero_leading(ffb_context* c, uint64_t p, size_t m, size_t ny, const
         Engine e{c, c->stream, f, variant, (int64_t)threshold, df.Lg, df.D};
         std::vector<int32_t> rows(N);
         for (int64_t i = 0; i < N; ++i) rows[i] = (int32_t)i;
-        HFact h = e.zero_leading(Yd, Zd, rows, 0);
+        HFact h = e.zero_leading(Yd, Zd, rows, upload(c, rows), 0);
         df.rank = h.rank;
         df.perm = h.perm;
         export_host(c, df, perm, lower, 8, dkind, dval, dval2, rank);
@@ -798,7 +831,7 @@ int ffb_ldlt_device(ffb_context* c, uint64_t p, size_t n, uint32_t* d_a, size_t 
         *rank = (size_t)r;
         if (n > 0) {
             const int32_t* dp = upload(c, df.perm);
-            FFB_CUDA(cudaMemcpyAsync(d_perm, dp, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
+            FFB_CUDA(cudaMemcpyAsync(d_perm, dp, n * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream)); pdl_fence(c->stream);
             DMat Lout;
             Lout.ptr = d_lower;
             Lout.ld = (int64_t)ldl;
@@ -806,9 +839,9 @@ int ffb_ldlt_device(ffb_context* c, uint64_t p, size_t n, uint32_t* d_a, size_t 
             Lout.cols = r;
             gather_lower_out(c->stream, Lout, df.Lg, dp);
             if (r > 0) {
-                FFB_CUDA(cudaMemcpyAsync(d_dkind, df.D.kind, r * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
-                FFB_CUDA(cudaMemcpyAsync(d_dval, df.D.val, r * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
-                FFB_CUDA(cudaMemcpyAsync(d_dval2, df.D.val2, r * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream));
+                FFB_CUDA(cudaMemcpyAsync(d_dkind, df.D.kind, r * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream)); pdl_fence(c->stream);
+                FFB_CUDA(cudaMemcpyAsync(d_dval, df.D.val, r * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream)); pdl_fence(c->stream);
+                FFB_CUDA(cudaMemcpyAsync(d_dval2, df.D.val2, r * sizeof(uint32_t), cudaMemcpyDeviceToDevice, c->stream)); pdl_fence(c->stream);
             }
         }
         FFB_CUDA(cudaStreamSynchronize(c->stream));
@@ -868,7 +901,7 @@ int ffb_trssyr2k(ffb_context* c, uint64_t p, size_t n, const uint64_t* u, const 
         DMat C = upload_matrix(c, f, cc, N, N, 8);
         DMat X = ws_mat(c, N, N);
         Engine e{c, c->stream, f, FFB_VARIANT_CASCADE, 64, DMat(), DDiag()};
-        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), c->stream));
+        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), c->stream)); pdl_fence(c->stream);
         e.trssyr2k_dev(U, UT, C, X, c->flag);
         if (f.char2 && *(const int32_t*)readback(c, c->flag, sizeof(int32_t)))
             throw Status(FFB_CHAR_TWO_NONZERO_DIAGONAL, "trssyr2k: diagonal entry has no solution");

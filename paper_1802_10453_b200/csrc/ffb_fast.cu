@@ -39,8 +39,8 @@ struct Ar<false> {
 };
 
 template <bool kSmall>
-__global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict__ A, int64_t lda,
-                                                int s, const int32_t* __restrict__ rows,
+__global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* A, int64_t lda,
+                                                int s, const int32_t* rows,
                                                 uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
                                                 int32_t* out) {
     FFB_PDL_ENTRY();
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* __restrict
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
         const int i = ty + 4 * q;
-        S[q] = (i < s && tx < s) ? __ldg(A + (int64_t)i * lda + tx) : 0;
+        S[q] = (i < s && tx < s) ? __ldcg(A + (int64_t)i * lda + tx) : 0;
     }
     for (int e = tid; e < 64 * 65; e += 256) (&Ls[0][0])[e] = 0;
     const SmemInv inv = stage_inverses(f, sinv);
@@ -193,7 +193,7 @@ __device__ __forceinline__ uint32_t dot_lt(const Fp& f, const uint32_t* a, int s
     return red64(f, acc);
 }
 template <int kMode>
-__global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
+__global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* T, int64_t ldt,
                                                  int64_t n, uint32_t* Tinv) {
     FFB_PDL_ENTRY();
     __shared__ uint32_t Ts[64][65];
@@ -256,8 +256,8 @@ __global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* __restric
 // from L2 per tile (they are shared by all column tiles).
 constexpr int PNL_COLS = 32;
 template <bool kSmall>
-__global__ void __launch_bounds__(256) k_trsm_panel(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
-                                                    const uint32_t* __restrict__ Tinv, uint32_t* B,
+__global__ void __launch_bounds__(256) k_trsm_panel(Fp f, const uint32_t* T, int64_t ldt,
+                                                    const uint32_t* Tinv, uint32_t* B,
                                                     int64_t ldb, int nb, int64_t ncols) {
     FFB_PDL_ENTRY();
     extern __shared__ uint32_t sm[];
@@ -323,13 +323,13 @@ constexpr int PM_COLS = 64, PM_XU = PM_COLS + 8, PM_XB = 256 + 16, PM_AB = 64 + 
 constexpr size_t PM_SMEM = (size_t)256 * PM_XU * 4 + (size_t)PM_COLS * PM_XB + (size_t)64 * PM_AB;
 
 // 64 x 64 block of u32 residues (rows < rv, cols < cv; zero elsewhere) -> centered int8 in Ab
-__device__ __forceinline__ void pm_load_a(int8_t* Ab, const uint32_t* __restrict__ src, int64_t ld, int rv,
+__device__ __forceinline__ void pm_load_a(int8_t* Ab, const uint32_t* src, int64_t ld, int rv,
                                           int cv, uint32_t p, uint32_t half) {
     uint32_t v[16];
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
         const int e = threadIdx.x + 256 * u, r = e >> 6, c = e & 63;
-        v[u] = (r < rv && c < cv) ? __ldg(src + (int64_t)r * ld + c) : 0u;
+        v[u] = (r < rv && c < cv) ? __ldcg(src + (int64_t)r * ld + c) : 0u;
     }
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
@@ -353,8 +353,8 @@ __device__ __forceinline__ void pm_mma(int (&acc)[4][4], const int8_t* Ab, const
         }
     }
 }
-__global__ void __launch_bounds__(256, 2) k_trsm_panel_mma(Fp f, const uint32_t* __restrict__ T, int64_t ldt,
-                                                           const uint32_t* __restrict__ Tinv, uint32_t* B,
+__global__ void __launch_bounds__(256, 2) k_trsm_panel_mma(Fp f, const uint32_t* T, int64_t ldt,
+                                                           const uint32_t* Tinv, uint32_t* B,
                                                            int64_t ldb, int nb, int64_t ncols) {
     FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint8_t pm_smem[];

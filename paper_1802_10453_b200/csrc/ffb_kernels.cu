@@ -83,9 +83,9 @@ namespace {
 constexpr int GB_M = 64, GB_N = 64, GB_K = 16;
 
 template <bool TA, bool TB, bool kLargeP>
-__global__ void __launch_bounds__(256) k_gemm_simt(Fp f, int mode, uint32_t* __restrict__ C,
-                                                   int64_t ldc, const uint32_t* __restrict__ A,
-                                                   int64_t lda, const uint32_t* __restrict__ B,
+__global__ void __launch_bounds__(256) k_gemm_simt(Fp f, int mode, uint32_t* C,
+                                                   int64_t ldc, const uint32_t* A,
+                                                   int64_t lda, const uint32_t* B,
                                                    int64_t ldb, int64_t M, int64_t N, int64_t K) {
     FFB_PDL_ENTRY();
     __shared__ uint32_t As[GB_K][GB_M + 4];
@@ -108,11 +108,11 @@ __global__ void __launch_bounds__(256) k_gemm_simt(Fp f, int mode, uint32_t* __r
             int i, kk;
             if (TA) { i = e % GB_M; kk = e / GB_M; } else { kk = e % GB_K; i = e / GB_K; }
             const int64_t gi = m0 + i, gk = k0 + kk;
-            ra[u] = (gi < M && gk < K) ? __ldg(TA ? A + gk * lda + gi : A + gi * lda + gk) : 0u;
+            ra[u] = (gi < M && gk < K) ? __ldcg(TA ? A + gk * lda + gi : A + gi * lda + gk) : 0u;
             int j, kb;
             if (TB) { kb = e % GB_K; j = e / GB_K; } else { j = e % GB_N; kb = e / GB_N; }
             const int64_t gj = n0 + j, gkb = k0 + kb;
-            rb[u] = (gj < N && gkb < K) ? __ldg(TB ? B + gj * ldb + gkb : B + gkb * ldb + gj) : 0u;
+            rb[u] = (gj < N && gkb < K) ? __ldcg(TB ? B + gj * ldb + gkb : B + gkb * ldb + gj) : 0u;
         }
     };
     auto stash = [&]() {
@@ -317,11 +317,11 @@ __global__ void k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int6
         const uint4* s4 = reinterpret_cast<const uint4*>(s);
         uint4* d4 = reinterpret_cast<uint4*>(d);
         for (; j + step < c4; j += 2 * step) {
-            const uint4 a = __ldg(s4 + j), b = __ldg(s4 + j + step);
+            const uint4 a = __ldcg(s4 + j), b = __ldcg(s4 + j + step);
             d4[j] = a;
             d4[j + step] = b;
         }
-        for (; j < c4; j += step) d4[j] = __ldg(s4 + j);
+        for (; j < c4; j += step) d4[j] = __ldcg(s4 + j);
         for (int64_t t = 4 * c4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cols; t += step) d[t] = s[t];
         return;
     }
@@ -386,14 +386,14 @@ __global__ void k_invert_vec(Fp f, uint32_t* out, const uint32_t* v, int64_t n) 
 }
 
 __global__ void k_any_nonzero(const uint32_t* m, int64_t ld, int64_t rows, int64_t cols,
-                              int32_t* flag) {
+                              int32_t* flag, int32_t value) {
     FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     int found = 0;
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
          j += (int64_t)gridDim.x * blockDim.x)
         found |= m[i * ld + j] != 0;
-    if (__syncthreads_or(found) && threadIdx.x == 0) atomicOr(flag, 1);
+    if (__syncthreads_or(found) && threadIdx.x == 0) *flag = value;  // same value from every CTA
 }
 
 // Symmetry check: block (x, y) compares the 32-row band y against the transposed
@@ -411,9 +411,9 @@ __global__ void k_any_asym(const uint32_t* a, int64_t ld, int64_t n, int32_t* fl
         for (int u = 0; u < 4; ++u) {
             const int k = threadIdx.y + 8 * u;
             const int64_t r = c0 + k, c = r0 + threadIdx.x;  // transposed tile
-            up[u] = (r < n && c < n) ? __ldg(a + r * ld + c) : 0u;
+            up[u] = (r < n && c < n) ? __ldcg(a + r * ld + c) : 0u;
             const int64_t rr = r0 + k, cc = c0 + threadIdx.x;
-            lo[u] = (rr < n && cc < n) ? __ldg(a + rr * ld + cc) : 0u;
+            lo[u] = (rr < n && cc < n) ? __ldcg(a + rr * ld + cc) : 0u;
         }
         __syncthreads();  // previous tile's comparisons done
 #pragma unroll
@@ -643,12 +643,12 @@ void invert_vec(const Fp& f, cudaStream_t st, uint32_t* out, const uint32_t* v, 
     FFB_CHECK_LAUNCH();
 }
 
-void any_nonzero(cudaStream_t st, DMat m, int32_t* flag) {
+void any_nonzero(cudaStream_t st, DMat m, int32_t* flag, int32_t value) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (m.rows <= 0 || m.cols <= 0) return;
     for (int64_t r0 = 0; r0 < m.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, m.rows - r0);
-        launch_k(k_any_nonzero, rowgrid(nr, m.cols), 256, 0, st, m.ptr + r0 * m.ld, m.ld, nr, m.cols, flag);
+        launch_k(k_any_nonzero, rowgrid(nr, m.cols), 256, 0, st, m.ptr + r0 * m.ld, m.ld, nr, m.cols, flag, value);
         count_launch();
     }
     FFB_CHECK_LAUNCH();
@@ -710,7 +710,7 @@ void zero_mat(cudaStream_t st, DMat m) {
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (m.rows <= 0 || m.cols <= 0) return;
     if (m.ld == m.cols) {
-        FFB_CUDA(cudaMemsetAsync(m.ptr, 0, (size_t)m.rows * m.cols * sizeof(uint32_t), st));
+        FFB_CUDA(cudaMemsetAsync(m.ptr, 0, (size_t)m.rows * m.cols * sizeof(uint32_t), st)); pdl_fence(st);
         return;
     }
     for (int64_t r0 = 0; r0 < m.rows; r0 += FFB_ROWCHUNK) {
@@ -781,8 +781,8 @@ struct LeafState {  // laid out after S in (shared or global) scratch
 };
 
 __global__ void __launch_bounds__(LEAF_THREADS)
-    k_leaf_crout(Fp f, const uint32_t* __restrict__ A, int64_t lda, int s, uint32_t* gscratch,
-                 int use_smem, const int32_t* __restrict__ rows, uint32_t* Lg, int64_t ldL,
+    k_leaf_crout(Fp f, const uint32_t* A, int64_t lda, int s, uint32_t* gscratch,
+                 int use_smem, const int32_t* rows, uint32_t* Lg, int64_t ldL,
                  int64_t coff, DDiag D, int32_t* out) {
     FFB_PDL_ENTRY();
     extern __shared__ uint32_t smem[];

@@ -99,7 +99,8 @@ void scale_T(const Fp& f, cudaStream_t st, DMat G, DMat X, const uint32_t* dinv)
 // out[i] = v[i]^-1
 void invert_vec(const Fp& f, cudaStream_t st, uint32_t* out, const uint32_t* v, int64_t n);
 // flag (device int) |= any nonzero in m
-void any_nonzero(cudaStream_t st, DMat m, int32_t* flag);
+// *flag = value when m has a nonzero entry (untouched otherwise)
+void any_nonzero(cudaStream_t st, DMat m, int32_t* flag, int32_t value = 1);
 // flag |= any a[i][j] != a[j][i]
 void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag);
 // Y <- strict_upper(Ct) + diag(Ct)/2 (odd p) or 0 (p = 2); lower part zeroed; in place.

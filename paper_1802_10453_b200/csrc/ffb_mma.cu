@@ -21,10 +21,10 @@ constexpr int MM_T = 64, MM_S = 64 + 16;  // tile edge, smem row stride in bytes
 // Split K: CTA z covers k in [z kc, (z+1) kc) and, when gridDim.z > 1, writes
 // its reduced partial tile to W[z] (M x N, ld N) for k_splitk_fold.
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* __restrict__ C, int64_t ldc,
-                                                  const uint32_t* __restrict__ A, int64_t lda,
-                                                  const uint32_t* __restrict__ B, int64_t ldb, int64_t M,
-                                                  int64_t N, int64_t K, int64_t kc, uint32_t* __restrict__ W) {
+__global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* C, int64_t ldc,
+                                                  const uint32_t* A, int64_t lda,
+                                                  const uint32_t* B, int64_t ldb, int64_t M,
+                                                  int64_t N, int64_t K, int64_t kc, uint32_t* W) {
     FFB_PDL_ENTRY();
     __shared__ __align__(16) int8_t As[MM_T * MM_S];  // op(A) tile [m][k]
     __shared__ __align__(16) int8_t Bs[MM_T * MM_S];  // op(B) tile transposed [n][k]
@@ -42,11 +42,11 @@ __global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* __re
             const int e = tid + 256 * u, hi = e >> 6, lo = e & 63;
             {
                 const int64_t m = m0 + (TA ? lo : hi), k = k0 + (TA ? hi : lo);
-                ra[u] = (m < M && k < K) ? __ldg(TA ? A + k * lda + m : A + m * lda + k) : 0u;
+                ra[u] = (m < M && k < K) ? __ldcg(TA ? A + k * lda + m : A + m * lda + k) : 0u;
             }
             {
                 const int64_t n = n0 + (TB ? hi : lo), k = k0 + (TB ? lo : hi);
-                rb[u] = (n < N && k < K) ? __ldg(TB ? B + n * ldb + k : B + k * ldb + n) : 0u;
+                rb[u] = (n < N && k < K) ? __ldcg(TB ? B + n * ldb + k : B + k * ldb + n) : 0u;
             }
         }
     };
@@ -202,9 +202,9 @@ __device__ __forceinline__ uint32_t pack4c(uint32_t a, uint32_t b, uint32_t c, u
 }
 
 template <bool TA, bool TB>
-__global__ void __launch_bounds__(256) k_rankk_dp4a(Fp f, int mode, uint32_t* __restrict__ C, int64_t ldc,
-                                                    const uint32_t* __restrict__ A, int64_t lda,
-                                                    const uint32_t* __restrict__ B, int64_t ldb, int64_t M,
+__global__ void __launch_bounds__(256) k_rankk_dp4a(Fp f, int mode, uint32_t* C, int64_t ldc,
+                                                    const uint32_t* A, int64_t lda,
+                                                    const uint32_t* B, int64_t ldb, int64_t M,
                                                     int64_t N, int K, int TR) {
     FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint32_t rk_sm[];
@@ -216,10 +216,10 @@ __global__ void __launch_bounds__(256) k_rankk_dp4a(Fp f, int mode, uint32_t* __
     const int rows = (int)std::min<int64_t>(TR, M - m0);
     const uint32_t p = f.p, half = (p - 1) / 2, bias = (uint32_t)(0x80000000ull % p);
     auto opB = [&](int k, int64_t n) -> uint32_t {
-        return (k < K && n < N) ? __ldg(TB ? B + n * ldb + k : B + (int64_t)k * ldb + n) : 0u;
+        return (k < K && n < N) ? __ldcg(TB ? B + n * ldb + k : B + (int64_t)k * ldb + n) : 0u;
     };
     auto opA = [&](int64_t m, int k) -> uint32_t {
-        return (k < K && m < M) ? __ldg(TA ? A + (int64_t)k * lda + m : A + m * lda + k) : 0u;
+        return (k < K && m < M) ? __ldcg(TA ? A + (int64_t)k * lda + m : A + m * lda + k) : 0u;
     };
     for (int e = tid; e < K4 * RK_COLS; e += 256) {
         const int q = e / RK_COLS, j = e - q * RK_COLS;
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(256) k_rankk_dp4a(Fp f, int mode, uint32_t* __
             cv[u] = make_uint4(0, 0, 0, 0);
             if (i < rows && mode != GEMM_SET) {
                 const uint32_t* cp = C + (m0 + i) * ldc + col;
-                if (vec) cv[u] = __ldg(reinterpret_cast<const uint4*>(cp));
+                if (vec) cv[u] = __ldcg(reinterpret_cast<const uint4*>(cp));
                 else {
                     cv[u].x = col < N ? cp[0] : 0u;
                     cv[u].y = col + 1 < N ? cp[1] : 0u;

@@ -324,7 +324,7 @@ constexpr int CRP_W = 256, CRP_G = 32, CRP_KMAX = 128;
 // of the independent columns are written to out[0 .. nb) in scan order.
 // Stops once k columns are found.  E, V, VC: shared (see k_crp_list).
 template <class ColFn>
-__device__ int crp_scan(const Fp& f, const SmemInv& inv, const uint32_t* __restrict__ RI, int64_t ldr,
+__device__ int crp_scan(const Fp& f, const SmemInv& inv, const uint32_t* RI, int64_t ldr,
                         int k, int total, ColFn colfn, uint32_t* E, uint32_t* V, uint32_t* VC, int* rho,
                         unsigned* fmask, BatchScratch& bs, int32_t* out) {
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
@@ -335,7 +335,7 @@ __device__ int crp_scan(const Fp& f, const SmemInv& inv, const uint32_t* __restr
 #pragma unroll
         for (int u = 0; u < CRP_KMAX / 8; ++u) {
             const int i = wp + 8 * u;
-            vv[u] = (ok && i < k) ? __ldg(src + (int64_t)i * ldr) : 0u;
+            vv[u] = (ok && i < k) ? __ldcg(src + (int64_t)i * ldr) : 0u;
         }
     };
     fetch(0);
@@ -365,7 +365,7 @@ __device__ int crp_scan(const Fp& f, const SmemInv& inv, const uint32_t* __restr
     return nb;
 }
 
-__global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* __restrict__ RI, int64_t ldr,
+__global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int64_t ldr,
                                                   int k, int64_t n, int32_t* out, int32_t* ocount) {
     FFB_PDL_ENTRY();
     extern __shared__ uint32_t sm[];
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(256) k_crp_rowelim(Fp f, const uint32_t* RI, i
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
                     const int j = j0 + 32 * u;
-                    vv[u] = j < C ? __ldg(RI + (int64_t)i * ldr + cand[j]) : 0u;
+                    vv[u] = j < C ? __ldcg(RI + (int64_t)i * ldr + cand[j]) : 0u;
                 }
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -516,8 +516,8 @@ __host__ __device__ inline size_t cf_smem_bytes(int k, int nblk, int* rc_cap) {
     return ((size_t)k * k + std::max<size_t>(std::max<size_t>((size_t)*rc_cap, scan), sketch)) * 4;
 }
 __global__ void __launch_bounds__(256) k_crp_finish(
-    Fp f, const uint32_t* __restrict__ RI, int64_t ldr, int k, const int32_t* __restrict__ lists,
-    const int32_t* __restrict__ counts, int nblk, int32_t* cand, int rc_cap, const int32_t* I, int64_t c0,
+    Fp f, const uint32_t* RI, int64_t ldr, int k, const int32_t* lists,
+    const int32_t* counts, int nblk, int32_t* cand, int rc_cap, const int32_t* I, int64_t c0,
     const uint32_t* S, int64_t lds, int s, uint32_t* Kinv, int32_t* Jout, uint32_t* UO, int64_t lduo,
     int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r, int32_t* fail) {
     FFB_PDL_ENTRY();
@@ -582,7 +582,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const int j = j0 + 32 * u;
-                vv[u] = j < Cx ? __ldg(RI + (int64_t)i * ldr + ids[j]) : 0u;
+                vv[u] = j < Cx ? __ldcg(RI + (int64_t)i * ldr + ids[j]) : 0u;
             }
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
@@ -657,7 +657,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     if (S) {  // UO rows: stage the k sketch rows S_I (coalesced) in the free M buffer
         uint32_t* SI = M;
         for (int u = wp; u < k; u += 8)
-            for (int col = lane; col < s; col += 32) SI[(size_t)u * s + col] = __ldg(S + (int64_t)Is[u] * lds + col);
+            for (int col = lane; col < s; col += 32) SI[(size_t)u * s + col] = __ldcg(S + (int64_t)Is[u] * lds + col);
         __syncthreads();
         for (int e = tid; e < k * s; e += 256) {
             const int t = e / s, col = e - t * s;
@@ -703,7 +703,7 @@ __global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t
     const SmemInv inv = stage_inverses(f, sinv);
     for (int e = tid; e < k * k; e += blockDim.x) {
         const int i = e / k, j = e % k;
-        const uint32_t v = __ldg(RI + (int64_t)i * ldr + J[j]);
+        const uint32_t v = __ldcg(RI + (int64_t)i * ldr + J[j]);
         A[e] = v;
         G[(size_t)i * 2 * k + j] = v;
         G[(size_t)i * 2 * k + k + j] = (i == j) ? 1 % f.p : 0;
@@ -913,7 +913,7 @@ void copy_mat(cudaStream_t st, DMat dst, DMat src) {
     ProfScope ps(K_MOVE, st, 0.0, 8.0 * src.rows * src.cols);
     if (dst.ld == src.ld && dst.ld == src.cols) {
         FFB_CUDA(cudaMemcpyAsync(dst.ptr, src.ptr, (size_t)src.rows * src.cols * 4,
-                                 cudaMemcpyDeviceToDevice, st));
+                                 cudaMemcpyDeviceToDevice, st)); pdl_fence(st);
         return;
     }
     FFB_CUDA(cudaMemcpy2DAsync(dst.ptr, dst.ld * 4, src.ptr, src.ld * 4, src.cols * 4, src.rows,
@@ -1012,7 +1012,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     bool side_pending = false;
     auto join_side = [&]() {
         if (side_pending) {
-            FFB_CUDA(cudaStreamWaitEvent(st, ev_side, 0));
+            FFB_CUDA(cudaStreamWaitEvent(st, ev_side, 0)); pdl_fence(st);
             side_pending = false;
         }
     };
@@ -1046,7 +1046,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         }
         if (sketching && overlap_ok) {
             FFB_CUDA(cudaEventRecord(ev_main, st));
-            FFB_CUDA(cudaStreamWaitEvent(side, ev_main, 0));
+            FFB_CUDA(cudaStreamWaitEvent(side, ev_main, 0)); pdl_fence(side);
             us = side;
         }
         {
@@ -1065,7 +1065,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     for (int attempt = 0; attempt < 2; ++attempt) {
         ws.release(mark1);
         r = 0;
-        FFB_CUDA(cudaMemsetAsync(dflag, 0, 4, st));
+        FFB_CUDA(cudaMemsetAsync(dflag, 0, 4, st)); pdl_fence(st);
         DMat YO;
         if (!exact) {  // Y * Omega, once
             DMat Om = ws.mat(n, SK);

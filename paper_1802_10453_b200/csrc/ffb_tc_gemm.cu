@@ -126,7 +126,7 @@ struct TcCfg {
 template <int BN, int ST>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_i8_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 uint32_t* __restrict__ C, int64_t ldc, int M, int N, int nk, Fp f, int mode) {
+                 uint32_t* C, int64_t ldc, int M, int N, int nk, Fp f, int mode) {
     FFB_PDL_ENTRY();
     using Cfg = TcCfg<BN, ST>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
             for (int rr = 0; rr < 32; ++rr) {
                 const int row = rbase + rr;
-                cv[rr] = (mode != GEMM_SET && colok && row < M) ? __ldg(C + (int64_t)row * ldc + col) : 0u;
+                cv[rr] = (mode != GEMM_SET && colok && row < M) ? __ldcg(C + (int64_t)row * ldc + col) : 0u;
             }
         };
         load_c(0);
@@ -272,7 +272,7 @@ constexpr uint32_t LB_IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(L
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_limb_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   uint32_t* __restrict__ C, int64_t ldc, int M, int N, int nk, int Mrows, int Nrows,
+                   uint32_t* C, int64_t ldc, int M, int N, int nk, int Mrows, int Nrows,
                    Fp f, int mode) {
     FFB_PDL_ENTRY();
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
                 for (int rr = 0; rr < 32; ++rr) {
                     const int row = rbase + rr;
-                    cv[rr] = (colok && row < M) ? __ldg(C + (int64_t)row * ldc + col) : 0u;
+                    cv[rr] = (colok && row < M) ? __ldcg(C + (int64_t)row * ldc + col) : 0u;
                 }
             }
 #pragma unroll
@@ -643,7 +643,7 @@ void tc_gemm_limb(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, b
     int8_t* Bp = buf + abytes;
     {
         ProfScope ps(K_PACK, st, 0.0, 7.0 * (M * K + N * K));
-        FFB_CUDA(cudaMemsetAsync(buf, 0, abytes + bbytes, st));
+        FFB_CUDA(cudaMemsetAsync(buf, 0, abytes + bbytes, st)); pdl_fence(st);
         auto pk = [&](int8_t* dst, size_t plane, DMat src, bool trans, int64_t rows) {
             if (!trans) {
                 for (int64_t r0 = 0; r0 < rows; r0 += 65535) {

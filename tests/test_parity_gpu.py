@@ -321,3 +321,18 @@ def test_trsm_panel_paths(gpu, oracle, n, cols, p):
     for up, tr in ((0, 0), (1, 0)):
         assert np.array_equal(ffb.trsm_inplace(t, up, tr, 1, bb, p, ctx=gpu),
                               oracle.trsm_inplace(p, t, up, tr, 1, bb))
+
+
+@pytest.mark.parametrize("p", [131, 8388593])
+def test_repeated_calls_same_context(gpu, oracle, p):
+    """Back-to-back factorizations on one context reuse the same workspace addresses, and
+    kernels are chained with programmatic dependent launch: a kernel that read producer
+    data through the non-coherent path could see a stale line from the previous call
+    (caught once as a rank-1 2x2 factored as rank 2).  Repeat small and medium cases."""
+    rng = np.random.default_rng(p)
+    cases = [np.array([[3531144, 3586508], [3586508, 3074401]], dtype=np.uint64) % p,
+             rand_low_rank(rng, p, 5, 2), rand_sym(rng, p, 70), rand_low_rank(rng, p, 130, 60)]
+    for rep in range(6):
+        for a in cases:
+            for v, t in (("recursive", 64), ("cascade", 4)):
+                check(gpu, oracle, p, a, v, t)
