@@ -275,9 +275,10 @@ Fp make_field(ffb_context* c, uint64_t p) {
 // ===========================================================================
 // The recursion.
 // ===========================================================================
-// Y with at most this many rows goes to the one-launch sequential PLDUQ.
+// Y with at most this many rows goes to the one-launch sequential PLDUQ (200:
+// measured crossover against the chunked pipeline on config 5).
 static int64_t PLDUQ_SEQ_MAX_ROWS =
-    getenv("FFB_PLDUQ_SEQ_ROWS") ? atoll(getenv("FFB_PLDUQ_SEQ_ROWS")) : 48;
+    getenv("FFB_PLDUQ_SEQ_ROWS") ? atoll(getenv("FFB_PLDUQ_SEQ_ROWS")) : 200;
 
 struct HFact {
     std::vector<int32_t> perm;  // image: position -> local input row
