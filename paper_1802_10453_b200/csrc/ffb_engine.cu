@@ -740,7 +740,11 @@ int ffb_create(ffb_context** out, int device) {
         ffb_context* c = new ffb_context();
         c->device = device;
         FFB_CUDA(cudaSetDevice(device));
-        FFB_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        {  // the recursion's critical path: highest stream priority (side streams use the lowest)
+            int least = 0, greatest = 0;
+            FFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            FFB_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest));
+        }
         c->up_cap = (size_t)64 << 20;
         FFB_CUDA(cudaMallocHost(&c->up_host, c->up_cap));
         c->down_cap = (size_t)16 << 20;

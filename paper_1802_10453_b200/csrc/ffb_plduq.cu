@@ -1005,7 +1005,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     static thread_local cudaEvent_t ev_main = nullptr, ev_side = nullptr;
     static const bool overlap_ok = !getenv("FFB_PLDUQ_NO_OVERLAP");  // test hook
     if (!side) {
-        FFB_CUDA(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+        int least = 0, greatest = 0;  // lowest priority: the main stream's chunk kernels go first
+        FFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        FFB_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, least));
         FFB_CUDA(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
         FFB_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
     }

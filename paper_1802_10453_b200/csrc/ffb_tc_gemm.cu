@@ -252,6 +252,179 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// Persistent variant for large products (p <= 255): one CTA per SM walks the
+// 128 x 256 output tiles (M fastest, so the CTAs in flight share B tiles);
+// the accumulator is double-buffered in TMEM (2 x 256 columns), so the
+// epilogue of tile t (8 warps: TMEM lane quadrant warp % 4, column half) runs
+// while the MMA warp accumulates tile t+1.  Pipelines: smem full/empty
+// (TMA <-> MMA) and TMEM full/empty (MMA <-> epilogue).
+// ---------------------------------------------------------------------------
+constexpr int TP_BN = 256, TP_STAGES = 3, TP_EPI_WARPS = 8, TP_THREADS = (2 + TP_EPI_WARPS) * 32;
+struct TpCfg {
+    static constexpr int A_BYTES = TC_BM * TC_BK;
+    static constexpr int B_BYTES = TP_BN * TC_BK;
+    static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+    static constexpr int EPI_BYTES = TP_EPI_WARPS * 32 * 33 * 4;
+    static constexpr int SMEM = 1024 + TP_STAGES * STAGE_BYTES + EPI_BYTES + 256;
+};
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(TP_THREADS, 1)
+    k_gemm_i8_tcp(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  uint32_t* C, int64_t ldc, int M, int N, int nk, Fp f, int mode, int num_m, int num_tiles) {
+    FFB_PDL_ENTRY();
+    extern __shared__ __align__(1024) uint8_t tp_raw[];
+    uint8_t* smem = (uint8_t*)(((uintptr_t)tp_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + TP_STAGES * TpCfg::A_BYTES;
+    uint32_t* sEpi = (uint32_t*)(smem + TP_STAGES * TpCfg::STAGE_BYTES);
+    uint64_t* full = (uint64_t*)(sEpi + TP_EPI_WARPS * 32 * 33);
+    uint64_t* empty = full + TP_STAGES;
+    uint64_t* tfull = empty + TP_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmB) : "memory");
+        for (int s = 0; s < TP_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], TP_EPI_WARPS);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(2u * TP_BN));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    constexpr uint32_t IDESC = TcCfg<TP_BN>::IDESC;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer ----
+            int s = 0;
+            uint32_t ph = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                const int m0 = (t % num_m) * TC_BM, n0 = (t / num_m) * TP_BN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    mbar_expect_tx(&full[s], TpCfg::STAGE_BYTES);
+                    tma_load_2d(sA + s * TpCfg::A_BYTES, &tmA, &full[s], kb * TC_BK, m0);
+                    tma_load_2d(sB + s * TpCfg::B_BYTES, &tmB, &full[s], kb * TC_BK, n0);
+                    if (++s == TP_STAGES) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer ----
+            int s = 0, acc = 0;
+            uint32_t ph = 0, aph = 0;
+            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                mbar_wait(&tempty[acc], aph ^ 1);  // the epilogue has drained this accumulator
+                tc_fence_after();
+                const uint32_t d = tmem + (uint32_t)(acc * TP_BN);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&full[s], ph);
+                    tc_fence_after();
+                    const uint32_t a0 = smem_u32(sA + s * TpCfg::A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + s * TpCfg::B_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < TC_BK / 32; ++kk)
+                        mma_i8(d, sw128_desc(a0 + kk * 32), sw128_desc(b0 + kk * 32), IDESC, (kb | kk) != 0);
+                    mma_commit(&empty[s]);
+                    if (++s == TP_STAGES) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+                mma_commit(&tfull[acc]);
+                if (++acc == 2) {
+                    acc = 0;
+                    aph ^= 1;
+                }
+            }
+        }
+    } else {
+        // ---- epilogue: TMEM lanes 32*(warp % 4), columns [128 h, 128 h + 128) ----
+        const int q = warp & 3, h = (warp - 2) >> 2;
+        uint32_t* tile = sEpi + (warp - 2) * 32 * 33;
+        const Fp16 hf(f.p);
+        const uint32_t bias = (uint32_t)((0x80000000ull) % f.p);
+        int acc = 0;
+        uint32_t aph = 0;
+        uint32_t cv[32];
+        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            const int m0 = (t % num_m) * TC_BM, n0 = (t / num_m) * TP_BN + 128 * h;
+            const int rbase = m0 + 32 * q;
+            auto load_c = [&](int c) {
+                const int col = n0 + c + lane;
+                const bool colok = col < N;
+#pragma unroll
+                for (int rr = 0; rr < 32; ++rr) {
+                    const int row = rbase + rr;
+                    cv[rr] = (mode != GEMM_SET && colok && row < M) ? __ldcg(C + (int64_t)row * ldc + col) : 0u;
+                }
+            };
+            load_c(0);  // C does not depend on the accumulator
+            mbar_wait(&tfull[acc], aph);
+            tc_fence_after();
+            for (int c = 0; c < 128; c += 32) {
+                if (n0 + c >= N) break;
+                uint32_t r[32];
+                tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(acc * TP_BN + 128 * h + c), r);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) tile[lane * 33 + j] = hf.sub(hf.red(r[j] ^ 0x80000000u), bias);
+                __syncwarp();
+                const int col = n0 + c + lane;
+                const bool colok = col < N;
+#pragma unroll
+                for (int rr = 0; rr < 32; ++rr) {
+                    const int row = rbase + rr;
+                    if (colok && row < M) {
+                        const uint32_t v = tile[rr * 33 + lane];
+                        uint32_t o;
+                        if (mode == GEMM_SUB) o = hf.sub(cv[rr], v);
+                        else if (mode == GEMM_ADD) o = fadd(f, cv[rr], v);
+                        else o = v;
+                        C[(int64_t)row * ldc + col] = o;
+                    }
+                }
+                if (c + 32 < 128 && n0 + c + 32 < N) load_c(c + 32);
+                __syncwarp();
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);  // accumulator free for tile t + 2
+            if (++acc == 2) {
+                acc = 0;
+                aph ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2u * TP_BN));
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Limb variant for 255 < p < 2^23 (configuration 3).  A centered residue x,
 // |x| < 2^22, is split into signed int8 limbs x = a0 + 2^8 a1 + 2^16 a2
 // (|a2| <= 64).  Per 32-deep K step the single MMA thread issues the 9 limb
@@ -484,29 +657,74 @@ struct PackJob {
     int64_t rows, K;
     int trans;
 };
-__global__ void k_pack2(PackJob j0, PackJob j1, uint32_t p) {
+// Both operands of a GEMM in one launch (blockIdx.z = job), 64 x 64 tiles of
+// the packed (rows x ldd) int8 output per CTA, 16-byte vector stores.  Not
+// transposed: thread = 16 consecutive k of one row (4 x 16-byte loads).
+// Transposed (src is K x rows): the tile goes through shared memory, loads
+// 16-byte along rows of src, stores 16 bytes along k.  Unaligned operands
+// take scalar loads (same tiles).
+__device__ __forceinline__ uint32_t pack4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t p) {
+    return (uint32_t)(uint8_t)center(a, p) | ((uint32_t)(uint8_t)center(b, p) << 8) |
+           ((uint32_t)(uint8_t)center(c, p) << 16) | ((uint32_t)(uint8_t)center(d, p) << 24);
+}
+__global__ void __launch_bounds__(256) k_pack2(PackJob j0, PackJob j1, uint32_t p) {
     FFB_PDL_ENTRY();
     const PackJob& j = blockIdx.z == 0 ? j0 : j1;
-    __shared__ int8_t tile[32][33];
-    const int64_t i0 = (int64_t)blockIdx.y * 32, k0 = (int64_t)blockIdx.x * 32;
+    __shared__ __align__(16) uint8_t tile[64][64 + 16];
+    const int64_t i0 = (int64_t)blockIdx.y * 64, k0 = (int64_t)blockIdx.x * 64;
     if (i0 >= j.rows || k0 >= j.ldd) return;  // uniform per block
+    const int t = threadIdx.x;
+    const bool vec = ((j.lds & 3) == 0) && ((((uintptr_t)j.src) & 15) == 0);
     if (!j.trans) {
-        for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
-            const int64_t i = i0 + yy, k = k0 + threadIdx.x;
-            if (i < j.rows && k < j.ldd)
-                j.dst[i * j.ldd + k] = (k < j.K) ? center(j.src[i * j.lds + k], p) : (int8_t)0;
+        const int64_t i = i0 + (t >> 2), k = k0 + 16 * (t & 3);
+        if (i >= j.rows || k >= j.ldd) return;
+        uint32_t v[16];
+        const uint32_t* sp = j.src + i * j.lds + k;
+        if (vec && k + 16 <= j.K) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint4 w = __ldcg(reinterpret_cast<const uint4*>(sp) + q);
+                v[4 * q] = w.x, v[4 * q + 1] = w.y, v[4 * q + 2] = w.z, v[4 * q + 3] = w.w;
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = (k + e < j.K) ? sp[e] : 0u;
         }
+        uint4 o;
+        o.x = pack4(v[0], v[1], v[2], v[3], p);
+        o.y = pack4(v[4], v[5], v[6], v[7], p);
+        o.z = pack4(v[8], v[9], v[10], v[11], p);
+        o.w = pack4(v[12], v[13], v[14], v[15], p);
+        *reinterpret_cast<uint4*>(j.dst + i * j.ldd + k) = o;  // ldd, k multiples of 16
         return;
     }
-    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
-        const int64_t k = k0 + yy, i = i0 + threadIdx.x;
-        tile[yy][threadIdx.x] = (k < j.K && i < j.rows) ? center(j.src[k * j.lds + i], p) : (int8_t)0;
+    // transposed: tile[kk][ii] = center(src[k0 + kk][i0 + ii])
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int kk = (t >> 4) + 16 * u, ii = 4 * (t & 15);
+        const int64_t k = k0 + kk, i = i0 + ii;
+        uint32_t w[4];
+        const uint32_t* sp = j.src + k * j.lds + i;
+        if (vec && k < j.K && i + 4 <= j.rows) {
+            const uint4 x = __ldcg(reinterpret_cast<const uint4*>(sp));
+            w[0] = x.x, w[1] = x.y, w[2] = x.z, w[3] = x.w;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) w[e] = (k < j.K && i + e < j.rows) ? sp[e] : 0u;
+        }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) tile[kk][ii + e] = (uint8_t)center(w[e], p);
     }
     __syncthreads();
-    for (int yy = threadIdx.y; yy < 32; yy += blockDim.y) {
-        const int64_t i = i0 + yy, k = k0 + threadIdx.x;
-        if (i < j.rows && k < j.ldd) j.dst[i * j.ldd + k] = tile[threadIdx.x][yy];
-    }
+    const int ii = t >> 2, ks = 16 * (t & 3);
+    const int64_t i = i0 + ii, k = k0 + ks;
+    if (i >= j.rows || k >= j.ldd) return;
+    uint32_t o[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+        o[q] = (uint32_t)tile[ks + 4 * q][ii] | ((uint32_t)tile[ks + 4 * q + 1][ii] << 8) |
+               ((uint32_t)tile[ks + 4 * q + 2][ii] << 16) | ((uint32_t)tile[ks + 4 * q + 3][ii] << 24);
+    *reinterpret_cast<uint4*>(j.dst + i * j.ldd + k) = make_uint4(o[0], o[1], o[2], o[3]);
 }
 
 // not transposed: op(src)[i][k] = src[i][k]
@@ -691,9 +909,9 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
         // B^T (N x K) is needed: transposed pack unless tb
         PackJob ja{Ap, Kp, A.ptr, A.ld, M, K, ta ? 1 : 0}, jb{Bp, Kp, B.ptr, B.ld, N, K, tb ? 0 : 1};
         const int64_t rmax = std::max(M, N);
-        if (rmax <= (int64_t)65535 * 32) {
-            dim3 grid((unsigned)cdiv(Kp, 32), (unsigned)cdiv(rmax, 32), 2);
-            launch_k(k_pack2, grid, dim3(32, 8), 0, st, ja, jb, f.p);
+        if (rmax <= (int64_t)65535 * 64) {
+            dim3 grid((unsigned)cdiv(Kp, 64), (unsigned)cdiv(rmax, 64), 2);
+            launch_k(k_pack2, grid, 256, 0, st, ja, jb, f.p);
             ++g_launches;
             FFB_CHECK_LAUNCH();
         } else {
@@ -707,6 +925,22 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
     if (nk <= 2) {  // short K: epilogue-bound, 2 CTAs per SM (2-stage pipeline)
         CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, 128);
         launch_tc<128, 2>(st, ma, mb, C, M, N, nk, f, mode);
+    } else if (wide && !getenv("FFB_TC_NONPERSISTENT")) {
+        CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, TP_BN);
+        static bool attr = false;
+        static int nsm = 148;
+        if (!attr) {
+            FFB_CUDA(cudaFuncSetAttribute(k_gemm_i8_tcp, cudaFuncAttributeMaxDynamicSharedMemorySize, TpCfg::SMEM));
+            int dev = 0;
+            FFB_CUDA(cudaGetDevice(&dev));
+            FFB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            attr = true;
+        }
+        const int num_m = (int)cdiv(M, TC_BM), num_tiles = num_m * (int)cdiv(N, TP_BN);
+        launch_k(k_gemm_i8_tcp, std::min(num_tiles, nsm), TP_THREADS, TpCfg::SMEM, st, ma, mb, C.ptr, C.ld,
+                 (int)M, (int)N, (int)nk, f, (int)mode, num_m, num_tiles);
+        ++g_launches;
+        FFB_CHECK_LAUNCH();
     } else if (wide) {
         CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, 256);
         launch_tc<256>(st, ma, mb, C, M, N, nk, f, mode);

@@ -81,3 +81,17 @@ def test_tc_limb_gemm(gpu, oracle, m, n, k, p):
     a2 = rng.integers(0, p, (k, n), dtype=np.uint64)
     b2 = rng.integers(0, p, (k, n), dtype=np.uint64)
     assert np.array_equal(ffb.syr2k_sub(c2, a2, b2, p, ctx=gpu), oracle.syr2k_sub(p, c2, a2, b2))
+
+
+@pytest.mark.parametrize("m,n,k", [(2048, 2560, 512), (3000, 2000, 300), (1100, 4400, 1000)])
+@pytest.mark.parametrize("p", [131, 2])
+def test_tc_gemm_persistent(gpu, oracle, m, n, k, p, monkeypatch):
+    """The persistent tcgen05 kernel (128x256 tiles, double-buffered TMEM accumulators):
+    large outputs with partial M/N tiles and K not a multiple of the 128-byte stage."""
+    import paper_1802_10453_b200 as ffb
+    monkeypatch.setenv("FFB_GEMM_PATH", "tc")
+    rng = np.random.default_rng(m + n + k + p)
+    a = rng.integers(0, p, (m, k), dtype=np.uint64)
+    b = rng.integers(0, p, (k, n), dtype=np.uint64)
+    c = rng.integers(0, p, (m, n), dtype=np.uint64)
+    assert np.array_equal(ffb.gemm_sub(c, a, b, p, ctx=gpu), oracle.gemm_sub(p, c, a, b))
