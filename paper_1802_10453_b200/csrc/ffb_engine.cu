@@ -539,8 +539,7 @@ struct Engine {
         //   Z rows (col_perm order):  even <- [G1; G2], odd <- [U1^T; V1^T]
         scatter_lg(st, Lg, up[1], coff, 2, py.L);
         const int32_t* didz = up[2];
-        scatter_lg(st, Lg, didz, coff, 2, G12);
-        scatter_lg(st, Lg, didz, coff + 1, 2, UpT);
+        scatter_lg_pair(st, Lg, didz, coff, G12, UpT);  // even <- [G1; G2], odd <- [U1^T; V1^T]
         write_pair_diag(f, st, D, coff, py.d, py.dinv, delta, r);  // :254-260
 
         std::vector<int32_t> rows3(idz.begin() + r, idz.end());

@@ -233,15 +233,33 @@ simt:
 // ===========================================================================
 namespace {
 
+// Row copy d[0..cols) = s[0..cols) by the threads of a grid-x stride loop:
+// 16-byte vectors (two in flight) when both rows are 16-byte aligned.
+__device__ __forceinline__ void copy_row(uint32_t* d, const uint32_t* s, int64_t cols) {
+    const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x;
+    if ((((uintptr_t)d | (uintptr_t)s) & 15) == 0) {
+        const int64_t c4 = cols >> 2;
+        const uint4* s4 = reinterpret_cast<const uint4*>(s);
+        uint4* d4 = reinterpret_cast<uint4*>(d);
+        int64_t j = start;
+        for (; j + step < c4; j += 2 * step) {
+            const uint4 a = __ldcg(s4 + j), b = __ldcg(s4 + j + step);
+            d4[j] = a;
+            d4[j + step] = b;
+        }
+        for (; j < c4; j += step) d4[j] = __ldcg(s4 + j);
+        for (int64_t t = 4 * c4 + start; t < cols; t += step) d[t] = s[t];
+        return;
+    }
+    for (int64_t j = start; j < cols; j += step) d[j] = s[j];
+}
+
 __global__ void k_gather_rows(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
                               const int32_t* idx, int64_t rows, int64_t cols) {
     FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
-    const uint32_t* s = src + (int64_t)idx[i] * lds;
-    uint32_t* d = dst + i * ldd;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
-         j += (int64_t)gridDim.x * blockDim.x)
-        d[j] = s[j];
+    copy_row(dst + i * ldd, src + (int64_t)idx[i] * lds, cols);
 }
 
 // Two independent row gathers in one launch (blockIdx.z): dst[i][j] = src[idx[i]][c0 + j].
@@ -258,11 +276,7 @@ __global__ void k_gather_rows2(RowGather g0, RowGather g1) {
     const RowGather& g = blockIdx.z == 0 ? g0 : g1;
     const int64_t i = blockIdx.y;
     if (i >= g.rows) return;
-    const uint32_t* s = g.src + (int64_t)g.idx[i] * g.lds + g.c0;
-    uint32_t* d = g.dst + i * g.ldd;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < g.cols;
-         j += (int64_t)gridDim.x * blockDim.x)
-        d[j] = s[j];
+    copy_row(g.dst + i * g.ldd, g.src + (int64_t)g.idx[i] * g.lds + g.c0, g.cols);
 }
 
 __global__ void k_gather_sym(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
@@ -299,9 +313,35 @@ __global__ void k_scatter_lg(uint32_t* Lg, int64_t ldl, const int32_t* ids, int6
     const int64_t i = blockIdx.y;
     uint32_t* d = Lg + (int64_t)ids[i] * ldl + col0;
     const uint32_t* s = src + i * lds;
+    if (cstride == 1) {
+        copy_row(d, s, cols);
+        return;
+    }
     for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
          j += (int64_t)gridDim.x * blockDim.x)
         d[j * cstride] = s[j];
+}
+
+// Interleaved pair scatter: Lg[ids[i]][col0 + 2j] = e[i][j], [col0 + 2j + 1] = o[i][j]
+// (the even/odd L columns of the 2x2 pivot pairs, one coalesced 8-byte store each).
+__global__ void k_scatter_lg_pair(uint32_t* Lg, int64_t ldl, const int32_t* ids, int64_t col0,
+                                  const uint32_t* e, int64_t lde, const uint32_t* o, int64_t ldo,
+                                  int64_t cols) {
+    FFB_PDL_ENTRY();
+    const int64_t i = blockIdx.y;
+    uint32_t* d = Lg + (int64_t)ids[i] * ldl + col0;
+    const uint32_t* se = e + i * lde;
+    const uint32_t* so = o + i * ldo;
+    const bool vec = ((((uintptr_t)d) & 7) == 0);
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
+         j += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t a = __ldcg(se + j), b = __ldcg(so + j);
+        if (vec) reinterpret_cast<uint2*>(d)[j] = make_uint2(a, b);
+        else {
+            d[2 * j] = a;
+            d[2 * j + 1] = b;
+        }
+    }
 }
 
 __global__ void k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int64_t ldl,
@@ -526,8 +566,8 @@ __global__ void k_convert_out(T* dst, const uint32_t* src, int64_t lds, int64_t 
         dst[i * cols + j] = (T)src[i * lds + j];
 }
 
-inline dim3 rowgrid(int64_t rows, int64_t cols, int threads = 256) {
-    int64_t gx = cdiv(cols, threads);
+inline dim3 rowgrid(int64_t rows, int64_t cols, int threads = 256, int per_thread = 1) {
+    int64_t gx = cdiv(cdiv(cols, per_thread), threads);
     if (gx > 64) gx = 64;
     if (gx < 1) gx = 1;
     return dim3((unsigned)gx, (unsigned)rows);
@@ -543,7 +583,7 @@ void gather_rows(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
     if (dst.rows <= 0 || dst.cols <= 0) return;
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
-        launch_k(k_gather_rows, rowgrid(nr, dst.cols), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
+        launch_k(k_gather_rows, rowgrid(nr, dst.cols, 256, 4), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
                                                              src.ld, idx + r0, nr, dst.cols);
         count_launch();
     }
@@ -584,6 +624,18 @@ void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int 
     FFB_CHECK_LAUNCH();
 }
 
+void scatter_lg_pair(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, DMat even, DMat odd) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
+    if (even.rows <= 0 || even.cols <= 0) return;
+    for (int64_t r0 = 0; r0 < even.rows; r0 += FFB_ROWCHUNK) {
+        const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, even.rows - r0);
+        launch_k(k_scatter_lg_pair, rowgrid(nr, even.cols), 256, 0, st, Lg.ptr, Lg.ld, ids + r0, col0,
+                 even.ptr + r0 * even.ld, even.ld, odd.ptr + r0 * odd.ld, odd.ld, even.cols);
+        count_launch();
+    }
+    FFB_CHECK_LAUNCH();
+}
+
 void gather_rows2(cudaStream_t st, DMat d0, DMat s0, const int32_t* i0, int64_t c0, DMat d1, DMat s1,
                   const int32_t* i1, int64_t c1) {
     const int64_t rows = std::max(d0.rows, d1.rows), cols = std::max(d0.cols, d1.cols);
@@ -596,7 +648,7 @@ void gather_rows2(cudaStream_t st, DMat d0, DMat s0, const int32_t* i0, int64_t 
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     RowGather g0{d0.ptr, d0.ld, s0.ptr, s0.ld, i0, c0, d0.cols > 0 ? d0.rows : 0, d0.cols};
     RowGather g1{d1.ptr, d1.ld, s1.ptr, s1.ld, i1, c1, d1.cols > 0 ? d1.rows : 0, d1.cols};
-    dim3 g = rowgrid(rows, cols);
+    dim3 g = rowgrid(rows, cols, 256, 4);
     g.z = 2;
     launch_k(k_gather_rows2, g, 256, 0, st, g0, g1);
     count_launch();

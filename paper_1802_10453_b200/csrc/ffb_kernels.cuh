@@ -84,6 +84,8 @@ void gather_sym(cudaStream_t st, DMat dst, DMat src, const int32_t* idx);
 // dst (cols x rows) = src^T
 void transpose(cudaStream_t st, DMat dst, DMat src);
 // Lg[ids[i]][col0 + j*cstride] = src[i][j]
+// Lg[ids[i]][col0 + 2j] = even[i][j], Lg[ids[i]][col0 + 2j + 1] = odd[i][j]
+void scatter_lg_pair(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, DMat even, DMat odd);
 void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int cstride, DMat src);
 // dst[i][k] = Lg[ids[i]][col0 + k]
 void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t col0);
