@@ -367,4 +367,26 @@ struct Fp16 {
         return a >= b ? a - b : a + p - b;
     }
 };
+// Field arithmetic selector: 32-bit Barrett for p < 2^16, 64-bit otherwise.
+template <bool kSmall>
+struct Ar;
+template <>
+struct Ar<true> {
+    Fp16 h;
+    Fp f;
+    __device__ explicit Ar(const Fp& ff) : h(ff.p), f(ff) {}
+    __device__ __forceinline__ uint32_t mul(uint32_t a, uint32_t b) const { return h.mul(a, b); }
+    __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const { return h.sub(a, b); }
+    __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) const { return fadd(f, a, b); }
+};
+template <>
+struct Ar<false> {
+    Fp f;
+    __device__ explicit Ar(const Fp& ff) : f(ff) {}
+    __device__ __forceinline__ uint32_t mul(uint32_t a, uint32_t b) const { return fmul(f, a, b); }
+    __device__ __forceinline__ uint32_t sub(uint32_t a, uint32_t b) const { return fsub(f, a, b); }
+    __device__ __forceinline__ uint32_t add(uint32_t a, uint32_t b) const { return fadd(f, a, b); }
+};
+
 }  // namespace ffb
+

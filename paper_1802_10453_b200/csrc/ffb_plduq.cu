@@ -524,6 +524,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t off[1025];
     __shared__ int32_t Js[CRP_KMAX], rho[CRP_KMAX], pci[CRP_KMAX], pcv[CRP_KMAX], sig[CRP_KMAX], Is[CRP_KMAX];
+    __shared__ int lead8[2][8];
     __shared__ uint32_t dinv[CRP_KMAX];
     __shared__ unsigned fmask[2];
     __shared__ BatchScratch bs;
@@ -591,17 +592,23 @@ __global__ void __launch_bounds__(256) k_crp_finish(
             }
         }
     __syncthreads();
-    // 2. row-order leftmost elimination on M, tracking L^-1 in G
+    // 2. row-order leftmost elimination on M, tracking L^-1 in G.  The leading
+    //    entry of row t: each thread scans a strided slice, warps reduce, one
+    //    barrier combines (lead8 rotates over 2 slots, so no reset barrier).
     for (int t = 0; t < k; ++t) {
         const uint32_t* rt = M + (size_t)t * Cx;
-        int jp = Cx;
-        for (int j0 = 0; j0 < Cx; j0 += 32) {
-            const unsigned bal = __ballot_sync(0xffffffffu, j0 + lane < Cx && rt[j0 + lane] != 0);
-            if (bal) {
-                jp = j0 + __ffs(bal) - 1;
+        int mine = Cx;
+        for (int j = tid; j < Cx; j += 256)
+            if (rt[j] != 0) {
+                mine = j;
                 break;
             }
-        }
+        mine = __reduce_min_sync(0xffffffffu, mine);
+        if (lane == 0) lead8[t & 1][wp] = mine;
+        __syncthreads();
+        int jp = lead8[t & 1][0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) jp = min(jp, lead8[t & 1][w]);
         if (jp >= Cx) {
             if (tid == 0) *fail = 1;
             return;
@@ -826,13 +833,16 @@ __global__ void k_m1_pattern(const uint32_t* M1, int64_t ldm, const int32_t* np,
 // LDU without pivoting of a <= 64 x 64 block in place (1 CTA):
 // strict lower <- L, diagonal <- d, strict upper <- U.
 // ---------------------------------------------------------------------------
+template <bool kSmall>
 __global__ void __launch_bounds__(256) k_ldu_base(Fp f, uint32_t* K, int64_t ldk, int n,
                                                   int32_t* fail) {
     FFB_PDL_ENTRY();
     // Register ownership as in the leaf: thread (ty, tx) holds K[ty + 4q][tx].
     // Step t broadcasts column t and row t (double-buffered) with one barrier.
+    // kSmall: 32-bit Barrett arithmetic (p < 2^16), no 64-bit path in the loop.
     __shared__ uint32_t colb[2][64], rowb[2][64];
     __shared__ uint32_t sinv[SINV_MAX];
+    const Ar<kSmall> ar(f);
     const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6;
     uint32_t A[16];
 #pragma unroll
@@ -856,16 +866,15 @@ __global__ void __launch_bounds__(256) k_ldu_base(Fp f, uint32_t* K, int64_t ldk
             return;  // uniform
         }
         const uint32_t di = inv(f, d);
-        const uint32_t uj = fmul(f, rb[tx], di);  // U[t][tx] for tx > t
+        const uint32_t uj = ar.mul(rb[tx], di);  // U[t][tx] for tx > t
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const int i = ty + 4 * q;
-            if (i > t) {
-                if (tx > t) A[q] = fsub(f, A[q], fmul(f, cb[i], uj));
-                else if (tx == t) A[q] = fmul(f, cb[i], di);  // L[i][t]
-            } else if (i == t && tx > t) {
-                A[q] = uj;  // U[t][tx]
-            }
+            const uint32_t ci = cb[i];
+            const uint32_t upd = ar.sub(A[q], ar.mul(ci, uj));
+            const uint32_t lij = ar.mul(ci, di);
+            // i > t: trailing update (tx > t) or L[i][t] (tx == t); i == t: U[t][tx] (tx > t)
+            A[q] = i > t ? (tx > t ? upd : (tx == t ? lij : A[q])) : ((i == t && tx > t) ? uj : A[q]);
         }
     }
 #pragma unroll
@@ -926,7 +935,10 @@ void ldu_inplace(const Fp& f, cudaStream_t st, DMat K, Workspace& ws, int32_t* f
     if (n <= 0) return;
     if (n <= 64) {
         ProfScope ps(K_LDU, st, 2.0 * n * n * n / 3.0, 8.0 * n * n);
-        launch_k(k_ldu_base, 1, 256, 0, st, f, K.ptr, K.ld, (int)n, fail);
+        if (f.p < 65536u)
+            launch_k(k_ldu_base<true>, 1, 256, 0, st, f, K.ptr, K.ld, (int)n, fail);
+        else
+            launch_k(k_ldu_base<false>, 1, 256, 0, st, f, K.ptr, K.ld, (int)n, fail);
         count_launch();
         FFB_CHECK_LAUNCH();
         return;
