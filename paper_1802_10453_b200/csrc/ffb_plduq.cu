@@ -578,15 +578,15 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     }
     for (int e = tid; e < k * k; e += 256) G[e] = (e / k == e % k) ? 1 % f.p : 0u;
     for (int i = wp; i < k; i += 8)
-        for (int j0 = lane; j0 < Cx; j0 += 128) {
-            uint32_t vv[4];
+        for (int j0 = lane; j0 < Cx; j0 += 512) {  // 16 scattered loads in flight per lane
+            uint32_t vv[16];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 16; ++u) {
                 const int j = j0 + 32 * u;
                 vv[u] = j < Cx ? __ldcg(RI + (int64_t)i * ldr + ids[j]) : 0u;
             }
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
+            for (int u = 0; u < 16; ++u) {
                 const int j = j0 + 32 * u;
                 if (j < Cx) M[(size_t)i * Cx + j] = vv[u];
             }
