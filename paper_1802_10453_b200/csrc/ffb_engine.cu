@@ -205,8 +205,12 @@ std::array<const int32_t*, N> upload_batch(ffb_context* c, const std::array<cons
 __global__ void __launch_bounds__(1024) k_post(const uint32_t* src, uint32_t* dst, int64_t words,
                                                volatile uint32_t* seq_ptr, uint32_t seq) {
     FFB_PDL_ENTRY();
-    for (int64_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldcg(src + i);
-    __threadfence_system();
+    // 16-byte stores over the bus where aligned, then one system-scope fence by
+    // the publishing thread (cumulative over the block's writes via the barrier)
+    const int64_t w4 = ((((uintptr_t)src) & 15) == 0) ? words >> 2 : 0;
+    for (int64_t i = threadIdx.x; i < w4; i += blockDim.x)
+        reinterpret_cast<uint4*>(dst)[i] = __ldcg(reinterpret_cast<const uint4*>(src) + i);
+    for (int64_t i = 4 * w4 + threadIdx.x; i < words; i += blockDim.x) dst[i] = __ldcg(src + i);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
@@ -219,8 +223,10 @@ const void* readback(ffb_context* c, const void* dev, size_t bytes) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!dma && bytes <= c->mbox_cap && (bytes & 3) == 0 && (((uintptr_t)dev) & 3) == 0) {
         const uint32_t seq = ++c->mbox_seq;
-        launch_k(k_post, 1, 1024, 0, c->stream, (const uint32_t*)dev, c->mbox_dev, (int64_t)(bytes / 4),
-                 c->mbox_seq_dev, seq);
+        const int64_t words = (int64_t)(bytes / 4);
+        const int threads = (int)std::min<int64_t>(1024, std::max<int64_t>(32, (cdiv(words, 4) + 31) / 32 * 32));
+        launch_k(k_post, 1, threads, 0, c->stream, (const uint32_t*)dev, c->mbox_dev, words, c->mbox_seq_dev,
+                 seq);
         volatile uint32_t* hs = c->mbox_seq_host;
         for (uint64_t spin = 1; *hs != seq; ++spin)
             if ((spin & 0xFFFF) == 0) {  // surface device faults instead of spinning forever
