@@ -171,17 +171,14 @@ __device__ __forceinline__ uint32_t dot_lt(const Fp& f, const uint32_t* a, int s
     }
     return red64(f, acc);
 }
+// X = inverse of the unit lower nb x nb block at Tb (nb <= 64, identity beyond),
+// in shared memory; Ts is scratch (W = C A^-1 of a level lives transposed in its
+// upper triangle).  All 256 threads; ends with a barrier.
 template <int kMode>
-__global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* T, int64_t ldt,
-                                                 int64_t n, uint32_t* Tinv) {
-    FFB_PDL_ENTRY();
-    __shared__ uint32_t Ts[64][65];
-    __shared__ uint32_t X[64][65];  // W = C A^-1 of a level is kept transposed in Ts's upper triangle
-    const int b = blockIdx.x;
-    const int64_t i0 = (int64_t)b * 64;
-    const int nb = (int)std::min<int64_t>(64, n - i0);
+__device__ __forceinline__ void trinv64_block(const Fp& f, const uint32_t* Tb, int64_t ldt, int nb,
+                                              uint32_t (*Ts)[65], uint32_t (*X)[65]) {
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-    load_tile<16>(&Ts[0][0], 65, T + i0 * ldt + i0, ldt, nb, nb);
+    load_tile<16>(&Ts[0][0], 65, Tb, ldt, nb, nb);
     __syncthreads();
     for (int e = tid; e < 64 * 64; e += 256) {
         const int i = e >> 6, k = e & 63;
@@ -225,8 +222,57 @@ __global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* T, int64_
         }
         __syncthreads();
     }
+}
+
+template <int kMode>
+__global__ void __launch_bounds__(256) k_trinv64(Fp f, const uint32_t* T, int64_t ldt,
+                                                 int64_t n, uint32_t* Tinv) {
+    FFB_PDL_ENTRY();
+    __shared__ uint32_t Ts[64][65];
+    __shared__ uint32_t X[64][65];
+    const int b = blockIdx.x;
+    const int64_t i0 = (int64_t)b * 64;
+    const int nb = (int)std::min<int64_t>(64, n - i0);
+    const int tid = threadIdx.x;
+    trinv64_block<kMode>(f, T + i0 * ldt + i0, ldt, nb, Ts, X);
     uint32_t* o = Tinv + (int64_t)b * 64 * 64;
     for (int e = tid; e < 64 * 64; e += 256) o[e] = X[e >> 6][e & 63];
+}
+
+// Unit lower solve for n <= 64 in one launch: every CTA inverts the block in
+// shared memory (as k_trinv64) and applies it to its 64-column tile of B,
+// X = T^-1 B, with register-blocked dot products (thread: one column, 16 rows).
+template <int kMode>
+__global__ void __launch_bounds__(256) k_trsm_small(Fp f, const uint32_t* T, int64_t ldt, int n, uint32_t* B,
+                                                    int64_t ldb, int64_t ncols) {
+    FFB_PDL_ENTRY();
+    __shared__ uint32_t Ts[64][65];
+    __shared__ uint32_t X[64][65];
+    const int tid = threadIdx.x;
+    trinv64_block<kMode>(f, T, ldt, n, Ts, X);
+    const int64_t c0 = (int64_t)blockIdx.x * 64;
+    const int bc = (int)std::min<int64_t>(64, ncols - c0);
+    load_tile<16>(&Ts[0][0], 65, B + c0, ldb, n, bc);  // Ts is free now: the B tile
+    __syncthreads();
+    const int j = tid & 63, i0 = tid >> 6;  // a warp shares its rows: X[i][k] is a broadcast
+    uint64_t acc[16];
+#pragma unroll
+    for (int q = 0; q < 16; ++q) acc[q] = 0;
+    for (int k = 0; k < n; ++k) {
+        const uint32_t bk = Ts[k][j];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const uint64_t prod = (uint64_t)X[i0 + 4 * q][k] * bk;  // X is lower: zero for k > i
+            acc[q] = kMode == 2 ? (uint64_t)red64(f, acc[q] + prod) : acc[q] + prod;
+        }
+    }
+    if (j < bc) {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int i = i0 + 4 * q;
+            if (i < n) B[(int64_t)i * ldb + c0 + j] = red64(f, acc[q]);
+        }
+    }
 }
 
 // Panel solve: rows [r0, r0 + nb) (nb <= 256, 64-aligned r0), column tile of
@@ -498,6 +544,17 @@ void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, 
 void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
     const int64_t n = T.rows;
     if (n <= 0 || B.cols <= 0) return;
+    if (n <= 64) {  // one launch: inverse and apply per 64-column tile
+        ProfScope ps(K_TRSM, st, (double)n * n * B.cols, 8.0 * n * B.cols, n, B.cols, 2);
+        const unsigned g = (unsigned)cdiv(B.cols, 64);
+        if (f.p < 4096u) launch_k(k_trsm_small<0>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
+        else if (f.p < (1u << 23))
+            launch_k(k_trsm_small<1>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
+        else launch_k(k_trsm_small<2>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
+        ++g_launches;
+        FFB_CHECK_LAUNCH();
+        return;
+    }
     const int64_t nblk = cdiv(n, 64);
     uint32_t* Tinv = trsm_scratch((size_t)nblk * 64 * 64);
     {
