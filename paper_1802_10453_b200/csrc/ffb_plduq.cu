@@ -376,12 +376,39 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
     __shared__ unsigned fmask[2];
     __shared__ BatchScratch bs;
     __shared__ uint32_t sinv[SINV_MAX];
+    __shared__ int32_t nzc[CRP_W];  // the block's nonzero columns, ascending
+    __shared__ int wcnt[CRP_W / 32];
     const int g = blockIdx.x;
     const int64_t c0 = (int64_t)g * CRP_W;
     const int total = (int)std::min<int64_t>(CRP_W, n - c0);
     const SmemInv inv = stage_inverses(f, sinv);
-    const int nb = crp_scan(f, inv, RI, ldr, k, total, [c0](int idx) { return (int32_t)(c0 + idx); }, E, V,
-                            VC, rho, fmask, bs, out + (int64_t)g * k);
+    // all-zero columns never enter the CRP: compact the nonzero ones (thread = column,
+    // all k loads in flight), so the scan below visits only those
+    {
+        const int t = threadIdx.x, lane = t & 31, wp = t >> 5;
+        int nz = 0;
+        if (t < total) {
+            const uint32_t* col = RI + c0 + t;
+            for (int i0 = 0; i0 < k; i0 += 16) {
+                uint32_t v[16];
+#pragma unroll
+                for (int u = 0; u < 16; ++u) v[u] = i0 + u < k ? __ldcg(col + (int64_t)(i0 + u) * ldr) : 0u;
+#pragma unroll
+                for (int u = 0; u < 16; ++u) nz |= v[u] != 0;
+            }
+        }
+        const unsigned bal = __ballot_sync(0xffffffffu, nz);
+        if (lane == 0) wcnt[wp] = __popc(bal);
+        __syncthreads();
+        int base = 0;
+        for (int w = 0; w < wp; ++w) base += wcnt[w];
+        if (nz) nzc[base + __popc(bal & ((1u << lane) - 1))] = (int32_t)(c0 + t);
+        __syncthreads();
+    }
+    int cnt = 0;
+    for (int w = 0; w < CRP_W / 32; ++w) cnt += wcnt[w];
+    const int nb = crp_scan(f, inv, RI, ldr, k, cnt, [&](int idx) { return nzc[idx]; }, E, V, VC, rho, fmask, bs,
+                            out + (int64_t)g * k);
     if (threadIdx.x == 0) ocount[g] = nb;
 }
 
