@@ -536,20 +536,30 @@ __global__ void __launch_bounds__(256) k_crp_rowelim(Fp f, const uint32_t* RI, i
 // dynamic smem: G (k^2) + max(rc_cap = min(k nblk k, CF_RC_WORDS), scan buffers)
 constexpr int CF_RC_WORDS = 32 * 1024;
 constexpr int CF_SMEM_WORDS = CRP_KMAX * CRP_KMAX + CF_RC_WORDS;
-__host__ __device__ inline size_t cf_smem_bytes(int k, int nblk, int* rc_cap) {
+// si_off: word offset of a dedicated S_I region (early copy) when everything fits
+// in 190 KB of dynamic smem, else -1 (S_I staged late into the free M buffer)
+__host__ __device__ inline size_t cf_smem_bytes(int k, int nblk, int* rc_cap, int* si_off) {
     *rc_cap = (int)std::min<int64_t>((int64_t)k * nblk * k, CF_RC_WORDS);
     const size_t scan = (size_t)(CRP_KMAX + CRP_G) * k + CRP_G * CRP_KMAX;
     const size_t sketch = (size_t)k * RD_S;  // staged S_I rows
-    return ((size_t)k * k + std::max<size_t>(std::max<size_t>((size_t)*rc_cap, scan), sketch)) * 4;
+    const size_t base = (size_t)k * k + std::max<size_t>(std::max<size_t>((size_t)*rc_cap, scan), sketch);
+    const size_t base4 = (base + 3) & ~(size_t)3;  // 16-byte aligned S_I region
+    if ((base4 + sketch) * 4 <= (size_t)190 * 1024) {
+        *si_off = (int)base4;
+        return (base4 + sketch) * 4;
+    }
+    *si_off = -1;
+    return base * 4;
 }
 __global__ void __launch_bounds__(256) k_crp_finish(
     Fp f, const uint32_t* RI, int64_t ldr, int k, const int32_t* lists,
-    const int32_t* counts, int nblk, int32_t* cand, int rc_cap, const int32_t* I, int64_t c0,
+    const int32_t* counts, int nblk, int32_t* cand_g, int rc_cap, const int32_t* I, int64_t c0,
     const uint32_t* S, int64_t lds, int s, uint32_t* Kinv, int32_t* Jout, uint32_t* UO, int64_t lduo,
-    int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r, int32_t* fail) {
+    int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r, int32_t* fail, int si_off) {
     FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t off[1025];
+    __shared__ int32_t cand_s[2048];  // candidate list in smem when it fits
     __shared__ int32_t Js[CRP_KMAX], rho[CRP_KMAX], pci[CRP_KMAX], pcv[CRP_KMAX], sig[CRP_KMAX], Is[CRP_KMAX];
     __shared__ int lead8[2][8];
     __shared__ uint32_t dinv[CRP_KMAX];
@@ -576,6 +586,22 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     }
     for (int t = tid; t < k; t += 256) Is[t] = I ? I[t] : 0;
     __syncthreads();
+    // the k sketch rows S_I depend only on the inputs: start their copy now
+    // (16-byte cp.async.cg into a dedicated region), consumed by the UO phase
+    const bool si_early = S && si_off >= 0 && ((lds & 3) == 0) && ((s & 3) == 0) &&
+                          ((((uintptr_t)S) & 15) == 0);
+    if (si_early) {
+        const int s4 = s >> 2;
+        for (int e = tid; e < k * s4; e += 256) {
+            const int u = e / s4, q = e - u * s4;
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(sm + si_off + (size_t)u * s + 4 * q)),
+                         "l"(S + (int64_t)Is[u] * lds + 4 * q));
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    }
+    const int C = total;
+    int32_t* cand = C <= 2048 ? cand_s : cand_g;
     for (int b = wp; b < nblk; b += 8) {
         const int cb = counts[b], ob = off[b];
         for (int q = lane; q < cb; q += 32) cand[ob + q] = lists[(int64_t)b * k + q];
@@ -585,7 +611,6 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     //    (Cx = C, ids = cand), else R_I on J = its column rank profile over the
     //    candidates, found by the batched scan (Cx = k, ids = Js): the RPM of R_I
     //    is the RPM of M either way, every other column depending on earlier ones
-    const int C = total;
     uint32_t* G = sm;                   // k x k: L^-1, then U'^-1 L^-1
     uint32_t* M = sm + (size_t)k * k;
     const bool direct = k * C <= rc_cap;
@@ -604,20 +629,14 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         __syncthreads();
     }
     for (int e = tid; e < k * k; e += 256) G[e] = (e / k == e % k) ? 1 % f.p : 0u;
-    for (int i = wp; i < k; i += 8)
-        for (int j0 = lane; j0 < Cx; j0 += 512) {  // 16 scattered loads in flight per lane
-            uint32_t vv[16];
-#pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const int j = j0 + 32 * u;
-                vv[u] = j < Cx ? __ldcg(RI + (int64_t)i * ldr + ids[j]) : 0u;
-            }
-#pragma unroll
-            for (int u = 0; u < 16; ++u) {
-                const int j = j0 + 32 * u;
-                if (j < Cx) M[(size_t)i * Cx + j] = vv[u];
-            }
-        }
+    for (int e = tid; e < k * Cx; e += 256) {  // scattered gather, every copy in flight
+        const int i = e / Cx, j = e - i * Cx;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(M + (size_t)i * Cx + j)),
+                     "l"(RI + (int64_t)i * ldr + ids[j]));
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
     // 2. row-order leftmost elimination on M, tracking L^-1 in G.  The leading
     //    entry of row t: each thread scans a strided slice, warps reduce, one
@@ -688,10 +707,11 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         const int t = e / k, j = e - t * k;
         Kinv[(int64_t)sig[t] * k + j] = G[e];
     }
-    if (S) {  // UO rows: stage the k sketch rows S_I (coalesced) in the free M buffer
-        uint32_t* SI = M;
-        for (int u = wp; u < k; u += 8)
-            for (int col = lane; col < s; col += 32) SI[(size_t)u * s + col] = __ldcg(S + (int64_t)Is[u] * lds + col);
+    if (S) {  // UO rows from the k sketch rows S_I (copied early, or staged now in the free M buffer)
+        uint32_t* SI = si_early ? sm + si_off : M;
+        if (!si_early)
+            for (int u = wp; u < k; u += 8)
+                for (int col = lane; col < s; col += 32) SI[(size_t)u * s + col] = __ldcg(S + (int64_t)Is[u] * lds + col);
         __syncthreads();
         for (int e = tid; e < k * s; e += 256) {
             const int t = e / s, col = e - t * s;
@@ -1157,13 +1177,13 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 {
                     ProfScope ps(K_PQ_ROWELIM, st, 0.0, 0.0);
                     // RPM of R_I on the candidates, Kinv and bookkeeping (1 CTA)
-                    int rc_cap;
-                    const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap);
+                    int rc_cap, si_off;
+                    const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap, &si_off);
                     DMat Kik = Kinv.sub(0, 0, k, k);
                     launch_k(k_crp_finish, 1, 256, cfmem, st, f, RI.ptr, RI.ld, k, lists[0], counts[0], nblk0,
                                                         (int32_t*)re_scratch, rc_cap, dI, c0, Sc.ptr, Sc.ld, SK,
                                                         Kik.ptr, lists[1], UO.ptr, UO.ld, d_uhat_col,
-                                                        d_prow, d_pcol, r, dflag);
+                                                        d_prow, d_pcol, r, dflag, si_off);
                     ++g_launches;
                     FFB_CHECK_LAUNCH();
                 }
@@ -1349,11 +1369,11 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
             launch_k(k_crp_list, nblk0, 256, crp_smem, st, f, d_in, n, k, n, lists0, counts0);
             FFB_CUDA(cudaEventRecord(e[1], st));
             {
-                int rc_cap;
-                const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap);
+                int rc_cap, si_off;
+                const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap, &si_off);
                 launch_k(k_crp_finish, 1, 256, cfmem, st, f, d_in, n, k, lists0, counts0, nblk0, (int32_t*)re_scratch,
                                                     rc_cap, dI, 0, nullptr, 0, 0, Kinv, lists1, nullptr, 0, ucol,
-                                                    prow, pcol, 0, flag);
+                                                    prow, pcol, 0, flag, si_off);
             }
             FFB_CUDA(cudaEventRecord(e[2], st));
             FFB_CUDA(cudaEventRecord(e[3], st));
