@@ -267,6 +267,16 @@ struct TpCfg {
     static constexpr int EPI_BYTES = TP_EPI_WARPS * 32 * 33 * 4;
     static constexpr int SMEM = 1024 + TP_STAGES * STAGE_BYTES + EPI_BYTES + 256;
 };
+// Grouped raster: groups of TP_GM M-tiles, N walking inside a group, so the
+// ~148 tiles in flight touch TP_GM A tiles and ~148/TP_GM B tiles (an L2-resident
+// working set) instead of every A tile per wave.
+constexpr int TP_GM = 16;
+__device__ __forceinline__ void tp_tile(int t, int num_m, int num_n, int& m_blk, int& n_blk) {
+    const int per = TP_GM * num_n, g = t / per, r = t - g * per;
+    const int gm = min(TP_GM, num_m - g * TP_GM);
+    m_blk = g * TP_GM + r % gm;
+    n_blk = r / gm;
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
@@ -274,6 +284,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 __global__ void __launch_bounds__(TP_THREADS, 1)
     k_gemm_i8_tcp(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   uint32_t* C, int64_t ldc, int M, int N, int nk, Fp f, int mode, int num_m, int num_tiles) {
+    const int num_n = num_tiles / num_m;
     FFB_PDL_ENTRY();
     extern __shared__ __align__(1024) uint8_t tp_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)tp_raw + 1023) & ~(uintptr_t)1023);
@@ -317,7 +328,9 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
             int s = 0;
             uint32_t ph = 0;
             for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-                const int m0 = (t % num_m) * TC_BM, n0 = (t / num_m) * TP_BN;
+                int mb, nbk;
+                tp_tile(t, num_m, num_n, mb, nbk);
+                const int m0 = mb * TC_BM, n0 = nbk * TP_BN;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
                     mbar_expect_tx(&full[s], TpCfg::STAGE_BYTES);
@@ -369,7 +382,9 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
         uint32_t aph = 0;
         uint32_t cv[32];
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
-            const int m0 = (t % num_m) * TC_BM, n0 = (t / num_m) * TP_BN + 128 * h;
+            int mb, nbk;
+            tp_tile(t, num_m, num_n, mb, nbk);
+            const int m0 = mb * TC_BM, n0 = nbk * TP_BN + 128 * h;
             const int rbase = m0 + 32 * q;
             auto load_c = [&](int c) {
                 const int col = n0 + c + lane;
