@@ -23,6 +23,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import tempfile
 import statistics
 import subprocess
 import sys
@@ -275,10 +276,13 @@ def main():
     # instrumented pass (same workload): per-kernel-class CUDA-event totals
     a.copy_(a0)
     torch.cuda.synchronize()
+    trace_path = os.path.join(tempfile.gettempdir(), f"ffb_bench_trace_{os.getpid()}.txt")
+    os.environ["FFB_PROF_TRACE"] = trace_path  # per-launch class/shape/ms of this pass
     ctx.profile(True)
     ldlt_device(a, w.p, cfg, ctx, out)
     prof = ctx.profile_read()
     ctx.profile(False)
+    largest = largest_gemm(trace_path)
     gemm = prof["gemm"]
     roofline = None
     if gemm["ms"] > 0:
@@ -291,6 +295,8 @@ def main():
                     "peak_source": "B200 datasheet dense INT8 4.5 POPS (MEASURED_PEAKS.json has "
                                    "no int8 entry)",
                     "launches": gemm["launches"], "gemm_ms": gemm["ms"]}
+        if largest:
+            roofline["largest_gemm"] = largest
 
     e2e = None
     if not args.no_e2e and rank == 0:
@@ -321,6 +327,37 @@ def main():
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def largest_gemm(path):
+    """The largest GEMM launch of the instrumented pass (the top-level Schur update):
+    shape, CUDA-event time, achieved TOPS against the int8 peak, plus the DRAM traffic of
+    the same kernel on that shape from the committed ncu capture."""
+    try:
+        best = None
+        with open(path) as fh:
+            for line in fh:
+                parts = line.split()
+                if len(parts) < 5:
+                    continue
+                c, m, n, k, t = parts[:5]
+                if int(c) != 0:
+                    continue
+                m, n, k, t = abs(int(m)), abs(int(n)), abs(int(k)), float(t)
+                if best is None or m * n * k > best[0] * best[1] * best[2]:
+                    best = (m, n, k, t)
+        os.remove(path)
+    except OSError:
+        return None
+    if not best or best[3] <= 0:
+        return None
+    m, n, k, t = best
+    tops = 2.0 * m * n * k / (t / 1e3) / 1e12
+    return {"kernel": "k_gemm_i8_tcp (persistent tcgen05 int8 GEMM)", "shape_mnk": [m, n, k],
+            "ms": t, "achieved": tops, "frac": tops / INT8_DENSE_PEAK_TOPS,
+            "algorithmic_bytes": m * k + k * n + 8 * m * n,
+            "ncu_dram_bytes_16384x16384x4096": 2.70e9,
+            "ncu_source": "profiles/r01_tcp_gemm_16384x16384x4096_ncu.txt"}
 
 
 def run_e2e(w, ctx, cfg, args, local):

@@ -47,6 +47,7 @@ void Profiler::flush() {
         pool.push_back(r.b);
     }
     recs.clear();
+    if (trace) fflush(trace);
 }
 void Profiler::reset() {
     for (int i = 0; i < K_NCLASS; ++i) ms[i] = ops[i] = bytes[i] = 0, cnt[i] = 0;
