@@ -63,6 +63,17 @@ __global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* C, i
     int acc[4][4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0;
+    // the C values of this thread's epilogue slots (rows wp + 8i, columns lane, lane + 32)
+    // do not depend on the product: load them now, overlapped with the K loop
+    uint32_t cpre[16];
+    const bool direct = gridDim.z == 1 && mode != GEMM_SET;
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t row = m0 + wp + 8 * i, col = n0 + lane + 32 * h;
+            cpre[2 * i + h] = (direct && row < M && col < N) ? __ldcg(C + row * ldc + col) : 0u;
+        }
     fetch(kb);
     for (int64_t k0 = kb; k0 < K; k0 += MM_T) {
         __syncthreads();  // the previous chunk's fragments have been read
@@ -89,7 +100,9 @@ __global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* C, i
             Cs[16 * mt + gid + 8 * (e >> 1)][8 * (nt0 + t) + 2 * tig + (e & 1)] = mma_reduce(f, acc[t][e], bias);
     __syncthreads();
     // coalesced epilogue: warp per row, lanes along the columns
-    for (int r = wp; r < MM_T; r += 8) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int r = wp + 8 * i;
         const int64_t row = m0 + r;
         if (row >= M) break;
 #pragma unroll
@@ -101,9 +114,10 @@ __global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* C, i
                 W[((int64_t)blockIdx.z * M + row) * N + col] = v;
                 continue;
             }
+            const uint32_t c0 = cpre[2 * i + h];
             uint32_t* c = C + row * ldc + col;
-            if (mode == GEMM_SUB) *c = fsub(f, *c, v);
-            else if (mode == GEMM_ADD) *c = fadd(f, *c, v);
+            if (mode == GEMM_SUB) *c = fsub(f, c0, v);
+            else if (mode == GEMM_ADD) *c = fadd(f, c0, v);
             else *c = v;
         }
     }
