@@ -248,11 +248,19 @@ __global__ void __launch_bounds__(256) k_trsm_small(Fp f, const uint32_t* T, int
     FFB_PDL_ENTRY();
     __shared__ uint32_t Ts[64][65];
     __shared__ uint32_t X[64][65];
-    const int tid = threadIdx.x;
-    trinv64_block<kMode>(f, T, ldt, n, Ts, X);
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     const int64_t c0 = (int64_t)blockIdx.x * 64;
     const int bc = (int)std::min<int64_t>(64, ncols - c0);
-    load_tile<16>(&Ts[0][0], 65, B + c0, ldb, n, bc);  // Ts is free now: the B tile
+    // the B tile does not depend on the inverse: its loads are issued first
+    uint32_t bv[16];
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+        const int r = wp + 8 * (u >> 1), c = lane + 32 * (u & 1);
+        bv[u] = (r < n && c < bc) ? __ldcg(B + (int64_t)r * ldb + c0 + c) : 0u;
+    }
+    trinv64_block<kMode>(f, T, ldt, n, Ts, X);
+#pragma unroll
+    for (int u = 0; u < 16; ++u) Ts[wp + 8 * (u >> 1)][lane + 32 * (u & 1)] = bv[u];  // Ts is free now
     __syncthreads();
     const int j = tid & 63, i0 = tid >> 6;  // a warp shares its rows: X[i][k] is a broadcast
     uint64_t acc[16];
