@@ -426,19 +426,43 @@ __global__ void __launch_bounds__(256, 2) k_trsm_panel_mma(Fp f, const uint32_t*
     auto reduce_acc = [&](int a) -> uint32_t {  // s32 accumulator -> residue
         return fsub(f, red32(f, (uint32_t)a ^ 0x80000000u), bias);
     };
-    for (int bi = 0; bi < nblk; ++bi) {
+    // A-operand blocks in processing order: T(bi, 0..bi-1), then Tinv(bi).  The next
+    // block's loads are in flight (registers) while the current one is multiplied.
+    uint32_t pv[16];
+    auto fetch = [&](int bi, int bj) {  // bj < 0: Tinv(bi)
         const int rb = bi * 64, rv = min(64, nb - rb);
+        const uint32_t* src = bj < 0 ? Tinv + (int64_t)bi * 64 * 64 : T + (int64_t)rb * ldt + bj * 64;
+        const int64_t ld = bj < 0 ? 64 : ldt;
+        const int rmax = bj < 0 ? 64 : rv;
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int e = threadIdx.x + 256 * u, r = e >> 6, c = e & 63;
+            pv[u] = r < rmax ? __ldcg(src + (int64_t)r * ld + c) : 0u;
+        }
+    };
+    auto store = [&]() {
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int e = threadIdx.x + 256 * u, r = e >> 6, c = e & 63;
+            Ab[r * PM_AB + c] = center8(pv[u], p, half);
+        }
+    };
+    fetch(0, -1);
+    for (int bi = 0; bi < nblk; ++bi) {
+        const int rb = bi * 64;
         int acc[4][4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0;
         for (int bj = 0; bj < bi; ++bj) {
             __syncthreads();  // Ab free, X_bj complete
-            pm_load_a(Ab, T + (int64_t)rb * ldt + bj * 64, ldt, rv, 64, p, half);
+            store();
             __syncthreads();
+            fetch(bi, bj + 1 < bi ? bj + 1 : -1);
             pm_mma(acc, Ab, XbT, bj * 64, mt, nt0, gid, tig);
         }
         __syncthreads();  // Ab free; XbT rows of block bi not read any more by the updates
-        pm_load_a(Ab, Tinv + (int64_t)bi * 64 * 64, 64, 64, 64, p, half);
+        store();  // Tinv(bi)
+        if (bi + 1 < nblk) fetch(bi + 1, 0);
         // Y = X_bi - acc (own fragment elements), exact and int8
 #pragma unroll
         for (int t = 0; t < 4; ++t)
