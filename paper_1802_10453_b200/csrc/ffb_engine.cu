@@ -359,13 +359,24 @@ struct Engine {
         DMat X = BP.sub(0, 0, r1, ns);
         trsm_lower_unit(f, st, LM.sub(0, 0, r1, r1), X);  // :310
         DMat Y = BP.sub(r1, 0, m - r1, ns);
-        gemm(f, st, GEMM_SUB, Y, LM.sub(r1, 0, m - r1, r1), false, X, false, m - r1, ns, r1);  // :312
         DMat G = ws_mat(c, ns, r1);
         inverse_apply_T(f, st, G, X, D, coff, Lg, up[2]);  // :313 + rows m..s of N1
         DMat Z = A.sub(m, m, ns, ns);
-        gemm(f, st, GEMM_SUB, Z, G, false, X, false, ns, ns, r1);  // Z = C - G D1 G^T (:315)
+        // Y = B'' - M1 X (:312) and Z = C - G X (:315); small ones as one paired launch
+        // whose Y epilogue also answers the zero test of zero_leading
+        int32_t ytag = 0;
+        if (r1 > 0 && m - r1 > 0) {
+            const int32_t tag = (int32_t)(++c->zero_gen);
+            if (mma_gemm_pair(f, st, Y, LM.sub(r1, 0, m - r1, r1), X, m - r1, ns, r1, Z, G, X, ns, ns, r1,
+                              c->zero_flag, tag))
+                ytag = tag;
+        }
+        if (!ytag) {
+            gemm(f, st, GEMM_SUB, Y, LM.sub(r1, 0, m - r1, r1), false, X, false, m - r1, ns, r1);
+            gemm(f, st, GEMM_SUB, Z, G, false, X, false, ns, ns, r1);
+        }
 
-        HFact f2 = zero_leading(Y, Z, rowsz, up[3], coff + r1);  // :317
+        HFact f2 = zero_leading(Y, Z, rowsz, up[3], coff + r1, ytag);  // :317
 
         HFact h;  // P = compose(embed(P1,0,n), embed(P2,r1,n)) (:332-334)
         h.rank = r1 + f2.rank;
@@ -379,16 +390,18 @@ struct Engine {
         return h;
     }
 
-    bool is_zero(DMat Y) {
+    bool is_zero(DMat Y, int32_t pretag = 0) {
         // generation tag instead of a memset: the flag holds an older tag unless Y != 0
-        const int32_t tag = (int32_t)(++c->zero_gen);
-        any_nonzero(st, Y, c->zero_flag, tag);
+        // (pretag: the producing GEMM already tagged the flag)
+        const int32_t tag = pretag ? pretag : (int32_t)(++c->zero_gen);
+        if (!pretag) any_nonzero(st, Y, c->zero_flag, tag);
         const int32_t v = *(const int32_t*)readback(c, c->zero_flag, sizeof(int32_t));
         return v != tag;
     }
 
     // sytrf.cpp:267-292
-    HFact zero_leading(DMat Y, DMat Z, const std::vector<int32_t>& rows, const int32_t* drows, int64_t coff) {
+    HFact zero_leading(DMat Y, DMat Z, const std::vector<int32_t>& rows, const int32_t* drows, int64_t coff,
+                       int32_t ytag = 0) {
         const int64_t m = Y.rows, nz = Z.rows;
         if (m == 0) return dispatch(Z, rows, drows, coff);
         HFact h;
@@ -397,7 +410,7 @@ struct Engine {
             for (int64_t i = 0; i < m; ++i) h.perm[i] = (int32_t)i;
             return h;
         }
-        if (is_zero(Y)) {  // :274-290
+        if (is_zero(Y, ytag)) {  // :274-290
             std::vector<int32_t> rz(rows.begin() + m, rows.end());
             HFact f3 = dispatch(Z, rz, drows ? drows + m : nullptr, coff);
             const int64_t r3 = f3.rank;

@@ -64,6 +64,11 @@ bool mma_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K);
 void mma_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
               int64_t M, int64_t N, int64_t K);
 
+// Two GEMM_SUB products in one mma.sync launch when both are small; problem 1 may set
+// *nzflag = tag when any of its outputs is nonzero.  Returns false when not applicable.
+bool mma_gemm_pair(const Fp& f, cudaStream_t st, DMat C1, DMat A1, DMat B1, int64_t M1, int64_t N1, int64_t K1,
+                   DMat C2, DMat A2, DMat B2, int64_t M2, int64_t N2, int64_t K2, int32_t* nzflag, int32_t tag);
+
 // short-K bandwidth kernel (ffb_mma.cu): p <= 255, K <= 128, dp4a on int8 packs.
 bool rankk_supported(const Fp& f, int64_t M, int64_t N, int64_t K);
 void rankk_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,

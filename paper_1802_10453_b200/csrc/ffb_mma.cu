@@ -20,12 +20,31 @@ constexpr int MM_T = 64, MM_S = 64 + 16;  // tile edge, smem row stride in bytes
 
 // Split K: CTA z covers k in [z kc, (z+1) kc) and, when gridDim.z > 1, writes
 // its reduced partial tile to W[z] (M x N, ld N) for k_splitk_fold.
+// Second problem of a paired launch (blockIdx.z = 1), same mode and orientation.
+struct MmaProb {
+    uint32_t* C;
+    int64_t ldc;
+    const uint32_t* A;
+    int64_t lda;
+    const uint32_t* B;
+    int64_t ldb;
+    int64_t M, N, K;
+};
 template <bool TA, bool TB>
 __global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* C, int64_t ldc,
                                                   const uint32_t* A, int64_t lda,
                                                   const uint32_t* B, int64_t ldb, int64_t M,
-                                                  int64_t N, int64_t K, int64_t kc, uint32_t* W) {
+                                                  int64_t N, int64_t K, int64_t kc, uint32_t* W,
+                                                  int pair, MmaProb p2, int32_t* nzflag, int32_t nztag) {
     FFB_PDL_ENTRY();
+    // pair: blockIdx.z selects the problem (no split-K); problem 0 may publish nztag
+    // to *nzflag when any output is nonzero (the zero test of the next recursion step)
+    if (pair && blockIdx.z == 1) {
+        C = p2.C, ldc = p2.ldc, A = p2.A, lda = p2.lda, B = p2.B, ldb = p2.ldb, M = p2.M, N = p2.N, K = p2.K;
+        nzflag = nullptr;
+    }
+    if ((int64_t)blockIdx.y * MM_T >= M || (int64_t)blockIdx.x * MM_T >= N) return;  // uniform
+    const bool splitk = !pair && gridDim.z > 1;
     __shared__ __align__(16) int8_t As[MM_T * MM_S];  // op(A) tile [m][k]
     __shared__ __align__(16) int8_t Bs[MM_T * MM_S];  // op(B) tile transposed [n][k]
     __shared__ uint32_t Cs[MM_T][MM_T + 1];           // reduced tile, for a coalesced epilogue
@@ -58,15 +77,15 @@ __global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* C, i
             Bs[(TB ? hi : lo) * MM_S + (TB ? lo : hi)] = center8(rb[u], p, half);
         }
     };
-    const int64_t kb = (int64_t)blockIdx.z * kc;
-    K = std::min<int64_t>(K, kb + kc);  // this CTA's K range is [kb, K)
+    const int64_t kb = splitk ? (int64_t)blockIdx.z * kc : 0;
+    K = splitk ? std::min<int64_t>(K, kb + kc) : K;  // this CTA's K range is [kb, K)
     int acc[4][4];
 #pragma unroll
     for (int t = 0; t < 4; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0;
     // the C values of this thread's epilogue slots (rows wp + 8i, columns lane, lane + 32)
     // do not depend on the product: load them now, overlapped with the K loop
     uint32_t cpre[16];
-    const bool direct = gridDim.z == 1 && mode != GEMM_SET;
+    const bool direct = !splitk && mode != GEMM_SET;
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
@@ -110,15 +129,18 @@ __global__ void __launch_bounds__(256) k_gemm_mma(Fp f, int mode, uint32_t* C, i
             const int64_t col = n0 + lane + 32 * h;
             if (col >= N) continue;
             const uint32_t v = Cs[r][lane + 32 * h];
-            if (gridDim.z > 1) {
+            if (splitk) {
                 W[((int64_t)blockIdx.z * M + row) * N + col] = v;
                 continue;
             }
             const uint32_t c0 = cpre[2 * i + h];
             uint32_t* c = C + row * ldc + col;
-            if (mode == GEMM_SUB) *c = fsub(f, c0, v);
-            else if (mode == GEMM_ADD) *c = fadd(f, c0, v);
-            else *c = v;
+            uint32_t o;
+            if (mode == GEMM_SUB) o = fsub(f, c0, v);
+            else if (mode == GEMM_ADD) o = fadd(f, c0, v);
+            else o = v;
+            *c = o;
+            if (nzflag && o) *nzflag = nztag;
         }
     }
 }
@@ -181,7 +203,7 @@ void mma_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool 
     const dim3 grid((unsigned)cdiv(N, MM_T), (unsigned)cdiv(M, MM_T), (unsigned)S);
 #define FFB_MMA_LAUNCH(TA, TB)                                                                       \
     launch_k(k_gemm_mma<TA, TB>, grid, 256, 0, st, f, (int)mode, C.ptr, C.ld, A.ptr, A.ld, B.ptr, B.ld, M, N, K, \
-                                             kc, W)
+                                             kc, W, 0, MmaProb{}, (int32_t*)nullptr, 0)
     if (!ta && !tb) FFB_MMA_LAUNCH(false, false);
     else if (ta && !tb) FFB_MMA_LAUNCH(true, false);
     else if (!ta && tb) FFB_MMA_LAUNCH(false, true);
@@ -299,6 +321,27 @@ __global__ void __launch_bounds__(256) k_rankk_dp4a(Fp f, int mode, uint32_t* C,
 }
 
 }  // namespace
+
+bool mma_gemm_pair(const Fp& f, cudaStream_t st, DMat C1, DMat A1, DMat B1, int64_t M1, int64_t N1, int64_t K1,
+                   DMat C2, DMat A2, DMat B2, int64_t M2, int64_t N2, int64_t K2, int32_t* nzflag, int32_t tag) {
+    // both on the mma path without split-K (small products), non-transposed, GEMM_SUB
+    auto small = [&](int64_t M, int64_t N, int64_t K) {
+        const int64_t tiles = cdiv(N, MM_T) * cdiv(M, MM_T);
+        const bool split = tiles < 148 && K >= 512 && M * N <= ((int64_t)1 << 24);
+        return M > 0 && N > 0 && K > 0 && !split && mma_gemm_supported(f, M, N, K) &&
+               !(M >= 128 && N >= 128 && (double)M * N * K >= 2.7e8) && !(K <= 32 && rankk_supported(f, M, N, K));
+    };
+    if (getenv("FFB_GEMM_PATH") || !small(M1, N1, K1) || !small(M2, N2, K2)) return false;
+    ProfScope ps(K_GEMM, st, 2.0 * (M1 * N1 * K1 + M2 * N2 * K2), 0.0, M1, -N1, K1);
+    const dim3 grid((unsigned)std::max(cdiv(N1, MM_T), cdiv(N2, MM_T)),
+                    (unsigned)std::max(cdiv(M1, MM_T), cdiv(M2, MM_T)), 2);
+    const MmaProb p2{C2.ptr, C2.ld, A2.ptr, A2.ld, B2.ptr, B2.ld, M2, N2, K2};
+    launch_k(k_gemm_mma<false, false>, grid, 256, 0, st, f, (int)GEMM_SUB, C1.ptr, C1.ld, A1.ptr, A1.ld, B1.ptr,
+             B1.ld, M1, N1, K1, K1, (uint32_t*)nullptr, 1, p2, nzflag, tag);
+    ++g_launches;
+    FFB_CHECK_LAUNCH();
+    return true;
+}
 
 bool rankk_supported(const Fp& f, int64_t M, int64_t N, int64_t K) {
     static const bool disabled = getenv("FFB_DISABLE_RANKK") != nullptr;  // test hook
