@@ -323,17 +323,20 @@ constexpr int CRP_W = 256, CRP_G = 32, CRP_KMAX = 128;
 // E in parallel; the flagged ones go through the blocked insertion.  The ids
 // of the independent columns are written to out[0 .. nb) in scan order.
 // Stops once k columns are found.  E, V, VC: shared (see k_crp_list).
-template <class ColFn>
+// NQ = ceil(k / 32): vector slots per lane (k <= 32 NQ), so short vectors do not pay
+// for the 128-entry maximum (the instantiation is picked at run time).
+template <int NQ, class ColFn>
 __device__ int crp_scan(const Fp& f, const SmemInv& inv, const uint32_t* RI, int64_t ldr,
                         int k, int total, ColFn colfn, uint32_t* E, uint32_t* V, uint32_t* VC, int* rho,
                         unsigned* fmask, BatchScratch& bs, int32_t* out) {
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-    uint32_t vv[CRP_KMAX / 8];  // thread (wp, lane) holds rows wp + 8u of column lane of a group
+    constexpr int RU = 4 * NQ;  // rows per lane: wp + 8u, u < RU covers k <= 32 NQ
+    uint32_t vv[RU];  // thread (wp, lane) holds rows wp + 8u of column lane of a group
     auto fetch = [&](int s0) {
         const bool ok = s0 + lane < total;
         const uint32_t* src = RI + (ok ? colfn(s0 + lane) : 0);
 #pragma unroll
-        for (int u = 0; u < CRP_KMAX / 8; ++u) {
+        for (int u = 0; u < RU; ++u) {
             const int i = wp + 8 * u;
             vv[u] = (ok && i < k) ? __ldcg(src + (int64_t)i * ldr) : 0u;
         }
@@ -343,7 +346,7 @@ __device__ int crp_scan(const Fp& f, const SmemInv& inv, const uint32_t* RI, int
     for (int s0 = 0; s0 < total && nb < k; s0 += CRP_G, ++gi) {
         const int gw = min(CRP_G, total - s0);
 #pragma unroll
-        for (int u = 0; u < CRP_KMAX / 8; ++u) {
+        for (int u = 0; u < RU; ++u) {
             const int i = wp + 8 * u;
             if (i < k) V[(size_t)lane * k + i] = vv[u];
         }
@@ -354,17 +357,20 @@ __device__ int crp_scan(const Fp& f, const SmemInv& inv, const uint32_t* RI, int
             for (int t = lane; t < nb; t += 32) VC[(size_t)c * CRP_KMAX + t] = V[(size_t)c * k + rho[t]];
         __syncthreads();
         // reduce the group against the basis; flagged columns are outside its span
-        reduce_rows_any<4>(f, V, k, V, k, VC, CRP_KMAX, E, k, gw, k, nb, &fmask[gi & 1]);
+        reduce_rows_any<NQ>(f, V, k, V, k, VC, CRP_KMAX, E, k, gw, k, nb, &fmask[gi & 1]);
         __syncthreads();
         const unsigned pending = fmask[gi & 1];
         if (!pending) continue;
-        const int cnt = batch_insert<4>(f, inv, V, k, pending, k, E, nb, k, rho, bs);
+        const int cnt = batch_insert<NQ>(f, inv, V, k, pending, k, E, nb, k, rho, bs);
         if (tid < cnt) out[nb + tid] = colfn(s0 + bs.ins[tid]);
         nb += cnt;
     }
     return nb;
 }
 
+#define FFB_CRP_SCAN(...)                                                 \
+    (k <= 32 ? crp_scan<1>(__VA_ARGS__) : k <= 64 ? crp_scan<2>(__VA_ARGS__) \
+             : k <= 96 ? crp_scan<3>(__VA_ARGS__) : crp_scan<4>(__VA_ARGS__))
 __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int64_t ldr,
                                                   int k, int64_t n, int32_t* out, int32_t* ocount) {
     FFB_PDL_ENTRY();
@@ -407,8 +413,8 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
     }
     int cnt = 0;
     for (int w = 0; w < CRP_W / 32; ++w) cnt += wcnt[w];
-    const int nb = crp_scan(f, inv, RI, ldr, k, cnt, [&](int idx) { return nzc[idx]; }, E, V, VC, rho, fmask, bs,
-                            out + (int64_t)g * k);
+    auto colfn = [&](int idx) { return nzc[idx]; };
+    const int nb = FFB_CRP_SCAN(f, inv, RI, ldr, k, cnt, colfn, E, V, VC, rho, fmask, bs, out + (int64_t)g * k);
     if (threadIdx.x == 0) ocount[g] = nb;
 }
 
@@ -620,8 +626,8 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         uint32_t* E = M;
         uint32_t* V = E + (size_t)CRP_KMAX * k;
         uint32_t* VC = V + (size_t)CRP_G * k;
-        const int nb = crp_scan(f, inv, RI, ldr, k, C, [cand](int idx) { return cand[idx]; }, E, V, VC, rho,
-                                fmask, bs, Js);
+        auto colfn = [cand](int idx) { return cand[idx]; };
+        const int nb = FFB_CRP_SCAN(f, inv, RI, ldr, k, C, colfn, E, V, VC, rho, fmask, bs, Js);
         if (nb < k) {  // R_I rank deficient: cannot happen for detected rows
             if (tid == 0) *fail = 1;
             return;
@@ -1135,9 +1141,21 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             YO = ws.mat(m, SK);
             gemm(f, st, GEMM_SET, YO, Y, false, Om, false, m, SK, n);
         }
+        // diagnostics: FFB_PLDUQ_CHUNK_TRACE=<file> records event marks per chunk (m >= 4096)
+        static FILE* ctr = getenv("FFB_PLDUQ_CHUNK_TRACE") ? fopen(getenv("FFB_PLDUQ_CHUNK_TRACE"), "a") : nullptr;
+        const bool ctrace = ctr && m >= 4096;
+        std::vector<cudaEvent_t> cev;
+        auto mark = [&]() {
+            if (!ctrace) return;
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            cudaEventRecord(e, st);
+            cev.push_back(e);
+        };
         for (int64_t c0 = 0; c0 < m; c0 += B) {
             const int64_t bc = std::min<int64_t>(B, m - c0);
             DMat Yc = Y.sub(c0, 0, bc, n);
+            mark();
             if (!exact) {
                 // sketch of the chunk residual, in place in its (otherwise unused)
                 // rows of Y*Omega: S = (Y Omega)_c - Y_c[:, pc] (Uhat Omega), a GEMM
@@ -1150,6 +1168,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     }
                     gemm(f, st, GEMM_SUB, Sc, Gc, false, UO.sub(0, 0, r, SK), false, bc, SK, r);
                 }
+                mark();
                 {
                     ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
                     launch_k(k_row_detect, 1, 256, rd_smem, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo);
@@ -1157,7 +1176,11 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     FFB_CHECK_LAUNCH();
                 }
                 const int k = *(const int32_t*)io.readback(dinfo, 4);
-                if (k == 0) continue;
+                mark();
+                if (k == 0) {
+                    mark(); mark(); mark();
+                    continue;
+                }
                 join_side();  // the previous chunk's Uhat update, before RI / Kinv / Upd are reused
                 const int32_t* dI = dinfo + 1;
                 // exact residual of the k detected rows: R_I = Y_I - Y_I[:, pc] Uhat
@@ -1168,6 +1191,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     gather2d(st, Gk, Y, dI, d_uhat_col, c0);
                     gemm(f, st, GEMM_SUB, RIk, Gk, false, Uhat.sub(0, 0, r, n), false, k, n, r);
                 }
+                mark();
                 {
                     ProfScope ps(K_PQ_CRP, st, 0.0, 0.0);
                     // level 0: local CRPs of 256-column blocks (parallel)
@@ -1196,6 +1220,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     fprintf(jtr, "%d %lld %lld %lld %d %d %d\n", k, (long long)n, (long long)C, (long long)r,
                             hj[0], hj[k / 2], hj[k - 1]);
                 }
+                mark();
                 absorb(r, k, dI, lists[1], c0, true, dsig, Sc, true);
                 r += k;
             } else {
@@ -1232,6 +1257,22 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             }
         }
         join_side();
+        if (ctrace && !cev.empty()) {  // 5 marks per chunk: start, detect, readback, crp, finish
+            mark();
+            cudaEventSynchronize(cev.back());
+            double acc[5] = {0, 0, 0, 0, 0};
+            const size_t nc = (cev.size() - 1) / 5;
+            for (size_t c = 0; c < nc; ++c)
+                for (int j = 0; j < 5; ++j) {
+                    float t = 0;
+                    cudaEventElapsedTime(&t, cev[5 * c + j], cev[5 * c + j + 1]);
+                    acc[j] += t;
+                }
+            fprintf(ctr, "m=%lld n=%lld chunks=%zu sketch=%.2f detect+post=%.2f gathers+residual=%.2f crp+finish=%.2f absorb+next=%.2f ms\n",
+                    (long long)m, (long long)n, nc, acc[0], acc[1], acc[2], acc[3], acc[4]);
+            fflush(ctr);
+            for (auto e : cev) cudaEventDestroy(e);
+        }
         out.r = r;
         std::vector<int32_t> pr, pcol_rows;
         if (r > 0) {  // d_prow and d_pcol are adjacent: one read-back
