@@ -60,6 +60,7 @@ struct ffb_context {
     uint32_t* mbox_seq_dev = nullptr;
     size_t mbox_cap = 0;
     uint32_t mbox_seq = 0;
+    cudaStream_t copy_stream = nullptr;  // host <-> device transfers overlapped with the engine
     Profiler prof;
 };
 
@@ -291,6 +292,14 @@ struct HFact {
     int64_t rank = 0;
 };
 
+// Input rows arriving in bands on the copy stream (ffb_ldlt_compact): row r of the
+// input view is usable on the engine stream once the band holding it has landed.
+struct UploadBands {
+    const uint32_t* base = nullptr;
+    int64_t ld = 0, rows = 0, ready = 0;      // rows [0, ready) known to be resident
+    std::vector<std::pair<int64_t, cudaEvent_t>> ev;  // (band end row, landed)
+};
+
 struct Engine {
     ffb_context* c;
     cudaStream_t st;
@@ -299,6 +308,20 @@ struct Engine {
     int64_t T;
     DMat Lg;
     DDiag D;
+    UploadBands* bands = nullptr;
+
+    // Before a node touches rows [m, s) of an input-resident A (the Z block): wait for them.
+    void ensure_rows(DMat A, int64_t s) {
+        if (!bands || bands->ready >= bands->rows) return;
+        if (A.ptr < bands->base || A.ptr >= bands->base + bands->rows * bands->ld) return;
+        const int64_t need = (A.ptr - bands->base) / bands->ld + s;
+        for (auto& be : bands->ev)
+            if (be.first > bands->ready && bands->ready < need) {
+                FFB_CUDA(cudaStreamWaitEvent(st, be.second, 0));
+                pdl_fence(st);
+                bands->ready = be.first;
+            }
+    }
 
     bool is_leaf(int64_t s) const {
         if (variant == FFB_VARIANT_CROUT) return true;
@@ -322,6 +345,7 @@ struct Engine {
         const int64_t s = A.rows;
         HFact h;
         if (s == 0) return h;
+        ensure_rows(A, s);  // (a leaf at the root of a Crout run reads every row)
         const WsMark mk{c->ws_top};
         const int32_t* drows = drows_in ? drows_in : upload(c, rows);
         int32_t* out = ws_vec<int32_t>(c, s + 1);
@@ -362,6 +386,7 @@ struct Engine {
         DMat G = ws_mat(c, ns, r1);
         inverse_apply_T(f, st, G, X, D, coff, Lg, up[2]);  // :313 + rows m..s of N1
         DMat Z = A.sub(m, m, ns, ns);
+        ensure_rows(A, s);  // Z and the recursion below read rows [m, s)
         // Y = B'' - M1 X (:312) and Z = C - G X (:315); small ones as one paired launch
         // whose Y epilogue also answers the zero test of zero_leading
         int32_t ytag = 0;
@@ -643,7 +668,7 @@ struct DevFact {
 
 // Run the factorization of the n x n device matrix W (destroyed).
 DevFact run_ldlt(ffb_context* c, const Fp& f, DMat W, int variant, int64_t threshold,
-                 bool check_symmetric) {
+                 bool check_symmetric, UploadBands* bands = nullptr) {
     const int64_t n = W.rows;
     cudaStream_t st = c->stream;
     DevFact out;
@@ -661,6 +686,7 @@ DevFact run_ldlt(ffb_context* c, const Fp& f, DMat W, int variant, int64_t thres
     out.D.val2 = ws_vec<uint32_t>(c, n);
     out.D.inv = ws_vec<uint32_t>(c, n);
     Engine e{c, st, f, variant, (int64_t)threshold, out.Lg, out.D};
+    e.bands = bands;
     std::vector<int32_t> rows(n);
     for (int64_t i = 0; i < n; ++i) rows[i] = (int32_t)i;
     if (n > 0) {
@@ -681,10 +707,34 @@ void export_host(ffb_context* c, const DevFact& df, int64_t* perm, void* lower, 
     if (n == 0) return;
     if (r > 0) {
         DMat Lout = ws_mat(c, n, r);
-        gather_lower_out(st, Lout, df.Lg, upload(c, df.perm));
+        const int32_t* dperm = upload(c, df.perm);
         void* dl = ws_alloc(c, (size_t)n * r * lower_eb);
-        convert_out(st, dl, lower_eb, Lout);
-        FFB_CUDA(cudaMemcpyAsync(lower, dl, (size_t)n * r * lower_eb, cudaMemcpyDeviceToHost, st)); pdl_fence(st);
+        // row bands: gather + convert on the engine stream, each band's copy to the
+        // host on the copy stream while the next band is gathered
+        const int64_t nb = n >= 4096 ? 8 : 1, step = cdiv(n, nb);
+        std::vector<cudaEvent_t> evs;
+        for (int64_t r0 = 0; r0 < n; r0 += step) {
+            const int64_t nr = std::min<int64_t>(step, n - r0);
+            gather_lower_out(st, Lout.sub(r0, 0, nr, r), df.Lg, dperm + r0);
+            char* dband = (char*)dl + (size_t)r0 * r * lower_eb;
+            convert_out(st, dband, lower_eb, Lout.sub(r0, 0, nr, r));
+            if (nb == 1) {
+                FFB_CUDA(cudaMemcpyAsync(lower, dl, (size_t)n * r * lower_eb, cudaMemcpyDeviceToHost, st));
+                pdl_fence(st);
+                break;
+            }
+            cudaEvent_t ev;
+            FFB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            FFB_CUDA(cudaEventRecord(ev, st));
+            evs.push_back(ev);
+            FFB_CUDA(cudaStreamWaitEvent(c->copy_stream, ev, 0));
+            FFB_CUDA(cudaMemcpyAsync((char*)lower + (size_t)r0 * r * lower_eb, dband, (size_t)nr * r * lower_eb,
+                                     cudaMemcpyDeviceToHost, c->copy_stream));
+        }
+        if (!evs.empty()) {
+            FFB_CUDA(cudaStreamSynchronize(c->copy_stream));
+            for (auto ev : evs) cudaEventDestroy(ev);
+        }
         std::vector<int32_t> k(r);
         std::vector<uint32_t> v(r), v2(r);
         FFB_CUDA(cudaMemcpyAsync(k.data(), df.D.kind, r * sizeof(int32_t), cudaMemcpyDeviceToHost, st)); pdl_fence(st);
@@ -779,6 +829,11 @@ int ffb_create(ffb_context** out, int device) {
             c->mbox_dev = (uint32_t*)d;
             c->mbox_seq_dev = (uint32_t*)((char*)d + c->mbox_cap);
         }
+        {
+            int least = 0, greatest = 0;
+            FFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            FFB_CUDA(cudaStreamCreateWithPriority(&c->copy_stream, cudaStreamNonBlocking, least));
+        }
         FFB_CUDA(cudaMalloc(&c->flag, 256));
         FFB_CUDA(cudaMemset(c->flag, 0, 256));
         c->zero_flag = c->flag + 32;
@@ -798,6 +853,7 @@ int ffb_destroy(ffb_context* c) {
     if (c->inv_table) cudaFree(c->inv_table);
     if (c->flag) cudaFree(c->flag);
     if (c->mbox_host) cudaFreeHost(c->mbox_host);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->up_host) cudaFreeHost(c->up_host);
     if (c->down_host) cudaFreeHost(c->down_host);
     cudaStreamDestroy(c->stream);
@@ -835,8 +891,70 @@ int ffb_ldlt_compact(ffb_context* c, uint64_t p, size_t n, const void* a, int a_
         ensure_workspace(c, workspace_bytes((int64_t)n) + (size_t)n * n * (aeb + leb));
         c->ws_top = 0;
         Fp f = make_field(c, p);
-        DMat W = upload_matrix(c, f, a, (int64_t)n, (int64_t)n, aeb);
-        DevFact df = run_ldlt(c, f, W, variant, (int64_t)threshold, true);
+        if (n < 4096 || getenv("FFB_NO_BANDS")) {
+            DMat W = upload_matrix(c, f, a, (int64_t)n, (int64_t)n, aeb);
+            DevFact df = run_ldlt(c, f, W, variant, (int64_t)threshold, true);
+            export_host(c, df, perm, lower, leb, dkind, dval, dval2, rank);
+            c->ws_top = 0;
+            return;
+        }
+        // Large n: the input arrives in row bands (n/16, n/8, n/4, n/2, n) on the copy
+        // stream, converted as it lands; the recursion starts on the first band and
+        // waits for later rows only where a node first reads them (Engine::ensure_rows).
+        // The engine reads only the upper blocks B and Z, so an asymmetric input factors
+        // harmlessly as another symmetric matrix; the check runs on the copy stream
+        // after the last band and the result is refused (NotSymmetric) before export.
+        const int64_t N = (int64_t)n;
+        DMat W = ws_mat(c, N, N);
+        char* tmp = (char*)ws_alloc(c, (size_t)N * N * aeb);
+        UploadBands bands;
+        bands.base = W.ptr;
+        bands.ld = W.ld;
+        bands.rows = N;
+        for (int64_t e : {N / 16, N / 8, N / 4, N / 2, N}) {
+            const int64_t r0 = bands.ev.empty() ? 0 : bands.ev.back().first;
+            if (e <= r0) continue;
+            FFB_CUDA(cudaMemcpyAsync(tmp + (size_t)r0 * N * aeb, (const char*)a + (size_t)r0 * N * aeb,
+                                     (size_t)(e - r0) * N * aeb, cudaMemcpyHostToDevice, c->copy_stream));
+            pdl_fence(c->copy_stream);
+            convert_in(f, c->copy_stream, W.sub(r0, 0, e - r0, N), tmp + (size_t)r0 * N * aeb, aeb);
+            cudaEvent_t ev;
+            FFB_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+            FFB_CUDA(cudaEventRecord(ev, c->copy_stream));
+            bands.ev.push_back({e, ev});
+        }
+        int32_t* aflag = c->flag + 16;  // asymmetry flag (copy stream)
+        FFB_CUDA(cudaMemsetAsync(aflag, 0, sizeof(int32_t), c->copy_stream));
+        pdl_fence(c->copy_stream);
+        any_asymmetric(c->copy_stream, W, aflag);
+        cudaEvent_t checked;
+        FFB_CUDA(cudaEventCreateWithFlags(&checked, cudaEventDisableTiming));
+        FFB_CUDA(cudaEventRecord(checked, c->copy_stream));
+        FFB_CUDA(cudaStreamWaitEvent(c->stream, bands.ev.front().second, 0));
+        pdl_fence(c->stream);
+        bands.ready = bands.ev.front().first;
+        auto release = [&] {
+            for (auto& be : bands.ev) cudaEventDestroy(be.second);
+            cudaEventDestroy(checked);
+        };
+        auto asymmetric = [&] {
+            FFB_CUDA(cudaStreamWaitEvent(c->stream, checked, 0));
+            pdl_fence(c->stream);
+            return *(const int32_t*)readback(c, aflag, sizeof(int32_t)) != 0;
+        };
+        DevFact df;
+        try {
+            df = run_ldlt(c, f, W, variant, (int64_t)threshold, false, &bands);
+        } catch (const Status&) {
+            cudaStreamSynchronize(c->copy_stream);
+            const bool asym = asymmetric();
+            release();
+            if (asym) throw Status(FFB_NOT_SYMMETRIC, "ldlt: matrix must be symmetric");
+            throw;
+        }
+        const bool asym = asymmetric();  // (also orders the last band before the export)
+        release();
+        if (asym) throw Status(FFB_NOT_SYMMETRIC, "ldlt: matrix must be symmetric");
         export_host(c, df, perm, lower, leb, dkind, dval, dval2, rank);
         c->ws_top = 0;
     });

@@ -336,3 +336,33 @@ def test_repeated_calls_same_context(gpu, oracle, p):
         for a in cases:
             for v, t in (("recursive", 64), ("cascade", 4)):
                 check(gpu, oracle, p, a, v, t)
+
+
+@pytest.mark.parametrize("v", ["cascade", "crout"])
+def test_banded_upload_matches_device_path(gpu, v):
+    """n >= 4096 host calls stream the input in row bands while the recursion runs
+    (ffb_ldlt_compact); the result must equal the device-resident path bit for bit."""
+    import torch
+    import paper_1802_10453_b200 as ffb
+    from paper_1802_10453_b200 import configs
+    from paper_1802_10453_b200.device import ldlt_device
+    n = 4096
+    w = configs.CONFIGS[5].scaled(n)
+    a = configs.generate(w)
+    g = ffb.ldlt(a, w.p, cfg(v, 64), ctx=gpu)
+    d = ldlt_device(torch.from_numpy(a.astype(np.int32)).cuda(), w.p, cfg(v, 64), gpu)
+    kind, val, val2 = g.diag.columns()
+    assert g.rank == d.rank == w.r
+    assert np.array_equal(g.perm.image_array(), d.perm.cpu().numpy())
+    assert np.array_equal(g.lower, d.lower[:, :d.rank].cpu().numpy().astype(np.uint64))
+    r = g.rank
+    assert np.array_equal(kind, d.dkind[:r].cpu().numpy())
+    assert np.array_equal(val, d.dval[:r].cpu().numpy().astype(np.uint64))
+    assert np.array_equal(val2, d.dval2[:r].cpu().numpy().astype(np.uint64))
+    # one asymmetric entry in the last band: refused, and the context stays usable
+    b = a.copy()
+    b[n - 1, 3] = (b[n - 1, 3] + 1) % w.p
+    with pytest.raises(ffb.NotSymmetric):
+        ffb.ldlt(b, w.p, cfg(v, 64), ctx=gpu)
+    g2 = ffb.ldlt(a, w.p, cfg(v, 64), ctx=gpu)
+    assert g2.rank == g.rank and np.array_equal(g2.lower, g.lower)
