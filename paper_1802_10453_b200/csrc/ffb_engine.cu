@@ -40,7 +40,8 @@ struct ffb_context {
     cudaStream_t stream = nullptr;
     char* ws_base = nullptr;
     size_t ws_cap = 0, ws_top = 0;
-    char* up_host = nullptr;
+    char* up_host = nullptr;  // mapped pinned ring
+    const char* up_dev = nullptr;  // its device alias
     size_t up_cap = 0, up_top = 0;
     char* down_host = nullptr;
     size_t down_cap = 0;
@@ -156,6 +157,19 @@ T* ws_vec(ffb_context* c, int64_t n) {
     return (T*)ws_alloc(c, (size_t)std::max<int64_t>(n, 1) * sizeof(T));
 }
 
+// Upload ring fetch: the engine stream pulls the words from the mapped pinned
+// ring with loads over the bus.  A kernel rather than a copy-engine operation:
+// it stays in the programmatic-launch chain, and it is not queued behind bulk
+// host-to-device copies on other streams (the banded input upload).
+__global__ void __launch_bounds__(512) k_fetch(uint32_t* dst, const uint32_t* src, int64_t words) {
+    FFB_PDL_ENTRY();
+    const int64_t w4 = words >> 2, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < w4; i += stride)
+        reinterpret_cast<uint4*>(dst)[i] = __ldcv(reinterpret_cast<const uint4*>(src) + i);
+    for (int64_t i = 4 * w4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += stride)
+        dst[i] = __ldcv(src + i);
+}
+
 // Pinned upload ring: index arrays going down to the device.
 const int32_t* upload(ffb_context* c, const int32_t* v, size_t n) {
     int32_t* d = ws_vec<int32_t>(c, (int64_t)n);
@@ -172,7 +186,15 @@ const int32_t* upload(ffb_context* c, const int32_t* v, size_t n) {
         off = 0;
     }
     memcpy(c->up_host + off, v, bytes);
-    FFB_CUDA(cudaMemcpyAsync(d, c->up_host + off, bytes, cudaMemcpyHostToDevice, c->stream)); pdl_fence(c->stream);
+    static const bool dma = getenv("FFB_UPLOAD_DMA") != nullptr;
+    if (dma) {
+        FFB_CUDA(cudaMemcpyAsync(d, c->up_host + off, bytes, cudaMemcpyHostToDevice, c->stream));
+        pdl_fence(c->stream);
+    } else {
+        const int64_t words = (int64_t)n;
+        const int blocks = (int)std::min<int64_t>(64, std::max<int64_t>(1, cdiv(words, 4 * 512)));
+        launch_k(k_fetch, blocks, 512, 0, c->stream, (uint32_t*)d, (const uint32_t*)(c->up_dev + off), words);
+    }
     ++c->uploads;
     c->up_top = off + bytes;
     return d;
@@ -563,7 +585,7 @@ struct Engine {
             gemm(f, st, GEMM_SUB, C1, H, true, U1, false, r, r, r);  // C1 -= U1^T diag(delta) U1
         }
         DMat X = ws_mat(c, r, r);
-        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), st)); pdl_fence(st);
+        fill_words(st, (uint32_t*)c->flag, 1, 0u);
         trssyr2k_dev(U1, U1T, C1, X, c->flag);  // :202
         DMat G12 = ws_mat(c, nz, r);  // [G1; G2]
         scale_T(f, st, G12.sub(0, 0, r, r), X, py.dinv);  // G1 = (diag(d)^-1 X)^T (:203)
@@ -674,7 +696,7 @@ DevFact run_ldlt(ffb_context* c, const Fp& f, DMat W, int variant, int64_t thres
     DevFact out;
     out.n = n;
     if (check_symmetric) {  // ldlt validation, sytrf.cpp:355-356
-        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), st)); pdl_fence(st);
+        fill_words(st, (uint32_t*)c->flag, 1, 0u);
         any_asymmetric(st, W, c->flag);
         if (*(const int32_t*)readback(c, c->flag, sizeof(int32_t)))
             throw Status(FFB_NOT_SYMMETRIC, "ldlt: matrix must be symmetric");
@@ -814,7 +836,14 @@ int ffb_create(ffb_context** out, int device) {
             FFB_CUDA(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest));
         }
         c->up_cap = (size_t)64 << 20;
-        FFB_CUDA(cudaMallocHost(&c->up_host, c->up_cap));
+        {
+            void* h = nullptr;
+            FFB_CUDA(cudaHostAlloc(&h, c->up_cap, cudaHostAllocMapped));
+            c->up_host = (char*)h;
+            void* d = nullptr;
+            FFB_CUDA(cudaHostGetDevicePointer(&d, h, 0));
+            c->up_dev = (const char*)d;
+        }
         c->down_cap = (size_t)16 << 20;
         FFB_CUDA(cudaMallocHost(&c->down_host, c->down_cap));
         {  // read-back mailbox: 256 KB of data + a sequence word, mapped pinned
@@ -984,7 +1013,7 @@ int ffb_ldlt_zero_leading(ffb_context* c, uint64_t p, size_t m, size_t ny, const
         Fp f = make_field(c, p);
         DMat Zd = upload_matrix(c, f, z, (int64_t)nz, (int64_t)nz, 8);
         {
-            FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), c->stream)); pdl_fence(c->stream);
+            fill_words(c->stream, (uint32_t*)c->flag, 1, 0u);
             any_asymmetric(c->stream, Zd, c->flag);
             if (*(const int32_t*)readback(c, c->flag, sizeof(int32_t)))
                 throw Status(FFB_NOT_SYMMETRIC, "ldlt_zero_leading: Z must be symmetric");
@@ -1096,7 +1125,7 @@ int ffb_trssyr2k(ffb_context* c, uint64_t p, size_t n, const uint64_t* u, const 
         DMat C = upload_matrix(c, f, cc, N, N, 8);
         DMat X = ws_mat(c, N, N);
         Engine e{c, c->stream, f, FFB_VARIANT_CASCADE, 64, DMat(), DDiag()};
-        FFB_CUDA(cudaMemsetAsync(c->flag, 0, sizeof(int32_t), c->stream)); pdl_fence(c->stream);
+        fill_words(c->stream, (uint32_t*)c->flag, 1, 0u);
         e.trssyr2k_dev(U, UT, C, X, c->flag);
         if (f.char2 && *(const int32_t*)readback(c, c->flag, sizeof(int32_t)))
             throw Status(FFB_CHAR_TWO_NONZERO_DIAGONAL, "trssyr2k: diagonal entry has no solution");

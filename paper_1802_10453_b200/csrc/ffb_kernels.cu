@@ -759,11 +759,33 @@ void add_scaled_rows_upper(const Fp& f, cudaStream_t st, DMat X, DMat U, const u
     FFB_CHECK_LAUNCH();
 }
 
+// Word fill as a kernel (not a copy-engine memset): stays in the programmatic-launch
+// chain and is not queued behind bulk host transfers on other streams.
+__global__ void k_fill(uint32_t* p, int64_t n, uint32_t v) {
+    FFB_PDL_ENTRY();
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t i0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t mis = (int64_t)((16 - ((uintptr_t)p & 15)) & 15) / 4;
+    const int64_t head = mis < n ? mis : n;
+    if (i0 < head) p[i0] = v;
+    const int64_t n4 = (n - head) >> 2;
+    uint4* q = reinterpret_cast<uint4*>(p + head);
+    for (int64_t i = i0; i < n4; i += stride) q[i] = make_uint4(v, v, v, v);
+    for (int64_t i = head + 4 * n4 + i0; i < n; i += stride) p[i] = v;
+}
+
+void fill_words(cudaStream_t st, uint32_t* p, int64_t n, uint32_t v) {
+    if (n <= 0) return;
+    const int64_t blocks = std::min<int64_t>(148 * 8, std::max<int64_t>(1, cdiv(n, 4 * 256)));
+    launch_k(k_fill, (unsigned)blocks, 256, 0, st, p, n, v);
+    count_launch();
+}
+
 void zero_mat(cudaStream_t st, DMat m) {
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (m.rows <= 0 || m.cols <= 0) return;
     if (m.ld == m.cols) {
-        FFB_CUDA(cudaMemsetAsync(m.ptr, 0, (size_t)m.rows * m.cols * sizeof(uint32_t), st)); pdl_fence(st);
+        fill_words(st, m.ptr, m.rows * m.cols, 0u);
         return;
     }
     for (int64_t r0 = 0; r0 < m.rows; r0 += FFB_ROWCHUNK) {

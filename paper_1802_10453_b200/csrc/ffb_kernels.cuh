@@ -124,6 +124,8 @@ void scale_rows(const Fp& f, cudaStream_t st, DMat H, DMat S, const uint32_t* v)
 void add_scaled_rows_upper(const Fp& f, cudaStream_t st, DMat X, DMat U, const uint32_t* v);
 // Set a view to zero.
 void zero_mat(cudaStream_t st, DMat m);
+// n words at p := v (a kernel launch)
+void fill_words(cudaStream_t st, uint32_t* p, int64_t n, uint32_t v);
 // Residue conversion at the host boundary.
 void convert_in(const Fp& f, cudaStream_t st, DMat dst, const void* src, int elem_bytes);
 void convert_out(cudaStream_t st, void* dst, int elem_bytes, DMat src);

@@ -1132,7 +1132,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     for (int attempt = 0; attempt < 2; ++attempt) {
         ws.release(mark1);
         r = 0;
-        FFB_CUDA(cudaMemsetAsync(dflag, 0, 4, st)); pdl_fence(st);
+        fill_words(st, (uint32_t*)dflag, 1, 0u);
         DMat YO;
         if (!exact) {  // Y * Omega, once
             DMat Om = ws.mat(n, SK);

@@ -61,6 +61,19 @@ def main():
         ldlt_device(work, w.p, cfg, ctx, out)
     with torch.cuda.stream(st):
         res["device_ms"] = timed(dev, st)
+    # the device run with an unrelated 1 GB H2D on a side stream at its start
+    side = torch.cuda.Stream()
+    d8 = torch.empty((n, n), dtype=torch.uint8, device="cuda")
+
+    def dev_busy():
+        side.wait_stream(st)
+        with torch.cuda.stream(side):
+            d8.copy_(host_a, non_blocking=True)
+        dev()
+        st.wait_stream(side)
+    with torch.cuda.stream(st):
+        res["device_ms_with_h2d"] = timed(dev_busy, st)
+    del d8
     perm = np.zeros(n, np.int64)
     dk = np.zeros(n, np.int32)
     dv = np.zeros(n, np.uint64)
