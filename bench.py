@@ -298,6 +298,17 @@ def main():
         if largest:
             roofline["largest_gemm"] = largest
 
+    # full-size correctness of the measured factorization (outside the timed region):
+    # P L D L^T P^T == A exactly, and for config 5 the rank profile matrix == generator R
+    from paper_1802_10453_b200.device import pivoting_partners, reconstruction_mismatches
+    verified = {"reconstruction_mismatches": reconstruction_mismatches(a0, f, w.p, ctx),
+                "rank": f.rank, "rank_expected": w.r or None,
+                "how": "ffb_verify_device (L D L^T by modular GEMM, entry-wise vs the input)"}
+    if w.config == 5:
+        import numpy as np
+        verified["rpm_equals_generator_R"] = bool(np.array_equal(
+            pivoting_partners(f, ctx).cpu().numpy(), configs.config5_partners(w).astype(np.int32)))
+
     e2e = None
     if not args.no_e2e and rank == 0:
         e2e = run_e2e(w, ctx, cfg, args, local)
@@ -319,7 +330,8 @@ def main():
             "frac_of_int8_peak": value / INT8_DENSE_PEAK_TOPS, "rank": rank_out,
             "rank_aware_tops": value * (2 * (rank_out ** 3 / 3 + w.n ** 2 * rank_out
                                              - rank_out ** 2 * w.n)) / ops if rank_out else 0,
-            "gpu_launches": launches, "host_syncs_per_step": syncs,
+            "gpu_launches": launches, "gpu_launches_per_step": launches // max(args.steps, 1),
+            "host_syncs_per_step": syncs, "verified": verified,
             "kernel_classes_ms": {k: round(v["ms"], 3) for k, v in prof.items()},
             "kernel_classes_launches": {k: v["launches"] for k, v in prof.items()},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks_info,

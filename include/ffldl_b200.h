@@ -121,6 +121,21 @@ int ffb_ldlt_device(ffb_context* ctx, uint64_t p, size_t n, uint32_t* d_a, size_
                     size_t ldl, int32_t* d_dkind, uint32_t* d_dval, uint32_t* d_dval2,
                     size_t* rank);
 
+/* Device-side verification, on the outputs of ffb_ldlt_device.
+ * ffb_verify_device: *mismatches = the number of entries (i, j) where P L D L^T P^T differs
+ * from A (Factorization::reconstruct, proj/include/ffldl/blockdiag.hpp:161-182; computed as
+ * one modular GEMM and an entry-wise comparison, so 0 is an exact proof of the identity).
+ * d_a is the ORIGINAL input (n x n uint32 residues, row stride lda), not overwritten. */
+int ffb_verify_device(ffb_context* ctx, uint64_t p, size_t n, const uint32_t* d_a, size_t lda,
+                      const int32_t* d_perm, const uint32_t* d_lower, size_t ldl,
+                      const int32_t* d_dkind, const uint32_t* d_dval, const uint32_t* d_dval2,
+                      size_t rank, uint64_t* mismatches);
+
+/* pivoting_matrix(f) -- proj/src/rpmtools.cpp:61-68.  Pi = P support(D) P^T has at most one
+ * nonzero per row; d_partner[i] = j where Pi(i, j) = 1, else -1 (n int32, device). */
+int ffb_pivoting_partners_device(ffb_context* ctx, size_t n, const int32_t* d_perm,
+                                 const int32_t* d_dkind, size_t rank, int32_t* d_partner);
+
 /* ffldl::plduq(b) -- proj/include/ffldl/plduq.hpp:42, proj/src/plduq.cpp:36-123.
  * Caller sizes: row_image[m], col_image[n], lower[m*min(m,n)], diag[min(m,n)],
  * upper[min(m,n)*n]; lower is m x r and upper r x n on return. */

@@ -21,7 +21,7 @@ EXPORTS = [
     "ffb_ldlt", "ffb_ldlt_compact", "ffb_ldlt_zero_leading",
     "ffb_ldlt_device", "ffb_plduq", "ffb_trssyr2k", "ffb_gemm_sub", "ffb_trmm_sub",
     "ffb_trsm_inplace", "ffb_syrdk_sub", "ffb_syr2k_sub", "ffb_gemm_device", "ffb_generate_host",
-    "ffb_generate_device", "ffb_config5_partners",
+    "ffb_generate_device", "ffb_config5_partners", "ffb_verify_device", "ffb_pivoting_partners_device",
 ]
 
 P = C.c_void_p
@@ -56,6 +56,8 @@ _SIGS = {
     "ffb_generate_host": (I, [I, SZ, SZ, U64, U64, P]),
     "ffb_generate_device": (I, [P, I, SZ, SZ, U64, U64, P]),
     "ffb_config5_partners": (I, [SZ, SZ, U64, P]),
+    "ffb_verify_device": (I, [P, U64, SZ, P, SZ, P, P, SZ, P, P, P, SZ, C.POINTER(U64)]),
+    "ffb_pivoting_partners_device": (I, [P, SZ, P, P, SZ, P]),
 }
 
 

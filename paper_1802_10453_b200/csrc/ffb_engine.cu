@@ -647,7 +647,8 @@ int guarded(ffb_context* c, F&& fn) {
     try {
         if (!c) throw Status(FFB_ERROR, "null context");
         FFB_CUDA(cudaSetDevice(c->device));
-        const uint64_t l0 = g_launches, s0 = c->syncs, u0 = c->uploads;
+        // every kernel goes through launch_k, which numbers them (pdl_launch_index)
+        const uint64_t l0 = (uint64_t)pdl_launch_index(), s0 = c->syncs, u0 = c->uploads;
         const auto t0 = std::chrono::steady_clock::now();
         const double w0 = c->sync_wait_ms;
         g_prof = &c->prof;
@@ -658,14 +659,14 @@ int guarded(ffb_context* c, F&& fn) {
             const double wall = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
             fprintf(stderr, "[ffb host] wall %.2f ms, blocked in %llu read-backs %.2f ms, launches %llu, uploads %llu\n",
                     wall, (unsigned long long)(c->syncs - s0), c->sync_wait_ms - w0,
-                    (unsigned long long)(g_launches - l0), (unsigned long long)(c->uploads - u0));
+                    (unsigned long long)((uint64_t)pdl_launch_index() - l0), (unsigned long long)(c->uploads - u0));
         }
         if (c->prof.on) {
             FFB_CUDA(cudaStreamSynchronize(c->stream));
             c->prof.flush();
         }
         g_prof = nullptr;
-        c->launches = g_launches - l0;
+        c->launches = (uint64_t)pdl_launch_index() - l0;
         c->syncs_last = c->syncs - s0;
         g_last_error.clear();
         return FFB_OK;
@@ -1070,6 +1071,44 @@ int ffb_ldlt_device(ffb_context* c, uint64_t p, size_t n, uint32_t* d_a, size_t 
         }
         FFB_CUDA(cudaStreamSynchronize(c->stream));
         c->ws_top = 0;
+    });
+}
+
+int ffb_verify_device(ffb_context* c, uint64_t p, size_t n, const uint32_t* d_a, size_t lda,
+                      const int32_t* d_perm, const uint32_t* d_lower, size_t ldl, const int32_t* d_dkind,
+                      const uint32_t* d_dval, const uint32_t* d_dval2, size_t rank, uint64_t* mismatches) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        if (rank > n) throw Status(FFB_DIMENSION_MISMATCH, "verify: rank exceeds n");
+        const int64_t N = (int64_t)n, r = (int64_t)rank;
+        ensure_workspace(c, (size_t)N * (r + N) * sizeof(uint32_t) + ((size_t)64 << 20));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat A, L;
+        A.ptr = const_cast<uint32_t*>(d_a);
+        A.ld = (int64_t)lda;
+        A.rows = A.cols = N;
+        L.ptr = const_cast<uint32_t*>(d_lower);
+        L.ld = (int64_t)ldl;
+        L.rows = N;
+        L.cols = r;
+        DDiag D{const_cast<int32_t*>(d_dkind), const_cast<uint32_t*>(d_dval), const_cast<uint32_t*>(d_dval2),
+                nullptr};
+        DMat H = ws_mat(c, N, std::max<int64_t>(r, 1)), C = ws_mat(c, N, N);
+        auto* cnt = (unsigned long long*)(c->flag + 24);  // bytes 96..103 of the flag block
+        fill_words(c->stream, (uint32_t*)cnt, 2, 0u);
+        reconstruct_mismatches(f, c->stream, A, d_perm, L, D, r, H, C, cnt);
+        *mismatches = *(const uint64_t*)readback(c, cnt, sizeof(uint64_t));
+        c->ws_top = 0;
+    });
+}
+
+int ffb_pivoting_partners_device(ffb_context* c, size_t n, const int32_t* d_perm, const int32_t* d_dkind,
+                                 size_t rank, int32_t* d_partner) {
+    return guarded(c, [&] {
+        if (rank > n) throw Status(FFB_DIMENSION_MISMATCH, "pivoting_partners: rank exceeds n");
+        pivoting_partners(c->stream, d_perm, d_dkind, (int64_t)n, (int64_t)rank, d_partner);
+        FFB_CUDA(cudaStreamSynchronize(c->stream));
     });
 }
 

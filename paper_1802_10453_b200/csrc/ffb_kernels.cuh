@@ -124,6 +124,12 @@ void scale_rows(const Fp& f, cudaStream_t st, DMat H, DMat S, const uint32_t* v)
 void add_scaled_rows_upper(const Fp& f, cudaStream_t st, DMat X, DMat U, const uint32_t* v);
 // Set a view to zero.
 void zero_mat(cudaStream_t st, DMat m);
+// Verification (ffb_verify.cu): *dcount += #{(i, j) : (L D L^T)(i, j) != A(perm i, perm j)}
+// using H (n x r) and C (n x n) as scratch; partner[perm(a)] = perm(b) over support(D).
+void reconstruct_mismatches(const Fp& f, cudaStream_t st, DMat A, const int32_t* perm, DMat L, DDiag D,
+                            int64_t r, DMat H, DMat C, unsigned long long* dcount);
+void pivoting_partners(cudaStream_t st, const int32_t* perm, const int32_t* kind, int64_t n, int64_t r,
+                       int32_t* partner);
 // n words at p := v (a kernel launch)
 void fill_words(cudaStream_t st, uint32_t* p, int64_t n, uint32_t v);
 // Residue conversion at the host boundary.

@@ -53,3 +53,29 @@ def ldlt_device(a, field, config: Optional[SytrfConfig] = None, ctx: Optional[Co
                                  out.dkind.data_ptr(), out.dval.data_ptr(), out.dval2.data_ptr(),
                                  C.byref(rank)))
     return DeviceFactorization(out.perm, out.lower, out.dkind, out.dval, out.dval2, rank.value)
+
+
+def reconstruction_mismatches(a, fact: DeviceFactorization, field, ctx: Optional[Context] = None) -> int:
+    """Entries where P L D L^T P^T != a (blockdiag.hpp:161-182), computed on the device:
+    0 proves the factorization reconstructs ``a`` exactly.  ``a`` is the original input
+    (n x n int32 residues), left unchanged."""
+    p = _p(field)
+    ctx = ctx or default_context()
+    n = a.shape[0]
+    bad = C.c_uint64(0)
+    _check(lib().ffb_verify_device(ctx.handle, p, n, a.data_ptr(), a.stride(0), fact.perm.data_ptr(),
+                                   fact.lower.data_ptr(), fact.lower.stride(0), fact.dkind.data_ptr(),
+                                   fact.dval.data_ptr(), fact.dval2.data_ptr(), fact.rank, C.byref(bad)))
+    return int(bad.value)
+
+
+def pivoting_partners(fact: DeviceFactorization, ctx: Optional[Context] = None):
+    """pivoting_matrix (rpmtools.cpp:61-68) as a partner array: int32 tensor, entry i = j
+    where Pi(i, j) = 1, else -1."""
+    import torch
+    ctx = ctx or default_context()
+    n = fact.perm.shape[0]
+    out = torch.empty(n, dtype=torch.int32, device=fact.perm.device)
+    _check(lib().ffb_pivoting_partners_device(ctx.handle, n, fact.perm.data_ptr(), fact.dkind.data_ptr(),
+                                              fact.rank, out.data_ptr()))
+    return out
