@@ -340,6 +340,22 @@ enum DKind : int32_t {
 };
 
 // Global device-side D arrays, indexed by global pivot column.
+// A read-back published directly by the producing kernel (no k_post launch): the
+// kernel writes its words to dst (mapped pinned memory), fences at system scope
+// and stores seq to *seq_ptr; the host spins on the sequence word.  dst == nullptr:
+// not requested (the caller falls back to a posted read-back).
+struct MboxPost {
+    uint32_t* dst = nullptr;
+    uint32_t* seq_ptr = nullptr;
+    uint32_t seq = 0;
+};
+// one thread: words src[0 .. n) to the mailbox, then the sequence word
+__device__ __forceinline__ void mbox_publish(const MboxPost& mp, const int32_t* src, int n) {
+    for (int i = 0; i < n; ++i) mp.dst[i] = (uint32_t)src[i];
+    __threadfence_system();
+    *(volatile uint32_t*)mp.seq_ptr = mp.seq;
+}
+
 struct DDiag {
     int32_t* kind;
     uint32_t* val;   // Scalar d / AntiDiag x / AntiTri c

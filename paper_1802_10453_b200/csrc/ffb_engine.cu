@@ -241,26 +241,48 @@ __global__ void __launch_bounds__(1024) k_post(const uint32_t* src, uint32_t* ds
     }
 }
 
-const void* readback(ffb_context* c, const void* dev, size_t bytes) {
-    static const bool dma = getenv("FFB_READBACK_DMA") != nullptr;
+static bool readback_dma() {
+    static const bool dma = getenv("FFB_READBACK_DMA") != nullptr;  // test hook
+    return dma;
+}
+
+// Reserve the next mailbox sequence number for a kernel that publishes its own
+// read-back (MboxPost); empty under FFB_READBACK_DMA.
+MboxPost mbox_reserve(ffb_context* c) {
+    MboxPost mp;
+    if (readback_dma()) return mp;
+    mp.dst = c->mbox_dev;
+    mp.seq_ptr = c->mbox_seq_dev;
+    mp.seq = ++c->mbox_seq;
+    return mp;
+}
+
+// Spin until the mailbox holds sequence mp.seq (published by k_post or by the
+// producing kernel itself); returns the mailbox words.
+const void* mbox_wait(ffb_context* c, const MboxPost& mp) {
     const auto t0 = std::chrono::steady_clock::now();
-    if (!dma && bytes <= c->mbox_cap && (bytes & 3) == 0 && (((uintptr_t)dev) & 3) == 0) {
-        const uint32_t seq = ++c->mbox_seq;
+    volatile uint32_t* hs = c->mbox_seq_host;
+    for (uint64_t spin = 1; *hs != mp.seq; ++spin)
+        if ((spin & 0xFFFF) == 0) {  // surface device faults instead of spinning forever
+            const cudaError_t q = cudaStreamQuery(c->stream);
+            if (q != cudaSuccess && q != cudaErrorNotReady) FFB_CUDA(q);
+        }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    c->sync_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    ++c->syncs;
+    c->up_top = 0;  // the publishing kernel ran after every upload issued so far
+    return c->mbox_host;
+}
+
+const void* readback(ffb_context* c, const void* dev, size_t bytes) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!readback_dma() && bytes <= c->mbox_cap && (bytes & 3) == 0 && (((uintptr_t)dev) & 3) == 0) {
+        const MboxPost mp = mbox_reserve(c);
         const int64_t words = (int64_t)(bytes / 4);
         const int threads = (int)std::min<int64_t>(1024, std::max<int64_t>(32, (cdiv(words, 4) + 31) / 32 * 32));
         launch_k(k_post, 1, threads, 0, c->stream, (const uint32_t*)dev, c->mbox_dev, words, c->mbox_seq_dev,
-                 seq);
-        volatile uint32_t* hs = c->mbox_seq_host;
-        for (uint64_t spin = 1; *hs != seq; ++spin)
-            if ((spin & 0xFFFF) == 0) {  // surface device faults instead of spinning forever
-                const cudaError_t q = cudaStreamQuery(c->stream);
-                if (q != cudaSuccess && q != cudaErrorNotReady) FFB_CUDA(q);
-            }
-        std::atomic_thread_fence(std::memory_order_acquire);
-        c->sync_wait_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-        ++c->syncs;
-        c->up_top = 0;  // the post kernel ran after every upload issued so far
-        return c->mbox_host;
+                 mp.seq);
+        return mbox_wait(c, mp);
     }
     if (bytes > c->down_cap) {
         if (c->down_host) FFB_CUDA(cudaFreeHost(c->down_host));
@@ -373,8 +395,10 @@ struct Engine {
         int32_t* out = ws_vec<int32_t>(c, s + 1);
         uint32_t* scratch = nullptr;
         if (s > 200) scratch = ws_vec<uint32_t>(c, (int64_t)leaf_scratch_words(s));
-        leaf_crout(f, st, A, drows, Lg, coff, D, out, scratch);
-        const int32_t* hb = (const int32_t*)readback(c, out, (size_t)(s + 1) * sizeof(int32_t));
+        const MboxPost mp = s <= 64 ? mbox_reserve(c) : MboxPost();
+        const int32_t* hb = (const int32_t*)(leaf_crout(f, st, A, drows, Lg, coff, D, out, scratch, mp)
+                                                 ? mbox_wait(c, mp)
+                                                 : readback(c, out, (size_t)(s + 1) * sizeof(int32_t)));
         h.rank = hb[0];
         h.perm.assign(hb + 1, hb + 1 + s);
         c->ws_top = mk.top;
@@ -514,6 +538,8 @@ struct Engine {
             PlduqIO io;
             io.upload = [this](const std::vector<int32_t>& v) { return upload(c, v); };
             io.readback = [this](const void* p, size_t b) { return readback(c, p, b); };
+            io.post = [this]() { return mbox_reserve(c); };
+            io.wait = [this](const MboxPost& mp) { return mbox_wait(c, mp); };
             io.Lo = Lo;
             io.Uo = Uo;
             io.d = pl.d;

@@ -21,7 +21,7 @@ template <bool kSmall>
 __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* A, int64_t lda,
                                                 int s, const int32_t* rows,
                                                 uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
-                                                int32_t* out) {
+                                                int32_t* out, MboxPost mp) {
     FFB_PDL_ENTRY();
     __shared__ uint32_t Ls[64][65];
     __shared__ uint32_t colb[2][64];  // residual column of the front row, double-buffered
@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* A, int64_t
             out[1 + r + a] = out[1 + r + b];
             out[1 + r + b] = tmp;
         }
+        if (mp.dst) mbox_publish(mp, out, s + 1);  // the host's read-back, without a k_post
     }
 }
 
@@ -562,13 +563,13 @@ void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tin
 bool leaf64_supported(int64_t s) { return s <= 64; }
 
 void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
-            DDiag D, int32_t* out) {
+            DDiag D, int32_t* out, const MboxPost& mp) {
     const int s = (int)A.rows;
     ProfScope ps(K_LEAF, st, 2.0 * s * s * s / 3.0, 4.0 * s * s);
     if (f.p < (1u << 16))
-        launch_k(k_leaf64<true>, 1, 256, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out);
+        launch_k(k_leaf64<true>, 1, 256, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out, mp);
     else
-        launch_k(k_leaf64<false>, 1, 256, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out);
+        launch_k(k_leaf64<false>, 1, 256, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out, mp);
     ++g_launches;
     FFB_CHECK_LAUNCH();
 }

@@ -1005,13 +1005,13 @@ __global__ void __launch_bounds__(LEAF_THREADS)
 
 size_t leaf_scratch_words(int64_t s) { return (size_t)s * s + 5 * (size_t)s + 8; }
 
-void leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
-                DDiag D, int32_t* out, uint32_t* scratch) {
+bool leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
+                DDiag D, int32_t* out, uint32_t* scratch, const MboxPost& mp) {
     const int s = (int)A.rows;
     static const bool generic_only = getenv("FFB_GENERIC_LEAF") != nullptr;  // test hook
     if (!generic_only && leaf64_supported(s)) {
-        leaf64(f, st, A, rows, Lg, coff, D, out);
-        return;
+        leaf64(f, st, A, rows, Lg, coff, D, out, mp);
+        return mp.dst != nullptr;
     }
     const bool smem = s <= LEAF_SMEM_MAX_S;
     size_t bytes = smem ? leaf_scratch_words(s) * sizeof(uint32_t) : 0;
@@ -1024,6 +1024,7 @@ void leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat 
                                                  Lg.ptr, Lg.ld, coff, D, out);
     count_launch();
     FFB_CHECK_LAUNCH();
+    return false;
 }
 
 // ===========================================================================

@@ -141,13 +141,15 @@ void gather_lower_out(cudaStream_t st, DMat out, DMat Lg, const int32_t* perm);
 // Crout leaf (Alg. 4, sytrf.cpp:35-139) on an s x s block; writes L columns
 // [coff, coff+rank) of rows rows[0..s) into Lg, D entries, and out[0] = rank,
 // out[1..s] = local permutation (image).  scratch: device buffer for large s.
-void leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg,
-                int64_t coff, DDiag D, int32_t* out, uint32_t* scratch);
+// mp: when mp.dst is set and the 64-leaf kernel runs, it publishes out[0 .. s] itself;
+// returns whether it did (else the caller reads out back)
+bool leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg,
+                int64_t coff, DDiag D, int32_t* out, uint32_t* scratch, const MboxPost& mp = MboxPost());
 size_t leaf_scratch_words(int64_t s);
 // Register-resident leaf for s <= 64 (ffb_fast.cu).
 bool leaf64_supported(int64_t s);
 void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
-            DDiag D, int32_t* out);
+            DDiag D, int32_t* out, const MboxPost& mp);
 
 // PLDUQ (plduq.cpp:36-123) of W (m x n, destroyed).  Outputs: info[0] = r,
 // info[1..m] row_image, info[1+m..1+m+n] col_image, pc[r] in info after that;

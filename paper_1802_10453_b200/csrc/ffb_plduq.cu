@@ -270,7 +270,7 @@ __device__ int batch_insert(const Fp& f, const SmemInv& inv, uint32_t* V, int ld
 // so only the flagged rows go through the sequential insertion.
 // out[0] = k, out[1..k] = independent rows (ascending).
 __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int64_t lds, int b,
-                                                    int s, int32_t* out) {
+                                                    int s, int32_t* out, MboxPost mp) {
     FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* Ss = sm;                          // b x s
@@ -305,7 +305,10 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
         if (tid < cnt) out[1 + k + tid] = i0 + bs.ins[tid];  // inserted in row order
         k += cnt;
     }
-    if (tid == 0) out[0] = k;
+    if (tid == 0) {
+        out[0] = k;
+        if (mp.dst) mbox_publish(mp, &k, 1);  // the host's read-back of k, without a k_post
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -647,14 +650,26 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     // 2. row-order leftmost elimination on M, tracking L^-1 in G.  The leading
     //    entry of row t: each thread scans a strided slice, warps reduce, one
     //    barrier combines (lead8 rotates over 2 slots, so no reset barrier).
+    // lazy: rows below the pivot accumulate unreduced sums x + (p - m) v (< p + k p^2),
+    // reduced only when a row becomes the pivot row (its leading search) or when a
+    // coefficient is read; exact per-term reduction otherwise
+    const bool lazy = (uint64_t)k * (f.p - 1) * (f.p - 1) + f.p < (1ull << 32);
     for (int t = 0; t < k; ++t) {
-        const uint32_t* rt = M + (size_t)t * Cx;
+        uint32_t* rt = M + (size_t)t * Cx;
         int mine = Cx;
-        for (int j = tid; j < Cx; j += 256)
-            if (rt[j] != 0) {
-                mine = j;
-                break;
+        if (lazy) {  // reduce the whole row (it feeds the elimination), first nonzero
+            for (int j = tid; j < Cx; j += 256) {
+                const uint32_t v = red32(f, rt[j]);
+                rt[j] = v;
+                if (v != 0 && mine == Cx) mine = j;
             }
+        } else {
+            for (int j = tid; j < Cx; j += 256)
+                if (rt[j] != 0) {
+                    mine = j;
+                    break;
+                }
+        }
         mine = __reduce_min_sync(0xffffffffu, mine);
         if (lane == 0) lead8[t & 1][wp] = mine;
         __syncthreads();
@@ -674,11 +689,33 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         const uint32_t* gt = G + (size_t)t * k;
         for (int i = t + 1 + wp; i < k; i += 8) {
             uint32_t* ri = M + (size_t)i * Cx;
-            const uint32_t c = ri[jp];
+            const uint32_t c = lazy ? red32(f, ri[jp]) : ri[jp];
             __syncwarp();
             if (!c) continue;
             const uint32_t m = fmul(f, c, il);
-            for (int j = jp + lane; j < Cx; j += 32) ri[j] = fmsub(f, ri[j], m, rt[j]);
+            int j = jp + lane;
+            if (lazy) {  // 4 independent load pairs in flight per lane
+                const uint32_t mn = f.p - m;
+                for (; j + 96 < Cx; j += 128) {
+                    const uint32_t a0 = ri[j], a1 = ri[j + 32], a2 = ri[j + 64], a3 = ri[j + 96];
+                    const uint32_t b0 = rt[j], b1 = rt[j + 32], b2 = rt[j + 64], b3 = rt[j + 96];
+                    ri[j] = a0 + mn * b0;
+                    ri[j + 32] = a1 + mn * b1;
+                    ri[j + 64] = a2 + mn * b2;
+                    ri[j + 96] = a3 + mn * b3;
+                }
+                for (; j < Cx; j += 32) ri[j] += mn * rt[j];
+            } else {
+                for (; j + 96 < Cx; j += 128) {
+                    const uint32_t a0 = ri[j], a1 = ri[j + 32], a2 = ri[j + 64], a3 = ri[j + 96];
+                    const uint32_t b0 = rt[j], b1 = rt[j + 32], b2 = rt[j + 64], b3 = rt[j + 96];
+                    ri[j] = fmsub(f, a0, m, b0);
+                    ri[j + 32] = fmsub(f, a1, m, b1);
+                    ri[j + 64] = fmsub(f, a2, m, b2);
+                    ri[j + 96] = fmsub(f, a3, m, b3);
+                }
+                for (; j < Cx; j += 32) ri[j] = fmsub(f, ri[j], m, rt[j]);
+            }
             uint32_t* gi = G + (size_t)i * k;
             for (int j = lane; j <= t; j += 32) gi[j] = fmsub(f, gi[j], m, gt[j]);
         }
@@ -1169,13 +1206,14 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     gemm(f, st, GEMM_SUB, Sc, Gc, false, UO.sub(0, 0, r, SK), false, bc, SK, r);
                 }
                 mark();
+                const MboxPost mp = io.post ? io.post() : MboxPost();
                 {
                     ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-                    launch_k(k_row_detect, 1, 256, rd_smem, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo);
+                    launch_k(k_row_detect, 1, 256, rd_smem, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp);
                     ++g_launches;
                     FFB_CHECK_LAUNCH();
                 }
-                const int k = *(const int32_t*)io.readback(dinfo, 4);
+                const int k = *(const int32_t*)(mp.dst ? io.wait(mp) : io.readback(dinfo, 4));
                 mark();
                 if (k == 0) {
                     mark(); mark(); mark();
@@ -1210,6 +1248,20 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                                                         d_prow, d_pcol, r, dflag, si_off);
                     ++g_launches;
                     FFB_CHECK_LAUNCH();
+                }
+                static const char* dump = getenv("FFB_PLDUQ_DUMP");  // diagnostics: one top-level R_I
+                static int dumped = 0;
+                if (dump && !dumped && n >= 16384 && c0 >= 20 * B) {
+                    dumped = 1;
+                    std::vector<uint32_t> h((size_t)k * n);
+                    FFB_CUDA(cudaStreamSynchronize(st));
+                    FFB_CUDA(cudaMemcpy2D(h.data(), n * 4, RI.ptr, RI.ld * 4, n * 4, k, cudaMemcpyDeviceToHost));
+                    if (FILE* fd = fopen(dump, "wb")) {
+                        const int64_t hdr[2] = {k, n};
+                        fwrite(hdr, sizeof(hdr), 1, fd);
+                        fwrite(h.data(), 4, h.size(), fd);
+                        fclose(fd);
+                    }
                 }
                 static FILE* jtr = getenv("FFB_PLDUQ_JTRACE") ? fopen(getenv("FFB_PLDUQ_JTRACE"), "a") : nullptr;
                 if (jtr) {  // diagnostics: k, n, candidate count, pivot column positions
@@ -1368,9 +1420,9 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         int32_t* info;
         FFB_CUDA(cudaMalloc(&info, (2 * RD_MAX_B + 16) * 4));
-        launch_k(k_row_detect, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info);
+        launch_k(k_row_detect, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info, MboxPost());
         FFB_CUDA(cudaEventRecord(e[0], st));
-        for (int i = 0; i < reps; ++i) launch_k(k_row_detect, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info);
+        for (int i = 0; i < reps; ++i) launch_k(k_row_detect, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info, MboxPost());
         FFB_CUDA(cudaEventRecord(e[1], st));
         FFB_CUDA(cudaEventSynchronize(e[1]));
         FFB_CUDA(cudaEventElapsedTime(&t, e[0], e[1]));

@@ -41,6 +41,9 @@ struct Workspace {
 struct PlduqIO {
     std::function<const int32_t*(const std::vector<int32_t>&)> upload;
     std::function<const void*(const void*, size_t)> readback;
+    // optional: reserve a kernel-published read-back, and wait for it
+    std::function<MboxPost()> post;
+    std::function<const void*(const MboxPost&)> wait;
     DMat Lo, Uo;        // m x min(m,n) and min(m,n) x n outputs
     uint32_t* d = nullptr;
     uint32_t* dinv = nullptr;

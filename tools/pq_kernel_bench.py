@@ -55,8 +55,23 @@ def main():
         m = row_detect_input(rng, p, 128, 144, k) if k else np.zeros((128, 144), np.int64)
         ms, out = bench(ctx, p, 0, m)
         print(json.dumps(dict(kernel="row_detect", b=128, s=144, k=k, k_found=out[0], us=round(ms[0] * 1e3, 2))))
-    for k, n, nz in ((25, 8192, 20), (25, 8192, 400), (64, 8192, 40), (128, 16384, 100)):
-        ms, out = bench(ctx, p, 1, crp_input(rng, p, k, n, nz))
+    cases = [tuple(int(x) for x in a.split(",")) for a in sys.argv[1:]] or \
+        [(25, 8192, 20), (25, 8192, 400), (64, 8192, 40), (128, 16384, 100), (26, 16384, 33)]
+    dump = os.environ.get("PQ_DUMP")  # an R_I written by FFB_PLDUQ_DUMP
+    if dump and os.path.exists(dump):
+        hdr = np.fromfile(dump, np.int64, 2)
+        ri = np.fromfile(dump, np.uint32, offset=16).reshape(int(hdr[0]), int(hdr[1]))
+        print("dump: k", ri.shape[0], "n", ri.shape[1], "nonzeros/row", (ri != 0).sum(1).mean(),
+              "nonzero columns", int((ri != 0).any(0).sum()))
+        cases = [("dump", ri)] + cases
+    for case in cases:
+        if case[0] == "dump":
+            m = case[1]
+            k, n, nz = m.shape[0], m.shape[1], -1
+        else:
+            k, n, nz = case
+            m = crp_input(rng, p, k, n, nz)
+        ms, out = bench(ctx, p, 1, m)
         print(json.dumps(dict(kernel="crp", k=k, n=n, nz=nz, fail=out[0],
                               crp_list_us=round(ms[0] * 1e3, 2), finish_us=round(ms[1] * 1e3, 2),
                               jsorted=bool(all(out[1 + i] < out[2 + i] for i in range(k - 1))))))
