@@ -245,7 +245,20 @@ struct SmemInv {
 };
 __device__ inline SmemInv stage_inverses(const Fp& f, uint32_t* buf /* SINV_MAX words */) {
     if (!f.inv || f.p > SINV_MAX) return SmemInv{nullptr};
-    for (uint32_t a = threadIdx.x; a < f.p; a += blockDim.x) buf[a] = __ldcg(f.inv + a);
+    // 8 loads in flight per thread (one round trip for p <= 8 * blockDim)
+    for (uint32_t a0 = threadIdx.x; a0 < f.p; a0 += 8 * blockDim.x) {
+        uint32_t v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t a = a0 + u * blockDim.x;
+            v[u] = a < f.p ? __ldcg(f.inv + a) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t a = a0 + u * blockDim.x;
+            if (a < f.p) buf[a] = v[u];
+        }
+    }
     __syncthreads();
     return SmemInv{buf};
 }

@@ -17,6 +17,30 @@ namespace ffb {
 
 namespace {
 
+// Leaf outputs (after a barrier): L columns [coff, coff + r) of the leaf rows
+// (warp w writes rows w, w+8, ...: coalesced row segments), and
+// out = [r, pivot order, pivotless rows ascending] -- to HBM and, when requested,
+// to the host mailbox by all threads in parallel (fence, barrier, sequence word).
+__device__ __forceinline__ void leaf_epilogue(int s, int r, const int32_t* srows, const uint32_t (*Ls)[65],
+                                              const int32_t* order, const int32_t* pless, uint32_t* Lg,
+                                              int64_t ldL, int64_t coff, int32_t* out, const MboxPost& mp) {
+    const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
+    for (int i = wp; i < s; i += 8) {
+        uint32_t* dst = Lg + (int64_t)srows[i] * ldL + coff;
+        for (int c = lane; c < r; c += 32) dst[c] = Ls[i][c];
+    }
+    for (int e = tid; e <= s; e += blockDim.x) {
+        const int32_t v = e == 0 ? r : (e <= r ? order[e - 1] : pless[e - 1 - r]);
+        out[e] = v;
+        if (mp.dst) mp.dst[e] = (uint32_t)v;
+    }
+    if (mp.dst) {
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) *(volatile uint32_t*)mp.seq_ptr = mp.seq;
+    }
+}
+
 template <bool kSmall>
 __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* A, int64_t lda,
                                                 int s, const int32_t* rows,
@@ -27,10 +51,13 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* A, int64_t
     __shared__ uint32_t colb[2][64];  // residual column of the front row, double-buffered
     __shared__ uint32_t col2[64];     // residual column of the 2x2 partner
     __shared__ int32_t order[64];
+    __shared__ int32_t pless[64];   // pivotless rows in discovery (= ascending) order
+    __shared__ int32_t srows[64];
     __shared__ uint32_t sinv[SINV_MAX];
     const Ar<kSmall> ar(f);
     const int tid = threadIdx.x, tx = tid & 63, ty = tid >> 6, lane = tid & 31;
     const uint32_t one = 1 % f.p;
+    if (tid < s) srows[tid] = __ldcg(rows + tid);
     uint32_t S[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
@@ -57,7 +84,7 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* A, int64_t
         const uint64_t msk = (((uint64_t)b1 << 32) | b0) & active;
         const int j = msk ? __ffsll((long long)msk) - 1 : s;
         if (j >= s) {  // pivotless (sytrf.cpp:82-85)
-            if (tid == 0) out[1 + (s - 1 - npl)] = p1;
+            if (tid == 0) pless[npl] = p1;
             ++npl;
             active &= ~(1ull << p1);
             continue;
@@ -132,20 +159,199 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* A, int64_t
         r += 2;
     }
     __syncthreads();
-    // L columns [coff, coff + r) of the leaf rows, one coalesced row write each
-    for (int e = tid; e < s * r; e += 256) {
-        const int i = e / r, c = e % r;
-        Lg[(int64_t)rows[i] * ldL + coff + c] = Ls[i][c];
-    }
-    if (tid == 0) {
-        out[0] = r;
-        for (int t = 0; t < r; ++t) out[1 + t] = order[t];
-        for (int a = 0, b = npl - 1; a < b; ++a, --b) {  // pivotless rows: ascending
-            const int32_t tmp = out[1 + r + a];
-            out[1 + r + a] = out[1 + r + b];
-            out[1 + r + b] = tmp;
+    leaf_epilogue(s, r, srows, Ls, order, pless, Lg, ldL, coff, out, mp);
+}
+
+// Lazily reduced leaf for 2 <= p < 4096 (same algorithm and outputs as k_leaf64).
+// 4 warps: warp w owns columns 16w .. 16w+15, lane l rows l and l+32 (32 int32
+// registers per thread, static indices).  A step:
+//   * the owner lane of row p1 (= column p1, mod p: S stays symmetric) in every
+//     warp stores the warp's 16 raw words of that row (4 x 16-byte stores); barrier;
+//   * every lane reduces the residual of its own two rows, c_i; ballot -> first
+//     active nonzero (sytrf.cpp:78-81);
+//   * row multipliers l_i = c_i x^-1 are computed redundantly by every warp and the
+//     16 column multipliers a warp needs are shuffled in: the update
+//     S[i][k] -= c_i l_k is 32 IMADs per thread, no reduction and no second barrier.
+// Entries only decrease, by < p^2 per pivot (< 1.5 p^2 per pivot for an AntiTri 2x2,
+// char 2), so after <= 64 pivots S lies in (-96 p^2, p): int32-safe, and
+// S + 96 p^2 < 2^32 is reduced by 32-bit Barrett.
+__device__ __forceinline__ uint32_t lz_red(const Fp& f, int32_t v, uint32_t off) {
+    return red32(f, (uint32_t)v + off);
+}
+__global__ void __launch_bounds__(128) k_leaf64_lazy(Fp f, const uint32_t* A, int64_t lda,
+                                                     int s, const int32_t* rows,
+                                                     uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
+                                                     int32_t* out, MboxPost mp) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __shared__ uint32_t Ls[64][65];                  // input tile first, then L
+    __shared__ __align__(16) int32_t rowb[2][64];    // raw residual row of the front
+    __shared__ __align__(16) int32_t row2[64];       // raw residual row of the 2x2 partner
+    __shared__ int32_t order[64];
+    __shared__ int32_t pless[64];
+    __shared__ int32_t srows[64];
+    __shared__ uint32_t sinv[SINV_MAX];
+    const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
+    const uint32_t one = 1 % f.p;
+    const uint32_t off = 96u * f.p * f.p;
+    const SmemInv inv = stage_inverses(f, sinv);  // independent of the predecessor
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    {  // coalesced tile load, all loads of a thread in flight at once
+        uint32_t v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            const int e = tid + 128 * u, i = e >> 6, k = e & 63;
+            v[u] = (i < s && k < s) ? __ldcg(A + (int64_t)i * lda + k) : 0u;
         }
-        if (mp.dst) mbox_publish(mp, out, s + 1);  // the host's read-back, without a k_post
+        if (tid < 64) srows[tid] = tid < s ? __ldcg(rows + tid) : 0;
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            const int e = tid + 128 * u;
+            Ls[e >> 6][e & 63] = v[u];
+        }
+    }
+    __syncthreads();
+    int32_t S0[16], S1[16];  // S[lane][16wp + t], S[lane + 32][16wp + t]
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+        S0[t] = (int32_t)Ls[lane][16 * wp + t];
+        S1[t] = (int32_t)Ls[lane + 32][16 * wp + t];
+    }
+    __syncthreads();
+    for (int e = tid; e < 64 * 65; e += 128) (&Ls[0][0])[e] = 0;
+    uint64_t active = (s == 64) ? ~0ull : ((1ull << s) - 1);
+    int r = 0, npl = 0, buf = 0;
+    const bool lo = wp < 2;  // this warp's columns are rows < 32
+    for (int p1 = 0; p1 < s; ++p1) {
+        if (!((active >> p1) & 1)) continue;  // consumed as a 2x2 partner (uniform)
+        int32_t* rb = rowb[buf];
+        buf ^= 1;
+        if (lane == (p1 & 31)) {
+            int4* d = reinterpret_cast<int4*>(rb + 16 * wp);
+            if (p1 < 32) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) d[q] = make_int4(S0[4 * q], S0[4 * q + 1], S0[4 * q + 2], S0[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) d[q] = make_int4(S1[4 * q], S1[4 * q + 1], S1[4 * q + 2], S1[4 * q + 3]);
+            }
+        }
+        __syncthreads();
+        const uint32_t c0 = lz_red(f, rb[lane], off), c1 = lz_red(f, rb[lane + 32], off);
+        const uint32_t b0 = __ballot_sync(0xffffffffu, c0 != 0);
+        const uint32_t b1 = __ballot_sync(0xffffffffu, c1 != 0);
+        const uint64_t msk = (((uint64_t)b1 << 32) | b0) & active;
+        const int j = msk ? __ffsll((long long)msk) - 1 : s;
+        if (j >= s) {  // pivotless (sytrf.cpp:82-85)
+            if (tid == 0) pless[npl] = p1;
+            ++npl;
+            active &= ~(1ull << p1);
+            continue;
+        }
+        if (j == p1) {  // 1x1 pivot (sytrf.cpp:87-97)
+            const uint32_t x = __shfl_sync(0xffffffffu, p1 < 32 ? c0 : c1, p1 & 31);
+            const uint32_t xi = inv(f, x);
+            active &= ~(1ull << p1);
+            const uint32_t l0 = red32(f, c0 * xi), l1 = red32(f, c1 * xi);  // row multipliers
+            const uint32_t lsrc = lo ? l0 : l1;
+#pragma unroll
+            for (int t = 0; t < 16; ++t) {
+                const int32_t lk = (int32_t)__shfl_sync(0xffffffffu, lsrc, (16 * wp + t) & 31);
+                S0[t] -= (int32_t)c0 * lk;
+                S1[t] -= (int32_t)c1 * lk;
+            }
+            if (wp == 0) {
+                if ((active >> lane) & 1) Ls[lane][r] = l0;
+                if ((active >> (lane + 32)) & 1) Ls[lane + 32][r] = l1;
+                if (lane == 0) {
+                    Ls[p1][r] = one;
+                    D.kind[coff + r] = D_SCALAR;
+                    D.val[coff + r] = x;
+                    D.val2[coff + r] = 0;
+                    D.inv[coff + r] = xi;
+                    order[r] = p1;
+                }
+            }
+            r += 1;
+            continue;
+        }
+        // 2x2 antidiagonal pivot pairing p1 with p2 = j (sytrf.cpp:99-131)
+        const int p2 = j;
+        if (lane == (p2 & 31)) {
+            int4* d = reinterpret_cast<int4*>(row2 + 16 * wp);
+            if (p2 < 32) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) d[q] = make_int4(S0[4 * q], S0[4 * q + 1], S0[4 * q + 2], S0[4 * q + 3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) d[q] = make_int4(S1[4 * q], S1[4 * q + 1], S1[4 * q + 2], S1[4 * q + 3]);
+            }
+        }
+        __syncthreads();
+        const uint32_t d0 = lz_red(f, row2[lane], off), d1 = lz_red(f, row2[lane + 32], off);
+        const uint32_t x = __shfl_sync(0xffffffffu, p2 < 32 ? c0 : c1, p2 & 31);
+        const uint32_t y = __shfl_sync(0xffffffffu, p2 < 32 ? d0 : d1, p2 & 31);
+        const uint32_t xi = inv(f, x);
+        const uint32_t y_eff = f.char2 ? y : fhalve(f, y);
+        const uint32_t yd = f.char2 ? y : 0;
+        active &= ~((1ull << p1) | (1ull << p2));
+        // row multipliers of this lane's rows: l2 = x^-1 c, l1 = x^-1 (d - y_eff l2)
+        const uint32_t l2a = red32(f, xi * c0), l2b = red32(f, xi * c1);
+        const uint32_t l1a = red32(f, xi * red32(f, d0 + f.p * f.p - y_eff * l2a));
+        const uint32_t l1b = red32(f, xi * red32(f, d1 + f.p * f.p - y_eff * l2b));
+        // S -= x l1_i l2_k + x l2_i l1_k (+ yd l2_i l2_k)
+        const int32_t ga = (int32_t)(red32(f, x * l1a) + red32(f, yd * l2a));
+        const int32_t gb = (int32_t)(red32(f, x * l1b) + red32(f, yd * l2b));
+        const int32_t ba = (int32_t)red32(f, x * l2a), bb = (int32_t)red32(f, x * l2b);
+        const uint32_t s2 = lo ? l2a : l2b, s1 = lo ? l1a : l1b;
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+            const int src = (16 * wp + t) & 31;
+            const int32_t l2k = (int32_t)__shfl_sync(0xffffffffu, s2, src);
+            const int32_t l1k = (int32_t)__shfl_sync(0xffffffffu, s1, src);
+            S0[t] -= ga * l2k + ba * l1k;
+            S1[t] -= gb * l2k + bb * l1k;
+        }
+        if (wp == 0) {
+            if ((active >> lane) & 1) {
+                Ls[lane][r] = l1a;
+                Ls[lane][r + 1] = l2a;
+            }
+            if ((active >> (lane + 32)) & 1) {
+                Ls[lane + 32][r] = l1b;
+                Ls[lane + 32][r + 1] = l2b;
+            }
+            if (lane == 0) {
+                Ls[p1][r] = one;
+                Ls[p2][r + 1] = one;
+                Ls[p2][r] = f.char2 ? 0 : red32(f, xi * y_eff);
+                const int32_t hk = yd ? D_ANTITRI_HEAD : D_ANTIDIAG_HEAD;
+                D.kind[coff + r] = hk;
+                D.kind[coff + r + 1] = hk + 1;
+                D.val[coff + r] = D.val[coff + r + 1] = x;
+                D.val2[coff + r] = D.val2[coff + r + 1] = yd;
+                D.inv[coff + r] = D.inv[coff + r + 1] = xi;
+                order[r] = p1;
+                order[r + 1] = p2;
+            }
+        }
+        r += 2;
+    }
+    __syncthreads();
+    // L columns [coff, coff + r) of the leaf rows: thread t < s writes row t
+    if (tid < s) {
+        uint32_t* d = Lg + (int64_t)srows[tid] * ldL + coff;
+#pragma unroll 8
+        for (int c = 0; c < r; ++c) d[c] = Ls[tid][c];
+    }
+    for (int e = tid; e <= s; e += 128) {
+        const int32_t v = e == 0 ? r : (e <= r ? order[e - 1] : pless[e - 1 - r]);
+        out[e] = v;
+        if (mp.dst) mp.dst[e] = (uint32_t)v;
+    }
+    if (mp.dst) {
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) *(volatile uint32_t*)mp.seq_ptr = mp.seq;
     }
 }
 
@@ -264,6 +470,24 @@ __global__ void __launch_bounds__(256) k_trsm_small(Fp f, const uint32_t* T, int
     for (int u = 0; u < 16; ++u) Ts[wp + 8 * (u >> 1)][lane + 32 * (u & 1)] = bv[u];  // Ts is free now
     __syncthreads();
     const int j = tid & 63, i0 = tid >> 6;  // a warp shares its rows: X[i][k] is a broadcast
+    if (kMode == 0) {  // p < 4096: 64 products < 2^24 sum in 32 bits
+        uint32_t acc[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) acc[q] = 0;
+        for (int k = 0; k < n; ++k) {
+            const uint32_t bk = Ts[k][j];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) acc[q] += X[i0 + 4 * q][k] * bk;
+        }
+        if (j < bc) {
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+                const int i = i0 + 4 * q;
+                if (i < n) B[(int64_t)i * ldb + c0 + j] = red32(f, acc[q]);
+            }
+        }
+        return;
+    }
     uint64_t acc[16];
 #pragma unroll
     for (int q = 0; q < 16; ++q) acc[q] = 0;
@@ -566,7 +790,10 @@ void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, 
             DDiag D, int32_t* out, const MboxPost& mp) {
     const int s = (int)A.rows;
     ProfScope ps(K_LEAF, st, 2.0 * s * s * s / 3.0, 4.0 * s * s);
-    if (f.p < (1u << 16))
+    static const bool eager = getenv("FFB_LEAF_EAGER") != nullptr;  // A/B hook
+    if (f.p < 4096u && !eager)
+        launch_k(k_leaf64_lazy, 1, 128, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out, mp);
+    else if (f.p < (1u << 16))
         launch_k(k_leaf64<true>, 1, 256, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out, mp);
     else
         launch_k(k_leaf64<false>, 1, 256, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out, mp);

@@ -357,12 +357,15 @@ __global__ void k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int6
         const int64_t c4 = cols >> 2;
         const uint4* s4 = reinterpret_cast<const uint4*>(s);
         uint4* d4 = reinterpret_cast<uint4*>(d);
-        for (; j + step < c4; j += 2 * step) {
-            const uint4 a = __ldcg(s4 + j), b = __ldcg(s4 + j + step);
-            d4[j] = a;
-            d4[j + step] = b;
+        for (; j + 3 * step < c4; j += 4 * step) {
+            const uint4 a = __ldcg(s4 + j), b = __ldcg(s4 + j + step), c = __ldcg(s4 + j + 2 * step),
+                        e = __ldcg(s4 + j + 3 * step);
+            __stcs(d4 + j, a);
+            __stcs(d4 + j + step, b);
+            __stcs(d4 + j + 2 * step, c);
+            __stcs(d4 + j + 3 * step, e);
         }
-        for (; j < c4; j += step) d4[j] = __ldcg(s4 + j);
+        for (; j < c4; j += step) __stcs(d4 + j, __ldcg(s4 + j));
         for (int64_t t = 4 * c4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cols; t += step) d[t] = s[t];
         return;
     }
@@ -661,7 +664,8 @@ void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t c
     if (dst.rows <= 0 || dst.cols <= 0) return;
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
-        launch_k(k_gather_lg, rowgrid(nr, dst.cols), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, Lg.ptr,
+        // 16 words (four 16-byte vectors) per thread: a few CTAs per row, loads in flight
+        launch_k(k_gather_lg, rowgrid(nr, dst.cols, 256, 16), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, Lg.ptr,
                                                            Lg.ld, ids + r0, col0, dst.cols);
         count_launch();
     }
