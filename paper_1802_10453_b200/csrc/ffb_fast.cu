@@ -508,6 +508,93 @@ __global__ void __launch_bounds__(256) k_trsm_small(Fp f, const uint32_t* T, int
     }
 }
 
+// Unit lower solve for n <= 64 by blocked forward substitution, X = T^-1 B, in
+// place.  CTA: 64 columns of B; warp w owns columns 8w .. 8w+7 and solves them
+// alone (no block barrier after staging): lane = 4 c + q handles column c's dot
+// products over k = q (mod 4) for a block of 4 rows, the partial sums meet by
+// xor-shuffles and lane q = 0 solves the block's 4 x 4 diagonal part.  Xs row stride 72 words: the 32 lanes of a warp hit 32 banks.
+// kMode 0 (p < 4096): 32-bit sums (63 products < 2^24); 1 (p < 2^23): 64-bit
+// sums; 2: reduce per product.  Only the strict lower part of T is read.
+template <int kMode>
+__global__ void __launch_bounds__(256) k_trsm_fwd(Fp f, const uint32_t* T, int64_t ldt, int n, uint32_t* B,
+                                                  int64_t ldb, int64_t ncols) {
+    FFB_PDL_ENTRY();
+    __shared__ uint32_t Ts[64][65];
+    __shared__ uint32_t Xs[64][72];
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    const int64_t c0 = (int64_t)blockIdx.x * 64;
+    const int bc = (int)std::min<int64_t>(64, ncols - c0);
+    {  // stage T (strict lower) and the B tile, all loads of a thread in flight
+        uint32_t tv[16], bv[16];
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int e = tid + 256 * u, i = e >> 6, k = e & 63;
+            tv[u] = (i < n && k < i) ? __ldcg(T + (int64_t)i * ldt + k) : 0u;
+            bv[u] = (i < n && k < bc) ? __ldcg(B + (int64_t)i * ldb + c0 + k) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 16; ++u) {
+            const int e = tid + 256 * u, i = e >> 6, k = e & 63;
+            Ts[i][k] = tv[u];
+            Xs[i][k] = bv[u];
+        }
+    }
+    __syncthreads();
+    const int c = 8 * wp + (lane >> 2), q = lane & 3;
+    // blocks of 4 rows: partial sums over the solved rows k < i0 (4-way split over the
+    // lanes), then lane q = 0 finishes the 4 x 4 unit-lower diagonal block serially
+    for (int i0 = 0; i0 < n; i0 += 4) {
+        uint32_t sum[4];
+        if (kMode == 0) {
+            uint32_t acc[4] = {0, 0, 0, 0};
+            for (int k = q; k < i0; k += 4) {
+                const uint32_t xk = Xs[k][c];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) acc[r] += Ts[i0 + r][k] * xk;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], 1);
+                acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], 2);
+                sum[r] = red32(f, acc[r]);
+            }
+        } else {
+            uint64_t acc[4] = {0, 0, 0, 0};
+            for (int k = q; k < i0; k += 4) {
+                const uint32_t xk = Xs[k][c];
+#pragma unroll
+                for (int r = 0; r < 4; ++r) {
+                    const uint64_t prod = (uint64_t)Ts[i0 + r][k] * xk;
+                    acc[r] = kMode == 2 ? (uint64_t)red64(f, acc[r] + prod) : acc[r] + prod;
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                if (kMode == 2) acc[r] = red64(f, acc[r]);
+                acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], 1);
+                acc[r] += __shfl_xor_sync(0xffffffffu, acc[r], 2);
+                sum[r] = red64(f, acc[r]);
+            }
+        }
+        if (q == 0) {
+            uint32_t x[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                uint32_t v = fsub(f, Xs[i0 + r][c], sum[r]);
+#pragma unroll
+                for (int t = 0; t < r; ++t) v = fsub(f, v, fmul(f, Ts[i0 + r][i0 + t], x[t]));
+                x[r] = v;
+                Xs[i0 + r][c] = v;
+            }
+        }
+        __syncwarp();
+    }
+    if (c < bc) {  // lanes q write rows q, q+4, ... of column c (each row segment of 8 columns
+                   // of the warp is one 32-byte sector)
+        for (int i = q; i < n; i += 4) B[(int64_t)i * ldb + c0 + c] = Xs[i][c];
+    }
+}
+
 // Panel solve: rows [r0, r0 + nb) (nb <= 256, 64-aligned r0), column tile of
 // 32: x_b = Tinv_b (b_b - sum_{c<b} T_{bc} x_c) block by block, in place.
 // The four diagonal inverses and the strictly lower 64x64 couplings are read
@@ -807,10 +894,18 @@ void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
     if (n <= 64) {  // one launch: inverse and apply per 64-column tile
         ProfScope ps(K_TRSM, st, (double)n * n * B.cols, 8.0 * n * B.cols, n, B.cols, 2);
         const unsigned g = (unsigned)cdiv(B.cols, 64);
-        if (f.p < 4096u) launch_k(k_trsm_small<0>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
-        else if (f.p < (1u << 23))
-            launch_k(k_trsm_small<1>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
-        else launch_k(k_trsm_small<2>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
+        static const bool inv_path = getenv("FFB_TRSM_INV") != nullptr;  // A/B hook
+        if (inv_path) {
+            if (f.p < 4096u) launch_k(k_trsm_small<0>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
+            else if (f.p < (1u << 23))
+                launch_k(k_trsm_small<1>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
+            else launch_k(k_trsm_small<2>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
+        } else {
+            if (f.p < 4096u) launch_k(k_trsm_fwd<0>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
+            else if (f.p < (1u << 23))
+                launch_k(k_trsm_fwd<1>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
+            else launch_k(k_trsm_fwd<2>, g, 256, 0, st, f, T.ptr, T.ld, (int)n, B.ptr, B.ld, B.cols);
+        }
         ++g_launches;
         FFB_CHECK_LAUNCH();
         return;
