@@ -379,7 +379,11 @@ struct Engine {
     HFact dispatch(DMat A, const std::vector<int32_t>& rows, const int32_t* drows, int64_t coff) {
         const int64_t saved = g_node;
         g_node = A.rows;  // trace tag: the innermost node a launch belongs to
-        HFact h = is_leaf(A.rows) ? crout(A, rows, drows, coff) : recursive_step(A, rows, drows, coff);
+        const int64_t teff = variant == FFB_VARIANT_RECURSIVE ? 1 : T;
+        HFact h = is_leaf(A.rows)                                ? crout(A, rows, drows, coff)
+                  : (variant != FFB_VARIANT_CROUT && node128_supported(f, A.rows, teff))
+                      ? node_fused(A, rows, drows, coff)
+                      : recursive_step(A, rows, drows, coff);
         g_node = saved;
         return h;
     }
@@ -401,6 +405,50 @@ struct Engine {
                                                  : readback(c, out, (size_t)(s + 1) * sizeof(int32_t)));
         h.rank = hb[0];
         h.perm.assign(hb + 1, hb + 1 + s);
+        c->ws_top = mk.top;
+        return h;
+    }
+
+    // recursive_step of a node whose children are leaves, fused into one launch
+    // (k_node128); when Y != 0 the kernel hands over after the Schur updates and the
+    // host continues with zero_leading_pairs exactly as recursive_step would.
+    HFact node_fused(DMat A, const std::vector<int32_t>& rows, const int32_t* drows_in, int64_t coff) {
+        const int64_t s = A.rows, m = s / 2, ns = s - m;
+        ensure_rows(A, s);
+        const WsMark mk{c->ws_top};
+        const int32_t* drows = drows_in ? drows_in : upload(c, rows);
+        int32_t* out = ws_vec<int32_t>(c, s + 2);
+        uint32_t* yout = ws_vec<uint32_t>(c, m * ns);
+        const MboxPost mp = mbox_reserve(c);
+        node128(f, st, A, drows, Lg, coff, D, yout, out, mp);
+        const int32_t* hb = (const int32_t*)(mp.dst ? mbox_wait(c, mp)
+                                                     : readback(c, out, (size_t)(s + 2) * sizeof(int32_t)));
+        HFact h;
+        if (hb[0] == 0) {
+            h.rank = hb[1];
+            h.perm.assign(hb + 2, hb + 2 + s);
+            c->ws_top = mk.top;
+            return h;
+        }
+        const int64_t r1 = hb[1];
+        std::vector<int32_t> perm1(hb + 2, hb + 2 + m);
+        std::vector<int32_t> rowsz;  // rows of [[0 Y],[Y^t Z]] (sytrf.cpp:317)
+        rowsz.reserve(s - r1);
+        for (int64_t i = r1; i < m; ++i) rowsz.push_back(rows[perm1[i]]);
+        for (int64_t i = m; i < s; ++i) rowsz.push_back(rows[i]);
+        DMat Y;
+        Y.ptr = yout;
+        Y.ld = ns;
+        Y.rows = m - r1;
+        Y.cols = ns;
+        HFact f2 = zero_leading_pairs(Y, A.sub(m, m, ns, ns), rowsz, coff + r1);
+        h.rank = r1 + f2.rank;  // (:332-334)
+        h.perm.resize(s);
+        for (int64_t pos = 0; pos < r1; ++pos) h.perm[pos] = perm1[pos];
+        for (int64_t pos = r1; pos < s; ++pos) {
+            const int64_t cix = f2.perm[pos - r1];
+            h.perm[pos] = cix < m - r1 ? perm1[r1 + cix] : (int32_t)(m + (cix - (m - r1)));
+        }
         c->ws_top = mk.top;
         return h;
     }

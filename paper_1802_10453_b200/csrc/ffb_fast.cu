@@ -178,52 +178,60 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* A, int64_t
 __device__ __forceinline__ uint32_t lz_red(const Fp& f, int32_t v, uint32_t off) {
     return red32(f, (uint32_t)v + off);
 }
-__global__ void __launch_bounds__(128) k_leaf64_lazy(Fp f, const uint32_t* A, int64_t lda,
-                                                     int s, const int32_t* rows,
-                                                     uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
-                                                     int32_t* out, MboxPost mp) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    __shared__ uint32_t Ls[64][65];                  // input tile first, then L
-    __shared__ __align__(16) int32_t rowb[2][64];    // raw residual row of the front
-    __shared__ __align__(16) int32_t row2[64];       // raw residual row of the 2x2 partner
-    __shared__ int32_t order[64];
-    __shared__ int32_t pless[64];
-    __shared__ int32_t srows[64];
-    __shared__ uint32_t sinv[SINV_MAX];
+// Shared memory of the lazy leaf core (one 128-thread CTA).
+struct LeafSmem {
+    uint32_t Ls[64][65];                  // input tile first, then L (row i, pivot column c)
+    __align__(16) int32_t rowb[2][64];    // raw residual row of the front
+    __align__(16) int32_t row2[64];       // raw residual row of the 2x2 partner
+    int32_t order[64];                    // pivot rows in pivot order
+    int32_t pless[64];                    // pivotless rows, ascending
+    int32_t dkind[64];                    // D of the leaf's pivot columns (also written to D)
+    uint32_t dval2[64], dinv[64];
+};
+
+// The leaf elimination (Alg. 4) of the s x s block at src (row stride lds; global
+// memory when kGlobal, else shared), s <= 64, by 128 threads.  Fills sm (L, order,
+// pless, D of columns coff ..) and writes D; returns the rank.  Ends with a barrier.
+template <bool kGlobal>
+__device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, int64_t lds, int s,
+                         LeafSmem& sm, DDiag D, int64_t coff) {
     const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
     const uint32_t one = 1 % f.p;
     const uint32_t off = 96u * f.p * f.p;
-    const SmemInv inv = stage_inverses(f, sinv);  // independent of the predecessor
-    asm volatile("griddepcontrol.wait;" ::: "memory");
     {  // coalesced tile load, all loads of a thread in flight at once
         uint32_t v[32];
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
             const int e = tid + 128 * u, i = e >> 6, k = e & 63;
-            v[u] = (i < s && k < s) ? __ldcg(A + (int64_t)i * lda + k) : 0u;
+            v[u] = (i < s && k < s) ? (kGlobal ? __ldcg(src + (int64_t)i * lds + k) : src[(int64_t)i * lds + k])
+                                    : 0u;
         }
-        if (tid < 64) srows[tid] = tid < s ? __ldcg(rows + tid) : 0;
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
             const int e = tid + 128 * u;
-            Ls[e >> 6][e & 63] = v[u];
+            sm.Ls[e >> 6][e & 63] = v[u];
         }
     }
     __syncthreads();
     int32_t S0[16], S1[16];  // S[lane][16wp + t], S[lane + 32][16wp + t]
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
-        S0[t] = (int32_t)Ls[lane][16 * wp + t];
-        S1[t] = (int32_t)Ls[lane + 32][16 * wp + t];
+        S0[t] = (int32_t)sm.Ls[lane][16 * wp + t];
+        S1[t] = (int32_t)sm.Ls[lane + 32][16 * wp + t];
     }
     __syncthreads();
-    for (int e = tid; e < 64 * 65; e += 128) (&Ls[0][0])[e] = 0;
-    uint64_t active = (s == 64) ? ~0ull : ((1ull << s) - 1);
+    for (int e = tid; e < 64 * 65; e += 128) (&sm.Ls[0][0])[e] = 0;
+    // active rows as two 32-bit halves (uniform)
+    uint32_t alo = s >= 32 ? 0xffffffffu : ((1u << s) - 1), ahi = s >= 64 ? 0xffffffffu : (s > 32 ? ((1u << (s - 32)) - 1) : 0u);
+    auto clear_bit = [&](int b) {
+        if (b < 32) alo &= ~(1u << b);
+        else ahi &= ~(1u << (b - 32));
+    };
     int r = 0, npl = 0, buf = 0;
     const bool lo = wp < 2;  // this warp's columns are rows < 32
     for (int p1 = 0; p1 < s; ++p1) {
-        if (!((active >> p1) & 1)) continue;  // consumed as a 2x2 partner (uniform)
-        int32_t* rb = rowb[buf];
+        if (!(((p1 < 32 ? alo : ahi) >> (p1 & 31)) & 1)) continue;  // consumed as a 2x2 partner (uniform)
+        int32_t* rb = sm.rowb[buf];
         buf ^= 1;
         if (lane == (p1 & 31)) {
             int4* d = reinterpret_cast<int4*>(rb + 16 * wp);
@@ -237,38 +245,47 @@ __global__ void __launch_bounds__(128) k_leaf64_lazy(Fp f, const uint32_t* A, in
         }
         __syncthreads();
         const uint32_t c0 = lz_red(f, rb[lane], off), c1 = lz_red(f, rb[lane + 32], off);
-        const uint32_t b0 = __ballot_sync(0xffffffffu, c0 != 0);
-        const uint32_t b1 = __ballot_sync(0xffffffffu, c1 != 0);
-        const uint64_t msk = (((uint64_t)b1 << 32) | b0) & active;
-        const int j = msk ? __ffsll((long long)msk) - 1 : s;
+        // off the critical path (they overlap the ballot chain): the inverse of this
+        // lane's residuals and the residuals of this warp's 16 columns
+        const uint32_t i0v = inv.t ? inv.t[c0] : 0u, i1v = inv.t ? inv.t[c1] : 0u;
+        const uint32_t csrc = lo ? c0 : c1;
+        int32_t ck[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) ck[t] = (int32_t)__shfl_sync(0xffffffffu, csrc, (16 * wp + t) & 31);
+        const uint32_t b0 = __ballot_sync(0xffffffffu, c0 != 0) & alo;
+        const uint32_t b1 = __ballot_sync(0xffffffffu, c1 != 0) & ahi;
+        const int j = b0 ? __ffs(b0) - 1 : (b1 ? 31 + __ffs(b1) : s);
         if (j >= s) {  // pivotless (sytrf.cpp:82-85)
-            if (tid == 0) pless[npl] = p1;
+            if (tid == 0) sm.pless[npl] = p1;
             ++npl;
-            active &= ~(1ull << p1);
+            clear_bit(p1);
             continue;
         }
         if (j == p1) {  // 1x1 pivot (sytrf.cpp:87-97)
-            const uint32_t x = __shfl_sync(0xffffffffu, p1 < 32 ? c0 : c1, p1 & 31);
-            const uint32_t xi = inv(f, x);
-            active &= ~(1ull << p1);
+            const int src_l = p1 & 31;
+            const uint32_t x = __shfl_sync(0xffffffffu, p1 < 32 ? c0 : c1, src_l);
+            const uint32_t xi = inv.t ? __shfl_sync(0xffffffffu, p1 < 32 ? i0v : i1v, src_l) : inv(f, x);
+            clear_bit(p1);
             const uint32_t l0 = red32(f, c0 * xi), l1 = red32(f, c1 * xi);  // row multipliers
-            const uint32_t lsrc = lo ? l0 : l1;
+            // S[i][k] -= c_i l_k = l_i c_k (mod p): row multiplier times column residual
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
-                const int32_t lk = (int32_t)__shfl_sync(0xffffffffu, lsrc, (16 * wp + t) & 31);
-                S0[t] -= (int32_t)c0 * lk;
-                S1[t] -= (int32_t)c1 * lk;
+                S0[t] -= (int32_t)l0 * ck[t];
+                S1[t] -= (int32_t)l1 * ck[t];
             }
             if (wp == 0) {
-                if ((active >> lane) & 1) Ls[lane][r] = l0;
-                if ((active >> (lane + 32)) & 1) Ls[lane + 32][r] = l1;
+                if ((alo >> lane) & 1) sm.Ls[lane][r] = l0;
+                if ((ahi >> lane) & 1) sm.Ls[lane + 32][r] = l1;
                 if (lane == 0) {
-                    Ls[p1][r] = one;
+                    sm.Ls[p1][r] = one;
                     D.kind[coff + r] = D_SCALAR;
                     D.val[coff + r] = x;
                     D.val2[coff + r] = 0;
                     D.inv[coff + r] = xi;
-                    order[r] = p1;
+                    sm.dkind[r] = D_SCALAR;
+                    sm.dval2[r] = 0;
+                    sm.dinv[r] = xi;
+                    sm.order[r] = p1;
                 }
             }
             r += 1;
@@ -277,7 +294,7 @@ __global__ void __launch_bounds__(128) k_leaf64_lazy(Fp f, const uint32_t* A, in
         // 2x2 antidiagonal pivot pairing p1 with p2 = j (sytrf.cpp:99-131)
         const int p2 = j;
         if (lane == (p2 & 31)) {
-            int4* d = reinterpret_cast<int4*>(row2 + 16 * wp);
+            int4* d = reinterpret_cast<int4*>(sm.row2 + 16 * wp);
             if (p2 < 32) {
 #pragma unroll
                 for (int q = 0; q < 4; ++q) d[q] = make_int4(S0[4 * q], S0[4 * q + 1], S0[4 * q + 2], S0[4 * q + 3]);
@@ -287,13 +304,14 @@ __global__ void __launch_bounds__(128) k_leaf64_lazy(Fp f, const uint32_t* A, in
             }
         }
         __syncthreads();
-        const uint32_t d0 = lz_red(f, row2[lane], off), d1 = lz_red(f, row2[lane + 32], off);
+        const uint32_t d0 = lz_red(f, sm.row2[lane], off), d1 = lz_red(f, sm.row2[lane + 32], off);
         const uint32_t x = __shfl_sync(0xffffffffu, p2 < 32 ? c0 : c1, p2 & 31);
         const uint32_t y = __shfl_sync(0xffffffffu, p2 < 32 ? d0 : d1, p2 & 31);
         const uint32_t xi = inv(f, x);
         const uint32_t y_eff = f.char2 ? y : fhalve(f, y);
         const uint32_t yd = f.char2 ? y : 0;
-        active &= ~((1ull << p1) | (1ull << p2));
+        clear_bit(p1);
+        clear_bit(p2);
         // row multipliers of this lane's rows: l2 = x^-1 c, l1 = x^-1 (d - y_eff l2)
         const uint32_t l2a = red32(f, xi * c0), l2b = red32(f, xi * c1);
         const uint32_t l1a = red32(f, xi * red32(f, d0 + f.p * f.p - y_eff * l2a));
@@ -305,48 +323,287 @@ __global__ void __launch_bounds__(128) k_leaf64_lazy(Fp f, const uint32_t* A, in
         const uint32_t s2 = lo ? l2a : l2b, s1 = lo ? l1a : l1b;
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
-            const int src = (16 * wp + t) & 31;
-            const int32_t l2k = (int32_t)__shfl_sync(0xffffffffu, s2, src);
-            const int32_t l1k = (int32_t)__shfl_sync(0xffffffffu, s1, src);
+            const int src_l = (16 * wp + t) & 31;
+            const int32_t l2k = (int32_t)__shfl_sync(0xffffffffu, s2, src_l);
+            const int32_t l1k = (int32_t)__shfl_sync(0xffffffffu, s1, src_l);
             S0[t] -= ga * l2k + ba * l1k;
             S1[t] -= gb * l2k + bb * l1k;
         }
         if (wp == 0) {
-            if ((active >> lane) & 1) {
-                Ls[lane][r] = l1a;
-                Ls[lane][r + 1] = l2a;
+            if ((alo >> lane) & 1) {
+                sm.Ls[lane][r] = l1a;
+                sm.Ls[lane][r + 1] = l2a;
             }
-            if ((active >> (lane + 32)) & 1) {
-                Ls[lane + 32][r] = l1b;
-                Ls[lane + 32][r + 1] = l2b;
+            if ((ahi >> lane) & 1) {
+                sm.Ls[lane + 32][r] = l1b;
+                sm.Ls[lane + 32][r + 1] = l2b;
             }
             if (lane == 0) {
-                Ls[p1][r] = one;
-                Ls[p2][r + 1] = one;
-                Ls[p2][r] = f.char2 ? 0 : red32(f, xi * y_eff);
+                sm.Ls[p1][r] = one;
+                sm.Ls[p2][r + 1] = one;
+                sm.Ls[p2][r] = f.char2 ? 0 : red32(f, xi * y_eff);
                 const int32_t hk = yd ? D_ANTITRI_HEAD : D_ANTIDIAG_HEAD;
                 D.kind[coff + r] = hk;
                 D.kind[coff + r + 1] = hk + 1;
                 D.val[coff + r] = D.val[coff + r + 1] = x;
                 D.val2[coff + r] = D.val2[coff + r + 1] = yd;
                 D.inv[coff + r] = D.inv[coff + r + 1] = xi;
-                order[r] = p1;
-                order[r + 1] = p2;
+                sm.dkind[r] = hk;
+                sm.dkind[r + 1] = hk + 1;
+                sm.dval2[r] = sm.dval2[r + 1] = yd;
+                sm.dinv[r] = sm.dinv[r + 1] = xi;
+                sm.order[r] = p1;
+                sm.order[r + 1] = p2;
             }
         }
         r += 2;
     }
     __syncthreads();
+    return r;
+}
+
+__global__ void __launch_bounds__(128) k_leaf64_lazy(Fp f, const uint32_t* A, int64_t lda,
+                                                     int s, const int32_t* rows,
+                                                     uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
+                                                     int32_t* out, MboxPost mp) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __shared__ LeafSmem sm;
+    __shared__ int32_t srows[64];
+    __shared__ uint32_t sinv[SINV_MAX];
+    const int tid = threadIdx.x;
+    const SmemInv inv = stage_inverses(f, sinv);  // independent of the predecessor
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (tid < 64) srows[tid] = tid < s ? __ldcg(rows + tid) : 0;
+    const int r = leaf_core<true>(f, inv, A, lda, s, sm, D, coff);
     // L columns [coff, coff + r) of the leaf rows: thread t < s writes row t
     if (tid < s) {
         uint32_t* d = Lg + (int64_t)srows[tid] * ldL + coff;
 #pragma unroll 8
-        for (int c = 0; c < r; ++c) d[c] = Ls[tid][c];
+        for (int c = 0; c < r; ++c) d[c] = sm.Ls[tid][c];
     }
     for (int e = tid; e <= s; e += 128) {
-        const int32_t v = e == 0 ? r : (e <= r ? order[e - 1] : pless[e - 1 - r]);
+        const int32_t v = e == 0 ? r : (e <= r ? sm.order[e - 1] : sm.pless[e - 1 - r]);
         out[e] = v;
         if (mp.dst) mp.dst[e] = (uint32_t)v;
+    }
+    if (mp.dst) {
+        __threadfence_system();
+        __syncthreads();
+        if (tid == 0) *(volatile uint32_t*)mp.seq_ptr = mp.seq;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Fused small node (p < 4096, children are leaves: s <= 2T, T <= 64): one CTA runs
+// recursive_step (sytrf.cpp:298-335) on an s x s node, s <= 128, held in shared
+// memory -- leaf(A1), B' = P1^T B, X = L1^-1 B'1, G = (D1^-1 X)^T (also written
+// to the L rows of N1), Y = B'2 - M1 X, Z = C - G X, then zero_leading
+// (sytrf.cpp:267-292): m - r1 = 0 or Y = 0 -> leaf(Z) and the permutation
+// composition on the device; Y != 0 (zero_leading_pairs) -> bail out: Y goes to
+// yout (ld ns), Z to A[m:, m:], and the host continues from leaf(A1)'s result.
+// out / mailbox: [0, rank, perm(s)] when done, [1, r1, perm1(m)] on bail-out.
+// ---------------------------------------------------------------------------
+constexpr int NODE_LD = 129;  // row stride of the node matrix in shared memory
+constexpr int NODE_W = 65;    // row stride of the 64-wide work matrices
+constexpr size_t node_smem_bytes() {
+    return (size_t)(128 * NODE_LD + 3 * 64 * NODE_W) * 4;
+}
+__global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda, int s, const int32_t* rows,
+                                                 uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
+                                                 uint32_t* yout, int32_t* out, MboxPost mp) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    extern __shared__ __align__(16) uint32_t nsm[];
+    uint32_t* Am = nsm;                       // s x s node (C becomes Z in place)
+    uint32_t* BP = Am + 128 * NODE_LD;        // m x ns: X in rows [0, r1), Y in [r1, m)
+    uint32_t* LM = BP + 64 * NODE_W;          // m x r1: [L1; M1]
+    uint32_t* Gs = LM + 64 * NODE_W;          // ns x r1: G
+    __shared__ LeafSmem sm;
+    __shared__ int32_t srows[128];
+    __shared__ int32_t perm1[64], perm2[128];
+    __shared__ uint32_t sinv[SINV_MAX];
+    __shared__ int ynz;
+    const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
+    const SmemInv inv = stage_inverses(f, sinv);  // independent of the predecessor
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int m = s / 2, ns = s - m;
+    for (int i0 = 0; i0 < s; i0 += 32) {  // node matrix: 32 rows per round, loads in flight
+        uint32_t v[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+            const int i = i0 + u, k = tid;
+            v[u] = (i < s && k < s) ? __ldcg(A + (int64_t)i * lda + k) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < 32; ++u) Am[(i0 + u) * NODE_LD + tid] = v[u];
+    }
+    srows[tid] = tid < s ? __ldcg(rows + tid) : 0;
+    if (tid == 0) ynz = 0;
+    __syncthreads();
+    // ---- leaf(A1) (:303) ----
+    const int r1 = leaf_core<false>(f, inv, Am, NODE_LD, m, sm, D, coff);
+    const int mp1 = m - r1;
+    if (tid < m) {
+        uint32_t* d = Lg + (int64_t)srows[tid] * ldL + coff;
+        for (int c = 0; c < r1; ++c) d[c] = sm.Ls[tid][c];
+        perm1[tid] = tid < r1 ? sm.order[tid] : sm.pless[tid - r1];
+    }
+    __syncthreads();
+    // ---- B' = P1^T B (:308), [L1; M1] in position order ----
+    for (int e = tid; e < m * 64; e += 128) {
+        const int i = e >> 6, j = e & 63, src = perm1[i];
+        if (j < ns) BP[i * NODE_W + j] = Am[src * NODE_LD + m + j];
+        if (j < r1) LM[i * NODE_W + j] = sm.Ls[src][j];
+    }
+    __syncthreads();
+    if (r1 > 0) {
+        // ---- X = L1^-1 B'1 (:310): warp w owns columns 16w + c, lanes 2c, 2c+1 split k ----
+        {
+            const int c = 16 * wp + (lane >> 1), q = lane & 1;
+            for (int i0 = 0; i0 < r1; i0 += 4) {
+                uint32_t acc[4] = {0, 0, 0, 0};
+                for (int k = q; k < i0; k += 2) {
+                    const uint32_t xk = BP[k * NODE_W + c];
+#pragma unroll
+                    for (int rr = 0; rr < 4; ++rr) acc[rr] += LM[(i0 + rr) * NODE_W + k] * xk;
+                }
+                uint32_t sum[4];
+#pragma unroll
+                for (int rr = 0; rr < 4; ++rr) sum[rr] = red32(f, acc[rr] + __shfl_xor_sync(0xffffffffu, acc[rr], 1));
+                if (q == 0 && c < ns) {
+                    uint32_t x[4];
+#pragma unroll
+                    for (int rr = 0; rr < 4; ++rr) {
+                        if (i0 + rr >= r1) break;
+                        uint32_t v = fsub(f, BP[(i0 + rr) * NODE_W + c], sum[rr]);
+#pragma unroll
+                        for (int t = 0; t < rr; ++t) v = fsub(f, v, fmul(f, LM[(i0 + rr) * NODE_W + i0 + t], x[t]));
+                        x[rr] = v;
+                        BP[(i0 + rr) * NODE_W + c] = v;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+        // ---- G = (D1^-1 X)^T (:313, blockdiag.hpp:112-138), also the L rows of N1 ----
+        for (int e = tid; e < ns * 64; e += 128) {
+            const int j = e >> 6, k = e & 63;
+            if (k >= r1) continue;
+            const int32_t kind = sm.dkind[k];
+            const uint32_t iv = sm.dinv[k];
+            uint32_t v;
+            if (kind == D_SCALAR) {
+                v = fmul(f, iv, BP[k * NODE_W + j]);
+            } else if (kind == D_ANTIDIAG_HEAD) {
+                v = fmul(f, iv, BP[(k + 1) * NODE_W + j]);
+            } else if (kind == D_ANTIDIAG_TAIL || kind == D_ANTITRI_TAIL) {
+                v = fmul(f, iv, BP[(k - 1) * NODE_W + j]);
+            } else {  // AntiTri head: -d c^-2 x_t + c^-1 x_{t+1}
+                const uint32_t top = fneg(f, fmul(f, sm.dval2[k], fmul(f, iv, iv)));
+                v = fadd(f, fmul(f, top, BP[k * NODE_W + j]), fmul(f, iv, BP[(k + 1) * NODE_W + j]));
+            }
+            Gs[j * NODE_W + k] = v;
+            Lg[(int64_t)srows[m + j] * ldL + coff + k] = v;
+        }
+        __syncthreads();
+    }
+    // ---- [Y; Z] -= [M1; G] X (:312, :315): thread = 8 rows x 8 columns ----
+    {
+        const int rg = tid >> 3, cg = tid & 7;
+        const int R = mp1 + ns;
+        uint32_t acc[8][8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a)
+#pragma unroll
+            for (int b = 0; b < 8; ++b) acc[a][b] = 0;
+        const uint32_t* lrow[8];
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int rho = 8 * rg + a;
+            lrow[a] = rho < mp1 ? LM + (r1 + rho) * NODE_W : Gs + (rho < R ? rho - mp1 : 0) * NODE_W;
+        }
+        for (int k = 0; k < r1; ++k) {
+            uint32_t xv[8], lv[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b) xv[b] = BP[k * NODE_W + 8 * cg + b];
+#pragma unroll
+            for (int a = 0; a < 8; ++a) lv[a] = lrow[a][k];
+#pragma unroll
+            for (int a = 0; a < 8; ++a)
+#pragma unroll
+                for (int b = 0; b < 8; ++b) acc[a][b] += lv[a] * xv[b];
+        }
+        int nz = 0;
+#pragma unroll
+        for (int a = 0; a < 8; ++a) {
+            const int rho = 8 * rg + a;
+            if (rho >= R) break;
+#pragma unroll
+            for (int b = 0; b < 8; ++b) {
+                const int j = 8 * cg + b;
+                if (j >= ns) break;
+                uint32_t* cp = rho < mp1 ? BP + (r1 + rho) * NODE_W + j : Am + (m + rho - mp1) * NODE_LD + m + j;
+                const uint32_t v = fsub(f, *cp, red32(f, acc[a][b]));
+                *cp = v;
+                if (rho < mp1) nz |= v != 0;
+            }
+        }
+        if (nz) ynz = 1;
+    }
+    __syncthreads();
+    if (mp1 > 0 && ynz) {
+        // ---- zero_leading_pairs: hand Y and Z to the host ----
+        for (int e = tid; e < mp1 * 64; e += 128) {
+            const int i = e >> 6, j = e & 63;
+            if (j < ns) yout[(int64_t)i * ns + j] = BP[(r1 + i) * NODE_W + j];
+        }
+        for (int e = tid; e < ns * 128; e += 128) {
+            const int i = e >> 7, j = e & 127;
+            if (j < ns) A[(int64_t)(m + i) * lda + m + j] = Am[(m + i) * NODE_LD + m + j];
+        }
+        for (int e = tid; e < m + 2; e += 128) {
+            const int32_t v = e == 0 ? 1 : (e == 1 ? r1 : perm1[e - 2]);
+            out[e] = v;
+            if (mp.dst) mp.dst[e] = (uint32_t)v;
+        }
+    } else {
+        // ---- leaf(Z) (:317 via zero_leading :273 / :276) ----
+        const int r3 = leaf_core<false>(f, inv, Am + m * NODE_LD + m, NODE_LD, ns, sm, D, coff + r1);
+        if (tid < ns) {
+            uint32_t* d = Lg + (int64_t)srows[m + tid] * ldL + coff + r1;
+            for (int c = 0; c < r3; ++c) d[c] = sm.Ls[tid][c];
+        }
+        // f2 = zero_leading's permutation of [Y rows (mp1), Z rows (ns)] (:284-289)
+        for (int pos = tid; pos < mp1 + ns; pos += 128) {
+            int v;
+            if (mp1 == 0) {
+                v = pos < r3 ? sm.order[pos] : sm.pless[pos - r3];
+            } else if (pos < r3) {
+                v = mp1 + sm.order[pos];
+            } else if (pos < r3 + mp1) {
+                v = pos - r3;
+            } else {
+                v = mp1 + sm.pless[pos - mp1 - r3];
+            }
+            perm2[pos] = v;
+        }
+        __syncthreads();
+        // P = compose(embed(P1, 0, n), embed(P2, r1, n)) (:332-334)
+        for (int e = tid; e < s + 2; e += 128) {
+            int32_t v;
+            if (e == 0) v = 0;
+            else if (e == 1) v = r1 + r3;
+            else {
+                const int pos = e - 2;
+                if (pos < r1) v = perm1[pos];
+                else {
+                    const int cix = perm2[pos - r1];
+                    v = cix < mp1 ? perm1[r1 + cix] : m + (cix - mp1);
+                }
+            }
+            out[e] = v;
+            if (mp.dst) mp.dst[e] = (uint32_t)v;
+        }
     }
     if (mp.dst) {
         __threadfence_system();
@@ -872,6 +1129,28 @@ void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tin
 }  // namespace
 
 bool leaf64_supported(int64_t s) { return s <= 64; }
+
+bool node128_supported(const Fp& f, int64_t s, int64_t T) {
+    static const bool off = getenv("FFB_NO_NODE128") != nullptr;  // A/B hook
+    return !off && f.p < 4096u && T <= 64 && s > T && s <= 2 * T && s <= 128;
+}
+
+void node128(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff, DDiag D,
+             uint32_t* yout, int32_t* out, const MboxPost& mp) {
+    const int s = (int)A.rows;
+    ProfScope ps(K_LEAF, st, 2.0 * s * s * s / 3.0, 4.0 * s * s);
+    static bool attr = false;
+    if (!attr) {
+        FFB_CUDA(cudaFuncSetAttribute(k_node128, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)node_smem_bytes()));
+        attr = true;
+    }
+    launch_k(k_node128, 1, 128, node_smem_bytes(), st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, yout, out,
+             mp);
+    ++g_launches;
+    FFB_CHECK_LAUNCH();
+}
+
 
 void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
             DDiag D, int32_t* out, const MboxPost& mp) {

@@ -150,6 +150,13 @@ size_t leaf_scratch_words(int64_t s);
 bool leaf64_supported(int64_t s);
 void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
             DDiag D, int32_t* out, const MboxPost& mp);
+// Fused small node (ffb_fast.cu): recursive_step + zero_leading of an s x s node whose
+// children are leaves, in one launch.  out[0..s+2) = [0, rank, perm] or, when Y != 0
+// (zero_leading_pairs), [1, r1, perm1(m)] with Y in yout (m - r1 x ns, ld ns) and
+// Z = C - G X written back to A[m:, m:].
+bool node128_supported(const Fp& f, int64_t s, int64_t T);
+void node128(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff, DDiag D,
+             uint32_t* yout, int32_t* out, const MboxPost& mp);
 
 // PLDUQ (plduq.cpp:36-123) of W (m x n, destroyed).  Outputs: info[0] = r,
 // info[1..m] row_image, info[1+m..1+m+n] col_image, pc[r] in info after that;
