@@ -601,8 +601,8 @@ __global__ void __launch_bounds__(256) k_crp_finish(
                           ((((uintptr_t)S) & 15) == 0);
     if (si_early) {
         const int s4 = s >> 2;
-        for (int e = tid; e < k * s4; e += 256) {
-            const int u = e / s4, q = e - u * s4;
+        for (int u = wp; u < k; u += 8)
+            for (int q = lane; q < s4; q += 32) {
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                              (uint32_t)__cvta_generic_to_shared(sm + si_off + (size_t)u * s + 4 * q)),
                          "l"(S + (int64_t)Is[u] * lds + 4 * q));
@@ -637,13 +637,13 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         }
         __syncthreads();
     }
-    for (int e = tid; e < k * k; e += 256) G[e] = (e / k == e % k) ? 1 % f.p : 0u;
-    for (int e = tid; e < k * Cx; e += 256) {  // scattered gather, every copy in flight
-        const int i = e / Cx, j = e - i * Cx;
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
-                         (uint32_t)__cvta_generic_to_shared(M + (size_t)i * Cx + j)),
-                     "l"(RI + (int64_t)i * ldr + ids[j]));
-    }
+    for (int i = wp; i < k; i += 8)
+        for (int j = lane; j < k; j += 32) G[(size_t)i * k + j] = (i == j) ? 1 % f.p : 0u;
+    for (int i = wp; i < k; i += 8)  // scattered gather, every copy in flight
+        for (int j = lane; j < Cx; j += 32)
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(
+                             (uint32_t)__cvta_generic_to_shared(M + (size_t)i * Cx + j)),
+                         "l"(RI + (int64_t)i * ldr + ids[j]));
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
@@ -744,11 +744,14 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         sig[t] = rank;
         Jout[rank] = v;
     }
-    for (int e = tid; e < k * k; e += 256) G[e] = fmul(f, G[e], dinv[e / k]);
     __syncthreads();
-    for (int e = tid; e < k * k; e += 256) {
-        const int t = e / k, j = e - t * k;
-        Kinv[(int64_t)sig[t] * k + j] = G[e];
+    for (int t = wp; t < k; t += 8) {  // row t of X, scaled: row sig[t] of Kinv
+        const uint32_t dt = dinv[t];
+        for (int j = lane; j < k; j += 32) {
+            const uint32_t v = fmul(f, G[(size_t)t * k + j], dt);
+            G[(size_t)t * k + j] = v;
+            Kinv[(int64_t)sig[t] * k + j] = v;
+        }
     }
     if (S) {  // UO rows from the k sketch rows S_I (copied early, or staged now in the free M buffer)
         uint32_t* SI = si_early ? sm + si_off : M;
@@ -756,15 +759,24 @@ __global__ void __launch_bounds__(256) k_crp_finish(
             for (int u = wp; u < k; u += 8)
                 for (int col = lane; col < s; col += 32) SI[(size_t)u * s + col] = __ldcg(S + (int64_t)Is[u] * lds + col);
         __syncthreads();
-        for (int e = tid; e < k * s; e += 256) {
-            const int t = e / s, col = e - t * s;
+        const bool lz = (uint64_t)k * (f.p - 1) * (f.p - 1) < (1ull << 32) && f.mu32;  // 32-bit sums
+        for (int t = wp; t < k; t += 8) {
             const uint32_t* xt = G + (size_t)t * k;
-            uint64_t acc = 0;
-            for (int u = 0; u < k; ++u) {
-                acc += (uint64_t)xt[u] * SI[(size_t)u * s + col];
-                if (f.p >= (1u << 23)) acc = red64(f, acc);
+            uint32_t* uo = UO + (r + sig[t]) * lduo;
+            for (int col = lane; col < s; col += 32) {
+                if (lz) {
+                    uint32_t acc = 0;
+                    for (int u = 0; u < k; ++u) acc += xt[u] * SI[(size_t)u * s + col];
+                    uo[col] = red32(f, acc);
+                } else {
+                    uint64_t acc = 0;
+                    for (int u = 0; u < k; ++u) {
+                        acc += (uint64_t)xt[u] * SI[(size_t)u * s + col];
+                        if (f.p >= (1u << 23)) acc = red64(f, acc);
+                    }
+                    uo[col] = red64(f, acc);
+                }
             }
-            UO[(r + sig[t]) * lduo + col] = red64(f, acc);
         }
     }
     for (int t = tid; t < k; t += 256) {
