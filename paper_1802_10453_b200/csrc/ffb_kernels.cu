@@ -429,15 +429,41 @@ __global__ void k_invert_vec(Fp f, uint32_t* out, const uint32_t* v, int64_t n) 
     if (i < n) out[i] = finv(f, v[i]);
 }
 
-__global__ void k_any_nonzero(const uint32_t* m, int64_t ld, int64_t rows, int64_t cols,
-                              int32_t* flag, int32_t value) {
+// *flag = value if any entry of m is nonzero.  Grid-stride over rows, a warp per
+// row (16-byte loads, 4 in flight per lane when aligned); a warp that finds a
+// nonzero publishes and exits, and every warp polls the flag (read at the start of
+// a row, tested after its loads) so a nonzero matrix is abandoned early.
+__global__ void __launch_bounds__(256) k_any_nonzero(const uint32_t* m, int64_t ld, int64_t rows, int64_t cols,
+                                                     int32_t* flag, int32_t value) {
     FFB_PDL_ENTRY();
-    const int64_t i = blockIdx.y;
-    int found = 0;
-    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cols;
-         j += (int64_t)gridDim.x * blockDim.x)
-        found |= m[i * ld + j] != 0;
-    if (__syncthreads_or(found) && threadIdx.x == 0) *flag = value;  // same value from every CTA
+    const int lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    const bool vec = ((((uintptr_t)m) & 15) == 0) && ((ld & 3) == 0) && ((cols & 3) == 0);
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < rows; i += nwarps) {
+        const int32_t seen = *(volatile const int32_t*)flag;
+        const uint32_t* row = m + i * ld;
+        bool nz = false;
+        if (vec) {
+            const uint4* r4 = reinterpret_cast<const uint4*>(row);
+            const int64_t c4 = cols >> 2;
+            int64_t j = lane;
+            for (; j + 96 < c4; j += 128) {
+                const uint4 a = __ldcg(r4 + j), b = __ldcg(r4 + j + 32), c = __ldcg(r4 + j + 64), d = __ldcg(r4 + j + 96);
+                nz |= (a.x | a.y | a.z | a.w | b.x | b.y | b.z | b.w | c.x | c.y | c.z | c.w | d.x | d.y | d.z | d.w) != 0;
+            }
+            for (; j < c4; j += 32) {
+                const uint4 a = __ldcg(r4 + j);
+                nz |= (a.x | a.y | a.z | a.w) != 0;
+            }
+        } else {
+            for (int64_t j = lane; j < cols; j += 32) nz |= __ldcg(row + j) != 0;
+        }
+        if (__any_sync(0xffffffffu, nz)) {
+            if (lane == 0) *flag = value;
+            return;
+        }
+        if (__shfl_sync(0xffffffffu, seen, 0) == value) return;  // another warp found one
+    }
 }
 
 // Symmetry check: block (x, y) compares the 32-row band y against the transposed
@@ -703,11 +729,10 @@ void invert_vec(const Fp& f, cudaStream_t st, uint32_t* out, const uint32_t* v, 
 void any_nonzero(cudaStream_t st, DMat m, int32_t* flag, int32_t value) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (m.rows <= 0 || m.cols <= 0) return;
-    for (int64_t r0 = 0; r0 < m.rows; r0 += FFB_ROWCHUNK) {
-        const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, m.rows - r0);
-        launch_k(k_any_nonzero, rowgrid(nr, m.cols), 256, 0, st, m.ptr + r0 * m.ld, m.ld, nr, m.cols, flag, value);
-        count_launch();
-    }
+    // a warp per row, at most 8 CTAs of 8 warps per SM
+    const unsigned g = (unsigned)std::min<int64_t>(cdiv(m.rows, 8), 148 * 8);
+    launch_k(k_any_nonzero, g, 256, 0, st, m.ptr, m.ld, m.rows, m.cols, flag, value);
+    count_launch();
     FFB_CHECK_LAUNCH();
 }
 
