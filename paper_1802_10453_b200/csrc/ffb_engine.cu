@@ -344,6 +344,10 @@ struct UploadBands {
     std::vector<std::pair<int64_t, cudaEvent_t>> ev;  // (band end row, landed)
 };
 
+// Schur updates at least this large overlap the zero test / PLDUQ of Y (side stream).
+static const int64_t Z_OVERLAP_MIN =
+    getenv("FFB_Z_OVERLAP_MIN") ? atoll(getenv("FFB_Z_OVERLAP_MIN")) : 2048;
+
 struct Engine {
     ffb_context* c;
     cudaStream_t st;
@@ -353,6 +357,40 @@ struct Engine {
     DMat Lg;
     DDiag D;
     UploadBands* bands = nullptr;
+    // side stream of the overlapped Schur update (lowest priority) and its events
+    cudaStream_t zst = nullptr;
+    cudaEvent_t zev_fork = nullptr, zev_done = nullptr;
+    bool zpending = false;
+    void z_fork() {
+        if (!zst) {
+            int least = 0, greatest = 0;
+            FFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            static thread_local cudaStream_t s_zst = nullptr;
+            static thread_local cudaEvent_t s_fork = nullptr, s_done = nullptr;
+            if (!s_zst) {
+                FFB_CUDA(cudaStreamCreateWithPriority(&s_zst, cudaStreamNonBlocking, least));
+                FFB_CUDA(cudaEventCreateWithFlags(&s_fork, cudaEventDisableTiming));
+                FFB_CUDA(cudaEventCreateWithFlags(&s_done, cudaEventDisableTiming));
+            }
+            zst = s_zst;
+            zev_fork = s_fork;
+            zev_done = s_done;
+        }
+        FFB_CUDA(cudaEventRecord(zev_fork, st));
+        FFB_CUDA(cudaStreamWaitEvent(zst, zev_fork, 0));
+        pdl_fence(zst);
+    }
+    void z_done() {
+        FFB_CUDA(cudaEventRecord(zev_done, zst));
+        zpending = true;
+    }
+    // the Schur update running beside the critical path must land before Z is read
+    void join_z() {
+        if (!zpending) return;
+        FFB_CUDA(cudaStreamWaitEvent(st, zev_done, 0));
+        pdl_fence(st);
+        zpending = false;
+    }
 
     // Before a node touches rows [m, s) of an input-resident A (the Z block): wait for them.
     void ensure_rows(DMat A, int64_t s) {
@@ -478,9 +516,37 @@ struct Engine {
         trsm_lower_unit(f, st, LM.sub(0, 0, r1, r1), X);  // :310
         DMat Y = BP.sub(r1, 0, m - r1, ns);
         DMat G = ws_mat(c, ns, r1);
-        inverse_apply_T(f, st, G, X, D, coff, Lg, up[2]);  // :313 + rows m..s of N1
         DMat Z = A.sub(m, m, ns, ns);
         ensure_rows(A, s);  // Z and the recursion below read rows [m, s)
+        // Large node with Y != empty: zero_leading's zero test and PLDUQ need Y only, so
+        // G and the Schur update Z = C - G X run on a low-priority side stream beside
+        // them; Z's consumers join first (join_z)
+        static const bool z_overlap_on = getenv("FFB_NO_Z_OVERLAP") == nullptr;
+        if (z_overlap_on && ns >= Z_OVERLAP_MIN && r1 > 0 && m - r1 > 0 && !zpending) {
+            gemm(f, st, GEMM_SUB, Y, LM.sub(r1, 0, m - r1, r1), false, X, false, m - r1, ns, r1);  // :312
+            z_fork();
+            {
+                SlotGuard slot(2);
+                g_tc_shared_sms = true;
+                inverse_apply_T(f, zst, G, X, D, coff, Lg, up[2]);  // :313 + rows m..s of N1
+                gemm(f, zst, GEMM_SUB, Z, G, false, X, false, ns, ns, r1);  // :315
+                g_tc_shared_sms = false;
+            }
+            z_done();
+            HFact f2 = zero_leading(Y, Z, rowsz, up[3], coff + r1, 0);  // :317
+            join_z();
+            HFact h;  // (:332-334)
+            h.rank = r1 + f2.rank;
+            h.perm.resize(s);
+            for (int64_t pos = 0; pos < r1; ++pos) h.perm[pos] = f1.perm[pos];
+            for (int64_t pos = r1; pos < s; ++pos) {
+                const int64_t cix = f2.perm[pos - r1];
+                h.perm[pos] = cix < m - r1 ? f1.perm[r1 + cix] : (int32_t)(m + (cix - (m - r1)));
+            }
+            c->ws_top = mk.top;
+            return h;
+        }
+        inverse_apply_T(f, st, G, X, D, coff, Lg, up[2]);  // :313 + rows m..s of N1
         // Y = B'' - M1 X (:312) and Z = C - G X (:315); small ones as one paired launch
         // whose Y epilogue also answers the zero test of zero_leading
         int32_t ytag = 0;
@@ -522,7 +588,10 @@ struct Engine {
     HFact zero_leading(DMat Y, DMat Z, const std::vector<int32_t>& rows, const int32_t* drows, int64_t coff,
                        int32_t ytag = 0) {
         const int64_t m = Y.rows, nz = Z.rows;
-        if (m == 0) return dispatch(Z, rows, drows, coff);
+        if (m == 0) {
+            join_z();
+            return dispatch(Z, rows, drows, coff);
+        }
         HFact h;
         if (nz == 0) {
             h.perm.resize(m);
@@ -530,6 +599,7 @@ struct Engine {
             return h;
         }
         if (is_zero(Y, ytag)) {  // :274-290
+            join_z();
             std::vector<int32_t> rz(rows.begin() + m, rows.end());
             HFact f3 = dispatch(Z, rz, drows ? drows + m : nullptr, coff);
             const int64_t r3 = f3.rank;
@@ -643,6 +713,7 @@ struct Engine {
         for (int64_t a = 0; a < nz; ++a) idz[a] = rows[m + q[a]];
         const auto up = upload_batch<3>(c, {&q, &idy, &idz});
         DMat Cp = ws_mat(c, nz, nz);  // C' = Q^T Z Q (:183)
+        join_z();
         gather_sym(st, Cp, Z, up[0]);
         DMat C1 = Cp.sub(0, 0, r, r), C2 = Cp.sub(0, r, r, nz - r), C3 = Cp.sub(r, r, nz - r, nz - r);
         DMat U1 = py.U.sub(0, 0, r, r), V1 = py.U.sub(0, r, r, nz - r);

@@ -17,6 +17,7 @@ namespace ffb {
 thread_local uint64_t g_launches = 0;
 thread_local int64_t g_node = 0;
 thread_local int g_slot = 0;
+thread_local bool g_tc_shared_sms = false;
 thread_local Profiler* g_prof = nullptr;
 
 static inline void count_launch() { ++g_launches; }

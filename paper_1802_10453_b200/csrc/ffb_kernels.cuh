@@ -38,6 +38,10 @@ extern thread_local int64_t g_node;
 // Scratch slot of the GEMM packing / split-K buffers: launches on a secondary
 // stream use slot 1 so they never share a buffer with the main stream.
 extern thread_local int g_slot;
+// Set while a GEMM runs beside the critical path on a low-priority stream: the
+// persistent tcgen05 GEMM then occupies only part of the SMs (FFB_Z_OVERLAP_SMS),
+// leaving the rest to the engine stream's latency kernels.
+extern thread_local bool g_tc_shared_sms;
 struct SlotGuard {
     int saved;
     explicit SlotGuard(int s) : saved(g_slot) { g_slot = s; }

@@ -804,7 +804,7 @@ struct Scratch {
     int8_t* ptr = nullptr;
     size_t cap = 0;
 };
-thread_local Scratch g_scratch_slots[2];
+thread_local Scratch g_scratch_slots[3];
 
 int8_t* scratch(size_t bytes) {
     Scratch& g_scratch = g_scratch_slots[g_slot];
@@ -952,7 +952,11 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
             attr = true;
         }
         const int num_m = (int)cdiv(M, TC_BM), num_tiles = num_m * (int)cdiv(N, TP_BN);
-        launch_k(k_gemm_i8_tcp, std::min(num_tiles, nsm), TP_THREADS, TpCfg::SMEM, st, ma, mb, C.ptr, C.ld,
+        // beside the critical path: a persistent grid on part of the SMs only, the rest
+        // stay free for the engine stream's latency kernels
+        static const int shared_sms = getenv("FFB_Z_OVERLAP_SMS") ? atoi(getenv("FFB_Z_OVERLAP_SMS")) : 100;
+        const int ctas = std::min(num_tiles, g_tc_shared_sms ? std::min(shared_sms, nsm) : nsm);
+        launch_k(k_gemm_i8_tcp, ctas, TP_THREADS, TpCfg::SMEM, st, ma, mb, C.ptr, C.ld,
                  (int)M, (int)N, (int)nk, f, (int)mode, num_m, num_tiles);
         ++g_launches;
         FFB_CHECK_LAUNCH();
