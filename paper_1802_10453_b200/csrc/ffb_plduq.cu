@@ -986,6 +986,90 @@ __global__ void __launch_bounds__(256) k_ldu_base(Fp f, uint32_t* K, int64_t ldk
     }
 }
 
+// ---------------------------------------------------------------------------
+// LDU without pivoting of an n <= 128 block in place, 2 <= p < 4096 (1 CTA of 512).
+// Right-looking elimination over the whole block (no recursion, no off-diagonal
+// solves): thread (rg, cg) keeps the 4 x 8 tile K[4rg .. +3][8cg .. +7] in
+// registers, lazily reduced -- entries only grow, by (p - l) u < p^2 per step, so
+// after <= 128 steps they stay below 2^32 (p < 4096) and are reduced by 32-bit
+// Barrett when they become a pivot row or column.  Step t: the owners of column t
+// and of row t publish them reduced (static register indices: the step loop is
+// unrolled by 8), one barrier, then every live tile takes its update.  Result:
+// strict lower <- L, diagonal <- d, strict upper <- U (unit upper, row t / d_t).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) k_ldu128(Fp f, uint32_t* K, int64_t ldk, int n, int32_t* fail) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __shared__ uint32_t colv[2][128], rowv[2][128];
+    __shared__ uint32_t sinv[SINV_MAX];
+    const int tid = threadIdx.x, rg = tid >> 4, cg = tid & 15;
+    const SmemInv inv = stage_inverses(f, sinv);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int r0 = 4 * rg, c0 = 8 * cg;
+    uint32_t T[4][8];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            T[a][b] = (r0 + a < n && c0 + b < n) ? __ldcg(K + (int64_t)(r0 + a) * ldk + c0 + b) : 0u;
+    const uint32_t p = f.p;
+    for (int tb = 0; tb < (n + 7) / 8; ++tb) {
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+            const int t = 8 * tb + jj;
+            if (t >= n) break;  // uniform
+            const int buf = t & 1;
+            if (cg == tb) {  // column t (reduced), rows of this tile
+#pragma unroll
+                for (int a = 0; a < 4; ++a) colv[buf][r0 + a] = red32(f, T[a][jj]);
+            }
+            if (rg == (t >> 2)) {  // row t (reduced), columns of this tile
+#pragma unroll
+                for (int b = 0; b < 8; ++b) rowv[buf][c0 + b] = red32(f, T[jj & 3][b]);
+            }
+            __syncthreads();
+            const uint32_t d = rowv[buf][t];
+            if (d == 0) {  // a singular leading minor: LDU without pivoting does not exist
+                if (tid == 0) *fail = 1;
+                return;  // uniform
+            }
+            const uint32_t di = inv(f, d);
+            const bool rows_live = r0 + 3 > t, cols_live = c0 + 7 > t;
+            if (rows_live || cols_live) {
+                uint32_t l[4], u[8];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) l[a] = red32(f, colv[buf][r0 + a] * di);
+#pragma unroll
+                for (int b = 0; b < 8; ++b) u[b] = rowv[buf][c0 + b];
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 8; ++b)
+                        if (r0 + a > t && c0 + b > t) T[a][b] += (p - l[a]) * u[b];
+                // outputs of step t: L column t, d, U row t
+                if (cg == tb) {
+#pragma unroll
+                    for (int a = 0; a < 4; ++a)
+                        if (r0 + a > t) T[a][jj] = l[a];
+                }
+                if (rg == (t >> 2)) {
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) {
+                        if (c0 + b > t) T[jj & 3][b] = red32(f, u[b] * di);
+                        else if (c0 + b == t) T[jj & 3][b] = d;
+                    }
+                }
+            } else if (rg == (t >> 2) && cg == tb) {
+                T[jj & 3][jj] = d;
+            }
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 8; ++b)
+            if (r0 + a < n && c0 + b < n) K[(int64_t)(r0 + a) * ldk + c0 + b] = T[a][b];
+}
+
 // L (unit lower with zeros above) from the packed LDU block; d from the diagonal.
 __global__ void k_unpack_l(uint32_t* L, int64_t ldl, const uint32_t* K, int64_t ldk, int64_t n,
                            uint32_t* d, uint32_t one) {
@@ -1035,6 +1119,14 @@ void copy_mat(cudaStream_t st, DMat dst, DMat src) {
 void ldu_inplace(const Fp& f, cudaStream_t st, DMat K, Workspace& ws, int32_t* fail) {
     const int64_t n = K.rows;
     if (n <= 0) return;
+    static const bool l128 = getenv("FFB_NO_LDU128") == nullptr;  // A/B hook
+    if (l128 && f.p < 4096u && f.mu32 && n <= 128) {
+        ProfScope ps(K_LDU, st, 2.0 * n * n * n / 3.0, 8.0 * n * n);
+        launch_k(k_ldu128, 1, 512, 0, st, f, K.ptr, K.ld, (int)n, fail);
+        count_launch();
+        FFB_CHECK_LAUNCH();
+        return;
+    }
     if (n <= 64) {
         ProfScope ps(K_LDU, st, 2.0 * n * n * n / 3.0, 8.0 * n * n);
         if (f.p < 65536u)
@@ -1045,8 +1137,9 @@ void ldu_inplace(const Fp& f, cudaStream_t st, DMat K, Workspace& ws, int32_t* f
         FFB_CHECK_LAUNCH();
         return;
     }
-    int64_t n1 = (n / 2) / 64 * 64;
-    if (n1 < 64) n1 = 64;
+    const int64_t base = (l128 && f.p < 4096u && f.mu32) ? 128 : 64;
+    int64_t n1 = (n / 2) / base * base;
+    if (n1 < base) n1 = base;
     const int64_t n2 = n - n1;
     DMat K11 = K.sub(0, 0, n1, n1), K12 = K.sub(0, n1, n1, n2), K21 = K.sub(n1, 0, n2, n1),
          K22 = K.sub(n1, n1, n2, n2);
