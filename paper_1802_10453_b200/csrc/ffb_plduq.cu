@@ -156,6 +156,8 @@ __device__ __forceinline__ void reduce_rows_any(const Fp& f, uint32_t* X, int ld
 }
 
 constexpr int RD_MAX_B = 128, RD_S = 144;
+constexpr int RD_NARROW = 64;  // sketch columns of the first row-detection pass
+static const bool rd_narrow_on = getenv("FFB_RD_WIDE") == nullptr;  // A/B hook
 
 constexpr int RD_BATCH = 16;
 
@@ -269,6 +271,7 @@ __device__ int batch_insert(const Fp& f, const SmemInv& inv, uint32_t* V, int ld
 // reduces to zero lies in the span of earlier rows and is dependent for good,
 // so only the flagged rows go through the sequential insertion.
 // out[0] = k, out[1..k] = independent rows (ascending).
+template <int NQ>  // ceil(s / 32)
 __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int64_t lds, int b,
                                                     int s, int32_t* out, MboxPost mp) {
     FFB_PDL_ENTRY();
@@ -296,12 +299,12 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
             for (int t = lane; t < k; t += 32) cfb[r][t] = Ss[(size_t)(i0 + r) * s + rho[t]];
         if (tid == 0) fmask[bi & 1] = 0;
         __syncthreads();
-        reduce_rows_any<5>(f, V, s, Ss + (size_t)i0 * s, s, &cfb[0][0], RD_MAX_B, E, s, nr, s, k,
+        reduce_rows_any<NQ>(f, V, s, Ss + (size_t)i0 * s, s, &cfb[0][0], RD_MAX_B, E, s, nr, s, k,
                            &fmask[bi & 1]);
         __syncthreads();
         const unsigned pending = fmask[bi & 1];  // rows outside the span of the batch-start basis
         if (!pending) continue;
-        const int cnt = batch_insert<5>(f, inv, V, s, pending, s, E, k, s, rho, bs);
+        const int cnt = batch_insert<NQ>(f, inv, V, s, pending, s, E, k, s, rho, bs);
         if (tid < cnt) out[1 + k + tid] = i0 + bs.ins[tid];  // inserted in row order
         k += cnt;
     }
@@ -1197,7 +1200,8 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + 2 * (size_t)CRP_G * CRP_KMAX) * 4;
     static bool attrs = false;
     if (!attrs) {
-        FFB_CUDA(cudaFuncSetAttribute(k_row_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
+        FFB_CUDA(cudaFuncSetAttribute(k_row_detect<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
+        FFB_CUDA(cudaFuncSetAttribute(k_row_detect<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_crp_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crp_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_pair2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * CRP_KMAX * CRP_KMAX * 4)));
         FFB_CUDA(cudaFuncSetAttribute(k_crp_rowelim, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1311,14 +1315,25 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     gemm(f, st, GEMM_SUB, Sc, Gc, false, UO.sub(0, 0, r, SK), false, bc, SK, r);
                 }
                 mark();
-                const MboxPost mp = io.post ? io.post() : MboxPost();
-                {
-                    ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-                    launch_k(k_row_detect, 1, 256, rd_smem, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp);
-                    ++g_launches;
-                    FFB_CHECK_LAUNCH();
+                // row detection on the first RD_NARROW sketch columns (2 ballot groups instead
+                // of 5): rows independent there are independent in R; a chunk that finds
+                // k >= RD_NARROW - 16 may have more than the narrow sketch can show, and is
+                // re-detected on all SK columns (the certificate guards both)
+                int k = 0;
+                for (int wide = (SK <= RD_NARROW || !rd_narrow_on) ? 1 : 0; wide < 2; ++wide) {
+                    const MboxPost mp = io.post ? io.post() : MboxPost();
+                    {
+                        ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
+                        if (wide)
+                            launch_k(k_row_detect<5>, 1, 256, rd_smem, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp);
+                        else
+                            launch_k(k_row_detect<2>, 1, 256, rd_smem, st, f, Sc.ptr, Sc.ld, (int)bc, RD_NARROW, dinfo, mp);
+                        ++g_launches;
+                        FFB_CHECK_LAUNCH();
+                    }
+                    k = *(const int32_t*)(mp.dst ? io.wait(mp) : io.readback(dinfo, 4));
+                    if (k < RD_NARROW - 16) break;
                 }
-                const int k = *(const int32_t*)(mp.dst ? io.wait(mp) : io.readback(dinfo, 4));
                 mark();
                 if (k == 0) {
                     mark(); mark(); mark();
@@ -1522,12 +1537,13 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
     float t = 0;
     if (which == 0) {
         const size_t rd_smem = ((size_t)2 * RD_MAX_B * cols + (size_t)RD_BATCH * cols) * 4;
-        FFB_CUDA(cudaFuncSetAttribute(k_row_detect, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
+        FFB_CUDA(cudaFuncSetAttribute(k_row_detect<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
+        FFB_CUDA(cudaFuncSetAttribute(k_row_detect<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         int32_t* info;
         FFB_CUDA(cudaMalloc(&info, (2 * RD_MAX_B + 16) * 4));
-        launch_k(k_row_detect, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info, MboxPost());
+        launch_k(k_row_detect<5>, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info, MboxPost());
         FFB_CUDA(cudaEventRecord(e[0], st));
-        for (int i = 0; i < reps; ++i) launch_k(k_row_detect, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info, MboxPost());
+        for (int i = 0; i < reps; ++i) launch_k(k_row_detect<5>, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info, MboxPost());
         FFB_CUDA(cudaEventRecord(e[1], st));
         FFB_CUDA(cudaEventSynchronize(e[1]));
         FFB_CUDA(cudaEventElapsedTime(&t, e[0], e[1]));
