@@ -157,9 +157,13 @@ __device__ __forceinline__ void reduce_rows_any(const Fp& f, uint32_t* X, int ld
 
 constexpr int RD_MAX_B = 128, RD_S = 144;
 constexpr int RD_NARROW = 64;  // sketch columns of the first row-detection pass
+constexpr int RD_MAX_ROWS = 512;  // chunk rows of a narrow row detection (adaptive chunks)
 static const bool rd_narrow_on = getenv("FFB_RD_WIDE") == nullptr;  // A/B hook
 
 constexpr int RD_BATCH = 16;
+__host__ __device__ inline size_t rd_smem_bytes(int b, int s) {
+    return ((size_t)b * s + (size_t)std::min(b, s) * s + (size_t)RD_BATCH * s) * 4;
+}
 
 // Blocked insertion of the flagged vectors of a reduced batch into a fully
 // reduced basis.  V holds nr <= 32 vectors (stride ldv, length len), each
@@ -276,9 +280,9 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
                                                     int s, int32_t* out, MboxPost mp) {
     FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint32_t sm[];
-    uint32_t* Ss = sm;                          // b x s
-    uint32_t* E = Ss + (size_t)RD_MAX_B * s;    // basis rows (fully reduced)
-    uint32_t* V = E + (size_t)RD_MAX_B * s;     // RD_BATCH reduced rows of the current batch
+    uint32_t* Ss = sm;                          // b x s (b <= RD_MAX_ROWS)
+    uint32_t* E = Ss + (size_t)b * s;           // basis rows (fully reduced), <= min(b, s)
+    uint32_t* V = E + (size_t)std::min(b, s) * s;  // RD_BATCH reduced rows of the current batch
     __shared__ int rho[RD_MAX_B];
     __shared__ uint32_t cfb[RD_BATCH][RD_MAX_B];  // batch coefficients S_i[rho_t]
     __shared__ unsigned fmask[2];
@@ -1180,11 +1184,14 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     const size_t mark0 = ws.mark();
     DMat Uhat = ws.mat(std::max<int64_t>(mn, 1), n);
     DMat UO = ws.mat(std::max<int64_t>(mn, 1), SK);   // Uhat * Omega
-    DMat RI = ws.mat(B, n), Gs = ws.mat(B, std::max<int64_t>(mn, 1));
+    // adaptive chunks: sparse residuals take up to RD_MAX_ROWS rows per chunk (narrow detection)
+    const bool adaptive = SK > RD_NARROW && rd_narrow_on && !getenv("FFB_PLDUQ_FIXED_CHUNKS");
+    const int Bmax = adaptive ? RD_MAX_ROWS : B;
+    DMat RI = ws.mat(B, n), Gs = ws.mat(Bmax, std::max<int64_t>(mn, 1));
     DMat Kinv = ws.mat(B, B), Gi = ws.mat(B, std::max<int64_t>(mn, 1));
     DMat Upd = ws.mat(std::max<int64_t>(mn, 1), B);
     const int nblk0 = (int)cdiv(n, CRP_W);
-    int32_t* dinfo = ws.vec<int32_t>(2 * B + 16);     // row detect: k, I[0..k)
+    int32_t* dinfo = ws.vec<int32_t>(2 * Bmax + 16);  // row detect: k, I[0..k)
     int32_t* lists[2] = {ws.vec<int32_t>((int64_t)nblk0 * B), ws.vec<int32_t>((int64_t)nblk0 * B)};
     int32_t* counts[2] = {ws.vec<int32_t>(nblk0), ws.vec<int32_t>(nblk0)};
     int32_t* dflag = ws.vec<int32_t>(4);
@@ -1196,7 +1203,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     int32_t* d_pcol = d_prow + pstride;
     const size_t mark1 = ws.mark();
 
-    const size_t rd_smem = ((size_t)2 * RD_MAX_B * SK + (size_t)RD_BATCH * SK) * 4;
+    const size_t rd_smem = std::max(rd_smem_bytes(RD_MAX_B, SK), rd_smem_bytes(RD_MAX_ROWS, RD_NARROW));
     const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + 2 * (size_t)CRP_G * CRP_KMAX) * 4;
     static bool attrs = false;
     if (!attrs) {
@@ -1279,9 +1286,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         ws.release(mark1);
         r = 0;
         fill_words(st, (uint32_t*)dflag, 1, 0u);
-        DMat YO;
+        DMat YO, Om;
         if (!exact) {  // Y * Omega, once
-            DMat Om = ws.mat(n, SK);
+            Om = ws.mat(n, SK);
             launch_k(k_random, (unsigned)cdiv(n * SK, 256), 256, 0, st, Om.ptr, n * SK, 0x5EEDull + n + 977 * attempt, f.p);
             ++g_launches;
             YO = ws.mat(m, SK);
@@ -1298,8 +1305,11 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             cudaEventRecord(e, st);
             cev.push_back(e);
         };
-        for (int64_t c0 = 0; c0 < m; c0 += B) {
-            const int64_t bc = std::min<int64_t>(B, m - c0);
+        // chunk rows: 128, or up to RD_MAX_ROWS where the previous chunk was sparse (target
+        // ~12 detected rows per chunk: the per-chunk cost is ~55 us + ~9 us per detected row)
+        int64_t bc = 0, Bcur = B;
+        for (int64_t c0 = 0; c0 < m; c0 += bc) {
+            bc = std::min<int64_t>(exact ? B : Bcur, m - c0);
             DMat Yc = Y.sub(c0, 0, bc, n);
             mark();
             if (!exact) {
@@ -1321,18 +1331,33 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 // re-detected on all SK columns (the certificate guards both)
                 int k = 0;
                 for (int wide = (SK <= RD_NARROW || !rd_narrow_on) ? 1 : 0; wide < 2; ++wide) {
+                    if (wide && bc > B) {
+                        // a dense chunk after all: keep its first B rows; the sketch rows
+                        // after them were overwritten in place and are recomputed, Y Omega
+                        gemm(f, st, GEMM_SET, YO.sub(c0 + B, 0, bc - B, SK), Y.sub(c0 + B, 0, bc - B, n), false, Om,
+                             false, bc - B, SK, n);
+                        bc = B;
+                        Yc = Y.sub(c0, 0, bc, n);
+                        Sc = YO.sub(c0, 0, bc, SK);
+                    }
                     const MboxPost mp = io.post ? io.post() : MboxPost();
                     {
                         ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
                         if (wide)
-                            launch_k(k_row_detect<5>, 1, 256, rd_smem, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp);
+                            launch_k(k_row_detect<5>, 1, 256, rd_smem_bytes((int)bc, SK), st, f, Sc.ptr, Sc.ld, (int)bc,
+                                     SK, dinfo, mp);
                         else
-                            launch_k(k_row_detect<2>, 1, 256, rd_smem, st, f, Sc.ptr, Sc.ld, (int)bc, RD_NARROW, dinfo, mp);
+                            launch_k(k_row_detect<2>, 1, 256, rd_smem_bytes((int)bc, RD_NARROW), st, f, Sc.ptr, Sc.ld,
+                                     (int)bc, RD_NARROW, dinfo, mp);
                         ++g_launches;
                         FFB_CHECK_LAUNCH();
                     }
                     k = *(const int32_t*)(mp.dst ? io.wait(mp) : io.readback(dinfo, 4));
                     if (k < RD_NARROW - 16) break;
+                }
+                if (adaptive) {  // next chunk size from this chunk's density
+                    const double target = k > 0 ? 12.0 * (double)bc / k : 1e30;
+                    Bcur = target >= RD_MAX_ROWS ? RD_MAX_ROWS : (target >= 256 ? 256 : B);
                 }
                 mark();
                 if (k == 0) {
