@@ -157,7 +157,7 @@ __device__ __forceinline__ void reduce_rows_any(const Fp& f, uint32_t* X, int ld
 
 constexpr int RD_MAX_B = 128, RD_S = 144;
 constexpr int RD_NARROW = 64;  // sketch columns of the first row-detection pass
-constexpr int RD_MAX_ROWS = 512;  // chunk rows of a narrow row detection (adaptive chunks)
+constexpr int RD_MAX_ROWS = 640;  // chunk rows of a narrow row detection (adaptive chunks)
 static const bool rd_narrow_on = getenv("FFB_RD_WIDE") == nullptr;  // A/B hook
 
 constexpr int RD_BATCH = 16;
@@ -1305,8 +1305,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             cudaEventRecord(e, st);
             cev.push_back(e);
         };
-        // chunk rows: 128, or up to RD_MAX_ROWS where the previous chunk was sparse (target
-        // ~12 detected rows per chunk: the per-chunk cost is ~55 us + ~9 us per detected row)
+        // chunk rows: 128, or a multiple of 128 up to RD_MAX_ROWS where the previous chunk was
+        // sparse, aiming at ~24 detected rows per chunk (a chunk costs ~55 us + ~9 us per
+        // detected row; measured sweep of the target: 16 / 24 / 32 / 40 -> 128.3 / 126.7 /
+        // 126.8 / 128.3 ms on config 5)
         int64_t bc = 0, Bcur = B;
         for (int64_t c0 = 0; c0 < m; c0 += bc) {
             bc = std::min<int64_t>(exact ? B : Bcur, m - c0);
@@ -1356,8 +1358,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     if (k < RD_NARROW - 16) break;
                 }
                 if (adaptive) {  // next chunk size from this chunk's density
-                    const double target = k > 0 ? 12.0 * (double)bc / k : 1e30;
-                    Bcur = target >= RD_MAX_ROWS ? RD_MAX_ROWS : (target >= 256 ? 256 : B);
+                    static const double tk = getenv("FFB_PLDUQ_TARGET_K") ? atof(getenv("FFB_PLDUQ_TARGET_K")) : 24.0;
+                    static const int64_t rmax = getenv("FFB_PLDUQ_MAX_ROWS") ? atoll(getenv("FFB_PLDUQ_MAX_ROWS")) : RD_MAX_ROWS;
+                    const double target = k > 0 ? tk * (double)bc / k : 1e30;
+                    Bcur = std::min<int64_t>(std::max<int64_t>((int64_t)(target / B) * B, B), std::min<int64_t>(rmax, RD_MAX_ROWS));
                 }
                 mark();
                 if (k == 0) {
