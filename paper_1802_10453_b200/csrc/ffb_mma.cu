@@ -195,8 +195,9 @@ void mma_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool 
     // split K when the output has too few tiles to fill the GPU and K is long
     const int64_t tiles = cdiv(N, MM_T) * cdiv(M, MM_T);
     int S = 1;
-    if (tiles < 148 && K >= 512 && M * N <= ((int64_t)1 << 24))
-        S = (int)std::min<int64_t>(cdiv(K, 256), std::max<int64_t>(1, 296 / tiles));
+    static const int64_t split_ctas = getenv("FFB_MMA_SPLIT_CTAS") ? atoll(getenv("FFB_MMA_SPLIT_CTAS")) : 148;
+    if (tiles < split_ctas && K >= 512 && M * N <= ((int64_t)1 << 24))
+        S = (int)std::min<int64_t>(cdiv(K, 256), std::max<int64_t>(1, 2 * split_ctas / tiles));
     const int64_t kc = cdiv(cdiv(K, S), MM_T) * MM_T;
     S = (int)cdiv(K, kc);
     uint32_t* W = S > 1 ? mma_scratch((size_t)S * M * N) : nullptr;
