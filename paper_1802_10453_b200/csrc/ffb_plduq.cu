@@ -1504,22 +1504,30 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             continue;
         }
         DMat Kf = ws.mat(r, r);
-        const int32_t* dpr = io.upload(pr);
-        const int32_t* dpc = io.upload(pcol_rows);
+        // every index array of phase 2 and the certificate in one upload (one fetch launch)
+        const int64_t rA = (r + 3) & ~3, nA = (n + 3) & ~3, mA = (m + 3) & ~3;
+        std::vector<int32_t> idx((size_t)(2 * rA + nA + 2 * mA), 0);
+        std::copy(pr.begin(), pr.end(), idx.begin());
+        std::copy(pcol_rows.begin(), pcol_rows.end(), idx.begin() + rA);
+        std::copy(out.cimg.begin(), out.cimg.end(), idx.begin() + 2 * rA);
+        std::copy(out.rimg.begin() + r, out.rimg.end(), idx.begin() + 2 * rA + nA);
+        std::copy(out.rimg.begin(), out.rimg.end(), idx.begin() + 2 * rA + nA + mA);
+        const int32_t* didx = io.upload(idx);
+        const int32_t* dpr = didx;
+        const int32_t* dpc = didx + rA;
         gather2d(st, Kf, Y, dpr, dpc, 0);
         ldu_inplace(f, st, Kf, ws, dflag);
         launch_k(k_unpack_l, rgrid(r, r), 256, 0, st, io.Lo.ptr, io.Lo.ld, Kf.ptr, Kf.ld, r, io.d, 1 % f.p);
         ++g_launches;
         invert_vec(f, st, io.dinv, io.d, r);
         DMat Uo = io.Uo.sub(0, 0, r, n);
-        const int32_t* dcimg = io.upload(out.cimg);
+        const int32_t* dcimg = didx + 2 * rA;
         gather2d(st, Uo, Y, dpr, dcimg, 0);
         trsm_lower_unit(f, st, io.Lo.sub(0, 0, r, r), Uo);
         scale_rows(f, st, Uo, Uo, io.dinv);
         const int32_t* dnp = nullptr;
         if (m > r) {
-            std::vector<int32_t> np(out.rimg.begin() + r, out.rimg.end());
-            dnp = io.upload(np);
+            dnp = didx + 2 * rA + nA;
             DMat T = ws.mat(m - r, r), Tt = ws.mat(r, m - r), U1t = ws.mat(r, r);
             gather2d(st, T, Y, dnp, dpc, 0);
             transpose(st, Tt, T);
@@ -1534,7 +1542,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         // ---- certificate (sketch path only) ----
         {
             DMat W = ws.mat(m, n), H = ws.mat(m, r);
-            gather2d(st, W, Y, io.upload(out.rimg), dcimg, 0);
+            gather2d(st, W, Y, didx + 2 * rA + nA + mA, dcimg, 0);
             launch_k(k_scale_cols, rgrid(m, r), 256, 0, st, f, H.ptr, H.ld, io.Lo.ptr, io.Lo.ld, io.d, r);
             ++g_launches;
             gemm(f, st, GEMM_SUB, W, H, false, Uo, false, m, n, r);
