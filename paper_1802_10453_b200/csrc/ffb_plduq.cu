@@ -1390,6 +1390,8 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     // RPM of R_I on the candidates, Kinv and bookkeeping (1 CTA)
                     int rc_cap, si_off;
                     const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap, &si_off);
+                    static const int rc_lim = getenv("FFB_CF_DIRECT_MAX") ? atoi(getenv("FFB_CF_DIRECT_MAX")) : -1;
+                    if (rc_lim >= 0) rc_cap = std::min(rc_cap, rc_lim);  // A/B hook: direct vs scan path
                     DMat Kik = Kinv.sub(0, 0, k, k);
                     launch_k(k_crp_finish, 1, 256, cfmem, st, f, RI.ptr, RI.ld, k, lists[0], counts[0], nblk0,
                                                         (int32_t*)re_scratch, rc_cap, dI, c0, Sc.ptr, Sc.ld, SK,
