@@ -1360,8 +1360,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 if (adaptive) {  // next chunk size from this chunk's density
                     static const double tk = getenv("FFB_PLDUQ_TARGET_K") ? atof(getenv("FFB_PLDUQ_TARGET_K")) : 24.0;
                     static const int64_t rmax = getenv("FFB_PLDUQ_MAX_ROWS") ? atoll(getenv("FFB_PLDUQ_MAX_ROWS")) : RD_MAX_ROWS;
-                    const double target = k > 0 ? tk * (double)bc / k : 1e30;
-                    Bcur = std::min<int64_t>(std::max<int64_t>((int64_t)(target / B) * B, B), std::min<int64_t>(rmax, RD_MAX_ROWS));
+                    const int64_t cap = std::min<int64_t>(rmax, RD_MAX_ROWS);
+                    const double target = k > 0 ? std::min(tk * (double)bc / k, (double)cap) : (double)cap;
+                    Bcur = std::min<int64_t>(std::max<int64_t>((int64_t)(target / B) * B, B), cap);
                 }
                 mark();
                 if (k == 0) {

@@ -366,3 +366,42 @@ def test_banded_upload_matches_device_path(gpu, v):
         ffb.ldlt(b, w.p, cfg(v, 64), ctx=gpu)
     g2 = ffb.ldlt(a, w.p, cfg(v, 64), ctx=gpu)
     assert g2.rank == g.rank and np.array_equal(g2.lower, g.lower)
+
+
+@pytest.mark.parametrize("p", [3, 131, 8388593])
+def test_plduq_adaptive_chunks(gpu, oracle, p):
+    """The parallel PLDUQ sizes its row chunks from the previous chunk's density (128 up to
+    640 rows, narrow 64-column row detection).  This Y is sparse on top (rank 4 over 768
+    rows: the chunks grow) and dense below (a 640-row chunk finds >= 48 rows, shrinks to
+    128 rows with its sketch rows recomputed, then dense 128-row chunks, then growth
+    again once the rank is exhausted).  Bit-exact against the oracle."""
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(p + 11)
+    m, n, top = 1500, 300, 768
+    basis = rng.integers(0, p, (4, n)).astype(object)
+    coef = rng.integers(0, p, (top, 4)).astype(object)
+    y = np.zeros((m, n), dtype=np.uint64)
+    y[:top] = (coef.dot(basis) % p).astype(np.uint64)
+    y[top:] = rng.integers(0, p, (m - top, n), dtype=np.uint64)
+    g = ffb.plduq(y, p, ctx=gpu)
+    o = oracle.plduq(p, y)
+    assert g.rank == o["rank"]
+    assert np.array_equal(g.row_perm.image_array(), o["row_image"])
+    assert np.array_equal(g.col_perm.image_array(), o["col_image"])
+    assert np.array_equal(g.lower, o["lower"]) and np.array_equal(g.upper, o["upper"])
+    assert np.array_equal(g.diag, o["diag"])
+
+
+@pytest.mark.parametrize("p", [2, 3, 131])
+def test_fused_small_nodes(gpu, oracle, p):
+    """k_node128 (recursive_step of a node whose children are leaves, in one launch): nodes
+    of 65..128 rows with rook-placement rank profiles take both of its exits -- leaf(Z) on
+    the device (Y = 0, or m - r1 = 0) and the hand-back to the host's zero_leading_pairs
+    (Y != 0) -- plus full-rank, hollow and low-rank inputs; thresholds 64 and 32."""
+    rng = np.random.default_rng(1000 + p)
+    for n in (65, 77, 96, 127, 128):
+        for a in (rand_rook_rpm(rng, p, n, n // 2), rand_rook_rpm(rng, p, n, n // 4),
+                  rand_sym(rng, p, n), hollow(rng, p, n), rand_low_rank(rng, p, n, 9)):
+            check(gpu, oracle, p, a, "cascade", 64)
+    for n in (33, 50, 64):
+        check(gpu, oracle, p, rand_rook_rpm(rng, p, n, n // 2), "cascade", 32)
