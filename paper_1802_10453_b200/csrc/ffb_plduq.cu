@@ -1309,7 +1309,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         // sparse, aiming at ~24 detected rows per chunk (a chunk costs ~55 us + ~9 us per
         // detected row; measured sweep of the target: 16 / 24 / 32 / 40 -> 128.3 / 126.7 /
         // 126.8 / 128.3 ms on config 5)
-        int64_t bc = 0, Bcur = B;
+        // the first chunk is optimistic (the largest narrow chunk): residuals that reach
+        // the parallel path are mostly sparse, and a dense first chunk only costs a shrink
+        static const bool first_big = getenv("FFB_PLDUQ_FIRST_128") == nullptr;  // A/B hook
+        int64_t bc = 0, Bcur = (adaptive && first_big) ? RD_MAX_ROWS : B;
         for (int64_t c0 = 0; c0 < m; c0 += bc) {
             bc = std::min<int64_t>(exact ? B : Bcur, m - c0);
             DMat Yc = Y.sub(c0, 0, bc, n);
