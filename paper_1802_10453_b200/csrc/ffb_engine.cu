@@ -1492,7 +1492,8 @@ extern "C" int ffb_dbg_pq_bench(ffb_context* c, uint64_t p, int which, int rows,
         uint32_t* d;
         FFB_CUDA(cudaMalloc(&d, (size_t)rows * cols * 4));
         FFB_CUDA(cudaMemcpy(d, host, (size_t)rows * cols * 4, cudaMemcpyHostToDevice));
-        dbg_pq_bench(f, c->stream, which, rows, cols, d, reps, ms, out);
+        if (which == 2) dbg_leaf_bench(f, c->stream, rows, d, reps, ms, out);
+        else dbg_pq_bench(f, c->stream, which, rows, cols, d, reps, ms, out);
         FFB_CUDA(cudaFree(d));
     });
 }

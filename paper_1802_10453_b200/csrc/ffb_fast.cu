@@ -9,6 +9,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <vector>
 
 #include "ffb_kernels.cuh"
 #include "ffb_mma.cuh"
@@ -245,22 +246,21 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
         }
         __syncthreads();
         const uint32_t c0 = lz_red(f, rb[lane], off), c1 = lz_red(f, rb[lane + 32], off);
-        // off the critical path (they overlap the ballot chain): the inverse of this
-        // lane's residuals and the residuals of this warp's 16 columns
-        const uint32_t i0v = inv.t ? inv.t[c0] : 0u, i1v = inv.t ? inv.t[c1] : 0u;
-        const uint32_t csrc = lo ? c0 : c1;
-        int32_t ck[16];
-#pragma unroll
-        for (int t = 0; t < 16; ++t) ck[t] = (int32_t)__shfl_sync(0xffffffffu, csrc, (16 * wp + t) & 31);
         const uint32_t b0 = __ballot_sync(0xffffffffu, c0 != 0) & alo;
         const uint32_t b1 = __ballot_sync(0xffffffffu, c1 != 0) & ahi;
-        const int j = b0 ? __ffs(b0) - 1 : (b1 ? 31 + __ffs(b1) : s);
-        if (j >= s) {  // pivotless (sytrf.cpp:82-85)
+        if (!(b0 | b1)) {  // pivotless (sytrf.cpp:82-85)
             if (tid == 0) sm.pless[npl] = p1;
             ++npl;
             clear_bit(p1);
             continue;
         }
+        const int j = b0 ? __ffs(b0) - 1 : 31 + __ffs(b1);
+        // the inverse of this lane's residuals and the residuals of this warp's 16 columns
+        const uint32_t i0v = inv.t ? inv.t[c0] : 0u, i1v = inv.t ? inv.t[c1] : 0u;
+        const uint32_t csrc = lo ? c0 : c1;
+        int32_t ck[16];
+#pragma unroll
+        for (int t = 0; t < 16; ++t) ck[t] = (int32_t)__shfl_sync(0xffffffffu, csrc, (16 * wp + t) & 31);
         if (j == p1) {  // 1x1 pivot (sytrf.cpp:87-97)
             const int src_l = p1 & 31;
             const uint32_t x = __shfl_sync(0xffffffffu, p1 < 32 ? c0 : c1, src_l);
@@ -1127,6 +1127,42 @@ void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tin
 }
 
 }  // namespace
+
+// Leaf micro-benchmark (tools/leaf_bench.py; not part of the C-ABI): reps launches of
+// the leaf kernel on an s x s device matrix, average ms (CUDA events), rank in out[0].
+void dbg_leaf_bench(const Fp& f, cudaStream_t st, int s, const uint32_t* d_a, int reps, double* ms,
+                    int32_t* out_rank) {
+    uint32_t* Lg;
+    int32_t *rows, *out;
+    DDiag D;
+    FFB_CUDA(cudaMalloc(&Lg, (size_t)s * s * 4));
+    FFB_CUDA(cudaMalloc(&rows, (size_t)s * 4 + 64));
+    FFB_CUDA(cudaMalloc(&out, (size_t)(s + 2) * 4 + 64));
+    FFB_CUDA(cudaMalloc(&D.kind, (size_t)s * 4 + 64));
+    FFB_CUDA(cudaMalloc(&D.val, (size_t)s * 4 + 64));
+    FFB_CUDA(cudaMalloc(&D.val2, (size_t)s * 4 + 64));
+    FFB_CUDA(cudaMalloc(&D.inv, (size_t)s * 4 + 64));
+    std::vector<int32_t> h(s);
+    for (int i = 0; i < s; ++i) h[i] = i;
+    FFB_CUDA(cudaMemcpy(rows, h.data(), (size_t)s * 4, cudaMemcpyHostToDevice));
+    DMat A{const_cast<uint32_t*>(d_a), s, s, s}, L{Lg, s, s, s};
+    cudaEvent_t e0, e1;
+    FFB_CUDA(cudaEventCreate(&e0));
+    FFB_CUDA(cudaEventCreate(&e1));
+    leaf64(f, st, A, rows, L, 0, D, out, MboxPost());
+    FFB_CUDA(cudaEventRecord(e0, st));
+    for (int i = 0; i < reps; ++i) leaf64(f, st, A, rows, L, 0, D, out, MboxPost());
+    FFB_CUDA(cudaEventRecord(e1, st));
+    FFB_CUDA(cudaEventSynchronize(e1));
+    float t = 0;
+    FFB_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t / reps;
+    FFB_CUDA(cudaMemcpy(out_rank, out, 4, cudaMemcpyDeviceToHost));
+    for (void* q : {(void*)Lg, (void*)rows, (void*)out, (void*)D.kind, (void*)D.val, (void*)D.val2, (void*)D.inv})
+        FFB_CUDA(cudaFree(q));
+    FFB_CUDA(cudaEventDestroy(e0));
+    FFB_CUDA(cudaEventDestroy(e1));
+}
 
 bool leaf64_supported(int64_t s) { return s <= 64; }
 

@@ -152,6 +152,8 @@ bool leaf_crout(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat 
 size_t leaf_scratch_words(int64_t s);
 // Register-resident leaf for s <= 64 (ffb_fast.cu).
 bool leaf64_supported(int64_t s);
+void dbg_leaf_bench(const Fp& f, cudaStream_t st, int s, const uint32_t* d_a, int reps, double* ms,
+                    int32_t* out_rank);
 void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff,
             DDiag D, int32_t* out, const MboxPost& mp);
 // Fused small node (ffb_fast.cu): recursive_step + zero_leading of an s x s node whose
