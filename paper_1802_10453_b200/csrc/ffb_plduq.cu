@@ -916,13 +916,24 @@ __global__ void __launch_bounds__(256) k_pair2(Fp f, const uint32_t* RI, int64_t
 }
 
 // H[i][t] = L[i][t] * d[t]
+// H[ridx ? ridx[i] : i][t] = L[i][t] d[t]
 __global__ void k_scale_cols(Fp f, uint32_t* H, int64_t ldh, const uint32_t* L, int64_t ldl,
-                             const uint32_t* d, int64_t cols) {
+                             const uint32_t* d, int64_t cols, const int32_t* ridx) {
     FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
+    uint32_t* h = H + (ridx ? (int64_t)ridx[i] : i) * ldh;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cols;
          t += (int64_t)gridDim.x * blockDim.x)
-        H[i * ldh + t] = fmul(f, L[i * ldl + t], d[t]);
+        h[t] = fmul(f, L[i * ldl + t], d[t]);
+}
+
+// dst[a][cidx[b]] = src[a][b]: columns back to their original positions
+__global__ void k_scatter_cols(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds, const int32_t* cidx,
+                               int64_t cols) {
+    FFB_PDL_ENTRY();
+    const int64_t a = blockIdx.y;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < cols; b += (int64_t)gridDim.x * blockDim.x)
+        dst[a * ldd + cidx[b]] = src[a * lds + b];
 }
 
 // Certificate part: pivotless row t (= np[a]) may only depend on pivots found before it.
@@ -1545,14 +1556,17 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             if (*(const int32_t*)io.readback(dflag, 4)) throw Status(FFB_ERROR, "plduq: singular pivot block");
             break;
         }
-        // ---- certificate (sketch path only) ----
+        // ---- certificate (sketch path only): Y - P L D U Q == 0, checked in place on Y in
+        // its own order (no m x n gather): H = P (L D), Up = U Q; Y is not needed after the
+        // PLDUQ, and a failed certificate adds the product back before the exact retry ----
+        DMat H = ws.mat(m, r), Up = ws.mat(r, n);
         {
-            DMat W = ws.mat(m, n), H = ws.mat(m, r);
-            gather2d(st, W, Y, didx + 2 * rA + nA + mA, dcimg, 0);
-            launch_k(k_scale_cols, rgrid(m, r), 256, 0, st, f, H.ptr, H.ld, io.Lo.ptr, io.Lo.ld, io.d, r);
-            ++g_launches;
-            gemm(f, st, GEMM_SUB, W, H, false, Uo, false, m, n, r);
-            any_nonzero(st, W, dflag);
+            launch_k(k_scale_cols, rgrid(m, r), 256, 0, st, f, H.ptr, H.ld, io.Lo.ptr, io.Lo.ld, io.d, r,
+                     didx + 2 * rA + nA + mA);
+            launch_k(k_scatter_cols, rgrid(r, n), 256, 0, st, Up.ptr, Up.ld, Uo.ptr, Uo.ld, dcimg, n);
+            g_launches += 2;
+            gemm(f, st, GEMM_SUB, Y, H, false, Up, false, m, n, r);
+            any_nonzero(st, Y, dflag);
             if (m > r) {
                 launch_k(k_m1_pattern, rgrid(m - r, r), 256, 0, st, io.Lo.ptr + r * io.Lo.ld, io.Lo.ld, dnp,
                                                               d_prow, r, dflag);
@@ -1560,6 +1574,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             }
         }
         if (*(const int32_t*)io.readback(dflag, 4) == 0) break;
+        gemm(f, st, GEMM_ADD, Y, H, false, Up, false, m, n, r);  // Y restored for the exact retry
         ++out.fallbacks;  // a sketch missed rank: redo the search exactly
         exact = true;
     }
