@@ -1088,6 +1088,14 @@ __global__ void __launch_bounds__(512) k_ldu128(Fp f, uint32_t* K, int64_t ldk, 
             if (r0 + a < n && c0 + b < n) K[(int64_t)(r0 + a) * ldk + c0 + b] = T[a][b];
 }
 
+// U (unit upper with zeros below) from the packed LDU block.
+__global__ void k_unpack_u(uint32_t* U, int64_t ldu, const uint32_t* K, int64_t ldk, int64_t n, uint32_t one) {
+    FFB_PDL_ENTRY();
+    const int64_t i = blockIdx.y;
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+        U[i * ldu + j] = j > i ? K[i * ldk + j] : (j == i ? one : 0);
+}
+
 // L (unit lower with zeros above) from the packed LDU block; d from the diagonal.
 __global__ void k_unpack_l(uint32_t* L, int64_t ldl, const uint32_t* K, int64_t ldk, int64_t n,
                            uint32_t* d, uint32_t one) {
@@ -1208,10 +1216,12 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     int32_t* dflag = ws.vec<int32_t>(4);
     int32_t* dsig = ws.vec<int32_t>(B);
     uint32_t* re_scratch = ws.vec<uint32_t>((int64_t)nblk0 * CRP_KMAX + 64);  // candidate list
-    int32_t* d_uhat_col = ws.vec<int32_t>(std::max<int64_t>(mn, 1));
+    // pivot rows, pivot columns (pivot order) and the pivot column of each Uhat row,
+    // adjacent: one read-back after the row loop
     const int64_t pstride = (std::max<int64_t>(mn, 1) + 63) / 64 * 64;
-    int32_t* d_prow = ws.vec<int32_t>(2 * pstride);
+    int32_t* d_prow = ws.vec<int32_t>(3 * pstride);
     int32_t* d_pcol = d_prow + pstride;
+    int32_t* d_uhat_col = d_prow + 2 * pstride;
     const size_t mark1 = ws.mark();
 
     const size_t rd_smem = std::max(rd_smem_bytes(RD_MAX_B, SK), rd_smem_bytes(RD_MAX_ROWS, RD_NARROW));
@@ -1492,11 +1502,12 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             for (auto e : cev) cudaEventDestroy(e);
         }
         out.r = r;
-        std::vector<int32_t> pr, pcol_rows;
-        if (r > 0) {  // d_prow and d_pcol are adjacent: one read-back
-            const int32_t* hp = (const int32_t*)io.readback(d_prow, (size_t)(2 * pstride) * 4);
+        std::vector<int32_t> pr, pcol_rows, uhat_cols;
+        if (r > 0) {  // d_prow, d_pcol and d_uhat_col are adjacent: one read-back
+            const int32_t* hp = (const int32_t*)io.readback(d_prow, (size_t)(3 * pstride) * 4);
             pr.assign(hp, hp + r);
             pcol_rows.assign(hp + pstride, hp + pstride + r);
+            uhat_cols.assign(hp + 2 * pstride, hp + 2 * pstride + r);
         }
 
         // ---- phase 2: factors from the pivots ----
@@ -1523,7 +1534,12 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         DMat Kf = ws.mat(r, r);
         // every index array of phase 2 and the certificate in one upload (one fetch launch)
         const int64_t rA = (r + 3) & ~3, nA = (n + 3) & ~3, mA = (m + 3) & ~3;
-        std::vector<int32_t> idx((size_t)(2 * rA + nA + 2 * mA), 0);
+        std::vector<int32_t> idx((size_t)(3 * rA + nA + 2 * mA), 0);
+        {  // upos[t]: the Uhat row whose pivot column is pc[t]
+            std::vector<int32_t> at(n, -1);
+            for (int64_t i = 0; i < r; ++i) at[uhat_cols[i]] = (int32_t)i;
+            for (int64_t t = 0; t < r; ++t) idx[2 * rA + nA + 2 * mA + t] = at[pcol_rows[t]];
+        }
         std::copy(pr.begin(), pr.end(), idx.begin());
         std::copy(pcol_rows.begin(), pcol_rows.end(), idx.begin() + rA);
         std::copy(out.cimg.begin(), out.cimg.end(), idx.begin() + 2 * rA);
@@ -1539,9 +1555,17 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         invert_vec(f, st, io.dinv, io.d, r);
         DMat Uo = io.Uo.sub(0, 0, r, n);
         const int32_t* dcimg = didx + 2 * rA;
-        gather2d(st, Uo, Y, dpr, dcimg, 0);
-        trsm_lower_unit(f, st, io.Lo.sub(0, 0, r, r), Uo);
-        scale_rows(f, st, Uo, Uo, io.dinv);
+        {
+            // U = D^-1 L1^-1 Y[pr, Q].  The row loop left Uhat = Y[pr, pcu]^-1 Y[pr, :]
+            // (fully reduced: identity on its pivot columns pcu), and Y[pr, pcu] = K Pi with
+            // K = L1 D U1, so U = U1 (Pi Uhat)[:, Q]: one r x r x n GEMM instead of the
+            // r x r triangular solve on r x n right-hand sides
+            DMat Ug = ws.mat(r, n), U1 = ws.mat(r, r);
+            gather2d(st, Ug, Uhat.sub(0, 0, r, n), didx + 2 * rA + nA + 2 * mA, dcimg, 0);
+            launch_k(k_unpack_u, rgrid(r, r), 256, 0, st, U1.ptr, U1.ld, Kf.ptr, Kf.ld, r, 1 % f.p);
+            ++g_launches;
+            gemm(f, st, GEMM_SET, Uo, U1, false, Ug, false, r, n, r);
+        }
         const int32_t* dnp = nullptr;
         if (m > r) {
             dnp = didx + 2 * rA + nA;
