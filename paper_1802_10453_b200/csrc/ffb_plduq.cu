@@ -30,6 +30,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <functional>
 #include <vector>
 
 #include "ffb_kernels.cuh"
@@ -52,6 +53,14 @@ __global__ void k_gather2d(uint32_t* dst, int64_t ldd, const uint32_t* src, int6
     for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < cols;
          b += (int64_t)gridDim.x * blockDim.x)
         d[b] = s[cidx[b]];
+}
+
+// rows [0, rows) of src into dst (grid.y = row, grid-stride columns)
+__global__ void k_copy_rows(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds, int64_t cols) {
+    FFB_PDL_ENTRY();
+    const int64_t a = blockIdx.y;
+    for (int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; b < cols; b += (int64_t)gridDim.x * blockDim.x)
+        dst[a * ldd + b] = __ldcg(src + a * lds + b);
 }
 
 __global__ void k_random(uint32_t* out, int64_t n, uint64_t seed, uint32_t p) {
@@ -161,6 +170,10 @@ constexpr int RD_MAX_ROWS = 640;  // chunk rows of a narrow row detection (adapt
 static const bool rd_narrow_on = getenv("FFB_RD_WIDE") == nullptr;  // A/B hook
 
 constexpr int RD_BATCH = 16;
+// pipelined detection: chunks of B rows whose predecessor found <= PIPE_KMAX rows; the
+// stacked detection is trusted up to PIPE_TRUST rows (a margin of RD_S - PIPE_TRUST sketch
+// columns), above that the chunk is detected again serially
+constexpr int PIPE_KMAX = 32, PIPE_TRUST = 64, RD_PIPE = 96;
 __host__ __device__ inline size_t rd_smem_bytes(int b, int s) {
     return ((size_t)b * s + (size_t)std::min(b, s) * s + (size_t)RD_BATCH * s) * 4;
 }
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
         __syncthreads();
         const unsigned pending = fmask[bi & 1];  // rows outside the span of the batch-start basis
         if (!pending) continue;
-        const int cnt = batch_insert<NQ>(f, inv, V, s, pending, s, E, k, s, rho, bs);
+        const int cnt = batch_insert<NQ>(f, inv, V, s, pending, s, E, k, min(s, RD_MAX_B), rho, bs);
         if (tid < cnt) out[1 + k + tid] = i0 + bs.ins[tid];  // inserted in row order
         k += cnt;
     }
@@ -571,7 +584,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     Fp f, const uint32_t* RI, int64_t ldr, int k, const int32_t* lists,
     const int32_t* counts, int nblk, int32_t* cand_g, int rc_cap, const int32_t* I, int64_t c0,
     const uint32_t* S, int64_t lds, int s, uint32_t* Kinv, int32_t* Jout, uint32_t* UO, int64_t lduo,
-    int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r, int32_t* fail, int si_off) {
+    int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r, int32_t* fail, int si_off, int s_compact) {
     FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t off[1025];
@@ -612,7 +625,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
             for (int q = lane; q < s4; q += 32) {
             asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
                              (uint32_t)__cvta_generic_to_shared(sm + si_off + (size_t)u * s + 4 * q)),
-                         "l"(S + (int64_t)Is[u] * lds + 4 * q));
+                         "l"(S + (int64_t)(s_compact ? u : Is[u]) * lds + 4 * q));
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     }
@@ -764,7 +777,8 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         uint32_t* SI = si_early ? sm + si_off : M;
         if (!si_early)
             for (int u = wp; u < k; u += 8)
-                for (int col = lane; col < s; col += 32) SI[(size_t)u * s + col] = __ldcg(S + (int64_t)Is[u] * lds + col);
+                for (int col = lane; col < s; col += 32)
+                    SI[(size_t)u * s + col] = __ldcg(S + (int64_t)(s_compact ? u : Is[u]) * lds + col);
         __syncthreads();
         const bool lz = (uint64_t)k * (f.p - 1) * (f.p - 1) < (1ull << 32) && f.mu32;  // 32-bit sums
         for (int t = wp; t < k; t += 8) {
@@ -1213,8 +1227,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     // adaptive chunks: sparse residuals take up to RD_MAX_ROWS rows per chunk (narrow detection)
     const bool adaptive = SK > RD_NARROW && rd_narrow_on && !getenv("FFB_PLDUQ_FIXED_CHUNKS");
     const int Bmax = adaptive ? RD_MAX_ROWS : B;
-    DMat RI = ws.mat(B, n), Gs = ws.mat(Bmax, std::max<int64_t>(mn, 1));
-    DMat Kinv = ws.mat(B, B), Gi = ws.mat(B, std::max<int64_t>(mn, 1));
+    DMat RIb[2] = {ws.mat(B, n), ws.mat(B, n)};
+    DMat RI = RIb[0], Gs = ws.mat(Bmax, std::max<int64_t>(mn, 1));
+    DMat Kinv = ws.mat(B, B), Gi = ws.mat(B, std::max<int64_t>(mn, 1)), Gi2 = ws.mat(B, std::max<int64_t>(mn, 1));
+    DMat Gi3 = ws.mat(B, std::max<int64_t>(mn, 1)), Cg = ws.mat(B, B);
     DMat Upd = ws.mat(std::max<int64_t>(mn, 1), B);
     const int nblk0 = (int)cdiv(n, CRP_W);
     int32_t* dinfo = ws.vec<int32_t>(2 * Bmax + 16);  // row detect: k, I[0..k)
@@ -1229,14 +1245,15 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     int32_t* d_prow = ws.vec<int32_t>(3 * pstride);
     int32_t* d_pcol = d_prow + pstride;
     int32_t* d_uhat_col = d_prow + 2 * pstride;
-    const size_t mark1 = ws.mark();
 
-    const size_t rd_smem = std::max(rd_smem_bytes(RD_MAX_B, SK), rd_smem_bytes(RD_MAX_ROWS, RD_NARROW));
+    const size_t rd_smem = std::max({rd_smem_bytes(RD_MAX_B, SK), rd_smem_bytes(RD_MAX_ROWS, RD_NARROW),
+                                      rd_smem_bytes(PIPE_KMAX + B, SK)});
     const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + 2 * (size_t)CRP_G * CRP_KMAX) * 4;
     static bool attrs = false;
     if (!attrs) {
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
+        FFB_CUDA(cudaFuncSetAttribute(k_row_detect<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_crp_list, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)crp_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_pair2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(3 * CRP_KMAX * CRP_KMAX * 4)));
         FFB_CUDA(cudaFuncSetAttribute(k_crp_rowelim, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1257,6 +1274,22 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         FFB_CUDA(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
         FFB_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
     }
+    // side2: pipelined sketch + row detection of the next chunk (highest priority: its
+    // 1-CTA detection is latency-bound and must not queue behind the Uhat updates)
+    static thread_local cudaStream_t side2 = nullptr;
+    static thread_local cudaEvent_t ev_gk = nullptr, ev_si = nullptr, ev_sk = nullptr, ev_det = nullptr,
+                                    ev_t1 = nullptr, ev_un = nullptr;
+    if (!side2) {
+        int least = 0, greatest = 0;
+        FFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        FFB_CUDA(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, greatest));
+        for (cudaEvent_t* e : {&ev_gk, &ev_si, &ev_sk, &ev_det, &ev_t1, &ev_un})
+            FFB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    static const bool pipe_on = overlap_ok && !getenv("FFB_PLDUQ_NO_PIPE");  // A/B hook
+    DMat T2[2] = {ws.mat(PIPE_KMAX + B, SK), ws.mat(PIPE_KMAX + B, SK)};
+    int32_t* pinfo[2] = {ws.vec<int32_t>(2 * (PIPE_KMAX + B) + 16), ws.vec<int32_t>(2 * (PIPE_KMAX + B) + 16)};
+    const size_t mark1b = ws.mark();
     bool side_pending = false;
     auto join_side = [&]() {
         if (side_pending) {
@@ -1269,7 +1302,8 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     // R_I in RI) and pivot column set dJ (ascending): pairing, Unew into Uhat
     // rows [r, r+k), old rows reduced at J, Uhat*Omega maintained when sketching.
     auto absorb = [&](int64_t r, int k, const int32_t* dI, const int32_t* dJ, int64_t c0,
-                      bool sketching, const int32_t* sigma_in, DMat Sk, bool paired) {
+                      bool sketching, const int32_t* sigma_in, DMat Sk, bool paired,
+                      const std::function<bool()>& mid = {}) {
         DMat RIk = RI.sub(0, 0, k, n), Kik = Kinv.sub(0, 0, k, k);
         Kik.ld = k;
         if (!paired) {
@@ -1292,6 +1326,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 gemm(f, st, GEMM_SUB, UO.sub(0, 0, r, SK), Up, false, UO.sub(r, 0, k, SK), false, r,
                      SK, k);
         }
+        // mid: issued between the main-stream part and the side part (the pipelined next
+        // chunk's T1, which must read Uhat_old before the update below); true: wait for it
+        const bool t1_wait = mid ? mid() : false;
         if (sketching && overlap_ok) {
             FFB_CUDA(cudaEventRecord(ev_main, st));
             FFB_CUDA(cudaStreamWaitEvent(side, ev_main, 0)); pdl_fence(side);
@@ -1300,6 +1337,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         {
             SlotGuard slot(us == st ? g_slot : 1);
             gemm(f, us, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);  // Unew = Kc^-1 R_I
+            FFB_CUDA(cudaEventRecord(ev_un, us));
+            if (t1_wait) {  // the next chunk's T1 reads Uhat_old first
+                FFB_CUDA(cudaStreamWaitEvent(us, ev_t1, 0)); pdl_fence(us);
+            }
             if (r > 0) gemm(f, us, GEMM_SUB, Uhat.sub(0, 0, r, n), Up, false, Un, false, r, n, k);
         }
         if (us != st) {
@@ -1311,7 +1352,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     int64_t r = 0;
     bool exact = force_exact;
     for (int attempt = 0; attempt < 2; ++attempt) {
-        ws.release(mark1);
+        ws.release(mark1b);
         r = 0;
         fill_words(st, (uint32_t*)dflag, 1, 0u);
         DMat YO, Om;
@@ -1341,52 +1382,87 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         // the parallel path are mostly sparse, and a dense first chunk only costs a shrink
         static const bool first_big = getenv("FFB_PLDUQ_FIRST_128") == nullptr;  // A/B hook
         int64_t bc = 0, Bcur = (adaptive && first_big) ? RD_MAX_ROWS : B;
+        // pipelined detection (dense chunks): chunk c+1's sketch and row detection run on
+        // side2 beside chunk c's residual / CRP / finish.  The sketch of c+1 is taken
+        // against the basis before chunk c (UO[0:r], r at chunk c), so the detection is
+        // run on the stack [S_I(c); S(c+1)]: S_I(c) = sketches of chunk c's detected rows
+        // against the same basis, inserted first.  A row of c+1 independent of them and
+        // of its earlier rows (modulo span(Uhat_old)) is independent of span(Uhat_new).
+        bool pre = false, pre_done = false, t1 = false;
+        int pre_k = 0, pb = 0, pre_kt = 0, rb = 0, prev_k = 0;
+        RI = RIb[0];
+        int64_t pre_bc = 0;
+        MboxPost pre_mp;
         for (int64_t c0 = 0; c0 < m; c0 += bc) {
             bc = std::min<int64_t>(exact ? B : Bcur, m - c0);
+            if (pre) bc = pre_bc;
             DMat Yc = Y.sub(c0, 0, bc, n);
             mark();
             if (!exact) {
-                // sketch of the chunk residual, in place in its (otherwise unused)
-                // rows of Y*Omega: S = (Y Omega)_c - Y_c[:, pc] (Uhat Omega), a GEMM
                 DMat Sc = YO.sub(c0, 0, bc, SK);
-                if (r > 0) {
-                    DMat Gc = Gs.sub(0, 0, bc, r);
-                    {
-                        ProfScope ps(K_PQ_SKETCH, st, 0.0, 0.0);
-                        gather2d(st, Gc, Yc, nullptr, d_uhat_col, 0);
-                    }
-                    gemm(f, st, GEMM_SUB, Sc, Gc, false, UO.sub(0, 0, r, SK), false, bc, SK, r);
-                }
-                mark();
-                // row detection on the first RD_NARROW sketch columns (2 ballot groups instead
-                // of 5): rows independent there are independent in R; a chunk that finds
-                // k >= RD_NARROW - 16 may have more than the narrow sketch can show, and is
-                // re-detected on all SK columns (the certificate guards both)
                 int k = 0;
-                for (int wide = (SK <= RD_NARROW || !rd_narrow_on) ? 1 : 0; wide < 2; ++wide) {
-                    if (wide && bc > B) {
-                        // a dense chunk after all: keep its first B rows; the sketch rows
-                        // after them were overwritten in place and are recomputed, Y Omega
-                        gemm(f, st, GEMM_SET, YO.sub(c0 + B, 0, bc - B, SK), Y.sub(c0 + B, 0, bc - B, n), false, Om,
-                             false, bc - B, SK, n);
-                        bc = B;
-                        Yc = Y.sub(c0, 0, bc, n);
-                        Sc = YO.sub(c0, 0, bc, SK);
+                const int32_t* dI = dinfo + 1;
+                int64_t base = c0;  // row c0' + dI[t] of Y is detected row t
+                bool det_pipe = false;
+                bool use_t1 = false;
+                if (pre) {
+                    pre = false;
+                    const int kt = pre_done ? pre_kt
+                                            : *(const int32_t*)(pre_mp.dst ? io.wait(pre_mp) : io.readback(pinfo[pb], 4));
+                    pre_done = false;
+                    use_t1 = t1;
+                    t1 = false;
+                    FFB_CUDA(cudaStreamWaitEvent(st, ev_det, 0)); pdl_fence(st);
+                    if (kt >= pre_k && kt <= PIPE_TRUST) {
+                        k = kt - pre_k;
+                        dI = pinfo[pb] + 1 + pre_k;
+                        base = c0 - pre_k;
+                        det_pipe = true;
+                    }  // else: near the sketch capacity -- detect again below, serially
+                }
+                if (!det_pipe) {
+                    // sketch of the chunk residual, in place in its (otherwise unused)
+                    // rows of Y*Omega: S = (Y Omega)_c - Y_c[:, pc] (Uhat Omega), a GEMM
+                    if (r > 0) {
+                        DMat Gc = Gs.sub(0, 0, bc, r);
+                        {
+                            ProfScope ps(K_PQ_SKETCH, st, 0.0, 0.0);
+                            gather2d(st, Gc, Yc, nullptr, d_uhat_col, 0);
+                        }
+                        gemm(f, st, GEMM_SUB, Sc, Gc, false, UO.sub(0, 0, r, SK), false, bc, SK, r);
                     }
-                    const MboxPost mp = io.post ? io.post() : MboxPost();
-                    {
-                        ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-                        if (wide)
-                            launch_k(k_row_detect<5>, 1, 256, rd_smem_bytes((int)bc, SK), st, f, Sc.ptr, Sc.ld, (int)bc,
-                                     SK, dinfo, mp);
-                        else
-                            launch_k(k_row_detect<2>, 1, 256, rd_smem_bytes((int)bc, RD_NARROW), st, f, Sc.ptr, Sc.ld,
-                                     (int)bc, RD_NARROW, dinfo, mp);
-                        ++g_launches;
-                        FFB_CHECK_LAUNCH();
+                    mark();
+                    // row detection on the first RD_NARROW sketch columns (2 ballot groups instead
+                    // of 5): rows independent there are independent in R; a chunk that finds
+                    // k >= RD_NARROW - 16 may have more than the narrow sketch can show, and is
+                    // re-detected on all SK columns (the certificate guards both)
+                    for (int wide = (SK <= RD_NARROW || !rd_narrow_on) ? 1 : 0; wide < 2; ++wide) {
+                        if (wide && bc > B) {
+                            // a dense chunk after all: keep its first B rows; the sketch rows
+                            // after them were overwritten in place and are recomputed, Y Omega
+                            gemm(f, st, GEMM_SET, YO.sub(c0 + B, 0, bc - B, SK), Y.sub(c0 + B, 0, bc - B, n), false, Om,
+                                 false, bc - B, SK, n);
+                            bc = B;
+                            Yc = Y.sub(c0, 0, bc, n);
+                            Sc = YO.sub(c0, 0, bc, SK);
+                        }
+                        const MboxPost mp = io.post ? io.post() : MboxPost();
+                        {
+                            ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
+                            if (wide)
+                                launch_k(k_row_detect<5>, 1, 256, rd_smem_bytes((int)bc, SK), st, f, Sc.ptr, Sc.ld, (int)bc,
+                                         SK, dinfo, mp);
+                            else
+                                launch_k(k_row_detect<2>, 1, 256, rd_smem_bytes((int)bc, RD_NARROW), st, f, Sc.ptr, Sc.ld,
+                                         (int)bc, RD_NARROW, dinfo, mp);
+                            ++g_launches;
+                            FFB_CHECK_LAUNCH();
+                        }
+                        k = *(const int32_t*)(mp.dst ? io.wait(mp) : io.readback(dinfo, 4));
+                        if (k < RD_NARROW - 16) break;
                     }
-                    k = *(const int32_t*)(mp.dst ? io.wait(mp) : io.readback(dinfo, 4));
-                    if (k < RD_NARROW - 16) break;
+                } else {
+                    mark();
                 }
                 if (adaptive) {  // next chunk size from this chunk's density
                     static const double tk = getenv("FFB_PLDUQ_TARGET_K") ? atof(getenv("FFB_PLDUQ_TARGET_K")) : 24.0;
@@ -1400,15 +1476,87 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     mark(); mark(); mark();
                     continue;
                 }
-                join_side();  // the previous chunk's Uhat update, before RI / Kinv / Upd are reused
-                const int32_t* dI = dinfo + 1;
-                // exact residual of the k detected rows: R_I = Y_I - Y_I[:, pc] Uhat
-                DMat RIk = RI.sub(0, 0, k, n);
-                gather_rows(st, RIk, Yc, dI);
-                if (r > 0) {
+                // On side2, beside this chunk's residual / CRP / finish: S_I against the
+                // current basis in T rows [0, k) (a detected chunk's own sketch rows when it
+                // was detected serially; recomputed from Y Omega after a pipelined
+                // detection), then chunk c+1's sketch and its stacked detection on the
+                // first RD_PIPE sketch columns
+                const int64_t c0n = c0 + bc;
+                const bool pipe = pipe_on && SK == RD_S && c0n < m && Bcur == B && k <= PIPE_KMAX;
+                const bool compact = pipe || det_pipe;
+                DMat Sfin = Sc;
+                if (compact) {
+                    pb ^= 1;
+                    DMat T = T2[pb];
+                    FFB_CUDA(cudaEventRecord(ev_gk, st));
+                    FFB_CUDA(cudaStreamWaitEvent(side2, ev_gk, 0)); pdl_fence(side2);
+                    SlotGuard slot(3);
+                    Sfin = T.sub(0, 0, k, SK);
+                    if (det_pipe) {
+                        gather_rows(side2, Sfin, YO.sub(base, 0, m - base, SK), dI);
+                        if (r > 0) {
+                            DMat Gk2 = Gi2.sub(0, 0, k, r);
+                            gather2d(side2, Gk2, Y, dI, d_uhat_col, base);
+                            gemm(f, side2, GEMM_SUB, Sfin, Gk2, false, UO.sub(0, 0, r, SK), false, k, SK, r);
+                        }
+                    } else {
+                        gather_rows(side2, Sfin, Sc, dI);
+                    }
+                    FFB_CUDA(cudaEventRecord(ev_si, side2));
+                    if (pipe) {
+                        const int64_t bcn = std::min<int64_t>(B, m - c0n);
+                        DMat Sn = T.sub(k, 0, bcn, SK);
+                        launch_k(k_copy_rows, dim3(1, (unsigned)bcn), 160, 0, side2, Sn.ptr, Sn.ld,
+                                 YO.ptr + c0n * YO.ld, YO.ld, (int64_t)SK);
+                        ++g_launches;
+                        if (r > 0) {
+                            DMat Gc = Gs.sub(0, 0, bcn, r);
+                            gather2d(side2, Gc, Y.sub(c0n, 0, bcn, n), nullptr, d_uhat_col, 0);
+                            gemm(f, side2, GEMM_SUB, Sn, Gc, false, UO.sub(0, 0, r, SK), false, bcn, SK, r);
+                        }
+                        FFB_CUDA(cudaEventRecord(ev_sk, side2));
+                        pre_mp = io.post ? io.post() : MboxPost();
+                        {
+                            ProfScope ps(K_PLDUQ, side2, 0.0, 0.0);
+                            launch_k(k_row_detect<3>, 1, 256, rd_smem_bytes((int)(k + bcn), RD_PIPE), side2, f, T.ptr,
+                                     T.ld, (int)(k + bcn), RD_PIPE, pinfo[pb], pre_mp);
+                            ++g_launches;
+                            FFB_CHECK_LAUNCH();
+                        }
+                        FFB_CUDA(cudaEventRecord(ev_det, side2));
+                        if (!pre_mp.dst) {  // read-back without a mailbox: plain copy after the event
+                            FFB_CUDA(cudaStreamWaitEvent(st, ev_det, 0)); pdl_fence(st);
+                        }
+                        pre = true;
+                        pre_k = k;
+                        pre_bc = bcn;
+                    }
+                }
+                DMat RIk;
+                if (use_t1) {
+                    // T1 = Y_I - Y_I[:, pc_old] Uhat_old was computed on side2 beside the previous
+                    // chunk's CRP (other RI buffer); with that chunk's rows Unew (pivot columns J):
+                    //   R_I = Y_I - Y_I[:, pc_new] Uhat_new = T1 - T1[:, J] Unew
+                    // so the Uhat_old update stays off this chain
+                    rb ^= 1;
+                    RI = RIb[rb];
+                    RIk = RI.sub(0, 0, k, n);
+                    FFB_CUDA(cudaStreamWaitEvent(st, ev_t1, 0));
+                    FFB_CUDA(cudaStreamWaitEvent(st, ev_un, 0)); pdl_fence(st);
+                    DMat Ck = Cg.sub(0, 0, k, prev_k);
+                    gather2d(st, Ck, RIk, nullptr, lists[1], 0);
+                    gemm(f, st, GEMM_SUB, RIk, Ck, false, Uhat.sub(r - prev_k, 0, prev_k, n), false, k, n, prev_k);
+                } else {
+                    join_side();  // the previous chunk's Uhat update, before RI / Kinv / Upd are reused
+                    // exact residual of the k detected rows: R_I = Y_I - Y_I[:, pc] Uhat
+                    RIk = RI.sub(0, 0, k, n);
+                    const DMat Yb = Y.sub(base, 0, m - base, n);
+                    gather_rows(st, RIk, Yb, dI);
                     DMat Gk = Gi.sub(0, 0, k, r);
-                    gather2d(st, Gk, Y, dI, d_uhat_col, c0);
-                    gemm(f, st, GEMM_SUB, RIk, Gk, false, Uhat.sub(0, 0, r, n), false, k, n, r);
+                    if (r > 0) {
+                        gather2d(st, Gk, Y, dI, d_uhat_col, base);
+                        gemm(f, st, GEMM_SUB, RIk, Gk, false, Uhat.sub(0, 0, r, n), false, k, n, r);
+                    }
                 }
                 mark();
                 {
@@ -1416,6 +1564,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     // level 0: local CRPs of 256-column blocks (parallel)
                     launch_k(k_crp_list, nblk0, 256, crp_smem, st, f, RI.ptr, RI.ld, k, n, lists[0], counts[0]);
                     ++g_launches;
+                }
+                if (compact) {
+                    FFB_CUDA(cudaStreamWaitEvent(st, ev_si, 0)); pdl_fence(st);
                 }
                 {
                     ProfScope ps(K_PQ_ROWELIM, st, 0.0, 0.0);
@@ -1426,11 +1577,14 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     if (rc_lim >= 0) rc_cap = std::min(rc_cap, rc_lim);  // A/B hook: direct vs scan path
                     DMat Kik = Kinv.sub(0, 0, k, k);
                     launch_k(k_crp_finish, 1, 256, cfmem, st, f, RI.ptr, RI.ld, k, lists[0], counts[0], nblk0,
-                                                        (int32_t*)re_scratch, rc_cap, dI, c0, Sc.ptr, Sc.ld, SK,
+                                                        (int32_t*)re_scratch, rc_cap, dI, base, Sfin.ptr, Sfin.ld, SK,
                                                         Kik.ptr, lists[1], UO.ptr, UO.ld, d_uhat_col,
-                                                        d_prow, d_pcol, r, dflag, si_off);
+                                                        d_prow, d_pcol, r, dflag, si_off, compact ? 1 : 0);
                     ++g_launches;
                     FFB_CHECK_LAUNCH();
+                }
+                if (pipe) {  // side2 read UO[0:r] and d_uhat_col[0:r]: before absorb changes UO
+                    FFB_CUDA(cudaStreamWaitEvent(st, ev_sk, 0)); pdl_fence(st);
                 }
                 static const char* dump = getenv("FFB_PLDUQ_DUMP");  // diagnostics: one top-level R_I
                 static int dumped = 0;
@@ -1447,7 +1601,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     }
                 }
                 static FILE* jtr = getenv("FFB_PLDUQ_JTRACE") ? fopen(getenv("FFB_PLDUQ_JTRACE"), "a") : nullptr;
-                if (jtr) {  // diagnostics: k, n, candidate count, pivot column positions
+                if (jtr && !pre) {  // diagnostics: k, n, candidate count, pivot column positions
                     const int32_t* hc = (const int32_t*)io.readback(counts[0], (size_t)nblk0 * 4);
                     int64_t C = 0;
                     for (int b = 0; b < nblk0; ++b) C += hc[b];
@@ -1455,8 +1609,40 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     fprintf(jtr, "%d %lld %lld %lld %d %d %d\n", k, (long long)n, (long long)C, (long long)r,
                             hj[0], hj[k / 2], hj[k - 1]);
                 }
+                bool t1_launch = false;
+                // chunk c+1's detection (side2) ends before this finish: after the absorb's
+                // main-stream part is queued, take its rows and start T1 = Y_I' - Y_I'[:, pc]
+                // Uhat (current basis) on side2, before the Uhat update of this chunk
+                auto launch_t1 = [&]() -> bool {
+                    if (!pipe) return false;
+                    pre_kt = *(const int32_t*)(pre_mp.dst ? io.wait(pre_mp) : io.readback(pinfo[pb], 4));
+                    pre_done = true;
+                    const int kn = pre_kt - k;
+                    if (!(pre_kt >= k && pre_kt <= PIPE_TRUST && kn > 0)) return false;
+                    SlotGuard slot(3);
+                    DMat RIn = RIb[rb ^ 1].sub(0, 0, kn, n);
+                    const int32_t* dIn = pinfo[pb] + 1 + k;
+                    const int64_t basen = c0n - k;
+                    // the previous chunk's Unew GEMM reads that RI buffer; Uhat must hold the
+                    // previous chunk's update (even when main joined it already)
+                    FFB_CUDA(cudaStreamWaitEvent(side2, ev_un, 0));
+                    FFB_CUDA(cudaStreamWaitEvent(side2, ev_side, 0));
+                    pdl_fence(side2);
+                    gather_rows(side2, RIn, Y.sub(basen, 0, m - basen, n), dIn);
+                    if (r > 0) {
+                        DMat G3 = Gi3.sub(0, 0, kn, r);
+                        gather2d(side2, G3, Y, dIn, d_uhat_col, basen);
+                        gemm(f, side2, GEMM_SUB, RIn, G3, false, Uhat.sub(0, 0, r, n), false, kn, n, r);
+                    }
+                    FFB_CUDA(cudaEventRecord(ev_t1, side2));
+                    t1_launch = true;
+                    return true;
+                };
+                join_side();  // Up below reads Uhat: the previous chunk's update first
                 mark();
-                absorb(r, k, dI, lists[1], c0, true, dsig, Sc, true);
+                absorb(r, k, dI, lists[1], base, true, dsig, Sc, true, launch_t1);
+                t1 = t1_launch;
+                prev_k = k;
                 r += k;
             } else {
                 // exact: residual of the whole chunk, then the row-sequential kernel
@@ -1676,7 +1862,7 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
                 const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap, &si_off);
                 launch_k(k_crp_finish, 1, 256, cfmem, st, f, d_in, n, k, lists0, counts0, nblk0, (int32_t*)re_scratch,
                                                     rc_cap, dI, 0, nullptr, 0, 0, Kinv, lists1, nullptr, 0, ucol,
-                                                    prow, pcol, 0, flag, si_off);
+                                                    prow, pcol, 0, flag, si_off, 0);
             }
             FFB_CUDA(cudaEventRecord(e[2], st));
             FFB_CUDA(cudaEventRecord(e[3], st));

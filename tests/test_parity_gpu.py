@@ -405,3 +405,29 @@ def test_fused_small_nodes(gpu, oracle, p):
             check(gpu, oracle, p, a, "cascade", 64)
     for n in (33, 50, 64):
         check(gpu, oracle, p, rand_rook_rpm(rng, p, n, n // 2), "cascade", 32)
+
+
+@pytest.mark.parametrize("p", [2, 131, 8388593])
+def test_plduq_pipelined_detection(gpu, oracle, p):
+    """Dense 128-row chunks that each add ~20 new directions: chunk c+1's sketch and row
+    detection run beside chunk c's CRP on a second stream, on the stack [S_I(c); S(c+1)]
+    (plduq_parallel, PIPE_KMAX).  A block with 40 new directions exceeds PIPE_KMAX (serial
+    detection again), and a zero block gives k = 0.  Bit-exact against the oracle."""
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(p + 5)
+    nb, n = 22, 500
+    basis = rng.integers(0, p, (n, n)).astype(object)
+    blocks, d = [], 0
+    for j in range(nb):
+        d = min(n, d + (40 if j == 7 else 0 if j == 12 else 20))
+        coef = rng.integers(0, p, (128, d)).astype(object)
+        blk = (coef.dot(basis[:d]) % p) if j != 12 else np.zeros((128, n), dtype=object)
+        blocks.append(blk)
+    y = np.vstack(blocks).astype(np.uint64)
+    g = ffb.plduq(y, p, ctx=gpu)
+    o = oracle.plduq(p, y)
+    assert g.rank == o["rank"]
+    assert np.array_equal(g.row_perm.image_array(), o["row_image"])
+    assert np.array_equal(g.col_perm.image_array(), o["col_image"])
+    assert np.array_equal(g.lower, o["lower"]) and np.array_equal(g.upper, o["upper"])
+    assert np.array_equal(g.diag, o["diag"])
