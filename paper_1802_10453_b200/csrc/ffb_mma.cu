@@ -166,7 +166,7 @@ struct MmaScratch {
     uint32_t* ptr = nullptr;
     size_t cap = 0;
 };
-thread_local MmaScratch g_mscratch_slots[4];
+thread_local MmaScratch g_mscratch_slots[5];
 uint32_t* mma_scratch(size_t words) {
     MmaScratch& g_mscratch = g_mscratch_slots[g_slot];
     if (g_mscratch.cap < words) {

@@ -177,6 +177,9 @@ constexpr int PIPE_KMAX = 32, PIPE_TRUST = 64, RD_PIPE = 96;
 __host__ __device__ inline size_t rd_smem_bytes(int b, int s) {
     return ((size_t)b * s + (size_t)std::min(b, s) * s + (size_t)RD_BATCH * s) * 4;
 }
+__host__ __device__ inline size_t rd_smem_bytes_pre(int b, int s) {  // with a pre-basis: s basis rows
+    return ((size_t)b * s + (size_t)s * s + (size_t)RD_BATCH * s) * 4;
+}
 
 // Blocked insertion of the flagged vectors of a reduced batch into a fully
 // reduced basis.  V holds nr <= 32 vectors (stride ldv, length len), each
@@ -288,14 +291,19 @@ __device__ int batch_insert(const Fp& f, const SmemInv& inv, uint32_t* V, int ld
 // reduces to zero lies in the span of earlier rows and is dependent for good,
 // so only the flagged rows go through the sequential insertion.
 // out[0] = k, out[1..k] = independent rows (ascending).
+// Optional pre-basis (pipelined detection): kpre = *kpre_ptr fully reduced rows Epre
+// (stride s) with pivots rho_pre are loaded first; rows are then detected modulo their
+// span (k counts the new rows only).  Eout / rho_out (optional): the final basis.
 template <int NQ>  // ceil(s / 32)
 __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int64_t lds, int b,
-                                                    int s, int32_t* out, MboxPost mp) {
+                                                    int s, int32_t* out, MboxPost mp, const uint32_t* Epre,
+                                                    const int32_t* rho_pre, const int32_t* kpre_ptr, uint32_t* Eout,
+                                                    int32_t* rho_out) {
     FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint32_t sm[];
     uint32_t* Ss = sm;                          // b x s (b <= RD_MAX_ROWS)
     uint32_t* E = Ss + (size_t)b * s;           // basis rows (fully reduced), <= min(b, s)
-    uint32_t* V = E + (size_t)std::min(b, s) * s;  // RD_BATCH reduced rows of the current batch
+    uint32_t* V = E + (size_t)(kpre_ptr ? s : std::min(b, s)) * s;  // RD_BATCH reduced rows of the current batch
     __shared__ int rho[RD_MAX_B];
     __shared__ uint32_t cfb[RD_BATCH][RD_MAX_B];  // batch coefficients S_i[rho_t]
     __shared__ unsigned fmask[2];
@@ -308,8 +316,14 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
     else
         load_tile<16>(Ss, s, S, lds, b, s);
     const SmemInv inv = stage_inverses(f, sinv);
-    __syncthreads();
     int k = 0, bi = 0;
+    if (kpre_ptr) {
+        k = min(__ldcg(kpre_ptr), min(s, RD_MAX_B));
+        for (int e = tid; e < k * s; e += 256) E[e] = __ldcg(Epre + e);
+        for (int t = tid; t < k; t += 256) rho[t] = __ldcg(rho_pre + t);
+    }
+    const int kp = k;
+    __syncthreads();
     for (int i0 = 0; i0 < b; i0 += RD_BATCH, ++bi) {
         const int nr = min(RD_BATCH, b - i0);
         for (int r = wp; r < nr; r += 8)
@@ -322,12 +336,17 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
         const unsigned pending = fmask[bi & 1];  // rows outside the span of the batch-start basis
         if (!pending) continue;
         const int cnt = batch_insert<NQ>(f, inv, V, s, pending, s, E, k, min(s, RD_MAX_B), rho, bs);
-        if (tid < cnt) out[1 + k + tid] = i0 + bs.ins[tid];  // inserted in row order
+        if (tid < cnt) out[1 + k - kp + tid] = i0 + bs.ins[tid];  // inserted in row order
         k += cnt;
     }
+    if (Eout) {
+        for (int e = tid; e < k * s; e += 256) Eout[e] = E[e];
+        for (int t = tid; t < k; t += 256) rho_out[t] = rho[t];
+    }
     if (tid == 0) {
-        out[0] = k;
-        if (mp.dst) mbox_publish(mp, &k, 1);  // the host's read-back of k, without a k_post
+        const int kn = k - kp;
+        out[0] = kn;
+        if (mp.dst) mbox_publish(mp, &kn, 1);  // the host's read-back of k, without a k_post
     }
 }
 
@@ -1276,19 +1295,24 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     }
     // side2: pipelined sketch + row detection of the next chunk (highest priority: its
     // 1-CTA detection is latency-bound and must not queue behind the Uhat updates)
-    static thread_local cudaStream_t side2 = nullptr;
+    static thread_local cudaStream_t side2 = nullptr, side3 = nullptr;
     static thread_local cudaEvent_t ev_gk = nullptr, ev_si = nullptr, ev_sk = nullptr, ev_det = nullptr,
                                     ev_t1 = nullptr, ev_un = nullptr;
     if (!side2) {
         int least = 0, greatest = 0;
         FFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
         FFB_CUDA(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, greatest));
+        FFB_CUDA(cudaStreamCreateWithPriority(&side3, cudaStreamNonBlocking, greatest));
         for (cudaEvent_t* e : {&ev_gk, &ev_si, &ev_sk, &ev_det, &ev_t1, &ev_un})
             FFB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
     static const bool pipe_on = overlap_ok && !getenv("FFB_PLDUQ_NO_PIPE");  // A/B hook
     DMat T2[2] = {ws.mat(PIPE_KMAX + B, SK), ws.mat(PIPE_KMAX + B, SK)};
     int32_t* pinfo[2] = {ws.vec<int32_t>(2 * (PIPE_KMAX + B) + 16), ws.vec<int32_t>(2 * (PIPE_KMAX + B) + 16)};
+    // pre-basis of the pipelined detection: reduced rows of S_I(c) (k_row_detect on S_I alone)
+    uint32_t* Epre = ws.vec<uint32_t>((int64_t)PIPE_KMAX * RD_PIPE);
+    int32_t* rho_pre = ws.vec<int32_t>(PIPE_KMAX);
+    int32_t* pre_out = ws.vec<int32_t>(2 * PIPE_KMAX + 16);
     const size_t mark1b = ws.mark();
     bool side_pending = false;
     auto join_side = [&]() {
@@ -1413,10 +1437,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     use_t1 = t1;
                     t1 = false;
                     FFB_CUDA(cudaStreamWaitEvent(st, ev_det, 0)); pdl_fence(st);
-                    if (kt >= pre_k && kt <= PIPE_TRUST) {
-                        k = kt - pre_k;
-                        dI = pinfo[pb] + 1 + pre_k;
-                        base = c0 - pre_k;
+                    if (pre_k + kt <= PIPE_TRUST) {
+                        k = kt;
+                        dI = pinfo[pb] + 1;
                         det_pipe = true;
                     }  // else: near the sketch capacity -- detect again below, serially
                 }
@@ -1451,10 +1474,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                             ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
                             if (wide)
                                 launch_k(k_row_detect<5>, 1, 256, rd_smem_bytes((int)bc, SK), st, f, Sc.ptr, Sc.ld, (int)bc,
-                                         SK, dinfo, mp);
+                                         SK, dinfo, mp, nullptr, nullptr, nullptr, nullptr, nullptr);
                             else
                                 launch_k(k_row_detect<2>, 1, 256, rd_smem_bytes((int)bc, RD_NARROW), st, f, Sc.ptr, Sc.ld,
-                                         (int)bc, RD_NARROW, dinfo, mp);
+                                         (int)bc, RD_NARROW, dinfo, mp, nullptr, nullptr, nullptr, nullptr, nullptr);
                             ++g_launches;
                             FFB_CHECK_LAUNCH();
                         }
@@ -1505,21 +1528,30 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     FFB_CUDA(cudaEventRecord(ev_si, side2));
                     if (pipe) {
                         const int64_t bcn = std::min<int64_t>(B, m - c0n);
-                        DMat Sn = T.sub(k, 0, bcn, SK);
-                        launch_k(k_copy_rows, dim3(1, (unsigned)bcn), 160, 0, side2, Sn.ptr, Sn.ld,
+                        // the reduced basis of S_I (side2) beside chunk c+1's sketch (side3),
+                        // then the detection of c+1 modulo that basis (side2)
+                        launch_k(k_row_detect<3>, 1, 256, rd_smem_bytes(k, RD_PIPE), side2, f, Sfin.ptr, Sfin.ld, k,
+                                 RD_PIPE, pre_out, MboxPost(), nullptr, nullptr, nullptr, Epre, rho_pre);
+                        ++g_launches;
+                        FFB_CUDA(cudaStreamWaitEvent(side3, ev_gk, 0)); pdl_fence(side3);
+                        SlotGuard slot3(4);
+                        DMat Sn = T.sub(PIPE_KMAX, 0, bcn, SK);
+                        launch_k(k_copy_rows, dim3(1, (unsigned)bcn), 160, 0, side3, Sn.ptr, Sn.ld,
                                  YO.ptr + c0n * YO.ld, YO.ld, (int64_t)SK);
                         ++g_launches;
                         if (r > 0) {
                             DMat Gc = Gs.sub(0, 0, bcn, r);
-                            gather2d(side2, Gc, Y.sub(c0n, 0, bcn, n), nullptr, d_uhat_col, 0);
-                            gemm(f, side2, GEMM_SUB, Sn, Gc, false, UO.sub(0, 0, r, SK), false, bcn, SK, r);
+                            gather2d(side3, Gc, Y.sub(c0n, 0, bcn, n), nullptr, d_uhat_col, 0);
+                            gemm(f, side3, GEMM_SUB, Sn, Gc, false, UO.sub(0, 0, r, SK), false, bcn, SK, r);
                         }
-                        FFB_CUDA(cudaEventRecord(ev_sk, side2));
+                        FFB_CUDA(cudaEventRecord(ev_sk, side3));
+                        FFB_CUDA(cudaStreamWaitEvent(side2, ev_sk, 0)); pdl_fence(side2);
                         pre_mp = io.post ? io.post() : MboxPost();
                         {
                             ProfScope ps(K_PLDUQ, side2, 0.0, 0.0);
-                            launch_k(k_row_detect<3>, 1, 256, rd_smem_bytes((int)(k + bcn), RD_PIPE), side2, f, T.ptr,
-                                     T.ld, (int)(k + bcn), RD_PIPE, pinfo[pb], pre_mp);
+                            launch_k(k_row_detect<3>, 1, 256, rd_smem_bytes_pre((int)bcn, RD_PIPE), side2, f, Sn.ptr,
+                                     Sn.ld, (int)bcn, RD_PIPE, pinfo[pb], pre_mp, Epre, rho_pre, pre_out, nullptr,
+                                     nullptr);
                             ++g_launches;
                             FFB_CHECK_LAUNCH();
                         }
@@ -1617,12 +1649,12 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     if (!pipe) return false;
                     pre_kt = *(const int32_t*)(pre_mp.dst ? io.wait(pre_mp) : io.readback(pinfo[pb], 4));
                     pre_done = true;
-                    const int kn = pre_kt - k;
-                    if (!(pre_kt >= k && pre_kt <= PIPE_TRUST && kn > 0)) return false;
+                    const int kn = pre_kt;
+                    if (!(k + kn <= PIPE_TRUST && kn > 0)) return false;
                     SlotGuard slot(3);
                     DMat RIn = RIb[rb ^ 1].sub(0, 0, kn, n);
-                    const int32_t* dIn = pinfo[pb] + 1 + k;
-                    const int64_t basen = c0n - k;
+                    const int32_t* dIn = pinfo[pb] + 1;
+                    const int64_t basen = c0n;
                     // the previous chunk's Unew GEMM reads that RI buffer; Uhat must hold the
                     // previous chunk's update (even when main joined it already)
                     FFB_CUDA(cudaStreamWaitEvent(side2, ev_un, 0));
@@ -1816,9 +1848,11 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         int32_t* info;
         FFB_CUDA(cudaMalloc(&info, (2 * RD_MAX_B + 16) * 4));
-        launch_k(k_row_detect<5>, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info, MboxPost());
+        launch_k(k_row_detect<5>, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info, MboxPost(), nullptr, nullptr, nullptr, nullptr,
+                 nullptr);
         FFB_CUDA(cudaEventRecord(e[0], st));
-        for (int i = 0; i < reps; ++i) launch_k(k_row_detect<5>, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info, MboxPost());
+        for (int i = 0; i < reps; ++i) launch_k(k_row_detect<5>, 1, 256, rd_smem, st, f, d_in, cols, rows, cols, info, MboxPost(), nullptr, nullptr, nullptr, nullptr,
+                 nullptr);
         FFB_CUDA(cudaEventRecord(e[1], st));
         FFB_CUDA(cudaEventSynchronize(e[1]));
         FFB_CUDA(cudaEventElapsedTime(&t, e[0], e[1]));

@@ -804,7 +804,7 @@ struct Scratch {
     int8_t* ptr = nullptr;
     size_t cap = 0;
 };
-thread_local Scratch g_scratch_slots[4];
+thread_local Scratch g_scratch_slots[5];
 
 int8_t* scratch(size_t bytes) {
     Scratch& g_scratch = g_scratch_slots[g_slot];
