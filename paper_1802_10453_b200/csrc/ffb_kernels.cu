@@ -257,11 +257,62 @@ __device__ __forceinline__ void copy_row(uint32_t* d, const uint32_t* s, int64_t
     for (int64_t j = start; j < cols; j += step) d[j] = s[j];
 }
 
+// Row kernels loop over rows (grid.y strides them): a few thousand CTAs move the whole
+// block instead of one tiny CTA per (row, column slice) -- at 16384 rows the per-CTA
+// launch cost, not HBM, bounded the one-row-per-CTA form.
+// dst[i][j] = src[idx[i]][c0 + j]: R rows per iteration, so each thread keeps R 16-byte
+// loads in flight behind one round of index loads
+template <int R>
+__device__ __forceinline__ void copy_rows_r(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
+                                            const int32_t* idx, int64_t c0, int64_t rows, int64_t cols) {
+    const int64_t start = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t step = (int64_t)gridDim.x * blockDim.x, gy = gridDim.y;
+    const bool vec = ((((uintptr_t)dst | (uintptr_t)(src + c0)) & 15) == 0) && (ldd & 3) == 0 && (lds & 3) == 0;
+    for (int64_t i0 = blockIdx.y; i0 < rows; i0 += R * gy) {
+        const uint32_t* s[R];
+        uint32_t* d[R];
+        bool ok[R];
+#pragma unroll
+        for (int u = 0; u < R; ++u) {
+            const int64_t i = i0 + u * gy;
+            ok[u] = i < rows;
+            s[u] = src + (ok[u] ? (int64_t)__ldcg(idx + i) : 0) * lds + c0;
+            d[u] = dst + (ok[u] ? i : 0) * ldd;
+        }
+        if (vec) {
+            const int64_t c4 = cols >> 2;
+            for (int64_t j = start; j < c4; j += step) {
+                uint4 v[R];
+#pragma unroll
+                for (int u = 0; u < R; ++u)
+                    if (ok[u]) v[u] = __ldcg(reinterpret_cast<const uint4*>(s[u]) + j);
+#pragma unroll
+                for (int u = 0; u < R; ++u)
+                    if (ok[u]) reinterpret_cast<uint4*>(d[u])[j] = v[u];
+            }
+            for (int64_t t = 4 * c4 + start; t < cols; t += step)
+#pragma unroll
+                for (int u = 0; u < R; ++u)
+                    if (ok[u]) d[u][t] = __ldcg(s[u] + t);
+        } else {
+            for (int64_t j = start; j < cols; j += step)
+#pragma unroll
+                for (int u = 0; u < R; ++u)
+                    if (ok[u]) d[u][j] = __ldcg(s[u] + j);
+        }
+    }
+}
+
 __global__ void k_gather_rows(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
                               const int32_t* idx, int64_t rows, int64_t cols) {
     FFB_PDL_ENTRY();
     const int64_t i = blockIdx.y;
     copy_row(dst + i * ldd, src + (int64_t)idx[i] * lds, cols);
+}
+__global__ void k_gather_rows_loop(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
+                                   const int32_t* idx, int64_t rows, int64_t cols) {
+    FFB_PDL_ENTRY();
+    copy_rows_r<4>(dst, ldd, src, lds, idx, 0, rows, cols);
 }
 
 // Two independent row gathers in one launch (blockIdx.z): dst[i][j] = src[idx[i]][c0 + j].
@@ -279,6 +330,33 @@ __global__ void k_gather_rows2(RowGather g0, RowGather g1) {
     const int64_t i = blockIdx.y;
     if (i >= g.rows) return;
     copy_row(g.dst + i * g.ldd, g.src + (int64_t)g.idx[i] * g.lds + g.c0, g.cols);
+}
+__global__ void k_gather_rows2_loop(RowGather g0, RowGather g1) {
+    FFB_PDL_ENTRY();
+    const RowGather& g = blockIdx.z == 0 ? g0 : g1;
+    copy_rows_r<4>(g.dst, g.ldd, g.src, g.lds, g.idx, g.c0, g.rows, g.cols);
+}
+
+// dst[a][b] = src[ridx[a]][idx[b]] with the source row staged in shared memory
+// (n words): coalesced 16-byte row reads, coalesced writes, the column permutation
+// served from smem.  One CTA per row at a time, rows strided by gridDim.x.
+__global__ void __launch_bounds__(512) k_gather_sym_smem(uint32_t* dst, int64_t ldd, const uint32_t* src,
+                                                        int64_t lds, const int32_t* ridx, const int32_t* idx,
+                                                        int64_t rows, int64_t n) {
+    FFB_PDL_ENTRY();
+    extern __shared__ __align__(16) uint32_t gs_row[];
+    const int64_t n4 = n >> 2;
+    for (int64_t a = blockIdx.x; a < rows; a += gridDim.x) {
+        const uint4* s4 = reinterpret_cast<const uint4*>(src + (int64_t)__ldcg(ridx + a) * lds);
+        for (int64_t j = threadIdx.x; j < n4; j += blockDim.x)
+            reinterpret_cast<uint4*>(gs_row)[j] = __ldcg(s4 + j);
+        for (int64_t j = 4 * n4 + threadIdx.x; j < n; j += blockDim.x)
+            gs_row[j] = __ldcg(src + (int64_t)__ldcg(ridx + a) * lds + j);
+        __syncthreads();
+        uint32_t* d = dst + a * ldd;
+        for (int64_t b = threadIdx.x; b < n; b += blockDim.x) d[b] = gs_row[__ldcg(idx + b)];
+        __syncthreads();
+    }
 }
 
 __global__ void k_gather_sym(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
@@ -347,30 +425,9 @@ __global__ void k_scatter_lg_pair(uint32_t* Lg, int64_t ldl, const int32_t* ids,
 }
 
 __global__ void k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int64_t ldl,
-                            const int32_t* ids, int64_t col0, int64_t cols) {
+                            const int32_t* ids, int64_t col0, int64_t cols, int64_t rows) {
     FFB_PDL_ENTRY();
-    const int64_t i = blockIdx.y;
-    const uint32_t* s = Lg + (int64_t)ids[i] * ldl + col0;
-    uint32_t* d = dst + i * ldd;
-    const int64_t step = (int64_t)gridDim.x * blockDim.x;
-    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if ((((uintptr_t)s | (uintptr_t)d) & 15) == 0) {  // 16-byte vectors, 2 in flight
-        const int64_t c4 = cols >> 2;
-        const uint4* s4 = reinterpret_cast<const uint4*>(s);
-        uint4* d4 = reinterpret_cast<uint4*>(d);
-        for (; j + 3 * step < c4; j += 4 * step) {
-            const uint4 a = __ldcg(s4 + j), b = __ldcg(s4 + j + step), c = __ldcg(s4 + j + 2 * step),
-                        e = __ldcg(s4 + j + 3 * step);
-            __stcs(d4 + j, a);
-            __stcs(d4 + j + step, b);
-            __stcs(d4 + j + 2 * step, c);
-            __stcs(d4 + j + 3 * step, e);
-        }
-        for (; j < c4; j += step) __stcs(d4 + j, __ldcg(s4 + j));
-        for (int64_t t = 4 * c4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cols; t += step) d[t] = s[t];
-        return;
-    }
-    for (; j < cols; j += step) d[j] = s[j];
+    copy_rows_r<4>(dst, ldd, Lg, ldl, ids, col0, rows, cols);
 }
 
 // G[j][k] = (D^-1 X)[k][j], X is r x ncols.  Tile: 32 k x 32 j, with one
@@ -597,6 +654,14 @@ __global__ void k_convert_out(T* dst, const uint32_t* src, int64_t lds, int64_t 
         dst[i * cols + j] = (T)src[i * lds + j];
 }
 
+// for the row-looping kernels: about 16 CTAs per SM in total
+inline dim3 rowgrid_loop(int64_t rows, int64_t cols, int threads = 256, int per_thread = 1) {
+    int64_t gx = cdiv(cdiv(cols, per_thread), threads);
+    if (gx > 64) gx = 64;
+    if (gx < 1) gx = 1;
+    const int64_t gy = std::min<int64_t>(std::max<int64_t>(rows, 1), std::max<int64_t>(1, 16 * 148 / gx));
+    return dim3((unsigned)gx, (unsigned)gy);
+}
 inline dim3 rowgrid(int64_t rows, int64_t cols, int threads = 256, int per_thread = 1) {
     int64_t gx = cdiv(cdiv(cols, per_thread), threads);
     if (gx > 64) gx = 64;
@@ -614,7 +679,10 @@ void gather_rows(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
     if (dst.rows <= 0 || dst.cols <= 0) return;
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
-        launch_k(k_gather_rows, rowgrid(nr, dst.cols, 256, 4), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
+        // big gathers: row-looping CTAs (fewer, fatter); small ones: a CTA per row slice
+        const bool big = nr * dst.cols >= ((int64_t)1 << 22);
+        launch_k(big ? k_gather_rows_loop : k_gather_rows, big ? rowgrid_loop(nr, dst.cols, 256, 4)
+                                                                : rowgrid(nr, dst.cols, 256, 4), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
                                                              src.ld, idx + r0, nr, dst.cols);
         count_launch();
     }
@@ -624,6 +692,21 @@ void gather_rows(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
 void gather_sym(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (dst.rows <= 0) return;
+    const size_t row_bytes = (size_t)dst.cols * 4;
+    if (dst.cols >= 1024 && row_bytes <= 200 * 1024 && (src.ld & 3) == 0 && (((uintptr_t)src.ptr) & 15) == 0) {
+        static bool attr = false;
+        if (!attr) {
+            FFB_CUDA(cudaFuncSetAttribute(k_gather_sym_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+            attr = true;
+        }
+        const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (int64_t)(227 * 1024) / (int64_t)(row_bytes + 1024)));
+        const int64_t grid = std::min<int64_t>(dst.rows, 148 * per_sm);
+        launch_k(k_gather_sym_smem, (unsigned)grid, 512, row_bytes, st, dst.ptr, dst.ld, src.ptr, src.ld, idx, idx,
+                 dst.rows, dst.cols);
+        count_launch();
+        FFB_CHECK_LAUNCH();
+        return;
+    }
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
         launch_k(k_gather_sym, rowgrid(nr, dst.cols), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, src.ptr,
@@ -679,9 +762,10 @@ void gather_rows2(cudaStream_t st, DMat d0, DMat s0, const int32_t* i0, int64_t 
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     RowGather g0{d0.ptr, d0.ld, s0.ptr, s0.ld, i0, c0, d0.cols > 0 ? d0.rows : 0, d0.cols};
     RowGather g1{d1.ptr, d1.ld, s1.ptr, s1.ld, i1, c1, d1.cols > 0 ? d1.rows : 0, d1.cols};
-    dim3 g = rowgrid(rows, cols, 256, 4);
+    const bool big = rows * cols >= ((int64_t)1 << 22);
+    dim3 g = big ? rowgrid_loop(rows, cols, 256, 4) : rowgrid(rows, cols, 256, 4);
     g.z = 2;
-    launch_k(k_gather_rows2, g, 256, 0, st, g0, g1);
+    launch_k(big ? k_gather_rows2_loop : k_gather_rows2, g, 256, 0, st, g0, g1);
     count_launch();
     FFB_CHECK_LAUNCH();
 }
@@ -692,8 +776,8 @@ void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t c
     for (int64_t r0 = 0; r0 < dst.rows; r0 += FFB_ROWCHUNK) {
         const int64_t nr = std::min<int64_t>(FFB_ROWCHUNK, dst.rows - r0);
         // 16 words (four 16-byte vectors) per thread: a few CTAs per row, loads in flight
-        launch_k(k_gather_lg, rowgrid(nr, dst.cols, 256, 16), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld, Lg.ptr,
-                                                           Lg.ld, ids + r0, col0, dst.cols);
+        launch_k(k_gather_lg, rowgrid_loop(nr, dst.cols, 256, 4), 256, 0, st, dst.ptr + r0 * dst.ld, dst.ld,
+                 Lg.ptr, Lg.ld, ids + r0, col0, dst.cols, nr);
         count_launch();
     }
     FFB_CHECK_LAUNCH();
