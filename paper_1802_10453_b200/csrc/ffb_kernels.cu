@@ -309,10 +309,10 @@ __global__ void k_gather_rows(uint32_t* dst, int64_t ldd, const uint32_t* src, i
     const int64_t i = blockIdx.y;
     copy_row(dst + i * ldd, src + (int64_t)idx[i] * lds, cols);
 }
-__global__ void k_gather_rows_loop(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
+__global__ void __launch_bounds__(256, 4) k_gather_rows_loop(uint32_t* dst, int64_t ldd, const uint32_t* src, int64_t lds,
                                    const int32_t* idx, int64_t rows, int64_t cols) {
     FFB_PDL_ENTRY();
-    copy_rows_r<4>(dst, ldd, src, lds, idx, 0, rows, cols);
+    copy_rows_r<2>(dst, ldd, src, lds, idx, 0, rows, cols);
 }
 
 // Two independent row gathers in one launch (blockIdx.z): dst[i][j] = src[idx[i]][c0 + j].
@@ -331,10 +331,10 @@ __global__ void k_gather_rows2(RowGather g0, RowGather g1) {
     if (i >= g.rows) return;
     copy_row(g.dst + i * g.ldd, g.src + (int64_t)g.idx[i] * g.lds + g.c0, g.cols);
 }
-__global__ void k_gather_rows2_loop(RowGather g0, RowGather g1) {
+__global__ void __launch_bounds__(256, 4) k_gather_rows2_loop(RowGather g0, RowGather g1) {
     FFB_PDL_ENTRY();
-    const RowGather& g = blockIdx.z == 0 ? g0 : g1;
-    copy_rows_r<4>(g.dst, g.ldd, g.src, g.lds, g.idx, g.c0, g.rows, g.cols);
+    if (blockIdx.z == 0) copy_rows_r<2>(g0.dst, g0.ldd, g0.src, g0.lds, g0.idx, g0.c0, g0.rows, g0.cols);
+    else copy_rows_r<2>(g1.dst, g1.ldd, g1.src, g1.lds, g1.idx, g1.c0, g1.rows, g1.cols);
 }
 
 // dst[a][b] = src[ridx[a]][idx[b]] with the source row staged in shared memory
@@ -424,10 +424,10 @@ __global__ void k_scatter_lg_pair(uint32_t* Lg, int64_t ldl, const int32_t* ids,
     }
 }
 
-__global__ void k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int64_t ldl,
+__global__ void __launch_bounds__(256, 4) k_gather_lg(uint32_t* dst, int64_t ldd, const uint32_t* Lg, int64_t ldl,
                             const int32_t* ids, int64_t col0, int64_t cols, int64_t rows) {
     FFB_PDL_ENTRY();
-    copy_rows_r<4>(dst, ldd, Lg, ldl, ids, col0, rows, cols);
+    copy_rows_r<2>(dst, ldd, Lg, ldl, ids, col0, rows, cols);
 }
 
 // G[j][k] = (D^-1 X)[k][j], X is r x ncols.  Tile: 32 k x 32 j, with one
