@@ -526,15 +526,18 @@ __global__ void __launch_bounds__(256) k_any_nonzero(const uint32_t* m, int64_t 
 
 // Symmetry check: block (x, y) compares the 32-row band y against the transposed
 // column tiles 8x .. 8x+7 (lower triangle only), both tiles' loads in flight.
+// Symmetry check: CTA (x, y) walks the 32x32 tiles of row band y left of the diagonal
+// with stride gridDim.x (no CTAs for the upper triangle), the next tile's loads issued
+// before the current tile's comparisons.
 __global__ void k_any_asym(const uint32_t* a, int64_t ld, int64_t n, int32_t* flag) {
     FFB_PDL_ENTRY();
     __shared__ uint32_t tile[32][33];
     const int64_t r0 = (int64_t)blockIdx.y * 32;
     int bad = 0;
-    for (int t = 0; t < 8; ++t) {
-        const int64_t c0 = ((int64_t)blockIdx.x * 8 + t) * 32;
-        if (c0 > r0 + 31 || c0 >= n) break;  // uniform
-        uint32_t up[4], lo[4];
+    auto valid = [&](int64_t t) { return t * 32 <= r0 + 31 && t * 32 < n; };
+    uint32_t up[4], lo[4];
+    auto load = [&](int64_t t) {
+        const int64_t c0 = t * 32;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int k = threadIdx.y + 8 * u;
@@ -543,16 +546,27 @@ __global__ void k_any_asym(const uint32_t* a, int64_t ld, int64_t n, int32_t* fl
             const int64_t rr = r0 + k, cc = c0 + threadIdx.x;
             lo[u] = (rr < n && cc < n) ? __ldcg(a + rr * ld + cc) : 0u;
         }
+    };
+    int64_t t = blockIdx.x;
+    if (valid(t)) load(t);
+    while (valid(t)) {  // uniform
+        const int64_t c0 = t * 32;
         __syncthreads();  // previous tile's comparisons done
 #pragma unroll
         for (int u = 0; u < 4; ++u) tile[threadIdx.y + 8 * u][threadIdx.x] = up[u];
         __syncthreads();
+        uint32_t cur[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) cur[u] = lo[u];
+        const int64_t tn = t + gridDim.x;
+        if (valid(tn)) load(tn);
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int k = threadIdx.y + 8 * u;
             const int64_t r = r0 + k, c = c0 + threadIdx.x;
-            if (r < n && c < n) bad |= lo[u] != tile[threadIdx.x][k];
+            if (r < n && c < n) bad |= cur[u] != tile[threadIdx.x][k];
         }
+        t = tn;
     }
     if (__syncthreads_or(bad) && threadIdx.x == 0 && threadIdx.y == 0) atomicOr(flag, 1);
 }
@@ -824,7 +838,7 @@ void any_nonzero(cudaStream_t st, DMat m, int32_t* flag, int32_t value) {
 void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (a.rows <= 1) return;
-    dim3 grid((unsigned)cdiv(cdiv(a.rows, 32), 8), (unsigned)cdiv(a.rows, 32));
+    dim3 grid((unsigned)std::min<int64_t>(8, cdiv(a.rows, 32)), (unsigned)cdiv(a.rows, 32));
     launch_k(k_any_asym, grid, dim3(32, 8), 0, st, a.ptr, a.ld, a.rows, flag);
     count_launch();
     FFB_CHECK_LAUNCH();

@@ -431,3 +431,18 @@ def test_plduq_pipelined_detection(gpu, oracle, p):
     assert np.array_equal(g.col_perm.image_array(), o["col_image"])
     assert np.array_equal(g.lower, o["lower"]) and np.array_equal(g.upper, o["upper"])
     assert np.array_equal(g.diag, o["diag"])
+
+
+@pytest.mark.parametrize("pos", [(1, 0), (31, 0), (32, 31), (999, 3), (500, 470), (999, 998), (640, 0)])
+def test_asymmetry_anywhere(gpu, pos):
+    """The device symmetry check (k_any_asym: row bands walk their tiles left of the
+    diagonal with a stride) finds a single asymmetric pair wherever it lies."""
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(sum(pos))
+    a = rand_sym(rng, 131, 1000)
+    i, j = pos
+    a[i, j] = (a[j, i] + 1) % 131
+    with pytest.raises(ffb.NotSymmetric):
+        ffb.ldlt(a, 131, ctx=gpu)
+    a[i, j] = a[j, i]
+    ffb.ldlt(a, 131, ctx=gpu)
