@@ -196,6 +196,19 @@ class Checker:
                                           _ptr(a), _ptr(b)))
         return c
 
+    def generate(self, config: int, n: int, r: int, p: int, seed: int) -> np.ndarray:
+        """Benchmark input of configuration `config` (oracle/gen_oracle.c; oracle only)."""
+        out = np.zeros((n, n), np.uint64)
+        self._check(self._fn("generate")(C.c_int(config), C.c_size_t(n), C.c_size_t(r),
+                                         C.c_uint64(p), C.c_uint64(seed), _ptr(out)))
+        return out
+
+    def config5_partners(self, n: int, r: int, seed: int) -> np.ndarray:
+        out = np.zeros(max(n, 1), np.int64)
+        self._check(self._fn("config5_partners")(C.c_size_t(n), C.c_size_t(r), C.c_uint64(seed),
+                                                 _ptr(out)))
+        return out[:n]
+
     def rank_profile(self, p, a) -> np.ndarray:
         """Brute-force RPM (reference only: rpmtools.cpp:43-59)."""
         a = _u64(a)

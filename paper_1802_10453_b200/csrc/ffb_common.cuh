@@ -12,12 +12,30 @@
 #include <stdio.h>
 #include <stdlib.h>
 
+#include <atomic>
 #include <stdexcept>
 #include <string>
 
 #include "../../include/ffldl_b200.h"
 
 namespace ffb {
+
+// Per-device CUDA state.  A context may live on any device and one thread may use
+// several (ffldl.default_context(device)), so streams, events, scratch buffers and
+// cudaFuncSetAttribute guards are kept per device, never per process or thread only.
+constexpr int FFB_MAX_DEVICES = 32;
+inline int current_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d & (FFB_MAX_DEVICES - 1);
+}
+// "done once on this device" flag (e.g. the >48 KB dynamic shared memory attribute):
+// if (!g.done()) { cudaFuncSetAttribute(...); g.mark(); }  -- a repeated set is harmless.
+struct DeviceOnce {
+    std::atomic<uint32_t> mask{0};
+    bool done() const { return (mask.load(std::memory_order_acquire) >> current_device()) & 1u; }
+    void mark() { mask.fetch_or(1u << current_device(), std::memory_order_release); }
+};
 
 // ---------------------------------------------------------------------------
 // Errors: the C-ABI maps these 1:1 to FFB_* status codes.

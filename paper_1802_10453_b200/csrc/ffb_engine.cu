@@ -365,16 +365,17 @@ struct Engine {
         if (!zst) {
             int least = 0, greatest = 0;
             FFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-            static thread_local cudaStream_t s_zst = nullptr;
-            static thread_local cudaEvent_t s_fork = nullptr, s_done = nullptr;
-            if (!s_zst) {
-                FFB_CUDA(cudaStreamCreateWithPriority(&s_zst, cudaStreamNonBlocking, least));
-                FFB_CUDA(cudaEventCreateWithFlags(&s_fork, cudaEventDisableTiming));
-                FFB_CUDA(cudaEventCreateWithFlags(&s_done, cudaEventDisableTiming));
+            static thread_local cudaStream_t s_zst[FFB_MAX_DEVICES] = {};
+            static thread_local cudaEvent_t s_fork[FFB_MAX_DEVICES] = {}, s_done[FFB_MAX_DEVICES] = {};
+            const int dev = current_device();
+            if (!s_zst[dev]) {
+                FFB_CUDA(cudaStreamCreateWithPriority(&s_zst[dev], cudaStreamNonBlocking, least));
+                FFB_CUDA(cudaEventCreateWithFlags(&s_fork[dev], cudaEventDisableTiming));
+                FFB_CUDA(cudaEventCreateWithFlags(&s_done[dev], cudaEventDisableTiming));
             }
-            zst = s_zst;
-            zev_fork = s_fork;
-            zev_done = s_done;
+            zst = s_zst[dev];
+            zev_fork = s_fork[dev];
+            zev_done = s_done[dev];
         }
         FFB_CUDA(cudaEventRecord(zev_fork, st));
         FFB_CUDA(cudaStreamWaitEvent(zst, zev_fork, 0));
@@ -1079,6 +1080,8 @@ int ffb_ldlt_compact(ffb_context* c, uint64_t p, size_t n, const void* a, int a_
         // The engine reads only the upper blocks B and Z, so an asymmetric input factors
         // harmlessly as another symmetric matrix; the check runs on the copy stream
         // after the last band and the result is refused (NotSymmetric) before export.
+        // It reads the raw staging buffer `tmp`, which the engine never writes (W is
+        // updated in place by the recursion, concurrently with the check).
         const int64_t N = (int64_t)n;
         DMat W = ws_mat(c, N, N);
         char* tmp = (char*)ws_alloc(c, (size_t)N * N * aeb);
@@ -1101,7 +1104,7 @@ int ffb_ldlt_compact(ffb_context* c, uint64_t p, size_t n, const void* a, int a_
         int32_t* aflag = c->flag + 16;  // asymmetry flag (copy stream)
         FFB_CUDA(cudaMemsetAsync(aflag, 0, sizeof(int32_t), c->copy_stream));
         pdl_fence(c->copy_stream);
-        any_asymmetric(c->copy_stream, W, aflag);
+        any_asymmetric_raw(c->copy_stream, tmp, N, aeb, p, aflag);
         cudaEvent_t checked;
         FFB_CUDA(cudaEventCreateWithFlags(&checked, cudaEventDisableTiming));
         FFB_CUDA(cudaEventRecord(checked, c->copy_stream));

@@ -1067,9 +1067,10 @@ struct TrsmScratch {
     uint32_t* ptr = nullptr;
     size_t cap = 0;
 };
-thread_local TrsmScratch g_tscratch;
+thread_local TrsmScratch g_tscratch_dev[FFB_MAX_DEVICES];
 
 uint32_t* trsm_scratch(size_t words) {
+    TrsmScratch& g_tscratch = g_tscratch_dev[current_device()];
     if (g_tscratch.cap < words) {
         if (g_tscratch.ptr) {
             FFB_CUDA(cudaDeviceSynchronize());
@@ -1089,11 +1090,11 @@ void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tin
         const uint32_t* ti = Tinv + (i0 / 64) * 64 * 64;
         static const bool no_mma = getenv("FFB_TRSM_SIMT") != nullptr;  // test hook
         if (f.p <= 255 && !no_mma) {
-            static bool attr_mma = false;
-            if (!attr_mma) {
+            static DeviceOnce attr_mma;
+            if (!attr_mma.done()) {
                 FFB_CUDA(cudaFuncSetAttribute(k_trsm_panel_mma, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                               (int)PM_SMEM));
-                attr_mma = true;
+                attr_mma.mark();
             }
             launch_k(k_trsm_panel_mma, (unsigned)cdiv(B.cols, PM_COLS), 256, PM_SMEM, st, f, T.ptr, T.ld, ti, B.ptr,
                                                                                  B.ld, (int)n, B.cols);
@@ -1102,11 +1103,11 @@ void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tin
             return;
         }
         const size_t smem = (size_t)(256 * (PNL_COLS + 1) + 64 * 65) * 4;
-        static bool attr = false;
-        if (!attr) {
+        static DeviceOnce attr;
+        if (!attr.done()) {
             FFB_CUDA(cudaFuncSetAttribute(k_trsm_panel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             FFB_CUDA(cudaFuncSetAttribute(k_trsm_panel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            attr = true;
+            attr.mark();
         }
         dim3 grid((unsigned)cdiv(B.cols, PNL_COLS));
         if (f.p < (1u << 23))
@@ -1175,11 +1176,11 @@ void node128(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg,
              uint32_t* yout, int32_t* out, const MboxPost& mp) {
     const int s = (int)A.rows;
     ProfScope ps(K_LEAF, st, 2.0 * s * s * s / 3.0, 4.0 * s * s);
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (!attr.done()) {
         FFB_CUDA(cudaFuncSetAttribute(k_node128, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)node_smem_bytes()));
-        attr = true;
+        attr.mark();
     }
     launch_k(k_node128, 1, 128, node_smem_bytes(), st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, yout, out,
              mp);

@@ -524,27 +524,29 @@ __global__ void __launch_bounds__(256) k_any_nonzero(const uint32_t* m, int64_t 
     }
 }
 
-// Symmetry check: block (x, y) compares the 32-row band y against the transposed
-// column tiles 8x .. 8x+7 (lower triangle only), both tiles' loads in flight.
 // Symmetry check: CTA (x, y) walks the 32x32 tiles of row band y left of the diagonal
 // with stride gridDim.x (no CTAs for the upper triangle), the next tile's loads issued
-// before the current tile's comparisons.
-__global__ void k_any_asym(const uint32_t* a, int64_t ld, int64_t n, int32_t* flag) {
+// before the current tile's comparisons.  T is the element type: uint32 residues of a
+// device matrix (p = 0: already reduced), or the caller's raw host element type staged
+// in HBM (u8/u16/u32/u64, compared as residues mod p; the reduction only runs for a pair
+// whose raw values differ).
+template <typename T>
+__global__ void k_any_asym(const T* a, int64_t ld, int64_t n, uint64_t p, int32_t* flag) {
     FFB_PDL_ENTRY();
-    __shared__ uint32_t tile[32][33];
+    __shared__ T tile[32][33];
     const int64_t r0 = (int64_t)blockIdx.y * 32;
     int bad = 0;
     auto valid = [&](int64_t t) { return t * 32 <= r0 + 31 && t * 32 < n; };
-    uint32_t up[4], lo[4];
+    T up[4], lo[4];
     auto load = [&](int64_t t) {
         const int64_t c0 = t * 32;
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int k = threadIdx.y + 8 * u;
             const int64_t r = c0 + k, c = r0 + threadIdx.x;  // transposed tile
-            up[u] = (r < n && c < n) ? __ldcg(a + r * ld + c) : 0u;
+            up[u] = (r < n && c < n) ? __ldcg(a + r * ld + c) : T(0);
             const int64_t rr = r0 + k, cc = c0 + threadIdx.x;
-            lo[u] = (rr < n && cc < n) ? __ldcg(a + rr * ld + cc) : 0u;
+            lo[u] = (rr < n && cc < n) ? __ldcg(a + rr * ld + cc) : T(0);
         }
     };
     int64_t t = blockIdx.x;
@@ -555,7 +557,7 @@ __global__ void k_any_asym(const uint32_t* a, int64_t ld, int64_t n, int32_t* fl
 #pragma unroll
         for (int u = 0; u < 4; ++u) tile[threadIdx.y + 8 * u][threadIdx.x] = up[u];
         __syncthreads();
-        uint32_t cur[4];
+        T cur[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) cur[u] = lo[u];
         const int64_t tn = t + gridDim.x;
@@ -564,7 +566,9 @@ __global__ void k_any_asym(const uint32_t* a, int64_t ld, int64_t n, int32_t* fl
         for (int u = 0; u < 4; ++u) {
             const int k = threadIdx.y + 8 * u;
             const int64_t r = r0 + k, c = c0 + threadIdx.x;
-            if (r < n && c < n) bad |= cur[u] != tile[threadIdx.x][k];
+            const T x = cur[u], y = tile[threadIdx.x][k];
+            if (r < n && c < n && x != y)
+                bad |= p == 0 || (uint64_t)x % p != (uint64_t)y % p;
         }
         t = tn;
     }
@@ -708,10 +712,10 @@ void gather_sym(cudaStream_t st, DMat dst, DMat src, const int32_t* idx) {
     if (dst.rows <= 0) return;
     const size_t row_bytes = (size_t)dst.cols * 4;
     if (dst.cols >= 1024 && row_bytes <= 200 * 1024 && (src.ld & 3) == 0 && (((uintptr_t)src.ptr) & 15) == 0) {
-        static bool attr = false;
-        if (!attr) {
+        static DeviceOnce attr;
+        if (!attr.done()) {
             FFB_CUDA(cudaFuncSetAttribute(k_gather_sym_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-            attr = true;
+            attr.mark();
         }
         const int64_t per_sm = std::max<int64_t>(1, std::min<int64_t>(4, (int64_t)(227 * 1024) / (int64_t)(row_bytes + 1024)));
         const int64_t grid = std::min<int64_t>(dst.rows, 148 * per_sm);
@@ -839,7 +843,20 @@ void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag) {
     ProfScope ps_(K_OTHER, st, 0.0, 0.0);
     if (a.rows <= 1) return;
     dim3 grid((unsigned)std::min<int64_t>(8, cdiv(a.rows, 32)), (unsigned)cdiv(a.rows, 32));
-    launch_k(k_any_asym, grid, dim3(32, 8), 0, st, a.ptr, a.ld, a.rows, flag);
+    launch_k(k_any_asym<uint32_t>, grid, dim3(32, 8), 0, st, (const uint32_t*)a.ptr, a.ld, a.rows,
+             (uint64_t)0, flag);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void any_asymmetric_raw(cudaStream_t st, const void* a, int64_t n, int eb, uint64_t p, int32_t* flag) {
+    ProfScope ps_(K_OTHER, st, 0.0, 0.0);
+    if (n <= 1) return;
+    dim3 grid((unsigned)std::min<int64_t>(8, cdiv(n, 32)), (unsigned)cdiv(n, 32));
+    if (eb == 8) launch_k(k_any_asym<uint64_t>, grid, dim3(32, 8), 0, st, (const uint64_t*)a, n, n, p, flag);
+    else if (eb == 4) launch_k(k_any_asym<uint32_t>, grid, dim3(32, 8), 0, st, (const uint32_t*)a, n, n, p, flag);
+    else if (eb == 2) launch_k(k_any_asym<uint16_t>, grid, dim3(32, 8), 0, st, (const uint16_t*)a, n, n, p, flag);
+    else launch_k(k_any_asym<uint8_t>, grid, dim3(32, 8), 0, st, (const uint8_t*)a, n, n, p, flag);
     count_launch();
     FFB_CHECK_LAUNCH();
 }

@@ -114,6 +114,9 @@ void invert_vec(const Fp& f, cudaStream_t st, uint32_t* out, const uint32_t* v, 
 void any_nonzero(cudaStream_t st, DMat m, int32_t* flag, int32_t value = 1);
 // flag |= any a[i][j] != a[j][i]
 void any_asymmetric(cudaStream_t st, DMat a, int32_t* flag);
+// flag |= any a[i][j] != a[j][i] (mod p) on a raw n x n row-major matrix of eb-byte
+// unsigned elements (the staged host input; the engine never writes it)
+void any_asymmetric_raw(cudaStream_t st, const void* a, int64_t n, int eb, uint64_t p, int32_t* flag);
 // Y <- strict_upper(Ct) + diag(Ct)/2 (odd p) or 0 (p = 2); lower part zeroed; in place.
 // flag |= nonzero diagonal when p = 2 (no solution: CharTwoNonzeroDiagonal).
 void trssyr2k_mid(const Fp& f, cudaStream_t st, DMat Ct, int32_t* flag);

@@ -166,9 +166,9 @@ struct MmaScratch {
     uint32_t* ptr = nullptr;
     size_t cap = 0;
 };
-thread_local MmaScratch g_mscratch_slots[5];
+thread_local MmaScratch g_mscratch_slots[FFB_MAX_DEVICES][5];
 uint32_t* mma_scratch(size_t words) {
-    MmaScratch& g_mscratch = g_mscratch_slots[g_slot];
+    MmaScratch& g_mscratch = g_mscratch_slots[current_device()][g_slot];
     if (g_mscratch.cap < words) {
         if (g_mscratch.ptr) {
             FFB_CUDA(cudaDeviceSynchronize());
@@ -358,12 +358,12 @@ void rankk_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, boo
     while (TR > 16 && ncb * cdiv(M, TR) < 4 * 148) TR /= 2;  // enough CTAs to fill the GPU
     const int K4 = (int)((K + 3) / 4);
     const size_t smem = ((size_t)K4 * RK_COLS + (size_t)TR * K4) * 4;
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (!attr.done()) {
         for (auto fn : {k_rankk_dp4a<false, false>, k_rankk_dp4a<true, false>, k_rankk_dp4a<false, true>,
                         k_rankk_dp4a<true, true>})
             FFB_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        attr = true;
+        attr.mark();
     }
     const dim3 grid((unsigned)ncb, (unsigned)cdiv(M, TR));
 #define FFB_RK_LAUNCH(TA, TB) \

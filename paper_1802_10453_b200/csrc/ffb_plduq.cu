@@ -1268,8 +1268,8 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     const size_t rd_smem = std::max({rd_smem_bytes(RD_MAX_B, SK), rd_smem_bytes(RD_MAX_ROWS, RD_NARROW),
                                       rd_smem_bytes(PIPE_KMAX + B, SK)});
     const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + 2 * (size_t)CRP_G * CRP_KMAX) * 4;
-    static bool attrs = false;
-    if (!attrs) {
+    static DeviceOnce attrs;
+    if (!attrs.done()) {
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
         FFB_CUDA(cudaFuncSetAttribute(k_row_detect<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rd_smem));
@@ -1278,34 +1278,35 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         FFB_CUDA(cudaFuncSetAttribute(k_crp_rowelim, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         FFB_CUDA(cudaFuncSetAttribute(k_crp_finish, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)((size_t)CF_SMEM_WORDS * 4)));
-        attrs = true;
+        attrs.mark();
     }
     static const bool force_exact = getenv("FFB_PLDUQ_FORCE_FALLBACK") != nullptr;  // test hook
 
     // side stream for the Uhat updates (see absorb)
-    static thread_local cudaStream_t side = nullptr;
-    static thread_local cudaEvent_t ev_main = nullptr, ev_side = nullptr;
+    // (per device: a thread may drive contexts on several GPUs)
+    struct SideStreams {
+        cudaStream_t side = nullptr, side2 = nullptr, side3 = nullptr;
+        cudaEvent_t ev_main = nullptr, ev_side = nullptr, ev_gk = nullptr, ev_si = nullptr, ev_sk = nullptr,
+                    ev_det = nullptr, ev_t1 = nullptr, ev_un = nullptr;
+    };
+    static thread_local SideStreams side_dev[FFB_MAX_DEVICES];
+    SideStreams& ss = side_dev[current_device()];
     static const bool overlap_ok = !getenv("FFB_PLDUQ_NO_OVERLAP");  // test hook
-    if (!side) {
+    if (!ss.side) {
         int least = 0, greatest = 0;  // lowest priority: the main stream's chunk kernels go first
         FFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        FFB_CUDA(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, least));
-        FFB_CUDA(cudaEventCreateWithFlags(&ev_main, cudaEventDisableTiming));
-        FFB_CUDA(cudaEventCreateWithFlags(&ev_side, cudaEventDisableTiming));
-    }
-    // side2: pipelined sketch + row detection of the next chunk (highest priority: its
-    // 1-CTA detection is latency-bound and must not queue behind the Uhat updates)
-    static thread_local cudaStream_t side2 = nullptr, side3 = nullptr;
-    static thread_local cudaEvent_t ev_gk = nullptr, ev_si = nullptr, ev_sk = nullptr, ev_det = nullptr,
-                                    ev_t1 = nullptr, ev_un = nullptr;
-    if (!side2) {
-        int least = 0, greatest = 0;
-        FFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        FFB_CUDA(cudaStreamCreateWithPriority(&side2, cudaStreamNonBlocking, greatest));
-        FFB_CUDA(cudaStreamCreateWithPriority(&side3, cudaStreamNonBlocking, greatest));
-        for (cudaEvent_t* e : {&ev_gk, &ev_si, &ev_sk, &ev_det, &ev_t1, &ev_un})
+        FFB_CUDA(cudaStreamCreateWithPriority(&ss.side, cudaStreamNonBlocking, least));
+        // side2: pipelined sketch + row detection of the next chunk (highest priority: its
+        // 1-CTA detection is latency-bound and must not queue behind the Uhat updates)
+        FFB_CUDA(cudaStreamCreateWithPriority(&ss.side2, cudaStreamNonBlocking, greatest));
+        FFB_CUDA(cudaStreamCreateWithPriority(&ss.side3, cudaStreamNonBlocking, greatest));
+        for (cudaEvent_t* e : {&ss.ev_main, &ss.ev_side, &ss.ev_gk, &ss.ev_si, &ss.ev_sk, &ss.ev_det, &ss.ev_t1,
+                               &ss.ev_un})
             FFB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
+    cudaStream_t side = ss.side, side2 = ss.side2, side3 = ss.side3;
+    cudaEvent_t ev_main = ss.ev_main, ev_side = ss.ev_side, ev_gk = ss.ev_gk, ev_si = ss.ev_si, ev_sk = ss.ev_sk,
+                ev_det = ss.ev_det, ev_t1 = ss.ev_t1, ev_un = ss.ev_un;
     static const bool pipe_on = overlap_ok && !getenv("FFB_PLDUQ_NO_PIPE");  // A/B hook
     DMat T2[2] = {ws.mat(PIPE_KMAX + B, SK), ws.mat(PIPE_KMAX + B, SK)};
     int32_t* pinfo[2] = {ws.vec<int32_t>(2 * (PIPE_KMAX + B) + 16), ws.vec<int32_t>(2 * (PIPE_KMAX + B) + 16)};

@@ -804,10 +804,10 @@ struct Scratch {
     int8_t* ptr = nullptr;
     size_t cap = 0;
 };
-thread_local Scratch g_scratch_slots[5];
+thread_local Scratch g_scratch_slots[FFB_MAX_DEVICES][5];
 
 int8_t* scratch(size_t bytes) {
-    Scratch& g_scratch = g_scratch_slots[g_slot];
+    Scratch& g_scratch = g_scratch_slots[current_device()][g_slot];
     if (g_scratch.cap < bytes) {
         if (g_scratch.ptr) {
             FFB_CUDA(cudaDeviceSynchronize());
@@ -840,11 +840,11 @@ template <int BN, int ST = 0>
 void launch_tc(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, DMat C, int64_t M,
                int64_t N, int64_t nk, const Fp& f, int mode) {
     using Cfg = TcCfg<BN, ST>;
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (!attr.done()) {
         FFB_CUDA(cudaFuncSetAttribute(k_gemm_i8_tc<BN, ST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       Cfg::SMEM));
-        attr = true;
+        attr.mark();
     }
     dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, TC_BM));
     launch_k(k_gemm_i8_tc<BN, ST>, grid, TC_THREADS, Cfg::SMEM, st, ma, mb, C.ptr, C.ld, (int)M, (int)N,
@@ -892,10 +892,10 @@ void tc_gemm_limb(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, b
         pk(Ap, aplane, A, ta, M);
         pk(Bp, bplane, B, !tb, N);
     }
-    static bool attr = false;
-    if (!attr) {
+    static DeviceOnce attr;
+    if (!attr.done()) {
         FFB_CUDA(cudaFuncSetAttribute(k_gemm_limb_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, LB_SMEM));
-        attr = true;
+        attr.mark();
     }
     ProfScope ps(K_GEMM, st, 2.0 * M * N * K, 3.0 * (M * K + N * K) + 8.0 * M * N, M, N, -K);
     CUtensorMap ma = make_map(Ap, 3 * Mr, Kp, TC_BM), mb = make_map(Bp, 3 * Nr, Kp, LB_BN);
@@ -942,15 +942,16 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
         launch_tc<128, 2>(st, ma, mb, C, M, N, nk, f, mode);
     } else if (wide && !getenv("FFB_TC_NONPERSISTENT")) {
         CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, TP_BN);
-        static bool attr = false;
-        static int nsm = 148;
-        if (!attr) {
+        static DeviceOnce attr;
+        static int nsm_dev[FFB_MAX_DEVICES];
+        if (!attr.done()) {
             FFB_CUDA(cudaFuncSetAttribute(k_gemm_i8_tcp, cudaFuncAttributeMaxDynamicSharedMemorySize, TpCfg::SMEM));
             int dev = 0;
             FFB_CUDA(cudaGetDevice(&dev));
-            FFB_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-            attr = true;
+            FFB_CUDA(cudaDeviceGetAttribute(&nsm_dev[current_device()], cudaDevAttrMultiProcessorCount, dev));
+            attr.mark();
         }
+        const int nsm = nsm_dev[current_device()];
         const int num_m = (int)cdiv(M, TC_BM), num_tiles = num_m * (int)cdiv(N, TP_BN);
         // beside the critical path: a persistent grid on part of the SMs only, the rest
         // stay free for the engine stream's latency kernels

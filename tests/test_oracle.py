@@ -201,3 +201,39 @@ def test_oracle_errors(oracle):
     with pytest.raises(CheckerError) as e:
         oracle.ldlt(8, np.zeros((2, 2), np.uint64))
     assert e.value.name == "NotPrime"
+
+
+def test_oracle_generators_match_product(oracle):
+    """oracle/gen_oracle.c (used by bench.py's CPU legs instead of the product library)
+    builds the same inputs as ffb_generate_host, element for element."""
+    from paper_1802_10453_b200 import configs
+    for c in (1, 2, 3, 4, 5):
+        for n in (1, 37, 300):
+            w = configs.CONFIGS[c].scaled(n)
+            want = configs.generate(w)
+            got = oracle.generate(c, w.n, w.r, w.p, w.seed)
+            assert np.array_equal(got, want), (c, n)
+    w = configs.CONFIGS[5].scaled(1000)
+    assert np.array_equal(oracle.config5_partners(w.n, w.r, w.seed), configs.config5_partners(w))
+
+
+def test_fullsize_golden_small_configs(oracle):
+    """tests/golden/fullsize.json (make_fullsize.py) re-derived for the configurations the
+    oracle factors in seconds (1: n=1024, 2: n=4096); the larger ones are checked on the
+    GPU against the same file (test_fullsize_gpu.py)."""
+    import sys
+    sys.path.insert(0, GOLDEN)
+    from make_fullsize import digest
+    with open(os.path.join(GOLDEN, "fullsize.json")) as fh:
+        gold = json.load(fh)
+    from paper_1802_10453_b200 import configs
+    for c in (1, 2):
+        w = configs.CONFIGS[c]
+        g = gold[str(c)]
+        assert (g["n"], g["p"], g["seed"], g["rank_param"]) == (w.n, w.p, w.seed, w.r)
+        o = oracle.ldlt(w.p, oracle.generate(c, w.n, w.r, w.p, w.seed))
+        d = digest(o.perm, o.lower, o.dkind, o.dval, o.dval2, o.rank)
+        for k in ("rank", "perm", "lower_blocks", "dkind", "dval", "dval2"):
+            assert d[k] == g[k], (c, k)
+    for c in (1, 2, 3, 4, 5):
+        assert str(c) in gold, f"config {c} missing from fullsize.json"

@@ -446,3 +446,56 @@ def test_asymmetry_anywhere(gpu, pos):
         ffb.ldlt(a, 131, ctx=gpu)
     a[i, j] = a[j, i]
     ffb.ldlt(a, 131, ctx=gpu)
+
+
+def test_banded_symmetry_check_race_free(gpu):
+    """with the banded upload the symmetry check runs on the copy stream
+    while the recursion already updates W in place.  The check reads the raw staging
+    buffer (never written by the engine), so a symmetric U64 input at n = 8192 is never
+    refused, over repeated calls; an unreduced pair (x, x + p) counts as symmetric (as on
+    the small-n path, which compares reduced residues), and a real asymmetry in each
+    element type is refused."""
+    import ctypes as C
+    import paper_1802_10453_b200 as ffb
+    from paper_1802_10453_b200 import configs
+    from paper_1802_10453_b200._lib import lib
+    w = configs.CONFIGS[5].scaled(8192)
+    a = configs.generate(w)
+    for _ in range(20):
+        g = ffb.ldlt(a, w.p, ctx=gpu)
+        assert g.rank == w.r
+    b = a.copy()
+    b[17, 4000] += w.p  # same residue as b[4000, 17]
+    assert ffb.ldlt(b, w.p, ctx=gpu).rank == w.r
+    n = 4096
+    a4 = configs.generate(configs.CONFIGS[1].scaled(n))
+    for dt, eb in ((np.uint8, 1), (np.uint16, 2), (np.uint32, 4), (np.uint64, 8)):
+        for i, j in ((n - 1, 0), (2048, 2047), (5, 4090)):
+            h = np.ascontiguousarray(a4.astype(dt))
+            h[i, j] = (int(h[j, i]) + 1) % 131
+            out = [np.zeros(n, np.int64), np.zeros(n * n * 8, np.uint8), np.zeros(n, np.int32),
+                   np.zeros(n, np.uint64), np.zeros(n, np.uint64)]
+            rank = C.c_size_t(0)
+            ptr = lambda x: x.ctypes.data_as(C.c_void_p)
+            code = lib().ffb_ldlt_compact(gpu.handle, 131, n, ptr(h), eb, 2, 64, ptr(out[0]),
+                                          ptr(out[1]), 8, ptr(out[2]), ptr(out[3]), ptr(out[4]),
+                                          C.byref(rank))
+            assert code == 2, (eb, i, j, code)  # FFB_NOT_SYMMETRIC
+
+
+def test_two_devices_one_thread():
+    """streams, scratch and kernel attributes are per device, so one
+    thread can drive contexts on two GPUs alternately."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    import paper_1802_10453_b200 as ffb
+    from paper_1802_10453_b200 import configs
+    w = configs.CONFIGS[5].scaled(2048)
+    a = configs.generate(w)
+    want = None
+    for dev in (0, 1, 0, 1):
+        g = ffb.ldlt(a, w.p, ctx=ffb.default_context(dev))
+        if want is None:
+            want = g
+        assert g.rank == want.rank and np.array_equal(g.lower, want.lower)
