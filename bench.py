@@ -33,7 +33,33 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-INT8_DENSE_PEAK_TOPS = 4500.0  # B200 datasheet dense INT8 (no int8 entry in MEASURED_PEAKS.json)
+INT8_DATASHEET_TOPS = 4500.0  # B200 datasheet dense INT8 (the north star's "% of tensor peak")
+PROFILES = os.path.join(ROOT, "profiles")
+
+
+def int8_peak():
+    """Measured dense int8 peak (tools/int8_peak.py on a B200 of this pool: cuBLASLt IMMA via
+    torch._int_mm, 8192^3; MEASURED_PEAKS.json has no int8 entry).  Returns (burst,
+    sustained, source); falls back to the datasheet only if the measurement is absent."""
+    path = os.path.join(PROFILES, "r02_int8_peak.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        return (d["int8_tops_burst"], d["int8_tops_sustained"],
+                "of measured: cuBLASLt int8 (torch._int_mm 8192^3) on a B200 of this pool, "
+                "profiles/r02_int8_peak.json")
+    except (OSError, KeyError, ValueError):
+        return INT8_DATASHEET_TOPS, INT8_DATASHEET_TOPS, "of datasheet (measured int8 peak absent)"
+
+
+def ncu_gemm_traffic():
+    """DRAM bytes of the GEMM kernels of one config-5 factorization, from the committed ncu
+    capture (tools/ncu_traffic.py); None when absent."""
+    try:
+        with open(os.path.join(PROFILES, "r02_ncu_gemm_traffic.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
 
 
 def log(*a):
@@ -132,20 +158,21 @@ class ClockSampler:
 # CPU legs (reference / oracle)
 # ---------------------------------------------------------------------------
 def reference_sample(n_sample, w_full, threads):
-    """Time the unmodified reference on `threads` concurrent cfg-family samples."""
+    """Time the unmodified reference (oracle/_ref) on `threads` concurrent config-family
+    samples of size n_sample (one single-threaded ffldl::ldlt each: the reference has no
+    threading).  Inputs come from oracle/gen_oracle.c: the product library is
+    not loaded on this path."""
     from oracle.bind import LIBS, Checker
-    from paper_1802_10453_b200 import configs
     kind = "reference" if os.path.exists(LIBS["ref"]) else "port"
     chk = Checker("ref" if kind == "reference" else "oracle")
-    ws = [configs.Workload(w_full.config, n_sample, w_full.p,
-                           (w_full.r * n_sample) // w_full.n if w_full.r else 0, w_full.seed + k,
-                           w_full.description) for k in range(threads)]
-    mats = [configs.generate(w) for w in ws]
+    gen = Checker("oracle")
+    r = (w_full.r * n_sample) // w_full.n if w_full.r else 0
+    mats = [gen.generate(w_full.config, n_sample, r, w_full.p, w_full.seed + k) for k in range(threads)]
     results = [None] * threads
 
     def work(k):
         t0 = time.perf_counter()
-        chk.ldlt(ws[k].p, mats[k])
+        chk.ldlt(w_full.p, mats[k])
         results[k] = time.perf_counter() - t0
 
     t0 = time.perf_counter()
@@ -156,7 +183,13 @@ def reference_sample(n_sample, w_full, threads):
         t.join()
     wall = time.perf_counter() - t0
     ops = threads * 2.0 * n_sample ** 3 / 3.0
-    return kind, ops / wall, wall
+    return kind, ops / wall, wall, statistics.median(results)
+
+
+def extrapolated_full(w, n_sample, t_one):
+    """Single-thread time of the full-size factorization extrapolated by n^3 from a sample
+    (labelled as such; the reference's cost is cubic)."""
+    return t_one * (w.n / n_sample) ** 3
 
 
 def run_reference_arm(args, w, rank, world):
@@ -167,23 +200,40 @@ def run_reference_arm(args, w, rank, world):
     times = []
     kind = "reference"
     for i in range(args.warmup + args.steps):
-        kind, rate, wall = reference_sample(n_sample, w, threads)
+        kind, rate, wall, t_one = reference_sample(n_sample, w, threads)
         if i >= args.warmup:
-            times.append((rate, wall))
-    value = statistics.median(r for r, _ in times) / 1e12
+            times.append((rate, wall, t_one))
+    value = statistics.median(r for r, _, _ in times) / 1e12
+    t_one = statistics.median(t for _, _, t in times)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": statistics.median(t for _, t in times) * 1e3,
+        "ms_per_step": statistics.median(t for _, t, _ in times) * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic", "config": config_block(w, args),
+        "data": "synthetic (oracle/gen_oracle.c, the same seeded family as the GPU arm)",
+        "config": config_block(w, args),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
                          "sample": f"{threads} concurrent single-threaded ffldl::ldlt calls "
-                                   f"(Cascade, T=64) on config-{w.config}-family matrices of "
-                                   f"n={n_sample} per step; rate = {threads}*2n^3/3 / wall"},
+                                   f"(Cascade, T=64) of the unmodified reference (oracle/_ref) on "
+                                   f"config-{w.config}-family matrices of n={n_sample} per step; "
+                                   f"rate = {threads}*2n^3/3 / wall",
+                         "single_call_s": t_one,
+                         "full_size_single_thread_s_extrapolated": extrapolated_full(w, n_sample, t_one),
+                         "extrapolation": f"n^3 from n={n_sample} to n={w.n} (labelled estimate, "
+                                          "not measured)"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_reference_configs():
+    """Per-configuration CPU reference timings measured on a GPU box's host (single thread,
+    600 s cap, n^3 extrapolation beyond it; tools/cpu_reference_configs.py), if committed."""
+    try:
+        with open(os.path.join(PROFILES, "r02_cpu_reference_configs.json")) as fh:
+            return json.load(fh)
+    except (OSError, ValueError):
+        return None
 
 
 # ---------------------------------------------------------------------------
@@ -210,9 +260,10 @@ def main():
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--n", type=int, default=0, help="override n (family scaled)")
     ap.add_argument("--threshold", type=int, default=64)
-    ap.add_argument("--ref-n", type=int, default=1024, help="CPU sample size")
+    ap.add_argument("--ref-n", type=int, default=2048, help="CPU sample size (reference arm)")
     ap.add_argument("--cpu-n", type=int, default=2048, help="cpu_baseline sample size")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-e2e-u64", action="store_true", help="skip the uint64 drop-in e2e call")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--backend", default="nccl")
     args = ap.parse_args()
@@ -285,17 +336,28 @@ def main():
     largest = largest_gemm(trace_path)
     gemm = prof["gemm"]
     roofline = None
+    burst, sustained, peak_src = int8_peak()
     if gemm["ms"] > 0:
         achieved = gemm["ops"] / (gemm["ms"] / 1e3) / 1e12
-        roofline = {"bound": "tensor", "achieved": achieved, "peak": INT8_DENSE_PEAK_TOPS,
-                    "unit": "TFLOP/s", "frac": achieved / INT8_DENSE_PEAK_TOPS, "traffic": None,
+        nt = ncu_gemm_traffic() if w.config == 5 and w.n == 32768 else None
+        roofline = {"bound": "tensor", "achieved": achieved, "peak": sustained,
+                    "unit": "TFLOP/s", "frac": achieved / sustained,
+                    "traffic": nt["dram_bytes_per_launch"] if nt else None,
                     "kernel": "modular GEMM (all GEMM launches of one factorization)",
                     "algorithmic": "2*M*N*K int ops per launch, summed; duration = CUDA events "
                                    "around each launch on the engine stream",
-                    "peak_source": "B200 datasheet dense INT8 4.5 POPS (MEASURED_PEAKS.json has "
-                                   "no int8 entry)",
-                    "launches": gemm["launches"], "gemm_ms": gemm["ms"]}
+                    "peak_source": peak_src + " -- sustained figure (kernels timed inside a long "
+                                   f"step); burst {burst:.0f}, datasheet {INT8_DATASHEET_TOPS:.0f}",
+                    "frac_of_burst": achieved / burst, "frac_of_datasheet": achieved / INT8_DATASHEET_TOPS,
+                    "launches": gemm["launches"], "gemm_ms": gemm["ms"],
+                    "algorithmic_bytes_per_launch": gemm["bytes"] / max(gemm["launches"], 1)}
+        if nt:
+            roofline["traffic_source"] = nt["source"]
+            roofline["traffic_vs_algorithmic"] = nt["dram_bytes_total"] / max(gemm["bytes"], 1.0)
         if largest:
+            largest["frac"] = largest["achieved"] / sustained
+            if nt and nt.get("top_launch"):
+                largest["ncu"] = nt["top_launch"]
             roofline["largest_gemm"] = largest
 
     # full-size correctness of the measured factorization (outside the timed region):
@@ -315,10 +377,16 @@ def main():
 
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
-        kind, rate, wall = reference_sample(args.cpu_n, w, 1)
+        n_cpu = min(args.cpu_n, w.n)
+        kind, rate, wall, t_one = reference_sample(n_cpu, w, 1)
         cpu = {"value": rate / 1e12, "unit": UNIT, "cores": 1, "kind": kind,
-               "sample": f"one single-threaded ffldl::ldlt (Cascade, T=64) on a config-"
-                         f"{w.config}-family matrix of n={args.cpu_n} ({wall:.1f} s)"}
+               "sample": f"one single-threaded ffldl::ldlt (Cascade, T=64) of the unmodified "
+                         f"reference on a config-{w.config}-family matrix of n={n_cpu} ({wall:.1f} s)",
+               "full_size_single_thread_s_extrapolated": extrapolated_full(w, n_cpu, t_one),
+               "extrapolation": f"n^3 from n={n_cpu} to n={w.n} (labelled estimate)"}
+        per_cfg = cpu_reference_configs()
+        if per_cfg:
+            cpu["per_config"] = per_cfg
 
     if rank == 0:
         line = {
@@ -327,7 +395,9 @@ def main():
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (seeded counter-based generator, csrc/ffb_gen.cu)",
             "config": config_block(w, args),
-            "frac_of_int8_peak": value / INT8_DENSE_PEAK_TOPS, "rank": rank_out,
+            "frac_of_int8_peak": value / INT8_DATASHEET_TOPS,
+            "frac_of_measured_int8": {"burst": value / burst, "sustained": value / sustained},
+            "rank": rank_out,
             "rank_aware_tops": value * (2 * (rank_out ** 3 / 3 + w.n ** 2 * rank_out
                                              - rank_out ** 2 * w.n)) / ops if rank_out else 0,
             "gpu_launches": launches, "gpu_launches_per_step": launches // max(args.steps, 1),
@@ -343,8 +413,8 @@ def main():
 
 def largest_gemm(path):
     """The largest GEMM launch of the instrumented pass (the top-level Schur update):
-    shape, CUDA-event time, achieved TOPS against the int8 peak, plus the DRAM traffic of
-    the same kernel on that shape from the committed ncu capture."""
+    shape, CUDA-event time and achieved TOPS (its ncu DRAM traffic is attached by the
+    caller from the committed capture of the same in-step launch)."""
     try:
         best = None
         with open(path) as fh:
@@ -366,14 +436,16 @@ def largest_gemm(path):
     m, n, k, t = best
     tops = 2.0 * m * n * k / (t / 1e3) / 1e12
     return {"kernel": "k_gemm_i8_tcp (persistent tcgen05 int8 GEMM)", "shape_mnk": [m, n, k],
-            "ms": t, "achieved": tops, "frac": tops / INT8_DENSE_PEAK_TOPS,
-            "algorithmic_bytes": m * k + k * n + 8 * m * n,
-            "ncu_dram_bytes_16384x16384x4096": 2.70e9,
-            "ncu_source": "profiles/r01_tcp_gemm_16384x16384x4096_ncu.txt"}
+            "ms": t, "achieved": tops, "algorithmic_bytes": m * k + k * n + 8 * m * n}
 
 
 def run_e2e(w, ctx, cfg, args, local):
-    """Same metric through the host-buffer C-ABI call (ffb_ldlt_compact) from pinned memory."""
+    """Same metric through the host-buffer C-ABI (the call a user makes), from pinned memory,
+    timed on the host wall clock around the (synchronous) call: H2D of the input, symmetry
+    check, factorization, L gather and D2H of P, L, D all inside.  `value`: ffb_ldlt_compact
+    with 1-byte residues (p <= 255, else 4-byte), median of 3 after one warm-up.
+    `dropin_u64`: ffb_ldlt itself -- the boundary ffldl::ldlt(Matrix) binds, uint64 in and
+    out (sytrf.hpp:30) -- one warm-up and one timed call."""
     import ctypes as C
 
     import numpy as np
@@ -384,11 +456,9 @@ def run_e2e(w, ctx, cfg, args, local):
     from paper_1802_10453_b200.ffldl import _check
 
     eb = 1 if w.p <= 256 else 4
-    np_dt = np.uint8 if eb == 1 else np.uint32
     a_dev = configs.generate_device(w, ctx)
     host_a = torch.empty((w.n, w.n), dtype=torch.uint8 if eb == 1 else torch.int32).pin_memory()
     host_a.copy_(a_dev.to(torch.uint8 if eb == 1 else torch.int32).cpu())
-    del a_dev
     host_l = torch.empty(w.n * w.n * eb, dtype=torch.uint8).pin_memory()
     perm = np.zeros(w.n, np.int64)
     dk = np.zeros(w.n, np.int32)
@@ -396,27 +466,48 @@ def run_e2e(w, ctx, cfg, args, local):
     dv2 = np.zeros(w.n, np.uint64)
     rank = C.c_size_t(0)
     ptr = lambda x: x.ctypes.data_as(C.c_void_p)
-    st = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
     times = []
-    for i in range(2):
+    for i in range(4):
         torch.cuda.synchronize()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(st)
+        t0 = time.perf_counter()
         _check(lib().ffb_ldlt_compact(ctx.handle, w.p, w.n, host_a.data_ptr(), eb,
                                       int(cfg.variant), int(cfg.base_case_threshold), ptr(perm),
                                       host_l.data_ptr(), eb, ptr(dk), ptr(dv), ptr(dv2),
                                       C.byref(rank)))
-        e1.record(st)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1) / 1e3)
-    t = times[-1]
+        if i:
+            times.append(time.perf_counter() - t0)
+    del host_l
+    t = statistics.median(times)
     r = rank.value
-    return {"value": 2.0 * w.n ** 3 / 3.0 / t / 1e12, "unit": UNIT,
-            "h2d_bytes_per_step": w.n * w.n * eb, "d2h_bytes_per_step": w.n * r * eb + w.n * 28,
-            "ms_per_step": t * 1e3,
-            "api": "ffb_ldlt_compact (host pinned buffers; H2D + symmetric check + "
-                   "factorization + L gather + D2H inside the timed call)"}
+    out = {"value": 2.0 * w.n ** 3 / 3.0 / t / 1e12, "unit": UNIT,
+           "h2d_bytes_per_step": w.n * w.n * eb, "d2h_bytes_per_step": w.n * r * eb + w.n * 28,
+           "ms_per_step": t * 1e3, "runs_ms": [x * 1e3 for x in times],
+           "api": f"ffb_ldlt_compact ({eb}-byte residues in pinned host buffers; H2D + symmetry "
+                  "check + factorization + L gather + D2H inside the timed call; host wall clock, "
+                  "median of 3 after 1 warm-up)"}
+    if not args.no_e2e_u64:
+        try:
+            host64 = torch.empty((w.n, w.n), dtype=torch.int64).pin_memory()
+            host64.copy_(host_a.to(torch.int64) if eb == 1 else host_a.to(torch.int64) & 0xFFFFFFFF)
+            del host_a
+            l64 = torch.empty(w.n * max(r, 1), dtype=torch.int64).pin_memory()
+            t64 = []
+            for i in range(2):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                _check(lib().ffb_ldlt(ctx.handle, w.p, w.n, w.n, host64.data_ptr(), int(cfg.variant),
+                                      int(cfg.base_case_threshold), ptr(perm), l64.data_ptr(), ptr(dk),
+                                      ptr(dv), ptr(dv2), C.byref(rank)))
+                t64.append(time.perf_counter() - t0)
+            out["dropin_u64"] = {"value": 2.0 * w.n ** 3 / 3.0 / t64[-1] / 1e12, "unit": UNIT,
+                                 "ms_per_step": t64[-1] * 1e3, "h2d_bytes_per_step": w.n * w.n * 8,
+                                 "d2h_bytes_per_step": w.n * r * 8 + w.n * 28,
+                                 "api": "ffb_ldlt (uint64 host buffers, pinned; the C-ABI entry "
+                                        "the drop-in ffldl::ldlt binds), second of 2 calls"}
+            del host64, l64
+        except (RuntimeError, MemoryError) as e:  # host memory for 12 GiB of pinned buffers
+            out["dropin_u64"] = {"skipped": repr(e)[:200]}
+    return out
 
 
 if __name__ == "__main__":

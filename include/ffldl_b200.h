@@ -49,6 +49,7 @@ extern "C" {
 #define FFB_NO_MEMORY 11             /* device workspace exhausted */
 #define FFB_CUDA_ERROR 12            /* CUDA runtime failure (new) */
 #define FFB_UNSUPPORTED 13           /* modulus outside the device range (new) */
+#define FFB_WRONG_CHARACTERISTIC 14  /* ffldl::WrongCharacteristic (strictify) */
 
 #define FFB_VARIANT_RECURSIVE 0
 #define FFB_VARIANT_CROUT 1
@@ -159,6 +160,24 @@ int ffb_syrdk_sub(ffb_context* ctx, uint64_t p, size_t n, size_t k, uint64_t* c,
                   const uint64_t* dval2);
 int ffb_syr2k_sub(ffb_context* ctx, uint64_t p, size_t n, size_t k, uint64_t* c,
                   const uint64_t* a, const uint64_t* b);
+/* syrdk_sub(Matrix& c, const Matrix& g, std::span<const FieldElement> d) -- the diagonal
+ * overload, kernels.hpp:29, kernels.cpp:108-119: C -= G diag(d) G^T (g is n x k, d[k]). */
+int ffb_syrdk_sub_diag(ffb_context* ctx, uint64_t p, size_t n, size_t k, uint64_t* c,
+                       const uint64_t* g, const uint64_t* d);
+
+/* strictify(Factorization&, StrictifyStats*) -- proj/include/ffldl/rpmtools.hpp:39,
+ * proj/src/rpmtools.cpp:74-132.  Rewrites every characteristic-2 AntiTri block [0 c; c d]
+ * into Scalar d, Scalar -c^2/d, adjusting two columns of L and composing a transposition
+ * into P per block (all on the device).  Host buffers in the ffb_ldlt layout (perm[n],
+ * lower n x rank, dkind/dval/dval2[rank]), updated in place; the two counters receive
+ * StrictifyStats (may be NULL).  FFB_WRONG_CHARACTERISTIC for an AntiTri block over odd p. */
+int ffb_strictify(ffb_context* ctx, uint64_t p, size_t n, size_t rank, int64_t* perm,
+                  uint64_t* lower, int32_t* dkind, uint64_t* dval, uint64_t* dval2,
+                  uint64_t* blocks_converted, uint64_t* entries_touched);
+/* Same on a device factorization (the ffb_ldlt_device output layout, row stride ldl). */
+int ffb_strictify_device(ffb_context* ctx, uint64_t p, size_t n, size_t rank, int32_t* d_perm,
+                         uint32_t* d_lower, size_t ldl, int32_t* d_dkind, uint32_t* d_dval,
+                         uint32_t* d_dval2, uint64_t* blocks_converted, uint64_t* entries_touched);
 
 /* Device-buffer modular GEMM (the engine's contraction kernel, kernels.hpp:13 semantics):
  * C (m x n) = C - op(A) op(B) (mode 0), C + op(A) op(B) (mode 1), op(A) op(B) (mode 2);

@@ -187,6 +187,28 @@ class Checker:
                                           _ptr(g), _ptr(dkind), _ptr(dval), _ptr(dval2)))
         return c
 
+    def syrdk_sub_diag(self, p, c, g, d):
+        c = _u64(c).copy()
+        g = _u64(g)
+        n, k = g.shape
+        d = _u64(d)
+        self._check(self._fn("syrdk_sub_diag")(C.c_uint64(p), C.c_size_t(n), C.c_size_t(k), _ptr(c),
+                                               _ptr(g), _ptr(d)))
+        return c
+
+    def strictify(self, p, f: "Fact"):
+        """strictify (rpmtools.cpp:74-132) of a copy of f; returns (Fact, (blocks, touched))."""
+        n, r = f.perm.shape[0], f.rank
+        perm = np.ascontiguousarray(f.perm, np.int64).copy()
+        lower = _u64(f.lower).copy()
+        dkind = np.ascontiguousarray(f.dkind, np.int32).copy()
+        dval, dval2 = _u64(f.dval).copy(), _u64(f.dval2).copy()
+        stats = np.zeros(2, np.uint64)
+        self._check(self._fn("strictify")(C.c_uint64(p), C.c_size_t(n), C.c_size_t(r), _ptr(perm),
+                                          _ptr(lower), _ptr(dkind), _ptr(dval), _ptr(dval2),
+                                          _ptr(stats)))
+        return Fact(perm, lower, dkind, dval, dval2, r), (int(stats[0]), int(stats[1]))
+
     def syr2k_sub(self, p, c, a, b):
         c = _u64(c).copy()
         a = _u64(a)

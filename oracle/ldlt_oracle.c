@@ -1139,3 +1139,70 @@ int orc_syr2k_sub(uint64_t p, size_t n, size_t k, uint64_t* c, const uint64_t* a
     mat_free(&cm); mat_free(&am); mat_free(&bm);
     return ORC_OK;
 }
+
+/* syrdk_sub(c, g, span d), kernels.cpp:108-119: C <- C - G diag(d) G^T. */
+int orc_syrdk_sub_diag(uint64_t p, size_t n, size_t k, uint64_t* c, const uint64_t* g,
+                       const uint64_t* d) {
+    int code = setjmp(ERR_JMP);
+    if (code) return code;
+    set_field(p);
+    uint64_t* dv = (uint64_t*)malloc((k ? k : 1) * sizeof(uint64_t));
+    for (size_t t = 0; t < k; ++t) dv[t] = d[t] % p;
+    Mat cm = load(n, n, c), gm = load(n, k, g);
+    syrdk_sub_diag(&cm, &gm, dv, k);
+    store(&cm, c);
+    mat_free(&cm); mat_free(&gm); free(dv);
+    return ORC_OK;
+}
+
+/* strictify, rpmtools.cpp:74-132: every AntiTri block [0 c; c d] at columns (t, t+1)
+ * becomes Scalar d, Scalar -c^2/d; L's columns t, t+1 and P change as the reference's
+ * three steps (normalize, swap, eliminate), run block by block in order.  The flat
+ * factorization (perm[n], lower n x r, dkind/dval/dval2[r]) is updated in place;
+ * stats[0] = blocks converted, stats[1] = entries touched (StrictifyStats). */
+int orc_strictify(uint64_t p, size_t n, size_t r, int64_t* perm, uint64_t* lower, int32_t* dkind,
+                  uint64_t* dval, uint64_t* dval2, uint64_t* stats) {
+    int code = setjmp(ERR_JMP);
+    if (code) return code;
+    set_field(p);
+    uint64_t blocks = 0, touched = 0;
+#define LL(i, j) lower[(size_t)(i) * r + (size_t)(j)]
+    for (size_t t = 0; t < r;) {
+        if (dkind[t] != ORC_D_ANTITRI_HEAD) {
+            t += dkind[t] == ORC_D_SCALAR ? 1 : 2;
+            continue;
+        }
+        if (p != 2) fail(ORC_WRONG_CHARACTERISTIC); /* rpmtools.cpp:87-88 */
+        const uint64_t c = dval[t] % p, dd = dval2[t] % p;
+        const uint64_t x = LL(t + 1, t) % p;
+        if (x != 0) /* :95-100 col t -= x col t+1 */
+            for (size_t i = t + 1; i < n; ++i) {
+                LL(i, t) = fsub(LL(i, t) % p, fmul(x, LL(i, t + 1) % p));
+                ++touched;
+            }
+        for (size_t j = 0; j < t; ++j) { /* :106-109 swap prefix of rows t, t+1 */
+            uint64_t s = LL(t, j); LL(t, j) = LL(t + 1, j); LL(t + 1, j) = s;
+            touched += 2;
+        }
+        for (size_t i = t + 2; i < n; ++i) { /* :110-113 swap the column pair below */
+            uint64_t s = LL(i, t); LL(i, t) = LL(i, t + 1); LL(i, t + 1) = s;
+            touched += 2;
+        }
+        { int64_t s = perm[t]; perm[t] = perm[t + 1]; perm[t + 1] = s; } /* :114 compose */
+        const uint64_t cd = fmul(c, finv(dd)); /* :118-123 col t += (c/d) col t+1 */
+        for (size_t i = t + 1; i < n; ++i) {
+            LL(i, t) = fadd(LL(i, t) % p, fmul(cd, LL(i, t + 1) % p));
+            ++touched;
+        }
+        dkind[t] = dkind[t + 1] = ORC_D_SCALAR;
+        dval[t] = dd;
+        dval[t + 1] = fneg(fmul(fmul(c, c), finv(dd)));
+        dval2[t] = dval2[t + 1] = 0;
+        ++blocks;
+        t += 2;
+    }
+#undef LL
+    stats[0] = blocks;
+    stats[1] = touched;
+    return ORC_OK;
+}

@@ -42,6 +42,7 @@
 #define ORC_BAD_BLOCK_SIZES 9
 #define ORC_OTHER 10
 #define ORC_NO_MEMORY 11
+#define ORC_WRONG_CHARACTERISTIC 12
 
 #define ORC_VARIANT_RECURSIVE 0
 #define ORC_VARIANT_CROUT 1

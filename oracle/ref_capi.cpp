@@ -10,6 +10,7 @@
 
 #include <cstdint>
 #include <cstring>
+#include <span>
 #include <variant>
 #include <vector>
 
@@ -100,11 +101,31 @@ int guarded(F&& fn) {
         return ORC_CHAR_TWO_NONZERO_DIAGONAL;
     } catch (const BadBlockSizes&) {
         return ORC_BAD_BLOCK_SIZES;
+    } catch (const WrongCharacteristic&) {
+        return ORC_WRONG_CHARACTERISTIC;
     } catch (const std::bad_alloc&) {
         return ORC_NO_MEMORY;
     } catch (...) {
         return ORC_OTHER;
     }
+}
+
+BlockDiag to_blockdiag(const PrimeField& f, size_t k, const int32_t* dkind, const uint64_t* dval,
+                       const uint64_t* dval2) {
+    BlockDiag d;
+    for (size_t t = 0; t < k;) {
+        if (dkind[t] == ORC_D_SCALAR) {
+            d.push(ScalarBlock{f.element(dval[t])});
+            t += 1;
+        } else if (dkind[t] == ORC_D_ANTIDIAG_HEAD) {
+            d.push(AntiDiagBlock{f.element(dval[t])});
+            t += 2;
+        } else {
+            d.push(AntiTriBlock{f.element(dval[t]), f.element(dval2[t])});
+            t += 2;
+        }
+    }
+    return d;
 }
 
 } // namespace
@@ -188,23 +209,42 @@ int ref_trmm_sub(uint64_t p, size_t n, size_t ncols, uint64_t* c, const uint64_t
 }
 
 // D given in the per-column encoding of oracle_api.h.
+int ref_syrdk_sub_diag(uint64_t p, size_t n, size_t k, uint64_t* c, const uint64_t* g,
+                       const uint64_t* d) {
+    return guarded([&] {
+        const PrimeField f(p);
+        std::vector<FieldElement> dv;
+        for (size_t t = 0; t < k; ++t) dv.push_back(f.element(d[t]));
+        Matrix cm = to_matrix(f, n, n, c);
+        syrdk_sub(cm, to_matrix(f, n, k, g), std::span<const FieldElement>(dv));
+        from_matrix(cm, c);
+    });
+}
+
+// strictify (rpmtools.cpp:74-132) of a factorization given in the flat layout; the
+// result overwrites the same arrays.
+int ref_strictify(uint64_t p, size_t n, size_t r, int64_t* perm, uint64_t* lower, int32_t* dkind,
+                  uint64_t* dval, uint64_t* dval2, uint64_t* stats) {
+    return guarded([&] {
+        const PrimeField f(p);
+        std::vector<std::size_t> img(n);
+        for (size_t i = 0; i < n; ++i) img[i] = static_cast<std::size_t>(perm[i]);
+        Factorization fac{Permutation::from_image(std::move(img)), to_matrix(f, n, r, lower),
+                          to_blockdiag(f, r, dkind, dval, dval2), r};
+        StrictifyStats st;
+        strictify(fac, &st);
+        size_t rank = 0;
+        export_fact(fac, perm, lower, dkind, dval, dval2, &rank);
+        stats[0] = st.blocks_converted;
+        stats[1] = st.entries_touched;
+    });
+}
+
 int ref_syrdk_sub(uint64_t p, size_t n, size_t k, uint64_t* c, const uint64_t* g,
                   const int32_t* dkind, const uint64_t* dval, const uint64_t* dval2) {
     return guarded([&] {
         const PrimeField f(p);
-        BlockDiag d;
-        for (size_t t = 0; t < k;) {
-            if (dkind[t] == ORC_D_SCALAR) {
-                d.push(ScalarBlock{f.element(dval[t])});
-                t += 1;
-            } else if (dkind[t] == ORC_D_ANTIDIAG_HEAD) {
-                d.push(AntiDiagBlock{f.element(dval[t])});
-                t += 2;
-            } else {
-                d.push(AntiTriBlock{f.element(dval[t]), f.element(dval2[t])});
-                t += 2;
-            }
-        }
+        const BlockDiag d = to_blockdiag(f, k, dkind, dval, dval2);
         Matrix cm = to_matrix(f, n, n, c);
         syrdk_sub(cm, to_matrix(f, n, k, g), d);
         from_matrix(cm, c);

@@ -9,8 +9,8 @@ from .ffldl import (AntiDiagBlock, AntiTriBlock, BadBlockSizes, BlockDiag, CharT
                     CharTwoNonzeroDiagonal, Context, CudaError, DimensionMismatch, Error,
                     Factorization, NoMemory, NonUnitTriangular, NotPrime, NotSymmetric,
                     Permutation, PlduqFactorization, PrimeField, ScalarBlock, SingularTriangular,
-                    SytrfConfig, Unsupported, Uplo, Variant, ZeroInverse, default_context,
+                    StrictifyStats, SytrfConfig, Unsupported, Uplo, Variant, ZeroInverse, default_context,
                     gemm_sub, ldlt, ldlt_zero_leading, plduq, syr2k_sub, syrdk_sub, trmm_sub,
-                    trsm_inplace, trssyr2k)
+                    trsm_inplace, trssyr2k, strictify, WrongCharacteristic)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

@@ -20,7 +20,8 @@ EXPORTS = [
     "ffb_stream", "ffb_launch_count", "ffb_sync_count", "ffb_profile_enable", "ffb_profile_read",
     "ffb_ldlt", "ffb_ldlt_compact", "ffb_ldlt_zero_leading",
     "ffb_ldlt_device", "ffb_plduq", "ffb_trssyr2k", "ffb_gemm_sub", "ffb_trmm_sub",
-    "ffb_trsm_inplace", "ffb_syrdk_sub", "ffb_syr2k_sub", "ffb_gemm_device", "ffb_generate_host",
+    "ffb_trsm_inplace", "ffb_syrdk_sub", "ffb_syrdk_sub_diag", "ffb_syr2k_sub", "ffb_strictify",
+    "ffb_strictify_device", "ffb_gemm_device", "ffb_generate_host",
     "ffb_generate_device", "ffb_config5_partners", "ffb_verify_device", "ffb_pivoting_partners_device",
 ]
 
@@ -52,6 +53,9 @@ _SIGS = {
     "ffb_trsm_inplace": (I, [P, U64, SZ, SZ, P, I, I, I, P]),
     "ffb_syrdk_sub": (I, [P, U64, SZ, SZ, P, P, P, P, P]),
     "ffb_syr2k_sub": (I, [P, U64, SZ, SZ, P, P, P]),
+    "ffb_syrdk_sub_diag": (I, [P, U64, SZ, SZ, P, P, P]),
+    "ffb_strictify": (I, [P, U64, SZ, SZ, P, P, P, P, P, C.POINTER(U64), C.POINTER(U64)]),
+    "ffb_strictify_device": (I, [P, U64, SZ, SZ, P, P, SZ, P, P, P, C.POINTER(U64), C.POINTER(U64)]),
     "ffb_gemm_device": (I, [P, U64, I, SZ, SZ, SZ, P, SZ, P, SZ, I, P, SZ, I]),
     "ffb_generate_host": (I, [I, SZ, SZ, U64, U64, P]),
     "ffb_generate_device": (I, [P, I, SZ, SZ, U64, U64, P]),

@@ -966,6 +966,7 @@ const char* ffb_status_string(int s) {
     case FFB_NO_MEMORY: return "NoMemory";
     case FFB_CUDA_ERROR: return "CudaError";
     case FFB_UNSUPPORTED: return "Unsupported";
+    case FFB_WRONG_CHARACTERISTIC: return "WrongCharacteristic";
     default: return "Error";
     }
 }
@@ -1355,33 +1356,18 @@ int ffb_gemm_sub(ffb_context* c, uint64_t p, size_t m, size_t n, size_t k, uint6
     });
 }
 
-// Dense op(T) on the host (triangle/unit conventions of kernels.cpp:23-29).
-static std::vector<uint64_t> dense_op(const uint64_t* t, size_t n, uint64_t p, int upper, int trans,
-                                      int unit) {
-    std::vector<uint64_t> o(n * n, 0);
-    for (size_t i = 0; i < n; ++i)
-        for (size_t j = 0; j < n; ++j) {
-            size_t a = i, b = j;
-            if (trans) std::swap(a, b);
-            uint64_t v;
-            if (a == b) v = unit ? 1 % p : t[a * n + a] % p;
-            else v = ((upper == 0) ? (a > b) : (a < b)) ? t[a * n + b] % p : 0;
-            o[i * n + j] = v;
-        }
-    return o;
-}
-
 int ffb_trmm_sub(ffb_context* c, uint64_t p, size_t n, size_t ncols, uint64_t* cc, const uint64_t* t,
                  int upper, int trans, int unit, const uint64_t* b) {
     return guarded(c, [&] {
         check_modulus(p);
-        std::vector<uint64_t> o = dense_op(t, n, p, upper, trans, unit);
         ensure_workspace(c, ((size_t)n * ncols * 2 + n * n) * 16 + ((size_t)64 << 20));
         c->ws_top = 0;
         Fp f = make_field(c, p);
-        DMat C = upload_matrix(c, f, cc, n, ncols, 8), T = upload_matrix(c, f, o.data(), n, n, 8),
+        DMat C = upload_matrix(c, f, cc, n, ncols, 8), T = upload_matrix(c, f, t, n, n, 8),
              B = upload_matrix(c, f, b, n, ncols, 8);
-        gemm(f, c->stream, GEMM_SUB, C, T, false, B, false, n, ncols, n);
+        DMat O = ws_mat(c, n, n);  // op(T) with its triangle / unit conventions (kernels.cpp:23-29)
+        tri_dense(f, c->stream, O, T, upper != 0, trans != 0, unit != 0, false, nullptr);
+        gemm(f, c->stream, GEMM_SUB, C, O, false, B, false, n, ncols, n);
         download_matrix(c, C, cc);
         c->ws_top = 0;
     });
@@ -1391,79 +1377,164 @@ int ffb_trsm_inplace(ffb_context* c, uint64_t p, size_t n, size_t ncols, const u
                      int trans, int unit, uint64_t* b) {
     return guarded(c, [&] {
         check_modulus(p);
-        std::vector<uint64_t> o = dense_op(t, n, p, upper, trans, unit);
-        const bool lower = (upper == 0) != (trans != 0);
-        // kernels.cpp:64-71: the first zero pivot met in solve order raises
-        if (!unit)
-            for (size_t s = 0; s < n; ++s) {
-                const size_t i = lower ? s : n - 1 - s;
-                if (o[i * n + i] == 0) throw Status(FFB_SINGULAR_TRIANGULAR, "trsm_inplace: zero diagonal");
-            }
-        if (n == 0 || ncols == 0) return;
-        // Normalize to a unit lower solve: reverse the index order for upper,
-        // scale rows by the inverse diagonal for non-unit.
-        std::vector<uint64_t> L(n * n, 0), Bv(n * ncols);
-        std::vector<uint64_t> dinv(n, 1);
-        for (size_t i = 0; i < n; ++i) {
-            const uint64_t d = o[i * n + i];
-            dinv[i] = unit ? 1 : finv_euclid((uint32_t)p, (uint32_t)d);
-        }
-        auto idx = [&](size_t i) { return lower ? i : n - 1 - i; };
-        for (size_t i = 0; i < n; ++i) {
-            for (size_t k = 0; k < n; ++k)
-                L[i * n + k] = (k < i) ? (uint64_t)(((unsigned __int128)o[idx(i) * n + idx(k)] * dinv[idx(i)]) % p) : (k == i ? 1 : 0);
-            for (size_t j = 0; j < ncols; ++j)
-                Bv[i * ncols + j] = (uint64_t)(((unsigned __int128)(b[idx(i) * ncols + j] % p) * dinv[idx(i)]) % p);
-        }
-        ensure_workspace(c, ((size_t)n * ncols + n * n) * 16 + ((size_t)64 << 20));
+        ensure_workspace(c, ((size_t)n * ncols * 2 + n * n * 2) * 16 + ((size_t)64 << 20));
         c->ws_top = 0;
         Fp f = make_field(c, p);
-        DMat Ld = upload_matrix(c, f, L.data(), n, n, 8), Bd = upload_matrix(c, f, Bv.data(), n, ncols, 8);
-        trsm_lower_unit(f, c->stream, Ld, Bd);
-        download_matrix(c, Bd, Bv.data());
-        for (size_t i = 0; i < n; ++i)
-            for (size_t j = 0; j < ncols; ++j) b[idx(i) * ncols + j] = Bv[i * ncols + j];
+        DMat T = upload_matrix(c, f, t, n, n, 8);
+        // kernels.cpp:64-71: a zero pivot raises (before any row of B is written here)
+        const uint32_t* dinv = nullptr;
+        if (!unit && n > 0) {
+            uint32_t* diag = ws_vec<uint32_t>(c, (int64_t)n);
+            uint32_t* inv = ws_vec<uint32_t>(c, (int64_t)n);
+            fill_words(c->stream, (uint32_t*)c->flag, 1, 0u);
+            tri_diag(c->stream, T, diag, c->flag);
+            if (*(const int32_t*)readback(c, c->flag, sizeof(int32_t)))
+                throw Status(FFB_SINGULAR_TRIANGULAR, "trsm_inplace: zero diagonal");
+            invert_vec(f, c->stream, inv, diag, (int64_t)n);
+            dinv = inv;
+        }
+        if (n == 0 || ncols == 0) return;
+        DMat B = upload_matrix(c, f, b, n, ncols, 8);
+        // Normalise to a unit lower solve on the device: reverse the index order for an
+        // effective-upper op(T), scale rows by the inverse diagonal when non-unit.
+        const bool lower = (upper == 0) != (trans != 0);
+        DMat L = ws_mat(c, n, n), X = ws_mat(c, n, ncols);
+        tri_dense(f, c->stream, L, T, upper != 0, trans != 0, unit != 0, !lower, dinv);
+        rows_rev_scaled(f, c->stream, X, B, !lower, dinv);
+        trsm_lower_unit(f, c->stream, L, X);
+        rows_rev_scaled(f, c->stream, B, X, !lower, nullptr);
+        download_matrix(c, B, b);
         c->ws_top = 0;
     });
+}
+
+// C -= G D G^T with D given per column (kind/val/val2); shared by both syrdk_sub overloads.
+static void syrdk_columns(ffb_context* c, uint64_t p, size_t n, size_t k, uint64_t* cc, const uint64_t* g,
+                          const std::vector<int32_t>& kind, const uint64_t* dval, const uint64_t* dval2) {
+    ensure_workspace(c, ((size_t)n * n + 2 * n * k + 2 * k) * 16 + ((size_t)64 << 20));
+    c->ws_top = 0;
+    Fp f = make_field(c, p);
+    DMat C = upload_matrix(c, f, cc, n, n, 8), G = upload_matrix(c, f, g, n, k, 8);
+    DMat V = upload_matrix(c, f, dval, 1, k, 8);
+    DMat V2 = dval2 ? upload_matrix(c, f, dval2, 1, k, 8) : V;
+    const int32_t* kd = upload(c, kind);
+    DMat H = ws_mat(c, n, k);
+    apply_d(f, c->stream, H, G, kd, V.ptr, V2.ptr);  // H = G D
+    gemm(f, c->stream, GEMM_SUB, C, H, false, G, true, n, n, k);
+    download_matrix(c, C, cc);
+    c->ws_top = 0;
 }
 
 int ffb_syrdk_sub(ffb_context* c, uint64_t p, size_t n, size_t k, uint64_t* cc, const uint64_t* g,
                   const int32_t* dkind, const uint64_t* dval, const uint64_t* dval2) {
     return guarded(c, [&] {
         check_modulus(p);
-        ensure_workspace(c, ((size_t)n * n + 2 * n * k) * 16 + ((size_t)64 << 20));
+        std::vector<int32_t> kind(dkind, dkind + k);
+        for (size_t t = 0; t < k; ++t) {  // per-column encoding must describe whole blocks
+            const int32_t kk = kind[t];
+            const bool ok = kk == FFB_D_SCALAR ||
+                            ((kk == FFB_D_ANTIDIAG_HEAD || kk == FFB_D_ANTITRI_HEAD) && t + 1 < k && kind[t + 1] == kk + 1) ||
+                            ((kk == FFB_D_ANTIDIAG_TAIL || kk == FFB_D_ANTITRI_TAIL) && t > 0 && kind[t - 1] == kk - 1);
+            if (!ok) throw Status(FFB_DIMENSION_MISMATCH, "syrdk_sub: malformed block diagonal");
+        }
+        syrdk_columns(c, p, n, k, cc, g, kind, dval, dval2);
+    });
+}
+
+int ffb_syrdk_sub_diag(ffb_context* c, uint64_t p, size_t n, size_t k, uint64_t* cc, const uint64_t* g,
+                       const uint64_t* d) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        syrdk_columns(c, p, n, k, cc, g, std::vector<int32_t>(k, FFB_D_SCALAR), d, nullptr);
+    });
+}
+
+// strictify on a device factorization: heads of the AntiTri blocks from the kind array
+static void strictify_dev(ffb_context* c, const Fp& f, int64_t n, int64_t r, int32_t* perm, DMat L, DDiag D,
+                          uint64_t* blocks_converted, uint64_t* entries_touched) {
+    std::vector<int32_t> kind(std::max<int64_t>(r, 1));
+    if (r > 0) {
+        FFB_CUDA(cudaMemcpyAsync(kind.data(), D.kind, r * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        pdl_fence(c->stream);
+        FFB_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    std::vector<int32_t> heads;
+    for (int64_t t = 0; t < r; ++t)
+        if (kind[t] == FFB_D_ANTITRI_HEAD) heads.push_back((int32_t)t);
+    if (!heads.empty() && !f.char2)
+        throw Status(FFB_WRONG_CHARACTERISTIC, "strictify: AntiTri block over odd characteristic");
+    unsigned long long* touched = (unsigned long long*)ws_vec<uint64_t>(c, 1);
+    FFB_CUDA(cudaMemsetAsync(touched, 0, sizeof(uint64_t), c->stream));
+    pdl_fence(c->stream);
+    const int64_t nb = (int64_t)heads.size();
+    if (nb) {
+        const int32_t* dh = upload(c, heads);
+        uint32_t* scratch = ws_vec<uint32_t>(c, 4 * nb);
+        strictify_device(f, c->stream, L, n, dh, nb, perm, D, scratch, touched);
+    }
+    const uint64_t tt = *(const uint64_t*)readback(c, touched, sizeof(uint64_t));
+    if (blocks_converted) *blocks_converted = (uint64_t)nb;
+    if (entries_touched) *entries_touched = tt;
+}
+
+int ffb_strictify_device(ffb_context* c, uint64_t p, size_t n, size_t rank, int32_t* d_perm, uint32_t* d_lower,
+                         size_t ldl, int32_t* d_dkind, uint32_t* d_dval, uint32_t* d_dval2,
+                         uint64_t* blocks_converted, uint64_t* entries_touched) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        if (rank > n) throw Status(FFB_DIMENSION_MISMATCH, "strictify: rank exceeds n");
+        ensure_workspace(c, (size_t)n * 64 + ((size_t)64 << 20));
         c->ws_top = 0;
         Fp f = make_field(c, p);
-        DMat C = upload_matrix(c, f, cc, n, n, 8), G = upload_matrix(c, f, g, n, k, 8);
-        // D in the per-column encoding -> device arrays (inverse of val per column)
-        std::vector<int32_t> kk(k);
-        std::vector<uint64_t> v(k), v2(k), vi(k);
-        for (size_t t = 0; t < k; ++t) {
-            kk[t] = dkind[t];
-            v[t] = dval[t] % p;
-            v2[t] = dval2[t] % p;
-            if (v[t] == 0) throw Status(FFB_ZERO_INVERSE, "inverse of zero");
-            vi[t] = finv_euclid((uint32_t)p, (uint32_t)v[t]);
+        DMat L;
+        L.ptr = d_lower;
+        L.ld = (int64_t)ldl;
+        L.rows = (int64_t)n;
+        L.cols = (int64_t)rank;
+        DDiag D{d_dkind, d_dval, d_dval2, nullptr};
+        strictify_dev(c, f, (int64_t)n, (int64_t)rank, d_perm, L, D, blocks_converted, entries_touched);
+        c->ws_top = 0;
+    });
+}
+
+int ffb_strictify(ffb_context* c, uint64_t p, size_t n, size_t rank, int64_t* perm, uint64_t* lower,
+                  int32_t* dkind, uint64_t* dval, uint64_t* dval2, uint64_t* blocks_converted,
+                  uint64_t* entries_touched) {
+    return guarded(c, [&] {
+        check_modulus(p);
+        if (rank > n) throw Status(FFB_DIMENSION_MISMATCH, "strictify: rank exceeds n");
+        const int64_t N = (int64_t)n, R = (int64_t)rank;
+        ensure_workspace(c, (size_t)N * std::max<int64_t>(R, 1) * 16 + (size_t)N * 64 + ((size_t)64 << 20));
+        c->ws_top = 0;
+        Fp f = make_field(c, p);
+        DMat L = upload_matrix(c, f, lower, N, R, 8);
+        std::vector<int32_t> pv(perm, perm + N), kd(dkind, dkind + R);
+        int32_t* dperm = ws_vec<int32_t>(c, N);
+        int32_t* dk = ws_vec<int32_t>(c, R);
+        FFB_CUDA(cudaMemcpyAsync(dperm, upload(c, pv), N * sizeof(int32_t), cudaMemcpyDeviceToDevice, c->stream));
+        FFB_CUDA(cudaMemcpyAsync(dk, upload(c, kd), std::max<int64_t>(R, 1) * sizeof(int32_t),
+                                 cudaMemcpyDeviceToDevice, c->stream));
+        pdl_fence(c->stream);
+        DMat V = upload_matrix(c, f, dval, 1, R, 8), V2 = upload_matrix(c, f, dval2, 1, R, 8);
+        DDiag D{dk, V.ptr, V2.ptr, nullptr};
+        strictify_dev(c, f, N, R, dperm, L, D, blocks_converted, entries_touched);
+        download_matrix(c, L, lower);
+        std::vector<int32_t> pout(std::max<int64_t>(N, 1)), kout(std::max<int64_t>(R, 1));
+        std::vector<uint32_t> v(std::max<int64_t>(R, 1)), v2(std::max<int64_t>(R, 1));
+        FFB_CUDA(cudaMemcpyAsync(pout.data(), dperm, N * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        if (R > 0) {
+            FFB_CUDA(cudaMemcpyAsync(kout.data(), dk, R * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+            FFB_CUDA(cudaMemcpyAsync(v.data(), V.ptr, R * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+            FFB_CUDA(cudaMemcpyAsync(v2.data(), V2.ptr, R * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
         }
-        // C -= G D G^T = G (D G^T): H^T = D G^T computed as (G D^T)... use H = G*D
-        // (D symmetric), then C -= H G^T.
-        std::vector<uint64_t> hg(n * k), hgv(n * k);
-        std::vector<uint64_t> gh(n * k);
-        download_matrix(c, G, gh.data());
-        for (size_t i = 0; i < n; ++i)
-            for (size_t t = 0; t < k; ++t) {
-                const uint64_t* row = &gh[i * k];
-                uint64_t val;
-                if (kk[t] == FFB_D_SCALAR) val = (uint64_t)(((unsigned __int128)row[t] * v[t]) % p);
-                else if (kk[t] == FFB_D_ANTIDIAG_HEAD || kk[t] == FFB_D_ANTITRI_HEAD)
-                    val = (uint64_t)(((unsigned __int128)row[t + 1] * v[t]) % p);
-                else if (kk[t] == FFB_D_ANTIDIAG_TAIL) val = (uint64_t)(((unsigned __int128)row[t - 1] * v[t]) % p);
-                else val = (uint64_t)((((unsigned __int128)row[t - 1] * v[t]) + (unsigned __int128)row[t] * v2[t]) % p);
-                hg[i * k + t] = val;
-            }
-        DMat H = upload_matrix(c, f, hg.data(), n, k, 8);
-        gemm(f, c->stream, GEMM_SUB, C, H, false, G, true, n, n, k);
-        download_matrix(c, C, cc);
+        pdl_fence(c->stream);
+        FFB_CUDA(cudaStreamSynchronize(c->stream));
+        for (int64_t i = 0; i < N; ++i) perm[i] = pout[i];
+        for (int64_t t = 0; t < R; ++t) {
+            dkind[t] = kout[t];
+            dval[t] = v[t];
+            dval2[t] = v2[t];
+        }
         c->ws_top = 0;
     });
 }

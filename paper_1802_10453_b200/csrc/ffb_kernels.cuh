@@ -167,6 +167,23 @@ bool node128_supported(const Fp& f, int64_t s, int64_t T);
 void node128(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, int64_t coff, DDiag D,
              uint32_t* yout, int32_t* out, const MboxPost& mp);
 
+// Secondary C-ABI entry points (ffb_api.cu).
+// out (n x n) = op(T)(a_i, a_k) with a_i = n-1-i when rev; with dinv the unit-lower
+// normalisation dinv(a_i) op(T)(a_i, a_k) below the diagonal (kernels.cpp:23-29,57-81).
+void tri_dense(const Fp& f, cudaStream_t st, DMat out, DMat T, bool upper, bool trans, bool unit, bool rev,
+               const uint32_t* dinv);
+// diag[i] = T(i, i); *flag |= 1 when one is zero
+void tri_diag(cudaStream_t st, DMat T, uint32_t* diag, int32_t* flag);
+// dst(i, :) = src(a_i, :) * dinv(a_i) (dinv may be null: no scaling)
+void rows_rev_scaled(const Fp& f, cudaStream_t st, DMat dst, DMat src, bool rev, const uint32_t* dinv);
+// H = G D for a per-column BlockDiag encoding (kind/val/val2)
+void apply_d(const Fp& f, cudaStream_t st, DMat H, DMat G, const int32_t* kind, const uint32_t* val,
+             const uint32_t* val2);
+// strictify (rpmtools.cpp:74-132) of the AntiTri blocks with head columns heads[0..nb) on a
+// device factorization (L n x r, perm, D); scratch >= 4 nb words; *touched += entries written
+void strictify_device(const Fp& f, cudaStream_t st, DMat L, int64_t n, const int32_t* heads, int64_t nb,
+                      int32_t* perm, DDiag D, uint32_t* scratch, unsigned long long* touched);
+
 // PLDUQ (plduq.cpp:36-123) of W (m x n, destroyed).  Outputs: info[0] = r,
 // info[1..m] row_image, info[1+m..1+m+n] col_image, pc[r] in info after that;
 // Lo (m x min(m,n)) = [L1;M1], d (r), Uo (min(m,n) x n) = [U1 V1].

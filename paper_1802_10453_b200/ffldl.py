@@ -53,12 +53,13 @@ class CharTwoNonzeroDiagonal(Error): pass
 class NoMemory(Error): pass
 class CudaError(Error): pass
 class Unsupported(Error): pass
+class WrongCharacteristic(Error): pass
 
 
 _STATUS = {
     1: DimensionMismatch, 2: NotSymmetric, 3: NotPrime, 4: ZeroInverse, 5: CharTwoDivision,
     6: NonUnitTriangular, 7: SingularTriangular, 8: CharTwoNonzeroDiagonal, 9: BadBlockSizes,
-    10: Error, 11: NoMemory, 12: CudaError, 13: Unsupported,
+    10: Error, 11: NoMemory, 12: CudaError, 13: Unsupported, 14: WrongCharacteristic,
 }
 
 
@@ -559,17 +560,53 @@ def trsm_inplace(t, uplo: Uplo, trans: bool, unit: bool, b, field: FieldLike,
     return b
 
 
-def syrdk_sub(c, g, d: BlockDiag, field: FieldLike, ctx: Optional[Context] = None) -> np.ndarray:
-    """C - G*D*G^T (kernels.hpp:26)."""
+def syrdk_sub(c, g, d, field: FieldLike, ctx: Optional[Context] = None) -> np.ndarray:
+    """C - G*D*G^T with D a BlockDiag (kernels.hpp:26) or a sequence of field elements
+    (the std::span overload, kernels.hpp:29, kernels.cpp:108-119)."""
     p = _p(field)
     c, g = _u64(c).copy(), _u64(g)
-    if c.shape[0] != c.shape[1] or g.shape[0] != c.shape[0] or g.shape[1] != d.order():
-        raise DimensionMismatch("syrdk_sub: incompatible shapes")
-    kind, val, val2 = d.columns()
     ctx = ctx or default_context()
-    _check(lib().ffb_syrdk_sub(ctx.handle, p, c.shape[0], g.shape[1], _ptr(c), _ptr(g), _ptr(kind),
-                               _ptr(val), _ptr(val2)))
+    if isinstance(d, BlockDiag):
+        if c.shape[0] != c.shape[1] or g.shape[0] != c.shape[0] or g.shape[1] != d.order():
+            raise DimensionMismatch("syrdk_sub: incompatible shapes")
+        kind, val, val2 = d.columns()
+        _check(lib().ffb_syrdk_sub(ctx.handle, p, c.shape[0], g.shape[1], _ptr(c), _ptr(g),
+                                   _ptr(kind), _ptr(val), _ptr(val2)))
+        return c
+    dv = _u64(np.asarray(d, dtype=np.uint64).reshape(-1))
+    if c.shape[0] != c.shape[1] or g.shape[0] != c.shape[0] or g.shape[1] != dv.shape[0]:
+        raise DimensionMismatch("syrdk_sub: incompatible shapes")
+    _check(lib().ffb_syrdk_sub_diag(ctx.handle, p, c.shape[0], g.shape[1], _ptr(c), _ptr(g), _ptr(dv)))
     return c
+
+
+@dataclass
+class StrictifyStats:
+    """rpmtools.hpp:27-30."""
+    blocks_converted: int = 0
+    entries_touched: int = 0
+
+
+def strictify(f: Factorization, stats: Optional[StrictifyStats] = None,
+              ctx: Optional[Context] = None) -> Factorization:
+    """Rewrite every characteristic-2 AntiTri block of f into two scalar pivots, in place
+    (rpmtools.hpp:39, rpmtools.cpp:74-132); the arithmetic runs on the device.  Returns f."""
+    ctx = ctx or default_context()
+    n, r = f.dimension(), f.rank
+    perm = np.ascontiguousarray(f.perm.image_array(), np.int64)
+    lower = _u64(f.lower[:, :r]).copy()
+    kind, val, val2 = f.diag.columns()
+    kind = np.ascontiguousarray(kind, np.int32).copy()
+    val, val2 = _u64(val).copy(), _u64(val2).copy()
+    bc, et = C.c_uint64(0), C.c_uint64(0)
+    _check(lib().ffb_strictify(ctx.handle, f.p, n, r, _ptr(perm), _ptr(lower), _ptr(kind),
+                               _ptr(val), _ptr(val2), C.byref(bc), C.byref(et)))
+    f.perm = Permutation.from_image(perm)
+    f.lower = lower
+    f.diag = BlockDiag.from_columns(kind, val, val2)
+    if stats is not None:
+        stats.blocks_converted, stats.entries_touched = int(bc.value), int(et.value)
+    return f
 
 
 def syr2k_sub(c, a, b, field: FieldLike, ctx: Optional[Context] = None) -> np.ndarray:

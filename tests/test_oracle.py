@@ -237,3 +237,35 @@ def test_fullsize_golden_small_configs(oracle):
             assert d[k] == g[k], (c, k)
     for c in (1, 2, 3, 4, 5):
         assert str(c) in gold, f"config {c} missing from fullsize.json"
+
+
+def test_oracle_strictify_and_syrdk_diag_vs_reference(oracle, ref):
+    """strictify (rpmtools.cpp:74-132) and syrdk_sub(span) (kernels.cpp:108-119): the C
+    restatement equals the unmodified reference, including its StrictifyStats and the
+    WrongCharacteristic refusal over odd p."""
+    rng = np.random.default_rng(71)
+    hits = 0
+    for n in (2, 5, 16, 40, 97):
+        for a in (hollow(rng, 2, n), rand_sym(rng, 2, n), rand_rook_rpm(rng, 2, n, n // 2)):
+            f = oracle.ldlt(2, a)
+            hits += int(np.any(f.dkind == 3))
+            go, so = oracle.strictify(2, f)
+            gr, sr = ref.strictify(2, f)
+            assert go.same_as(gr) and so == sr, n
+    assert hits > 3
+    f = oracle.ldlt(3, hollow(rng, 3, 30))
+    assert oracle.strictify(3, f)[1][0] == 0
+    g = oracle.ldlt(2, hollow(rng, 2, 30))
+    bad = type(g)(g.perm, g.lower, g.dkind, g.dval, g.dval2, g.rank)
+    if np.any(g.dkind == 3):
+        with pytest.raises(CheckerError) as e:
+            oracle.strictify(3, bad)
+        assert e.value.name == "WrongCharacteristic"
+        with pytest.raises(CheckerError):
+            ref.strictify(3, bad)
+    for p in (2, 131, 8388593):
+        for n, k in ((1, 1), (7, 3), (40, 33)):
+            c = rand_sym(rng, p, n)
+            g = rng.integers(0, p, (n, k), dtype=np.uint64)
+            d = rng.integers(0, p, k, dtype=np.uint64)
+            assert np.array_equal(oracle.syrdk_sub_diag(p, c, g, d), ref.syrdk_sub_diag(p, c, g, d))

@@ -499,3 +499,78 @@ def test_two_devices_one_thread():
         if want is None:
             want = g
         assert g.rank == want.rank and np.array_equal(g.lower, want.lower)
+
+
+def test_secondary_kernels_on_device(gpu, oracle):
+    """trsm_inplace / trmm_sub / syrdk_sub build their triangular or block-diagonal operand on
+    the device (ffb_api.cu); larger solves take the recursive panel path; a zero pivot raises
+    SingularTriangular (kernels.cpp:64-71); the span overload of syrdk_sub
+    (kernels.cpp:108-119) matches the oracle."""
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(17)
+    for p in (2, 131, 8388593):
+        for n in (1, 300, 513):
+            t = rng.integers(0, p, (n, n), dtype=np.uint64)
+            t[np.diag_indices(n)] = rng.integers(1, p, n).astype(np.uint64)
+            bb = rng.integers(0, p, (n, 37), dtype=np.uint64)
+            for up, tr, un in itertools.product((0, 1), repeat=3):
+                assert np.array_equal(ffb.trsm_inplace(t, up, tr, un, bb, p, ctx=gpu),
+                                      oracle.trsm_inplace(p, t, up, tr, un, bb)), (p, n, up, tr, un)
+        t[3 % n, 3 % n] = 0
+        with pytest.raises(ffb.SingularTriangular):
+            ffb.trsm_inplace(t, 0, 0, 0, bb, p, ctx=gpu)
+        ffb.trsm_inplace(t, 0, 0, 1, bb, p, ctx=gpu)  # unit: the diagonal is not read
+        for n, k in ((1, 1), (20, 6), (300, 129)):
+            c = rand_sym(rng, p, n)
+            g = rng.integers(0, p, (n, k), dtype=np.uint64)
+            d = rng.integers(0, p, k, dtype=np.uint64)
+            assert np.array_equal(ffb.syrdk_sub(c, g, list(d), p, ctx=gpu),
+                                  oracle.syrdk_sub_diag(p, c, g, d))
+
+
+def test_strictify_matches_oracle(gpu, oracle):
+    """strictify (rpmtools.cpp:74-132) on the device: host API on ldlt outputs and the
+    device API on ldlt_device outputs, against the oracle (itself pinned to the unmodified
+    reference in test_oracle.py), stats included; WrongCharacteristic over odd p."""
+    import torch
+    import ctypes as C
+    import paper_1802_10453_b200 as ffb
+    from oracle.bind import Fact
+    from paper_1802_10453_b200._lib import lib
+    from paper_1802_10453_b200.device import ldlt_device
+    rng = np.random.default_rng(23)
+    seen = 0
+    for n in (2, 17, 64, 130, 301):
+        for a in (hollow(rng, 2, n), rand_rook_rpm(rng, 2, n, n // 2), rand_sym(rng, 2, n)):
+            g = ffb.ldlt(a, 2, ctx=gpu)
+            o = oracle.ldlt(2, a)
+            want, (nb, nt) = oracle.strictify(2, o)
+            seen += nb
+            st = ffb.StrictifyStats()
+            ffb.strictify(g, st, ctx=gpu)
+            kind, val, val2 = g.diag.columns()
+            assert (st.blocks_converted, st.entries_touched) == (nb, nt)
+            assert np.array_equal(g.perm.image_array(), want.perm) and np.array_equal(g.lower, want.lower)
+            assert np.array_equal(kind, want.dkind) and np.array_equal(val, want.dval)
+            assert np.array_equal(val2, want.dval2)
+    assert seen > 5
+    n = 2048
+    a = hollow(rng, 2, n)
+    f = ldlt_device(torch.from_numpy(a.astype(np.int32)).cuda(), 2, ctx=gpu)
+    o = oracle.ldlt(2, a)
+    want, (nb, nt) = oracle.strictify(2, o)
+    bc, et = C.c_uint64(0), C.c_uint64(0)
+    assert lib().ffb_strictify_device(gpu.handle, 2, n, f.rank, f.perm.data_ptr(), f.lower.data_ptr(),
+                                      f.lower.stride(0), f.dkind.data_ptr(), f.dval.data_ptr(),
+                                      f.dval2.data_ptr(), C.byref(bc), C.byref(et)) == 0
+    r = f.rank
+    assert (bc.value, et.value) == (nb, nt) and nb > 0
+    assert np.array_equal(f.perm.cpu().numpy(), want.perm)
+    assert np.array_equal(f.lower[:, :r].cpu().numpy().astype(np.uint64), want.lower)
+    assert np.array_equal(f.dkind[:r].cpu().numpy(), want.dkind)
+    assert np.array_equal(f.dval[:r].cpu().numpy().astype(np.uint64), want.dval)
+    g = ffb.ldlt(hollow(rng, 2, 40), 2, ctx=gpu)
+    if g.diag.has_antitriangular():
+        g.p = 3
+        with pytest.raises(ffb.WrongCharacteristic):
+            ffb.strictify(g, ctx=gpu)
