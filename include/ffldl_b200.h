@@ -50,6 +50,7 @@ extern "C" {
 #define FFB_CUDA_ERROR 12            /* CUDA runtime failure (new) */
 #define FFB_UNSUPPORTED 13           /* modulus outside the device range (new) */
 #define FFB_WRONG_CHARACTERISTIC 14  /* ffldl::WrongCharacteristic (strictify) */
+#define FFB_PARSE_ERROR 15           /* ffldl::ParseError (matrix / factorization files) */
 
 #define FFB_VARIANT_RECURSIVE 0
 #define FFB_VARIANT_CROUT 1
@@ -186,6 +187,22 @@ int ffb_strictify_device(ffb_context* ctx, uint64_t p, size_t n, size_t rank, in
 int ffb_gemm_device(ffb_context* ctx, uint64_t p, int mode, size_t m, size_t n, size_t k,
                     uint32_t* d_c, size_t ldc, const uint32_t* d_a, size_t lda, int ta,
                     const uint32_t* d_b, size_t ldb, int tb);
+
+/* Matrix and factorization files: MatrixFile / FactorizationFile,
+ * proj/include/ffldl/io.hpp:22-62, proj/src/io.cpp:39-222.  Readers accept the reference's
+ * text format (byte-compatible) and a checksummed binary format (binary != 0 on write; see
+ * csrc/ffb_io.cu).  Read with NULL arrays first to get the dimensions, then again with
+ * caller-sized buffers (values rows*cols; perm n, lower n*rank, dkind/dval/dval2 rank) in
+ * the element type given.  Parse failures return FFB_PARSE_ERROR (ffldl::ParseError). */
+int ffb_matrix_read(const char* path, uint64_t* rows, uint64_t* cols, uint64_t* modulus, int* symmetric,
+                    void* values, int elem_type);
+int ffb_matrix_write(const char* path, int binary, uint64_t rows, uint64_t cols, uint64_t modulus,
+                     int symmetric, const void* values, int elem_type);
+int ffb_factorization_read(const char* path, uint64_t* n, uint64_t* modulus, uint64_t* rank, int64_t* perm,
+                           void* lower, int lower_type, int32_t* dkind, uint64_t* dval, uint64_t* dval2);
+int ffb_factorization_write(const char* path, int binary, uint64_t n, uint64_t modulus, uint64_t rank,
+                            const int64_t* perm, const void* lower, int lower_type, const int32_t* dkind,
+                            const uint64_t* dval, const uint64_t* dval2);
 
 /* Seeded counter-based generators of the benchmark configurations
  * (BASELINE.json configs 1..5).  Host version

@@ -231,6 +231,18 @@ class Checker:
                                                  _ptr(out)))
         return out[:n]
 
+    def file_reemit(self, kind: int, src: str, dst: str) -> None:
+        """Reference only: parse `src` (0 MatrixFile, 1 FactorizationFile) and emit to dst."""
+        self._check(self._fn("file_reemit")(C.c_int(kind), src.encode(), dst.encode()))
+
+    def factorization_emit(self, p, f: "Fact", dst: str) -> None:
+        """Reference only: FactorizationFile::from(f).emit into dst."""
+        n = f.perm.shape[0]
+        self._check(self._fn("factorization_emit")(
+            C.c_uint64(p), C.c_size_t(n), C.c_size_t(f.rank), _ptr(np.ascontiguousarray(f.perm, np.int64)),
+            _ptr(_u64(f.lower)), _ptr(np.ascontiguousarray(f.dkind, np.int32)), _ptr(_u64(f.dval)),
+            _ptr(_u64(f.dval2)), dst.encode()))
+
     def rank_profile(self, p, a) -> np.ndarray:
         """Brute-force RPM (reference only: rpmtools.cpp:43-59)."""
         a = _u64(a)

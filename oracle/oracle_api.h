@@ -43,6 +43,7 @@
 #define ORC_OTHER 10
 #define ORC_NO_MEMORY 11
 #define ORC_WRONG_CHARACTERISTIC 12
+#define ORC_PARSE_ERROR 13
 
 #define ORC_VARIANT_RECURSIVE 0
 #define ORC_VARIANT_CROUT 1

@@ -10,11 +10,14 @@
 
 #include <cstdint>
 #include <cstring>
+#include <fstream>
+#include <sstream>
 #include <span>
 #include <variant>
 #include <vector>
 
 #include "ffldl/errors.hpp"
+#include "ffldl/io.hpp"
 #include "ffldl/kernels.hpp"
 #include "ffldl/plduq.hpp"
 #include "ffldl/rpmtools.hpp"
@@ -103,6 +106,8 @@ int guarded(F&& fn) {
         return ORC_BAD_BLOCK_SIZES;
     } catch (const WrongCharacteristic&) {
         return ORC_WRONG_CHARACTERISTIC;
+    } catch (const ParseError&) {
+        return ORC_PARSE_ERROR;
     } catch (const std::bad_alloc&) {
         return ORC_NO_MEMORY;
     } catch (...) {
@@ -265,6 +270,36 @@ int ref_rank_profile(uint64_t p, size_t m, size_t n, const uint64_t* a, uint64_t
     return guarded([&] {
         const PrimeField f(p);
         from_matrix(rank_profile_bruteforce(to_matrix(f, m, n, a)), out);
+    });
+}
+
+// Files (io.cpp): the reference parses `in` (MatrixFile or FactorizationFile, by `kind`
+// 0/1) and emits it again to `out` -- so a file written by the B200 library can be checked
+// byte for byte against the reference's own emit, and read by the reference's parser.
+int ref_file_reemit(int kind, const char* in, const char* out) {
+    return guarded([&] {
+        std::ifstream is(in, std::ios::binary);
+        if (!is) throw ParseError("cannot open input");
+        std::ostringstream os;
+        if (kind == 0) MatrixFile::parse(is).emit(os);
+        else FactorizationFile::parse(is).emit(os);
+        std::ofstream o(out, std::ios::binary);
+        o << os.str();
+    });
+}
+
+// FactorizationFile::from(f).emit of a flat factorization (the reference's writer).
+int ref_factorization_emit(uint64_t p, size_t n, size_t r, const int64_t* perm, const uint64_t* lower,
+                           const int32_t* dkind, const uint64_t* dval, const uint64_t* dval2,
+                           const char* out) {
+    return guarded([&] {
+        const PrimeField f(p);
+        std::vector<std::size_t> img(n);
+        for (size_t i = 0; i < n; ++i) img[i] = static_cast<std::size_t>(perm[i]);
+        const Factorization fac{Permutation::from_image(std::move(img)), to_matrix(f, n, r, lower),
+                                to_blockdiag(f, r, dkind, dval, dval2), r};
+        std::ofstream o(out, std::ios::binary);
+        FactorizationFile::from(fac).emit(o);
     });
 }
 

@@ -11,6 +11,7 @@ from .ffldl import (AntiDiagBlock, AntiTriBlock, BadBlockSizes, BlockDiag, CharT
                     Permutation, PlduqFactorization, PrimeField, ScalarBlock, SingularTriangular,
                     StrictifyStats, SytrfConfig, Unsupported, Uplo, Variant, ZeroInverse, default_context,
                     gemm_sub, ldlt, ldlt_zero_leading, plduq, syr2k_sub, syrdk_sub, trmm_sub,
-                    trsm_inplace, trssyr2k, strictify, WrongCharacteristic)
+                    trsm_inplace, trssyr2k, strictify, WrongCharacteristic, ParseError,
+                    read_factorization, read_matrix, write_factorization, write_matrix)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

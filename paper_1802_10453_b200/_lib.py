@@ -21,7 +21,8 @@ EXPORTS = [
     "ffb_ldlt", "ffb_ldlt_compact", "ffb_ldlt_zero_leading",
     "ffb_ldlt_device", "ffb_plduq", "ffb_trssyr2k", "ffb_gemm_sub", "ffb_trmm_sub",
     "ffb_trsm_inplace", "ffb_syrdk_sub", "ffb_syrdk_sub_diag", "ffb_syr2k_sub", "ffb_strictify",
-    "ffb_strictify_device", "ffb_gemm_device", "ffb_generate_host",
+    "ffb_strictify_device", "ffb_matrix_read", "ffb_matrix_write", "ffb_factorization_read",
+    "ffb_factorization_write", "ffb_gemm_device", "ffb_generate_host",
     "ffb_generate_device", "ffb_config5_partners", "ffb_verify_device", "ffb_pivoting_partners_device",
 ]
 
@@ -54,6 +55,11 @@ _SIGS = {
     "ffb_syrdk_sub": (I, [P, U64, SZ, SZ, P, P, P, P, P]),
     "ffb_syr2k_sub": (I, [P, U64, SZ, SZ, P, P, P]),
     "ffb_syrdk_sub_diag": (I, [P, U64, SZ, SZ, P, P, P]),
+    "ffb_matrix_read": (I, [C.c_char_p, C.POINTER(U64), C.POINTER(U64), C.POINTER(U64), C.POINTER(I), P, I]),
+    "ffb_matrix_write": (I, [C.c_char_p, I, U64, U64, U64, I, P, I]),
+    "ffb_factorization_read": (I, [C.c_char_p, C.POINTER(U64), C.POINTER(U64), C.POINTER(U64), P, P, I, P, P,
+                                   P]),
+    "ffb_factorization_write": (I, [C.c_char_p, I, U64, U64, U64, P, P, I, P, P, P]),
     "ffb_strictify": (I, [P, U64, SZ, SZ, P, P, P, P, P, C.POINTER(U64), C.POINTER(U64)]),
     "ffb_strictify_device": (I, [P, U64, SZ, SZ, P, P, SZ, P, P, P, C.POINTER(U64), C.POINTER(U64)]),
     "ffb_gemm_device": (I, [P, U64, I, SZ, SZ, SZ, P, SZ, P, SZ, I, P, SZ, I]),

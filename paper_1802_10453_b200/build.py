@@ -29,11 +29,27 @@ def headers() -> list[str]:
     return sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(HERE, "..", "include", "*.h")))
 
 
+CLI_SRC = os.path.join(HERE, "cli", "ffldl_b200_main.cpp")
+CLI = os.path.join(HERE, "ffldl_b200")
+CUDA_HOME = os.path.dirname(os.path.dirname(NVCC))
+
+
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    if not os.path.exists(LIB) or not os.path.exists(CLI):
         return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(s) <= t for s in sources() + headers())
+    t = min(os.path.getmtime(LIB), os.path.getmtime(CLI))
+    return all(os.path.getmtime(s) <= t for s in sources() + headers() + [CLI_SRC])
+
+
+def build_cli() -> str:
+    """The command line front end (cli/ffldl_b200_main.cpp) linked against the library."""
+    tmp = CLI + ".tmp"
+    cmd = ["g++", "-std=c++17", "-O2", "-Wall", "-I", os.path.join(HERE, "..", "include"),
+           "-I", os.path.join(CUDA_HOME, "include"), CLI_SRC, "-o", tmp, "-L", HERE, "-lffldl_b200",
+           "-L", os.path.join(CUDA_HOME, "lib64"), "-lcudart", "-Wl,-rpath,$ORIGIN"]
+    subprocess.run(cmd, check=True)
+    os.replace(tmp, CLI)
+    return CLI
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -64,6 +80,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmd = [NVCC, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", tmp, *objs, "-lcuda", "-lgomp"]
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
+    build_cli()
     return LIB
 
 

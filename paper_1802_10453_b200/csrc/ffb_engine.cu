@@ -65,9 +65,10 @@ struct ffb_context {
     Profiler prof;
 };
 
-namespace {
-
+// Detail of the calling thread's last non-OK status (ffb_last_error); also set by ffb_io.cu.
 thread_local std::string g_last_error;
+
+namespace {
 
 // ---------------------------------------------------------------------------
 // Field setup (PrimeField checks, field.hpp:73-80).
@@ -967,6 +968,7 @@ const char* ffb_status_string(int s) {
     case FFB_CUDA_ERROR: return "CudaError";
     case FFB_UNSUPPORTED: return "Unsupported";
     case FFB_WRONG_CHARACTERISTIC: return "WrongCharacteristic";
+    case FFB_PARSE_ERROR: return "ParseError";
     default: return "Error";
     }
 }

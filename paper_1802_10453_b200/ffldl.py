@@ -54,12 +54,14 @@ class NoMemory(Error): pass
 class CudaError(Error): pass
 class Unsupported(Error): pass
 class WrongCharacteristic(Error): pass
+class ParseError(Error): pass
 
 
 _STATUS = {
     1: DimensionMismatch, 2: NotSymmetric, 3: NotPrime, 4: ZeroInverse, 5: CharTwoDivision,
     6: NonUnitTriangular, 7: SingularTriangular, 8: CharTwoNonzeroDiagonal, 9: BadBlockSizes,
     10: Error, 11: NoMemory, 12: CudaError, 13: Unsupported, 14: WrongCharacteristic,
+    15: ParseError,
 }
 
 
@@ -618,3 +620,56 @@ def syr2k_sub(c, a, b, field: FieldLike, ctx: Optional[Context] = None) -> np.nd
     ctx = ctx or default_context()
     _check(lib().ffb_syr2k_sub(ctx.handle, p, c.shape[0], a.shape[0], _ptr(c), _ptr(a), _ptr(b)))
     return c
+
+
+# ---------------------------------------------------------------------------
+# Files: MatrixFile / FactorizationFile (io.hpp:22-62), text format byte-compatible with the
+# reference, plus a checksummed binary format (csrc/ffb_io.cu).  Host-side only.
+# ---------------------------------------------------------------------------
+
+
+def write_matrix(path: str, a, field: FieldLike, symmetric: bool = True, binary: bool = False) -> None:
+    """MatrixFile::from(a, symmetric).emit (io.cpp:70-95), or the binary form."""
+    a = _u64(a)
+    if a.ndim != 2:
+        raise DimensionMismatch("write_matrix: a matrix is required")
+    _check(lib().ffb_matrix_write(path.encode(), int(binary), a.shape[0], a.shape[1], _p(field),
+                                  int(symmetric), _ptr(a), 8))
+
+
+def read_matrix(path: str):
+    """MatrixFile::parse (io.cpp:39-67) of a text or binary file -> (values uint64 array,
+    modulus, symmetric)."""
+    r, c, m, sym = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0), C.c_int(0)
+    _check(lib().ffb_matrix_read(path.encode(), C.byref(r), C.byref(c), C.byref(m), C.byref(sym), None, 8))
+    out = np.zeros((r.value, c.value), np.uint64)
+    _check(lib().ffb_matrix_read(path.encode(), C.byref(r), C.byref(c), C.byref(m), C.byref(sym),
+                                 _ptr(out), 8))
+    return out, int(m.value), bool(sym.value)
+
+
+def write_factorization(path: str, f: Factorization, binary: bool = False) -> None:
+    """FactorizationFile::from(f).emit (io.cpp:149-198), or the binary form."""
+    n, r = f.dimension(), f.rank
+    perm = np.ascontiguousarray(f.perm.image_array(), np.int64)
+    lower = _u64(f.lower[:, :r])
+    kind, val, val2 = f.diag.columns()
+    kind = np.ascontiguousarray(kind, np.int32)
+    _check(lib().ffb_factorization_write(path.encode(), int(binary), n, f.p, r, _ptr(perm), _ptr(lower), 8,
+                                         _ptr(kind), _ptr(_u64(val)), _ptr(_u64(val2))))
+
+
+def read_factorization(path: str) -> Factorization:
+    """FactorizationFile::parse + bind (io.cpp:104-146,200-222) of a text or binary file."""
+    n, m, r = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+    _check(lib().ffb_factorization_read(path.encode(), C.byref(n), C.byref(m), C.byref(r), None, None, 8,
+                                        None, None, None))
+    N, R = n.value, r.value
+    perm = np.zeros(max(N, 1), np.int64)
+    lower = np.zeros(max(N * R, 1), np.uint64)
+    kind = np.zeros(max(R, 1), np.int32)
+    val = np.zeros(max(R, 1), np.uint64)
+    val2 = np.zeros(max(R, 1), np.uint64)
+    _check(lib().ffb_factorization_read(path.encode(), C.byref(n), C.byref(m), C.byref(r), _ptr(perm),
+                                        _ptr(lower), 8, _ptr(kind), _ptr(val), _ptr(val2)))
+    return _make_fact(N, int(m.value), perm, lower, kind, val, val2, R)
