@@ -3,5 +3,6 @@
 #include "ffldl/errors.hpp"
 #include "ffldl/kernels.hpp"
 #include "ffldl/plduq.hpp"
+#include "ffldl/rpmtools.hpp"
 #include "ffldl/sytrf.hpp"
 #include "ffldl/trssyr2k.hpp"

@@ -13,6 +13,9 @@
 //   plduq                plduq.hpp:42      -> plduq.cpp:36-123 (+ reconstruct/rank_profile)
 //   trssyr2k[_inplace]   trssyr2k.hpp:17,20 -> trssyr2k.cpp:55-77
 //   gemm_sub, trmm_sub, trsm_inplace, syrdk_sub x2, syr2k_sub  kernels.hpp:13-32
+//   strictify            rpmtools.hpp:39   -> rpmtools.cpp:74-132 (with the rest of
+//                        rpmtools.cpp: pivoting_matrix, rank_profile_bruteforce,
+//                        verify_revealing -- compile this file instead of rpmtools.cpp too)
 #include <cstdlib>
 #include <mutex>
 #include <variant>
@@ -48,6 +51,8 @@ ffb_context* ctx() {
     case FFB_SINGULAR_TRIANGULAR: throw SingularTriangular(msg);
     case FFB_CHAR_TWO_NONZERO_DIAGONAL: throw CharTwoNonzeroDiagonal(msg);
     case FFB_BAD_BLOCK_SIZES: throw BadBlockSizes(msg);
+    case FFB_WRONG_CHARACTERISTIC: throw WrongCharacteristic(msg);
+    case FFB_PARSE_ERROR: throw ParseError(msg);
     default: throw Error("ffldl_b200: " + msg);
     }
 }
@@ -243,20 +248,10 @@ void syrdk_sub(Matrix& c, const Matrix& g, const BlockDiag& d) {
 void syrdk_sub(Matrix& c, const Matrix& g, std::span<const FieldElement> d) {
     if (c.rows() != c.cols() || g.rows() != c.rows() || g.cols() != d.size())
         throw DimensionMismatch("syrdk_sub: incompatible shapes");
-    BlockDiag bd;
-    std::vector<uint64_t> gcopy = flat(g);
-    // zero entries of diag(d) are legal here (kernels.cpp:108-119): fold them by
-    // zeroing the matching columns of G and using a unit scalar block.
-    Matrix gz = g;
-    for (std::size_t k = 0; k < d.size(); ++k) {
-        if (d[k].value == 0) {
-            for (std::size_t i = 0; i < g.rows(); ++i) gz(i, k) = c.field().zero();
-            bd.push(ScalarBlock{c.field().one()});
-        } else {
-            bd.push(ScalarBlock{d[k]});
-        }
-    }
-    syrdk_sub(c, gz, bd);
+    std::vector<uint64_t> cv = flat(c), gv = flat(g), dv(d.size() + 1);
+    for (std::size_t k = 0; k < d.size(); ++k) dv[k] = d[k].value;
+    check(ffb_syrdk_sub_diag(ctx(), c.field().modulus(), c.rows(), d.size(), cv.data(), gv.data(), dv.data()));
+    c = unflat(c.field(), c.rows(), c.cols(), cv.data());
 }
 
 void syr2k_sub(Matrix& c, const Matrix& a, const Matrix& b) {
@@ -265,6 +260,93 @@ void syr2k_sub(Matrix& c, const Matrix& a, const Matrix& b) {
     std::vector<uint64_t> cv = flat(c), av = flat(a), bv = flat(b);
     check(ffb_syr2k_sub(ctx(), c.field().modulus(), c.rows(), a.rows(), cv.data(), av.data(), bv.data()));
     c = unflat(c.field(), c.rows(), c.cols(), cv.data());
+}
+
+// ---- rpmtools.hpp (replaces rpmtools.cpp) ------------------------------------------
+
+// strictify, rpmtools.cpp:74-132: on the device (ffb_strictify), the factorization is
+// rewritten in place like the reference's.
+void strictify(Factorization& f, StrictifyStats* stats) {
+    const PrimeField& field = f.lower.field();
+    const std::size_t n = f.dimension(), r = f.rank;
+    std::vector<int64_t> perm(n + 1);
+    for (std::size_t i = 0; i < n; ++i) perm[i] = (int64_t)f.perm.image(i);
+    std::vector<uint64_t> lower = flat(f.lower);
+    lower.resize(n * r + 1);
+    std::vector<int32_t> kind(r + 1);
+    std::vector<uint64_t> val(r + 1), val2(r + 1);
+    for (std::size_t b = 0; b < f.diag.block_count(); ++b) {
+        const std::size_t t = f.diag.offset(b);
+        if (const auto* s = std::get_if<ScalarBlock>(&f.diag.block(b))) {
+            kind[t] = FFB_D_SCALAR;
+            val[t] = s->d.value;
+        } else if (const auto* a = std::get_if<AntiDiagBlock>(&f.diag.block(b))) {
+            kind[t] = FFB_D_ANTIDIAG_HEAD;
+            kind[t + 1] = FFB_D_ANTIDIAG_TAIL;
+            val[t] = val[t + 1] = a->x.value;
+        } else {
+            const auto& at = std::get<AntiTriBlock>(f.diag.block(b));
+            kind[t] = FFB_D_ANTITRI_HEAD;
+            kind[t + 1] = FFB_D_ANTITRI_TAIL;
+            val[t] = val[t + 1] = at.c.value;
+            val2[t] = val2[t + 1] = at.d.value;
+        }
+    }
+    uint64_t blocks = 0, touched = 0;
+    check(ffb_strictify(ctx(), field.modulus(), n, r, perm.data(), lower.data(), kind.data(), val.data(),
+                        val2.data(), &blocks, &touched));
+    f = make_fact(field, n, perm, lower, kind, val, val2, r);
+    if (stats != nullptr) {
+        stats->blocks_converted = blocks;
+        stats->entries_touched = touched;
+    }
+}
+
+Matrix pivoting_matrix(const Factorization& f) {  // rpmtools.cpp:61-68
+    const PrimeField& field = f.lower.field();
+    const std::size_t n = f.dimension();
+    Matrix pi(field, n, n);
+    for (const auto& [a, b] : f.diag.support()) pi(f.perm.image(a), f.perm.image(b)) = field.one();
+    return pi;
+}
+
+// The brute-force checker of rpmtools.cpp:43-59 (verification only, host): the column rank
+// profile of the first i rows grows by the leading column of row i reduced against the
+// reduced basis of the earlier rows, and R(i, that column) = 1 -- the same matrix as the
+// reference's inclusion-exclusion over leading ranks.
+Matrix rank_profile_bruteforce(const Matrix& a) {
+    const PrimeField& f = a.field();
+    const std::size_t m = a.rows(), n = a.cols();
+    Matrix r(f, m, n);
+    std::vector<std::vector<FieldElement>> basis;
+    std::vector<std::size_t> piv;
+    for (std::size_t i = 0; i < m; ++i) {
+        std::vector<FieldElement> row(n);
+        for (std::size_t j = 0; j < n; ++j) row[j] = a(i, j);
+        for (std::size_t b = 0; b < basis.size(); ++b) {
+            const FieldElement c = row[piv[b]];
+            if (f.is_zero(c)) continue;
+            for (std::size_t j = 0; j < n; ++j) row[j] = f.sub(row[j], f.mul(c, basis[b][j]));
+        }
+        std::size_t c = 0;
+        while (c < n && f.is_zero(row[c])) ++c;
+        if (c == n) continue;
+        const FieldElement s = f.inv(row[c]);
+        for (auto& x : row) x = f.mul(x, s);
+        for (std::size_t b = 0; b < basis.size(); ++b) {
+            const FieldElement t = basis[b][c];
+            if (f.is_zero(t)) continue;
+            for (std::size_t j = 0; j < n; ++j) basis[b][j] = f.sub(basis[b][j], f.mul(t, row[j]));
+        }
+        basis.push_back(row);
+        piv.push_back(c);
+        r(i, c) = f.one();
+    }
+    return r;
+}
+
+bool verify_revealing(const Factorization& f, const Matrix& a) {  // rpmtools.cpp:70-72
+    return f.reconstruct() == a && pivoting_matrix(f) == rank_profile_bruteforce(a);
 }
 
 }  // namespace ffldl
