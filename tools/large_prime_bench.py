@@ -41,6 +41,7 @@ def best_ms(fn, reps=5):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "large_prime.json"))
+    ap.add_argument("--nodes", default="8192,4096,2048,1024", help="node sizes s (shape (s/2)^3)")
     args = ap.parse_args()
     import paper_1802_10453_b200 as ffb
     from paper_1802_10453_b200._lib import lib
@@ -49,7 +50,7 @@ def main():
     ctx = ffb.default_context(0)
     st = torch.cuda.ExternalStream(ctx.stream)
     rows = []
-    for s in (8192, 4096, 2048, 1024):
+    for s in (int(x) for x in args.nodes.split(",")):
         M = N = K = s // 2
         g = torch.Generator(device="cuda").manual_seed(s)
         A = torch.randint(0, p, (M, K), dtype=torch.int32, device="cuda", generator=g)
