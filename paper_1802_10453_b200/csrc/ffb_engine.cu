@@ -407,6 +407,18 @@ struct Engine {
             }
     }
 
+    // Symmetric Schur updates (Z = C - G X, C3 -= Y2^T V1 + V1^T Y2) only need the upper
+    // band j >= i - halo of their output: recursive_step reads the upper blocks B and the
+    // diagonal blocks, and the leaves / fused nodes read diagonal blocks of <= max(T, 128)
+    // rows.  zero_leading_pairs mirrors the strict lower part back before its symmetric
+    // gather (mirror_lower).  -1: full updates (FFB_NO_BAND, or very large leaves).
+    int band_halo() const {
+        static const bool off = getenv("FFB_NO_BAND") != nullptr;  // A/B hook
+        if (off || variant == FFB_VARIANT_CROUT) return -1;
+        const int64_t t = variant == FFB_VARIANT_RECURSIVE ? 1 : T;
+        return t > 1024 ? -1 : (int)std::max<int64_t>(128, t);
+    }
+
     bool is_leaf(int64_t s) const {
         if (variant == FFB_VARIANT_CROUT) return true;
         if (variant == FFB_VARIANT_RECURSIVE) return s <= 1;
@@ -531,6 +543,7 @@ struct Engine {
                 SlotGuard slot(2);
                 g_tc_shared_sms = true;
                 inverse_apply_T(f, zst, G, X, D, coff, Lg, up[2]);  // :313 + rows m..s of N1
+                BandScope band(band_halo());
                 gemm(f, zst, GEMM_SUB, Z, G, false, X, false, ns, ns, r1);  // :315
                 g_tc_shared_sms = false;
             }
@@ -560,6 +573,7 @@ struct Engine {
         }
         if (!ytag) {
             gemm(f, st, GEMM_SUB, Y, LM.sub(r1, 0, m - r1, r1), false, X, false, m - r1, ns, r1);
+            BandScope band(band_halo());
             gemm(f, st, GEMM_SUB, Z, G, false, X, false, ns, ns, r1);
         }
 
@@ -716,6 +730,7 @@ struct Engine {
         const auto up = upload_batch<3>(c, {&q, &idy, &idz});
         DMat Cp = ws_mat(c, nz, nz);  // C' = Q^T Z Q (:183)
         join_z();
+        if (band_halo() >= 0) mirror_lower(st, Z, band_halo());  // Z may hold a band-only update
         gather_sym(st, Cp, Z, up[0]);
         DMat C1 = Cp.sub(0, 0, r, r), C2 = Cp.sub(0, r, r, nz - r), C3 = Cp.sub(r, r, nz - r, nz - r);
         DMat U1 = py.U.sub(0, 0, r, r), V1 = py.U.sub(0, r, r, nz - r);
@@ -739,12 +754,15 @@ struct Engine {
         if (f.char2) add_scaled_rows_upper(f, st, X, U1, delta);  // X += Delta U1 (:204-208)
         gemm(f, st, GEMM_SUB, C2, X, true, V1, false, r, nz - r, r);  // C2 -= X^T V1 (:210)
         trsm_lower_unit(f, st, U1T, C2);  // Y2 = U1^-T C2 (:211)
-        gemm(f, st, GEMM_SUB, C3, C2, true, V1, false, nz - r, nz - r, r);  // :213
-        gemm(f, st, GEMM_SUB, C3, V1, true, C2, false, nz - r, nz - r, r);
-        if (f.char2) {  // :214
-            DMat H = ws_mat(c, r, nz - r);
-            scale_rows(f, st, H, V1, delta);
-            gemm(f, st, GEMM_SUB, C3, H, true, V1, false, nz - r, nz - r, r);
+        {
+            BandScope band(band_halo());  // C3 is symmetric and read like Z
+            gemm(f, st, GEMM_SUB, C3, C2, true, V1, false, nz - r, nz - r, r);  // :213
+            gemm(f, st, GEMM_SUB, C3, V1, true, C2, false, nz - r, nz - r, r);
+            if (f.char2) {  // :214
+                DMat H = ws_mat(c, r, nz - r);
+                scale_rows(f, st, H, V1, delta);
+                gemm(f, st, GEMM_SUB, C3, H, true, V1, false, nz - r, nz - r, r);
+            }
         }
         scale_T(f, st, G12.sub(r, 0, nz - r, r), C2, py.dinv);  // G2 (:215)
 

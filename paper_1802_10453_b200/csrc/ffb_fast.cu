@@ -184,6 +184,7 @@ struct LeafSmem {
     uint32_t Ls[64][65];                  // input tile first, then L (row i, pivot column c)
     __align__(16) int32_t rowb[2][64];    // raw residual row of the front
     __align__(16) int32_t row2[64];       // raw residual row of the 2x2 partner
+    uint32_t nzm[2][4][2];                // per-warp masks of rows with a nonzero residual
     int32_t order[64];                    // pivot rows in pivot order
     int32_t pless[64];                    // pivotless rows, ascending
     int32_t dkind[64];                    // D of the leaf's pivot columns (also written to D)
@@ -228,7 +229,7 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
         if (b < 32) alo &= ~(1u << b);
         else ahi &= ~(1u << (b - 32));
     };
-    int r = 0, npl = 0, buf = 0;
+    int r = 0, npl = 0, buf = 0, nzbuf = 0;
     const bool lo = wp < 2;  // this warp's columns are rows < 32
     for (int p1 = 0; p1 < s; ++p1) {
         if (!(((p1 < 32 ? alo : ahi) >> (p1 & 31)) & 1)) continue;  // consumed as a 2x2 partner (uniform)
@@ -252,6 +253,45 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
             if (tid == 0) sm.pless[npl] = p1;
             ++npl;
             clear_bit(p1);
+            // Pivotless run: until the next pivot nothing updates S, so every active row
+            // after p1 whose residual row is zero on the active columns is pivotless too
+            // (S is symmetric: its column is zero as well, so dropping it changes no other
+            // row's test).  Find the next row with a nonzero residual in one pass instead
+            // of one step per pivotless row.
+            {
+                const uint32_t am = ((wp < 2 ? alo : ahi) >> (16 * (wp & 1))) & 0xffffu;
+                bool n0 = false, n1 = false;
+#pragma unroll
+                for (int t = 0; t < 16; ++t)
+                    if ((am >> t) & 1u) {
+                        n0 |= lz_red(f, S0[t], off) != 0;
+                        n1 |= lz_red(f, S1[t], off) != 0;
+                    }
+                const uint32_t m0 = __ballot_sync(0xffffffffu, n0), m1 = __ballot_sync(0xffffffffu, n1);
+                uint32_t(*nz)[2] = sm.nzm[nzbuf];
+                nzbuf ^= 1;
+                if (lane == 0) {
+                    nz[wp][0] = m0;
+                    nz[wp][1] = m1;
+                }
+                __syncthreads();
+                const uint64_t nzr = ((uint64_t)(nz[0][1] | nz[1][1] | nz[2][1] | nz[3][1]) << 32) |
+                                     (nz[0][0] | nz[1][0] | nz[2][0] | nz[3][0]);
+                const uint64_t act = ((uint64_t)ahi << 32) | alo;
+                const uint64_t after = p1 >= 63 ? 0ull : (~0ull << (p1 + 1));
+                const uint64_t live = act & after;  // rows still to visit, in order
+                const uint64_t nzl = nzr & live;
+                const int q = nzl ? __ffsll((long long)nzl) - 1 : s;  // next pivot row
+                uint64_t dead = live & (q >= 64 ? ~0ull : ((1ull << q) - 1));
+                while (dead) {  // uniform
+                    const int i = __ffsll((long long)dead) - 1;
+                    dead &= dead - 1;
+                    if (tid == 0) sm.pless[npl] = i;
+                    ++npl;
+                    clear_bit(i);
+                }
+                p1 = q - 1;  // the loop continues at q
+            }
             continue;
         }
         const int j = b0 ? __ffs(b0) - 1 : 31 + __ffs(b1);

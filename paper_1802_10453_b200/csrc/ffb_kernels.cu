@@ -18,6 +18,7 @@ thread_local uint64_t g_launches = 0;
 thread_local int64_t g_node = 0;
 thread_local int g_slot = 0;
 thread_local bool g_tc_shared_sms = false;
+thread_local int g_band_halo = -1;
 thread_local Profiler* g_prof = nullptr;
 
 static inline void count_launch() { ++g_launches; }
@@ -386,6 +387,25 @@ __global__ void k_transpose(uint32_t* dst, int64_t ldd, const uint32_t* src, int
     }
 }
 
+// Z[i][j] = Z[j][i] for j < i - halo: restores the strict lower part a band-only
+// symmetric update (g_band_halo) left stale.  CTA (x, y): the 32x32 tile (y, x) of the
+// lower triangle, read through the transposed tile (x, y) of the upper triangle.
+__global__ void k_mirror_lower(uint32_t* Z, int64_t ld, int64_t n, int64_t halo) {
+    FFB_PDL_ENTRY();
+    const int64_t r0 = (int64_t)blockIdx.y * 32, c0 = (int64_t)blockIdx.x * 32;
+    if (c0 >= r0 + 31 - halo) return;  // no entry with j < i - halo in this tile
+    __shared__ uint32_t tile[32][33];
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {  // upper tile (c0.., r0..)
+        const int64_t r = c0 + k, c = r0 + threadIdx.x;
+        if (r < n && c < n) tile[k][threadIdx.x] = __ldcg(Z + r * ld + c);
+    }
+    __syncthreads();
+    for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+        const int64_t i = r0 + k, j = c0 + threadIdx.x;
+        if (i < n && j < n && j < i - halo) Z[i * ld + j] = tile[threadIdx.x][k];
+    }
+}
+
 __global__ void k_scatter_lg(uint32_t* Lg, int64_t ldl, const int32_t* ids, int64_t col0,
                              int cstride, const uint32_t* src, int64_t lds, int64_t rows,
                              int64_t cols) {
@@ -739,6 +759,16 @@ void transpose(cudaStream_t st, DMat dst, DMat src) {
     if (src.rows <= 0 || src.cols <= 0) return;
     dim3 grid((unsigned)cdiv(src.cols, 32), (unsigned)cdiv(src.rows, 32));
     launch_k(k_transpose, grid, dim3(32, 8), 0, st, dst.ptr, dst.ld, src.ptr, src.ld, src.rows, src.cols);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+}
+
+void mirror_lower(cudaStream_t st, DMat Z, int halo) {
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
+    if (Z.rows <= halo + 1) return;
+    const int64_t nt = cdiv(Z.rows, 32);  // <= 65535 tile rows for n < 2^21
+    launch_k(k_mirror_lower, dim3((unsigned)nt, (unsigned)nt), dim3(32, 8), 0, st, Z.ptr, Z.ld, Z.rows,
+             (int64_t)halo);
     count_launch();
     FFB_CHECK_LAUNCH();
 }

@@ -42,6 +42,16 @@ extern thread_local int g_slot;
 // persistent tcgen05 GEMM then occupies only part of the SMs (FFB_Z_OVERLAP_SMS),
 // leaving the rest to the engine stream's latency kernels.
 extern thread_local bool g_tc_shared_sms;
+// >= 0 while a symmetric Schur update is issued whose consumers read only its upper band
+// (entries j >= i - halo, halo >= the largest diagonal block a leaf reads): the tcgen05
+// kernels skip the output tiles below that band (SYRK-style work); paths without tile
+// skipping compute everything, a superset.  See BandScope.
+extern thread_local int g_band_halo;
+struct BandScope {
+    int saved;
+    explicit BandScope(int halo) : saved(g_band_halo) { g_band_halo = halo; }
+    ~BandScope() { g_band_halo = saved; }
+};
 struct SlotGuard {
     int saved;
     explicit SlotGuard(int s) : saved(g_slot) { g_slot = s; }
@@ -129,6 +139,8 @@ void char2_delta(const Fp& f, cudaStream_t st, DMat C1, DMat U1, uint32_t* delta
 void scale_rows(const Fp& f, cudaStream_t st, DMat H, DMat S, const uint32_t* v);
 // X[i][j] += v[i] * U[i][j] for j >= i
 void add_scaled_rows_upper(const Fp& f, cudaStream_t st, DMat X, DMat U, const uint32_t* v);
+// Z[i][j] = Z[j][i] for j < i - halo (after a band-only symmetric update, see BandScope)
+void mirror_lower(cudaStream_t st, DMat Z, int halo);
 // Set a view to zero.
 void zero_mat(cudaStream_t st, DMat m);
 // Verification (ffb_verify.cu): *dcount += #{(i, j) : (L D L^T)(i, j) != A(perm i, perm j)}

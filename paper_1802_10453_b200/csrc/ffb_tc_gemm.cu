@@ -126,9 +126,11 @@ struct TcCfg {
 template <int BN, int ST>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     k_gemm_i8_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                 uint32_t* C, int64_t ldc, int M, int N, int nk, Fp f, int mode) {
+                 uint32_t* C, int64_t ldc, int M, int N, int nk, Fp f, int mode, int halo) {
     FFB_PDL_ENTRY();
     using Cfg = TcCfg<BN, ST>;
+    // upper band (halo >= 0): tiles entirely below the band j >= i - halo are not computed
+    if (halo >= 0 && (int64_t)(blockIdx.x + 1) * BN + halo <= (int64_t)blockIdx.y * TC_BM) return;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* sA = smem;
@@ -277,13 +279,21 @@ __device__ __forceinline__ void tp_tile(int t, int num_m, int num_n, int& m_blk,
     m_blk = g * TP_GM + r % gm;
     n_blk = r / gm;
 }
+// Upper band (halo >= 0): tile (mb, nb) is live iff it holds an entry with j >= i - halo.
+__device__ __forceinline__ bool tp_live(int t, int num_m, int num_n, int halo) {
+    if (halo < 0) return true;
+    int mb, nb;
+    tp_tile(t, num_m, num_n, mb, nb);
+    return (int64_t)(nb + 1) * TP_BN + halo > (int64_t)mb * TC_BM;
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __global__ void __launch_bounds__(TP_THREADS, 1)
     k_gemm_i8_tcp(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  uint32_t* C, int64_t ldc, int M, int N, int nk, Fp f, int mode, int num_m, int num_tiles) {
+                  uint32_t* C, int64_t ldc, int M, int N, int nk, Fp f, int mode, int num_m, int num_tiles,
+                  int halo) {
     const int num_n = num_tiles / num_m;
     FFB_PDL_ENTRY();
     extern __shared__ __align__(1024) uint8_t tp_raw[];
@@ -328,6 +338,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
             int s = 0;
             uint32_t ph = 0;
             for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                if (!tp_live(t, num_m, num_n, halo)) continue;
                 int mb, nbk;
                 tp_tile(t, num_m, num_n, mb, nbk);
                 const int m0 = mb * TC_BM, n0 = nbk * TP_BN;
@@ -348,6 +359,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
             int s = 0, acc = 0;
             uint32_t ph = 0, aph = 0;
             for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+                if (!tp_live(t, num_m, num_n, halo)) continue;
                 mbar_wait(&tempty[acc], aph ^ 1);  // the epilogue has drained this accumulator
                 tc_fence_after();
                 const uint32_t d = tmem + (uint32_t)(acc * TP_BN);
@@ -382,6 +394,7 @@ __global__ void __launch_bounds__(TP_THREADS, 1)
         uint32_t aph = 0;
         uint32_t cv[32];
         for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            if (!tp_live(t, num_m, num_n, halo)) continue;
             int mb, nbk;
             tp_tile(t, num_m, num_n, mb, nbk);
             const int m0 = mb * TC_BM, n0 = nbk * TP_BN + 128 * h;
@@ -838,7 +851,7 @@ void pack(cudaStream_t st, int8_t* dst, int64_t ldd, DMat src, bool trans, int64
 
 template <int BN, int ST = 0>
 void launch_tc(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, DMat C, int64_t M,
-               int64_t N, int64_t nk, const Fp& f, int mode) {
+               int64_t N, int64_t nk, const Fp& f, int mode, int halo) {
     using Cfg = TcCfg<BN, ST>;
     static DeviceOnce attr;
     if (!attr.done()) {
@@ -848,7 +861,7 @@ void launch_tc(cudaStream_t st, const CUtensorMap& ma, const CUtensorMap& mb, DM
     }
     dim3 grid((unsigned)cdiv(N, BN), (unsigned)cdiv(M, TC_BM));
     launch_k(k_gemm_i8_tc<BN, ST>, grid, TC_THREADS, Cfg::SMEM, st, ma, mb, C.ptr, C.ld, (int)M, (int)N,
-                                                          (int)nk, f, mode);
+                                                          (int)nk, f, mode, halo);
     ++g_launches;
     FFB_CHECK_LAUNCH();
 }
@@ -906,6 +919,16 @@ void tc_gemm_limb(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, b
     FFB_CHECK_LAUNCH();
 }
 
+// Fraction of the M x N output in tiles (bm x bn) that touch the band j >= i - halo.
+double band_fraction(int64_t M, int64_t N, int bm, int bn, int halo) {
+    if (halo < 0 || M <= 0 || N <= 0) return 1.0;
+    const int64_t nm = cdiv(M, bm), nn = cdiv(N, bn);
+    int64_t live = 0;
+    for (int64_t mb = 0; mb < nm; ++mb)
+        for (int64_t nb = 0; nb < nn; ++nb) live += (nb + 1) * bn + halo > mb * bm;
+    return (double)live / (double)(nm * nn);
+}
+
 void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
              int64_t M, int64_t N, int64_t K) {
     load_encode();
@@ -936,10 +959,13 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
     }
     const int64_t nk = cdiv(Kp, TC_BK);
     const bool wide = N >= 256 && M * N >= (int64_t)148 * 128 * 256;
-    ProfScope ps(K_GEMM, st, 2.0 * M * N * K, (double)M * K + N * K + 8.0 * M * N, M, N, K);
+    const int halo = g_band_halo;  // >= 0: only the upper band of a symmetric update
+    const int bn = nk <= 2 || !wide ? 128 : 256;
+    const double live = band_fraction(M, N, TC_BM, bn, halo);
+    ProfScope ps(K_GEMM, st, 2.0 * M * N * K * live, (double)M * K + N * K + 8.0 * M * N * live, M, N, K);
     if (nk <= 2) {  // short K: epilogue-bound, 2 CTAs per SM (2-stage pipeline)
         CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, 128);
-        launch_tc<128, 2>(st, ma, mb, C, M, N, nk, f, mode);
+        launch_tc<128, 2>(st, ma, mb, C, M, N, nk, f, mode, halo);
     } else if (wide && !getenv("FFB_TC_NONPERSISTENT")) {
         CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, TP_BN);
         static DeviceOnce attr;
@@ -958,15 +984,15 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
         static const int shared_sms = getenv("FFB_Z_OVERLAP_SMS") ? atoi(getenv("FFB_Z_OVERLAP_SMS")) : 100;
         const int ctas = std::min(num_tiles, g_tc_shared_sms ? std::min(shared_sms, nsm) : nsm);
         launch_k(k_gemm_i8_tcp, ctas, TP_THREADS, TpCfg::SMEM, st, ma, mb, C.ptr, C.ld,
-                 (int)M, (int)N, (int)nk, f, (int)mode, num_m, num_tiles);
+                 (int)M, (int)N, (int)nk, f, (int)mode, num_m, num_tiles, halo);
         ++g_launches;
         FFB_CHECK_LAUNCH();
     } else if (wide) {
         CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, 256);
-        launch_tc<256>(st, ma, mb, C, M, N, nk, f, mode);
+        launch_tc<256>(st, ma, mb, C, M, N, nk, f, mode, halo);
     } else {
         CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, 128);
-        launch_tc<128>(st, ma, mb, C, M, N, nk, f, mode);
+        launch_tc<128>(st, ma, mb, C, M, N, nk, f, mode, halo);
     }
 }
 

@@ -17,6 +17,7 @@ from helpers import describe_diff, fact_equal, hollow, rand_low_rank, rand_rook_
 pytestmark = pytest.mark.gpu
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 VARIANTS = [("cascade", 64), ("recursive", 64), ("crout", 64), ("cascade", 2), ("cascade", 4),
             ("cascade", 8)]
 
@@ -555,7 +556,7 @@ def test_strictify_matches_oracle(gpu, oracle):
             assert np.array_equal(val2, want.dval2)
     assert seen > 5
     n = 2048
-    a = hollow(rng, 2, n)
+    a = rand_sym(rng, 2, n)  # random diagonal: 2x2 pivots with y != 0 (AntiTri) occur
     f = ldlt_device(torch.from_numpy(a.astype(np.int32)).cuda(), 2, ctx=gpu)
     o = oracle.ldlt(2, a)
     want, (nb, nt) = oracle.strictify(2, o)
@@ -574,3 +575,29 @@ def test_strictify_matches_oracle(gpu, oracle):
         g.p = 3
         with pytest.raises(ffb.WrongCharacteristic):
             ffb.strictify(g, ctx=gpu)
+
+
+@pytest.mark.parametrize("t", [64, 128, 256])
+def test_band_schur_updates(gpu, oracle, t):
+    """The symmetric Schur updates compute only the upper band of their output on the
+    tcgen05 path (BandScope; tiles below j >= i - max(T, 128) are skipped) and
+    zero_leading_pairs mirrors the lower part back before its symmetric gather: at n = 4096
+    (rank-half rook profiles, so pairs nodes at several levels) the result is bit-exact
+    against the oracle for T = 64, 128, 256, and equals the full-update run."""
+    import subprocess
+    import sys
+    import paper_1802_10453_b200 as ffb
+    from paper_1802_10453_b200 import configs
+    w = configs.CONFIGS[5].scaled(4096)
+    a = configs.generate(w)
+    g = check(gpu, oracle, w.p, a, "cascade", t)
+    code = ("import sys, numpy as np; sys.path.insert(0, %r); import paper_1802_10453_b200 as ffb; "
+            "from paper_1802_10453_b200 import configs; w = configs.CONFIGS[5].scaled(4096); "
+            "g = ffb.ldlt(configs.generate(w), w.p, ffb.SytrfConfig(ffb.Variant.Cascade, %d)); "
+            "np.save(sys.argv[1], g.lower)" % (ROOT, t))
+    import os
+    import tempfile
+    out = os.path.join(tempfile.mkdtemp(), "full.npy")
+    env = dict(os.environ, FFB_NO_BAND="1")
+    subprocess.run([sys.executable, "-c", code, out], check=True, env=env)
+    assert np.array_equal(np.load(out), g.lower)

@@ -42,6 +42,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "large_prime.json"))
     ap.add_argument("--nodes", default="8192,4096,2048,1024", help="node sizes s (shape (s/2)^3)")
+    ap.add_argument("--dgemm-only", action="store_true", help="only the cuBLAS DGEMM (ncu target)")
     args = ap.parse_args()
     import paper_1802_10453_b200 as ffb
     from paper_1802_10453_b200._lib import lib
@@ -57,6 +58,12 @@ def main():
         B = torch.randint(0, p, (K, N), dtype=torch.int32, device="cuda", generator=g)
         C0 = torch.randint(0, p, (M, N), dtype=torch.int32, device="cuda", generator=g)
         C = C0.clone()
+        if args.dgemm_only:
+            Ad, Bd = A.double() - p // 2, B.double() - p // 2
+            for _ in range(3):
+                torch.matmul(Ad, Bd)
+            torch.cuda.synchronize()
+            continue
 
         def ours():
             _check(lib().ffb_gemm_device(ctx.handle, p, 0, M, N, K, C.data_ptr(), N, A.data_ptr(), K, 0,
