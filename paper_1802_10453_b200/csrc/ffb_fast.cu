@@ -176,30 +176,68 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* A, int64_t
 // Entries only decrease, by < p^2 per pivot (< 1.5 p^2 per pivot for an AntiTri 2x2,
 // char 2), so after <= 64 pivots S lies in (-96 p^2, p): int32-safe, and
 // S + 96 p^2 < 2^32 is reduced by 32-bit Barrett.
-__device__ __forceinline__ uint32_t lz_red(const Fp& f, int32_t v, uint32_t off) {
-    return red32(f, (uint32_t)v + off);
-}
+// Accumulator traits of the lazy leaf.  Narrow (p < 4096): int32 entries, products
+// < 2^24 reduced by 32-bit Barrett.  Wide (4096 <= p < 2^26, config 3's large prime):
+// int64 entries, the same bounds with 64-bit products (96 p^2 < 2^59), 64-bit Barrett.
+struct LzNarrow {
+    using T = int32_t;
+    static constexpr int VEC = 4;  // int4 words per 16 entries
+    __device__ __forceinline__ static uint32_t off(const Fp& f) { return 96u * f.p * f.p; }
+    __device__ __forceinline__ static uint32_t red(const Fp& f, T v, uint32_t o) {
+        return red32(f, (uint32_t)v + o);
+    }
+    __device__ __forceinline__ static uint32_t mul(const Fp& f, uint32_t a, uint32_t b) { return red32(f, a * b); }
+    // d - y l (all reduced)
+    __device__ __forceinline__ static uint32_t msub(const Fp& f, uint32_t d, uint32_t y, uint32_t l) {
+        return red32(f, d + f.p * f.p - y * l);
+    }
+};
+struct LzWide {
+    using T = int64_t;
+    static constexpr int VEC = 8;
+    __device__ __forceinline__ static uint64_t off(const Fp& f) { return 96ull * f.p * f.p; }
+    __device__ __forceinline__ static uint32_t red(const Fp& f, T v, uint64_t o) {
+        return red64(f, (uint64_t)v + o);
+    }
+    __device__ __forceinline__ static uint32_t mul(const Fp& f, uint32_t a, uint32_t b) {
+        return red64(f, (uint64_t)a * b);
+    }
+    __device__ __forceinline__ static uint32_t msub(const Fp& f, uint32_t d, uint32_t y, uint32_t l) {
+        return fsub(f, d, red64(f, (uint64_t)y * l));
+    }
+};
 // Shared memory of the lazy leaf core (one 128-thread CTA).
-struct LeafSmem {
-    uint32_t Ls[64][65];                  // input tile first, then L (row i, pivot column c)
-    __align__(16) int32_t rowb[2][64];    // raw residual row of the front
-    __align__(16) int32_t row2[64];       // raw residual row of the 2x2 partner
-    uint32_t nzm[2][4][2];                // per-warp masks of rows with a nonzero residual
-    int32_t order[64];                    // pivot rows in pivot order
-    int32_t pless[64];                    // pivotless rows, ascending
-    int32_t dkind[64];                    // D of the leaf's pivot columns (also written to D)
+template <class Acc>
+struct LeafSmemT {
+    uint32_t Ls[64][65];                          // input tile first, then L (row i, pivot column c)
+    __align__(16) typename Acc::T rowb[2][64];    // raw residual row of the front
+    __align__(16) typename Acc::T row2[64];       // raw residual row of the 2x2 partner
+    uint32_t nzm[2][4][2];                        // per-warp masks of rows with a nonzero residual
+    int32_t order[64];                            // pivot rows in pivot order
+    int32_t pless[64];                            // pivotless rows, ascending
+    int32_t dkind[64];                            // D of the leaf's pivot columns (also written to D)
     uint32_t dval2[64], dinv[64];
 };
+using LeafSmem = LeafSmemT<LzNarrow>;
+// the warp's 16 raw entries of one row -> dst (16-byte stores)
+template <class T>
+__device__ __forceinline__ void lz_store16(T* dst, const T (&v)[16]) {
+    int4* d = reinterpret_cast<int4*>(dst);
+    const int4* s = reinterpret_cast<const int4*>(v);
+#pragma unroll
+    for (int q = 0; q < (int)(16 * sizeof(T) / 16); ++q) d[q] = s[q];
+}
 
 // The leaf elimination (Alg. 4) of the s x s block at src (row stride lds; global
 // memory when kGlobal, else shared), s <= 64, by 128 threads.  Fills sm (L, order,
 // pless, D of columns coff ..) and writes D; returns the rank.  Ends with a barrier.
-template <bool kGlobal>
+template <bool kGlobal, class Acc = LzNarrow>
 __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, int64_t lds, int s,
-                         LeafSmem& sm, DDiag D, int64_t coff) {
+                         LeafSmemT<Acc>& sm, DDiag D, int64_t coff) {
+    using T = typename Acc::T;
     const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
     const uint32_t one = 1 % f.p;
-    const uint32_t off = 96u * f.p * f.p;
+    const auto off = Acc::off(f);
     {  // coalesced tile load, all loads of a thread in flight at once
         uint32_t v[32];
 #pragma unroll
@@ -215,11 +253,11 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
         }
     }
     __syncthreads();
-    int32_t S0[16], S1[16];  // S[lane][16wp + t], S[lane + 32][16wp + t]
+    T S0[16], S1[16];  // S[lane][16wp + t], S[lane + 32][16wp + t]
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
-        S0[t] = (int32_t)sm.Ls[lane][16 * wp + t];
-        S1[t] = (int32_t)sm.Ls[lane + 32][16 * wp + t];
+        S0[t] = (T)sm.Ls[lane][16 * wp + t];
+        S1[t] = (T)sm.Ls[lane + 32][16 * wp + t];
     }
     __syncthreads();
     for (int e = tid; e < 64 * 65; e += 128) (&sm.Ls[0][0])[e] = 0;
@@ -233,20 +271,14 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
     const bool lo = wp < 2;  // this warp's columns are rows < 32
     for (int p1 = 0; p1 < s; ++p1) {
         if (!(((p1 < 32 ? alo : ahi) >> (p1 & 31)) & 1)) continue;  // consumed as a 2x2 partner (uniform)
-        int32_t* rb = sm.rowb[buf];
+        T* rb = sm.rowb[buf];
         buf ^= 1;
         if (lane == (p1 & 31)) {
-            int4* d = reinterpret_cast<int4*>(rb + 16 * wp);
-            if (p1 < 32) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) d[q] = make_int4(S0[4 * q], S0[4 * q + 1], S0[4 * q + 2], S0[4 * q + 3]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) d[q] = make_int4(S1[4 * q], S1[4 * q + 1], S1[4 * q + 2], S1[4 * q + 3]);
-            }
+            if (p1 < 32) lz_store16(rb + 16 * wp, S0);
+            else lz_store16(rb + 16 * wp, S1);
         }
         __syncthreads();
-        const uint32_t c0 = lz_red(f, rb[lane], off), c1 = lz_red(f, rb[lane + 32], off);
+        const uint32_t c0 = Acc::red(f, rb[lane], off), c1 = Acc::red(f, rb[lane + 32], off);
         const uint32_t b0 = __ballot_sync(0xffffffffu, c0 != 0) & alo;
         const uint32_t b1 = __ballot_sync(0xffffffffu, c1 != 0) & ahi;
         if (!(b0 | b1)) {  // pivotless (sytrf.cpp:82-85)
@@ -264,8 +296,8 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
 #pragma unroll
                 for (int t = 0; t < 16; ++t)
                     if ((am >> t) & 1u) {
-                        n0 |= lz_red(f, S0[t], off) != 0;
-                        n1 |= lz_red(f, S1[t], off) != 0;
+                        n0 |= Acc::red(f, S0[t], off) != 0;
+                        n1 |= Acc::red(f, S1[t], off) != 0;
                     }
                 const uint32_t m0 = __ballot_sync(0xffffffffu, n0), m1 = __ballot_sync(0xffffffffu, n1);
                 uint32_t(*nz)[2] = sm.nzm[nzbuf];
@@ -298,20 +330,20 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
         // the inverse of this lane's residuals and the residuals of this warp's 16 columns
         const uint32_t i0v = inv.t ? inv.t[c0] : 0u, i1v = inv.t ? inv.t[c1] : 0u;
         const uint32_t csrc = lo ? c0 : c1;
-        int32_t ck[16];
+        uint32_t ck[16];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) ck[t] = (int32_t)__shfl_sync(0xffffffffu, csrc, (16 * wp + t) & 31);
+        for (int t = 0; t < 16; ++t) ck[t] = __shfl_sync(0xffffffffu, csrc, (16 * wp + t) & 31);
         if (j == p1) {  // 1x1 pivot (sytrf.cpp:87-97)
             const int src_l = p1 & 31;
             const uint32_t x = __shfl_sync(0xffffffffu, p1 < 32 ? c0 : c1, src_l);
             const uint32_t xi = inv.t ? __shfl_sync(0xffffffffu, p1 < 32 ? i0v : i1v, src_l) : inv(f, x);
             clear_bit(p1);
-            const uint32_t l0 = red32(f, c0 * xi), l1 = red32(f, c1 * xi);  // row multipliers
+            const uint32_t l0 = Acc::mul(f, c0, xi), l1 = Acc::mul(f, c1, xi);  // row multipliers
             // S[i][k] -= c_i l_k = l_i c_k (mod p): row multiplier times column residual
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
-                S0[t] -= (int32_t)l0 * ck[t];
-                S1[t] -= (int32_t)l1 * ck[t];
+                S0[t] -= (T)l0 * (T)ck[t];
+                S1[t] -= (T)l1 * (T)ck[t];
             }
             if (wp == 0) {
                 if ((alo >> lane) & 1) sm.Ls[lane][r] = l0;
@@ -334,17 +366,11 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
         // 2x2 antidiagonal pivot pairing p1 with p2 = j (sytrf.cpp:99-131)
         const int p2 = j;
         if (lane == (p2 & 31)) {
-            int4* d = reinterpret_cast<int4*>(sm.row2 + 16 * wp);
-            if (p2 < 32) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) d[q] = make_int4(S0[4 * q], S0[4 * q + 1], S0[4 * q + 2], S0[4 * q + 3]);
-            } else {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) d[q] = make_int4(S1[4 * q], S1[4 * q + 1], S1[4 * q + 2], S1[4 * q + 3]);
-            }
+            if (p2 < 32) lz_store16(sm.row2 + 16 * wp, S0);
+            else lz_store16(sm.row2 + 16 * wp, S1);
         }
         __syncthreads();
-        const uint32_t d0 = lz_red(f, sm.row2[lane], off), d1 = lz_red(f, sm.row2[lane + 32], off);
+        const uint32_t d0 = Acc::red(f, sm.row2[lane], off), d1 = Acc::red(f, sm.row2[lane + 32], off);
         const uint32_t x = __shfl_sync(0xffffffffu, p2 < 32 ? c0 : c1, p2 & 31);
         const uint32_t y = __shfl_sync(0xffffffffu, p2 < 32 ? d0 : d1, p2 & 31);
         const uint32_t xi = inv(f, x);
@@ -353,19 +379,19 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
         clear_bit(p1);
         clear_bit(p2);
         // row multipliers of this lane's rows: l2 = x^-1 c, l1 = x^-1 (d - y_eff l2)
-        const uint32_t l2a = red32(f, xi * c0), l2b = red32(f, xi * c1);
-        const uint32_t l1a = red32(f, xi * red32(f, d0 + f.p * f.p - y_eff * l2a));
-        const uint32_t l1b = red32(f, xi * red32(f, d1 + f.p * f.p - y_eff * l2b));
+        const uint32_t l2a = Acc::mul(f, xi, c0), l2b = Acc::mul(f, xi, c1);
+        const uint32_t l1a = Acc::mul(f, xi, Acc::msub(f, d0, y_eff, l2a));
+        const uint32_t l1b = Acc::mul(f, xi, Acc::msub(f, d1, y_eff, l2b));
         // S -= x l1_i l2_k + x l2_i l1_k (+ yd l2_i l2_k)
-        const int32_t ga = (int32_t)(red32(f, x * l1a) + red32(f, yd * l2a));
-        const int32_t gb = (int32_t)(red32(f, x * l1b) + red32(f, yd * l2b));
-        const int32_t ba = (int32_t)red32(f, x * l2a), bb = (int32_t)red32(f, x * l2b);
+        const T ga = (T)(Acc::mul(f, x, l1a) + Acc::mul(f, yd, l2a));
+        const T gb = (T)(Acc::mul(f, x, l1b) + Acc::mul(f, yd, l2b));
+        const T ba = (T)Acc::mul(f, x, l2a), bb = (T)Acc::mul(f, x, l2b);
         const uint32_t s2 = lo ? l2a : l2b, s1 = lo ? l1a : l1b;
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
             const int src_l = (16 * wp + t) & 31;
-            const int32_t l2k = (int32_t)__shfl_sync(0xffffffffu, s2, src_l);
-            const int32_t l1k = (int32_t)__shfl_sync(0xffffffffu, s1, src_l);
+            const T l2k = (T)__shfl_sync(0xffffffffu, s2, src_l);
+            const T l1k = (T)__shfl_sync(0xffffffffu, s1, src_l);
             S0[t] -= ga * l2k + ba * l1k;
             S1[t] -= gb * l2k + bb * l1k;
         }
@@ -381,7 +407,7 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
             if (lane == 0) {
                 sm.Ls[p1][r] = one;
                 sm.Ls[p2][r + 1] = one;
-                sm.Ls[p2][r] = f.char2 ? 0 : red32(f, xi * y_eff);
+                sm.Ls[p2][r] = f.char2 ? 0 : Acc::mul(f, xi, y_eff);
                 const int32_t hk = yd ? D_ANTITRI_HEAD : D_ANTIDIAG_HEAD;
                 D.kind[coff + r] = hk;
                 D.kind[coff + r + 1] = hk + 1;
@@ -402,19 +428,20 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
     return r;
 }
 
+template <class Acc>
 __global__ void __launch_bounds__(128) k_leaf64_lazy(Fp f, const uint32_t* A, int64_t lda,
                                                      int s, const int32_t* rows,
                                                      uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
                                                      int32_t* out, MboxPost mp) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    __shared__ LeafSmem sm;
+    __shared__ LeafSmemT<Acc> sm;
     __shared__ int32_t srows[64];
     __shared__ uint32_t sinv[SINV_MAX];
     const int tid = threadIdx.x;
     const SmemInv inv = stage_inverses(f, sinv);  // independent of the predecessor
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (tid < 64) srows[tid] = tid < s ? __ldcg(rows + tid) : 0;
-    const int r = leaf_core<true>(f, inv, A, lda, s, sm, D, coff);
+    const int r = leaf_core<true, Acc>(f, inv, A, lda, s, sm, D, coff);
     // L columns [coff, coff + r) of the leaf rows: thread t < s writes row t
     if (tid < s) {
         uint32_t* d = Lg + (int64_t)srows[tid] * ldL + coff;
@@ -1235,7 +1262,9 @@ void leaf64(const Fp& f, cudaStream_t st, DMat A, const int32_t* rows, DMat Lg, 
     ProfScope ps(K_LEAF, st, 2.0 * s * s * s / 3.0, 4.0 * s * s);
     static const bool eager = getenv("FFB_LEAF_EAGER") != nullptr;  // A/B hook
     if (f.p < 4096u && !eager)
-        launch_k(k_leaf64_lazy, 1, 128, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out, mp);
+        launch_k(k_leaf64_lazy<LzNarrow>, 1, 128, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out, mp);
+    else if (f.p < (1u << 26) && !eager)  // large primes (config 3): int64 lazy entries
+        launch_k(k_leaf64_lazy<LzWide>, 1, 128, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out, mp);
     else if (f.p < (1u << 16))
         launch_k(k_leaf64<true>, 1, 256, 0, st, f, A.ptr, A.ld, s, rows, Lg.ptr, Lg.ld, coff, D, out, mp);
     else
