@@ -212,7 +212,6 @@ struct LeafSmemT {
     uint32_t Ls[64][65];                          // input tile first, then L (row i, pivot column c)
     __align__(16) typename Acc::T rowb[2][64];    // raw residual row of the front
     __align__(16) typename Acc::T row2[64];       // raw residual row of the 2x2 partner
-    uint32_t nzm[2][4][2];                        // per-warp masks of rows with a nonzero residual
     int32_t order[64];                            // pivot rows in pivot order
     int32_t pless[64];                            // pivotless rows, ascending
     int32_t dkind[64];                            // D of the leaf's pivot columns (also written to D)
@@ -220,12 +219,15 @@ struct LeafSmemT {
 };
 using LeafSmem = LeafSmemT<LzNarrow>;
 // the warp's 16 raw entries of one row -> dst (16-byte stores)
-template <class T>
-__device__ __forceinline__ void lz_store16(T* dst, const T (&v)[16]) {
+__device__ __forceinline__ void lz_store16(int32_t* dst, const int32_t (&v)[16]) {
     int4* d = reinterpret_cast<int4*>(dst);
-    const int4* s = reinterpret_cast<const int4*>(v);
 #pragma unroll
-    for (int q = 0; q < (int)(16 * sizeof(T) / 16); ++q) d[q] = s[q];
+    for (int q = 0; q < 4; ++q) d[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+}
+__device__ __forceinline__ void lz_store16(int64_t* dst, const int64_t (&v)[16]) {
+    longlong2* d = reinterpret_cast<longlong2*>(dst);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) d[q] = make_longlong2(v[2 * q], v[2 * q + 1]);
 }
 
 // The leaf elimination (Alg. 4) of the s x s block at src (row stride lds; global
@@ -235,6 +237,7 @@ template <bool kGlobal, class Acc = LzNarrow>
 __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, int64_t lds, int s,
                          LeafSmemT<Acc>& sm, DDiag D, int64_t coff) {
     using T = typename Acc::T;
+    constexpr bool kWide = sizeof(T) == 8;
     const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
     const uint32_t one = 1 % f.p;
     const auto off = Acc::off(f);
@@ -246,13 +249,22 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
             v[u] = (i < s && k < s) ? (kGlobal ? __ldcg(src + (int64_t)i * lds + k) : src[(int64_t)i * lds + k])
                                     : 0u;
         }
+        bool nzt = false;
 #pragma unroll
         for (int u = 0; u < 32; ++u) {
             const int e = tid + 128 * u;
             sm.Ls[e >> 6][e & 63] = v[u];
+            nzt |= v[u] != 0;
+        }
+        // an all-zero block (rank-0 leaves of exactly zero Schur complements, config 2):
+        // every row is pivotless, in order (sytrf.cpp:82-85 at each front)
+        if (!__syncthreads_or(nzt)) {
+            for (int e = tid; e < 64 * 65; e += 128) (&sm.Ls[0][0])[e] = 0;
+            for (int i = tid; i < s; i += 128) sm.pless[i] = i;
+            __syncthreads();
+            return 0;
         }
     }
-    __syncthreads();
     T S0[16], S1[16];  // S[lane][16wp + t], S[lane + 32][16wp + t]
 #pragma unroll
     for (int t = 0; t < 16; ++t) {
@@ -267,7 +279,7 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
         if (b < 32) alo &= ~(1u << b);
         else ahi &= ~(1u << (b - 32));
     };
-    int r = 0, npl = 0, buf = 0, nzbuf = 0;
+    int r = 0, npl = 0, buf = 0;
     const bool lo = wp < 2;  // this warp's columns are rows < 32
     for (int p1 = 0; p1 < s; ++p1) {
         if (!(((p1 < 32 ? alo : ahi) >> (p1 & 31)) & 1)) continue;  // consumed as a 2x2 partner (uniform)
@@ -285,65 +297,29 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
             if (tid == 0) sm.pless[npl] = p1;
             ++npl;
             clear_bit(p1);
-            // Pivotless run: until the next pivot nothing updates S, so every active row
-            // after p1 whose residual row is zero on the active columns is pivotless too
-            // (S is symmetric: its column is zero as well, so dropping it changes no other
-            // row's test).  Find the next row with a nonzero residual in one pass instead
-            // of one step per pivotless row.
-            {
-                const uint32_t am = ((wp < 2 ? alo : ahi) >> (16 * (wp & 1))) & 0xffffu;
-                bool n0 = false, n1 = false;
-#pragma unroll
-                for (int t = 0; t < 16; ++t)
-                    if ((am >> t) & 1u) {
-                        n0 |= Acc::red(f, S0[t], off) != 0;
-                        n1 |= Acc::red(f, S1[t], off) != 0;
-                    }
-                const uint32_t m0 = __ballot_sync(0xffffffffu, n0), m1 = __ballot_sync(0xffffffffu, n1);
-                uint32_t(*nz)[2] = sm.nzm[nzbuf];
-                nzbuf ^= 1;
-                if (lane == 0) {
-                    nz[wp][0] = m0;
-                    nz[wp][1] = m1;
-                }
-                __syncthreads();
-                const uint64_t nzr = ((uint64_t)(nz[0][1] | nz[1][1] | nz[2][1] | nz[3][1]) << 32) |
-                                     (nz[0][0] | nz[1][0] | nz[2][0] | nz[3][0]);
-                const uint64_t act = ((uint64_t)ahi << 32) | alo;
-                const uint64_t after = p1 >= 63 ? 0ull : (~0ull << (p1 + 1));
-                const uint64_t live = act & after;  // rows still to visit, in order
-                const uint64_t nzl = nzr & live;
-                const int q = nzl ? __ffsll((long long)nzl) - 1 : s;  // next pivot row
-                uint64_t dead = live & (q >= 64 ? ~0ull : ((1ull << q) - 1));
-                while (dead) {  // uniform
-                    const int i = __ffsll((long long)dead) - 1;
-                    dead &= dead - 1;
-                    if (tid == 0) sm.pless[npl] = i;
-                    ++npl;
-                    clear_bit(i);
-                }
-                p1 = q - 1;  // the loop continues at q
-            }
             continue;
         }
         const int j = b0 ? __ffs(b0) - 1 : 31 + __ffs(b1);
         // the inverse of this lane's residuals and the residuals of this warp's 16 columns
-        const uint32_t i0v = inv.t ? inv.t[c0] : 0u, i1v = inv.t ? inv.t[c1] : 0u;
+        // (wide: one broadcast load of the pivot's inverse from the global table once the
+        // pivot is known -- per-lane prefetches of every candidate measured slower)
+        const uint32_t* itab = kWide ? nullptr : inv.t;
+        const uint32_t i0v = itab ? itab[c0] : 0u, i1v = itab ? itab[c1] : 0u;
         const uint32_t csrc = lo ? c0 : c1;
-        uint32_t ck[16];
+        T ck[16];
 #pragma unroll
-        for (int t = 0; t < 16; ++t) ck[t] = __shfl_sync(0xffffffffu, csrc, (16 * wp + t) & 31);
+        for (int t = 0; t < 16; ++t) ck[t] = (T)__shfl_sync(0xffffffffu, csrc, (16 * wp + t) & 31);
         if (j == p1) {  // 1x1 pivot (sytrf.cpp:87-97)
             const int src_l = p1 & 31;
             const uint32_t x = __shfl_sync(0xffffffffu, p1 < 32 ? c0 : c1, src_l);
-            const uint32_t xi = inv.t ? __shfl_sync(0xffffffffu, p1 < 32 ? i0v : i1v, src_l) : inv(f, x);
+            const uint32_t xi = itab ? __shfl_sync(0xffffffffu, p1 < 32 ? i0v : i1v, src_l) : inv(f, x);
             clear_bit(p1);
             const uint32_t l0 = Acc::mul(f, c0, xi), l1 = Acc::mul(f, c1, xi);  // row multipliers
             // S[i][k] -= c_i l_k = l_i c_k (mod p): row multiplier times column residual
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
-                S0[t] -= (T)l0 * (T)ck[t];
-                S1[t] -= (T)l1 * (T)ck[t];
+                S0[t] -= (T)l0 * ck[t];
+                S1[t] -= (T)l1 * ck[t];
             }
             if (wp == 0) {
                 if ((alo >> lane) & 1) sm.Ls[lane][r] = l0;
@@ -373,7 +349,7 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
         const uint32_t d0 = Acc::red(f, sm.row2[lane], off), d1 = Acc::red(f, sm.row2[lane + 32], off);
         const uint32_t x = __shfl_sync(0xffffffffu, p2 < 32 ? c0 : c1, p2 & 31);
         const uint32_t y = __shfl_sync(0xffffffffu, p2 < 32 ? d0 : d1, p2 & 31);
-        const uint32_t xi = inv(f, x);
+        const uint32_t xi = itab ? __shfl_sync(0xffffffffu, p2 < 32 ? i0v : i1v, p2 & 31) : inv(f, x);
         const uint32_t y_eff = f.char2 ? y : fhalve(f, y);
         const uint32_t yd = f.char2 ? y : 0;
         clear_bit(p1);
