@@ -40,14 +40,25 @@ def main():
     ctx.profile(False)
     agg = defaultdict(lambda: [0, 0.0])
     tot = defaultdict(lambda: [0, 0.0])
+    shapes = defaultdict(lambda: [0, 0.0])
     for line in open(path):
         cls, m, nn, k, t, node = line.split()
+        if CLASSES[int(cls)] in ("gemm", "trsm"):
+            def b2(x):
+                x = abs(int(x))
+                return 0 if x == 0 else 1 << (x - 1).bit_length()
+            shapes[(CLASSES[int(cls)], b2(m), b2(nn), b2(k))][0] += 1
+            shapes[(CLASSES[int(cls)], b2(m), b2(nn), b2(k))][1] += float(t)
         b = 1 << max(0, (int(node) - 1)).bit_length()
         agg[(b, CLASSES[int(cls)])][0] += 1
         agg[(b, CLASSES[int(cls)])][1] += float(t)
         tot[b][0] += 1
         tot[b][1] += float(t)
     os.remove(path)
+    print("top GEMM / TRSM shape buckets (M, N, K rounded up to powers of 2) by total ms:")
+    for key, (k, t) in sorted(shapes.items(), key=lambda x: -x[1][1])[:30]:
+        print(f"  {key[0]:5s} M<={key[1]:6d} N<={key[2]:6d} K<={key[3]:6d}: {k:5d} launches {t:8.3f} ms "
+              f"{t / k * 1e3:7.1f} us avg")
     print(f"config {c} n={n}: launches and CUDA-event ms by node size (<= bucket) and class")
     for b in sorted(tot):
         print(f"node<={b:6d}: {tot[b][0]:6d} launches {tot[b][1]:9.3f} ms")
