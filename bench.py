@@ -52,6 +52,30 @@ def int8_peak():
         return INT8_DATASHEET_TOPS, INT8_DATASHEET_TOPS, "of datasheet (measured int8 peak absent)"
 
 
+def isolated_top_update():
+    """The top Schur update's kernel (k_gemm_i8_tcp) in isolation on 16384^2 x 4096, from the
+    committed ncu --set full capture: duration, tensor-pipe activity, DRAM bytes."""
+    path = os.path.join(PROFILES, "r02_tcp_gemm_16384x16384x4096_ncu.txt")
+    out = {"source": "profiles/r02_tcp_gemm_16384x16384x4096_ncu.txt", "shape_mnk": [16384, 16384, 4096]}
+    try:
+        for line in open(path):
+            if ":" not in line or line.startswith("#"):
+                continue
+            k, v = line.split(":", 1)
+            val = v.split()[0] if v.split() else ""
+            if k == "gpu__time_duration.sum":
+                out["ncu_us"] = float(val)
+            elif k == "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed":
+                out["tensor_pipe_active_pct"] = float(val)
+            elif k == "SM Frequency":
+                out["sm_ghz"] = float(val)
+    except (OSError, ValueError):
+        return None
+    if "ncu_us" in out:
+        out["tops"] = 2.0 * 16384 * 16384 * 4096 / (out["ncu_us"] / 1e6) / 1e12
+    return out
+
+
 def ncu_gemm_traffic():
     """DRAM bytes of the GEMM kernels of one config-5 factorization, from the committed ncu
     capture (tools/ncu_traffic.py); None when absent."""
@@ -359,6 +383,10 @@ def main():
             if nt and nt.get("top_launch"):
                 largest["ncu"] = nt["top_launch"]
             roofline["largest_gemm"] = largest
+        iso = isolated_top_update()
+        if iso and "tops" in iso:
+            iso["frac_of_measured_burst"] = iso["tops"] / burst
+            roofline["isolated_top_update"] = iso
 
     # full-size correctness of the measured factorization (outside the timed region):
     # P L D L^T P^T == A exactly, and for config 5 the rank profile matrix == generator R

@@ -756,8 +756,8 @@ struct Engine {
         trsm_lower_unit(f, st, U1T, C2);  // Y2 = U1^-T C2 (:211)
         {
             BandScope band(band_halo());  // C3 is symmetric and read like Z
-            gemm(f, st, GEMM_SUB, C3, C2, true, V1, false, nz - r, nz - r, r);  // :213
-            gemm(f, st, GEMM_SUB, C3, V1, true, C2, false, nz - r, nz - r, r);
+            // C3 -= Y2^T V1 + V1^T Y2 (:213), both terms into one accumulator
+            gemm2(f, st, GEMM_SUB, C3, C2, true, V1, false, V1, true, C2, false, nz - r, nz - r, r, r);
             if (f.char2) {  // :214
                 DMat H = ws_mat(c, r, nz - r);
                 scale_rows(f, st, H, V1, delta);
@@ -1568,8 +1568,7 @@ int ffb_syr2k_sub(ffb_context* c, uint64_t p, size_t n, size_t k, uint64_t* cc, 
         Fp f = make_field(c, p);
         DMat C = upload_matrix(c, f, cc, n, n, 8), A = upload_matrix(c, f, a, k, n, 8),
              B = upload_matrix(c, f, b, k, n, 8);
-        gemm(f, c->stream, GEMM_SUB, C, A, true, B, false, n, n, k);
-        gemm(f, c->stream, GEMM_SUB, C, B, true, A, false, n, n, k);
+        gemm2(f, c->stream, GEMM_SUB, C, A, true, B, false, B, true, A, false, n, n, k, k);
         download_matrix(c, C, cc);
         c->ws_top = 0;
     });

@@ -231,6 +231,20 @@ simt:
     else launch_gemm_simt<true, true>(f, st, mode, C, A, B, M, N, K);
 }
 
+// C op= op(A1) op(B1) + op(A2) op(B2) (e.g. SYR2K, kernels.cpp:121-135): one tcgen05
+// accumulator over the K-concatenated terms when the tensor-core path applies (C is read
+// and written once), else two GEMMs.
+void gemm2(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A1, bool ta1, DMat B1, bool tb1, DMat A2,
+           bool ta2, DMat B2, bool tb2, int64_t M, int64_t N, int64_t K1, int64_t K2) {
+    if (M <= 0 || N <= 0) return;
+    const bool big = M >= 128 && N >= 128 && (double)M * N * (K1 + K2) >= 2.7e8;
+    if (big && K1 > 0 && K2 > 0 && !getenv("FFB_GEMM_PATH") &&
+        tc_gemm2(f, st, mode, C, A1, ta1, B1, tb1, A2, ta2, B2, tb2, M, N, K1, K2))
+        return;
+    gemm(f, st, mode, C, A1, ta1, B1, tb1, M, N, K1);
+    gemm(f, st, mode == GEMM_SET ? GEMM_ADD : mode, C, A2, ta2, B2, tb2, M, N, K2);
+}
+
 // ===========================================================================
 // Bandwidth-bound data movement.
 // ===========================================================================

@@ -73,6 +73,12 @@ enum GemmMode { GEMM_SUB = 0, GEMM_ADD = 1, GEMM_SET = 2 };
 void gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
           int64_t M, int64_t N, int64_t K);
 
+// C op= op(A1) op(B1) + op(A2) op(B2): one accumulator on the tcgen05 path, else two gemm()
+void gemm2(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A1, bool ta1, DMat B1, bool tb1, DMat A2,
+           bool ta2, DMat B2, bool tb2, int64_t M, int64_t N, int64_t K1, int64_t K2);
+bool tc_gemm2(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A1, bool ta1, DMat B1, bool tb1, DMat A2,
+              bool ta2, DMat B2, bool tb2, int64_t M, int64_t N, int64_t K1, int64_t K2);
+
 // int8 mma.sync path (ffb_mma.cu): p <= 255, small and mid shapes, no operand packing.
 bool mma_gemm_supported(const Fp& f, int64_t M, int64_t N, int64_t K);
 void mma_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,

@@ -679,11 +679,12 @@ __device__ __forceinline__ int8_t center(uint32_t x, uint32_t p) {
 // Both operands in one launch: blockIdx.z selects the job.
 struct PackJob {
     int8_t* dst;
-    int64_t ldd;
+    int64_t ldd;  // row stride of the packed operand
     const uint32_t* src;
     int64_t lds;
     int64_t rows, K;
     int trans;
+    int64_t kw;  // packed k written: [0, kw) (= ldd, or one K segment of a concatenation)
 };
 // Both operands of a GEMM in one launch (blockIdx.z = job), 64 x 64 tiles of
 // the packed (rows x ldd) int8 output per CTA, 16-byte vector stores.  Not
@@ -700,12 +701,12 @@ __global__ void __launch_bounds__(256) k_pack2(PackJob j0, PackJob j1, uint32_t 
     const PackJob& j = blockIdx.z == 0 ? j0 : j1;
     __shared__ __align__(16) uint8_t tile[64][64 + 16];
     const int64_t i0 = (int64_t)blockIdx.y * 64, k0 = (int64_t)blockIdx.x * 64;
-    if (i0 >= j.rows || k0 >= j.ldd) return;  // uniform per block
+    if (i0 >= j.rows || k0 >= j.kw) return;  // uniform per block
     const int t = threadIdx.x;
     const bool vec = ((j.lds & 3) == 0) && ((((uintptr_t)j.src) & 15) == 0);
     if (!j.trans) {
         const int64_t i = i0 + (t >> 2), k = k0 + 16 * (t & 3);
-        if (i >= j.rows || k >= j.ldd) return;
+        if (i >= j.rows || k >= j.kw) return;
         uint32_t v[16];
         const uint32_t* sp = j.src + i * j.lds + k;
         if (vec && k + 16 <= j.K) {
@@ -746,7 +747,7 @@ __global__ void __launch_bounds__(256) k_pack2(PackJob j0, PackJob j1, uint32_t 
     __syncthreads();
     const int ii = t >> 2, ks = 16 * (t & 3);
     const int64_t i = i0 + ii, k = k0 + ks;
-    if (i >= j.rows || k >= j.ldd) return;
+    if (i >= j.rows || k >= j.kw) return;
     uint32_t o[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q)
@@ -929,14 +930,25 @@ double band_fraction(int64_t M, int64_t N, int bm, int bn, int halo) {
     return (double)live / (double)(nm * nn);
 }
 
-void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
-             int64_t M, int64_t N, int64_t K) {
-    load_encode();
-    if (f.p > 255) {
-        tc_gemm_limb(f, st, mode, C, A, ta, B, tb, M, N, K);
-        return;
+// One GEMM term op(A) op(B) with inner dimension K; several terms share one accumulator
+// when their operands are packed as one K-concatenated problem (tc_gemm2).
+struct TcSeg {
+    DMat A;
+    bool ta;
+    DMat B;
+    bool tb;
+    int64_t K;
+};
+
+// Pack the terms side by side along k (each segment padded to 16) and run one tcgen05 GEMM:
+// C op= sum_s op(A_s) op(B_s).  p <= 255.
+static void tc_run(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, int64_t M, int64_t N, const TcSeg* sg,
+                   int nseg) {
+    int64_t Kp = 0, K = 0;
+    for (int i = 0; i < nseg; ++i) {
+        Kp += (sg[i].K + 15) / 16 * 16;
+        K += sg[i].K;
     }
-    const int64_t Kp = (K + 15) / 16 * 16;
     const size_t abytes = ((size_t)M * Kp + 1023) / 1024 * 1024;
     const size_t bbytes = ((size_t)N * Kp + 1023) / 1024 * 1024;
     int8_t* buf = scratch(abytes + bbytes);
@@ -944,17 +956,24 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
     int8_t* Bp = buf + abytes;
     {
         ProfScope ps(K_PACK, st, 0.0, 5.0 * (M * K + N * K));
-        // B^T (N x K) is needed: transposed pack unless tb
-        PackJob ja{Ap, Kp, A.ptr, A.ld, M, K, ta ? 1 : 0}, jb{Bp, Kp, B.ptr, B.ld, N, K, tb ? 0 : 1};
-        const int64_t rmax = std::max(M, N);
-        if (rmax <= (int64_t)65535 * 64) {
-            dim3 grid((unsigned)cdiv(Kp, 64), (unsigned)cdiv(rmax, 64), 2);
-            launch_k(k_pack2, grid, 256, 0, st, ja, jb, f.p);
-            ++g_launches;
-            FFB_CHECK_LAUNCH();
-        } else {
-            pack(st, Ap, Kp, A, ta, M, K, f.p);
-            pack(st, Bp, Kp, B, !tb, N, K, f.p);
+        int64_t off = 0;
+        for (int i = 0; i < nseg; ++i) {
+            const TcSeg& q = sg[i];
+            const int64_t kw = (q.K + 15) / 16 * 16;
+            // B^T (N x K) is needed: transposed pack unless tb
+            PackJob ja{Ap + off, Kp, q.A.ptr, q.A.ld, M, q.K, q.ta ? 1 : 0, kw},
+                jb{Bp + off, Kp, q.B.ptr, q.B.ld, N, q.K, q.tb ? 0 : 1, kw};
+            const int64_t rmax = std::max(M, N);
+            if (rmax <= (int64_t)65535 * 64) {
+                dim3 grid((unsigned)cdiv(kw, 64), (unsigned)cdiv(rmax, 64), 2);
+                launch_k(k_pack2, grid, 256, 0, st, ja, jb, f.p);
+                ++g_launches;
+                FFB_CHECK_LAUNCH();
+            } else {  // (a single term only: see tc_gemm2)
+                pack(st, Ap, Kp, q.A, q.ta, M, q.K, f.p);
+                pack(st, Bp, Kp, q.B, !q.tb, N, q.K, f.p);
+            }
+            off += kw;
         }
     }
     const int64_t nk = cdiv(Kp, TC_BK);
@@ -994,6 +1013,27 @@ void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool t
         CUtensorMap ma = make_map(Ap, M, Kp, TC_BM), mb = make_map(Bp, N, Kp, 128);
         launch_tc<128>(st, ma, mb, C, M, N, nk, f, mode, halo);
     }
+}
+
+
+void tc_gemm(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A, bool ta, DMat B, bool tb,
+             int64_t M, int64_t N, int64_t K) {
+    load_encode();
+    if (f.p > 255) {
+        tc_gemm_limb(f, st, mode, C, A, ta, B, tb, M, N, K);
+        return;
+    }
+    const TcSeg sg{A, ta, B, tb, K};
+    tc_run(f, st, mode, C, M, N, &sg, 1);
+}
+
+bool tc_gemm2(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, DMat A1, bool ta1, DMat B1, bool tb1, DMat A2,
+              bool ta2, DMat B2, bool tb2, int64_t M, int64_t N, int64_t K1, int64_t K2) {
+    if (f.p > 255 || std::max(M, N) > (int64_t)65535 * 64 || !tc_gemm_supported(f, M, N, K1 + K2)) return false;
+    load_encode();
+    const TcSeg sg[2] = {{A1, ta1, B1, tb1, K1}, {A2, ta2, B2, tb2, K2}};
+    tc_run(f, st, mode, C, M, N, sg, 2);
+    return true;
 }
 
 }  // namespace ffb

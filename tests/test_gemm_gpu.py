@@ -95,3 +95,17 @@ def test_tc_gemm_persistent(gpu, oracle, m, n, k, p, monkeypatch):
     b = rng.integers(0, p, (k, n), dtype=np.uint64)
     c = rng.integers(0, p, (m, n), dtype=np.uint64)
     assert np.array_equal(ffb.gemm_sub(c, a, b, p, ctx=gpu), oracle.gemm_sub(p, c, a, b))
+
+
+@pytest.mark.parametrize("n,k", [(1024, 131), (1536, 200), (2304, 64)])
+@pytest.mark.parametrize("p", [2, 131])
+def test_syr2k_single_accumulator(gpu, oracle, n, k, p):
+    """SYR2K C -= A^T B + B^T A as ONE tcgen05 GEMM over the K-concatenated terms
+    (tc_gemm2: each 16-padded K segment packed side by side, one TMEM accumulator,
+    kernels.cpp:121-135), including odd K (zero padding between the segments)."""
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(n + k + p)
+    c = rand_sym(rng, p, n)
+    a = rng.integers(0, p, (k, n), dtype=np.uint64)
+    b = rng.integers(0, p, (k, n), dtype=np.uint64)
+    assert np.array_equal(ffb.syr2k_sub(c, a, b, p, ctx=gpu), oracle.syr2k_sub(p, c, a, b))
