@@ -7,6 +7,7 @@
 // (or a table for p < 2^16), halve for odd p.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -31,11 +32,76 @@ inline int current_device() {
 }
 // "done once on this device" flag (e.g. the >48 KB dynamic shared memory attribute):
 // if (!g.done()) { cudaFuncSetAttribute(...); g.mark(); }  -- a repeated set is harmless.
-struct DeviceOnce {
-    std::atomic<uint32_t> mask{0};
-    bool done() const { return (mask.load(std::memory_order_acquire) >> current_device()) & 1u; }
-    void mark() { mask.fetch_or(1u << current_device(), std::memory_order_release); }
+// Driver-API entry points used by the engine, resolved at run time through the runtime
+// (cudaGetDriverEntryPoint) so the library has no link-time dependency on libcuda and still
+// loads on a host without a GPU driver (null entries: feature unavailable).
+struct DriverApi {
+    decltype(&cuCtxGetCurrent) ctxGetCurrent = nullptr;
+    decltype(&cuCtxSetCurrent) ctxSetCurrent = nullptr;
+    decltype(&cuDeviceGet) deviceGet = nullptr;
+    decltype(&cuDeviceGetDevResource) deviceGetDevResource = nullptr;
+    decltype(&cuDevSmResourceSplitByCount) smResourceSplitByCount = nullptr;
+    decltype(&cuDevResourceGenerateDesc) resourceGenerateDesc = nullptr;
+    decltype(&cuGreenCtxCreate) greenCtxCreate = nullptr;
+    decltype(&cuCtxFromGreenCtx) ctxFromGreenCtx = nullptr;
+    decltype(&cuGreenCtxStreamCreate) greenCtxStreamCreate = nullptr;
 };
+const DriverApi& drv();  // ffb_engine.cu
+inline CUcontext current_ctx() {
+    CUcontext c = nullptr;
+    if (drv().ctxGetCurrent) drv().ctxGetCurrent(&c);
+    return c;
+}
+
+// Kernel attributes belong to a CUDA context: keyed by the current one (the device's primary
+// context, or the side-stream green context of GreenScope).
+struct DeviceOnce {
+    std::atomic<void*> ctx[16] = {};
+    bool done() const {
+        const CUcontext c = current_ctx();
+        for (const auto& x : ctx)
+            if (x.load(std::memory_order_acquire) == (void*)c) return true;
+        return false;
+    }
+    void mark() {
+        const CUcontext c = current_ctx();
+        for (auto& x : ctx) {
+            void* e = nullptr;
+            if (x.compare_exchange_strong(e, (void*)c) || e == (void*)c) return;
+        }
+    }
+};
+
+// Optional SM partition (FFB_GREEN=1) for the streams that run bulk updates beside the
+// critical path (the large Schur update on zst, PLDUQ's Uhat absorb): a green context
+// holding all but a reserve of SMs (FFB_GREEN_RESERVE, default 16), so the 1-CTA latency
+// kernels of the critical path never share an SM with those GEMMs.  Work enqueued on such a
+// stream is issued with the green context current (GreenScope).  Measured neutral on
+// config 5 (113.8 vs 113.1 ms), so off by default.
+struct GreenSide {
+    bool ok = false;
+    CUgreenCtx g = nullptr;
+    CUcontext gctx = nullptr;
+    int sms = 0;
+};
+GreenSide& green_side();  // per device, created on first use (ffb_engine.cu)
+struct GreenScope {
+    CUcontext prev = nullptr;
+    bool on = false;
+    explicit GreenScope(bool enable) {
+        if (!enable) return;
+        GreenSide& g = green_side();
+        if (!g.ok) return;
+        drv().ctxGetCurrent(&prev);
+        drv().ctxSetCurrent(g.gctx);
+        on = true;
+    }
+    ~GreenScope() {
+        if (on) drv().ctxSetCurrent(prev);
+    }
+};
+// A stream of the device's green context (or an ordinary stream when it is disabled).
+cudaStream_t make_side_stream(int priority);
 
 // ---------------------------------------------------------------------------
 // Errors: the C-ABI maps these 1:1 to FFB_* status codes.

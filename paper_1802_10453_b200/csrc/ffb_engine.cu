@@ -23,6 +23,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <type_traits>
+#include <mutex>
 #include <atomic>
 #include <array>
 #include <vector>
@@ -64,6 +66,74 @@ struct ffb_context {
     cudaStream_t copy_stream = nullptr;  // host <-> device transfers overlapped with the engine
     Profiler prof;
 };
+
+namespace ffb {
+const DriverApi& drv() {
+    static DriverApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        auto get = [](const char* name, auto& fn) {
+            void* p = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
+        };
+        get("cuCtxGetCurrent", api.ctxGetCurrent);
+        get("cuCtxSetCurrent", api.ctxSetCurrent);
+        get("cuDeviceGet", api.deviceGet);
+        get("cuDeviceGetDevResource", api.deviceGetDevResource);
+        get("cuDevSmResourceSplitByCount", api.smResourceSplitByCount);
+        get("cuDevResourceGenerateDesc", api.resourceGenerateDesc);
+        get("cuGreenCtxCreate", api.greenCtxCreate);
+        get("cuCtxFromGreenCtx", api.ctxFromGreenCtx);
+        get("cuGreenCtxStreamCreate", api.greenCtxStreamCreate);
+    });
+    return api;
+}
+
+GreenSide& green_side() {
+    static GreenSide gs[FFB_MAX_DEVICES];
+    static std::once_flag once[FFB_MAX_DEVICES];
+    const int d = current_device();
+    std::call_once(once[d], [d] {
+        GreenSide& g = gs[d];
+        const DriverApi& a = drv();
+        if (!getenv("FFB_GREEN") || !a.ctxGetCurrent || !a.ctxSetCurrent || !a.deviceGet ||
+            !a.deviceGetDevResource || !a.smResourceSplitByCount || !a.resourceGenerateDesc || !a.greenCtxCreate ||
+            !a.ctxFromGreenCtx || !a.greenCtxStreamCreate)
+            return;
+        const int reserve = getenv("FFB_GREEN_RESERVE") ? atoi(getenv("FFB_GREEN_RESERVE")) : 16;
+        CUdevice dev;
+        CUdevResource full, part, rem;
+        unsigned nb = 1;
+        if (a.deviceGet(&dev, d) != CUDA_SUCCESS) return;
+        if (a.deviceGetDevResource(dev, &full, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return;
+        const int want = (((int)full.sm.smCount - reserve) / 8) * 8;
+        if (want < 8) return;
+        if (a.smResourceSplitByCount(&part, &nb, &full, &rem, 0, (unsigned)want) != CUDA_SUCCESS || nb < 1)
+            return;
+        CUdevResourceDesc desc;
+        if (a.resourceGenerateDesc(&desc, &part, 1) != CUDA_SUCCESS) return;
+        if (a.greenCtxCreate(&g.g, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS) return;
+        if (a.ctxFromGreenCtx(&g.gctx, g.g) != CUDA_SUCCESS) return;
+        g.sms = (int)part.sm.smCount;
+        g.ok = true;
+    });
+    return gs[d];
+}
+cudaStream_t make_side_stream(int priority) {
+    GreenSide& g = green_side();
+    cudaStream_t s = nullptr;
+    if (g.ok) {
+        CUstream cs = nullptr;
+        if (drv().greenCtxStreamCreate(&cs, g.g, CU_STREAM_NON_BLOCKING, priority) == CUDA_SUCCESS)
+            return (cudaStream_t)cs;
+    }
+    FFB_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, priority));
+    return s;
+}
+}  // namespace ffb
 
 // Detail of the calling thread's last non-OK status (ffb_last_error); also set by ffb_io.cu.
 thread_local std::string g_last_error;
@@ -370,7 +440,7 @@ struct Engine {
             static thread_local cudaEvent_t s_fork[FFB_MAX_DEVICES] = {}, s_done[FFB_MAX_DEVICES] = {};
             const int dev = current_device();
             if (!s_zst[dev]) {
-                FFB_CUDA(cudaStreamCreateWithPriority(&s_zst[dev], cudaStreamNonBlocking, least));
+                s_zst[dev] = make_side_stream(least);
                 FFB_CUDA(cudaEventCreateWithFlags(&s_fork[dev], cudaEventDisableTiming));
                 FFB_CUDA(cudaEventCreateWithFlags(&s_done[dev], cudaEventDisableTiming));
             }
@@ -538,16 +608,17 @@ struct Engine {
         static const bool z_overlap_on = getenv("FFB_NO_Z_OVERLAP") == nullptr;
         if (z_overlap_on && ns >= Z_OVERLAP_MIN && r1 > 0 && m - r1 > 0 && !zpending) {
             gemm(f, st, GEMM_SUB, Y, LM.sub(r1, 0, m - r1, r1), false, X, false, m - r1, ns, r1);  // :312
-            z_fork();
             {
+                GreenScope green(true);  // zst lives in the SM partition of the bulk updates
+                z_fork();
                 SlotGuard slot(2);
                 g_tc_shared_sms = true;
                 inverse_apply_T(f, zst, G, X, D, coff, Lg, up[2]);  // :313 + rows m..s of N1
                 BandScope band(band_halo());
                 gemm(f, zst, GEMM_SUB, Z, G, false, X, false, ns, ns, r1);  // :315
                 g_tc_shared_sms = false;
+                z_done();
             }
-            z_done();
             HFact f2 = zero_leading(Y, Z, rowsz, up[3], coff + r1, 0);  // :317
             join_z();
             HFact h;  // (:332-334)

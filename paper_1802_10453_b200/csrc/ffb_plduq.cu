@@ -1295,7 +1295,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     if (!ss.side) {
         int least = 0, greatest = 0;  // lowest priority: the main stream's chunk kernels go first
         FFB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-        FFB_CUDA(cudaStreamCreateWithPriority(&ss.side, cudaStreamNonBlocking, least));
+        ss.side = make_side_stream(least);  // the Uhat absorb: in the bulk-update SM partition
         // side2: pipelined sketch + row detection of the next chunk (highest priority: its
         // 1-CTA detection is latency-bound and must not queue behind the Uhat updates)
         FFB_CUDA(cudaStreamCreateWithPriority(&ss.side2, cudaStreamNonBlocking, greatest));
@@ -1360,6 +1360,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             us = side;
         }
         {
+            GreenScope green(us != st);
             SlotGuard slot(us == st ? g_slot : 1);
             gemm(f, us, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);  // Unew = Kc^-1 R_I
             FFB_CUDA(cudaEventRecord(ev_un, us));
@@ -1367,10 +1368,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 FFB_CUDA(cudaStreamWaitEvent(us, ev_t1, 0)); pdl_fence(us);
             }
             if (r > 0) gemm(f, us, GEMM_SUB, Uhat.sub(0, 0, r, n), Up, false, Un, false, r, n, k);
-        }
-        if (us != st) {
-            FFB_CUDA(cudaEventRecord(ev_side, side));
-            side_pending = true;
+            if (us != st) {
+                FFB_CUDA(cudaEventRecord(ev_side, side));
+                side_pending = true;
+            }
         }
     };
 

@@ -1000,7 +1000,10 @@ static void tc_run(const Fp& f, cudaStream_t st, GemmMode mode, DMat C, int64_t 
         const int num_m = (int)cdiv(M, TC_BM), num_tiles = num_m * (int)cdiv(N, TP_BN);
         // beside the critical path: a persistent grid on part of the SMs only, the rest
         // stay free for the engine stream's latency kernels
-        static const int shared_sms = getenv("FFB_Z_OVERLAP_SMS") ? atoi(getenv("FFB_Z_OVERLAP_SMS")) : 100;
+        // (inside the green SM partition the whole partition is available to it)
+        static const int shared_env = getenv("FFB_Z_OVERLAP_SMS") ? atoi(getenv("FFB_Z_OVERLAP_SMS")) : 0;
+        const GreenSide& gs = green_side();
+        const int shared_sms = shared_env ? shared_env : (gs.ok ? gs.sms : 100);
         const int ctas = std::min(num_tiles, g_tc_shared_sms ? std::min(shared_sms, nsm) : nsm);
         launch_k(k_gemm_i8_tcp, ctas, TP_THREADS, TpCfg::SMEM, st, ma, mb, C.ptr, C.ld,
                  (int)M, (int)N, (int)nk, f, (int)mode, num_m, num_tiles, halo);
