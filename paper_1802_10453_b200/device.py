@@ -38,14 +38,27 @@ class DeviceBuffers:
         self.dval2 = torch.empty(n, dtype=torch.int32, device=dev)
 
 
+def _after_torch(ctx: Context) -> None:
+    """Order the context stream after the work already queued on torch's current stream
+    (the input tensors may still be in flight there, e.g. a fresh ``a.clone()``)."""
+    import torch
+    dev = torch.device("cuda", ctx.device)
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream(dev))
+    torch.cuda.ExternalStream(ctx.stream, device=dev).wait_event(ev)
+
+
 def ldlt_device(a, field, config: Optional[SytrfConfig] = None, ctx: Optional[Context] = None,
                 out: Optional[DeviceBuffers] = None) -> DeviceFactorization:
-    """Factor the device matrix ``a`` (n x n int32 tensor of residues; OVERWRITTEN)."""
+    """Factor the device matrix ``a`` (n x n int32 tensor of residues; OVERWRITTEN).
+    The call runs on the context stream, after the work queued so far on torch's current
+    stream, and returns when the factorization is complete."""
     config = config or SytrfConfig()
     p = _p(field)
     ctx = ctx or default_context()
     n = a.shape[0]
     out = out or DeviceBuffers(n, ctx.device)
+    _after_torch(ctx)
     rank = C.c_size_t(0)
     _check(lib().ffb_ldlt_device(ctx.handle, p, n, a.data_ptr(), a.stride(0),
                                  int(config.variant), int(config.base_case_threshold),
@@ -62,6 +75,7 @@ def reconstruction_mismatches(a, fact: DeviceFactorization, field, ctx: Optional
     p = _p(field)
     ctx = ctx or default_context()
     n = a.shape[0]
+    _after_torch(ctx)
     bad = C.c_uint64(0)
     _check(lib().ffb_verify_device(ctx.handle, p, n, a.data_ptr(), a.stride(0), fact.perm.data_ptr(),
                                    fact.lower.data_ptr(), fact.lower.stride(0), fact.dkind.data_ptr(),
@@ -76,6 +90,7 @@ def pivoting_partners(fact: DeviceFactorization, ctx: Optional[Context] = None):
     ctx = ctx or default_context()
     n = fact.perm.shape[0]
     out = torch.empty(n, dtype=torch.int32, device=fact.perm.device)
+    _after_torch(ctx)
     _check(lib().ffb_pivoting_partners_device(ctx.handle, n, fact.perm.data_ptr(), fact.dkind.data_ptr(),
                                               fact.rank, out.data_ptr()))
     return out
