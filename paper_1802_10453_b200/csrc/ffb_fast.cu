@@ -900,57 +900,78 @@ __global__ void __launch_bounds__(256) k_trsm_fwd(Fp f, const uint32_t* T, int64
 // The four diagonal inverses and the strictly lower 64x64 couplings are read
 // from L2 per tile (they are shared by all column tiles).
 constexpr int PNL_COLS = 32;
-template <bool kSmall>
+// NC columns per CTA (32, or 8 for narrow right-hand sides: 4x the CTAs, a quarter of the
+// per-stage work); 256 / NC row groups, thread rows rg + G u (u < 64 / G) of each block.
+template <bool kSmall, int NC = PNL_COLS>
 __global__ void __launch_bounds__(256) k_trsm_panel(Fp f, const uint32_t* T, int64_t ldt,
                                                     const uint32_t* Tinv, uint32_t* B,
                                                     int64_t ldb, int nb, int64_t ncols) {
     FFB_PDL_ENTRY();
+    constexpr int G = 256 / NC, RU = 64 / G;
     extern __shared__ uint32_t sm[];
-    uint32_t* Xs = sm;                     // 256 x (PNL_COLS+1)
-    uint32_t* Ms = Xs + 256 * (PNL_COLS + 1);  // one 64 x 65 matrix block
+    uint32_t* Xs = sm;                  // 256 x (NC+1)
+    uint32_t* Ms = Xs + 256 * (NC + 1);  // one 64 x 65 matrix block
     const int tid = threadIdx.x;
-    const int64_t c0 = (int64_t)blockIdx.x * PNL_COLS;
-    const int bc = (int)std::min<int64_t>(PNL_COLS, ncols - c0);
-    load_tile<8>(Xs, PNL_COLS + 1, B + c0, ldb, nb, bc);
+    const int64_t c0 = (int64_t)blockIdx.x * NC;
+    const int bc = (int)std::min<int64_t>(NC, ncols - c0);
+    load_tile<8>(Xs, NC + 1, B + c0, ldb, nb, bc);
     const int nblk = (nb + 63) / 64;
-    const int col = tid & 31, rg = tid >> 5;  // 8 row groups of 8 rows
+    const int col = tid % NC, rg = tid / NC;
     for (int bi = 0; bi < nblk; ++bi) {
         const int rb = bi * 64, rows = std::min(64, nb - rb);
-        // b_bi -= T_{bi,bj} x_bj for bj < bi
+        // b_bi -= T_{bi,bj} x_bj for bj < bi: the thread's RU rows are independent
+        // accumulator chains sharing each x load (stale Ms rows >= `rows` are discarded)
         for (int bj = 0; bj < bi; ++bj) {
             __syncthreads();
             load_tile<16>(Ms, 65, T + (int64_t)rb * ldt + bj * 64, ldt, rows, 64);
             __syncthreads();
-            for (int r = rg; r < rows; r += 8) {
-                uint64_t acc = 0;
-                for (int k = 0; k < 64; ++k) {
-                    const uint64_t prod = (uint64_t)Ms[r * 65 + k] * Xs[(bj * 64 + k) * (PNL_COLS + 1) + col];
-                    acc += kSmall ? prod : (uint64_t)red64(f, prod);
+            uint64_t acc[RU];
+#pragma unroll
+            for (int u = 0; u < RU; ++u) acc[u] = 0;
+            for (int k = 0; k < 64; ++k) {
+                const uint64_t xv = Xs[(bj * 64 + k) * (NC + 1) + col];
+#pragma unroll
+                for (int u = 0; u < RU; ++u) {
+                    const uint64_t prod = (uint64_t)Ms[(rg + G * u) * 65 + k] * xv;
+                    acc[u] = kSmall ? acc[u] + prod : (uint64_t)red64(f, acc[u] + prod);
                 }
-                uint32_t* x = &Xs[(rb + r) * (PNL_COLS + 1) + col];
-                *x = fsub(f, *x, red64(f, acc));
+            }
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const int r = rg + G * u;
+                if (r < rows) {
+                    uint32_t* x = &Xs[(rb + r) * (NC + 1) + col];
+                    *x = fsub(f, *x, red64(f, acc[u]));
+                }
             }
         }
-        // x_bi = Tinv_bi b_bi
+        // x_bi = Tinv_bi b_bi (Tinv lower triangular: the k > r terms are masked)
         __syncthreads();
         load_tile<16>(Ms, 65, Tinv + (int64_t)(rb / 64) * 64 * 64, 64, 64, 64);
         __syncthreads();
-        uint32_t outv[8];
-        for (int t = 0, r = rg; r < rows; r += 8, ++t) {
-            uint64_t acc = 0;
-            for (int k = 0; k <= r; ++k) {
-                const uint64_t prod = (uint64_t)Ms[r * 65 + k] * Xs[(rb + k) * (PNL_COLS + 1) + col];
-                acc += kSmall ? prod : (uint64_t)red64(f, prod);
+        uint64_t acc[RU];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) acc[u] = 0;
+        for (int k = 0; k < 64; ++k) {
+            const uint64_t xv = Xs[(rb + k) * (NC + 1) + col];
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const int r = rg + G * u;
+                const uint64_t prod = k <= r ? (uint64_t)Ms[r * 65 + k] * xv : 0ull;
+                acc[u] = kSmall ? acc[u] + prod : (uint64_t)red64(f, acc[u] + prod);
             }
-            outv[t] = red64(f, acc);
         }
         __syncthreads();
-        for (int t = 0, r = rg; r < rows; r += 8, ++t) Xs[(rb + r) * (PNL_COLS + 1) + col] = outv[t];
+#pragma unroll
+        for (int u = 0; u < RU; ++u) {
+            const int r = rg + G * u;
+            if (r < rows) Xs[(rb + r) * (NC + 1) + col] = red64(f, acc[u]);
+        }
     }
     __syncthreads();
     for (int e = tid; e < nb * bc; e += 256) {
         const int r = e / bc, cc = e % bc;
-        B[(int64_t)r * ldb + c0 + cc] = Xs[r * (PNL_COLS + 1) + cc];
+        B[(int64_t)r * ldb + c0 + cc] = Xs[r * (NC + 1) + cc];
     }
 }
 
@@ -1152,11 +1173,21 @@ void solve_rec(const Fp& f, cudaStream_t st, DMat T, DMat B, const uint32_t* Tin
             FFB_CUDA(cudaFuncSetAttribute(k_trsm_panel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             attr.mark();
         }
-        dim3 grid((unsigned)cdiv(B.cols, PNL_COLS));
-        if (f.p < (1u << 23))
-            launch_k(k_trsm_panel<true>, grid, 256, smem, st, f, T.ptr, T.ld, ti, B.ptr, B.ld, (int)n, B.cols);
+        // narrow right-hand sides (< 4 CTAs per SM at 32 columns): 8 columns per CTA
+        const bool narrow = B.cols < (int64_t)PNL_COLS * 148;
+        const size_t smem8 = (size_t)(256 * (8 + 1) + 64 * 65) * 4;
+        if (narrow && f.p < (1u << 23))
+            launch_k(k_trsm_panel<true, 8>, dim3((unsigned)cdiv(B.cols, 8)), 256, smem8, st, f, T.ptr, T.ld, ti,
+                     B.ptr, B.ld, (int)n, B.cols);
+        else if (narrow)
+            launch_k(k_trsm_panel<false, 8>, dim3((unsigned)cdiv(B.cols, 8)), 256, smem8, st, f, T.ptr, T.ld, ti,
+                     B.ptr, B.ld, (int)n, B.cols);
+        else if (f.p < (1u << 23))
+            launch_k(k_trsm_panel<true>, dim3((unsigned)cdiv(B.cols, PNL_COLS)), 256, smem, st, f, T.ptr, T.ld, ti,
+                     B.ptr, B.ld, (int)n, B.cols);
         else
-            launch_k(k_trsm_panel<false>, grid, 256, smem, st, f, T.ptr, T.ld, ti, B.ptr, B.ld, (int)n, B.cols);
+            launch_k(k_trsm_panel<false>, dim3((unsigned)cdiv(B.cols, PNL_COLS)), 256, smem, st, f, T.ptr, T.ld, ti,
+                     B.ptr, B.ld, (int)n, B.cols);
         ++g_launches;
         FFB_CHECK_LAUNCH();
         return;
