@@ -181,7 +181,6 @@ __global__ void __launch_bounds__(256) k_leaf64(Fp f, const uint32_t* A, int64_t
 // int64 entries, the same bounds with 64-bit products (96 p^2 < 2^59), 64-bit Barrett.
 struct LzNarrow {
     using T = int32_t;
-    static constexpr int VEC = 4;  // int4 words per 16 entries
     __device__ __forceinline__ static uint32_t off(const Fp& f) { return 96u * f.p * f.p; }
     __device__ __forceinline__ static uint32_t red(const Fp& f, T v, uint32_t o) {
         return red32(f, (uint32_t)v + o);
@@ -194,7 +193,6 @@ struct LzNarrow {
 };
 struct LzWide {
     using T = int64_t;
-    static constexpr int VEC = 8;
     __device__ __forceinline__ static uint64_t off(const Fp& f) { return 96ull * f.p * f.p; }
     __device__ __forceinline__ static uint32_t red(const Fp& f, T v, uint64_t o) {
         return red64(f, (uint64_t)v + o);
