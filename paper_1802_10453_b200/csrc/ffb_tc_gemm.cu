@@ -555,23 +555,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         uint32_t* tile = sEpi + (warp - 2) * 32 * 33;
         const uint32_t mu32 = (uint32_t)(0x100000000ull / f.p);
         const uint32_t bias = (uint32_t)((0x80000000ull) % f.p);
-        uint32_t wsh[5];
-        {
-            uint64_t w = 1 % f.p;
-            for (int s = 0; s < 5; ++s) {
-                wsh[s] = (uint32_t)w;
-                w = (w << 8) % f.p;
-            }
-        }
         mbar_wait(accfull, 0);
         tc_fence_after();
         const int rbase = m0 + 32 * q;
         for (int c = 0; c < LB_BN; c += 32) {
             if (n0 + c >= N) break;
-            uint32_t v[32];
+            // sum_s 2^(8s) class_s mod p: 64-bit sums of reduced terms (< 5 p^2 < 2^49), one
+            // 64-bit reduction per element; the class loop is not unrolled (code size: a short
+            // launch is otherwise bound by instruction fetch)
+            uint64_t v[32];
 #pragma unroll
             for (int j = 0; j < 32; ++j) v[j] = 0;
-#pragma unroll
+            uint32_t w = 1 % f.p;  // 2^(8s) mod p
+#pragma unroll 1
             for (int s = 0; s < 5; ++s) {
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(s * LB_BN + c), r);
@@ -582,11 +578,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                     uint32_t rr = x - qq * f.p;
                     if (rr >= f.p) rr -= f.p;
                     rr = fsub(f, rr, bias);                  // acc mod p
-                    v[j] = fadd(f, v[j], fmul(f, rr, wsh[s]));
+                    v[j] += (uint64_t)rr * w;
                 }
+                w = (uint32_t)(((uint64_t)w << 8) % f.p);
             }
 #pragma unroll
-            for (int j = 0; j < 32; ++j) tile[lane * 33 + j] = v[j];
+            for (int j = 0; j < 32; ++j) tile[lane * 33 + j] = red64(f, v[j]);
             __syncwarp();
             const int col = n0 + c + lane;
             const bool colok = col < N;
