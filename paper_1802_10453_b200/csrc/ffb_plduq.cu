@@ -351,6 +351,164 @@ __global__ void __launch_bounds__(256) k_row_detect(Fp f, const uint32_t* S, int
 }
 
 // ---------------------------------------------------------------------------
+// Row rank profile, register-resident (p < 4096; same contract as k_row_detect).
+// The stack [Epre; S] (kpre + b rows x s columns) lives in registers: warp w holds
+// rows w + NW u (u < RU), lane l the columns l + 32 q (q < NQ), as lazy sums (< p +
+// 128 p^2 < 2^32).  Rows are visited in rounds of NW (rows NW u .. NW u + NW - 1):
+// every warp reduces its row of the round, one barrier publishes the nonzero flags,
+// and the first nonzero row is the next pivot -- the pending rows before it are
+// dependent for good (the span only grows).  A pivot step is right-looking: the
+// owner normalizes its row at its first nonzero column and publishes it, one barrier,
+// then every warp subtracts it from its later rows (and, when the basis is written
+// out, from the earlier pivot rows: Gauss-Jordan, so Eout is fully reduced).  A
+// round costs one barrier, a pivot two; no per-row insertion chain.
+// ---------------------------------------------------------------------------
+template <int NQ, int RU, int NW>
+__global__ void __launch_bounds__(32 * NW) k_rrp(Fp f, const uint32_t* S, int64_t lds, int b, int s, int32_t* out,
+                                                 MboxPost mp, const uint32_t* Epre, const int32_t* kpre_ptr,
+                                                 uint32_t* Eout, int32_t* rho_out) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __shared__ uint32_t sinv[SINV_MAX];
+    __shared__ __align__(16) uint32_t prow[2][32 * NQ];
+    __shared__ int tflag[2][NW];
+    __shared__ int pcol_s[2];
+    __shared__ int16_t rho_s[RD_MAX_B], tof[RU * NW];
+    const SmemInv inv = stage_inverses(f, sinv);  // independent of the predecessor
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    const int kpre = kpre_ptr ? min(__ldcg(kpre_ptr), min(s, RD_MAX_B)) : 0;
+    const int nrows = min(kpre + b, RU * NW);
+    uint32_t v[RU][NQ];
+#pragma unroll
+    for (int u = 0; u < RU; ++u) {
+        const int i = NW * u + wp;
+        const uint32_t* src = i < kpre ? Epre + (int64_t)i * s : S + (int64_t)(i - kpre) * lds;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int c = lane + 32 * q;
+            v[u][q] = (i < nrows && c < s) ? __ldcg(src + c) : 0u;
+        }
+    }
+    const bool gj = Eout != nullptr;  // Gauss-Jordan: earlier pivot rows take the updates too
+    uint32_t ispiv = 0;               // bit u: this warp's row of round u is a pivot (warp-uniform)
+    int k = 0, kn = 0, tb = 0, pb = 0;
+    for (int u = 0; u < RU; ++u) {
+        const int base = NW * u;
+        if (base >= nrows) break;
+        unsigned pend = nrows - base >= NW ? (NW == 32 ? 0xffffffffu : (1u << NW) - 1u) : (1u << (nrows - base)) - 1u;
+        // the round's row lives in cur[] while the round runs (rows v[u] is stale until written back)
+        uint32_t cur[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            uint32_t x = v[0][q];
+#pragma unroll
+            for (int uu = 1; uu < RU; ++uu) x = uu == u ? v[uu][q] : x;
+            cur[q] = x;
+        }
+        while (pend) {
+            bool nz = false;
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                cur[q] = red32(f, cur[q]);
+                nz |= cur[q] != 0;
+            }
+            nz = __any_sync(0xffffffffu, nz);
+            if (lane == 0) tflag[tb][wp] = nz;
+            __syncthreads();
+            const unsigned nzm =
+                __ballot_sync(0xffffffffu, lane < NW && ((pend >> lane) & 1) && tflag[tb][lane & (NW - 1)]);
+            tb ^= 1;
+            if (!nzm) break;  // every pending row of the round is dependent
+            const int ws = __ffs(nzm) - 1;
+            pend &= ~((2u << ws) - 1u);
+            if (wp == ws) {  // normalize the pivot row at its first nonzero column, publish it
+                int cq = NQ;
+                unsigned bl = 0;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const unsigned bq = __ballot_sync(0xffffffffu, cur[q] != 0);
+                    if (cq == NQ && bq) {
+                        cq = q;
+                        bl = bq;
+                    }
+                }
+                const int cl = __ffs(bl) - 1;
+                uint32_t xp = cur[0];
+#pragma unroll
+                for (int q = 1; q < NQ; ++q) xp = q == cq ? cur[q] : xp;
+                const uint32_t il = inv(f, __shfl_sync(0xffffffffu, xp, cl));
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    cur[q] = red32(f, cur[q] * il);
+                    prow[pb][lane + 32 * q] = cur[q];
+                }
+                if (lane == 0) {
+                    pcol_s[pb] = 32 * cq + cl;
+                    rho_s[k] = (int16_t)(32 * cq + cl);
+                    tof[base + ws] = (int16_t)k;
+                }
+                ispiv |= 1u << u;
+            }
+            __syncthreads();
+            const int col = pcol_s[pb], cq = col >> 5, cl = col & 31;
+            uint32_t pr[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) pr[q] = prow[pb][lane + 32 * q];
+            pb ^= 1;
+            // rows of later rounds, and (Gauss-Jordan) earlier pivot rows: branch-free, a masked
+            // row adds 0; an unmasked row with a zero multiplier adds p * pr (= 0 mod p)
+            const uint32_t later = u + 1 < RU ? ~0u << (u + 1) : 0u;
+            const uint32_t upd = later | (gj ? ispiv & ~(1u << u) : 0u);
+#pragma unroll
+            for (int uu = 0; uu < RU; ++uu) {
+                uint32_t mv = v[uu][0];
+#pragma unroll
+                for (int q = 1; q < NQ; ++q) mv = q == cq ? v[uu][q] : mv;
+                const uint32_t mn = ((upd >> uu) & 1) ? f.p - red32(f, __shfl_sync(0xffffffffu, mv, cl)) : 0u;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) v[uu][q] += mn * pr[q];
+            }
+            {  // this round's rows after the pivot (and, Gauss-Jordan, a pivot row of this round)
+                uint32_t mv = cur[0];
+#pragma unroll
+                for (int q = 1; q < NQ; ++q) mv = q == cq ? cur[q] : mv;
+                const bool on = wp > ws || (gj && ((ispiv >> u) & 1) && wp != ws);
+                const uint32_t mn = on ? f.p - red32(f, __shfl_sync(0xffffffffu, mv, cl)) : 0u;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) cur[q] += mn * pr[q];
+            }
+            if (base + ws >= kpre) {
+                if (tid == 0) out[1 + kn] = base + ws - kpre;
+                ++kn;
+            }
+            ++k;
+        }
+#pragma unroll
+        for (int uu = 0; uu < RU; ++uu)
+            if (uu == u)
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) v[uu][q] = cur[q];
+    }
+    if (Eout) {  // the pivot rows, fully reduced, in pivot order
+#pragma unroll
+        for (int uu = 0; uu < RU; ++uu)
+            if ((ispiv >> uu) & 1) {
+                const int t = tof[NW * uu + wp];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int c = lane + 32 * q;
+                    if (c < s) Eout[(int64_t)t * s + c] = red32(f, v[uu][q]);
+                }
+            }
+        for (int t = tid; t < k; t += blockDim.x) rho_out[t] = rho_s[t];
+    }
+    if (tid == 0) {
+        out[0] = kn;
+        if (mp.dst) mbox_publish(mp, &kn, 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Candidate columns for the column rank profile of RI (k x n): CTA g scans
 // columns [g*CRP_W, (g+1)*CRP_W) in groups of CRP_G and keeps those
 // independent of the earlier columns of its range (a local CRP).  A dropped
@@ -1281,6 +1439,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         attrs.mark();
     }
     static const bool force_exact = getenv("FFB_PLDUQ_FORCE_FALLBACK") != nullptr;  // test hook
+    // register-resident row detection (k_rrp) for p < 4096; FFB_RD_BATCHED: the batched kernel (A/B hook)
+    static const bool rrp_env = getenv("FFB_RD_BATCHED") == nullptr;
+    const bool rrp = rrp_env && f.p < 4096u && f.mu32;
 
     // side stream for the Uhat updates (see absorb)
     // (per device: a thread may drive contexts on several GPUs)
@@ -1474,7 +1635,13 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         const MboxPost mp = io.post ? io.post() : MboxPost();
                         {
                             ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-                            if (wide)
+                            if (rrp && wide)
+                                launch_k(k_rrp<5, 16, 8>, 1, 256, 0, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp, nullptr,
+                                         nullptr, nullptr, nullptr);
+                            else if (rrp)
+                                launch_k(k_rrp<2, 20, 32>, 1, 1024, 0, st, f, Sc.ptr, Sc.ld, (int)bc, RD_NARROW, dinfo, mp,
+                                         nullptr, nullptr, nullptr, nullptr);
+                            else if (wide)
                                 launch_k(k_row_detect<5>, 1, 256, rd_smem_bytes((int)bc, SK), st, f, Sc.ptr, Sc.ld, (int)bc,
                                          SK, dinfo, mp, nullptr, nullptr, nullptr, nullptr, nullptr);
                             else
@@ -1532,8 +1699,12 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         const int64_t bcn = std::min<int64_t>(B, m - c0n);
                         // the reduced basis of S_I (side2) beside chunk c+1's sketch (side3),
                         // then the detection of c+1 modulo that basis (side2)
-                        launch_k(k_row_detect<3>, 1, 256, rd_smem_bytes(k, RD_PIPE), side2, f, Sfin.ptr, Sfin.ld, k,
-                                 RD_PIPE, pre_out, MboxPost(), nullptr, nullptr, nullptr, Epre, rho_pre);
+                        if (rrp)
+                            launch_k(k_rrp<3, 20, 8>, 1, 256, 0, side2, f, Sfin.ptr, Sfin.ld, k, RD_PIPE, pre_out,
+                                     MboxPost(), nullptr, nullptr, Epre, rho_pre);
+                        else
+                            launch_k(k_row_detect<3>, 1, 256, rd_smem_bytes(k, RD_PIPE), side2, f, Sfin.ptr, Sfin.ld,
+                                     k, RD_PIPE, pre_out, MboxPost(), nullptr, nullptr, nullptr, Epre, rho_pre);
                         ++g_launches;
                         FFB_CUDA(cudaStreamWaitEvent(side3, ev_gk, 0)); pdl_fence(side3);
                         SlotGuard slot3(4);
@@ -1551,9 +1722,13 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         pre_mp = io.post ? io.post() : MboxPost();
                         {
                             ProfScope ps(K_PLDUQ, side2, 0.0, 0.0);
-                            launch_k(k_row_detect<3>, 1, 256, rd_smem_bytes_pre((int)bcn, RD_PIPE), side2, f, Sn.ptr,
-                                     Sn.ld, (int)bcn, RD_PIPE, pinfo[pb], pre_mp, Epre, rho_pre, pre_out, nullptr,
-                                     nullptr);
+                            if (rrp)
+                                launch_k(k_rrp<3, 20, 8>, 1, 256, 0, side2, f, Sn.ptr, Sn.ld, (int)bcn, RD_PIPE,
+                                         pinfo[pb], pre_mp, Epre, pre_out, nullptr, nullptr);
+                            else
+                                launch_k(k_row_detect<3>, 1, 256, rd_smem_bytes_pre((int)bcn, RD_PIPE), side2, f,
+                                         Sn.ptr, Sn.ld, (int)bcn, RD_PIPE, pinfo[pb], pre_mp, Epre, rho_pre, pre_out,
+                                         nullptr, nullptr);
                             ++g_launches;
                             FFB_CHECK_LAUNCH();
                         }
@@ -1859,7 +2034,27 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
         FFB_CUDA(cudaEventSynchronize(e[1]));
         FFB_CUDA(cudaEventElapsedTime(&t, e[0], e[1]));
         ms[0] = t / reps;
-        FFB_CUDA(cudaMemcpy(out_k, info, 4, cudaMemcpyDeviceToHost));
+        FFB_CUDA(cudaMemcpy(out_k, info, (size_t)(1 + std::min(rows, cols)) * 4, cudaMemcpyDeviceToHost));
+        if (rows <= 128 && cols <= 160 && f.p < 4096u) {  // the register-resident kernel on the same sketch
+            int32_t* info2;
+            FFB_CUDA(cudaMalloc(&info2, (2 * RD_MAX_B + 16) * 4));
+            launch_k(k_rrp<5, 16, 8>, 1, 256, 0, st, f, d_in, cols, rows, cols, info2, MboxPost(), nullptr, nullptr,
+                     nullptr, nullptr);
+            FFB_CUDA(cudaEventRecord(e[2], st));
+            for (int i = 0; i < reps; ++i)
+                launch_k(k_rrp<5, 16, 8>, 1, 256, 0, st, f, d_in, cols, rows, cols, info2, MboxPost(), nullptr,
+                         nullptr, nullptr, nullptr);
+            FFB_CUDA(cudaEventRecord(e[3], st));
+            FFB_CUDA(cudaEventSynchronize(e[3]));
+            FFB_CUDA(cudaEventElapsedTime(&t, e[2], e[3]));
+            ms[1] = t / reps;
+            std::vector<int32_t> h2(1 + std::min(rows, cols));
+            FFB_CUDA(cudaMemcpy(h2.data(), info2, h2.size() * 4, cudaMemcpyDeviceToHost));
+            ms[2] = 1.0;  // identical row sets
+            for (int j = 0; j <= h2[0] && j < (int)h2.size(); ++j)
+                if (h2[j] != out_k[j]) ms[2] = 0.0;
+            FFB_CUDA(cudaFree(info2));
+        }
         FFB_CUDA(cudaFree(info));
     } else {
         const int k = rows;

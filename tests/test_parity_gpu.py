@@ -601,3 +601,32 @@ def test_band_schur_updates(gpu, oracle, t):
     env = dict(os.environ, FFB_NO_BAND="1")
     subprocess.run([sys.executable, "-c", code, out], check=True, env=env)
     assert np.array_equal(np.load(out), g.lower)
+
+
+@pytest.mark.parametrize("p", [2, 131, 4093])
+def test_plduq_staircase_wide(gpu, oracle, p):
+    """Chunk residuals R_I whose pivot columns spread over many column blocks (a staircase
+    basis over n = 9000 columns, chunk ranks 25 and one 40-row chunk), as in config 5's
+    large PLDUQs.  Bit-exact against the oracle."""
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(p + 21)
+    m, n, r = 896, 9000, 150
+    # staircase basis: row t is zero left of its start column, dense after it
+    starts = np.sort(rng.choice(n - 50, r, replace=False))
+    basis = rng.integers(0, p, (r, n)).astype(object)
+    for t in range(r):
+        basis[t, :starts[t]] = 0
+    perm = rng.permutation(r)
+    blocks, d = [], 0
+    for j in range(m // 128):
+        d = min(r, d + (40 if j == 3 else 25))
+        coef = rng.integers(0, p, (128, d)).astype(object)
+        blocks.append(coef.dot(basis[perm[:d]]) % p)
+    y = np.vstack(blocks).astype(np.uint64)
+    g = ffb.plduq(y, p, ctx=gpu)
+    o = oracle.plduq(p, y)
+    assert g.rank == o["rank"]
+    assert np.array_equal(g.row_perm.image_array(), o["row_image"])
+    assert np.array_equal(g.col_perm.image_array(), o["col_image"])
+    assert np.array_equal(g.lower, o["lower"]) and np.array_equal(g.upper, o["upper"])
+    assert np.array_equal(g.diag, o["diag"])

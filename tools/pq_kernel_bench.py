@@ -54,7 +54,8 @@ def main():
     for k in (0, 1, 8, 25, 64, 128):
         m = row_detect_input(rng, p, 128, 144, k) if k else np.zeros((128, 144), np.int64)
         ms, out = bench(ctx, p, 0, m)
-        print(json.dumps(dict(kernel="row_detect", b=128, s=144, k=k, k_found=out[0], us=round(ms[0] * 1e3, 2))))
+        print(json.dumps(dict(kernel="row_detect", b=128, s=144, k=k, k_found=out[0], us=round(ms[0] * 1e3, 2),
+                              rrp_us=round(ms[1] * 1e3, 2), rrp_identical=bool(ms[2] == 1.0))))
     cases = [tuple(int(x) for x in a.split(",")) for a in sys.argv[1:]] or \
         [(25, 8192, 20), (25, 8192, 400), (64, 8192, 40), (128, 16384, 100), (26, 16384, 33)]
     dump = os.environ.get("PQ_DUMP")  # an R_I written by FFB_PLDUQ_DUMP
