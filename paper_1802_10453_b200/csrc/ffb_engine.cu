@@ -242,8 +242,12 @@ __global__ void __launch_bounds__(512) k_fetch(uint32_t* dst, const uint32_t* sr
 }
 
 // Pinned upload ring: index arrays going down to the device.
+const int32_t* upload_into(ffb_context* c, int32_t* d, const int32_t* v, size_t n);
 const int32_t* upload(ffb_context* c, const int32_t* v, size_t n) {
-    int32_t* d = ws_vec<int32_t>(c, (int64_t)n);
+    return upload_into(c, ws_vec<int32_t>(c, (int64_t)n), v, n);
+}
+// ... into a given device buffer
+const int32_t* upload_into(ffb_context* c, int32_t* d, const int32_t* v, size_t n) {
     if (n == 0) return d;
     const size_t bytes = n * sizeof(int32_t);
     if (bytes > c->up_cap) {  // rare: larger than the ring, copy synchronously
@@ -432,6 +436,7 @@ struct Engine {
     cudaStream_t zst = nullptr;
     cudaEvent_t zev_fork = nullptr, zev_done = nullptr;
     bool zpending = false;
+    const uint32_t* z_mirrored = nullptr;  // the Z block whose lower part zst already restored
     void z_fork() {
         if (!zst) {
             int least = 0, greatest = 0;
@@ -617,10 +622,17 @@ struct Engine {
                 BandScope band(band_halo());
                 gemm(f, zst, GEMM_SUB, Z, G, false, X, false, ns, ns, r1);  // :315
                 g_tc_shared_sms = false;
+                // zero_leading_pairs' symmetric gather reads the lower part too: mirror it
+                // back here, beside Y's zero test and PLDUQ
+                if (band_halo() >= 0) {
+                    mirror_lower(zst, Z, band_halo());
+                    z_mirrored = Z.ptr;
+                }
                 z_done();
             }
             HFact f2 = zero_leading(Y, Z, rowsz, up[3], coff + r1, 0);  // :317
             join_z();
+            z_mirrored = nullptr;
             HFact h;  // (:332-334)
             h.rank = r1 + f2.rank;
             h.perm.resize(s);
@@ -687,6 +699,7 @@ struct Engine {
         }
         if (is_zero(Y, ytag)) {  // :274-290
             join_z();
+            z_mirrored = nullptr;
             std::vector<int32_t> rz(rows.begin() + m, rows.end());
             HFact f3 = dispatch(Z, rz, drows ? drows + m : nullptr, coff);
             const int64_t r3 = f3.rank;
@@ -708,7 +721,7 @@ struct Engine {
         uint32_t *d, *dinv;
     };
     double pq_t0 = 0;
-    Pl run_plduq(DMat Y) {
+    Pl run_plduq(DMat Y, const std::function<void(const std::vector<int32_t>&)>& pivots_ready = {}) {
         const int64_t m = Y.rows, n = Y.cols, mn = std::min(m, n);
         static const bool pq_pdl = getenv("FFB_PDL_NO_PLDUQ") == nullptr;  // bisection hook
         PdlScope pdl_scope(pq_pdl);
@@ -745,6 +758,7 @@ struct Engine {
             io.readback = [this](const void* p, size_t b) { return readback(c, p, b); };
             io.post = [this]() { return mbox_reserve(c); };
             io.wait = [this](const MboxPost& mp) { return mbox_wait(c, mp); };
+            io.pivots_ready = pivots_ready;
             io.Lo = Lo;
             io.Uo = Uo;
             io.d = pl.d;
@@ -789,7 +803,24 @@ struct Engine {
     HFact zero_leading_pairs(DMat Y, DMat Z, const std::vector<int32_t>& rows, int64_t coff) {
         const int64_t m = Y.rows, nz = Z.rows;
         const WsMark mk{c->ws_top};
-        Pl py = run_plduq(Y);  // :175
+        DMat Cp = ws_mat(c, nz, nz);  // C' = Q^T Z Q (:183)
+        int32_t* dq = ws_vec<int32_t>(c, nz);  // Q for the early gather (outside the PLDUQ's workspace)
+        // C' needs only Q = the PLDUQ's column image: once the pivots are known it is
+        // gathered on the Schur-update stream (after Z's update, mirrored back when
+        // band-only), beside the PLDUQ's factor phase on the engine stream
+        static const bool cp_overlap = getenv("FFB_NO_CP_OVERLAP") == nullptr;  // A/B hook
+        bool cp_done = false;
+        auto on_pivots = [&](const std::vector<int32_t>& qimg) {
+            upload_into(c, dq, qimg.data(), qimg.size());
+            z_fork();
+            GreenScope green(true);
+            if (band_halo() >= 0 && z_mirrored != Z.ptr) mirror_lower(zst, Z, band_halo());
+            z_mirrored = Z.ptr;
+            gather_sym(zst, Cp, Z, dq);
+            z_done();
+            cp_done = true;
+        };
+        Pl py = cp_overlap ? run_plduq(Y, on_pivots) : run_plduq(Y);  // :175
         const int64_t r = py.r;
         const std::vector<int32_t>& q = py.cimg;
 
@@ -799,10 +830,12 @@ struct Engine {
         for (int64_t a = 0; a < m; ++a) idy[a] = rows[py.rimg[a]];
         for (int64_t a = 0; a < nz; ++a) idz[a] = rows[m + q[a]];
         const auto up = upload_batch<3>(c, {&q, &idy, &idz});
-        DMat Cp = ws_mat(c, nz, nz);  // C' = Q^T Z Q (:183)
         join_z();
-        if (band_halo() >= 0) mirror_lower(st, Z, band_halo());  // Z may hold a band-only update
-        gather_sym(st, Cp, Z, up[0]);
+        if (!cp_done) {
+            if (band_halo() >= 0 && z_mirrored != Z.ptr) mirror_lower(st, Z, band_halo());  // band-only update
+            gather_sym(st, Cp, Z, up[0]);
+        }
+        z_mirrored = nullptr;
         DMat C1 = Cp.sub(0, 0, r, r), C2 = Cp.sub(0, r, r, nz - r), C3 = Cp.sub(r, r, nz - r, nz - r);
         DMat U1 = py.U.sub(0, 0, r, r), V1 = py.U.sub(0, r, r, nz - r);
         DMat UpT = ws_mat(c, nz, r);  // [U1^T; V1^T]

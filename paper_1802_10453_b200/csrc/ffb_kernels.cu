@@ -40,8 +40,8 @@ void Profiler::flush() {
         float t = 0.f;
         if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) ms[r.cls] += t;
         if (trace)
-            fprintf(trace, "%d %lld %lld %lld %.4f %lld\n", r.cls, (long long)r.m, (long long)r.n, (long long)r.k, t,
-                    (long long)r.node);
+            fprintf(trace, "%d %lld %lld %lld %.4f %lld %.6g\n", r.cls, (long long)r.m, (long long)r.n,
+                    (long long)r.k, t, (long long)r.node, r.ops);
         ops[r.cls] += r.ops;
         bytes[r.cls] += r.bytes;
         cnt[r.cls] += 1;

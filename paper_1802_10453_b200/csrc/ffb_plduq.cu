@@ -1924,6 +1924,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         out.cimg = pcol_rows;
         for (int64_t j = 0; j < n; ++j)
             if (!isp[j]) out.cimg.push_back((int32_t)j);
+        if (io.pivots_ready && r > 0) io.pivots_ready(out.cimg);
         if (r == 0) {
             if (exact) break;
             // certificate: Y must be zero

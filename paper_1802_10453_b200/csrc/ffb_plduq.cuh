@@ -44,6 +44,9 @@ struct PlduqIO {
     // optional: reserve a kernel-published read-back, and wait for it
     std::function<MboxPost()> post;
     std::function<const void*(const MboxPost&)> wait;
+    // optional: called with the column image as soon as the pivots are known (before the
+    // factors are formed; again if a failed certificate forces the exact retry)
+    std::function<void(const std::vector<int32_t>&)> pivots_ready;
     DMat Lo, Uo;        // m x min(m,n) and min(m,n) x n outputs
     uint32_t* d = nullptr;
     uint32_t* dinv = nullptr;

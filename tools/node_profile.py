@@ -42,7 +42,7 @@ def main():
     tot = defaultdict(lambda: [0, 0.0])
     shapes = defaultdict(lambda: [0, 0.0])
     for line in open(path):
-        cls, m, nn, k, t, node = line.split()
+        cls, m, nn, k, t, node = line.split()[:6]
         if CLASSES[int(cls)] in ("gemm", "trsm"):
             def b2(x):
                 x = abs(int(x))
