@@ -761,7 +761,8 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     Fp f, const uint32_t* RI, int64_t ldr, int k, const int32_t* lists,
     const int32_t* counts, int nblk, int32_t* cand_g, int rc_cap, const int32_t* I, int64_t c0,
     const uint32_t* S, int64_t lds, int s, uint32_t* Kinv, int32_t* Jout, uint32_t* UO, int64_t lduo,
-    int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r, int32_t* fail, int si_off, int s_compact) {
+    int32_t* uhat_col, int32_t* prow, int32_t* pcol, int64_t r, int32_t* fail, int si_off, int s_compact,
+    uint32_t* Ld, uint32_t* dval) {
     FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint32_t sm[];
     __shared__ int32_t off[1025];
@@ -917,6 +918,13 @@ __global__ void __launch_bounds__(256) k_crp_finish(
             for (int j = lane; j <= t; j += 32) gi[j] = fmsub(f, gi[j], m, gt[j]);
         }
         __syncthreads();
+    }
+    // 2b. the chunk's block of the PLDUQ's D and of D^-1 L^-1 (row order = pivot order):
+    //     R_I = L D U'' with U'' the chunk's rows of the echelon U, so U'' = (D^-1 L^-1) R_I
+    if (Ld) {
+        for (int t = wp; t < k; t += 8)
+            for (int j = lane; j < k; j += 32) Ld[(int64_t)t * k + j] = j <= t ? fmul(f, G[(size_t)t * k + j], dinv[t]) : 0u;
+        for (int t = tid; t < k; t += 256) dval[t] = M[(size_t)t * Cx + pci[t]];
     }
     // 3. back substitution X = U'^-1 L^-1, U'[t][t'] = M[t][pci[t']]
     for (int tp = k - 1; tp > 0; --tp) {
@@ -1407,6 +1415,11 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     DMat RIb[2] = {ws.mat(B, n), ws.mat(B, n)};
     DMat RI = RIb[0], Gs = ws.mat(Bmax, std::max<int64_t>(mn, 1));
     DMat Kinv = ws.mat(B, B), Gi = ws.mat(B, std::max<int64_t>(mn, 1)), Gi2 = ws.mat(B, std::max<int64_t>(mn, 1));
+    // the echelon U of the PLDUQ, chunk by chunk: rows (D^-1 L^-1)_c R_I in pivot order, natural
+    // columns (k_crp_finish's Ld block times R_I), with D written into io.d as the chunks go;
+    // the factor phase then needs no LDU of K (FFB_PLDUQ_LDU: the LDU-based phase, A/B hook)
+    static const bool ufull_env = getenv("FFB_PLDUQ_LDU") == nullptr;
+    DMat Ldb = ws.mat(B, B), Ufull = ufull_env ? ws.mat(std::max<int64_t>(mn, 1), n) : DMat{};
     DMat Gi3 = ws.mat(B, std::max<int64_t>(mn, 1)), Cg = ws.mat(B, B);
     DMat Upd = ws.mat(std::max<int64_t>(mn, 1), B);
     const int nblk0 = (int)cdiv(n, CRP_W);
@@ -1524,6 +1537,11 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             GreenScope green(us != st);
             SlotGuard slot(us == st ? g_slot : 1);
             gemm(f, us, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);  // Unew = Kc^-1 R_I
+            if (ufull_env && paired) {  // the chunk's rows of the echelon U (before RI is reused)
+                DMat Ldk = Ldb.sub(0, 0, k, k);
+                Ldk.ld = k;
+                gemm(f, us, GEMM_SET, Ufull.sub(r, 0, k, n), Ldk, false, RIk, false, k, n, k);
+            }
             FFB_CUDA(cudaEventRecord(ev_un, us));
             if (t1_wait) {  // the next chunk's T1 reads Uhat_old first
                 FFB_CUDA(cudaStreamWaitEvent(us, ev_t1, 0)); pdl_fence(us);
@@ -1788,7 +1806,8 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     launch_k(k_crp_finish, 1, 256, cfmem, st, f, RI.ptr, RI.ld, k, lists[0], counts[0], nblk0,
                                                         (int32_t*)re_scratch, rc_cap, dI, base, Sfin.ptr, Sfin.ld, SK,
                                                         Kik.ptr, lists[1], UO.ptr, UO.ld, d_uhat_col,
-                                                        d_prow, d_pcol, r, dflag, si_off, compact ? 1 : 0);
+                                                        d_prow, d_pcol, r, dflag, si_off, compact ? 1 : 0,
+                                                        Ldb.ptr, io.d + r);
                     ++g_launches;
                     FFB_CHECK_LAUNCH();
                 }
@@ -1934,7 +1953,6 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             exact = true;
             continue;
         }
-        DMat Kf = ws.mat(r, r);
         // every index array of phase 2 and the certificate in one upload (one fetch launch)
         const int64_t rA = (r + 3) & ~3, nA = (n + 3) & ~3, mA = (m + 3) & ~3;
         std::vector<int32_t> idx((size_t)(3 * rA + nA + 2 * mA), 0);
@@ -1951,13 +1969,28 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         const int32_t* didx = io.upload(idx);
         const int32_t* dpr = didx;
         const int32_t* dpc = didx + rA;
+        DMat Uo = io.Uo.sub(0, 0, r, n);
+        const int32_t* dcimg = didx + 2 * rA;
+        const int32_t* dnp = nullptr;
+        if (!exact && ufull_env) {
+            // U = the echelon rows gathered by Q; D from the chunks; [L1; M1] = Y[P, pc] U1^-1 D^-1
+            // for all m rows at once (K = L1 D U1 gives L1 exactly: unit lower, no LDU of K)
+            gather2d(st, Uo, Ufull.sub(0, 0, r, n), nullptr, dcimg, 0);
+            invert_vec(f, st, io.dinv, io.d, r);
+            DMat T = ws.mat(m, r), Tt = ws.mat(r, m), U1t = ws.mat(r, r);
+            gather2d(st, T, Y, didx + 2 * rA + nA + mA, dpc, 0);
+            transpose(st, Tt, T);
+            transpose(st, U1t, Uo.sub(0, 0, r, r));
+            trsm_lower_unit(f, st, U1t, Tt);
+            scale_T(f, st, io.Lo.sub(0, 0, m, r), Tt, io.dinv);
+            if (m > r) dnp = didx + 2 * rA + nA;
+        } else {
+        DMat Kf = ws.mat(r, r);
         gather2d(st, Kf, Y, dpr, dpc, 0);
         ldu_inplace(f, st, Kf, ws, dflag);
         launch_k(k_unpack_l, rgrid(r, r), 256, 0, st, io.Lo.ptr, io.Lo.ld, Kf.ptr, Kf.ld, r, io.d, 1 % f.p);
         ++g_launches;
         invert_vec(f, st, io.dinv, io.d, r);
-        DMat Uo = io.Uo.sub(0, 0, r, n);
-        const int32_t* dcimg = didx + 2 * rA;
         {
             // U = D^-1 L1^-1 Y[pr, Q].  The row loop left Uhat = Y[pr, pcu]^-1 Y[pr, :]
             // (fully reduced: identity on its pivot columns pcu), and Y[pr, pcu] = K Pi with
@@ -1969,7 +2002,6 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             ++g_launches;
             gemm(f, st, GEMM_SET, Uo, U1, false, Ug, false, r, n, r);
         }
-        const int32_t* dnp = nullptr;
         if (m > r) {
             dnp = didx + 2 * rA + nA;
             DMat T = ws.mat(m - r, r), Tt = ws.mat(r, m - r), U1t = ws.mat(r, r);
@@ -1978,6 +2010,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             transpose(st, U1t, Uo.sub(0, 0, r, r));
             trsm_lower_unit(f, st, U1t, Tt);
             scale_T(f, st, io.Lo.sub(r, 0, m - r, r), Tt, io.dinv);
+        }
         }
         if (exact) {
             if (*(const int32_t*)io.readback(dflag, 4)) throw Status(FFB_ERROR, "plduq: singular pivot block");
@@ -2094,7 +2127,7 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
                 const size_t cfmem = cf_smem_bytes(k, nblk0, &rc_cap, &si_off);
                 launch_k(k_crp_finish, 1, 256, cfmem, st, f, d_in, n, k, lists0, counts0, nblk0, (int32_t*)re_scratch,
                                                     rc_cap, dI, 0, nullptr, 0, 0, Kinv, lists1, nullptr, 0, ucol,
-                                                    prow, pcol, 0, flag, si_off, 0);
+                                                    prow, pcol, 0, flag, si_off, 0, nullptr, nullptr);
             }
             FFB_CUDA(cudaEventRecord(e[2], st));
             FFB_CUDA(cudaEventRecord(e[3], st));
