@@ -619,6 +619,124 @@ __global__ void __launch_bounds__(256) k_crp_list(Fp f, const uint32_t* RI, int6
 }
 
 // ---------------------------------------------------------------------------
+// Local CRP of a 256-column block, register-resident (k <= K <= 32, p < 4096;
+// same contract as k_crp_list).  Thread t owns column c0 + t, its k entries in
+// registers.  Gaussian elimination by pivot steps, not by columns: with the
+// pivots so far applied (right-looking), a column is independent of the earlier
+// ones iff its residual is nonzero on a row that is not yet a pivot row, so the
+// next CRP column is the first such column right of the last one (one block
+// min-reduction), and the columns skipped on the way are dependent for good
+// (later pivot rows are zero there).  Its owner takes the first live row with a
+// nonzero as the pivot row and publishes its column; every later column c
+// subtracts v_jp * (v_c[pr] / x).  Two barriers per pivot, none per dependent
+// column.  Entries are never reduced: each pivot adds < p^2, so they stay below
+// p + 32 p^2 < 2^32, and a zero test is one multiplication by p^-1 mod 2^32 (odd
+// p: p | v iff v p^-1 mod 2^32 <= (2^32 - 1) / p; p = 2: the low bit).
+// ---------------------------------------------------------------------------
+struct ZeroTest {
+    // odd p: p^-1 mod 2^32 and (2^32 - 1) / p; p = 2: 2^31 and 0 (v 2^31 mod 2^32 != 0 iff v odd)
+    uint32_t pinv, thr;
+    __device__ explicit ZeroTest(uint32_t p) {
+        uint32_t x = p;  // Newton: x = p^-1 mod 2^(2^i) (odd p)
+#pragma unroll
+        for (int i = 0; i < 5; ++i) x *= 2u - p * x;
+        pinv = (p & 1) ? x : 0x80000000u;
+        thr = (p & 1) ? 0xffffffffu / p : 0u;
+    }
+    __device__ __forceinline__ bool nonzero(uint32_t v) const { return v * pinv > thr; }
+};
+// v[idx] with a log-depth select tree (idx < K, K a power of two)
+template <int K>
+__device__ __forceinline__ uint32_t sel_tree(const uint32_t (&v)[K], int idx) {
+    uint32_t t[K / 2];
+#pragma unroll
+    for (int i = 0; i < K / 2; ++i) t[i] = (idx & 1) ? v[2 * i + 1] : v[2 * i];
+#pragma unroll
+    for (int w = K / 4, b = 2; w >= 1; w /= 2, b *= 2)
+#pragma unroll
+        for (int i = 0; i < w; ++i) t[i] = (idx & b) ? t[2 * i + 1] : t[2 * i];
+    return t[0];
+}
+// bit i set iff v[i] != 0 mod p, OR-tree
+template <int K>
+__device__ __forceinline__ uint32_t nz_mask(const ZeroTest& zt, const uint32_t (&v)[K]) {
+    uint32_t t[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) t[i] = (uint32_t)zt.nonzero(v[i]) << i;
+#pragma unroll
+    for (int w = K / 2; w >= 1; w /= 2)
+#pragma unroll
+        for (int i = 0; i < w; ++i) t[i] |= t[i + w];
+    return t[0];
+}
+template <int K>
+__global__ void __launch_bounds__(256) k_crp_list_reg(Fp f, const uint32_t* RI, int64_t ldr, int k, int64_t n,
+                                                      int32_t* out, int32_t* ocount) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    __shared__ uint32_t sinv[SINV_MAX];
+    __shared__ __align__(16) uint32_t raw[2][32];  // the pivot column (owner's registers)
+    __shared__ __align__(16) uint32_t qcol[2][32];  // p - v_jp[i] (reduced) on live rows != pr, else 0
+    __shared__ int wmin[2][8];
+    __shared__ int prow_s[2];
+    __shared__ uint32_t xinv_s[2];
+    const SmemInv inv = stage_inverses(f, sinv);  // independent of the predecessor
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    const int64_t c0 = (int64_t)blockIdx.x * CRP_W;
+    const bool have = c0 + tid < n;
+    const ZeroTest zt(f.p);
+    uint32_t v[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) v[i] = (have && i < k) ? __ldcg(RI + (int64_t)i * ldr + c0 + tid) : 0u;
+    uint32_t live = k >= 32 ? 0xffffffffu : (1u << k) - 1u;  // rows not yet pivot rows (uniform)
+    int last = -1, nb = 0, par = 0;
+    int32_t* o = out + (int64_t)blockIdx.x * k;
+    for (;;) {
+        const uint32_t nzm = nz_mask<K>(zt, v) & live;
+        const int cand = __reduce_min_sync(0xffffffffu, (nzm && tid > last) ? tid : CRP_W);
+        if (lane == 0) wmin[par][wp] = cand;
+        __syncthreads();
+        int jp = wmin[par][0];
+#pragma unroll
+        for (int w = 1; w < 8; ++w) jp = min(jp, wmin[par][w]);
+        if (jp >= CRP_W) break;
+        if (wp == (jp >> 5)) {  // the owner's warp publishes the pivot column
+            if (tid == jp) {
+                const int pr = __ffs(nzm) - 1;
+                const uint32_t x = sel_tree<K>(v, pr);
+#pragma unroll
+                for (int i = 0; i < K; i += 4)
+                    *reinterpret_cast<uint4*>(&raw[par][i]) = make_uint4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                prow_s[par] = pr;
+                xinv_s[par] = inv(f, red32(f, x));
+                o[nb] = (int32_t)(c0 + jp);
+            }
+            __syncwarp();
+            const int pr = prow_s[par];
+            qcol[par][lane] = (lane < K && ((live >> lane) & 1) && lane != pr) ? f.p - red32(f, raw[par][lane]) : 0u;
+        }
+        __syncthreads();
+        const int pr = prow_s[par];
+        const uint32_t xi = xinv_s[par];
+        live &= ~(1u << pr);
+        last = jp;
+        ++nb;
+        if (!live) break;
+        const uint32_t b = tid > jp ? red32(f, red32(f, sel_tree<K>(v, pr)) * xi) : 0u;  // v_c[pr] / x
+#pragma unroll
+        for (int i = 0; i < K; i += 4) {
+            const uint4 q = *reinterpret_cast<const uint4*>(&qcol[par][i]);
+            v[i] += q.x * b;
+            v[i + 1] += q.y * b;
+            v[i + 2] += q.z * b;
+            v[i + 3] += q.w * b;
+        }
+        par ^= 1;
+    }
+    if (tid == 0) ocount[blockIdx.x] = nb;
+}
+
+// ---------------------------------------------------------------------------
 // RPM of the chunk's pivot rows from the level-0 candidates (1 CTA).  Every
 // column dropped by a level-0 scan depends on earlier columns, so the RPM of
 // R_I equals the RPM of R_I restricted to the candidate columns C (ascending).
@@ -757,6 +875,17 @@ __host__ __device__ inline size_t cf_smem_bytes(int k, int nblk, int* rc_cap, in
     *si_off = -1;
     return base * 4;
 }
+// phase timestamps of the last k_crp_finish (globaltimer, thread 0; read by dbg_pq_bench)
+__device__ unsigned long long g_cf_stamp[8];
+#define CF_STAMP(i)                                                                           \
+    do {                                                                                      \
+        __syncthreads();                                                                      \
+        if (threadIdx.x == 0) {                                                               \
+            unsigned long long t_;                                                            \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                            \
+            g_cf_stamp[i] = t_;                                                               \
+        }                                                                                     \
+    } while (0)
 __global__ void __launch_bounds__(256) k_crp_finish(
     Fp f, const uint32_t* RI, int64_t ldr, int k, const int32_t* lists,
     const int32_t* counts, int nblk, int32_t* cand_g, int rc_cap, const int32_t* I, int64_t c0,
@@ -775,6 +904,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     __shared__ uint32_t sinv[SINV_MAX];
     __shared__ int total;
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    CF_STAMP(0);
     const SmemInv inv = stage_inverses(f, sinv);
     if (wp == 0) {  // exclusive offsets of the level-0 lists
         int run = 0;
@@ -845,6 +975,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
     asm volatile("cp.async.commit_group;" ::: "memory");
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
+    CF_STAMP(1);
     // 2. row-order leftmost elimination on M, tracking L^-1 in G.  The leading
     //    entry of row t: each thread scans a strided slice, warps reduce, one
     //    barrier combines (lead8 rotates over 2 slots, so no reset barrier).
@@ -919,6 +1050,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         }
         __syncthreads();
     }
+    CF_STAMP(2);
     // 2b. the chunk's block of the PLDUQ's D and of D^-1 L^-1 (row order = pivot order):
     //     R_I = L D U'' with U'' the chunk's rows of the echelon U, so U'' = (D^-1 L^-1) R_I
     if (Ld) {
@@ -940,6 +1072,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         }
         __syncthreads();
     }
+    CF_STAMP(3);
     // 4. outputs: J = sorted pivot columns, sigma[t] = rank of row t's column,
     //    Kinv row sigma[t] = X[t]
     for (int t = tid; t < k; t += 256) {
@@ -958,6 +1091,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
             Kinv[(int64_t)sig[t] * k + j] = v;
         }
     }
+    CF_STAMP(4);
     if (S) {  // UO rows from the k sketch rows S_I (copied early, or staged now in the free M buffer)
         uint32_t* SI = si_early ? sm + si_off : M;
         if (!si_early)
@@ -990,6 +1124,7 @@ __global__ void __launch_bounds__(256) k_crp_finish(
         prow[r + t] = (int32_t)(c0 + Is[t]);
         pcol[r + t] = pcv[t];
     }
+    CF_STAMP(5);
 }
 
 // ---------------------------------------------------------------------------
@@ -1455,6 +1590,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     // register-resident row detection (k_rrp) for p < 4096; FFB_RD_BATCHED: the batched kernel (A/B hook)
     static const bool rrp_env = getenv("FFB_RD_BATCHED") == nullptr;
     const bool rrp = rrp_env && f.p < 4096u && f.mu32;
+    // register-resident local CRPs (k_crp_list_reg) for k <= 32, p < 2^16; FFB_CRP_SCAN: the scan kernel (A/B hook)
+    static const bool crp_reg_env = getenv("FFB_CRP_SCAN") == nullptr;
+    const bool crp_reg = crp_reg_env && f.p < 4096u && f.mu32;
 
     // side stream for the Uhat updates (see absorb)
     // (per device: a thread may drive contexts on several GPUs)
@@ -1789,7 +1927,12 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 {
                     ProfScope ps(K_PQ_CRP, st, 0.0, 0.0);
                     // level 0: local CRPs of 256-column blocks (parallel)
-                    launch_k(k_crp_list, nblk0, 256, crp_smem, st, f, RI.ptr, RI.ld, k, n, lists[0], counts[0]);
+                    if (crp_reg && k <= 16)
+                        launch_k(k_crp_list_reg<16>, nblk0, 256, 0, st, f, RI.ptr, RI.ld, k, n, lists[0], counts[0]);
+                    else if (crp_reg && k <= 32)
+                        launch_k(k_crp_list_reg<32>, nblk0, 256, 0, st, f, RI.ptr, RI.ld, k, n, lists[0], counts[0]);
+                    else
+                        launch_k(k_crp_list, nblk0, 256, crp_smem, st, f, RI.ptr, RI.ld, k, n, lists[0], counts[0]);
                     ++g_launches;
                 }
                 if (compact) {
@@ -2103,6 +2246,9 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
         int32_t *lists0, *counts0, *lists1, *dsig, *flag, *ucol, *prow, *pcol, *dI;
         uint32_t *re_scratch, *Kinv;
         FFB_CUDA(cudaMalloc(&lists0, (size_t)nblk0 * k * 4));
+        int32_t *lists_r, *counts_r;
+        FFB_CUDA(cudaMalloc(&lists_r, (size_t)nblk0 * k * 4));
+        FFB_CUDA(cudaMalloc(&counts_r, (size_t)nblk0 * 4));
         FFB_CUDA(cudaMalloc(&counts0, (size_t)nblk0 * 4));
         FFB_CUDA(cudaMalloc(&lists1, (size_t)k * 4 + 64));
         FFB_CUDA(cudaMalloc(&dsig, (size_t)k * 4 + 64));
@@ -2130,6 +2276,10 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
                                                     prow, pcol, 0, flag, si_off, 0, nullptr, nullptr);
             }
             FFB_CUDA(cudaEventRecord(e[2], st));
+            if (k <= 16 && f.p < 4096u)
+                launch_k(k_crp_list_reg<16>, nblk0, 256, 0, st, f, d_in, n, k, n, lists_r, counts_r);
+            else if (k <= 32 && f.p < 4096u)
+                launch_k(k_crp_list_reg<32>, nblk0, 256, 0, st, f, d_in, n, k, n, lists_r, counts_r);
             FFB_CUDA(cudaEventRecord(e[3], st));
             FFB_CUDA(cudaEventSynchronize(e[3]));
             if (i == 0) continue;  // warm-up
@@ -2139,13 +2289,31 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
             }
         }
         for (int j = 0; j < 3; ++j) ms[j] = acc[j] / reps;
+        {  // the register-resident list kernel must give the same lists
+            std::vector<int32_t> ha((size_t)nblk0 * (k + 1)), hb((size_t)nblk0 * (k + 1));
+            FFB_CUDA(cudaMemcpy(ha.data(), counts0, (size_t)nblk0 * 4, cudaMemcpyDeviceToHost));
+            FFB_CUDA(cudaMemcpy(hb.data(), counts_r, (size_t)nblk0 * 4, cudaMemcpyDeviceToHost));
+            std::vector<int32_t> la((size_t)nblk0 * k), lb((size_t)nblk0 * k);
+            FFB_CUDA(cudaMemcpy(la.data(), lists0, la.size() * 4, cudaMemcpyDeviceToHost));
+            FFB_CUDA(cudaMemcpy(lb.data(), lists_r, lb.size() * 4, cudaMemcpyDeviceToHost));
+            int same = 1;
+            for (int b = 0; b < nblk0 && same; ++b) {
+                if (ha[b] != hb[b]) same = 0;
+                for (int t = 0; t < ha[b] && same; ++t) same = la[(size_t)b * k + t] == lb[(size_t)b * k + t];
+            }
+            out_k[1 + 2 * k] = (k <= 32 && f.p < 4096u) ? same : -1;
+            unsigned long long st8[8];
+            FFB_CUDA(cudaMemcpyFromSymbol(st8, g_cf_stamp, sizeof(st8)));
+            for (int q = 0; q < 5; ++q) out_k[2 + 2 * k + q] = (int32_t)(st8[q + 1] - st8[q]);  // ns per phase
+        }
         int32_t hf = 0;
         FFB_CUDA(cudaMemcpy(&hf, flag, 4, cudaMemcpyDeviceToHost));
         out_k[0] = hf;
         FFB_CUDA(cudaMemcpy(out_k + 1, lists1, (size_t)k * 4, cudaMemcpyDeviceToHost));
         FFB_CUDA(cudaMemcpy(out_k + 1 + k, dsig, (size_t)k * 4, cudaMemcpyDeviceToHost));
         for (void* q : {(void*)lists0, (void*)counts0, (void*)lists1, (void*)dsig, (void*)flag, (void*)ucol,
-                        (void*)prow, (void*)pcol, (void*)dI, (void*)Kinv, (void*)re_scratch})
+                        (void*)prow, (void*)pcol, (void*)dI, (void*)Kinv, (void*)re_scratch, (void*)lists_r,
+                        (void*)counts_r})
             FFB_CUDA(cudaFree(q));
     }
     FFB_CHECK_LAUNCH();

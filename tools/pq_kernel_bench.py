@@ -75,6 +75,8 @@ def main():
         ms, out = bench(ctx, p, 1, m)
         print(json.dumps(dict(kernel="crp", k=k, n=n, nz=nz, fail=out[0],
                               crp_list_us=round(ms[0] * 1e3, 2), finish_us=round(ms[1] * 1e3, 2),
+                              list_reg_us=round(ms[2] * 1e3, 2), list_reg_same=out[1 + 2 * k],
+                              finish_phase_us=[round(x / 1e3, 2) for x in out[2 + 2 * k:7 + 2 * k]],
                               jsorted=bool(all(out[1 + i] < out[2 + i] for i in range(k - 1))))))
 
 
