@@ -585,8 +585,10 @@ struct Engine {
         const int64_t s = A.rows, m = s / 2, ns = s - m;
         const WsMark mk{c->ws_top};
         std::vector<int32_t> rows1(rows.begin(), rows.begin() + m);
+        phase_mark("rs: begin", s, st);
         HFact f1 = dispatch(A.sub(0, 0, m, m), rows1, drows, coff);  // :303
         const int64_t r1 = f1.rank;
+        phase_mark("rs: A1 factored", s, st);
 
         // B' = P1^T B (:308) and [L1; M1] in f1's position order (from Lg), one launch
         DMat BP = ws_mat(c, m, ns);
@@ -602,7 +604,9 @@ struct Engine {
         DMat LM = ws_mat(c, m, r1);
         gather_rows2(st, BP, A, up[0], m, LM, Lg, up[1], coff);
         DMat X = BP.sub(0, 0, r1, ns);
+        phase_mark("rs: B' gathered", s, st);
         trsm_lower_unit(f, st, LM.sub(0, 0, r1, r1), X);  // :310
+        phase_mark("rs: X = L1^-1 B'", s, st);
         DMat Y = BP.sub(r1, 0, m - r1, ns);
         DMat G = ws_mat(c, ns, r1);
         DMat Z = A.sub(m, m, ns, ns);
@@ -630,7 +634,9 @@ struct Engine {
                 }
                 z_done();
             }
+            phase_mark("rs: Y updated, Z forked", s, st);
             HFact f2 = zero_leading(Y, Z, rowsz, up[3], coff + r1, 0);  // :317
+            phase_mark("rs: zero_leading done", s, st);
             join_z();
             z_mirrored = nullptr;
             HFact h;  // (:332-334)
@@ -820,7 +826,9 @@ struct Engine {
             z_done();
             cp_done = true;
         };
+        phase_mark("zlp: begin", m + nz, st);
         Pl py = cp_overlap ? run_plduq(Y, on_pivots) : run_plduq(Y);  // :175
+        phase_mark("zlp: plduq done", m + nz, st);
         const int64_t r = py.r;
         const std::vector<int32_t>& q = py.cimg;
 
@@ -852,12 +860,15 @@ struct Engine {
         }
         DMat X = ws_mat(c, r, r);
         fill_words(st, (uint32_t*)c->flag, 1, 0u);
+        phase_mark("zlp: C' ready, U^T", m + nz, st);
         trssyr2k_dev(U1, U1T, C1, X, c->flag);  // :202
+        phase_mark("zlp: trssyr2k", m + nz, st);
         DMat G12 = ws_mat(c, nz, r);  // [G1; G2]
         scale_T(f, st, G12.sub(0, 0, r, r), X, py.dinv);  // G1 = (diag(d)^-1 X)^T (:203)
         if (f.char2) add_scaled_rows_upper(f, st, X, U1, delta);  // X += Delta U1 (:204-208)
         gemm(f, st, GEMM_SUB, C2, X, true, V1, false, r, nz - r, r);  // C2 -= X^T V1 (:210)
         trsm_lower_unit(f, st, U1T, C2);  // Y2 = U1^-T C2 (:211)
+        phase_mark("zlp: C2, Y2", m + nz, st);
         {
             BandScope band(band_halo());  // C3 is symmetric and read like Z
             // C3 -= Y2^T V1 + V1^T Y2 (:213), both terms into one accumulator
@@ -878,7 +889,9 @@ struct Engine {
         write_pair_diag(f, st, D, coff, py.d, py.dinv, delta, r);  // :254-260
 
         std::vector<int32_t> rows3(idz.begin() + r, idz.end());
+        phase_mark("zlp: C3 updated, L scattered", m + nz, st);
         HFact f3 = dispatch(C3, rows3, didz + r, coff + 2 * r);  // :217
+        phase_mark("zlp: C3 factored", m + nz, st);
         const int64_t r3 = f3.rank;
 
         HFact h;  // P_i interleave + rotations (:226-251)
@@ -983,6 +996,7 @@ DevFact run_ldlt(ffb_context* c, const Fp& f, DMat W, int variant, int64_t thres
     for (int64_t i = 0; i < n; ++i) rows[i] = (int32_t)i;
     if (n > 0) {
         HFact h = e.dispatch(W, rows, upload(c, rows), 0);
+        phase_dump(st);
         out.rank = h.rank;
         out.perm = std::move(h.perm);
     }

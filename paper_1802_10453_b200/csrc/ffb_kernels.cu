@@ -76,6 +76,40 @@ ProfScope::~ProfScope() {
     g_prof->recs.push_back(rec);
 }
 
+namespace {
+struct PhaseRec { const char* label; int64_t size; cudaEvent_t e; };
+thread_local std::vector<PhaseRec> g_phase;
+const char* phase_path() {
+    static const char* p = getenv("FFB_PHASE_TRACE");
+    return p;
+}
+}  // namespace
+void phase_mark(const char* label, int64_t size, cudaStream_t st) {
+    static const int64_t min_size = getenv("FFB_PHASE_MIN") ? atoll(getenv("FFB_PHASE_MIN")) : 8192;
+    if (!phase_path() || size < min_size) return;
+    cudaEvent_t e;
+    FFB_CUDA(cudaEventCreate(&e));
+    FFB_CUDA(cudaEventRecord(e, st));
+    g_phase.push_back({label, size, e});
+}
+void phase_dump(cudaStream_t st) {
+    if (!phase_path() || g_phase.empty()) return;
+    FFB_CUDA(cudaStreamSynchronize(st));
+    if (FILE* fd = fopen(phase_path(), "a")) {
+        float prev = 0.f;
+        for (const PhaseRec& r : g_phase) {
+            float t = 0.f;
+            cudaEventElapsedTime(&t, g_phase[0].e, r.e);
+            fprintf(fd, "%9.3f %8.3f %6lld %s\n", t, t - prev, (long long)r.size, r.label);
+            prev = t;
+        }
+        fprintf(fd, "--\n");
+        fclose(fd);
+    }
+    for (const PhaseRec& r : g_phase) cudaEventDestroy(r.e);
+    g_phase.clear();
+}
+
 // ===========================================================================
 // Generic modular GEMM (SIMT).  64x64 tile, 256 threads, 4x4 per thread,
 // uint64 accumulation with delayed reduction (p < 2^23: one reduction per

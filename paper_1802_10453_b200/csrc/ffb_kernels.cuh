@@ -66,6 +66,11 @@ struct ProfScope {
     ~ProfScope();
 };
 
+// FFB_PHASE_TRACE=<file>: event marks at the phase boundaries of large nodes (no
+// synchronisation; elapsed times are written by phase_dump() after the run).
+void phase_mark(const char* label, int64_t size, cudaStream_t st);
+void phase_dump(cudaStream_t st);
+
 enum GemmMode { GEMM_SUB = 0, GEMM_ADD = 1, GEMM_SET = 2 };
 
 // C (M x N) = C -/+ op(A) * op(B)  or  C = op(A) * op(B), all mod p.

@@ -77,6 +77,7 @@ def main():
                               crp_list_us=round(ms[0] * 1e3, 2), finish_us=round(ms[1] * 1e3, 2),
                               list_reg_us=round(ms[2] * 1e3, 2), list_reg_same=out[1 + 2 * k],
                               finish_phase_us=[round(x / 1e3, 2) for x in out[2 + 2 * k:7 + 2 * k]],
+                              finish_reg_us=round(out[8 + 2 * k] / 1e3, 2), finish_reg_same=out[7 + 2 * k],
                               jsorted=bool(all(out[1 + i] < out[2 + i] for i in range(k - 1))))))
 
 
