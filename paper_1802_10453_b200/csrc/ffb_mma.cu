@@ -166,7 +166,7 @@ struct MmaScratch {
     uint32_t* ptr = nullptr;
     size_t cap = 0;
 };
-thread_local MmaScratch g_mscratch_slots[FFB_MAX_DEVICES][5];
+thread_local MmaScratch g_mscratch_slots[FFB_MAX_DEVICES][6];
 uint32_t* mma_scratch(size_t words) {
     MmaScratch& g_mscratch = g_mscratch_slots[current_device()][g_slot];
     if (g_mscratch.cap < words) {

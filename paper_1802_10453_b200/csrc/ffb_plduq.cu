@@ -510,6 +510,389 @@ __global__ void __launch_bounds__(32 * NW) k_rrp(Fp f, const uint32_t* S, int64_
 }
 
 // ---------------------------------------------------------------------------
+// Row rank profile, left-looking rounds (p < 4096; same contract as k_row_detect with
+// rho_pre as the pre-basis pivots).  The basis E lives in shared memory, normalized and
+// fully reduced (Gauss-Jordan): the coefficients of a row against it are the row's own
+// entries at the pivot columns, so a row is reduced against all k basis rows without a
+// dependency chain -- lane t takes coefficient t from the warp's copy of the row, the
+// loop over t is shuffles and multiply-adds.  Rows are visited in rounds of NW (one row
+// per warp, the next round's row prefetched): reduce, one barrier for the nonzero flags;
+// the first nonzero pending row is a pivot (the pending rows before it are dependent for
+// good).  A pivot step touches only the round's later pending rows and the basis (row t
+// of E by warp t mod NW), two barriers.  A pre-basis costs no pivot steps at all.
+// ---------------------------------------------------------------------------
+template <int NQ>
+__device__ __forceinline__ uint32_t reg_col(const uint32_t (&v)[NQ], int col, int lane) {
+    uint32_t mv = v[0];
+#pragma unroll
+    for (int q = 1; q < NQ; ++q) mv = q == (col >> 5) ? v[q] : mv;
+    return __shfl_sync(0xffffffffu, mv, col & 31);
+}
+template <int NQ, int NW>
+__global__ void __launch_bounds__(32 * NW) k_rrp2(Fp f, const uint32_t* S, int64_t lds, int b, int s, int32_t* out,
+                                                  MboxPost mp, const uint32_t* Epre, const int32_t* rho_pre,
+                                                  const int32_t* kpre_ptr, uint32_t* Eout, int32_t* rho_out) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    constexpr int W = 32 * NQ, KMAX = W < 128 ? W : 128, KS = KMAX / 32, SINV = 1024;
+    __shared__ uint16_t E[KMAX][W];
+    __shared__ uint16_t rowbuf[NW][W];
+    __shared__ int16_t rho[KMAX];
+    __shared__ int flag[2][NW];
+    __shared__ int pcol_s[2];
+    __shared__ uint32_t sinv[SINV];
+    const SmemInv inv = f.p <= (uint32_t)SINV ? stage_inverses(f, sinv) : SmemInv{nullptr};
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    const int kpre = kpre_ptr ? min(__ldcg(kpre_ptr), min(s, KMAX)) : 0;
+    for (int e = tid; e < kpre * W; e += 32 * NW) {
+        const int t = e / W, c = e - t * W;
+        E[t][c] = c < s ? (uint16_t)__ldcg(Epre + (int64_t)t * s + c) : (uint16_t)0;
+    }
+    for (int t = tid; t < kpre; t += 32 * NW) rho[t] = (int16_t)__ldcg(rho_pre + t);
+    uint32_t nxt[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) nxt[q] = (wp < b && lane + 32 * q < s) ? __ldcg(S + (int64_t)wp * lds + lane + 32 * q) : 0u;
+    __syncthreads();
+    int k = kpre, kn = 0, tb = 0, pb = 0;
+    for (int base = 0; base < b && k < KMAX; base += NW) {
+        const int i = base + wp;
+        uint32_t cur[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            cur[q] = nxt[q];
+            nxt[q] = (i + NW < b && lane + 32 * q < s) ? __ldcg(S + (int64_t)(i + NW) * lds + lane + 32 * q) : 0u;
+        }
+        if (k > 0) {  // cur -= sum_t cur[rho_t] E_t
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) rowbuf[wp][lane + 32 * q] = (uint16_t)cur[q];
+            __syncwarp();
+            uint32_t cs[KS];
+#pragma unroll
+            for (int j = 0; j < KS; ++j) {
+                const int t = lane + 32 * j;
+                const uint32_t c = t < k ? rowbuf[wp][rho[t]] : 0u;
+                cs[j] = c ? f.p - c : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < KS; ++j) {
+                const int kt = min(32, k - 32 * j);  // uniform
+#pragma unroll 4
+                for (int tt = 0; tt < kt; ++tt) {
+                    const uint32_t c = __shfl_sync(0xffffffffu, cs[j], tt);
+                    const uint16_t* er = E[32 * j + tt];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) cur[q] += c * er[lane + 32 * q];
+                }
+            }
+            __syncwarp();
+        }
+        bool nz = false;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            cur[q] = red32(f, cur[q]);
+            nz |= cur[q] != 0;
+        }
+        nz = __any_sync(0xffffffffu, nz);
+        if (lane == 0) flag[tb][wp] = nz;
+        __syncthreads();
+        unsigned pend = b - base >= NW ? (NW == 32 ? 0xffffffffu : (1u << NW) - 1u) : (1u << (b - base)) - 1u;
+        while (k < KMAX) {
+            const unsigned nzm = __ballot_sync(0xffffffffu, lane < NW && ((pend >> lane) & 1) && flag[tb][lane & (NW - 1)]);
+            tb ^= 1;
+            if (!nzm) break;  // every pending row of the round is dependent
+            const int ws = __ffs(nzm) - 1;
+            pend &= ~((2u << ws) - 1u);
+            if (wp == ws) {  // normalize at the first nonzero column, append to the basis
+                int cq = NQ;
+                unsigned bl = 0;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const unsigned bq = __ballot_sync(0xffffffffu, cur[q] != 0);
+                    if (cq == NQ && bq) {
+                        cq = q;
+                        bl = bq;
+                    }
+                }
+                const int cl = __ffs(bl) - 1;
+                uint32_t xp = cur[0];
+#pragma unroll
+                for (int q = 1; q < NQ; ++q) xp = q == cq ? cur[q] : xp;
+                const uint32_t il = inv(f, __shfl_sync(0xffffffffu, xp, cl));
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) E[k][lane + 32 * q] = (uint16_t)red32(f, cur[q] * il);
+                if (lane == 0) {
+                    pcol_s[pb] = 32 * cq + cl;
+                    rho[k] = (int16_t)(32 * cq + cl);
+                    out[1 + kn] = i;
+                }
+            }
+            __syncthreads();
+            const int col = pcol_s[pb];
+            pb ^= 1;
+            uint32_t en[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) en[q] = E[k][lane + 32 * q];
+            if (wp > ws && ((pend >> wp) & 1)) {  // the round's later rows (warp-uniform)
+                const uint32_t m = reg_col<NQ>(cur, col, lane);
+                const uint32_t mn = m ? f.p - m : 0u;
+                bool z = false;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    cur[q] = red32(f, cur[q] + mn * en[q]);
+                    z |= cur[q] != 0;
+                }
+                z = __any_sync(0xffffffffu, z);
+                if (lane == 0) flag[tb][wp] = z;
+            }
+            for (int t = wp; t < k; t += NW) {  // basis rows: E_t -= E_t[col] E_k
+                const uint32_t m = E[t][col];
+                __syncwarp();
+                if (m) {
+                    const uint32_t mn = f.p - m;
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q)
+                        E[t][lane + 32 * q] = (uint16_t)red32(f, E[t][lane + 32 * q] + mn * en[q]);
+                }
+            }
+            ++k;
+            ++kn;
+            __syncthreads();
+        }
+    }
+    if (Eout) {  // the basis, fully reduced, in pivot order
+        for (int e = tid; e < k * s; e += 32 * NW) {
+            const int t = e / s, c = e - t * s;
+            Eout[e] = E[t][c];
+        }
+        for (int t = tid; t < k; t += 32 * NW) rho_out[t] = rho[t];
+    }
+    if (tid == 0) {
+        out[0] = kn;
+        if (mp.dst) mbox_publish(mp, &kn, 1);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Row rank profile for p <= 255: k_rrp2's rounds with the basis stored as packed bytes,
+// E8[g][c] = (E[4g][c], .., E[4g+3][c]), so the reduction of a row against the basis is
+// one dp4a per four basis rows and column (coefficient words broadcast from shared
+// memory).  The basis update is deferred to the end of a round: a new pivot row stays in
+// its warp's registers and takes the round's later pivots there (fully reduced when the
+// round ends), a pivot step only publishes the normalized row and updates the round's
+// later pending rows (two barriers); then group g of E8 is rewritten by warp g mod NW in
+// one pass -- E_t -= sum_i E_t[col_i] N_i with the multipliers read before any write
+// (the N_i are zero at each other's pivot columns), again dp4a over i -- and the new rows
+// are appended by the warp that owns their group.
+// ---------------------------------------------------------------------------
+// SM-clock stamps of the last k_rrp3 (thread 0): entry, after the prologue, after each round
+// (the first 20), exit; read by dbg_pq_bench
+__device__ long long g_rrp_stamp[24];
+template <int NQ, int NW>
+__global__ void __launch_bounds__(32 * NW) k_rrp3(Fp f, const uint32_t* S, int64_t lds, int b, int s, int32_t* out,
+                                                  MboxPost mp, const uint32_t* Epre, const int32_t* rho_pre,
+                                                  const int32_t* kpre_ptr, uint32_t* Eout, int32_t* rho_out) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    constexpr int W = 32 * NQ, KMAX = W < 128 ? W : 128, KG = KMAX / 4, NH = NW / 4;
+    __shared__ uint32_t E8[KG][W];
+    __shared__ uint32_t Npk[NH][W];
+    __shared__ __align__(4) uint8_t cbuf[NW][KMAX];
+    __shared__ uint8_t rowbuf[NW][W];
+    __shared__ __align__(4) uint8_t mbuf[NW][4][NW];
+    __shared__ uint8_t prow[2][W];
+    __shared__ int16_t rho[KMAX], ncol_s[NW];
+    __shared__ int flag[2][NW];
+    __shared__ uint32_t sinv[256];
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    if (tid == 0) g_rrp_stamp[0] = clock64();
+    const SmemInv inv = stage_inverses(f, sinv);
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int kpre = kpre_ptr ? min(__ldcg(kpre_ptr), min(s, KMAX)) : 0;
+    for (int e = tid; e < KG * W; e += 32 * NW) {
+        const int g = e / W, c = e - g * W;
+        uint32_t w = 0;
+#pragma unroll
+        for (int tb = 0; tb < 4; ++tb)
+            if (4 * g + tb < kpre && c < s) w |= __ldcg(Epre + (int64_t)(4 * g + tb) * s + c) << (8 * tb);
+        E8[g][c] = w;
+    }
+    for (int t = tid; t < kpre; t += 32 * NW) rho[t] = (int16_t)__ldcg(rho_pre + t);
+    uint32_t nxt0[NQ], nxt1[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int c = lane + 32 * q;
+        nxt0[q] = (wp < b && c < s) ? __ldcg(S + (int64_t)wp * lds + c) : 0u;
+        nxt1[q] = (wp + NW < b && c < s) ? __ldcg(S + (int64_t)(wp + NW) * lds + c) : 0u;
+    }
+    __syncthreads();
+    if (tid == 0) g_rrp_stamp[1] = clock64();
+    int k = kpre, kn = 0, tb = 0, pb = 0;
+    for (int base = 0; base < b && k < KMAX; base += NW) {
+        const int i = base + wp;
+        if (tid == 0 && base > 0 && base <= 20 * NW) g_rrp_stamp[1 + base / NW] = clock64();
+        uint32_t cur[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int c = lane + 32 * q;
+            cur[q] = nxt0[q];
+            nxt0[q] = nxt1[q];
+            nxt1[q] = (i + 2 * NW < b && c < s) ? __ldcg(S + (int64_t)(i + 2 * NW) * lds + c) : 0u;
+        }
+        if (k > 0) {  // cur -= sum_t cur[rho_t] E_t
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) rowbuf[wp][lane + 32 * q] = (uint8_t)cur[q];
+            __syncwarp();
+            const int k4 = (k + 3) & ~3;
+            for (int t = lane; t < k4; t += 32) {
+                const uint32_t c = t < k ? rowbuf[wp][rho[t]] : 0u;
+                cbuf[wp][t] = (uint8_t)(c ? f.p - c : 0u);
+            }
+            __syncwarp();
+            const uint32_t* cw = reinterpret_cast<const uint32_t*>(cbuf[wp]);
+#pragma unroll 4
+            for (int g = 0; g < (k4 >> 2); ++g) {
+                const uint32_t w = cw[g];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) cur[q] = __dp4a(E8[g][lane + 32 * q], w, cur[q]);
+            }
+        }
+        bool nz = false;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            cur[q] = red32(f, cur[q]);
+            nz |= cur[q] != 0;
+        }
+        nz = __any_sync(0xffffffffu, nz);
+        if (lane == 0) flag[tb][wp] = nz;
+        __syncthreads();
+        unsigned pend = b - base >= NW ? (NW == 32 ? 0xffffffffu : (1u << NW) - 1u) : (1u << (b - base)) - 1u;
+        int j = 0, myidx = 0;
+        bool ispiv = false;
+        uint32_t mine[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) mine[q] = 0;
+        while (k + j < KMAX) {
+            const unsigned nzm = __ballot_sync(0xffffffffu, lane < NW && ((pend >> lane) & 1) && flag[tb][lane & (NW - 1)]);
+            tb ^= 1;
+            if (!nzm) break;  // every pending row of the round is dependent
+            const int ws = __ffs(nzm) - 1;
+            pend &= ~((2u << ws) - 1u);
+            if (wp == ws) {  // normalize at the first nonzero column, publish
+                int cq = NQ;
+                unsigned bl = 0;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const unsigned bq = __ballot_sync(0xffffffffu, cur[q] != 0);
+                    if (cq == NQ && bq) {
+                        cq = q;
+                        bl = bq;
+                    }
+                }
+                const int cl = __ffs(bl) - 1;
+                uint32_t xp = cur[0];
+#pragma unroll
+                for (int q = 1; q < NQ; ++q) xp = q == cq ? cur[q] : xp;
+                const uint32_t il = inv(f, __shfl_sync(0xffffffffu, xp, cl));
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    mine[q] = red32(f, cur[q] * il);
+                    prow[pb][lane + 32 * q] = (uint8_t)mine[q];
+                }
+                if (lane == 0) {
+                    ncol_s[j] = (int16_t)(32 * cq + cl);
+                    rho[k + j] = (int16_t)(32 * cq + cl);
+                    out[1 + kn + j] = i;
+                }
+                ispiv = true;
+                myidx = j;
+            }
+            __syncthreads();
+            const int col = ncol_s[j];
+            uint32_t en[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) en[q] = prow[pb][lane + 32 * q];
+            pb ^= 1;
+            if (wp > ws && ((pend >> wp) & 1)) {  // the round's later rows (warp-uniform)
+                const uint32_t m = reg_col<NQ>(cur, col, lane);
+                const uint32_t mn = m ? f.p - m : 0u;
+                bool z = false;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    cur[q] = red32(f, cur[q] + mn * en[q]);
+                    z |= cur[q] != 0;
+                }
+                z = __any_sync(0xffffffffu, z);
+                if (lane == 0) flag[tb][wp] = z;
+            } else if (ispiv && wp != ws) {  // the round's earlier pivot rows, in registers
+                const uint32_t m = reg_col<NQ>(mine, col, lane);
+                const uint32_t mn = m ? f.p - m : 0u;
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) mine[q] = red32(f, mine[q] + mn * en[q]);
+            }
+            ++j;
+            __syncthreads();
+        }
+        if (j > 0) {  // the round's pivots into the basis
+            if (ispiv) {
+#pragma unroll
+                for (int q = 0; q < NQ; ++q)
+                    reinterpret_cast<uint8_t*>(&Npk[myidx >> 2][lane + 32 * q])[myidx & 3] = (uint8_t)mine[q];
+            }
+            __syncthreads();
+            const int gmax = (k + j - 1) >> 2, jh = (j + 3) >> 2;
+            for (int g = wp; g <= gmax; g += NW) {
+                for (int i0 = 0; i0 < j; i0 += 8) {  // multipliers p - E_t[col_i], bytes [tb][i]
+                    const int ii = i0 + (lane >> 2), t8 = lane & 3;
+                    const uint32_t m =
+                        (ii < j && 4 * g + t8 < k) ? reinterpret_cast<const uint8_t*>(&E8[g][ncol_s[ii]])[t8] : 0u;
+                    mbuf[wp][t8][ii] = (uint8_t)(m ? f.p - m : 0u);
+                }
+                __syncwarp();
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    const int c = lane + 32 * q;
+                    const uint32_t w = E8[g][c];
+                    uint32_t acc[4];
+#pragma unroll
+                    for (int t8 = 0; t8 < 4; ++t8) acc[t8] = (w >> (8 * t8)) & 0xffu;
+                    for (int h = 0; h < jh; ++h) {
+                        const uint32_t np = Npk[h][c];
+#pragma unroll
+                        for (int t8 = 0; t8 < 4; ++t8)
+                            acc[t8] = __dp4a(np, *reinterpret_cast<const uint32_t*>(&mbuf[wp][t8][4 * h]), acc[t8]);
+                    }
+                    uint32_t o = 0;
+#pragma unroll
+                    for (int t8 = 0; t8 < 4; ++t8) {
+                        const int t = 4 * g + t8;
+                        uint32_t v = 0;
+                        if (t < k) v = red32(f, acc[t8]);
+                        else if (t < k + j) v = (Npk[(t - k) >> 2][c] >> (8 * ((t - k) & 3))) & 0xffu;
+                        o |= v << (8 * t8);
+                    }
+                    E8[g][c] = o;
+                }
+                __syncwarp();
+            }
+            k += j;
+            kn += j;
+            __syncthreads();
+        }
+    }
+    if (Eout) {  // the basis, fully reduced, in pivot order
+        for (int e = tid; e < k * s; e += 32 * NW) {
+            const int t = e / s, c = e - t * s;
+            Eout[e] = (E8[t >> 2][c] >> (8 * (t & 3))) & 0xffu;
+        }
+        for (int t = tid; t < k; t += 32 * NW) rho_out[t] = rho[t];
+    }
+    if (tid == 0) {
+        out[0] = kn;
+        if (mp.dst) mbox_publish(mp, &kn, 1);
+        g_rrp_stamp[23] = clock64();
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Candidate columns for the column rank profile of RI (k x n): CTA g scans
 // columns [g*CRP_W, (g+1)*CRP_W) in groups of CRP_G and keeps those
 // independent of the earlier columns of its range (a local CRP).  A dropped
@@ -1814,6 +2197,12 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     // register-resident row detection (k_rrp) for p < 4096; FFB_RD_BATCHED: the batched kernel (A/B hook)
     static const bool rrp_env = getenv("FFB_RD_BATCHED") == nullptr;
     const bool rrp = rrp_env && f.p < 4096u && f.mu32;
+    // left-looking rounds over a shared Gauss-Jordan basis (k_rrp2); FFB_RRP_V1: the right-looking kernel (A/B hook)
+    static const bool rrp2_env = getenv("FFB_RRP_V1") == nullptr;
+    const bool rrp2 = rrp && rrp2_env;
+    // packed-byte basis with dp4a reductions (k_rrp3) for p <= 255; FFB_RRP_V2: k_rrp2 (A/B hook)
+    static const bool rrp3_env = getenv("FFB_RRP_V2") == nullptr;
+    const bool rrp3 = rrp2 && rrp3_env && f.p <= 255u;
     // register-resident local CRPs (k_crp_list_reg) for k <= 32, p < 2^16; FFB_CRP_SCAN: the scan kernel (A/B hook)
     static const bool crp_reg_env = getenv("FFB_CRP_SCAN") == nullptr;
     const bool crp_reg = crp_reg_env && f.p < 4096u && f.mu32;
@@ -1821,9 +2210,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     // side stream for the Uhat updates (see absorb)
     // (per device: a thread may drive contexts on several GPUs)
     struct SideStreams {
-        cudaStream_t side = nullptr, side2 = nullptr, side3 = nullptr;
+        cudaStream_t side = nullptr, side2 = nullptr, side3 = nullptr, side4 = nullptr;
         cudaEvent_t ev_main = nullptr, ev_side = nullptr, ev_gk = nullptr, ev_si = nullptr, ev_sk = nullptr,
-                    ev_det = nullptr, ev_t1 = nullptr, ev_un = nullptr;
+                    ev_det = nullptr, ev_t1 = nullptr, ev_un = nullptr, ev_uf = nullptr;
     };
     static thread_local SideStreams side_dev[FFB_MAX_DEVICES];
     SideStreams& ss = side_dev[current_device()];
@@ -1836,13 +2225,14 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         // 1-CTA detection is latency-bound and must not queue behind the Uhat updates)
         FFB_CUDA(cudaStreamCreateWithPriority(&ss.side2, cudaStreamNonBlocking, greatest));
         FFB_CUDA(cudaStreamCreateWithPriority(&ss.side3, cudaStreamNonBlocking, greatest));
+        FFB_CUDA(cudaStreamCreateWithPriority(&ss.side4, cudaStreamNonBlocking, greatest));  // T1 of the next chunk
         for (cudaEvent_t* e : {&ss.ev_main, &ss.ev_side, &ss.ev_gk, &ss.ev_si, &ss.ev_sk, &ss.ev_det, &ss.ev_t1,
-                               &ss.ev_un})
+                               &ss.ev_un, &ss.ev_uf})
             FFB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
-    cudaStream_t side = ss.side, side2 = ss.side2, side3 = ss.side3;
+    cudaStream_t side = ss.side, side2 = ss.side2, side3 = ss.side3, side4 = ss.side4;
     cudaEvent_t ev_main = ss.ev_main, ev_side = ss.ev_side, ev_gk = ss.ev_gk, ev_si = ss.ev_si, ev_sk = ss.ev_sk,
-                ev_det = ss.ev_det, ev_t1 = ss.ev_t1, ev_un = ss.ev_un;
+                ev_det = ss.ev_det, ev_t1 = ss.ev_t1, ev_un = ss.ev_un, ev_uf = ss.ev_uf;
     static const bool pipe_on = overlap_ok && !getenv("FFB_PLDUQ_NO_PIPE");  // A/B hook
     DMat T2[2] = {ws.mat(PIPE_KMAX + B, SK), ws.mat(PIPE_KMAX + B, SK)};
     int32_t* pinfo[2] = {ws.vec<int32_t>(2 * (PIPE_KMAX + B) + 16), ws.vec<int32_t>(2 * (PIPE_KMAX + B) + 16)};
@@ -1878,18 +2268,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         // Unew = Kc^-1 R_I and Uhat_old -= Up Unew are needed only by the next
         // chunk's residual: when sketching they run on the side stream, overlapped
         // with the next chunk's sketch, row detection and read-back (join_side).
+        // Unew goes first (the next chunk's residual correction waits for it, ev_un),
+        // the echelon U rows after it (ev_uf), then the main-stream part (Up, Uhat Omega).
         cudaStream_t us = st;
-        DMat Up;
-        if (r > 0) {  // Up = Uhat_old[:, J] before Uhat_old changes
-            Up = Upd.sub(0, 0, r, k);
-            gather2d(st, Up, Uhat.sub(0, 0, r, n), nullptr, dJ, 0);
-            if (sketching)
-                gemm(f, st, GEMM_SUB, UO.sub(0, 0, r, SK), Up, false, UO.sub(r, 0, k, SK), false, r,
-                     SK, k);
-        }
-        // mid: issued between the main-stream part and the side part (the pipelined next
-        // chunk's T1, which must read Uhat_old before the update below); true: wait for it
-        const bool t1_wait = mid ? mid() : false;
         if (sketching && overlap_ok) {
             FFB_CUDA(cudaEventRecord(ev_main, st));
             FFB_CUDA(cudaStreamWaitEvent(side, ev_main, 0)); pdl_fence(side);
@@ -1899,12 +2280,32 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             GreenScope green(us != st);
             SlotGuard slot(us == st ? g_slot : 1);
             gemm(f, us, GEMM_SET, Un, Kik, false, RIk, false, k, n, k);  // Unew = Kc^-1 R_I
+            FFB_CUDA(cudaEventRecord(ev_un, us));
             if (ufull_env && paired) {  // the chunk's rows of the echelon U (before RI is reused)
                 DMat Ldk = Ldb.sub(0, 0, k, k);
                 Ldk.ld = k;
                 gemm(f, us, GEMM_SET, Ufull.sub(r, 0, k, n), Ldk, false, RIk, false, k, n, k);
             }
-            FFB_CUDA(cudaEventRecord(ev_un, us));
+            FFB_CUDA(cudaEventRecord(ev_uf, us));
+        }
+        DMat Up;
+        if (r > 0) {  // Up = Uhat_old[:, J] before Uhat_old changes
+            Up = Upd.sub(0, 0, r, k);
+            gather2d(st, Up, Uhat.sub(0, 0, r, n), nullptr, dJ, 0);
+            if (sketching)
+                gemm(f, st, GEMM_SUB, UO.sub(0, 0, r, SK), Up, false, UO.sub(r, 0, k, SK), false, r,
+                     SK, k);
+        }
+        // mid: issued between the main-stream part and the Uhat update (the pipelined next
+        // chunk's T1, which must read Uhat_old before the update below); true: wait for it
+        const bool t1_wait = mid ? mid() : false;
+        if (us != st) {
+            FFB_CUDA(cudaEventRecord(ev_main, st));
+            FFB_CUDA(cudaStreamWaitEvent(side, ev_main, 0)); pdl_fence(side);
+        }
+        {
+            GreenScope green(us != st);
+            SlotGuard slot(us == st ? g_slot : 1);
             if (t1_wait) {  // the next chunk's T1 reads Uhat_old first
                 FFB_CUDA(cudaStreamWaitEvent(us, ev_t1, 0)); pdl_fence(us);
             }
@@ -2017,7 +2418,19 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         const MboxPost mp = io.post ? io.post() : MboxPost();
                         {
                             ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-                            if (rrp && wide)
+                            if (rrp3 && wide)
+                                launch_k(k_rrp3<5, 8>, 1, 256, 0, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp, nullptr,
+                                         nullptr, nullptr, nullptr, nullptr);
+                            else if (rrp3)
+                                launch_k(k_rrp3<2, 32>, 1, 1024, 0, st, f, Sc.ptr, Sc.ld, (int)bc, RD_NARROW, dinfo, mp,
+                                         nullptr, nullptr, nullptr, nullptr, nullptr);
+                            else if (rrp2 && wide)
+                                launch_k(k_rrp2<5, 8>, 1, 256, 0, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp, nullptr,
+                                         nullptr, nullptr, nullptr, nullptr);
+                            else if (rrp2)
+                                launch_k(k_rrp2<2, 32>, 1, 1024, 0, st, f, Sc.ptr, Sc.ld, (int)bc, RD_NARROW, dinfo, mp,
+                                         nullptr, nullptr, nullptr, nullptr, nullptr);
+                            else if (rrp && wide)
                                 launch_k(k_rrp<5, 16, 8>, 1, 256, 0, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp, nullptr,
                                          nullptr, nullptr, nullptr);
                             else if (rrp)
@@ -2081,7 +2494,13 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         const int64_t bcn = std::min<int64_t>(B, m - c0n);
                         // the reduced basis of S_I (side2) beside chunk c+1's sketch (side3),
                         // then the detection of c+1 modulo that basis (side2)
-                        if (rrp)
+                        if (rrp3)
+                            launch_k(k_rrp3<3, 8>, 1, 256, 0, side2, f, Sfin.ptr, Sfin.ld, k, RD_PIPE, pre_out,
+                                     MboxPost(), nullptr, nullptr, nullptr, Epre, rho_pre);
+                        else if (rrp2)
+                            launch_k(k_rrp2<3, 8>, 1, 256, 0, side2, f, Sfin.ptr, Sfin.ld, k, RD_PIPE, pre_out,
+                                     MboxPost(), nullptr, nullptr, nullptr, Epre, rho_pre);
+                        else if (rrp)
                             launch_k(k_rrp<3, 20, 8>, 1, 256, 0, side2, f, Sfin.ptr, Sfin.ld, k, RD_PIPE, pre_out,
                                      MboxPost(), nullptr, nullptr, Epre, rho_pre);
                         else
@@ -2104,7 +2523,13 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         pre_mp = io.post ? io.post() : MboxPost();
                         {
                             ProfScope ps(K_PLDUQ, side2, 0.0, 0.0);
-                            if (rrp)
+                            if (rrp3)
+                                launch_k(k_rrp3<3, 8>, 1, 256, 0, side2, f, Sn.ptr, Sn.ld, (int)bcn, RD_PIPE,
+                                         pinfo[pb], pre_mp, Epre, rho_pre, pre_out, nullptr, nullptr);
+                            else if (rrp2)
+                                launch_k(k_rrp2<3, 8>, 1, 256, 0, side2, f, Sn.ptr, Sn.ld, (int)bcn, RD_PIPE,
+                                         pinfo[pb], pre_mp, Epre, rho_pre, pre_out, nullptr, nullptr);
+                            else if (rrp)
                                 launch_k(k_rrp<3, 20, 8>, 1, 256, 0, side2, f, Sn.ptr, Sn.ld, (int)bcn, RD_PIPE,
                                          pinfo[pb], pre_mp, Epre, pre_out, nullptr, nullptr);
                             else
@@ -2163,6 +2588,9 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                 }
                 if (compact) {
                     FFB_CUDA(cudaStreamWaitEvent(st, ev_si, 0)); pdl_fence(st);
+                }
+                if (use_t1) {  // the finish rewrites Ldb: the previous chunk's echelon-U GEMM reads it
+                    FFB_CUDA(cudaStreamWaitEvent(st, ev_uf, 0)); pdl_fence(st);
                 }
                 {
                     ProfScope ps(K_PQ_ROWELIM, st, 0.0, 0.0);
@@ -2223,22 +2651,23 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     pre_done = true;
                     const int kn = pre_kt;
                     if (!(k + kn <= PIPE_TRUST && kn > 0)) return false;
-                    SlotGuard slot(3);
+                    SlotGuard slot(5);
                     DMat RIn = RIb[rb ^ 1].sub(0, 0, kn, n);
                     const int32_t* dIn = pinfo[pb] + 1;
                     const int64_t basen = c0n;
-                    // the previous chunk's Unew GEMM reads that RI buffer; Uhat must hold the
-                    // previous chunk's update (even when main joined it already)
-                    FFB_CUDA(cudaStreamWaitEvent(side2, ev_un, 0));
-                    FFB_CUDA(cudaStreamWaitEvent(side2, ev_side, 0));
-                    pdl_fence(side2);
-                    gather_rows(side2, RIn, Y.sub(basen, 0, m - basen, n), dIn);
+                    // on side4 (beside S_I and the stacked detection of the chunk after, side2):
+                    // after the detection that wrote dIn; the chunk before this one read that RI
+                    // buffer in its Unew / echelon GEMMs and Uhat must hold its update (ev_side)
+                    FFB_CUDA(cudaStreamWaitEvent(side4, ev_det, 0));
+                    FFB_CUDA(cudaStreamWaitEvent(side4, ev_side, 0));
+                    pdl_fence(side4);
+                    gather_rows(side4, RIn, Y.sub(basen, 0, m - basen, n), dIn);
                     if (r > 0) {
                         DMat G3 = Gi3.sub(0, 0, kn, r);
-                        gather2d(side2, G3, Y, dIn, d_uhat_col, basen);
-                        gemm(f, side2, GEMM_SUB, RIn, G3, false, Uhat.sub(0, 0, r, n), false, kn, n, r);
+                        gather2d(side4, G3, Y, dIn, d_uhat_col, basen);
+                        gemm(f, side4, GEMM_SUB, RIn, G3, false, Uhat.sub(0, 0, r, n), false, kn, n, r);
                     }
-                    FFB_CUDA(cudaEventRecord(ev_t1, side2));
+                    FFB_CUDA(cudaEventRecord(ev_t1, side4));
                     t1_launch = true;
                     return true;
                 };
@@ -2451,11 +2880,12 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
         if (rows <= 128 && cols <= 160 && f.p < 4096u) {  // the register-resident kernel on the same sketch
             int32_t* info2;
             FFB_CUDA(cudaMalloc(&info2, (2 * RD_MAX_B + 16) * 4));
-            launch_k(k_rrp<5, 16, 8>, 1, 256, 0, st, f, d_in, cols, rows, cols, info2, MboxPost(), nullptr, nullptr,
+            auto rrp_k = f.p <= 255u ? k_rrp3<5, 8> : k_rrp2<5, 8>;
+            launch_k(rrp_k, 1, 256, 0, st, f, d_in, cols, rows, cols, info2, MboxPost(), nullptr, nullptr, nullptr,
                      nullptr, nullptr);
             FFB_CUDA(cudaEventRecord(e[2], st));
             for (int i = 0; i < reps; ++i)
-                launch_k(k_rrp<5, 16, 8>, 1, 256, 0, st, f, d_in, cols, rows, cols, info2, MboxPost(), nullptr,
+                launch_k(rrp_k, 1, 256, 0, st, f, d_in, cols, rows, cols, info2, MboxPost(), nullptr, nullptr,
                          nullptr, nullptr, nullptr);
             FFB_CUDA(cudaEventRecord(e[3], st));
             FFB_CUDA(cudaEventSynchronize(e[3]));
@@ -2463,6 +2893,14 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
             ms[1] = t / reps;
             std::vector<int32_t> h2(1 + std::min(rows, cols));
             FFB_CUDA(cudaMemcpy(h2.data(), info2, h2.size() * 4, cudaMemcpyDeviceToHost));
+            if (f.p <= 255u) {
+                long long hs[24];
+                FFB_CUDA(cudaMemcpyFromSymbol(hs, g_rrp_stamp, sizeof(hs)));
+                fprintf(stderr, "k_rrp3 cycles: prologue %lld, rounds", hs[1] - hs[0]);
+                const int nr = std::min((rows + 7) / 8, 20);
+                for (int u = 1; u < nr; ++u) fprintf(stderr, " %lld", hs[1 + u] - hs[u]);
+                fprintf(stderr, ", last round + exit %lld, total %lld\n", hs[23] - hs[nr], hs[23] - hs[0]);
+            }
             ms[2] = 1.0;  // identical row sets
             for (int j = 0; j <= h2[0] && j < (int)h2.size(); ++j)
                 if (h2[j] != out_k[j]) ms[2] = 0.0;

@@ -815,7 +815,7 @@ struct Scratch {
     int8_t* ptr = nullptr;
     size_t cap = 0;
 };
-thread_local Scratch g_scratch_slots[FFB_MAX_DEVICES][5];
+thread_local Scratch g_scratch_slots[FFB_MAX_DEVICES][6];
 
 int8_t* scratch(size_t bytes) {
     Scratch& g_scratch = g_scratch_slots[current_device()][g_slot];
