@@ -1265,29 +1265,46 @@ __global__ void __launch_bounds__(PLDUQ_THREADS)
     k_plduq_v1(Fp f, uint32_t* W, int64_t ldw, int m, int n, int32_t* info, int32_t* colflag,
                uint32_t* lvec, uint32_t* Lo, int64_t ldlo, uint32_t* d, uint32_t* Uo, int64_t lduo) {
     FFB_PDL_ENTRY();
-    __shared__ int jmin;
+    __shared__ int jmin, nrow;
     __shared__ uint32_t sxi;
     const int tid = threadIdx.x;
     int32_t* row_image = info + 1;
     int32_t* col_image = info + 1 + m;
     int32_t* pc = info + 1 + m + n;
     for (int j = tid; j < n; j += PLDUQ_THREADS) colflag[j] = 0;
+    if (tid == 0) nrow = m;
     __syncthreads();
-    int r = 0, nm = 0;
-    for (int i = 0; i < m; ++i) {
-        if (tid == 0) jmin = n;
+    {  // the first row with a nonzero entry
+        int mine = m;
+        const int64_t total = (int64_t)m * n;
+        for (int64_t e = tid; e < total; e += PLDUQ_THREADS) {
+            const int i2 = (int)(e / n);
+            if (i2 < mine && W[(int64_t)i2 * ldw + (int)(e % n)] != 0) mine = i2;
+        }
+        if (mine < m) atomicMin(&nrow, mine);
+    }
+    int r = 0, nm = 0, i = 0;
+    // The trailing update of a pivot step also finds the next row whose residual is nonzero:
+    // the rows before it are pivotless (plduq.cpp:60-63) and are skipped in one step, so the
+    // loop runs once per pivot, not once per row.
+    while (true) {
+        __syncthreads();
+        const int nx = nrow;
+        for (int t = tid; t < nx - i; t += PLDUQ_THREADS) row_image[m - 1 - (nm + t)] = i + t;  // from the back for now
+        nm += nx - i;
+        if (nx >= m) break;
+        i = nx;
+        __syncthreads();
+        if (tid == 0) {
+            jmin = n;
+            nrow = m;
+        }
         __syncthreads();
         uint32_t* wi = W + (int64_t)i * ldw;
         for (int j = tid; j < n; j += PLDUQ_THREADS)
             if (!colflag[j] && wi[j] != 0) atomicMin(&jmin, j);
         __syncthreads();
         const int jp = jmin;
-        if (jp == n) {  // pivotless row (plduq.cpp:60-63); stored from the back for now
-            if (tid == 0) row_image[m - 1 - nm] = i;
-            ++nm;
-            __syncthreads();
-            continue;
-        }
         if (tid == 0) {
             const uint32_t x = wi[jp];
             sxi = finv(f, x);
@@ -1304,18 +1321,26 @@ __global__ void __launch_bounds__(PLDUQ_THREADS)
         // trailing rows: residual update on non-pivot columns, L multiplier in column jp
         const int rows_left = m - i - 1;
         const int64_t total = (int64_t)rows_left * n;
+        int mine = m;
         for (int64_t e = tid; e < total; e += PLDUQ_THREADS) {
             const int i2 = i + 1 + (int)(e / n), j = (int)(e % n);
             if (colflag[j]) continue;
             uint32_t* w = W + (int64_t)i2 * ldw + j;
-            if (j == jp) *w = fmul(f, lvec[i2], xi);
-            else *w = fsub(f, *w, fmul(f, lvec[i2], wi[j]));
+            if (j == jp) {
+                *w = fmul(f, lvec[i2], xi);
+            } else {
+                const uint32_t v = fsub(f, *w, fmul(f, lvec[i2], wi[j]));
+                *w = v;
+                if (v != 0 && i2 < mine) mine = i2;
+            }
         }
+        if (mine < m) atomicMin(&nrow, mine);
         __syncthreads();
         if (tid == 0) colflag[jp] = 1;
         ++r;
-        __syncthreads();
+        ++i;
     }
+    __syncthreads();
     // Pivotless rows ascending after the pivot rows (plduq.cpp:86-90).
     if (tid == 0) {
         info[0] = r;

@@ -673,226 +673,6 @@ __global__ void __launch_bounds__(32 * NW) k_rrp2(Fp f, const uint32_t* S, int64
 }
 
 // ---------------------------------------------------------------------------
-// Row rank profile for p <= 255: k_rrp2's rounds with the basis stored as packed bytes,
-// E8[g][c] = (E[4g][c], .., E[4g+3][c]), so the reduction of a row against the basis is
-// one dp4a per four basis rows and column (coefficient words broadcast from shared
-// memory).  The basis update is deferred to the end of a round: a new pivot row stays in
-// its warp's registers and takes the round's later pivots there (fully reduced when the
-// round ends), a pivot step only publishes the normalized row and updates the round's
-// later pending rows (two barriers); then group g of E8 is rewritten by warp g mod NW in
-// one pass -- E_t -= sum_i E_t[col_i] N_i with the multipliers read before any write
-// (the N_i are zero at each other's pivot columns), again dp4a over i -- and the new rows
-// are appended by the warp that owns their group.
-// ---------------------------------------------------------------------------
-// SM-clock stamps of the last k_rrp3 (thread 0): entry, after the prologue, after each round
-// (the first 20), exit; read by dbg_pq_bench
-__device__ long long g_rrp_stamp[24];
-template <int NQ, int NW>
-__global__ void __launch_bounds__(32 * NW) k_rrp3(Fp f, const uint32_t* S, int64_t lds, int b, int s, int32_t* out,
-                                                  MboxPost mp, const uint32_t* Epre, const int32_t* rho_pre,
-                                                  const int32_t* kpre_ptr, uint32_t* Eout, int32_t* rho_out) {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-    constexpr int W = 32 * NQ, KMAX = W < 128 ? W : 128, KG = KMAX / 4, NH = NW / 4;
-    __shared__ uint32_t E8[KG][W];
-    __shared__ uint32_t Npk[NH][W];
-    __shared__ __align__(4) uint8_t cbuf[NW][KMAX];
-    __shared__ uint8_t rowbuf[NW][W];
-    __shared__ __align__(4) uint8_t mbuf[NW][4][NW];
-    __shared__ uint8_t prow[2][W];
-    __shared__ int16_t rho[KMAX], ncol_s[NW];
-    __shared__ int flag[2][NW];
-    __shared__ uint32_t sinv[256];
-    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-    if (tid == 0) g_rrp_stamp[0] = clock64();
-    const SmemInv inv = stage_inverses(f, sinv);
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int kpre = kpre_ptr ? min(__ldcg(kpre_ptr), min(s, KMAX)) : 0;
-    for (int e = tid; e < KG * W; e += 32 * NW) {
-        const int g = e / W, c = e - g * W;
-        uint32_t w = 0;
-#pragma unroll
-        for (int tb = 0; tb < 4; ++tb)
-            if (4 * g + tb < kpre && c < s) w |= __ldcg(Epre + (int64_t)(4 * g + tb) * s + c) << (8 * tb);
-        E8[g][c] = w;
-    }
-    for (int t = tid; t < kpre; t += 32 * NW) rho[t] = (int16_t)__ldcg(rho_pre + t);
-    uint32_t nxt0[NQ], nxt1[NQ];
-#pragma unroll
-    for (int q = 0; q < NQ; ++q) {
-        const int c = lane + 32 * q;
-        nxt0[q] = (wp < b && c < s) ? __ldcg(S + (int64_t)wp * lds + c) : 0u;
-        nxt1[q] = (wp + NW < b && c < s) ? __ldcg(S + (int64_t)(wp + NW) * lds + c) : 0u;
-    }
-    __syncthreads();
-    if (tid == 0) g_rrp_stamp[1] = clock64();
-    int k = kpre, kn = 0, tb = 0, pb = 0;
-    for (int base = 0; base < b && k < KMAX; base += NW) {
-        const int i = base + wp;
-        if (tid == 0 && base > 0 && base <= 20 * NW) g_rrp_stamp[1 + base / NW] = clock64();
-        uint32_t cur[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            const int c = lane + 32 * q;
-            cur[q] = nxt0[q];
-            nxt0[q] = nxt1[q];
-            nxt1[q] = (i + 2 * NW < b && c < s) ? __ldcg(S + (int64_t)(i + 2 * NW) * lds + c) : 0u;
-        }
-        if (k > 0) {  // cur -= sum_t cur[rho_t] E_t
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) rowbuf[wp][lane + 32 * q] = (uint8_t)cur[q];
-            __syncwarp();
-            const int k4 = (k + 3) & ~3;
-            for (int t = lane; t < k4; t += 32) {
-                const uint32_t c = t < k ? rowbuf[wp][rho[t]] : 0u;
-                cbuf[wp][t] = (uint8_t)(c ? f.p - c : 0u);
-            }
-            __syncwarp();
-            const uint32_t* cw = reinterpret_cast<const uint32_t*>(cbuf[wp]);
-#pragma unroll 4
-            for (int g = 0; g < (k4 >> 2); ++g) {
-                const uint32_t w = cw[g];
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) cur[q] = __dp4a(E8[g][lane + 32 * q], w, cur[q]);
-            }
-        }
-        bool nz = false;
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) {
-            cur[q] = red32(f, cur[q]);
-            nz |= cur[q] != 0;
-        }
-        nz = __any_sync(0xffffffffu, nz);
-        if (lane == 0) flag[tb][wp] = nz;
-        __syncthreads();
-        unsigned pend = b - base >= NW ? (NW == 32 ? 0xffffffffu : (1u << NW) - 1u) : (1u << (b - base)) - 1u;
-        int j = 0, myidx = 0;
-        bool ispiv = false;
-        uint32_t mine[NQ];
-#pragma unroll
-        for (int q = 0; q < NQ; ++q) mine[q] = 0;
-        while (k + j < KMAX) {
-            const unsigned nzm = __ballot_sync(0xffffffffu, lane < NW && ((pend >> lane) & 1) && flag[tb][lane & (NW - 1)]);
-            tb ^= 1;
-            if (!nzm) break;  // every pending row of the round is dependent
-            const int ws = __ffs(nzm) - 1;
-            pend &= ~((2u << ws) - 1u);
-            if (wp == ws) {  // normalize at the first nonzero column, publish
-                int cq = NQ;
-                unsigned bl = 0;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const unsigned bq = __ballot_sync(0xffffffffu, cur[q] != 0);
-                    if (cq == NQ && bq) {
-                        cq = q;
-                        bl = bq;
-                    }
-                }
-                const int cl = __ffs(bl) - 1;
-                uint32_t xp = cur[0];
-#pragma unroll
-                for (int q = 1; q < NQ; ++q) xp = q == cq ? cur[q] : xp;
-                const uint32_t il = inv(f, __shfl_sync(0xffffffffu, xp, cl));
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    mine[q] = red32(f, cur[q] * il);
-                    prow[pb][lane + 32 * q] = (uint8_t)mine[q];
-                }
-                if (lane == 0) {
-                    ncol_s[j] = (int16_t)(32 * cq + cl);
-                    rho[k + j] = (int16_t)(32 * cq + cl);
-                    out[1 + kn + j] = i;
-                }
-                ispiv = true;
-                myidx = j;
-            }
-            __syncthreads();
-            const int col = ncol_s[j];
-            uint32_t en[NQ];
-#pragma unroll
-            for (int q = 0; q < NQ; ++q) en[q] = prow[pb][lane + 32 * q];
-            pb ^= 1;
-            if (wp > ws && ((pend >> wp) & 1)) {  // the round's later rows (warp-uniform)
-                const uint32_t m = reg_col<NQ>(cur, col, lane);
-                const uint32_t mn = m ? f.p - m : 0u;
-                bool z = false;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    cur[q] = red32(f, cur[q] + mn * en[q]);
-                    z |= cur[q] != 0;
-                }
-                z = __any_sync(0xffffffffu, z);
-                if (lane == 0) flag[tb][wp] = z;
-            } else if (ispiv && wp != ws) {  // the round's earlier pivot rows, in registers
-                const uint32_t m = reg_col<NQ>(mine, col, lane);
-                const uint32_t mn = m ? f.p - m : 0u;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) mine[q] = red32(f, mine[q] + mn * en[q]);
-            }
-            ++j;
-            __syncthreads();
-        }
-        if (j > 0) {  // the round's pivots into the basis
-            if (ispiv) {
-#pragma unroll
-                for (int q = 0; q < NQ; ++q)
-                    reinterpret_cast<uint8_t*>(&Npk[myidx >> 2][lane + 32 * q])[myidx & 3] = (uint8_t)mine[q];
-            }
-            __syncthreads();
-            const int gmax = (k + j - 1) >> 2, jh = (j + 3) >> 2;
-            for (int g = wp; g <= gmax; g += NW) {
-                for (int i0 = 0; i0 < j; i0 += 8) {  // multipliers p - E_t[col_i], bytes [tb][i]
-                    const int ii = i0 + (lane >> 2), t8 = lane & 3;
-                    const uint32_t m =
-                        (ii < j && 4 * g + t8 < k) ? reinterpret_cast<const uint8_t*>(&E8[g][ncol_s[ii]])[t8] : 0u;
-                    mbuf[wp][t8][ii] = (uint8_t)(m ? f.p - m : 0u);
-                }
-                __syncwarp();
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const int c = lane + 32 * q;
-                    const uint32_t w = E8[g][c];
-                    uint32_t acc[4];
-#pragma unroll
-                    for (int t8 = 0; t8 < 4; ++t8) acc[t8] = (w >> (8 * t8)) & 0xffu;
-                    for (int h = 0; h < jh; ++h) {
-                        const uint32_t np = Npk[h][c];
-#pragma unroll
-                        for (int t8 = 0; t8 < 4; ++t8)
-                            acc[t8] = __dp4a(np, *reinterpret_cast<const uint32_t*>(&mbuf[wp][t8][4 * h]), acc[t8]);
-                    }
-                    uint32_t o = 0;
-#pragma unroll
-                    for (int t8 = 0; t8 < 4; ++t8) {
-                        const int t = 4 * g + t8;
-                        uint32_t v = 0;
-                        if (t < k) v = red32(f, acc[t8]);
-                        else if (t < k + j) v = (Npk[(t - k) >> 2][c] >> (8 * ((t - k) & 3))) & 0xffu;
-                        o |= v << (8 * t8);
-                    }
-                    E8[g][c] = o;
-                }
-                __syncwarp();
-            }
-            k += j;
-            kn += j;
-            __syncthreads();
-        }
-    }
-    if (Eout) {  // the basis, fully reduced, in pivot order
-        for (int e = tid; e < k * s; e += 32 * NW) {
-            const int t = e / s, c = e - t * s;
-            Eout[e] = (E8[t >> 2][c] >> (8 * (t & 3))) & 0xffu;
-        }
-        for (int t = tid; t < k; t += 32 * NW) rho_out[t] = rho[t];
-    }
-    if (tid == 0) {
-        out[0] = kn;
-        if (mp.dst) mbox_publish(mp, &kn, 1);
-        g_rrp_stamp[23] = clock64();
-    }
-}
-
-// ---------------------------------------------------------------------------
 // Candidate columns for the column rank profile of RI (k x n): CTA g scans
 // columns [g*CRP_W, (g+1)*CRP_W) in groups of CRP_G and keeps those
 // independent of the earlier columns of its range (a local CRP).  A dropped
@@ -2200,9 +1980,6 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     // left-looking rounds over a shared Gauss-Jordan basis (k_rrp2); FFB_RRP_V1: the right-looking kernel (A/B hook)
     static const bool rrp2_env = getenv("FFB_RRP_V1") == nullptr;
     const bool rrp2 = rrp && rrp2_env;
-    // packed-byte basis with dp4a reductions (k_rrp3) for p <= 255; FFB_RRP_V2: k_rrp2 (A/B hook)
-    static const bool rrp3_env = getenv("FFB_RRP_V2") == nullptr;
-    const bool rrp3 = rrp2 && rrp3_env && f.p <= 255u;
     // register-resident local CRPs (k_crp_list_reg) for k <= 32, p < 2^16; FFB_CRP_SCAN: the scan kernel (A/B hook)
     static const bool crp_reg_env = getenv("FFB_CRP_SCAN") == nullptr;
     const bool crp_reg = crp_reg_env && f.p < 4096u && f.mu32;
@@ -2418,13 +2195,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         const MboxPost mp = io.post ? io.post() : MboxPost();
                         {
                             ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
-                            if (rrp3 && wide)
-                                launch_k(k_rrp3<5, 8>, 1, 256, 0, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp, nullptr,
-                                         nullptr, nullptr, nullptr, nullptr);
-                            else if (rrp3)
-                                launch_k(k_rrp3<2, 32>, 1, 1024, 0, st, f, Sc.ptr, Sc.ld, (int)bc, RD_NARROW, dinfo, mp,
-                                         nullptr, nullptr, nullptr, nullptr, nullptr);
-                            else if (rrp2 && wide)
+                            if (rrp2 && wide)
                                 launch_k(k_rrp2<5, 8>, 1, 256, 0, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp, nullptr,
                                          nullptr, nullptr, nullptr, nullptr);
                             else if (rrp2)
@@ -2494,10 +2265,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         const int64_t bcn = std::min<int64_t>(B, m - c0n);
                         // the reduced basis of S_I (side2) beside chunk c+1's sketch (side3),
                         // then the detection of c+1 modulo that basis (side2)
-                        if (rrp3)
-                            launch_k(k_rrp3<3, 8>, 1, 256, 0, side2, f, Sfin.ptr, Sfin.ld, k, RD_PIPE, pre_out,
-                                     MboxPost(), nullptr, nullptr, nullptr, Epre, rho_pre);
-                        else if (rrp2)
+                        if (rrp2)
                             launch_k(k_rrp2<3, 8>, 1, 256, 0, side2, f, Sfin.ptr, Sfin.ld, k, RD_PIPE, pre_out,
                                      MboxPost(), nullptr, nullptr, nullptr, Epre, rho_pre);
                         else if (rrp)
@@ -2523,10 +2291,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         pre_mp = io.post ? io.post() : MboxPost();
                         {
                             ProfScope ps(K_PLDUQ, side2, 0.0, 0.0);
-                            if (rrp3)
-                                launch_k(k_rrp3<3, 8>, 1, 256, 0, side2, f, Sn.ptr, Sn.ld, (int)bcn, RD_PIPE,
-                                         pinfo[pb], pre_mp, Epre, rho_pre, pre_out, nullptr, nullptr);
-                            else if (rrp2)
+                            if (rrp2)
                                 launch_k(k_rrp2<3, 8>, 1, 256, 0, side2, f, Sn.ptr, Sn.ld, (int)bcn, RD_PIPE,
                                          pinfo[pb], pre_mp, Epre, rho_pre, pre_out, nullptr, nullptr);
                             else if (rrp)
@@ -2880,7 +2645,7 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
         if (rows <= 128 && cols <= 160 && f.p < 4096u) {  // the register-resident kernel on the same sketch
             int32_t* info2;
             FFB_CUDA(cudaMalloc(&info2, (2 * RD_MAX_B + 16) * 4));
-            auto rrp_k = f.p <= 255u ? k_rrp3<5, 8> : k_rrp2<5, 8>;
+            auto rrp_k = k_rrp2<5, 8>;
             launch_k(rrp_k, 1, 256, 0, st, f, d_in, cols, rows, cols, info2, MboxPost(), nullptr, nullptr, nullptr,
                      nullptr, nullptr);
             FFB_CUDA(cudaEventRecord(e[2], st));
@@ -2893,14 +2658,6 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
             ms[1] = t / reps;
             std::vector<int32_t> h2(1 + std::min(rows, cols));
             FFB_CUDA(cudaMemcpy(h2.data(), info2, h2.size() * 4, cudaMemcpyDeviceToHost));
-            if (f.p <= 255u) {
-                long long hs[24];
-                FFB_CUDA(cudaMemcpyFromSymbol(hs, g_rrp_stamp, sizeof(hs)));
-                fprintf(stderr, "k_rrp3 cycles: prologue %lld, rounds", hs[1] - hs[0]);
-                const int nr = std::min((rows + 7) / 8, 20);
-                for (int u = 1; u < nr; ++u) fprintf(stderr, " %lld", hs[1 + u] - hs[u]);
-                fprintf(stderr, ", last round + exit %lld, total %lld\n", hs[23] - hs[nr], hs[23] - hs[0]);
-            }
             ms[2] = 1.0;  // identical row sets
             for (int j = 0; j <= h2[0] && j < (int)h2.size(); ++j)
                 if (h2[j] != out_k[j]) ms[2] = 0.0;
