@@ -784,6 +784,7 @@ struct Engine {
             const double t1 = std::chrono::duration<double, std::milli>(
                                   std::chrono::steady_clock::now().time_since_epoch()).count();
             fprintf(tr, "%lld %lld %lld %.3f\n", (long long)m, (long long)n, (long long)pl.r, t1 - pq_t0);
+            fflush(tr);
         }
         return pl;
     }
@@ -1403,7 +1404,9 @@ int ffb_plduq(ffb_context* c, uint64_t p, size_t m, size_t n, const uint64_t* b,
               int64_t* col_image, uint64_t* lower, uint64_t* diag, uint64_t* upper, size_t* rank) {
     return guarded(c, [&] {
         check_modulus(p);
-        ensure_workspace(c, (size_t)(m + 1) * (n + 1) * 40 + ((size_t)64 << 20));
+        // the chunked PLDUQ of a full-rank square input holds ~46 m x n word matrices at its peak
+        // (factors, both bases, phase-2 products); measured at n = 2048
+        ensure_workspace(c, (size_t)(m + 1) * (n + 1) * 256 + ((size_t)128 << 20));
         c->ws_top = 0;
         Fp f = make_field(c, p);
         DMat Y = upload_matrix(c, f, b, (int64_t)m, (int64_t)n, 8);

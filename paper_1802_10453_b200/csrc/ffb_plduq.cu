@@ -520,6 +520,8 @@ __global__ void __launch_bounds__(32 * NW) k_rrp(Fp f, const uint32_t* S, int64_
 // the first nonzero pending row is a pivot (the pending rows before it are dependent for
 // good).  A pivot step touches only the round's later pending rows and the basis (row t
 // of E by warp t mod NW), two barriers.  A pre-basis costs no pivot steps at all.
+// kcap > 0: stop after kcap new rows; out[0] then carries the rows consumed in bits 16..
+// (the chunk is cut there: the fast CRP kernels take at most 32 rows).
 // ---------------------------------------------------------------------------
 template <int NQ>
 __device__ __forceinline__ uint32_t reg_col(const uint32_t (&v)[NQ], int col, int lane) {
@@ -531,7 +533,7 @@ __device__ __forceinline__ uint32_t reg_col(const uint32_t (&v)[NQ], int col, in
 template <int NQ, int NW>
 __global__ void __launch_bounds__(32 * NW) k_rrp2(Fp f, const uint32_t* S, int64_t lds, int b, int s, int32_t* out,
                                                   MboxPost mp, const uint32_t* Epre, const int32_t* rho_pre,
-                                                  const int32_t* kpre_ptr, uint32_t* Eout, int32_t* rho_out) {
+                                                  const int32_t* kpre_ptr, uint32_t* Eout, int32_t* rho_out, int kcap) {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     constexpr int W = 32 * NQ, KMAX = W < 128 ? W : 128, KS = KMAX / 32, SINV = 1024;
     __shared__ uint16_t E[KMAX][W];
@@ -553,8 +555,9 @@ __global__ void __launch_bounds__(32 * NW) k_rrp2(Fp f, const uint32_t* S, int64
 #pragma unroll
     for (int q = 0; q < NQ; ++q) nxt[q] = (wp < b && lane + 32 * q < s) ? __ldcg(S + (int64_t)wp * lds + lane + 32 * q) : 0u;
     __syncthreads();
-    int k = kpre, kn = 0, tb = 0, pb = 0;
-    for (int base = 0; base < b && k < KMAX; base += NW) {
+    if (kcap <= 0) kcap = KMAX;
+    int k = kpre, kn = 0, tb = 0, pb = 0, done = 0;
+    for (int base = 0; base < b && k < KMAX && kn < kcap; base += NW) {
         const int i = base + wp;
         uint32_t cur[NQ];
 #pragma unroll
@@ -596,11 +599,11 @@ __global__ void __launch_bounds__(32 * NW) k_rrp2(Fp f, const uint32_t* S, int64
         if (lane == 0) flag[tb][wp] = nz;
         __syncthreads();
         unsigned pend = b - base >= NW ? (NW == 32 ? 0xffffffffu : (1u << NW) - 1u) : (1u << (b - base)) - 1u;
-        while (k < KMAX) {
+        while (k < KMAX && kn < kcap) {
             const unsigned nzm = __ballot_sync(0xffffffffu, lane < NW && ((pend >> lane) & 1) && flag[tb][lane & (NW - 1)]);
             tb ^= 1;
             if (!nzm) break;  // every pending row of the round is dependent
-            const int ws = __ffs(nzm) - 1;
+            const int ws = __ffs(nzm) - 1, i_piv = base + ws;
             pend &= ~((2u << ws) - 1u);
             if (wp == ws) {  // normalize at the first nonzero column, append to the basis
                 int cq = NQ;
@@ -656,6 +659,7 @@ __global__ void __launch_bounds__(32 * NW) k_rrp2(Fp f, const uint32_t* S, int64
             }
             ++k;
             ++kn;
+            if (kn == kcap) done = i_piv + 1;  // rows after the capped pivot stay for the next chunk
             __syncthreads();
         }
     }
@@ -666,9 +670,10 @@ __global__ void __launch_bounds__(32 * NW) k_rrp2(Fp f, const uint32_t* S, int64
         }
         for (int t = tid; t < k; t += 32 * NW) rho_out[t] = rho[t];
     }
-    if (tid == 0) {
-        out[0] = kn;
-        if (mp.dst) mbox_publish(mp, &kn, 1);
+    if (tid == 0) {  // new rows found; bits 16..: rows consumed when the cap cut the chunk short, else 0
+        const int word = kn | ((done > 0 && done < b) ? done << 16 : 0);
+        out[0] = word;
+        if (mp.dst) mbox_publish(mp, &word, 1);
     }
 }
 
@@ -1980,6 +1985,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     // left-looking rounds over a shared Gauss-Jordan basis (k_rrp2); FFB_RRP_V1: the right-looking kernel (A/B hook)
     static const bool rrp2_env = getenv("FFB_RRP_V1") == nullptr;
     const bool rrp2 = rrp && rrp2_env;
+    // detection stops after kcap rows and cuts the chunk there, so every chunk takes the
+    // register-resident CRP kernels (k <= 32) and stays in the pipeline; FFB_PLDUQ_KCAP=0: no cap (A/B hook)
+    static const int kcap_env = getenv("FFB_PLDUQ_KCAP") ? atoi(getenv("FFB_PLDUQ_KCAP")) : 32;
+    const int kcap = rrp2 ? kcap_env : 0;
     // register-resident local CRPs (k_crp_list_reg) for k <= 32, p < 2^16; FFB_CRP_SCAN: the scan kernel (A/B hook)
     static const bool crp_reg_env = getenv("FFB_CRP_SCAN") == nullptr;
     const bool crp_reg = crp_reg_env && f.p < 4096u && f.mu32;
@@ -2147,15 +2156,16 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
             mark();
             if (!exact) {
                 DMat Sc = YO.sub(c0, 0, bc, SK);
-                int k = 0;
+                int k = 0, cut = 0;
                 const int32_t* dI = dinfo + 1;
                 int64_t base = c0;  // row c0' + dI[t] of Y is detected row t
                 bool det_pipe = false;
                 bool use_t1 = false;
                 if (pre) {
                     pre = false;
-                    const int kt = pre_done ? pre_kt
-                                            : *(const int32_t*)(pre_mp.dst ? io.wait(pre_mp) : io.readback(pinfo[pb], 4));
+                    const int32_t word =
+                        pre_done ? pre_kt : *(const int32_t*)(pre_mp.dst ? io.wait(pre_mp) : io.readback(pinfo[pb], 4));
+                    const int kt = word & 0xffff;
                     pre_done = false;
                     use_t1 = t1;
                     t1 = false;
@@ -2164,6 +2174,11 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         k = kt;
                         dI = pinfo[pb] + 1;
                         det_pipe = true;
+                        if ((word >> 16) > 0 && (word >> 16) < bc) {  // capped: the chunk ends at the cut
+                            bc = word >> 16;
+                            Yc = Y.sub(c0, 0, bc, n);
+                            Sc = YO.sub(c0, 0, bc, SK);
+                        }
                     }  // else: near the sketch capacity -- detect again below, serially
                 }
                 if (!det_pipe) {
@@ -2197,10 +2212,10 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                             ProfScope ps(K_PLDUQ, st, 0.0, 0.0);
                             if (rrp2 && wide)
                                 launch_k(k_rrp2<5, 8>, 1, 256, 0, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp, nullptr,
-                                         nullptr, nullptr, nullptr, nullptr);
+                                         nullptr, nullptr, nullptr, nullptr, kcap);
                             else if (rrp2)
                                 launch_k(k_rrp2<2, 32>, 1, 1024, 0, st, f, Sc.ptr, Sc.ld, (int)bc, RD_NARROW, dinfo, mp,
-                                         nullptr, nullptr, nullptr, nullptr, nullptr);
+                                         nullptr, nullptr, nullptr, nullptr, nullptr, kcap);
                             else if (rrp && wide)
                                 launch_k(k_rrp<5, 16, 8>, 1, 256, 0, st, f, Sc.ptr, Sc.ld, (int)bc, SK, dinfo, mp, nullptr,
                                          nullptr, nullptr, nullptr);
@@ -2216,8 +2231,19 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                             ++g_launches;
                             FFB_CHECK_LAUNCH();
                         }
-                        k = *(const int32_t*)(mp.dst ? io.wait(mp) : io.readback(dinfo, 4));
+                        const int32_t word = *(const int32_t*)(mp.dst ? io.wait(mp) : io.readback(dinfo, 4));
+                        k = word & 0xffff;
+                        cut = word >> 16;
                         if (k < RD_NARROW - 16) break;
+                    }
+                    if (cut > 0 && cut < bc) {  // capped: the rows after the cut go to the next chunk;
+                        // their sketch rows were overwritten in place and are recomputed, Y Omega
+                        if (r > 0)
+                            gemm(f, st, GEMM_SET, YO.sub(c0 + cut, 0, bc - cut, SK), Y.sub(c0 + cut, 0, bc - cut, n),
+                                 false, Om, false, bc - cut, SK, n);
+                        bc = cut;
+                        Yc = Y.sub(c0, 0, bc, n);
+                        Sc = YO.sub(c0, 0, bc, SK);
                     }
                 } else {
                     mark();
@@ -2267,7 +2293,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                         // then the detection of c+1 modulo that basis (side2)
                         if (rrp2)
                             launch_k(k_rrp2<3, 8>, 1, 256, 0, side2, f, Sfin.ptr, Sfin.ld, k, RD_PIPE, pre_out,
-                                     MboxPost(), nullptr, nullptr, nullptr, Epre, rho_pre);
+                                     MboxPost(), nullptr, nullptr, nullptr, Epre, rho_pre, 0);
                         else if (rrp)
                             launch_k(k_rrp<3, 20, 8>, 1, 256, 0, side2, f, Sfin.ptr, Sfin.ld, k, RD_PIPE, pre_out,
                                      MboxPost(), nullptr, nullptr, Epre, rho_pre);
@@ -2293,7 +2319,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                             ProfScope ps(K_PLDUQ, side2, 0.0, 0.0);
                             if (rrp2)
                                 launch_k(k_rrp2<3, 8>, 1, 256, 0, side2, f, Sn.ptr, Sn.ld, (int)bcn, RD_PIPE,
-                                         pinfo[pb], pre_mp, Epre, rho_pre, pre_out, nullptr, nullptr);
+                                         pinfo[pb], pre_mp, Epre, rho_pre, pre_out, nullptr, nullptr, kcap);
                             else if (rrp)
                                 launch_k(k_rrp<3, 20, 8>, 1, 256, 0, side2, f, Sn.ptr, Sn.ld, (int)bcn, RD_PIPE,
                                          pinfo[pb], pre_mp, Epre, pre_out, nullptr, nullptr);
@@ -2414,7 +2440,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
                     if (!pipe) return false;
                     pre_kt = *(const int32_t*)(pre_mp.dst ? io.wait(pre_mp) : io.readback(pinfo[pb], 4));
                     pre_done = true;
-                    const int kn = pre_kt;
+                    const int kn = pre_kt & 0xffff;
                     if (!(k + kn <= PIPE_TRUST && kn > 0)) return false;
                     SlotGuard slot(5);
                     DMat RIn = RIb[rb ^ 1].sub(0, 0, kn, n);
@@ -2647,11 +2673,11 @@ void dbg_pq_bench(const Fp& f, cudaStream_t st, int which, int rows, int cols, c
             FFB_CUDA(cudaMalloc(&info2, (2 * RD_MAX_B + 16) * 4));
             auto rrp_k = k_rrp2<5, 8>;
             launch_k(rrp_k, 1, 256, 0, st, f, d_in, cols, rows, cols, info2, MboxPost(), nullptr, nullptr, nullptr,
-                     nullptr, nullptr);
+                     nullptr, nullptr, 0);
             FFB_CUDA(cudaEventRecord(e[2], st));
             for (int i = 0; i < reps; ++i)
                 launch_k(rrp_k, 1, 256, 0, st, f, d_in, cols, rows, cols, info2, MboxPost(), nullptr, nullptr,
-                         nullptr, nullptr, nullptr);
+                         nullptr, nullptr, nullptr, 0);
             FFB_CUDA(cudaEventRecord(e[3], st));
             FFB_CUDA(cudaEventSynchronize(e[3]));
             FFB_CUDA(cudaEventElapsedTime(&t, e[2], e[3]));
