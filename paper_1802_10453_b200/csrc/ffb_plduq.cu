@@ -1931,7 +1931,20 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     const int64_t m = Y.rows, n = Y.cols, mn = std::min(m, n);
     // test hook: a narrow sketch makes misses likely, exercising the certificate
     static const int sk_env = getenv("FFB_PLDUQ_SKETCH_COLS") ? atoi(getenv("FFB_PLDUQ_SKETCH_COLS")) : 0;
-    const int B = 128, SK = (sk_env > 0 && sk_env <= RD_S) ? sk_env : RD_S;
+    // register-resident row detection (k_rrp) for p < 4096; FFB_RD_BATCHED: the batched kernel (A/B hook)
+    static const bool rrp_env = getenv("FFB_RD_BATCHED") == nullptr;
+    const bool rrp = rrp_env && f.p < 4096u && f.mu32;
+    // left-looking rounds over a shared Gauss-Jordan basis (k_rrp2); FFB_RRP_V1: the right-looking kernel (A/B hook)
+    static const bool rrp2_env = getenv("FFB_RRP_V1") == nullptr;
+    const bool rrp2 = rrp && rrp2_env;
+    // detection stops after kcap rows and cuts the chunk there, so every chunk takes the
+    // register-resident CRP kernels (k <= 32) and stays in the pipeline; FFB_PLDUQ_KCAP=0: no cap (A/B hook)
+    static const int kcap_env = getenv("FFB_PLDUQ_KCAP") ? atoi(getenv("FFB_PLDUQ_KCAP")) : 32;
+    const int kcap = rrp2 ? kcap_env : 0;
+    // chunk rows (taller chunks with the cap, 160 / 192 / 256 rows: 86.8 / 86.2 / 86.1 ms against 86.6 ms
+    // on config 5 -- not worth a second size for the exact path's buffers)
+    const int B = 128;
+    const int SK = (sk_env > 0 && sk_env <= RD_S) ? sk_env : RD_S;
     PlduqOut out;
     const size_t mark0 = ws.mark();
     DMat Uhat = ws.mat(std::max<int64_t>(mn, 1), n);
@@ -1964,7 +1977,7 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
     int32_t* d_uhat_col = d_prow + 2 * pstride;
 
     const size_t rd_smem = std::max({rd_smem_bytes(RD_MAX_B, SK), rd_smem_bytes(RD_MAX_ROWS, RD_NARROW),
-                                      rd_smem_bytes(PIPE_KMAX + B, SK)});
+                                      rd_smem_bytes(PIPE_KMAX + 128, SK)});
     const size_t crp_smem = ((size_t)CRP_KMAX * CRP_KMAX + 2 * (size_t)CRP_G * CRP_KMAX) * 4;
     static DeviceOnce attrs;
     if (!attrs.done()) {
@@ -1979,16 +1992,6 @@ PlduqOut plduq_parallel(const Fp& f, cudaStream_t st, DMat Y, Workspace& ws, con
         attrs.mark();
     }
     static const bool force_exact = getenv("FFB_PLDUQ_FORCE_FALLBACK") != nullptr;  // test hook
-    // register-resident row detection (k_rrp) for p < 4096; FFB_RD_BATCHED: the batched kernel (A/B hook)
-    static const bool rrp_env = getenv("FFB_RD_BATCHED") == nullptr;
-    const bool rrp = rrp_env && f.p < 4096u && f.mu32;
-    // left-looking rounds over a shared Gauss-Jordan basis (k_rrp2); FFB_RRP_V1: the right-looking kernel (A/B hook)
-    static const bool rrp2_env = getenv("FFB_RRP_V1") == nullptr;
-    const bool rrp2 = rrp && rrp2_env;
-    // detection stops after kcap rows and cuts the chunk there, so every chunk takes the
-    // register-resident CRP kernels (k <= 32) and stays in the pipeline; FFB_PLDUQ_KCAP=0: no cap (A/B hook)
-    static const int kcap_env = getenv("FFB_PLDUQ_KCAP") ? atoi(getenv("FFB_PLDUQ_KCAP")) : 32;
-    const int kcap = rrp2 ? kcap_env : 0;
     // register-resident local CRPs (k_crp_list_reg) for k <= 32, p < 2^16; FFB_CRP_SCAN: the scan kernel (A/B hook)
     static const bool crp_reg_env = getenv("FFB_CRP_SCAN") == nullptr;
     const bool crp_reg = crp_reg_env && f.p < 4096u && f.mu32;
