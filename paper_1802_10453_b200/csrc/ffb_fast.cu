@@ -446,9 +446,17 @@ __global__ void __launch_bounds__(128) k_leaf64_lazy(Fp f, const uint32_t* A, in
 // ---------------------------------------------------------------------------
 constexpr int NODE_LD = 129;  // row stride of the node matrix in shared memory
 constexpr int NODE_W = 65;    // row stride of the 64-wide work matrices
+constexpr int NODE_B8 = 68;   // row stride (bytes) of the K-contiguous byte copies (17 words: conflict-free)
 constexpr size_t node_smem_bytes() {
-    return (size_t)(128 * NODE_LD + 3 * 64 * NODE_W) * 4;
+    return (size_t)(128 * NODE_LD + 3 * 64 * NODE_W) * 4 + 3 * 64 * NODE_B8;
 }
+// SM-clock stamps of the last k_node128 (thread 0; diagnostics read by ffb_dbg_node_stamps):
+// wait done, node loaded, leaf(A1), B'/[L1; M1] gathered, X, G, [Y; Z] updated, leaf(Z), exit
+__device__ long long g_node_stamp[9];
+#define NODE_STAMP(i)                                  \
+    do {                                               \
+        if (threadIdx.x == 0) g_node_stamp[i] = clock64(); \
+    } while (0)
 __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda, int s, const int32_t* rows,
                                                  uint32_t* Lg, int64_t ldL, int64_t coff, DDiag D,
                                                  uint32_t* yout, int32_t* out, MboxPost mp) {
@@ -458,6 +466,11 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
     uint32_t* BP = Am + 128 * NODE_LD;        // m x ns: X in rows [0, r1), Y in [r1, m)
     uint32_t* LM = BP + 64 * NODE_W;          // m x r1: [L1; M1]
     uint32_t* Gs = LM + 64 * NODE_W;          // ns x r1: G
+    // p <= 255: byte copies with K contiguous for the dp4a update -- M1 rows, G rows, X^T rows
+    uint8_t* M8 = reinterpret_cast<uint8_t*>(Gs + 64 * NODE_W);
+    uint8_t* G8 = M8 + 64 * NODE_B8;
+    uint8_t* XT8 = G8 + 64 * NODE_B8;
+    const bool bytes = f.p <= 255u;
     __shared__ LeafSmem sm;
     __shared__ int32_t srows[128];
     __shared__ int32_t perm1[64], perm2[128];
@@ -466,6 +479,7 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
     const int tid = threadIdx.x, wp = tid >> 5, lane = tid & 31;
     const SmemInv inv = stage_inverses(f, sinv);  // independent of the predecessor
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    NODE_STAMP(0);
     const int m = s / 2, ns = s - m;
     for (int i0 = 0; i0 < s; i0 += 32) {  // node matrix: 32 rows per round, loads in flight
         uint32_t v[32];
@@ -480,8 +494,10 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
     srows[tid] = tid < s ? __ldcg(rows + tid) : 0;
     if (tid == 0) ynz = 0;
     __syncthreads();
+    NODE_STAMP(1);
     // ---- leaf(A1) (:303) ----
     const int r1 = leaf_core<false>(f, inv, Am, NODE_LD, m, sm, D, coff);
+    NODE_STAMP(2);
     const int mp1 = m - r1;
     if (tid < m) {
         uint32_t* d = Lg + (int64_t)srows[tid] * ldL + coff;
@@ -490,12 +506,36 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
     }
     __syncthreads();
     // ---- B' = P1^T B (:308), [L1; M1] in position order ----
-    for (int e = tid; e < m * 64; e += 128) {
-        const int i = e >> 6, j = e & 63, src = perm1[i];
-        if (j < ns) BP[i * NODE_W + j] = Am[src * NODE_LD + m + j];
-        if (j < r1) LM[i * NODE_W + j] = sm.Ls[src][j];
+    {  // thread = column j, rows ih + 2u; 8 rows of loads in flight
+        const int j = tid & 63, ih = tid >> 6;
+#pragma unroll
+        for (int ub = 0; ub < 32; ub += 8) {
+            if (ih + 2 * ub >= m) break;  // uniform per warp
+            int src[8];
+            uint32_t vb[8], vl[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = ih + 2 * (ub + u);
+                src[u] = i < m ? perm1[i] : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                vb[u] = Am[src[u] * NODE_LD + m + j];
+                vl[u] = sm.Ls[src[u]][j];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int i = ih + 2 * (ub + u);
+                if (i < m) {
+                    if (j < ns) BP[i * NODE_W + j] = vb[u];
+                    if (j < r1) LM[i * NODE_W + j] = vl[u];
+                    if (bytes && i >= r1) M8[(i - r1) * NODE_B8 + j] = (uint8_t)(j < r1 ? vl[u] : 0u);
+                }
+            }
+        }
     }
     __syncthreads();
+    NODE_STAMP(3);
     if (r1 > 0) {
         // ---- X = L1^-1 B'1 (:310): warp w owns columns 16w + c, lanes 2c, 2c+1 split k ----
         {
@@ -520,34 +560,60 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
                         for (int t = 0; t < rr; ++t) v = fsub(f, v, fmul(f, LM[(i0 + rr) * NODE_W + i0 + t], x[t]));
                         x[rr] = v;
                         BP[(i0 + rr) * NODE_W + c] = v;
+                        if (bytes) XT8[c * NODE_B8 + i0 + rr] = (uint8_t)v;
                     }
                 }
                 __syncwarp();
             }
         }
         __syncthreads();
+        NODE_STAMP(4);
         // ---- G = (D1^-1 X)^T (:313, blockdiag.hpp:112-138), also the L rows of N1 ----
-        for (int e = tid; e < ns * 64; e += 128) {
-            const int j = e >> 6, k = e & 63;
-            if (k >= r1) continue;
-            const int32_t kind = sm.dkind[k];
-            const uint32_t iv = sm.dinv[k];
-            uint32_t v;
-            if (kind == D_SCALAR) {
-                v = fmul(f, iv, BP[k * NODE_W + j]);
-            } else if (kind == D_ANTIDIAG_HEAD) {
-                v = fmul(f, iv, BP[(k + 1) * NODE_W + j]);
-            } else if (kind == D_ANTIDIAG_TAIL || kind == D_ANTITRI_TAIL) {
-                v = fmul(f, iv, BP[(k - 1) * NODE_W + j]);
-            } else {  // AntiTri head: -d c^-2 x_t + c^-1 x_{t+1}
-                const uint32_t top = fneg(f, fmul(f, sm.dval2[k], fmul(f, iv, iv)));
-                v = fadd(f, fmul(f, top, BP[k * NODE_W + j]), fmul(f, iv, BP[(k + 1) * NODE_W + j]));
+        {  // thread = pivot column k, rows jh + 2u: v = ca X[k1][j] + cb X[k2][j]
+            const int k = tid & 63, jh = tid >> 6;
+            int k1 = 0, k2 = 0;
+            uint32_t ca = 0, cb = 0;
+            if (k < r1) {
+                const int32_t kind = sm.dkind[k];
+                const uint32_t iv = sm.dinv[k];
+                k1 = k2 = k;
+                ca = iv;
+                if (kind == D_ANTIDIAG_HEAD) {
+                    k1 = k + 1;
+                } else if (kind == D_ANTIDIAG_TAIL || kind == D_ANTITRI_TAIL) {
+                    k1 = k - 1;
+                } else if (kind != D_SCALAR) {  // AntiTri head: -d c^-2 x_t + c^-1 x_{t+1}
+                    ca = fneg(f, fmul(f, sm.dval2[k], fmul(f, iv, iv)));
+                    k2 = k + 1;
+                    cb = iv;
+                }
             }
-            Gs[j * NODE_W + k] = v;
-            Lg[(int64_t)srows[m + j] * ldL + coff + k] = v;
+#pragma unroll
+            for (int ub = 0; ub < 32; ub += 8) {
+                if (jh + 2 * ub >= ns) break;  // uniform per warp
+                uint32_t x1[8], x2[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = min(jh + 2 * (ub + u), ns - 1);
+                    x1[u] = BP[k1 * NODE_W + j];
+                    x2[u] = BP[k2 * NODE_W + j];
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int j = jh + 2 * (ub + u);
+                    if (j >= ns) continue;
+                    const uint32_t v = red32(f, ca * x1[u] + cb * x2[u]);
+                    if (k < r1) {
+                        Gs[j * NODE_W + k] = v;
+                        Lg[(int64_t)srows[m + j] * ldL + coff + k] = v;
+                    }
+                    if (bytes) G8[j * NODE_B8 + k] = (uint8_t)(k < r1 ? v : 0u);
+                }
+            }
         }
         __syncthreads();
     }
+    NODE_STAMP(5);
     // ---- [Y; Z] -= [M1; G] X (:312, :315): thread = 8 rows x 8 columns ----
     {
         const int rg = tid >> 3, cg = tid & 7;
@@ -563,16 +629,40 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
             const int rho = 8 * rg + a;
             lrow[a] = rho < mp1 ? LM + (r1 + rho) * NODE_W : Gs + (rho < R ? rho - mp1 : 0) * NODE_W;
         }
-        for (int k = 0; k < r1; ++k) {
-            uint32_t xv[8], lv[8];
+        if (bytes) {  // four k per dp4a: the byte rows of [M1; G] against the byte rows of X^T
+            const uint32_t* lw8[8];
 #pragma unroll
-            for (int b = 0; b < 8; ++b) xv[b] = BP[k * NODE_W + 8 * cg + b];
+            for (int a = 0; a < 8; ++a) {
+                const int rho = 8 * rg + a;
+                lw8[a] = reinterpret_cast<const uint32_t*>(
+                    rho < mp1 ? M8 + rho * NODE_B8 : G8 + (rho < R ? rho - mp1 : 0) * NODE_B8);
+            }
+            const uint32_t* xw8 = reinterpret_cast<const uint32_t*>(XT8 + 8 * cg * NODE_B8);
+            const int k4n = (r1 + 3) >> 2;
+#pragma unroll 2
+            for (int k4 = 0; k4 < k4n; ++k4) {
+                uint32_t xv[8], lv[8];
 #pragma unroll
-            for (int a = 0; a < 8; ++a) lv[a] = lrow[a][k];
+                for (int b = 0; b < 8; ++b) xv[b] = xw8[b * (NODE_B8 / 4) + k4];
 #pragma unroll
-            for (int a = 0; a < 8; ++a)
+                for (int a = 0; a < 8; ++a) lv[a] = lw8[a][k4];
 #pragma unroll
-                for (int b = 0; b < 8; ++b) acc[a][b] += lv[a] * xv[b];
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) acc[a][b] = __dp4a(lv[a], xv[b], acc[a][b]);
+            }
+        } else {
+            for (int k = 0; k < r1; ++k) {
+                uint32_t xv[8], lv[8];
+#pragma unroll
+                for (int b = 0; b < 8; ++b) xv[b] = BP[k * NODE_W + 8 * cg + b];
+#pragma unroll
+                for (int a = 0; a < 8; ++a) lv[a] = lrow[a][k];
+#pragma unroll
+                for (int a = 0; a < 8; ++a)
+#pragma unroll
+                    for (int b = 0; b < 8; ++b) acc[a][b] += lv[a] * xv[b];
+            }
         }
         int nz = 0;
 #pragma unroll
@@ -592,6 +682,7 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
         if (nz) ynz = 1;
     }
     __syncthreads();
+    NODE_STAMP(6);
     if (mp1 > 0 && ynz) {
         // ---- zero_leading_pairs: hand Y and Z to the host ----
         for (int e = tid; e < mp1 * 64; e += 128) {
@@ -610,6 +701,7 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
     } else {
         // ---- leaf(Z) (:317 via zero_leading :273 / :276) ----
         const int r3 = leaf_core<false>(f, inv, Am + m * NODE_LD + m, NODE_LD, ns, sm, D, coff + r1);
+        NODE_STAMP(7);
         if (tid < ns) {
             uint32_t* d = Lg + (int64_t)srows[m + tid] * ldL + coff + r1;
             for (int c = 0; c < r3; ++c) d[c] = sm.Ls[tid][c];
@@ -651,6 +743,7 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
         __syncthreads();
         if (tid == 0) *(volatile uint32_t*)mp.seq_ptr = mp.seq;
     }
+    NODE_STAMP(8);
 }
 
 // Inverse of the unit lower triangular 64x64 diagonal blocks of T, one CTA per
@@ -1317,3 +1410,8 @@ void trsm_lower_unit(const Fp& f, cudaStream_t st, DMat T, DMat B) {
 }
 
 }  // namespace ffb
+
+// diagnostics: SM-clock stamps of the last fused small node (tools/node_stamps.py)
+extern "C" int ffb_dbg_node_stamps(long long* out9) {
+    return cudaMemcpyFromSymbol(out9, ffb::g_node_stamp, 9 * sizeof(long long)) == cudaSuccess ? 0 : 1;
+}
