@@ -508,7 +508,7 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
     // ---- B' = P1^T B (:308), [L1; M1] in position order ----
     {  // thread = column j, rows ih + 2u; 8 rows of loads in flight
         const int j = tid & 63, ih = tid >> 6;
-#pragma unroll
+#pragma unroll 1
         for (int ub = 0; ub < 32; ub += 8) {
             if (ih + 2 * ub >= m) break;  // uniform per warp
             int src[8];
@@ -588,7 +588,7 @@ __global__ void __launch_bounds__(128) k_node128(Fp f, uint32_t* A, int64_t lda,
                     cb = iv;
                 }
             }
-#pragma unroll
+#pragma unroll 1
             for (int ub = 0; ub < 32; ub += 8) {
                 if (jh + 2 * ub >= ns) break;  // uniform per warp
                 uint32_t x1[8], x2[8];

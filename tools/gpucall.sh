@@ -1,9 +1,10 @@
 mkdir -p gpurun_out
-python tools/timeline.py 5 32768 gpurun_out/tl5.json > gpurun_out/timeline_cfg5.txt 2>&1
-python tools/tl_attr.py gpurun_out/tl5.json 6
-python tools/timeline.py 1 1024 gpurun_out/tl1.json > gpurun_out/timeline_cfg1.txt 2>&1
-python tools/tl_attr.py gpurun_out/tl1.json 6
-python tools/tl_window.py gpurun_out/tl1.json 0 2 | grep node128
-python tools/timeline.py 4 16384 gpurun_out/tl4.json > gpurun_out/timeline_cfg4.txt 2>&1
-python tools/tl_attr.py gpurun_out/tl4.json 8
-rm gpurun_out/tl1.json gpurun_out/tl4.json; gzip -f gpurun_out/tl5.json
+python tools/node_stamps.py 1 1024
+python tools/node_stamps.py 5 1024
+timeout 1500 python -m pytest tests/test_parity_gpu.py -m gpu -q -x -k "fused or golden or config or exhaust or small" > gpurun_out/pytest_pq.log 2>&1; echo pytest rc=$?
+tail -3 gpurun_out/pytest_pq.log
+for c in 5 4; do
+python bench.py --config $c --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_q.json 2>gpurun_out/bench_q.err; echo rc=$?
+python -c "
+import json;d=json.loads(open('gpurun_out/bench_q.json').read().strip().splitlines()[-1]);print($c, d['ms_per_step'],d['verified']['reconstruction_mismatches'], d['gpu_launches_per_step'])"
+done
