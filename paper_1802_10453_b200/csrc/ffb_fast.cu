@@ -314,10 +314,12 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
             clear_bit(p1);
             const uint32_t l0 = Acc::mul(f, c0, xi), l1 = Acc::mul(f, c1, xi);  // row multipliers
             // S[i][k] -= c_i l_k = l_i c_k (mod p): row multiplier times column residual
+            // negated multipliers: two negations instead of one per column residual
+            const T nl0 = (T)0 - (T)l0, nl1 = (T)0 - (T)l1;
 #pragma unroll
             for (int t = 0; t < 16; ++t) {
-                S0[t] -= (T)l0 * ck[t];
-                S1[t] -= (T)l1 * ck[t];
+                S0[t] += nl0 * ck[t];
+                S1[t] += nl1 * ck[t];
             }
             if (wp == 0) {
                 if ((alo >> lane) & 1) sm.Ls[lane][r] = l0;
@@ -357,17 +359,17 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
         const uint32_t l1a = Acc::mul(f, xi, Acc::msub(f, d0, y_eff, l2a));
         const uint32_t l1b = Acc::mul(f, xi, Acc::msub(f, d1, y_eff, l2b));
         // S -= x l1_i l2_k + x l2_i l1_k (+ yd l2_i l2_k)
-        const T ga = (T)(Acc::mul(f, x, l1a) + Acc::mul(f, yd, l2a));
-        const T gb = (T)(Acc::mul(f, x, l1b) + Acc::mul(f, yd, l2b));
-        const T ba = (T)Acc::mul(f, x, l2a), bb = (T)Acc::mul(f, x, l2b);
+        const T ga = (T)0 - (T)(Acc::mul(f, x, l1a) + Acc::mul(f, yd, l2a));  // negated, as above
+        const T gb = (T)0 - (T)(Acc::mul(f, x, l1b) + Acc::mul(f, yd, l2b));
+        const T ba = (T)0 - (T)Acc::mul(f, x, l2a), bb = (T)0 - (T)Acc::mul(f, x, l2b);
         const uint32_t s2 = lo ? l2a : l2b, s1 = lo ? l1a : l1b;
 #pragma unroll
         for (int t = 0; t < 16; ++t) {
             const int src_l = (16 * wp + t) & 31;
             const T l2k = (T)__shfl_sync(0xffffffffu, s2, src_l);
             const T l1k = (T)__shfl_sync(0xffffffffu, s1, src_l);
-            S0[t] -= ga * l2k + ba * l1k;
-            S1[t] -= gb * l2k + bb * l1k;
+            S0[t] += ga * l2k + ba * l1k;
+            S1[t] += gb * l2k + bb * l1k;
         }
         if (wp == 0) {
             if ((alo >> lane) & 1) {
