@@ -373,9 +373,10 @@ def test_banded_upload_matches_device_path(gpu, v):
 def test_plduq_adaptive_chunks(gpu, oracle, p):
     """The parallel PLDUQ sizes its row chunks from the previous chunk's density (128 up to
     640 rows, narrow 64-column row detection).  This Y is sparse on top (rank 4 over 768
-    rows: the chunks grow) and dense below (a 640-row chunk finds >= 48 rows, shrinks to
-    128 rows with its sketch rows recomputed, then dense 128-row chunks, then growth
-    again once the rank is exhausted).  Bit-exact against the oracle."""
+    rows: the chunks grow) and dense below (a 640-row chunk is cut after its first 32 new
+    rows -- p >= 4096: finds >= 48 rows and shrinks to 128 rows -- with its sketch rows
+    recomputed, then dense 128-row chunks, then growth again once the rank is exhausted).
+    Bit-exact against the oracle."""
     import paper_1802_10453_b200 as ffb
     rng = np.random.default_rng(p + 11)
     m, n, top = 1500, 300, 768
@@ -387,6 +388,30 @@ def test_plduq_adaptive_chunks(gpu, oracle, p):
     g = ffb.plduq(y, p, ctx=gpu)
     o = oracle.plduq(p, y)
     assert g.rank == o["rank"]
+    assert np.array_equal(g.row_perm.image_array(), o["row_image"])
+    assert np.array_equal(g.col_perm.image_array(), o["col_image"])
+    assert np.array_equal(g.lower, o["lower"]) and np.array_equal(g.upper, o["upper"])
+    assert np.array_equal(g.diag, o["diag"])
+
+
+@pytest.mark.parametrize("p", [3, 131, 251])
+def test_plduq_detection_cap(gpu, oracle, p):
+    """Row detection stops after 32 new rows and cuts the chunk there (k_rrp2, p < 4096), so
+    the register-resident CRP kernels (k <= 32) take every chunk.  Dense rows give a cut in
+    almost every chunk: serially detected chunks (the sketch rows after the cut were
+    overwritten in place and are recomputed) and pipelined ones (the stacked detection is
+    capped too), after a sparse top block and until the rank is exhausted; the rows after
+    that are dependent.  Bit-exact against the oracle."""
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(3 * p + 1)
+    m, n, top = 1100, 400, 140
+    basis = rng.integers(0, p, (10, n)).astype(object)
+    y = np.zeros((m, n), dtype=np.uint64)
+    y[:top] = (rng.integers(0, p, (top, 10)).astype(object).dot(basis) % p).astype(np.uint64)
+    y[top:] = rng.integers(0, p, (m - top, n), dtype=np.uint64)
+    g = ffb.plduq(y, p, ctx=gpu)
+    o = oracle.plduq(p, y)
+    assert g.rank == o["rank"] == n
     assert np.array_equal(g.row_perm.image_array(), o["row_image"])
     assert np.array_equal(g.col_perm.image_array(), o["col_image"])
     assert np.array_equal(g.lower, o["lower"]) and np.array_equal(g.upper, o["upper"])
