@@ -10,6 +10,7 @@ started -- a read-back bubble or a launch-latency bubble.
 """
 import json
 import os
+import re
 import sys
 from collections import defaultdict
 
@@ -55,7 +56,8 @@ def main():
     idle = 0.0
     total_busy = 0.0
     for e in ks:
-        nm = e["name"].split("(")[0].split("<")[0].replace("void ", "").replace("ffb::", "")
+        mm = re.search(r"(k_\w+)", e["name"])
+        nm = mm.group(1) if mm else e["name"].split("(")[0][:28]
         g = e["ts"] - end
         if g > 0:
             gaps[nm] += g
