@@ -212,8 +212,8 @@ struct LeafSmemT {
     __align__(16) typename Acc::T row2[64];       // raw residual row of the 2x2 partner
     int32_t order[64];                            // pivot rows in pivot order
     int32_t pless[64];                            // pivotless rows, ascending
-    int32_t dkind[64];                            // D of the leaf's pivot columns (also written to D)
-    uint32_t dval2[64], dinv[64];
+    int32_t dkind[64];                            // D of the leaf's pivot columns (written to D after the loop)
+    uint32_t dval[64], dval2[64], dinv[64];
 };
 using LeafSmem = LeafSmemT<LzNarrow>;
 // the warp's 16 raw entries of one row -> dst (16-byte stores)
@@ -326,11 +326,8 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
                 if ((ahi >> lane) & 1) sm.Ls[lane + 32][r] = l1;
                 if (lane == 0) {
                     sm.Ls[p1][r] = one;
-                    D.kind[coff + r] = D_SCALAR;
-                    D.val[coff + r] = x;
-                    D.val2[coff + r] = 0;
-                    D.inv[coff + r] = xi;
                     sm.dkind[r] = D_SCALAR;
+                    sm.dval[r] = x;
                     sm.dval2[r] = 0;
                     sm.dinv[r] = xi;
                     sm.order[r] = p1;
@@ -385,11 +382,7 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
                 sm.Ls[p2][r + 1] = one;
                 sm.Ls[p2][r] = f.char2 ? 0 : Acc::mul(f, xi, y_eff);
                 const int32_t hk = yd ? D_ANTITRI_HEAD : D_ANTIDIAG_HEAD;
-                D.kind[coff + r] = hk;
-                D.kind[coff + r + 1] = hk + 1;
-                D.val[coff + r] = D.val[coff + r + 1] = x;
-                D.val2[coff + r] = D.val2[coff + r + 1] = yd;
-                D.inv[coff + r] = D.inv[coff + r + 1] = xi;
+                sm.dval[r] = sm.dval[r + 1] = x;
                 sm.dkind[r] = hk;
                 sm.dkind[r + 1] = hk + 1;
                 sm.dval2[r] = sm.dval2[r + 1] = yd;
@@ -401,6 +394,14 @@ __device__ int leaf_core(const Fp& f, const SmemInv& inv, const uint32_t* src, i
         r += 2;
     }
     __syncthreads();
+    // D of the leaf's pivot columns, in one coalesced pass (the per-pivot global stores sat on
+    // warp 0's path to the next barrier)
+    for (int t = tid; t < r; t += 128) {
+        D.kind[coff + t] = sm.dkind[t];
+        D.val[coff + t] = sm.dval[t];
+        D.val2[coff + t] = sm.dval2[t];
+        D.inv[coff + t] = sm.dinv[t];
+    }
     return r;
 }
 
