@@ -405,6 +405,12 @@ Fp make_field(ffb_context* c, uint64_t p) {
 // measured crossover against the chunked pipeline on config 5).
 static int64_t PLDUQ_SEQ_MAX_ROWS =
     getenv("FFB_PLDUQ_SEQ_ROWS") ? atoll(getenv("FFB_PLDUQ_SEQ_ROWS")) : 200;
+// The shared-memory sequential kernel (p <= 255, Y as bytes <= 200 KB): rows and pivot cap of
+// its speculative use above PLDUQ_SEQ_MAX_ROWS; FFB_PLDUQ_NO_SMEM: off (A/B hook).
+static const bool PLDUQ_SMEM_ON = getenv("FFB_PLDUQ_NO_SMEM") == nullptr;
+static int64_t PLDUQ_SMEM_MAX_ROWS =
+    getenv("FFB_PLDUQ_SMEM_ROWS") ? atoll(getenv("FFB_PLDUQ_SMEM_ROWS")) : 512;
+static int PLDUQ_SMEM_RCAP = getenv("FFB_PLDUQ_SMEM_RCAP") ? atoi(getenv("FFB_PLDUQ_SMEM_RCAP")) : 12;
 
 struct HFact {
     std::vector<int32_t> perm;  // image: position -> local input row
@@ -746,17 +752,37 @@ struct Engine {
         DMat Lo = ws_mat(c, m, mn), Uo = ws_mat(c, mn, n);
         pl.d = ws_vec<uint32_t>(c, mn);
         pl.dinv = ws_vec<uint32_t>(c, mn);
-        if (m <= PLDUQ_SEQ_MAX_ROWS) {
+        auto take_seq = [&](const int32_t* hb) {
+            pl.r = hb[0];
+            pl.rimg.assign(hb + 1, hb + 1 + m);
+            pl.cimg.assign(hb + 1 + m, hb + 1 + m + n);
+            invert_vec(f, st, pl.dinv, pl.d, pl.r);
+        };
+        // p <= 255 and Y fits shared memory as bytes: the sequential elimination there costs ~ its
+        // rank, not its rows.  Short Y always; taller Y (up to PLDUQ_SMEM_MAX_ROWS) with a cap on the
+        // pivots -- the kernel only reads Y, so past the cap the chunked pipeline starts from scratch.
+        bool seq_done = false;
+        if (m <= PLDUQ_SMEM_MAX_ROWS && PLDUQ_SMEM_ON) {
+            const WsMark mk{c->ws_top};
+            int32_t* info = ws_vec<int32_t>(c, 1 + m + n + mn);
+            const int rcap = m <= PLDUQ_SEQ_MAX_ROWS ? (int)mn : PLDUQ_SMEM_RCAP;
+            if (plduq_smem(f, st, Y, info, Lo, pl.d, Uo, rcap)) {
+                const int32_t* hb = (const int32_t*)readback(c, info, (size_t)(1 + m + n) * sizeof(int32_t));
+                if (hb[0] >= 0) {
+                    take_seq(hb);
+                    seq_done = true;
+                }
+            }
+            if (!seq_done) c->ws_top = mk.top;
+        }
+        if (seq_done) {
+        } else if (m <= PLDUQ_SEQ_MAX_ROWS) {
             // short Y: one launch of the row-sequential kernel
             int32_t* info = ws_vec<int32_t>(c, 1 + m + n + mn);
             int32_t* colflag = ws_vec<int32_t>(c, n);
             uint32_t* lvec = ws_vec<uint32_t>(c, m);
             plduq(f, st, Y, info, colflag, lvec, Lo, pl.d, Uo);
-            const int32_t* hb = (const int32_t*)readback(c, info, (size_t)(1 + m + n) * sizeof(int32_t));
-            pl.r = hb[0];
-            pl.rimg.assign(hb + 1, hb + 1 + m);
-            pl.cimg.assign(hb + 1 + m, hb + 1 + m + n);
-            invert_vec(f, st, pl.dinv, pl.d, pl.r);
+            take_seq((const int32_t*)readback(c, info, (size_t)(1 + m + n) * sizeof(int32_t)));
         } else {
             Workspace ws{c->ws_base, c->ws_cap, &c->ws_top};
             PlduqIO io;

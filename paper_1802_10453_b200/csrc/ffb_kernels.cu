@@ -1372,6 +1372,159 @@ __global__ void __launch_bounds__(PLDUQ_THREADS)
     }
 }
 
+
+// The same elimination for p <= 255 with W held in shared memory as bytes (m * n up to
+// ~200 KB): the passes of a pivot step (U coefficients, trailing update with the search for
+// the next nonzero row, one warp per row) run at shared-memory speed and cost ~ the rank, so
+// short-and-wide or low-rank Y need not take the chunked pipeline.  W in global memory is only
+// read: with rcap < min(m, n) the kernel gives up after rcap pivots (info[0] = -1, nothing
+// else written that matters) and the caller runs the parallel PLDUQ on the untouched input.
+__global__ void __launch_bounds__(PLDUQ_THREADS)
+    k_plduq_smem(Fp f, const uint32_t* W, int64_t ldw, int m, int n, int32_t* info, uint32_t* Lo, int64_t ldlo,
+                 uint32_t* d, uint32_t* Uo, int64_t lduo, int rcap) {
+    FFB_PDL_ENTRY();
+    extern __shared__ __align__(16) uint8_t ps_raw[];
+    const int ns = (n + 3) & ~3, ms4 = (m + 3) & ~3;
+    uint8_t* W8 = ps_raw;                                   // m x ns
+    uint8_t* cf = W8 + (size_t)m * ns;                      // ns column flags
+    uint8_t* lv = cf + ns;                                  // m multipliers of the pivot column
+    int32_t* rimg = reinterpret_cast<int32_t*>(lv + ms4);   // m
+    int32_t* pcs = rimg + m;                                // min(m, n) pivot columns
+    int32_t* cimg = pcs + min(m, n);                        // n
+    __shared__ int jmin, nrow;
+    __shared__ uint32_t sxi;
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    {  // stage W (a warp per row) and find the first row with a nonzero entry
+        int mine = m;
+        for (int i = wp; i < m; i += 32) {
+            bool nz = false;
+            for (int j = lane; j < ns; j += 32) {
+                const uint32_t v = j < n ? __ldcg(W + (int64_t)i * ldw + j) : 0u;
+                W8[(size_t)i * ns + j] = (uint8_t)v;
+                nz |= v != 0;
+            }
+            if (__any_sync(0xffffffffu, nz) && i < mine) mine = i;
+        }
+        for (int j = tid; j < ns; j += PLDUQ_THREADS) cf[j] = 0;
+        if (tid == 0) nrow = m;
+        __syncthreads();
+        if (lane == 0 && mine < m) atomicMin(&nrow, mine);
+    }
+    int r = 0, nm = 0, i = 0;
+    bool bail = false;
+    while (true) {
+        __syncthreads();
+        const int nx = nrow;
+        for (int t = tid; t < nx - i; t += PLDUQ_THREADS) rimg[m - 1 - (nm + t)] = i + t;  // from the back for now
+        nm += nx - i;
+        if (nx >= m) break;
+        if (r >= rcap) {  // uniform
+            bail = true;
+            break;
+        }
+        i = nx;
+        __syncthreads();
+        if (tid == 0) {
+            jmin = n;
+            nrow = m;
+        }
+        __syncthreads();
+        uint8_t* wi = W8 + (size_t)i * ns;
+        for (int j = tid; j < n; j += PLDUQ_THREADS)
+            if (!cf[j] && wi[j] != 0) atomicMin(&jmin, j);
+        __syncthreads();
+        const int jp = jmin;
+        if (tid == 0) {
+            const uint32_t x = wi[jp];
+            sxi = finv(f, x);
+            d[r] = x;
+            rimg[r] = i;
+            pcs[r] = jp;
+        }
+        __syncthreads();
+        const uint32_t xi = sxi;
+        for (int j = tid; j < n; j += PLDUQ_THREADS)  // U coefficients (plduq.cpp:65-70)
+            if (!cf[j] && j != jp) wi[j] = (uint8_t)red32(f, xi * wi[j]);
+        for (int i2 = i + 1 + tid; i2 < m; i2 += PLDUQ_THREADS) lv[i2] = W8[(size_t)i2 * ns + jp];
+        __syncthreads();
+        int mine = m;
+        for (int i2 = i + 1 + wp; i2 < m; i2 += 32) {  // trailing rows, a warp per row
+            const uint32_t l = lv[i2];
+            uint8_t* w = W8 + (size_t)i2 * ns;
+            bool nz = false;
+            if (l) {  // residual update on non-pivot columns, L multiplier in column jp
+                const uint32_t nl = f.p - l;
+                for (int j = lane; j < n; j += 32) {
+                    if (cf[j]) continue;
+                    if (j == jp) {
+                        w[j] = (uint8_t)red32(f, l * xi);
+                    } else {
+                        const uint32_t v = red32(f, w[j] + nl * wi[j]);
+                        w[j] = (uint8_t)v;
+                        nz |= v != 0;
+                    }
+                }
+            } else {  // multiplier 0: the row is unchanged (its entry in column jp is 0)
+                for (int j = lane; j < n; j += 32) nz |= !cf[j] && j != jp && w[j] != 0;
+            }
+            if (__any_sync(0xffffffffu, nz) && i2 < mine) mine = i2;
+        }
+        if (lane == 0 && mine < m) atomicMin(&nrow, mine);
+        __syncthreads();
+        if (tid == 0) cf[jp] = 1;
+        ++r;
+        ++i;
+    }
+    __syncthreads();
+    if (bail) {
+        if (tid == 0) info[0] = -1;
+        return;
+    }
+    // pivotless rows ascending after the pivot rows (plduq.cpp:86-90); column image: the pivot
+    // columns in pivot order, then the others ascending
+    for (int t = tid; t < nm / 2; t += PLDUQ_THREADS) {
+        const int32_t a = rimg[r + t];
+        rimg[r + t] = rimg[r + nm - 1 - t];
+        rimg[r + nm - 1 - t] = a;
+    }
+    for (int k = tid; k < r; k += PLDUQ_THREADS) cimg[k] = pcs[k];
+    if (wp == 0) {
+        int q = r;
+        for (int j0 = 0; j0 < n; j0 += 32) {
+            const int j = j0 + lane;
+            const bool fr = j < n && !cf[j];
+            const unsigned bal = __ballot_sync(0xffffffffu, fr);
+            if (fr) cimg[q + __popc(bal & ((1u << lane) - 1u))] = j;
+            q += __popc(bal);
+        }
+    }
+    __syncthreads();
+    int32_t* row_image = info + 1;
+    int32_t* col_image = info + 1 + m;
+    int32_t* pc = info + 1 + m + n;
+    if (tid == 0) info[0] = r;
+    for (int t = tid; t < m; t += PLDUQ_THREADS) row_image[t] = rimg[t];
+    for (int t = tid; t < n; t += PLDUQ_THREADS) col_image[t] = cimg[t];
+    for (int t = tid; t < r; t += PLDUQ_THREADS) pc[t] = pcs[t];
+    // dense factors (plduq.cpp:96-115)
+    for (int64_t e = tid; e < (int64_t)m * r; e += PLDUQ_THREADS) {
+        const int a = (int)(e / r), k = (int)(e % r);
+        uint32_t v = 0;
+        if (a == k) v = 1 % f.p;
+        else if (a > k) v = W8[(size_t)rimg[a] * ns + pcs[k]];
+        Lo[(int64_t)a * ldlo + k] = v;
+    }
+    for (int k = wp; k < r; k += 32) {  // a warp per U row
+        const uint8_t* wr = W8 + (size_t)rimg[k] * ns;
+        for (int a = lane; a < n; a += 32) {
+            uint32_t v = 0;
+            if (a == k) v = 1 % f.p;
+            else if (a > k) v = wr[cimg[a]];
+            Uo[(int64_t)k * lduo + a] = v;
+        }
+    }
+}
+
 }  // namespace
 
 void plduq(const Fp& f, cudaStream_t st, DMat W, int32_t* info, int32_t* colflag, uint32_t* lvec,
@@ -1381,6 +1534,27 @@ void plduq(const Fp& f, cudaStream_t st, DMat W, int32_t* info, int32_t* colflag
                                             lvec, Lo.ptr, Lo.ld, d, Uo.ptr, Uo.ld);
     count_launch();
     FFB_CHECK_LAUNCH();
+}
+
+size_t plduq_smem_bytes(int64_t m, int64_t n) {
+    const int64_t ns = (n + 3) & ~3, ms4 = (m + 3) & ~3;
+    return (size_t)(m * ns + ns + ms4 + 4 * (m + std::min(m, n) + n));
+}
+
+bool plduq_smem(const Fp& f, cudaStream_t st, DMat W, int32_t* info, DMat Lo, uint32_t* d, DMat Uo, int rcap) {
+    const size_t bytes = plduq_smem_bytes(W.rows, W.cols);
+    if (f.p > 255u || !f.mu32 || bytes > (size_t)200 * 1024 || W.rows <= 0 || W.cols <= 0) return false;
+    static DeviceOnce attr;
+    if (!attr.done()) {
+        FFB_CUDA(cudaFuncSetAttribute(k_plduq_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        attr.mark();
+    }
+    ProfScope ps(K_PLDUQ, st, 0.0, 4.0 * W.rows * W.cols);
+    launch_k(k_plduq_smem, 1, PLDUQ_THREADS, bytes, st, f, (const uint32_t*)W.ptr, W.ld, (int)W.rows, (int)W.cols, info,
+             Lo.ptr, Lo.ld, d, Uo.ptr, Uo.ld, rcap);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+    return true;
 }
 
 }  // namespace ffb

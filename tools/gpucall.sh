@@ -1,8 +1,15 @@
 mkdir -p gpurun_out
-python bench.py > gpurun_out/bench_cfg5.json 2> gpurun_out/bench_cfg5.err; echo bench rc=$?
-for c in 1 2 3 4; do
-  python bench.py --config $c --steps 10 --warmup 3 > gpurun_out/bench_cfg$c.json 2> gpurun_out/bench_cfg$c.err; echo cfg$c rc=$?
-done
-timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_final.log 2>&1; echo pytest rc=$?
-tail -3 gpurun_out/pytest_gpu_final.log
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')"
+timeout 1500 python -m pytest tests/test_parity_gpu.py -m gpu -q -x > gpurun_out/pytest_pq.log 2>&1; echo pytest rc=$?
+tail -3 gpurun_out/pytest_pq.log
+run() {
+python bench.py --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/bench_q.json 2>gpurun_out/bench_q.err
+python -c "
+import json,os;d=json.loads(open('gpurun_out/bench_q.json').read().strip().splitlines()[-1]);print('$1', d['ms_per_step'],d['verified']['reconstruction_mismatches'], d['gpu_launches_per_step'], d['host_syncs_per_step'])"
+}
+run default
+FFB_PLDUQ_NO_SMEM=1 run off
+FFB_PLDUQ_SMEM_ROWS=200 run rows200
+FFB_PLDUQ_SMEM_ROWS=1024 run rows1024
+FFB_PLDUQ_SMEM_RCAP=6 run rcap6
+FFB_PLDUQ_SMEM_RCAP=24 run rcap24
+FFB_PLDUQ_SMEM_ROWS=1024 FFB_PLDUQ_SMEM_RCAP=24 run rows1024rcap24
