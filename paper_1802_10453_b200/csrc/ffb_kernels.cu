@@ -1398,10 +1398,17 @@ __global__ void __launch_bounds__(PLDUQ_THREADS)
         int mine = m;
         for (int i = wp; i < m; i += 32) {
             bool nz = false;
-            for (int j = lane; j < ns; j += 32) {
-                const uint32_t v = j < n ? __ldcg(W + (int64_t)i * ldw + j) : 0u;
-                W8[(size_t)i * ns + j] = (uint8_t)v;
-                nz |= v != 0;
+            const uint32_t* src = W + (int64_t)i * ldw;
+            for (int j0 = lane; j0 < ns; j0 += 32 * 8) {  // 8 loads in flight per lane
+                uint32_t v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = j0 + 32 * u < n ? __ldcg(src + j0 + 32 * u) : 0u;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (j0 + 32 * u < ns) {
+                        W8[(size_t)i * ns + j0 + 32 * u] = (uint8_t)v[u];
+                        nz |= v[u] != 0;
+                    }
             }
             if (__any_sync(0xffffffffu, nz) && i < mine) mine = i;
         }
@@ -1446,32 +1453,36 @@ __global__ void __launch_bounds__(PLDUQ_THREADS)
         for (int j = tid; j < n; j += PLDUQ_THREADS)  // U coefficients (plduq.cpp:65-70)
             if (!cf[j] && j != jp) wi[j] = (uint8_t)red32(f, xi * wi[j]);
         for (int i2 = i + 1 + tid; i2 < m; i2 += PLDUQ_THREADS) lv[i2] = W8[(size_t)i2 * ns + jp];
+        if (tid == 0) cf[jp] = 1;  // from here on column jp is a pivot column (skipped below)
         __syncthreads();
         int mine = m;
-        for (int i2 = i + 1 + wp; i2 < m; i2 += 32) {  // trailing rows, a warp per row
+        const uint32_t* cfw = reinterpret_cast<const uint32_t*>(cf);
+        const uint32_t* uw = reinterpret_cast<const uint32_t*>(wi);
+        for (int i2 = i + 1 + wp; i2 < m; i2 += 32) {  // trailing rows, a warp per row, 4 columns per lane
             const uint32_t l = lv[i2];
-            uint8_t* w = W8 + (size_t)i2 * ns;
+            uint32_t* w = reinterpret_cast<uint32_t*>(W8 + (size_t)i2 * ns);
             bool nz = false;
             if (l) {  // residual update on non-pivot columns, L multiplier in column jp
                 const uint32_t nl = f.p - l;
-                for (int j = lane; j < n; j += 32) {
-                    if (cf[j]) continue;
-                    if (j == jp) {
-                        w[j] = (uint8_t)red32(f, l * xi);
-                    } else {
-                        const uint32_t v = red32(f, w[j] + nl * wi[j]);
-                        w[j] = (uint8_t)v;
-                        nz |= v != 0;
+                for (int jw = lane; jw < (ns >> 2); jw += 32) {
+                    const uint32_t fm = cfw[jw] * 0xffu, u4 = uw[jw], w4 = w[jw];
+                    uint32_t o = w4 & fm;  // pivot columns keep their L multipliers
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) {
+                        const uint32_t v = red32(f, ((w4 >> (8 * b)) & 0xffu) + nl * ((u4 >> (8 * b)) & 0xffu));
+                        o |= (v << (8 * b)) & ~fm;
                     }
+                    w[jw] = o;
+                    nz |= (o & ~fm) != 0;
                 }
+                __syncwarp();
+                if (lane == 0) W8[(size_t)i2 * ns + jp] = (uint8_t)red32(f, l * xi);
             } else {  // multiplier 0: the row is unchanged (its entry in column jp is 0)
-                for (int j = lane; j < n; j += 32) nz |= !cf[j] && j != jp && w[j] != 0;
+                for (int jw = lane; jw < (ns >> 2); jw += 32) nz |= (w[jw] & ~(cfw[jw] * 0xffu)) != 0;
             }
             if (__any_sync(0xffffffffu, nz) && i2 < mine) mine = i2;
         }
         if (lane == 0 && mine < m) atomicMin(&nrow, mine);
-        __syncthreads();
-        if (tid == 0) cf[jp] = 1;
         ++r;
         ++i;
     }

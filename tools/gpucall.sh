@@ -1,4 +1,7 @@
 mkdir -p gpurun_out
+rm -f gpurun_out/plduq_calls.txt
+FFB_PLDUQ_TRACE=gpurun_out/plduq_calls.txt python tools/one_factorization.py 5 32768 > /dev/null 2>&1
+FFB_PLDUQ_TRACE=gpurun_out/plduq_calls.txt python tools/one_factorization.py 5 32768 > /dev/null 2>&1
 timeout 1500 python -m pytest tests/test_parity_gpu.py -m gpu -q -x > gpurun_out/pytest_pq.log 2>&1; echo pytest rc=$?
 tail -3 gpurun_out/pytest_pq.log
 run() {
@@ -8,8 +11,3 @@ import json,os;d=json.loads(open('gpurun_out/bench_q.json').read().strip().split
 }
 run default
 FFB_PLDUQ_NO_SMEM=1 run off
-FFB_PLDUQ_SMEM_ROWS=200 run rows200
-FFB_PLDUQ_SMEM_ROWS=1024 run rows1024
-FFB_PLDUQ_SMEM_RCAP=6 run rcap6
-FFB_PLDUQ_SMEM_RCAP=24 run rcap24
-FFB_PLDUQ_SMEM_ROWS=1024 FFB_PLDUQ_SMEM_RCAP=24 run rows1024rcap24
