@@ -394,6 +394,29 @@ def test_plduq_adaptive_chunks(gpu, oracle, p):
     assert np.array_equal(g.diag, o["diag"])
 
 
+@pytest.mark.parametrize("p", [2, 131, 251, 257])
+def test_plduq_shared_memory_kernel(gpu, oracle, p):
+    """k_plduq_smem (p <= 255, Y as bytes in shared memory): every short Y, and speculatively Y
+    up to 512 rows with a cap of 12 pivots -- rank 3 and 12 finish there, rank 13 and 40 give
+    up and take the chunked pipeline on the untouched input; a Y too large for shared memory
+    (480 x 700) and p = 257 never enter it.  Leading zero rows and columns, bit-exact."""
+    import paper_1802_10453_b200 as ffb
+    rng = np.random.default_rng(7 * p + 2)
+    for m, n, r in [(150, 1200, 9), (199, 260, 150), (260, 300, 3), (400, 450, 12), (400, 450, 13),
+                    (512, 380, 40), (480, 700, 5), (300, 257, 0)]:
+        y = (rng.integers(0, p, (m, max(r, 1))).astype(object).dot(rng.integers(0, p, (max(r, 1), n))) % p)
+        y = y.astype(np.uint64) if r else np.zeros((m, n), np.uint64)
+        y[:7] = 0
+        y[:, :3] = 0
+        g = ffb.plduq(y, p, ctx=gpu)
+        o = oracle.plduq(p, y)
+        assert g.rank == o["rank"], (m, n, r)
+        assert np.array_equal(g.row_perm.image_array(), o["row_image"])
+        assert np.array_equal(g.col_perm.image_array(), o["col_image"])
+        assert np.array_equal(g.lower, o["lower"]) and np.array_equal(g.upper, o["upper"])
+        assert np.array_equal(g.diag, o["diag"])
+
+
 @pytest.mark.parametrize("p", [3, 131, 251])
 def test_plduq_detection_cap(gpu, oracle, p):
     """Row detection stops after 32 new rows and cuts the chunk there (k_rrp2, p < 4096), so
