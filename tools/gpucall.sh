@@ -1,3 +1,5 @@
+# Scratch command file for gpurun (what the last call ran); the round-end pass is tools/final_measure.sh.
 mkdir -p gpurun_out
-ncu --set full --warp-sampling-interval 0 --clock-control none --import-source on -k regex:k_plduq_smem -s 40 -c 1 -f -o gpurun_out/plduq_smem python tools/one_factorization.py 5 32768 > gpurun_out/ncu_smem.log 2>&1; echo rc=$?
-tail -2 gpurun_out/ncu_smem.log
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu_final.log 2>&1; echo pytest rc=$?
+tail -3 gpurun_out/pytest_gpu_final.log
+python bench.py > gpurun_out/bench_cfg5.json 2> gpurun_out/bench_cfg5.err; echo bench rc=$?
