@@ -1374,7 +1374,7 @@ __global__ void __launch_bounds__(PLDUQ_THREADS)
 
 
 // The same elimination for p <= 255 with W held in shared memory as bytes (m * n up to
-// ~200 KB): the passes of a pivot step (U coefficients, trailing update with the search for
+// ~220 KB): the passes of a pivot step (U coefficients, trailing update with the search for
 // the next nonzero row, one warp per row) run at shared-memory speed and cost ~ the rank, so
 // short-and-wide or low-rank Y need not take the chunked pipeline.  W in global memory is only
 // read: with rcap < min(m, n) the kernel gives up after rcap pivots (info[0] = -1, nothing
@@ -1554,10 +1554,11 @@ size_t plduq_smem_bytes(int64_t m, int64_t n) {
 
 bool plduq_smem(const Fp& f, cudaStream_t st, DMat W, int32_t* info, DMat Lo, uint32_t* d, DMat Uo, int rcap) {
     const size_t bytes = plduq_smem_bytes(W.rows, W.cols);
-    if (f.p > 255u || !f.mu32 || bytes > (size_t)200 * 1024 || W.rows <= 0 || W.cols <= 0) return false;
+    constexpr size_t cap = (size_t)226 * 1024;  // 227 KB per CTA less the static words
+    if (f.p > 255u || !f.mu32 || bytes > cap || W.rows <= 0 || W.cols <= 0) return false;
     static DeviceOnce attr;
     if (!attr.done()) {
-        FFB_CUDA(cudaFuncSetAttribute(k_plduq_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        FFB_CUDA(cudaFuncSetAttribute(k_plduq_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
         attr.mark();
     }
     ProfScope ps(K_PLDUQ, st, 0.0, 4.0 * W.rows * W.cols);
