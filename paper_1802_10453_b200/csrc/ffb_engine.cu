@@ -886,7 +886,7 @@ struct Engine {
             gemm(f, st, GEMM_SUB, C1, H, true, U1, false, r, r, r);  // C1 -= U1^T diag(delta) U1
         }
         DMat X = ws_mat(c, r, r);
-        fill_words(st, (uint32_t*)c->flag, 1, 0u);
+        if (f.char2) fill_words(st, (uint32_t*)c->flag, 1, 0u);  // (only characteristic 2 writes the flag)
         phase_mark("zlp: C' ready, U^T", m + nz, st);
         trssyr2k_dev(U1, U1T, C1, X, c->flag);  // :202
         phase_mark("zlp: trssyr2k", m + nz, st);
