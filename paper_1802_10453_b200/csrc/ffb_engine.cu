@@ -910,10 +910,12 @@ struct Engine {
 
         //   Y rows (row_perm order):  even columns <- [L1; M1]
         //   Z rows (col_perm order):  even <- [G1; G2], odd <- [U1^T; V1^T]
-        scatter_lg(st, Lg, up[1], coff, 2, py.L);
         const int32_t* didz = up[2];
-        scatter_lg_pair(st, Lg, didz, coff, G12, UpT);  // even <- [G1; G2], odd <- [U1^T; V1^T]
-        write_pair_diag(f, st, D, coff, py.d, py.dinv, delta, r);  // :254-260
+        if (!zlp_scatter(st, Lg, coff, up[1], py.L, didz, G12, UpT, D, py.d, py.dinv, delta, r)) {
+            scatter_lg(st, Lg, up[1], coff, 2, py.L);
+            scatter_lg_pair(st, Lg, didz, coff, G12, UpT);  // even <- [G1; G2], odd <- [U1^T; V1^T]
+            write_pair_diag(f, st, D, coff, py.d, py.dinv, delta, r);  // :254-260
+        }
 
         std::vector<int32_t> rows3(idz.begin() + r, idz.end());
         phase_mark("zlp: C3 updated, L scattered", m + nz, st);

@@ -834,6 +834,56 @@ void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int 
     FFB_CHECK_LAUNCH();
 }
 
+// The three writes that end zero_leading_pairs in one launch (rows of [L1; M1] into the even
+// columns, rows of [G1; G2] / [U1^T; V1^T] into the column pairs, the 2x2 blocks of D): block
+// row y < my scatters a Y row, y < my + nz a Z row, the last block row writes D.
+__global__ void k_zlp_scatter(uint32_t* Lg, int64_t ldl, int64_t col0, const int32_t* idy, int64_t my,
+                              const uint32_t* L, int64_t ldL, const int32_t* idz, int64_t nz, const uint32_t* e,
+                              int64_t lde, const uint32_t* o, int64_t ldo, int64_t r, DDiag D, const uint32_t* dv,
+                              const uint32_t* dinv, const uint32_t* delta) {
+    FFB_PDL_ENTRY();
+    const int64_t y = blockIdx.y, t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                  step = (int64_t)gridDim.x * blockDim.x;
+    if (y < my) {
+        uint32_t* d = Lg + (int64_t)__ldcg(idy + y) * ldl + col0;
+        const uint32_t* s = L + y * ldL;
+        for (int64_t j = t0; j < r; j += step) d[2 * j] = __ldcg(s + j);
+    } else if (y < my + nz) {
+        const int64_t i = y - my;
+        uint32_t* d = Lg + (int64_t)__ldcg(idz + i) * ldl + col0;
+        const uint32_t* se = e + i * lde;
+        const uint32_t* so = o + i * ldo;
+        const bool vec = ((((uintptr_t)d) & 7) == 0);
+        for (int64_t j = t0; j < r; j += step) {
+            const uint32_t a = __ldcg(se + j), b = __ldcg(so + j);
+            if (vec) reinterpret_cast<uint2*>(d)[j] = make_uint2(a, b);
+            else {
+                d[2 * j] = a;
+                d[2 * j + 1] = b;
+            }
+        }
+    } else {
+        for (int64_t i = t0; i < r; i += step) {
+            const uint32_t dl = delta ? __ldcg(delta + i) : 0;
+            const int64_t t = col0 + 2 * i;
+            D.kind[t] = dl ? D_ANTITRI_HEAD : D_ANTIDIAG_HEAD;
+            D.kind[t + 1] = dl ? D_ANTITRI_TAIL : D_ANTIDIAG_TAIL;
+            D.val[t] = D.val[t + 1] = __ldcg(dv + i);
+            D.val2[t] = D.val2[t + 1] = dl;
+            D.inv[t] = D.inv[t + 1] = __ldcg(dinv + i);
+        }
+    }
+}
+bool zlp_scatter(cudaStream_t st, DMat Lg, int64_t col0, const int32_t* idy, DMat L, const int32_t* idz, DMat even,
+                 DMat odd, DDiag D, const uint32_t* d, const uint32_t* dinv, const uint32_t* delta, int64_t r) {
+    if (r <= 0 || L.rows + even.rows + 1 > 65535) return false;
+    ProfScope ps_(K_MOVE, st, 0.0, 0.0);
+    launch_k(k_zlp_scatter, rowgrid(L.rows + even.rows + 1, r), 256, 0, st, Lg.ptr, Lg.ld, col0, idy, L.rows, L.ptr,
+             L.ld, idz, even.rows, even.ptr, even.ld, odd.ptr, odd.ld, r, D, d, dinv, delta);
+    count_launch();
+    FFB_CHECK_LAUNCH();
+    return true;
+}
 void scatter_lg_pair(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, DMat even, DMat odd) {
     ProfScope ps_(K_MOVE, st, 0.0, 0.0);
     if (even.rows <= 0 || even.cols <= 0) return;

@@ -116,6 +116,10 @@ void transpose(cudaStream_t st, DMat dst, DMat src);
 // Lg[ids[i]][col0 + j*cstride] = src[i][j]
 // Lg[ids[i]][col0 + 2j] = even[i][j], Lg[ids[i]][col0 + 2j + 1] = odd[i][j]
 void scatter_lg_pair(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, DMat even, DMat odd);
+// scatter_lg (stride 2) + scatter_lg_pair + write_pair_diag of zero_leading_pairs in one launch;
+// false (nothing launched) when r == 0 or the rows exceed one grid.
+bool zlp_scatter(cudaStream_t st, DMat Lg, int64_t col0, const int32_t* idy, DMat L, const int32_t* idz, DMat even,
+                 DMat odd, DDiag D, const uint32_t* d, const uint32_t* dinv, const uint32_t* delta, int64_t r);
 void scatter_lg(cudaStream_t st, DMat Lg, const int32_t* ids, int64_t col0, int cstride, DMat src);
 // dst[i][k] = Lg[ids[i]][col0 + k]
 void gather_lg(cudaStream_t st, DMat dst, DMat Lg, const int32_t* ids, int64_t col0);
