@@ -752,11 +752,11 @@ struct Engine {
         DMat Lo = ws_mat(c, m, mn), Uo = ws_mat(c, mn, n);
         pl.d = ws_vec<uint32_t>(c, mn);
         pl.dinv = ws_vec<uint32_t>(c, mn);
-        auto take_seq = [&](const int32_t* hb) {
+        auto take_seq = [&](const int32_t* hb, bool has_dinv) {
             pl.r = hb[0];
             pl.rimg.assign(hb + 1, hb + 1 + m);
             pl.cimg.assign(hb + 1 + m, hb + 1 + m + n);
-            invert_vec(f, st, pl.dinv, pl.d, pl.r);
+            if (!has_dinv) invert_vec(f, st, pl.dinv, pl.d, pl.r);
         };
         // p <= 255 and Y fits shared memory as bytes: the sequential elimination there costs ~ its
         // rank, not its rows.  Short Y always; taller Y (up to PLDUQ_SMEM_MAX_ROWS) with a cap on the
@@ -766,10 +766,10 @@ struct Engine {
             const WsMark mk{c->ws_top};
             int32_t* info = ws_vec<int32_t>(c, 1 + m + n + mn);
             const int rcap = m <= PLDUQ_SEQ_MAX_ROWS ? (int)mn : PLDUQ_SMEM_RCAP;
-            if (plduq_smem(f, st, Y, info, Lo, pl.d, Uo, rcap)) {
+            if (plduq_smem(f, st, Y, info, Lo, pl.d, pl.dinv, Uo, rcap)) {
                 const int32_t* hb = (const int32_t*)readback(c, info, (size_t)(1 + m + n) * sizeof(int32_t));
                 if (hb[0] >= 0) {
-                    take_seq(hb);
+                    take_seq(hb, true);
                     seq_done = true;
                 }
             }
@@ -782,7 +782,7 @@ struct Engine {
             int32_t* colflag = ws_vec<int32_t>(c, n);
             uint32_t* lvec = ws_vec<uint32_t>(c, m);
             plduq(f, st, Y, info, colflag, lvec, Lo, pl.d, Uo);
-            take_seq((const int32_t*)readback(c, info, (size_t)(1 + m + n) * sizeof(int32_t)));
+            take_seq((const int32_t*)readback(c, info, (size_t)(1 + m + n) * sizeof(int32_t)), false);
         } else {
             Workspace ws{c->ws_base, c->ws_cap, &c->ws_top};
             PlduqIO io;

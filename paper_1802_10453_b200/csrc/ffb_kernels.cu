@@ -1431,7 +1431,7 @@ __global__ void __launch_bounds__(PLDUQ_THREADS)
 // else written that matters) and the caller runs the parallel PLDUQ on the untouched input.
 __global__ void __launch_bounds__(PLDUQ_THREADS)
     k_plduq_smem(Fp f, const uint32_t* W, int64_t ldw, int m, int n, int32_t* info, uint32_t* Lo, int64_t ldlo,
-                 uint32_t* d, uint32_t* Uo, int64_t lduo, int rcap) {
+                 uint32_t* d, uint32_t* dinv, uint32_t* Uo, int64_t lduo, int rcap) {
     FFB_PDL_ENTRY();
     extern __shared__ __align__(16) uint8_t ps_raw[];
     const int ns = (n + 3) & ~3, ms4 = (m + 3) & ~3;
@@ -1495,6 +1495,7 @@ __global__ void __launch_bounds__(PLDUQ_THREADS)
             const uint32_t x = wi[jp];
             sxi = finv(f, x);
             d[r] = x;
+            dinv[r] = sxi;
             rimg[r] = i;
             pcs[r] = jp;
         }
@@ -1602,7 +1603,8 @@ size_t plduq_smem_bytes(int64_t m, int64_t n) {
     return (size_t)(m * ns + ns + ms4 + 4 * (m + std::min(m, n) + n));
 }
 
-bool plduq_smem(const Fp& f, cudaStream_t st, DMat W, int32_t* info, DMat Lo, uint32_t* d, DMat Uo, int rcap) {
+bool plduq_smem(const Fp& f, cudaStream_t st, DMat W, int32_t* info, DMat Lo, uint32_t* d, uint32_t* dinv, DMat Uo,
+                int rcap) {
     const size_t bytes = plduq_smem_bytes(W.rows, W.cols);
     constexpr size_t cap = (size_t)226 * 1024;  // 227 KB per CTA less the static words
     if (f.p > 255u || !f.mu32 || bytes > cap || W.rows <= 0 || W.cols <= 0) return false;
@@ -1613,7 +1615,7 @@ bool plduq_smem(const Fp& f, cudaStream_t st, DMat W, int32_t* info, DMat Lo, ui
     }
     ProfScope ps(K_PLDUQ, st, 0.0, 4.0 * W.rows * W.cols);
     launch_k(k_plduq_smem, 1, PLDUQ_THREADS, bytes, st, f, (const uint32_t*)W.ptr, W.ld, (int)W.rows, (int)W.cols, info,
-             Lo.ptr, Lo.ld, d, Uo.ptr, Uo.ld, rcap);
+             Lo.ptr, Lo.ld, d, dinv, Uo.ptr, Uo.ld, rcap);
     count_launch();
     FFB_CHECK_LAUNCH();
     return true;

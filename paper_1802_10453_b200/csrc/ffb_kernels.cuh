@@ -219,6 +219,7 @@ void plduq(const Fp& f, cudaStream_t st, DMat W, int32_t* info, int32_t* colflag
 // The same with W (only read) staged in shared memory as bytes: p <= 255 and
 // plduq_smem_bytes(m, n) <= 226 KB, else returns false without a launch.  Stops after rcap
 // pivots when more would follow: info[0] = -1 and the other outputs are unspecified.
-bool plduq_smem(const Fp& f, cudaStream_t st, DMat W, int32_t* info, DMat Lo, uint32_t* d, DMat Uo, int rcap);
+bool plduq_smem(const Fp& f, cudaStream_t st, DMat W, int32_t* info, DMat Lo, uint32_t* d, uint32_t* dinv, DMat Uo,
+                int rcap);  // (also writes the pivots' inverses)
 
 }  // namespace ffb
